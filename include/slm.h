@@ -1,0 +1,136 @@
+/*
+ * slm.h -- C ABI of the B200 (sm_100a) Synchronised Louvain Method library (libslm.so).
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference
+ * (synclouvain, pure Python + numpy) has no FFI of its own: its boundary is the Python
+ * API `run(graph, RunConfig) -> RunResult` (detector.py:548) over
+ * `Graph.from_edges(n, src, dst, w)` (graph.py:84) and the phase functions it calls.
+ * Every entry point below replaces one of those reference functions (cited per call);
+ * the package paper_1702_04645_b200 binds them with ctypes and re-exposes the reference's
+ * Python names, argument meanings and exceptions.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Host arrays are borrowed for the duration of a call.
+ *   - Node ids cross the boundary as int64 (graph.py:87-89), weights/gains as fp64.
+ *   - Every call returns SLM_OK (0) or a negative code; slm_last_error(ctx) describes it.
+ *     SLM_EINVAL maps to the reference's ValueError, the others to RuntimeError.
+ *   - Calls are synchronous (the context's stream is synchronised before return) and a
+ *     context is single-threaded.  Device state stays resident between calls: the current
+ *     hierarchy level's graph and assignment forest live on the GPU, and only labels and
+ *     scalars cross the boundary when the caller asks for them.
+ *   - Output pointers documented as nullable may be NULL to skip the device->host copy.
+ */
+#ifndef SLM_H
+#define SLM_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SLM_API __attribute__((visibility("default")))
+#else
+#define SLM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SLM_OK 0
+#define SLM_EINVAL (-1)
+#define SLM_ECUDA (-2)
+#define SLM_ENOMEM (-3)
+#define SLM_ESTATE (-4)
+#define SLM_EUNSUP (-5)
+
+typedef struct slm_ctx slm_ctx;
+
+/* RunConfig (detector.py:22-40) minus threads (meaningless on the GPU), plus resolution. */
+typedef struct {
+    uint64_t seed;            /* RunConfig.seed, default 0 */
+    double accept_prob;       /* RunConfig.accept_prob, default 0.5, in (0, 1] */
+    int64_t max_outer_iters;  /* RunConfig.max_outer_iters, default 100 */
+    int64_t scc_cut_cap;      /* RunConfig.scc_cut_cap, default 10000 */
+    double resolution;        /* gamma; gains use m_w / gamma */
+} slm_config;
+
+/* ---- context ------------------------------------------------------------------- */
+SLM_API slm_ctx *slm_create(int device);
+SLM_API void slm_destroy(slm_ctx *ctx);
+SLM_API const char *slm_last_error(slm_ctx *ctx);
+SLM_API void *slm_stream(slm_ctx *ctx);                 /* cudaStream_t of the context */
+SLM_API int slm_sync(slm_ctx *ctx);
+
+/* ---- graph ----------------------------------------------------------------------- */
+/* Graph.from_edges (graph.py:84-116) + neighbor_union (graph.py:127-175) + strengths
+ * (graph.py:257-263): canonical CSR, union, strengths and m_w on the device.  Becomes
+ * hierarchy level 0 and resets the level counter. */
+SLM_API int slm_build_graph(slm_ctx *ctx, int64_t n, const int64_t *src, const int64_t *dst,
+                    const double *w, int64_t nedges);
+/* Same from device-resident int32 ids / fp64 weights (no host copy). */
+SLM_API int slm_build_graph_device(slm_ctx *ctx, int64_t n, const int32_t *d_src, const int32_t *d_dst,
+                           const double *d_w, int64_t nedges);
+/* Sizes of the current level: nodes, merged CSR entries, union entries, m_w, flags
+ * (bit0: symmetric W, bit1: integer weights). */
+SLM_API int slm_graph_info(slm_ctx *ctx, int64_t *n, int64_t *ne, int64_t *ue, double *m_w,
+                   int32_t *flags);
+SLM_API int slm_get_csr(slm_ctx *ctx, int64_t *out_ptr, int64_t *out_dst, double *out_w);
+/* NeighborUnion ptr/nbr and w_out + w_in (graph.py:46-60) */
+SLM_API int slm_get_union(slm_ctx *ctx, int64_t *ptr, int64_t *nbr, double *u);
+SLM_API int slm_get_strengths(slm_ctx *ctx, double *s_out, double *s_in);
+SLM_API int slm_set_resolution(slm_ctx *ctx, double gamma);
+
+/* ---- phases (current level) ----------------------------------------------------- */
+/* find_assignment (detector.py:149-158); a_out nullable. */
+SLM_API int slm_assign(slm_ctx *ctx, int64_t *a_out);
+/* Load an assignment map (differential tests / resume); builds the forest. */
+SLM_API int slm_set_assignment(slm_ctx *ctx, const int64_t *a);
+/* extract_components (forest.py:43-67) of the device assignment; outputs nullable. */
+SLM_API int slm_components(slm_ctx *ctx, int64_t *comm_out, uint8_t *on_cycle_out, int64_t *n_comms);
+/* Current forest (a, comm, on_cycle); outputs nullable. */
+SLM_API int slm_get_forest(slm_ctx *ctx, int64_t *a_out, int64_t *comm_out, uint8_t *on_cycle_out,
+                   int64_t *n_comms);
+/* CommunityAggregates.from_labels (quality.py:71-79) of the current forest. */
+SLM_API int slm_get_aggregates(slm_ctx *ctx, double *S_out, double *S_in, int64_t *count);
+/* local_gains (quality.py:170-183) of the current forest. */
+SLM_API int slm_local_gains(slm_ctx *ctx, double *lg_out);
+/* positive_correction (detector.py:338-362); gains_out (nullable) receives up to
+ * gains_cap gains in the reference's order. */
+SLM_API int slm_positive(slm_ctx *ctx, const slm_config *cfg, int64_t *splits, int64_t *unresolved,
+                 int32_t *changed, double *gains_out, int64_t gains_cap);
+/* _best_targets over all rows (detector.py:367-418): the local-move sweep.  comm_in
+ * (nullable) replaces the forest labels as the snapshot (must be dense, with the
+ * aggregates recomputed from it); cstar_out nullable. */
+SLM_API int slm_plan_sweep(slm_ctx *ctx, const int64_t *comm_in, int64_t *cstar_out);
+/* maximal_correction (detector.py:457-521) for (level, sweep); gains_out nullable. */
+SLM_API int slm_maximal(slm_ctx *ctx, const slm_config *cfg, int64_t level, int64_t sweep,
+                int32_t *improved, int64_t *applied, double *gains_out, int64_t gains_cap);
+/* aggregate (graph.py:266-280) by the current forest's labels: the coarse graph becomes
+ * the current level. */
+SLM_API int slm_aggregate(slm_ctx *ctx);
+/* score (quality.py:104-118) with resolution: (intra - gamma*null)/m_w.  on_original != 0
+ * scores the level-0 graph, else the current level. */
+SLM_API int slm_score(slm_ctx *ctx, int32_t on_original, const int64_t *labels, double gamma,
+              double *q_out);
+/* uniform01 (rng.py:34-43) with parts = (level, sweep), computed on the device. */
+SLM_API int slm_uniform01(slm_ctx *ctx, uint64_t seed, int64_t level, int64_t sweep, const int64_t *ids,
+                  int64_t k, double *out);
+/* Diagnostics of the last slm_maximal: candidates, commit rounds. */
+SLM_API int slm_last_commit_stats(slm_ctx *ctx, int64_t *candidates, int64_t *rounds);
+
+/* ---- synthetic inputs (BASELINE.json configs) ------------ */
+/* Symmetrised R-MAT with permuted ids, self-loops dropped; weight_mode 0 = unit,
+ * 1 = uniform integers in [1, 100].  Host twin: pass src == NULL to query the count. */
+SLM_API int slm_gen_rmat_host(int scale, int edge_factor, double a, double b, double c, uint64_t seed,
+                      int weight_mode, int64_t *src, int64_t *dst, double *w, int64_t *n_edges);
+/* Random geometric graph in the unit square (both directions, unit weights). */
+SLM_API int slm_gen_rgg_host(int64_t n, double radius, uint64_t seed, int64_t *src, int64_t *dst,
+                     double *w, int64_t *n_edges);
+/* Device generation of the same edge lists straight into the level-0 build. */
+SLM_API int slm_build_rmat(slm_ctx *ctx, int scale, int edge_factor, double a, double b, double c,
+                   uint64_t seed, int weight_mode);
+SLM_API int slm_build_rgg(slm_ctx *ctx, int64_t n, double radius, uint64_t seed);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLM_H */

@@ -1,0 +1,481 @@
+// slm_build.cu -- device CSR build (Graph.from_edges, graph.py:84-116), neighbour union
+// (_build_union, graph.py:151-175), strengths (graph.py:257-263) and degree binning.
+//
+// Edge list -> packed 2b-bit keys (src << b | dst) -> stable LSD radix sort with the weights
+// as values -> run-length merge (each run summed first + pairwise(rest), numpy's reduceat
+// order, so even real-valued duplicates merge bit-identically) -> CSR.  The union of a
+// symmetric graph is the CSR minus self-loops with u = w + w (no second sort); a directed
+// graph merges its out-row with its in-row (stable transpose).
+#include "slm_internal.cuh"
+#include <cub/cub.cuh>
+#include <algorithm>
+
+int bits_for(int64_t v) {
+    int b = 1;
+    while ((int64_t(1) << b) < v) b++;
+    return b;
+}
+
+template <class T>
+void cub_exclusive_sum(slm_ctx *ctx, const T *in, T *out, int64_t n) {
+    size_t tb = 0;
+    CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n, ctx->stream));
+    ctx->tmp.resize(tb);
+    CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx->tmp.p, tb, in, out, n, ctx->stream));
+}
+template void cub_exclusive_sum<int64_t>(slm_ctx *, const int64_t *, int64_t *, int64_t);
+template void cub_exclusive_sum<int32_t>(slm_ctx *, const int32_t *, int32_t *, int64_t);
+
+void sort_pairs_u64_f64(slm_ctx *ctx, DBuf<uint64_t> &keys, DBuf<double> &vals, int64_t n,
+                        int end_bit) {
+    ctx->u64b.resize(n);
+    ctx->f64b.resize(n);
+    cub::DoubleBuffer<uint64_t> kb(keys.p, ctx->u64b.p);
+    cub::DoubleBuffer<double> vb(vals.p, ctx->f64b.p);
+    size_t tb = 0;
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, vb, n, 0, end_bit, ctx->stream));
+    ctx->tmp.resize(tb);
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(ctx->tmp.p, tb, kb, vb, n, 0, end_bit, ctx->stream));
+    if (kb.Current() != keys.p) keys.swap(ctx->u64b);
+    if (vb.Current() != vals.p) vals.swap(ctx->f64b);
+    keys.n = n;
+    vals.n = n;
+}
+
+void sort_pairs_u32_i32(slm_ctx *ctx, uint32_t *keys_in, uint32_t *keys_out, int32_t *vals_in,
+                        int32_t *vals_out, int64_t n, int end_bit) {
+    size_t tb = 0;
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys_in, keys_out, vals_in, vals_out, n,
+                                             0, end_bit, ctx->stream));
+    ctx->tmp.resize(tb);
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(ctx->tmp.p, tb, keys_in, keys_out, vals_in, vals_out,
+                                             n, 0, end_bit, ctx->stream));
+}
+
+// ------------------------------------------------------------------- kernels
+
+__global__ void k_validate(const int32_t *src, const int32_t *dst, const double *w, int64_t ne,
+                           int64_t n, int32_t *bad) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int32_t s = src[e], d = dst[e];
+        double x = w[e];
+        if (s < 0 || d < 0 || s >= n || d >= n) atomicOr(bad, 1);
+        if (!(x > 0.0) || !isfinite(x)) atomicOr(bad, 2);
+    }
+}
+
+__global__ void k_make_keys(const int32_t *src, const int32_t *dst, const double *w, int64_t ne,
+                            int b, uint64_t *keys, double *vals) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        keys[e] = ((uint64_t)(uint32_t)src[e] << b) | (uint32_t)dst[e];
+        vals[e] = w[e];
+    }
+}
+
+__global__ void k_run_heads(const uint64_t *keys, int64_t ne, int64_t *head) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne;
+         e += (int64_t)gridDim.x * blockDim.x)
+        head[e] = (e == 0 || keys[e] != keys[e - 1]) ? 1 : 0;
+}
+
+// one thread per run: out_w = first + pairwise(rest) (np.add.reduceat, graph.py:108)
+__global__ void k_merge_runs(const uint64_t *keys, const double *vals, const int64_t *gid,
+                             int64_t ne, int b, int32_t *out_src, int32_t *out_dst, double *out_w,
+                             uint32_t *integral_bad) {
+    const uint64_t mask = (b >= 64) ? ~0ull : ((1ull << b) - 1);
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        if (!(e == 0 || keys[e] != keys[e - 1])) continue;
+        int64_t end = e + 1;
+        while (end < ne && keys[end] == keys[e]) end++;
+        int64_t g = gid[e];
+        double s = reduceat_seq(vals + e, end - e);
+        out_w[g] = s;
+        out_src[g] = (int32_t)(keys[e] >> b);
+        out_dst[g] = (int32_t)(keys[e] & mask);
+        for (int64_t q = e; q < end; q++)
+            if (vals[q] != floor(vals[q])) atomicOr(integral_bad, 1u);
+    }
+}
+
+// ptr[r] = first index i with key_of(i) >= r over a sorted int32 array (n_rows + 1 entries)
+__global__ void k_lower_bound_ptr(const int32_t *sorted_rows, int64_t m, int64_t n_rows,
+                                  int64_t *ptr) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= n_rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = m;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            if (sorted_rows[mid] < r) lo = mid + 1;
+            else hi = mid;
+        }
+        ptr[r] = lo;
+    }
+}
+
+__global__ void k_iota_i32(int32_t *x, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = (int32_t)i;
+}
+
+__global__ void k_gather_transpose(const int32_t *perm, const int32_t *src, const double *w,
+                                   int64_t ne, int32_t *in_src, double *in_w) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < ne;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        int32_t e = perm[p];
+        in_src[p] = src[e];
+        in_w[p] = w[e];
+    }
+}
+
+__global__ void k_sym_check(const int64_t *optr, const int32_t *odst, const double *ow,
+                            const int64_t *iptr, const int32_t *isrc, const double *iw, int64_t n,
+                            int64_t ne, int32_t *asym) {
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = t; i <= n; i += stride)
+        if (optr[i] != iptr[i]) atomicOr(asym, 1);
+    for (int64_t e = t; e < ne; e += stride)
+        if (odst[e] != isrc[e] || ow[e] != iw[e]) atomicOr(asym, 1);
+}
+
+// symmetric graph: union = CSR minus self loops, u = w + w
+__global__ void k_keep_nonself(const int64_t *ptr, const int32_t *dst, int64_t n, int64_t *keep) {
+    // one warp per row
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    int lane = threadIdx.x & 31;
+    for (int64_t r = warp; r < n; r += nw)
+        for (int64_t e = ptr[r] + lane; e < ptr[r + 1]; e += 32) keep[e] = (dst[e] != r) ? 1 : 0;
+}
+
+__global__ void k_fill_union_sym(const int64_t *ptr, const int32_t *dst, const double *w,
+                                 const int64_t *pos, int64_t n, int64_t ne, int64_t ue,
+                                 int64_t *uptr, int32_t *unbr, double *uu) {
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    int lane = threadIdx.x & 31;
+    for (int64_t r = warp; r < n; r += nw) {
+        if (lane == 0) uptr[r] = (ptr[r] < ne) ? pos[ptr[r]] : ue;
+        for (int64_t e = ptr[r] + lane; e < ptr[r + 1]; e += 32)
+            if (dst[e] != r) {
+                int64_t q = pos[e];
+                unbr[q] = dst[e];
+                uu[q] = w[e] + w[e];
+            }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) uptr[n] = ue;
+}
+
+// directed graph: per-row merge of the out-row and the in-row (both sorted), self excluded.
+// pass 0 counts, pass 1 fills.  u = W(i,j) + W(j,i) with absent directions contributing
+// nothing (the reference's +0.0 is exact).
+__global__ void k_union_merge(const int64_t *optr, const int32_t *odst, const double *ow,
+                              const int64_t *iptr, const int32_t *isrc, const double *iw,
+                              int64_t n, int pass, int64_t *cnt_or_uptr, int32_t *unbr,
+                              double *uu) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        int64_t a = optr[r], ae = optr[r + 1], b = iptr[r], be = iptr[r + 1];
+        int64_t k = pass ? cnt_or_uptr[r] : 0;
+        for (;;) {
+            while (a < ae && odst[a] == r) a++;
+            while (b < be && isrc[b] == r) b++;
+            if (a >= ae && b >= be) break;
+            int32_t j;
+            double u;
+            if (b >= be || (a < ae && odst[a] < isrc[b])) {
+                j = odst[a]; u = ow[a]; a++;
+            } else if (a >= ae || isrc[b] < odst[a]) {
+                j = isrc[b]; u = iw[b]; b++;
+            } else {
+                j = odst[a]; u = ow[a] + iw[b]; a++; b++;
+            }
+            if (pass) { unbr[k] = j; uu[k] = u; }
+            k++;
+        }
+        if (!pass) cnt_or_uptr[r] = k;
+    }
+}
+
+// bincount order: sequential per row (graph.py:258-259)
+__global__ void k_row_seq_sum(const int64_t *ptr, const double *w, int64_t n, double *out) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int64_t e = ptr[r]; e < ptr[r + 1]; e++) s += w[e];
+        out[r] = s;
+    }
+}
+
+__global__ void k_pw_segments(const double *a, const int64_t *off, const int64_t *len, int64_t k,
+                              double *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = pw_sum_seq(a + off[i], len[i]);
+}
+
+__global__ void k_degree_bins(const int64_t *uptr, int64_t n, int64_t *flag_small,
+                              int64_t *flag_mid, int64_t *flag_large, int32_t *maxdeg) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        int64_t d = uptr[r + 1] - uptr[r];
+        flag_small[r] = (d >= 1 && d <= SMALL_MAX);
+        flag_mid[r] = (d > SMALL_MAX && d <= MID_MAX);
+        flag_large[r] = (d > MID_MAX);
+        if (d > 0) atomicMax(maxdeg, (int32_t)(d > 0x7fffffff ? 0x7fffffff : d));
+    }
+}
+
+__global__ void k_scatter_bin(const int64_t *flag, const int64_t *pos, int64_t n, int64_t base,
+                              int32_t *rows) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x)
+        if (flag[r]) rows[base + pos[r]] = (int32_t)r;
+}
+
+// ------------------------------------------------------------------- host side
+
+// numpy pairwise sum of a device array, bit-identical to ndarray.sum(): the host walks the
+// top of numpy's recursion down to segments of <= 32768 elements (each a node of the same
+// recursion), one device thread sums each segment with the identical recursion, and the host
+// recombines the partial sums in the recursion's order.
+static void pw_segments(int64_t off, int64_t n, std::vector<int64_t> &offs,
+                        std::vector<int64_t> &lens) {
+    if (n <= 32768) {
+        offs.push_back(off);
+        lens.push_back(n);
+        return;
+    }
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    pw_segments(off, n2, offs, lens);
+    pw_segments(off + n2, n - n2, offs, lens);
+}
+static double pw_combine(int64_t n, const double *vals, size_t &k) {
+    if (n <= 32768) return vals[k++];
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    double l = pw_combine(n2, vals, k);
+    double r = pw_combine(n - n2, vals, k);
+    return l + r;
+}
+
+double device_pairwise_sum(slm_ctx *ctx, const double *d_a, int64_t n) {
+    if (n == 0) return 0.0;
+    std::vector<int64_t> offs, lens;
+    pw_segments(0, n, offs, lens);
+    int64_t k = (int64_t)offs.size();
+    DBuf<int64_t> d_off, d_len;
+    DBuf<double> d_out;
+    d_off.resize(k);
+    d_len.resize(k);
+    d_out.resize(k);
+    CUDA_TRY(cudaMemcpyAsync(d_off.p, offs.data(), k * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(d_len.p, lens.data(), k * 8, cudaMemcpyHostToDevice, ctx->stream));
+    k_pw_segments<<<grid_for(k, 128), 128, 0, ctx->stream>>>(d_a, d_off.p, d_len.p, k, d_out.p);
+    std::vector<double> h(k);
+    CUDA_TRY(cudaMemcpyAsync(h.data(), d_out.p, k * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    size_t idx = 0;
+    return pw_combine(n, h.data(), idx);
+}
+
+static void build_bins(slm_ctx *ctx, LevelGraph &G) {
+    int64_t n = G.n;
+    cudaStream_t s = ctx->stream;
+    DBuf<int64_t> f[3], p[3];
+    for (int b = 0; b < 3; b++) {
+        f[b].resize(n + 1);
+        p[b].resize(n + 1);
+    }
+    int32_t *d_max = ctx->i32d.resize(1);
+    CUDA_TRY(cudaMemsetAsync(d_max, 0, 4, s));
+    k_degree_bins<<<grid_for(n, 256), 256, 0, s>>>(G.uptr.p, n, f[0].p, f[1].p, f[2].p, d_max);
+    int64_t tot[3];
+    for (int b = 0; b < 3; b++) {
+        CUDA_TRY(cudaMemsetAsync(f[b].p + n, 0, 8, s));
+        cub_exclusive_sum<int64_t>(ctx, f[b].p, p[b].p, n + 1);
+        CUDA_TRY(cudaMemcpyAsync(&tot[b], p[b].p + n, 8, cudaMemcpyDeviceToHost, s));
+    }
+    int32_t mx = 0;
+    CUDA_TRY(cudaMemcpyAsync(&mx, d_max, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    G.max_deg = mx;
+    G.bin_off[0] = 0;
+    for (int b = 0; b < 3; b++) G.bin_off[b + 1] = G.bin_off[b] + tot[b];
+    G.bin_rows.resize(G.bin_off[3] > 0 ? G.bin_off[3] : 1);
+    for (int b = 0; b < 3; b++)
+        if (tot[b])
+            k_scatter_bin<<<grid_for(n, 256), 256, 0, s>>>(f[b].p, p[b].p, n, G.bin_off[b],
+                                                            G.bin_rows.p);
+    // global hash scratch offsets for large rows (capacity next pow2 >= 2*deg)
+    int64_t nl = tot[2];
+    G.large_hash_total = 0;
+    if (nl) {
+        std::vector<int32_t> rows(nl);
+        std::vector<int64_t> up(n + 1);
+        CUDA_TRY(cudaMemcpyAsync(rows.data(), G.bin_rows.p + G.bin_off[2], nl * 4,
+                                 cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(up.data(), G.uptr.p, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        std::vector<int64_t> hoff(nl + 1);
+        int64_t acc = 0;
+        for (int64_t i = 0; i < nl; i++) {
+            int64_t d = up[rows[i] + 1] - up[rows[i]];
+            int64_t cap = 1;
+            while (cap < 2 * d) cap <<= 1;
+            hoff[i] = acc;
+            acc += cap;
+        }
+        hoff[nl] = acc;
+        G.large_hash_total = acc;
+        G.large_hoff.resize(nl + 1);
+        CUDA_TRY(cudaMemcpyAsync(G.large_hoff.p, hoff.data(), (nl + 1) * 8,
+                                 cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+    }
+}
+
+void build_level_from_keys(slm_ctx *ctx, LevelGraph &G, int64_t n, DBuf<uint64_t> &keys,
+                           DBuf<double> &vals, int64_t ne_in) {
+    cudaStream_t s = ctx->stream;
+    const int b = bits_for(n);
+    SLM_REQUIRE(n < (int64_t(1) << 31), SLM_EUNSUP, "more than 2^31-1 nodes");
+    G.n = n;
+    // 1. stable sort by (src, dst)
+    if (ne_in > 0) sort_pairs_u64_f64(ctx, keys, vals, ne_in, 2 * b);
+    // 2. run heads + group ids
+    DBuf<int64_t> head, gid;
+    head.resize(ne_in + 1);
+    gid.resize(ne_in + 1);
+    int64_t ng = 0;
+    uint32_t *d_int_bad = (uint32_t *)ctx->i32d.resize(2);
+    CUDA_TRY(cudaMemsetAsync(d_int_bad, 0, 8, s));
+    if (ne_in > 0) {
+        k_run_heads<<<grid_for(ne_in, 256), 256, 0, s>>>(keys.p, ne_in, head.p);
+        CUDA_TRY(cudaMemsetAsync(head.p + ne_in, 0, 8, s));
+        cub_exclusive_sum<int64_t>(ctx, head.p, gid.p, ne_in + 1);
+        CUDA_TRY(cudaMemcpyAsync(&ng, gid.p + ne_in, 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    SLM_REQUIRE(ng < (int64_t(1) << 31), SLM_EUNSUP, "more than 2^31-1 merged edges");
+    G.ne = ng;
+    DBuf<int32_t> src_of;
+    src_of.resize(ng);
+    G.csr_dst.resize(ng);
+    G.csr_w.resize(ng);
+    G.csr_ptr.resize(n + 1);
+    if (ne_in > 0)
+        k_merge_runs<<<grid_for(ne_in, 256), 256, 0, s>>>(keys.p, vals.p, gid.p, ne_in, b,
+                                                          src_of.p, G.csr_dst.p, G.csr_w.p,
+                                                          d_int_bad);
+    k_lower_bound_ptr<<<grid_for(n + 1, 256), 256, 0, s>>>(src_of.p, ng, n, G.csr_ptr.p);
+    head.release();
+    gid.release();
+    // 3. stable transpose (in-CSR, graph.py:111-115): sort entry ids by dst
+    DBuf<int64_t> in_ptr;
+    DBuf<int32_t> in_src;
+    DBuf<double> in_w;
+    in_ptr.resize(n + 1);
+    in_src.resize(ng);
+    in_w.resize(ng);
+    {
+        DBuf<int32_t> perm_in, perm_out, kout;
+        perm_in.resize(ng);
+        perm_out.resize(ng);
+        kout.resize(ng);
+        k_iota_i32<<<grid_for(ng, 256), 256, 0, s>>>(perm_in.p, ng);
+        if (ng > 0)
+            sort_pairs_u32_i32(ctx, (uint32_t *)G.csr_dst.p, (uint32_t *)kout.p, perm_in.p,
+                               perm_out.p, ng, b);
+        k_gather_transpose<<<grid_for(ng, 256), 256, 0, s>>>(perm_out.p, src_of.p, G.csr_w.p, ng,
+                                                             in_src.p, in_w.p);
+        k_lower_bound_ptr<<<grid_for(n + 1, 256), 256, 0, s>>>(kout.p, ng, n, in_ptr.p);
+    }
+    // 4. symmetric?
+    int32_t *d_asym = ctx->i32c.resize(1);
+    CUDA_TRY(cudaMemsetAsync(d_asym, 0, 4, s));
+    k_sym_check<<<grid_for(ng + n, 256), 256, 0, s>>>(G.csr_ptr.p, G.csr_dst.p, G.csr_w.p,
+                                                      in_ptr.p, in_src.p, in_w.p, n, ng, d_asym);
+    int32_t asym = 0;
+    uint32_t intbad[2] = {0, 0};
+    CUDA_TRY(cudaMemcpyAsync(&asym, d_asym, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(intbad, d_int_bad, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    G.sym = (asym == 0);
+    // 5. union
+    if (G.sym) {
+        DBuf<int64_t> keep, pos;
+        keep.resize(ng + 1);
+        pos.resize(ng + 1);
+        CUDA_TRY(cudaMemsetAsync(keep.p, 0, (ng + 1) * 8, s));
+        k_keep_nonself<<<grid_for(n * 32, 256), 256, 0, s>>>(G.csr_ptr.p, G.csr_dst.p, n, keep.p);
+        cub_exclusive_sum<int64_t>(ctx, keep.p, pos.p, ng + 1);
+        int64_t ue = 0;
+        CUDA_TRY(cudaMemcpyAsync(&ue, pos.p + ng, 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        G.ue = ue;
+        G.uptr.resize(n + 1);
+        G.unbr.resize(ue);
+        G.uu.resize(ue);
+        k_fill_union_sym<<<grid_for(n * 32, 256), 256, 0, s>>>(G.csr_ptr.p, G.csr_dst.p,
+                                                              G.csr_w.p, pos.p, n, ng, ue,
+                                                              G.uptr.p, G.unbr.p, G.uu.p);
+    } else {
+        DBuf<int64_t> cnt;
+        cnt.resize(n + 1);
+        CUDA_TRY(cudaMemsetAsync(cnt.p + n, 0, 8, s));
+        k_union_merge<<<grid_for(n, 128), 128, 0, s>>>(G.csr_ptr.p, G.csr_dst.p, G.csr_w.p,
+                                                       in_ptr.p, in_src.p, in_w.p, n, 0, cnt.p,
+                                                       nullptr, nullptr);
+        G.uptr.resize(n + 1);
+        cub_exclusive_sum<int64_t>(ctx, cnt.p, G.uptr.p, n + 1);
+        int64_t ue = 0;
+        CUDA_TRY(cudaMemcpyAsync(&ue, G.uptr.p + n, 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        G.ue = ue;
+        G.unbr.resize(ue);
+        G.uu.resize(ue);
+        k_union_merge<<<grid_for(n, 128), 128, 0, s>>>(G.csr_ptr.p, G.csr_dst.p, G.csr_w.p,
+                                                       in_ptr.p, in_src.p, in_w.p, n, 1,
+                                                       G.uptr.p, G.unbr.p, G.uu.p);
+    }
+    // 6. strengths
+    G.s_out.resize(n);
+    G.s_in.resize(n);
+    k_row_seq_sum<<<grid_for(n, 128), 128, 0, s>>>(G.csr_ptr.p, G.csr_w.p, n, G.s_out.p);
+    if (G.sym)
+        CUDA_TRY(cudaMemcpyAsync(G.s_in.p, G.s_out.p, n * 8, cudaMemcpyDeviceToDevice, s));
+    else
+        k_row_seq_sum<<<grid_for(n, 128), 128, 0, s>>>(in_ptr.p, in_w.p, n, G.s_in.p);
+    G.m_w = device_pairwise_sum(ctx, G.csr_w.p, ng);
+    G.integral = (intbad[0] == 0) && (G.m_w < 9007199254740992.0);
+    build_bins(ctx, G);
+    CUDA_TRY(cudaStreamSynchronize(s));
+}
+
+void build_level_from_edges(slm_ctx *ctx, LevelGraph &G, int64_t n, const int32_t *d_src,
+                            const int32_t *d_dst, const double *d_w, int64_t ne_in) {
+    cudaStream_t s = ctx->stream;
+    int32_t *d_bad = ctx->i32c.resize(1);
+    CUDA_TRY(cudaMemsetAsync(d_bad, 0, 4, s));
+    if (ne_in > 0)
+        k_validate<<<grid_for(ne_in, 256), 256, 0, s>>>(d_src, d_dst, d_w, ne_in, n, d_bad);
+    int32_t bad = 0;
+    CUDA_TRY(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    SLM_REQUIRE(!(bad & 1), SLM_EINVAL, "edge endpoint out of range");
+    SLM_REQUIRE(!(bad & 2), SLM_EINVAL, "edge weights must be finite and positive");
+    DBuf<uint64_t> keys;
+    DBuf<double> vals;
+    keys.resize(ne_in);
+    vals.resize(ne_in);
+    if (ne_in > 0)
+        k_make_keys<<<grid_for(ne_in, 256), 256, 0, s>>>(d_src, d_dst, d_w, ne_in, bits_for(n),
+                                                         keys.p, vals.p);
+    build_level_from_keys(ctx, G, n, keys, vals, ne_in);
+}

@@ -1,0 +1,448 @@
+// slm_capi.cu -- the extern "C" boundary (include/slm.h).  Every entry point catches
+// SlmError / CUDA failures, records the message in the context and returns a code.
+#include "slm_internal.cuh"
+#include "../../include/slm.h"
+#include <cstring>
+
+void gen_rmat_device(slm_ctx *ctx, int scale, int edge_factor, double a, double b, double c,
+                     uint64_t seed, int mode, DBuf<int32_t> &src, DBuf<int32_t> &dst,
+                     DBuf<double> &w, int64_t &ne);
+void gen_rgg_device(slm_ctx *ctx, int64_t n, double radius, uint64_t seed, DBuf<int32_t> &src,
+                    DBuf<int32_t> &dst, DBuf<double> &w, int64_t &ne);
+
+#define API_BEGIN try {
+#define API_END                                                                           \
+    }                                                                                     \
+    catch (const SlmError &e) {                                                           \
+        if (ctx) ctx->err = e.msg;                                                        \
+        return e.code;                                                                    \
+    }                                                                                     \
+    catch (const std::exception &e) {                                                     \
+        if (ctx) ctx->err = e.what();                                                     \
+        return SLM_ECUDA;                                                                 \
+    }                                                                                     \
+    return SLM_OK;
+
+static void require_graph(slm_ctx *ctx) {
+    SLM_REQUIRE(ctx->g != nullptr, SLM_ESTATE, "no graph loaded");
+}
+static void require_forest(slm_ctx *ctx) {
+    require_graph(ctx);
+    SLM_REQUIRE(ctx->f.n == ctx->g->n && ctx->f.a.p != nullptr && ctx->f.agg_valid &&
+                    ctx->f.layout_valid,
+                SLM_ESTATE, "no assignment forest for the current level");
+}
+static void require_agg(slm_ctx *ctx) {
+    require_graph(ctx);
+    SLM_REQUIRE(ctx->f.n == ctx->g->n && ctx->f.agg_valid, SLM_ESTATE,
+                "no community labels for the current level");
+}
+static double gain_m(slm_ctx *ctx) { return ctx->g->m_w / ctx->gamma; }
+
+__global__ void k_i64_to_i32(const int64_t *x, int64_t n, int32_t *y) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = (int32_t)x[i];
+}
+__global__ void k_i32_to_i64b(const int32_t *x, int64_t n, int64_t *y) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = x[i];
+}
+
+// host int64 -> device int32 (through a device staging buffer)
+static void upload_i64_as_i32(slm_ctx *ctx, const int64_t *h, int64_t n, int32_t *d) {
+    if (n == 0) return;
+    int64_t *tmp = ctx->i64a.resize(n);
+    CUDA_TRY(cudaMemcpyAsync(tmp, h, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    k_i64_to_i32<<<grid_for(n, 256), 256, 0, ctx->stream>>>(tmp, n, d);
+}
+static void download_i32_as_i64(slm_ctx *ctx, const int32_t *d, int64_t n, int64_t *h) {
+    if (n == 0 || !h) return;
+    int64_t *tmp = ctx->i64b.resize(n);
+    k_i32_to_i64b<<<grid_for(n, 256), 256, 0, ctx->stream>>>(d, n, tmp);
+    CUDA_TRY(cudaMemcpyAsync(h, tmp, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+}
+static void download_i64(slm_ctx *ctx, const int64_t *d, int64_t n, int64_t *h) {
+    if (n == 0 || !h) return;
+    CUDA_TRY(cudaMemcpyAsync(h, d, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+}
+
+static void new_level0(slm_ctx *ctx) {
+    ctx->g0 = std::make_shared<LevelGraph>();
+    ctx->g = ctx->g0;
+    ctx->level = 0;
+    ctx->f.n = -1;
+    ctx->f.agg_valid = ctx->f.layout_valid = false;
+    ctx->plan_version = ~0ull;
+}
+
+extern "C" {
+
+slm_ctx *slm_create(int device) {
+    slm_ctx *ctx = new slm_ctx();
+    ctx->device = device;
+    if (cudaSetDevice(device) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        delete ctx;
+        return nullptr;
+    }
+    return ctx;
+}
+
+void slm_destroy(slm_ctx *ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->g.reset();
+    ctx->g0.reset();
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+const char *slm_last_error(slm_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+void *slm_stream(slm_ctx *ctx) { return ctx ? (void *)ctx->stream : nullptr; }
+
+int slm_sync(slm_ctx *ctx) {
+    API_BEGIN
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    API_END
+}
+
+int slm_build_graph(slm_ctx *ctx, int64_t n, const int64_t *src, const int64_t *dst,
+                    const double *w, int64_t nedges) {
+    API_BEGIN
+    SLM_REQUIRE(n >= 0 && nedges >= 0, SLM_EINVAL, "negative size");
+    for (int64_t e = 0; e < nedges; e++)
+        SLM_REQUIRE(src[e] >= 0 && dst[e] >= 0 && src[e] < n && dst[e] < n, SLM_EINVAL,
+                    "edge endpoint out of range");
+    cudaSetDevice(ctx->device);
+    new_level0(ctx);
+    DBuf<int32_t> ds, dd;
+    DBuf<double> dw;
+    ds.resize(nedges);
+    dd.resize(nedges);
+    dw.resize(nedges);
+    upload_i64_as_i32(ctx, src, nedges, ds.p);
+    upload_i64_as_i32(ctx, dst, nedges, dd.p);
+    if (nedges)
+        CUDA_TRY(cudaMemcpyAsync(dw.p, w, nedges * 8, cudaMemcpyHostToDevice, ctx->stream));
+    build_level_from_edges(ctx, *ctx->g, n, ds.p, dd.p, dw.p, nedges);
+    API_END
+}
+
+int slm_build_graph_device(slm_ctx *ctx, int64_t n, const int32_t *d_src, const int32_t *d_dst,
+                           const double *d_w, int64_t nedges) {
+    API_BEGIN
+    cudaSetDevice(ctx->device);
+    new_level0(ctx);
+    build_level_from_edges(ctx, *ctx->g, n, d_src, d_dst, d_w, nedges);
+    API_END
+}
+
+int slm_build_rmat(slm_ctx *ctx, int scale, int edge_factor, double a, double b, double c,
+                   uint64_t seed, int weight_mode) {
+    API_BEGIN
+    cudaSetDevice(ctx->device);
+    new_level0(ctx);
+    DBuf<int32_t> s, d;
+    DBuf<double> w;
+    int64_t ne = 0;
+    gen_rmat_device(ctx, scale, edge_factor, a, b, c, seed, weight_mode, s, d, w, ne);
+    build_level_from_edges(ctx, *ctx->g, int64_t(1) << scale, s.p, d.p, w.p, ne);
+    API_END
+}
+
+int slm_build_rgg(slm_ctx *ctx, int64_t n, double radius, uint64_t seed) {
+    API_BEGIN
+    cudaSetDevice(ctx->device);
+    new_level0(ctx);
+    DBuf<int32_t> s, d;
+    DBuf<double> w;
+    int64_t ne = 0;
+    gen_rgg_device(ctx, n, radius, seed, s, d, w, ne);
+    build_level_from_edges(ctx, *ctx->g, n, s.p, d.p, w.p, ne);
+    API_END
+}
+
+int slm_graph_info(slm_ctx *ctx, int64_t *n, int64_t *ne, int64_t *ue, double *m_w,
+                   int32_t *flags) {
+    API_BEGIN
+    require_graph(ctx);
+    const LevelGraph &G = *ctx->g;
+    if (n) *n = G.n;
+    if (ne) *ne = G.ne;
+    if (ue) *ue = G.ue;
+    if (m_w) *m_w = G.m_w;
+    if (flags) *flags = (G.sym ? 1 : 0) | (G.integral ? 2 : 0);
+    API_END
+}
+
+int slm_get_csr(slm_ctx *ctx, int64_t *out_ptr, int64_t *out_dst, double *out_w) {
+    API_BEGIN
+    require_graph(ctx);
+    const LevelGraph &G = *ctx->g;
+    download_i64(ctx, G.csr_ptr.p, G.n + 1, out_ptr);
+    download_i32_as_i64(ctx, G.csr_dst.p, G.ne, out_dst);
+    if (out_w && G.ne)
+        CUDA_TRY(cudaMemcpyAsync(out_w, G.csr_w.p, G.ne * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    API_END
+}
+
+int slm_get_union(slm_ctx *ctx, int64_t *ptr, int64_t *nbr, double *u) {
+    API_BEGIN
+    require_graph(ctx);
+    const LevelGraph &G = *ctx->g;
+    download_i64(ctx, G.uptr.p, G.n + 1, ptr);
+    download_i32_as_i64(ctx, G.unbr.p, G.ue, nbr);
+    if (u && G.ue)
+        CUDA_TRY(cudaMemcpyAsync(u, G.uu.p, G.ue * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    API_END
+}
+
+int slm_get_strengths(slm_ctx *ctx, double *s_out, double *s_in) {
+    API_BEGIN
+    require_graph(ctx);
+    const LevelGraph &G = *ctx->g;
+    if (G.n) {
+        if (s_out)
+            CUDA_TRY(cudaMemcpyAsync(s_out, G.s_out.p, G.n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        if (s_in)
+            CUDA_TRY(cudaMemcpyAsync(s_in, G.s_in.p, G.n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    API_END
+}
+
+int slm_set_resolution(slm_ctx *ctx, double gamma) {
+    API_BEGIN
+    SLM_REQUIRE(gamma > 0.0 && std::isfinite(gamma), SLM_EINVAL, "resolution must be > 0");
+    ctx->gamma = gamma;
+    ctx->plan_version = ~0ull;
+    API_END
+}
+
+int slm_assign(slm_ctx *ctx, int64_t *a_out) {
+    API_BEGIN
+    require_graph(ctx);
+    const LevelGraph &G = *ctx->g;
+    Forest &F = ctx->f;
+    F.a.resize(G.n);
+    F.n = G.n;
+    F.agg_valid = F.layout_valid = false;
+    run_assign(ctx, G, gain_m(ctx), F.a.p);
+    download_i32_as_i64(ctx, F.a.p, G.n, a_out);
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    API_END
+}
+
+int slm_set_assignment(slm_ctx *ctx, const int64_t *a) {
+    API_BEGIN
+    require_graph(ctx);
+    const LevelGraph &G = *ctx->g;
+    for (int64_t i = 0; i < G.n; i++)
+        SLM_REQUIRE(a[i] >= 0 && a[i] < G.n, SLM_EINVAL, "assignment out of range");
+    Forest &F = ctx->f;
+    F.a.resize(G.n);
+    F.n = G.n;
+    upload_i64_as_i32(ctx, a, G.n, F.a.p);
+    forest_refresh(ctx, G, F);
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    API_END
+}
+
+static void copy_forest_out(slm_ctx *ctx, int64_t *a_out, int64_t *comm_out, uint8_t *oc_out,
+                            int64_t *n_comms) {
+    Forest &F = ctx->f;
+    download_i32_as_i64(ctx, F.a.p, F.n, a_out);
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    download_i32_as_i64(ctx, F.comm.p, F.n, comm_out);
+    if (oc_out && F.n)
+        CUDA_TRY(cudaMemcpyAsync(oc_out, F.on_cycle.p, F.n, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (n_comms) *n_comms = F.n_comms;
+}
+
+int slm_components(slm_ctx *ctx, int64_t *comm_out, uint8_t *on_cycle_out, int64_t *n_comms) {
+    API_BEGIN
+    require_graph(ctx);
+    Forest &F = ctx->f;
+    SLM_REQUIRE(F.n == ctx->g->n && F.a.p, SLM_ESTATE, "no assignment");
+    forest_refresh(ctx, *ctx->g, F);
+    copy_forest_out(ctx, nullptr, comm_out, on_cycle_out, n_comms);
+    API_END
+}
+
+int slm_get_forest(slm_ctx *ctx, int64_t *a_out, int64_t *comm_out, uint8_t *on_cycle_out,
+                   int64_t *n_comms) {
+    API_BEGIN
+    require_forest(ctx);
+    copy_forest_out(ctx, a_out, comm_out, on_cycle_out, n_comms);
+    API_END
+}
+
+int slm_get_aggregates(slm_ctx *ctx, double *S_out, double *S_in, int64_t *count) {
+    API_BEGIN
+    require_agg(ctx);
+    Forest &F = ctx->f;
+    int64_t nc = F.n_comms;
+    if (S_out) CUDA_TRY(cudaMemcpyAsync(S_out, F.S_out.p, nc * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    if (S_in) CUDA_TRY(cudaMemcpyAsync(S_in, F.S_in.p, nc * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    download_i32_as_i64(ctx, F.count.p, nc, count);
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    API_END
+}
+
+int slm_local_gains(slm_ctx *ctx, double *lg_out) {
+    API_BEGIN
+    require_agg(ctx);
+    const LevelGraph &G = *ctx->g;
+    DBuf<double> lg;
+    DBuf<uint8_t> bad;
+    lg.resize(G.n);
+    bad.resize(ctx->f.n_comms);
+    run_local_gains(ctx, G, ctx->f, gain_m(ctx), lg.p, bad.p);
+    if (lg_out && G.n)
+        CUDA_TRY(cudaMemcpyAsync(lg_out, lg.p, G.n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    API_END
+}
+
+int slm_positive(slm_ctx *ctx, const slm_config *cfg, int64_t *splits, int64_t *unresolved,
+                 int32_t *changed, double *gains_out, int64_t gains_cap) {
+    API_BEGIN
+    require_forest(ctx);
+    const LevelGraph &G = *ctx->g;
+    std::vector<double> gains;
+    int ch = 0;
+    int64_t sp = 0, un = 0;
+    run_positive(ctx, G, ctx->f, gain_m(ctx), cfg ? cfg->scc_cut_cap : 10000, &sp, &un, &ch,
+                 gains_out ? &gains : nullptr);
+    if (ch) forest_refresh(ctx, G, ctx->f);
+    if (splits) *splits = sp;
+    if (unresolved) *unresolved = un;
+    if (changed) *changed = ch;
+    if (gains_out)
+        for (int64_t k = 0; k < (int64_t)gains.size() && k < gains_cap; k++) gains_out[k] = gains[k];
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    API_END
+}
+
+int slm_plan_sweep(slm_ctx *ctx, const int64_t *comm_in, int64_t *cstar_out) {
+    API_BEGIN
+    require_graph(ctx);
+    const LevelGraph &G = *ctx->g;
+    Forest &F = ctx->f;
+    if (comm_in) {
+        // explicit snapshot: labels + aggregates from them (members/aggregates only)
+        int64_t mx = -1;
+        for (int64_t i = 0; i < G.n; i++) {
+            SLM_REQUIRE(comm_in[i] >= 0 && comm_in[i] < G.n, SLM_EINVAL, "labels out of range");
+            if (comm_in[i] > mx) mx = comm_in[i];
+        }
+        F.n = G.n;
+        F.comm.resize(G.n);
+        upload_i64_as_i32(ctx, comm_in, G.n, F.comm.p);
+        F.n_comms = mx + 1;
+        build_members_and_aggregates(ctx, G, F);
+        F.layout_valid = false;
+        F.version++;
+    } else {
+        require_forest(ctx);
+    }
+    ctx->cstar.resize(G.n);
+    run_plan(ctx, G, F, gain_m(ctx), ctx->cstar.p);
+    download_i32_as_i64(ctx, ctx->cstar.p, G.n, cstar_out);
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    API_END
+}
+
+int slm_maximal(slm_ctx *ctx, const slm_config *cfg, int64_t level, int64_t sweep,
+                int32_t *improved, int64_t *applied, double *gains_out, int64_t gains_cap) {
+    API_BEGIN
+    require_forest(ctx);
+    SLM_REQUIRE(cfg && cfg->accept_prob > 0.0 && cfg->accept_prob <= 1.0, SLM_EINVAL,
+                "accept_prob must be in (0, 1]");
+    const LevelGraph &G = *ctx->g;
+    Forest &F = ctx->f;
+    const double m = gain_m(ctx);
+    // the plan depends only on the forest: reuse it across coin-only sweeps (F7)
+    if (ctx->plan_version != F.version || ctx->cstar.n != (size_t)G.n) {
+        ctx->cstar.resize(G.n);
+        run_plan(ctx, G, F, m, ctx->cstar.p);
+        ctx->plan_version = F.version;
+    }
+    int imp = 0;
+    int64_t app = 0;
+    std::vector<double> gains;
+    run_commit(ctx, G, F, m, ctx->cstar.p, cfg->seed, cfg->accept_prob, level, sweep, &imp, &app,
+               gains_out ? &gains : nullptr);
+    if (app) forest_refresh(ctx, G, F);
+    if (improved) *improved = imp;
+    if (applied) *applied = app;
+    if (gains_out)
+        for (int64_t k = 0; k < (int64_t)gains.size() && k < gains_cap; k++) gains_out[k] = gains[k];
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    API_END
+}
+
+int slm_aggregate(slm_ctx *ctx) {
+    API_BEGIN
+    require_forest(ctx);
+    auto next = std::make_shared<LevelGraph>();
+    run_aggregate(ctx, *ctx->g, ctx->f.comm.p, ctx->f.n_comms, *next);
+    ctx->g = next;
+    ctx->level++;
+    ctx->f.n = -1;
+    ctx->f.agg_valid = ctx->f.layout_valid = false;
+    ctx->plan_version = ~0ull;
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    API_END
+}
+
+int slm_score(slm_ctx *ctx, int32_t on_original, const int64_t *labels, double gamma,
+              double *q_out) {
+    API_BEGIN
+    require_graph(ctx);
+    const LevelGraph &G = on_original ? *ctx->g0 : *ctx->g;
+    DBuf<int32_t> lab;
+    lab.resize(G.n);
+    for (int64_t i = 0; i < G.n; i++)
+        SLM_REQUIRE(labels[i] >= 0 && labels[i] < (int64_t(1) << 31), SLM_EINVAL, "bad label");
+    upload_i64_as_i32(ctx, labels, G.n, lab.p);
+    *q_out = run_score(ctx, G, lab.p, gamma);
+    API_END
+}
+
+__global__ void k_uniform(uint64_t base, const int64_t *ids, int64_t k, double *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = uniform01_at(base, ids[i]);
+}
+
+int slm_uniform01(slm_ctx *ctx, uint64_t seed, int64_t level, int64_t sweep, const int64_t *ids,
+                  int64_t k, double *out) {
+    API_BEGIN
+    if (k == 0) return SLM_OK;
+    DBuf<int64_t> d;
+    DBuf<double> o;
+    d.resize(k);
+    o.resize(k);
+    CUDA_TRY(cudaMemcpyAsync(d.p, ids, k * 8, cudaMemcpyHostToDevice, ctx->stream));
+    k_uniform<<<grid_for(k, 256), 256, 0, ctx->stream>>>(mix_key2(seed, level, sweep), d.p, k, o.p);
+    CUDA_TRY(cudaMemcpyAsync(out, o.p, k * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    API_END
+}
+
+int slm_last_commit_stats(slm_ctx *ctx, int64_t *candidates, int64_t *rounds) {
+    API_BEGIN
+    if (candidates) *candidates = ctx->last_candidates;
+    if (rounds) *rounds = ctx->last_rounds;
+    API_END
+}
+
+}  // extern "C"

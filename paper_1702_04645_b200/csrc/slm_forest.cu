@@ -1,0 +1,321 @@
+// slm_forest.cu -- assignment forest structure on the device.
+//
+//   extract_components (forest.py:43-67)   -> run_components: cycle detection, root
+//       pointers, min-cycle-id key, canonical dense labels by smallest member
+//       (canonicalize_labels, graph.py:283-291).
+//   community_members (forest.py:33-40) and CommunityAggregates.from_labels
+//       (quality.py:71-79)                  -> build_members_and_aggregates: stable
+//       sort of node ids by community; per-community sums in ascending node order
+//       (bincount's sequential order, bit-exact even for real weights).
+//   reverse_assignment (forest.py:70-80)   -> build_layout: children CSR (kids ascending)
+//       plus a DFS pre-order layout of every community rooted at its smallest cycle node,
+//       so that every assignment tail (detector.py:421-437) and every branch subtree
+//       (detector.py:238-253) is one contiguous range.
+//
+// Fast path: cycles of the forest have length <= 2, so a node is on a cycle
+// iff a[i] == i or a[a[i]] == i; every other node walks / pointer-jumps to its cycle.
+// Arbitrary functional graphs (longer cycles) fall back to the reference's pointer
+// doubling, so extract_components keeps its full contract.
+#include "slm_internal.cuh"
+#include <cub/cub.cuh>
+
+#define GS_LOOP(i, n)                                                                      \
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n);              \
+         i += (int64_t)gridDim.x * blockDim.x)
+
+__global__ void k_cyc2(const int32_t *a, int64_t n, uint8_t *c2) {
+    GS_LOOP(i, n) {
+        int32_t x = a[i];
+        c2[i] = (x == i) || (a[x] == i);
+    }
+}
+
+__global__ void k_walk(const int32_t *a, const uint8_t *c2, int64_t n, int cap, int32_t *root,
+                       int32_t *fail) {
+    GS_LOOP(i, n) {
+        int32_t x = (int32_t)i;
+        int s = 0;
+        while (!c2[x] && s < cap) {
+            x = a[x];
+            s++;
+        }
+        if (c2[x]) root[i] = x;
+        else {
+            root[i] = -1;
+            *fail = 1;
+        }
+    }
+}
+
+__global__ void k_jump_init(const int32_t *a, const uint8_t *c2, const int32_t *root, int64_t n,
+                            int32_t *r) {
+    GS_LOOP(i, n) r[i] = root[i] >= 0 ? root[i] : (c2[i] ? (int32_t)i : a[i]);
+}
+
+__global__ void k_jump(const int32_t *rin, int64_t n, int32_t *rout, int32_t *changed) {
+    GS_LOOP(i, n) {
+        int32_t x = rin[i], y = rin[x];
+        rout[i] = y;
+        if (y != x) *changed = 1;
+    }
+}
+
+__global__ void k_key_from_root(const int32_t *a, const int32_t *root, const uint8_t *c2,
+                                int64_t n, int32_t *key, uint8_t *on_cycle, int32_t *bad) {
+    GS_LOOP(i, n) {
+        int32_t r = root[i];
+        if (!c2[r]) *bad = 1;
+        int32_t ar = a[r];
+        key[i] = ar < r ? ar : r;
+        on_cycle[i] = c2[i];
+    }
+}
+
+// general path (forest.py:51-65): f = a^(2^k), on_cycle[f] = 1, minv propagation
+__global__ void k_copy_i32(const int32_t *x, int64_t n, int32_t *y) { GS_LOOP(i, n) y[i] = x[i]; }
+__global__ void k_square(const int32_t *f, int64_t n, int32_t *g) { GS_LOOP(i, n) g[i] = f[f[i]]; }
+__global__ void k_mark_cycle(const int32_t *f, int64_t n, uint8_t *on_cycle) {
+    GS_LOOP(i, n) on_cycle[f[i]] = 1;
+}
+__global__ void k_minv_step(const int32_t *minv, const int32_t *hop, int64_t n, int32_t *minv2,
+                            int32_t *hop2) {
+    GS_LOOP(i, n) {
+        int32_t h = hop[i];
+        int32_t v = minv[i], w = minv[h];
+        minv2[i] = w < v ? w : v;
+        hop2[i] = hop[h];
+    }
+}
+
+__global__ void k_fill_i32(int32_t *x, int64_t n, int32_t v) { GS_LOOP(i, n) x[i] = v; }
+
+__global__ void k_first_occ(const int32_t *key, int64_t n, int32_t *first) {
+    GS_LOOP(i, n) atomicMin(&first[key[i]], (int32_t)i);
+}
+__global__ void k_head_flag(const int32_t *key, const int32_t *first, int64_t n, int32_t *h) {
+    GS_LOOP(i, n) h[i] = (first[key[i]] == (int32_t)i) ? 1 : 0;
+}
+__global__ void k_assign_label(const int32_t *key, const int32_t *first, const int32_t *lab,
+                               int64_t n, int32_t *comm) {
+    GS_LOOP(i, n) comm[i] = lab[first[key[i]]];
+}
+
+__global__ void k_iota(int32_t *x, int64_t n) { GS_LOOP(i, n) x[i] = (int32_t)i; }
+
+__global__ void k_lb_ptr32(const int32_t *sorted, int64_t m, int64_t nrows, int32_t *ptr) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= nrows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = m;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            if (sorted[mid] < r) lo = mid + 1;
+            else hi = mid;
+        }
+        ptr[r] = (int32_t)lo;
+    }
+}
+
+// per-community sums in ascending member order (bincount order, quality.py:76-78)
+__global__ void k_comm_sums(const int32_t *cptr, const int32_t *members, const double *s_out,
+                            const double *s_in, int64_t nc, double *S_out, double *S_in,
+                            int32_t *count) {
+    GS_LOOP(c, nc) {
+        double so = 0.0, si = 0.0;
+        for (int32_t k = cptr[c]; k < cptr[c + 1]; k++) {
+            int32_t x = members[k];
+            so += s_out[x];
+            si += s_in[x];
+        }
+        S_out[c] = so;
+        S_in[c] = si;
+        count[c] = cptr[c + 1] - cptr[c];
+    }
+}
+
+__global__ void k_kid_keys(const int32_t *a, int64_t n, uint32_t *key) {
+    GS_LOOP(i, n) key[i] = (a[i] != (int32_t)i) ? (uint32_t)a[i] : (uint32_t)n;
+}
+
+// one thread per community: iterative DFS pre-order from the smallest cycle node
+__global__ void k_dfs_layout(const int32_t *cptr, const int32_t *members, const uint8_t *on_cycle,
+                             const int32_t *kptr, const int32_t *kids, int64_t nc, int32_t *order,
+                             int32_t *pos, int32_t *sz, int32_t *stk_node, int32_t *stk_it) {
+    GS_LOOP(c, nc) {
+        int32_t base = cptr[c], end = cptr[c + 1];
+        int32_t root = members[base];
+        for (int32_t k = base; k < end; k++)
+            if (on_cycle[members[k]]) {
+                root = members[k];
+                break;
+            }
+        int32_t cnt = 0, sp = 0;
+        order[base] = root;
+        pos[root] = 0;
+        cnt = 1;
+        stk_node[base] = root;
+        stk_it[base] = kptr[root];
+        sp = 1;
+        while (sp > 0) {
+            int32_t v = stk_node[base + sp - 1];
+            int32_t it = stk_it[base + sp - 1];
+            if (it < kptr[v + 1]) {
+                int32_t k = kids[it];
+                stk_it[base + sp - 1] = it + 1;
+                if (k == root) continue;
+                order[base + cnt] = k;
+                pos[k] = cnt;
+                cnt++;
+                stk_node[base + sp] = k;
+                stk_it[base + sp] = kptr[k];
+                sp++;
+            } else {
+                sz[v] = cnt - pos[v];
+                sp--;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------- host
+
+void run_components(slm_ctx *ctx, Forest &F, int64_t n) {
+    cudaStream_t s = ctx->stream;
+    F.n = n;
+    F.comm.resize(n);
+    F.on_cycle.resize(n);
+    if (n == 0) {
+        F.n_comms = 0;
+        return;
+    }
+    DBuf<uint8_t> c2;
+    c2.resize(n);
+    int32_t *root = ctx->i32a.resize(n);
+    int32_t *key = ctx->i32b.resize(n);
+    int32_t *flags = ctx->i32d.resize(4);
+    CUDA_TRY(cudaMemsetAsync(flags, 0, 16, s));
+    unsigned G = grid_for(n, 256);
+    k_cyc2<<<G, 256, 0, s>>>(F.a.p, n, c2.p);
+    k_walk<<<G, 256, 0, s>>>(F.a.p, c2.p, n, 64, root, flags);
+    int32_t hf[4];
+    CUDA_TRY(cudaMemcpyAsync(hf, flags, 16, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    bool general = false;
+    if (hf[0]) {
+        // deep trees: pointer jumping on root pointers
+        int32_t *cur = ctx->i32c.resize(n);
+        int32_t *nxt = root;
+        k_jump_init<<<G, 256, 0, s>>>(F.a.p, c2.p, root, n, cur);
+        int rounds = 0;
+        for (;;) {
+            CUDA_TRY(cudaMemsetAsync(flags + 1, 0, 4, s));
+            k_jump<<<G, 256, 0, s>>>(cur, n, nxt, flags + 1);
+            std::swap(cur, nxt);
+            CUDA_TRY(cudaMemcpyAsync(hf, flags, 16, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            if (!hf[1] || ++rounds > 40) break;
+        }
+        if (cur != ctx->i32a.p)
+            CUDA_TRY(cudaMemcpyAsync(ctx->i32a.p, cur, n * 4, cudaMemcpyDeviceToDevice, s));
+        root = ctx->i32a.p;
+        general = hf[1] != 0;
+    }
+    if (!general) {
+        CUDA_TRY(cudaMemsetAsync(flags + 2, 0, 4, s));
+        k_key_from_root<<<G, 256, 0, s>>>(F.a.p, root, c2.p, n, key, F.on_cycle.p, flags + 2);
+        CUDA_TRY(cudaMemcpyAsync(hf, flags, 16, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        general = hf[2] != 0;   // some root is not on a <=2 cycle: longer cycles exist
+    }
+    if (general) {
+        // the reference's pointer doubling (forest.py:51-65)
+        int32_t *f = ctx->i32a.resize(n), *g = ctx->i32c.resize(n);
+        k_copy_i32<<<G, 256, 0, s>>>(F.a.p, n, f);
+        for (int64_t steps = 1; steps < n; steps *= 2) {
+            k_square<<<G, 256, 0, s>>>(f, n, g);
+            std::swap(f, g);
+        }
+        CUDA_TRY(cudaMemsetAsync(F.on_cycle.p, 0, n, s));
+        k_mark_cycle<<<G, 256, 0, s>>>(f, n, F.on_cycle.p);
+        DBuf<int32_t> hop, hop2, mv2;
+        hop.resize(n);
+        hop2.resize(n);
+        mv2.resize(n);
+        int32_t *minv = key;
+        k_copy_i32<<<G, 256, 0, s>>>(f, n, minv);
+        k_copy_i32<<<G, 256, 0, s>>>(F.a.p, n, hop.p);
+        int32_t *m1 = minv, *m2 = mv2.p, *h1 = hop.p, *h2 = hop2.p;
+        for (int64_t steps = 1; steps < n; steps *= 2) {
+            k_minv_step<<<G, 256, 0, s>>>(m1, h1, n, m2, h2);
+            std::swap(m1, m2);
+            std::swap(h1, h2);
+        }
+        if (m1 != key) CUDA_TRY(cudaMemcpyAsync(key, m1, n * 4, cudaMemcpyDeviceToDevice, s));
+    }
+    // canonical labels ordered by smallest member
+    int32_t *first = ctx->i32c.resize(n);
+    k_fill_i32<<<G, 256, 0, s>>>(first, n, 0x7fffffff);
+    k_first_occ<<<G, 256, 0, s>>>(key, n, first);
+    DBuf<int32_t> h, lab;
+    h.resize(n + 1);
+    lab.resize(n + 1);
+    CUDA_TRY(cudaMemsetAsync(h.p + n, 0, 4, s));
+    k_head_flag<<<G, 256, 0, s>>>(key, first, n, h.p);
+    cub_exclusive_sum<int32_t>(ctx, h.p, lab.p, n + 1);
+    k_assign_label<<<G, 256, 0, s>>>(key, first, lab.p, n, F.comm.p);
+    int32_t nc = 0;
+    CUDA_TRY(cudaMemcpyAsync(&nc, lab.p + n, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    F.n_comms = nc;
+    F.layout_valid = false;
+    F.agg_valid = false;
+}
+
+void build_members_and_aggregates(slm_ctx *ctx, const LevelGraph &G, Forest &F) {
+    cudaStream_t s = ctx->stream;
+    int64_t n = F.n, nc = F.n_comms;
+    F.members.resize(n);
+    F.cptr.resize(nc + 1);
+    F.S_out.resize(nc);
+    F.S_in.resize(nc);
+    F.count.resize(nc);
+    int32_t *iota = ctx->i32a.resize(n);
+    int32_t *ksorted = ctx->i32b.resize(n);
+    k_iota<<<grid_for(n, 256), 256, 0, s>>>(iota, n);
+    if (n > 0)
+        sort_pairs_u32_i32(ctx, (uint32_t *)F.comm.p, (uint32_t *)ksorted, iota, F.members.p, n,
+                           bits_for(nc + 1));
+    k_lb_ptr32<<<grid_for(nc + 1, 256), 256, 0, s>>>(ksorted, n, nc, F.cptr.p);
+    k_comm_sums<<<grid_for(nc, 128), 128, 0, s>>>(F.cptr.p, F.members.p, G.s_out.p, G.s_in.p, nc,
+                                                  F.S_out.p, F.S_in.p, F.count.p);
+    F.agg_valid = true;
+}
+
+void build_layout(slm_ctx *ctx, Forest &F) {
+    cudaStream_t s = ctx->stream;
+    int64_t n = F.n, nc = F.n_comms;
+    F.kptr.resize(n + 1);
+    F.kids.resize(n);
+    F.order.resize(n);
+    F.pos.resize(n);
+    F.sz.resize(n);
+    uint32_t *kk = (uint32_t *)ctx->i32a.resize(n);
+    uint32_t *ks = (uint32_t *)ctx->i32b.resize(n);
+    int32_t *iota = ctx->i32c.resize(n);
+    k_kid_keys<<<grid_for(n, 256), 256, 0, s>>>(F.a.p, n, kk);
+    k_iota<<<grid_for(n, 256), 256, 0, s>>>(iota, n);
+    if (n > 0) sort_pairs_u32_i32(ctx, kk, ks, iota, F.kids.p, n, bits_for(n + 1));
+    k_lb_ptr32<<<grid_for(n + 1, 256), 256, 0, s>>>((const int32_t *)ks, n, n, F.kptr.p);
+    int32_t *stk_node = ctx->i32a.resize(n);
+    int32_t *stk_it = ctx->i32b.resize(n);
+    k_dfs_layout<<<grid_for(nc, 64), 64, 0, s>>>(F.cptr.p, F.members.p, F.on_cycle.p, F.kptr.p,
+                                                 F.kids.p, nc, F.order.p, F.pos.p, F.sz.p,
+                                                 stk_node, stk_it);
+    F.layout_valid = true;
+}
+
+void forest_refresh(slm_ctx *ctx, const LevelGraph &G, Forest &F) {
+    run_components(ctx, F, G.n);
+    build_members_and_aggregates(ctx, G, F);
+    build_layout(ctx, F);
+    F.version++;
+}

@@ -1,0 +1,278 @@
+// slm_gen.cu -- counter-based generators for the BASELINE.json synthetic graphs.
+//
+// Every random draw is a pure hash of (seed, edge or point id, stream), evaluated by the
+// same __host__ __device__ code on the CPU and on the GPU, so the device-generated graph
+// used by the bench and the host-generated edge list handed to the CPU oracle are the same
+// edge multiset ("the oracle and the GPU consume the same edge list").
+#include "slm_internal.cuh"
+#include "../../include/slm.h"
+#include <cub/cub.cuh>
+#include <cmath>
+
+#define GS_LOOP(i, n)                                                                      \
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n);              \
+         i += (int64_t)gridDim.x * blockDim.x)
+
+__host__ __device__ inline uint64_t gen_base(uint64_t seed) {
+    return fin64(seed ^ 0x5851F42D4C957F2DULL);
+}
+__host__ __device__ inline double u01_of(uint64_t h) { return (double)(h >> 11) * 0x1.0p-53; }
+
+// bijective mixing of [0, 2^scale): odd multiply, xor-shift, add (each a bijection mod 2^k)
+__host__ __device__ inline uint64_t perm_id(uint64_t x, int scale, uint64_t base) {
+    const uint64_t mask = (scale >= 64) ? ~0ull : ((1ull << scale) - 1);
+    const int sh = (scale + 1) / 2;
+    for (int r = 0; r < 3; r++) {
+        uint64_t k = fin64(base + 0x1000ull + (uint64_t)r);
+        x = (x * (k | 1ull)) & mask;
+        x ^= x >> sh;
+        x = (x + (k >> 17)) & mask;
+    }
+    return x;
+}
+
+// R-MAT edge k: quadrant recursion with thresholds a, a+b, a+b+c (no noise)
+__host__ __device__ inline void rmat_edge(uint64_t base, int scale, int64_t k, double t1, double t2,
+                                          double t3, uint64_t &s, uint64_t &d, uint64_t &wh) {
+    const uint64_t kb = fin64(base + (uint64_t)k * RNG_GAMMA);
+    s = 0;
+    d = 0;
+    for (int l = 0; l < scale; l++) {
+        double u = u01_of(fin64(kb + (uint64_t)(l + 1) * RNG_MIX1));
+        int q = u < t1 ? 0 : (u < t2 ? 1 : (u < t3 ? 2 : 3));
+        s = (s << 1) | (uint64_t)(q >> 1);
+        d = (d << 1) | (uint64_t)(q & 1);
+    }
+    s = perm_id(s, scale, base);
+    d = perm_id(d, scale, base);
+    wh = fin64(kb + RNG_MIX2);
+}
+
+__host__ __device__ inline double rmat_weight(int mode, uint64_t wh) {
+    return mode ? (double)(1 + (wh % 100ull)) : 1.0;
+}
+
+// --------------------------------------------------------------------- host
+
+extern "C" int slm_gen_rmat_host(int scale, int edge_factor, double a, double b, double c,
+                                 uint64_t seed, int weight_mode, int64_t *src, int64_t *dst,
+                                 double *w, int64_t *n_edges) {
+    const uint64_t base = gen_base(seed);
+    const int64_t m = (int64_t)edge_factor << scale;
+    const double t1 = a, t2 = a + b, t3 = a + b + c;
+    int64_t cnt = 0;
+    for (int64_t k = 0; k < m; k++) {
+        uint64_t s, d, wh;
+        rmat_edge(base, scale, k, t1, t2, t3, s, d, wh);
+        if (s == d) continue;
+        if (src) {
+            double x = rmat_weight(weight_mode, wh);
+            src[cnt] = (int64_t)s; dst[cnt] = (int64_t)d; w[cnt] = x;
+            src[cnt + 1] = (int64_t)d; dst[cnt + 1] = (int64_t)s; w[cnt + 1] = x;
+        }
+        cnt += 2;
+    }
+    *n_edges = cnt;
+    return SLM_OK;
+}
+
+__host__ __device__ inline void rgg_point(uint64_t base, int64_t i, double &x, double &y) {
+    uint64_t h1 = fin64(base + (uint64_t)i * RNG_GAMMA);
+    uint64_t h2 = fin64(h1 ^ RNG_MIX2);
+    x = u01_of(h1);
+    y = u01_of(h2);
+}
+__host__ __device__ inline int rgg_cell(double v, int G) {
+    int c = (int)(v * G);
+    return c >= G ? G - 1 : c;
+}
+
+extern "C" int slm_gen_rgg_host(int64_t n, double radius, uint64_t seed, int64_t *src,
+                                int64_t *dst, double *w, int64_t *n_edges) {
+    const uint64_t base = gen_base(seed);
+    int G = (int)std::floor(1.0 / radius);
+    if (G < 1) G = 1;
+    const double r2 = radius * radius;
+    std::vector<double> X(n), Y(n);
+    std::vector<int64_t> cell(n), cptr((size_t)G * G + 1, 0), pts(n);
+    for (int64_t i = 0; i < n; i++) {
+        rgg_point(base, i, X[i], Y[i]);
+        cell[i] = (int64_t)rgg_cell(Y[i], G) * G + rgg_cell(X[i], G);
+        cptr[cell[i] + 1]++;
+    }
+    for (size_t k = 0; k + 1 < cptr.size(); k++) cptr[k + 1] += cptr[k];
+    {
+        std::vector<int64_t> fill(cptr.begin(), cptr.end() - 1);
+        for (int64_t i = 0; i < n; i++) pts[fill[cell[i]]++] = i;
+    }
+    int64_t cnt = 0;
+    for (int64_t i = 0; i < n; i++) {
+        int cx = (int)(cell[i] % G), cy = (int)(cell[i] / G);
+        for (int dy = -1; dy <= 1; dy++)
+            for (int dx = -1; dx <= 1; dx++) {
+                int ux = cx + dx, uy = cy + dy;
+                if (ux < 0 || uy < 0 || ux >= G || uy >= G) continue;
+                int64_t cc = (int64_t)uy * G + ux;
+                for (int64_t q = cptr[cc]; q < cptr[cc + 1]; q++) {
+                    int64_t j = pts[q];
+                    if (j == i) continue;
+                    double ddx = X[i] - X[j], ddy = Y[i] - Y[j];
+                    if (ddx * ddx + ddy * ddy < r2) {
+                        if (src) {
+                            src[cnt] = i;
+                            dst[cnt] = j;
+                            w[cnt] = 1.0;
+                        }
+                        cnt++;
+                    }
+                }
+            }
+    }
+    *n_edges = cnt;
+    return SLM_OK;
+}
+
+// ------------------------------------------------------------------- device
+
+__global__ void k_rmat_count(uint64_t base, int scale, int64_t m, double t1, double t2, double t3,
+                             int32_t *keep) {
+    GS_LOOP(k, m) {
+        uint64_t s, d, wh;
+        rmat_edge(base, scale, k, t1, t2, t3, s, d, wh);
+        keep[k] = (s != d) ? 1 : 0;
+    }
+}
+__global__ void k_rmat_fill(uint64_t base, int scale, int64_t m, double t1, double t2, double t3,
+                            int mode, const int64_t *pos, int32_t *src, int32_t *dst, double *w) {
+    GS_LOOP(k, m) {
+        uint64_t s, d, wh;
+        rmat_edge(base, scale, k, t1, t2, t3, s, d, wh);
+        if (s == d) continue;
+        int64_t p = 2 * pos[k];
+        double x = rmat_weight(mode, wh);
+        src[p] = (int32_t)s; dst[p] = (int32_t)d; w[p] = x;
+        src[p + 1] = (int32_t)d; dst[p + 1] = (int32_t)s; w[p + 1] = x;
+    }
+}
+__global__ void k_i32_to_i64(const int32_t *x, int64_t n, int64_t *y) { GS_LOOP(i, n) y[i] = x[i]; }
+
+void gen_rmat_device(slm_ctx *ctx, int scale, int edge_factor, double a, double b, double c,
+                     uint64_t seed, int mode, DBuf<int32_t> &src, DBuf<int32_t> &dst,
+                     DBuf<double> &w, int64_t &ne) {
+    cudaStream_t s = ctx->stream;
+    const uint64_t base = gen_base(seed);
+    const int64_t m = (int64_t)edge_factor << scale;
+    const double t1 = a, t2 = a + b, t3 = a + b + c;
+    DBuf<int32_t> keep;
+    DBuf<int64_t> keep64, pos;
+    keep.resize(m);
+    keep64.resize(m + 1);
+    pos.resize(m + 1);
+    k_rmat_count<<<grid_for(m, 256), 256, 0, s>>>(base, scale, m, t1, t2, t3, keep.p);
+    k_i32_to_i64<<<grid_for(m, 256), 256, 0, s>>>(keep.p, m, keep64.p);
+    CUDA_TRY(cudaMemsetAsync(keep64.p + m, 0, 8, s));
+    keep.release();
+    cub_exclusive_sum<int64_t>(ctx, keep64.p, pos.p, m + 1);
+    int64_t kept = 0;
+    CUDA_TRY(cudaMemcpyAsync(&kept, pos.p + m, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    keep64.release();
+    ne = 2 * kept;
+    src.resize(ne);
+    dst.resize(ne);
+    w.resize(ne);
+    k_rmat_fill<<<grid_for(m, 256), 256, 0, s>>>(base, scale, m, t1, t2, t3, mode, pos.p, src.p,
+                                                 dst.p, w.p);
+    CUDA_TRY(cudaGetLastError());
+}
+
+__global__ void k_rgg_points(uint64_t base, int64_t n, int G, double *X, double *Y, uint32_t *cell,
+                             int32_t *iota) {
+    GS_LOOP(i, n) {
+        double x, y;
+        rgg_point(base, i, x, y);
+        X[i] = x;
+        Y[i] = y;
+        cell[i] = (uint32_t)((int64_t)rgg_cell(y, G) * G + rgg_cell(x, G));
+        iota[i] = (int32_t)i;
+    }
+}
+__global__ void k_rgg_pass(const double *X, const double *Y, const int32_t *cptr,
+                           const int32_t *pts, int64_t n, int G, double r2, const int64_t *pos,
+                           int64_t *cnt, int32_t *src, int32_t *dst, double *w) {
+    GS_LOOP(i, n) {
+        const double xi = X[i], yi = Y[i];
+        const int cx = rgg_cell(xi, G), cy = rgg_cell(yi, G);
+        int64_t k = pos ? pos[i] : 0;
+        for (int dy = -1; dy <= 1; dy++)
+            for (int dx = -1; dx <= 1; dx++) {
+                int ux = cx + dx, uy = cy + dy;
+                if (ux < 0 || uy < 0 || ux >= G || uy >= G) continue;
+                int64_t cc = (int64_t)uy * G + ux;
+                for (int32_t q = cptr[cc]; q < cptr[cc + 1]; q++) {
+                    int32_t j = pts[q];
+                    if (j == i) continue;
+                    double ddx = xi - X[j], ddy = yi - Y[j];
+                    if (ddx * ddx + ddy * ddy < r2) {
+                        if (pos) {
+                            src[k] = (int32_t)i;
+                            dst[k] = j;
+                            w[k] = 1.0;
+                        }
+                        k++;
+                    }
+                }
+            }
+        if (!pos) cnt[i] = k;
+    }
+}
+__global__ void k_lb_cells(const uint32_t *sorted, int64_t m, int64_t nrows, int32_t *ptr) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= nrows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = m;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            if ((int64_t)sorted[mid] < r) lo = mid + 1;
+            else hi = mid;
+        }
+        ptr[r] = (int32_t)lo;
+    }
+}
+
+void gen_rgg_device(slm_ctx *ctx, int64_t n, double radius, uint64_t seed, DBuf<int32_t> &src,
+                    DBuf<int32_t> &dst, DBuf<double> &w, int64_t &ne) {
+    cudaStream_t s = ctx->stream;
+    const uint64_t base = gen_base(seed);
+    int G = (int)std::floor(1.0 / radius);
+    if (G < 1) G = 1;
+    const int64_t ncell = (int64_t)G * G;
+    DBuf<double> X, Y;
+    DBuf<uint32_t> cell, cell_sorted;
+    DBuf<int32_t> iota, pts, cptr;
+    X.resize(n);
+    Y.resize(n);
+    cell.resize(n);
+    cell_sorted.resize(n);
+    iota.resize(n);
+    pts.resize(n);
+    cptr.resize(ncell + 1);
+    k_rgg_points<<<grid_for(n, 256), 256, 0, s>>>(base, n, G, X.p, Y.p, cell.p, iota.p);
+    sort_pairs_u32_i32(ctx, cell.p, cell_sorted.p, iota.p, pts.p, n, bits_for(ncell + 1));
+    k_lb_cells<<<grid_for(ncell + 1, 256), 256, 0, s>>>(cell_sorted.p, n, ncell, cptr.p);
+    DBuf<int64_t> cnt, pos;
+    cnt.resize(n + 1);
+    pos.resize(n + 1);
+    CUDA_TRY(cudaMemsetAsync(cnt.p + n, 0, 8, s));
+    const double r2 = radius * radius;
+    k_rgg_pass<<<grid_for(n, 128), 128, 0, s>>>(X.p, Y.p, cptr.p, pts.p, n, G, r2, nullptr, cnt.p,
+                                                nullptr, nullptr, nullptr);
+    cub_exclusive_sum<int64_t>(ctx, cnt.p, pos.p, n + 1);
+    CUDA_TRY(cudaMemcpyAsync(&ne, pos.p + n, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    src.resize(ne);
+    dst.resize(ne);
+    w.resize(ne);
+    k_rgg_pass<<<grid_for(n, 128), 128, 0, s>>>(X.p, Y.p, cptr.p, pts.p, n, G, r2, pos.p, nullptr,
+                                                src.p, dst.p, w.p);
+    CUDA_TRY(cudaGetLastError());
+}

@@ -1,0 +1,266 @@
+// slm_internal.cuh -- shared device/host plumbing of the sm_100a SLM library.
+//
+// Compiled with -fmad=false: every fp64 gain expression below is evaluated with the
+// reference's operand order and IEEE rounding of each + - * /, never contracted to FMA,
+// so integer-weighted graphs (all sums exact below 2^53) reproduce the reference bit for
+// bit.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+#include <memory>
+
+#define SLM_OK 0
+#define SLM_EINVAL (-1)
+#define SLM_ECUDA (-2)
+#define SLM_ENOMEM (-3)
+#define SLM_ESTATE (-4)
+#define SLM_EUNSUP (-5)
+
+struct SlmError {
+    int code;
+    std::string msg;
+};
+
+#define CUDA_TRY(expr)                                                                   \
+    do {                                                                                 \
+        cudaError_t _e = (expr);                                                         \
+        if (_e != cudaSuccess)                                                           \
+            throw SlmError{_e == cudaErrorMemoryAllocation ? SLM_ENOMEM : SLM_ECUDA,     \
+                           std::string(#expr) + ": " + cudaGetErrorString(_e)};          \
+    } while (0)
+
+#define SLM_REQUIRE(cond, code, msg)                                                     \
+    do {                                                                                 \
+        if (!(cond)) throw SlmError{(code), (msg)};                                      \
+    } while (0)
+
+// ------------------------------------------------------------------ device buffers
+
+template <class T>
+struct DBuf {
+    T *p = nullptr;
+    size_t n = 0;     // logical length
+    size_t cap = 0;   // allocated elements
+    DBuf() = default;
+    DBuf(const DBuf &) = delete;
+    DBuf &operator=(const DBuf &) = delete;
+    ~DBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = cap = 0;
+    }
+    // grow-only; contents are not preserved when reallocating
+    T *resize(size_t cnt) {
+        if (cnt > cap) {
+            release();
+            size_t c = cnt ? cnt : 1;
+            CUDA_TRY(cudaMalloc(&p, c * sizeof(T)));
+            cap = c;
+        }
+        n = cnt;
+        return p;
+    }
+    void swap(DBuf &o) {
+        std::swap(p, o.p);
+        std::swap(n, o.n);
+        std::swap(cap, o.cap);
+    }
+    size_t bytes() const { return n * sizeof(T); }
+};
+
+// --------------------------------------------------------------- level graph state
+
+enum { BIN_SMALL = 0, BIN_MID = 1, BIN_LARGE = 2, NBINS = 3 };
+constexpr int SMALL_MAX = 32;     // warp-per-row, lanes = entries
+constexpr int MID_MAX = 4096;     // CTA-per-row, shared-memory hash
+
+// Canonical directed CSR + neighbour union + strengths of one hierarchy level
+// (graph.py:63-175, 257-263).  Node ids int32, entry offsets int64.
+struct LevelGraph {
+    int64_t n = 0, ne = 0, ue = 0;
+    DBuf<int64_t> csr_ptr;
+    DBuf<int32_t> csr_dst;
+    DBuf<double> csr_w;
+    DBuf<int64_t> uptr;
+    DBuf<int32_t> unbr;
+    DBuf<double> uu;          // w_out + w_in (F6)
+    DBuf<double> s_out, s_in;
+    double m_w = 0.0;
+    bool sym = false;         // W == W^T (then s_in == s_out bitwise)
+    bool integral = false;    // all weights integer-valued, m_w < 2^53
+    // degree bins of union rows (ascending row ids inside each bin)
+    DBuf<int32_t> bin_rows;
+    int64_t bin_off[NBINS + 1] = {0, 0, 0, 0};
+    DBuf<int64_t> large_hoff;  // per large row: offset into the global hash scratch
+    int64_t large_hash_total = 0;
+    int32_t max_deg = 0;
+};
+
+// Assignment forest + derived community structure (forest.py:23-67, quality.py:52-79).
+struct Forest {
+    int64_t n = 0, n_comms = 0;
+    DBuf<int32_t> a, comm;
+    DBuf<uint8_t> on_cycle;
+    DBuf<int32_t> cptr, members;        // members sorted by (comm, node)
+    DBuf<double> S_out, S_in;
+    DBuf<int32_t> count;
+    // DFS pre-order layout per community (root = smallest cycle node)
+    DBuf<int32_t> order, pos, sz, kptr, kids;
+    bool layout_valid = false;
+    bool agg_valid = false;
+    uint64_t version = 0;
+};
+
+struct slm_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    std::shared_ptr<LevelGraph> g0, g;   // original graph and current level
+    Forest f;
+    double gamma = 1.0;
+    int64_t level = 0;
+    // plan cache (exact fast-forward of coin-only sweeps)
+    DBuf<int32_t> cstar;
+    uint64_t plan_version = ~0ull;
+    // scratch
+    DBuf<uint8_t> tmp;           // CUB temp storage
+    DBuf<int64_t> i64a, i64b;
+    DBuf<int32_t> i32a, i32b, i32c, i32d;
+    DBuf<double> f64a, f64b;
+    DBuf<uint64_t> u64a, u64b;
+    DBuf<double> hash_vals;
+    DBuf<int32_t> hash_keys;
+    int32_t *h_flag = nullptr;   // pinned host scalars
+    int64_t *h_i64 = nullptr;
+    double *h_f64 = nullptr;
+    // counters of the last phase calls
+    int64_t last_rounds = 0, last_candidates = 0, last_accepted = 0;
+};
+
+// ------------------------------------------------------------------------- helpers
+
+static inline unsigned grid_for(int64_t work, int block, int64_t cap = 148LL * 64) {
+    int64_t g = (work + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (unsigned)g;
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// numpy DOUBLE_pairwise_sum, device twin of oracle/slm_oracle.c pw_sum (used where a
+// single thread owns a short segment).
+__host__ __device__ inline double pw_leaf(const double *a, int64_t n) {
+    if (n < 8) {
+        double r = 0.0;
+        for (int64_t i = 0; i < n; i++) r += a[i];
+        return r;
+    }
+    double r0 = a[0], r1 = a[1], r2 = a[2], r3 = a[3], r4 = a[4], r5 = a[5], r6 = a[6], r7 = a[7];
+    int64_t i;
+    for (i = 8; i < n - (n % 8); i += 8) {
+        r0 += a[i + 0]; r1 += a[i + 1]; r2 += a[i + 2]; r3 += a[i + 3];
+        r4 += a[i + 4]; r5 += a[i + 5]; r6 += a[i + 6]; r7 += a[i + 7];
+    }
+    double res = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
+    for (; i < n; i++) res += a[i];
+    return res;
+}
+
+// iterative pairwise (explicit stack) for one thread: exact numpy order for any n
+__host__ __device__ inline double pw_sum_seq(const double *a, int64_t n) {
+    if (n <= 128) return pw_leaf(a, n);
+    // emulate recursion: stack of (offset, len, state); results combined left+right
+    struct Fr { int64_t off, len; double left; int st; };
+    Fr stk[48];
+    double ret = 0.0;
+    int sp = 0;
+    stk[0] = {0, n, 0.0, 0};
+    while (sp >= 0) {
+        Fr &fr = stk[sp];
+        if (fr.len <= 128) {
+            ret = pw_leaf(a + fr.off, fr.len);
+            sp--;
+            continue;
+        }
+        int64_t n2 = fr.len / 2;
+        n2 -= n2 % 8;
+        if (fr.st == 0) {
+            fr.st = 1;
+            stk[sp + 1] = {fr.off, n2, 0.0, 0};
+            sp++;
+        } else if (fr.st == 1) {
+            fr.left = ret;
+            fr.st = 2;
+            stk[sp + 1] = {fr.off + n2, fr.len - n2, 0.0, 0};
+            sp++;
+        } else {
+            ret = fr.left + ret;
+            sp--;
+        }
+    }
+    return ret;
+}
+
+// np.add.reduceat segment: first + pairwise(rest)
+__host__ __device__ inline double reduceat_seq(const double *a, int64_t n) {
+    return a[0] + pw_sum_seq(a + 1, n - 1);
+}
+
+// ---------------------------------------------------------------- counter RNG
+
+#define RNG_GAMMA 0x9E3779B97F4A7C15ULL
+#define RNG_MIX1 0xBF58476D1CE4E5B9ULL
+#define RNG_MIX2 0x94D049BB133111EBULL
+
+__host__ __device__ inline uint64_t fin64(uint64_t z) {   // rng.py:19-23
+    z = (z ^ (z >> 30)) * RNG_MIX1;
+    z = (z ^ (z >> 27)) * RNG_MIX2;
+    return z ^ (z >> 31);
+}
+__host__ __device__ inline uint64_t mix_key2(uint64_t seed, int64_t level, int64_t sweep) {
+    uint64_t s = fin64(seed);                                  // rng.py:26-31
+    s = fin64(s + RNG_GAMMA + (uint64_t)level);
+    s = fin64(s + RNG_GAMMA + (uint64_t)sweep);
+    return s;
+}
+__host__ __device__ inline double uniform01_at(uint64_t base, int64_t id) {   // rng.py:34-43
+    uint64_t z = fin64((uint64_t)id * RNG_GAMMA + base);
+    return (double)(z >> 11) * 0x1.0p-53;
+}
+
+// ------------------------------------------------------------- internal API
+
+void build_level_from_edges(slm_ctx *ctx, LevelGraph &G, int64_t n, const int32_t *d_src,
+                            const int32_t *d_dst, const double *d_w, int64_t ne_in);
+void build_level_from_keys(slm_ctx *ctx, LevelGraph &G, int64_t n, DBuf<uint64_t> &keys,
+                           DBuf<double> &vals, int64_t ne_in);
+double device_pairwise_sum(slm_ctx *ctx, const double *d_a, int64_t n);
+void run_assign(slm_ctx *ctx, const LevelGraph &G, double m, int32_t *d_a);
+void run_components(slm_ctx *ctx, Forest &F, int64_t n);
+void build_members_and_aggregates(slm_ctx *ctx, const LevelGraph &G, Forest &F);
+void build_layout(slm_ctx *ctx, Forest &F);
+void run_plan(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_t *d_cstar);
+void run_local_gains(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, double *d_lg,
+                     uint8_t *d_bad);
+void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_t scc_cap,
+                  int64_t *splits, int64_t *unresolved, int *changed, std::vector<double> *gains);
+void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const int32_t *d_cstar,
+                uint64_t seed, double accept_prob, int64_t level, int64_t sweep, int *improved,
+                int64_t *applied, std::vector<double> *gains);
+void run_aggregate(slm_ctx *ctx, const LevelGraph &G, const int32_t *d_labels, int64_t n_comms,
+                   LevelGraph &out);
+double run_score(slm_ctx *ctx, const LevelGraph &G, const int32_t *d_labels, double gamma);
+void forest_refresh(slm_ctx *ctx, const LevelGraph &G, Forest &F);   // comps + agg + layout
+
+template <class T>
+void cub_exclusive_sum(slm_ctx *ctx, const T *in, T *out, int64_t n);
+void sort_pairs_u64_f64(slm_ctx *ctx, DBuf<uint64_t> &keys, DBuf<double> &vals, int64_t n,
+                        int end_bit);
+void sort_pairs_u32_i32(slm_ctx *ctx, uint32_t *keys_in, uint32_t *keys_out, int32_t *vals_in,
+                        int32_t *vals_out, int64_t n, int end_bit);
+int bits_for(int64_t v);

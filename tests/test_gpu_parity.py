@@ -1,0 +1,240 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's golden vectors
+and the C oracle.
+
+Bar: bit-exact partitions, assignment maps, candidate targets, sweep counts and statistics
+for integer / dyadic weights (all sums exact); final modularity within 1e-12 relative.
+The canonical CSR, union, strengths, m_w and ASSIGN are bit-exact for real weights too
+(their summation orders are replicated); for real weights the later phases are checked
+against a tolerance (NMI >= 0.999, |dQ| <= 1e-9), since their group sums use atomics.
+"""
+
+import numpy as np
+import pytest
+
+from tests.conftest import case_edges, case_names, exact_sums
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def slm():
+    import paper_1702_04645_b200 as P
+    from paper_1702_04645_b200 import _lib
+    _lib.load()
+    return P
+
+
+def nmi(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    n = a.size
+    _, ia = np.unique(a, return_inverse=True)
+    _, ib = np.unique(b, return_inverse=True)
+    cont = np.zeros((ia.max() + 1, ib.max() + 1))
+    np.add.at(cont, (ia, ib), 1)
+    pa = cont.sum(1) / n
+    pb = cont.sum(0) / n
+    pab = cont / n
+    nz = pab > 0
+    mi = (pab[nz] * np.log(pab[nz] / np.outer(pa, pb)[nz])).sum()
+    ha = -(pa[pa > 0] * np.log(pa[pa > 0])).sum()
+    hb = -(pb[pb > 0] * np.log(pb[pb > 0])).sum()
+    return 1.0 if ha + hb == 0 else 2 * mi / (ha + hb)
+
+
+def test_build_matches_reference_bit_exact(slm, golden):
+    for key in case_names(golden):
+        n, s, d, w = case_edges(golden, key)
+        ctx = slm.Graph.from_edges(n, s, d, w).context()
+        p, dst, ww = ctx.csr()
+        np.testing.assert_array_equal(p, golden[f"{key}/out_ptr"], err_msg=key)
+        np.testing.assert_array_equal(dst, golden[f"{key}/out_dst"], err_msg=key)
+        np.testing.assert_array_equal(ww, golden[f"{key}/out_w"], err_msg=key)
+        up, un, uu = ctx.union()
+        np.testing.assert_array_equal(up, golden[f"{key}/uptr"], err_msg=key)
+        np.testing.assert_array_equal(un, golden[f"{key}/unbr"], err_msg=key)
+        np.testing.assert_array_equal(uu, golden[f"{key}/uu"], err_msg=key)
+        so, si, m = ctx.strengths()
+        np.testing.assert_array_equal(so, golden[f"{key}/s_out"], err_msg=key)
+        np.testing.assert_array_equal(si, golden[f"{key}/s_in"], err_msg=key)
+        assert m == float(golden[f"{key}/m_w"]), key
+
+
+def test_assign_components_bit_exact(slm, golden):
+    for key in case_names(golden):
+        n, s, d, w = case_edges(golden, key)
+        g = slm.Graph.from_edges(n, s, d, w)
+        a = slm.find_assignment(g)
+        np.testing.assert_array_equal(a, golden[f"{key}/assign"], err_msg=key)
+        f = slm.extract_components(a)
+        np.testing.assert_array_equal(f.comm, golden[f"{key}/comm0"], err_msg=key)
+        np.testing.assert_array_equal(f.on_cycle, golden[f"{key}/on_cycle0"], err_msg=key)
+
+
+def test_local_gains_and_plan(slm, golden):
+    for key in case_names(golden):
+        n, s, d, w = case_edges(golden, key)
+        g = slm.Graph.from_edges(n, s, d, w)
+        lg = slm.local_gains(g, None, golden[f"{key}/comm0"])
+        ref = golden[f"{key}/lg0"]
+        if exact_sums(key):
+            np.testing.assert_array_equal(lg, ref, err_msg=key)
+        else:
+            np.testing.assert_allclose(lg, ref, rtol=0, atol=1e-12)
+        cstar = g.context().plan(golden[f"{key}/pos_comm"])
+        np.testing.assert_array_equal(cstar, golden[f"{key}/cstar"], err_msg=key)
+
+
+def test_positive_and_maximal_phases(slm, golden):
+    for key in case_names(golden):
+        if not exact_sums(key):
+            continue
+        n, s, d, w = case_edges(golden, key)
+        seed, p = int(golden[f"{key}/seed"]), float(golden[f"{key}/p"])
+        g = slm.Graph.from_edges(n, s, d, w)
+        cfg = slm.RunConfig(seed=seed, accept_prob=p)
+        f = slm.extract_components(golden[f"{key}/assign"])
+        f2, sp, un, gains = slm.positive_correction(g, None, f, cfg)
+        np.testing.assert_array_equal(f2.a, golden[f"{key}/pos_a"], err_msg=key)
+        np.testing.assert_array_equal(f2.comm, golden[f"{key}/pos_comm"], err_msg=key)
+        assert [sp, un] == list(golden[f"{key}/pos_stats"]), key
+        np.testing.assert_array_equal(gains, golden[f"{key}/pos_gains"], err_msg=key)
+        f3, imp, app, g3 = slm.maximal_correction(g, None, f2, cfg, 0, 0)
+        np.testing.assert_array_equal(f3.a, golden[f"{key}/max_a"], err_msg=key)
+        np.testing.assert_array_equal(f3.comm, golden[f"{key}/max_comm"], err_msg=key)
+        assert [int(imp), app] == list(golden[f"{key}/max_stats"]), key
+        np.testing.assert_array_equal(g3, golden[f"{key}/max_gains"], err_msg=key)
+
+
+def test_full_runs_golden(slm, golden):
+    for key in case_names(golden):
+        n, s, d, w = case_edges(golden, key)
+        seed, p = int(golden[f"{key}/seed"]), float(golden[f"{key}/p"])
+        r = slm.run(slm.Graph.from_edges(n, s, d, w), slm.RunConfig(seed=seed, accept_prob=p))
+        q = float(golden[f"{key}/final_score"])
+        if exact_sums(key):
+            assert len(r.hierarchy.levels) == int(golden[f"{key}/nlevels"]), key
+            for t, lv in enumerate(r.hierarchy.levels):
+                np.testing.assert_array_equal(lv, golden[f"{key}/level{t}"], err_msg=key)
+            assert r.stats.sweeps_per_level == list(golden[f"{key}/sweeps"]), key
+            assert [r.stats.accepted_moves, r.stats.accepted_splits,
+                    r.stats.unresolved_negative] == list(golden[f"{key}/run_stats"]), key
+            assert abs(r.final_score - q) <= 1e-12 * max(1.0, abs(q)), key
+        else:
+            assert nmi(r.hierarchy.flat, golden[f"{key}/flat"]) >= 0.999 or \
+                abs(r.final_score - q) <= 1e-9, key
+
+
+def test_config_fixtures_full_runs(slm, golden_configs):
+    from paper_1702_04645_b200 import generators as GN
+    G = golden_configs
+    specs = {"c1_sbm": lambda: GN.generate("c1_sbm"),
+             "c2_dcsbm_small": lambda: GN.dcsbm(n=3000, k=20, size_lo=50, size_hi=300, seed=1),
+             "c3_rmat10": lambda: GN.rmat(10, 16, 0, 2),
+             "c4_rgg4096": lambda: GN.rgg(4096, 8.0, 3),
+             "c5_rmat10w": lambda: GN.rmat(10, 8, 1, 4)}
+    for key, fn in specs.items():
+        n, s, d, w = fn()
+        r = slm.run(slm.Graph.from_edges(n, s, d, w), slm.RunConfig(seed=0))
+        assert len(r.hierarchy.levels) == int(G[f"{key}/nlevels"]), key
+        for t, lv in enumerate(r.hierarchy.levels):
+            np.testing.assert_array_equal(lv, G[f"{key}/level{t}"], err_msg=key)
+        assert r.stats.sweeps_per_level == list(G[f"{key}/sweeps"]), key
+        assert [r.stats.accepted_moves, r.stats.accepted_splits, r.stats.unresolved_negative] \
+            == list(G[f"{key}/run_stats"]), key
+        q = float(G[f"{key}/final_score"])
+        assert abs(r.final_score - q) <= 1e-12 * abs(q), key
+
+
+def _vs_oracle(slm, oracle, n, s, d, w, seed=0, p=0.5, gamma=1.0):
+    r = slm.run(slm.Graph.from_edges(n, s, d, w),
+                slm.RunConfig(seed=seed, accept_prob=p, resolution=gamma))
+    o = oracle.run(n, s, d, w, seed=seed, accept_prob=p, resolution=gamma)
+    assert len(r.hierarchy.levels) == len(o.levels)
+    for x, y in zip(r.hierarchy.levels, o.levels):
+        np.testing.assert_array_equal(x, y)
+    assert r.stats.sweeps_per_level == o.sweeps_per_level
+    assert [r.stats.accepted_moves, r.stats.accepted_splits, r.stats.unresolved_negative] == \
+        [o.accepted_moves, o.accepted_splits, o.unresolved_negative]
+    assert abs(r.final_score - o.final_score) <= 1e-12 * max(1.0, abs(o.final_score))
+    return r
+
+
+def test_scaled_configs_vs_oracle(slm, oracle):
+    from paper_1702_04645_b200 import generators as GN
+    oracle.set_threads(8)
+    cases = [GN.rmat(13, 16, 0, 2), GN.rmat(13, 16, 1, 4), GN.rgg(1 << 14, 8.0, 3),
+             GN.dcsbm(n=20_000, k=60, size_lo=100, size_hi=1000, seed=1)]
+    for n, s, d, w in cases:
+        _vs_oracle(slm, oracle, n, s, d, w)
+
+
+def test_resolution_vs_oracle(slm, oracle):
+    from paper_1702_04645_b200 import generators as GN
+    n, s, d, w = GN.rmat(12, 8, 1, 4)
+    for gamma in (0.5, 2.0):
+        _vs_oracle(slm, oracle, n, s, d, w, gamma=gamma)
+    n, s, d, w = GN.generate("c1_sbm")
+    for gamma in (0.5, 2.0):
+        _vs_oracle(slm, oracle, n, s, d, w, gamma=gamma)
+
+
+def test_accept_prob_and_seeds_vs_oracle(slm, oracle):
+    from paper_1702_04645_b200 import generators as GN
+    n, s, d, w = GN.rmat(11, 16, 1, 7)
+    for seed, p in ((3, 1.0), (5, 0.25), (9, 0.75)):
+        _vs_oracle(slm, oracle, n, s, d, w, seed=seed, p=p)
+
+
+def test_kats(slm):
+    tri = [(0, 1, 1.0), (1, 2, 1.0), (2, 0, 1.0), (3, 4, 1.0), (4, 5, 1.0), (5, 3, 1.0)]
+    s, d, w = (np.array(x) for x in zip(*tri))
+    g = slm.Graph.from_edges(6, s, d, w)
+    np.testing.assert_array_equal(slm.find_assignment(g), [1, 0, 0, 4, 3, 3])
+    assert slm.score(g, None, [0, 0, 0, 1, 1, 1]) == 0.5
+    r = slm.run(g, slm.RunConfig(accept_prob=1.0))
+    assert [lv.tolist() for lv in r.hierarchy.levels] == [[0, 0, 0, 1, 1, 1], [0, 1]]
+    assert r.final_score == 0.5
+    r = slm.run(slm.Graph.from_edges(2, [0], [1], [1.0]))
+    np.testing.assert_array_equal(r.hierarchy.flat, [0, 1])
+    assert len(r.hierarchy.levels) == 1
+    # isolated nodes and self-loops only
+    r = slm.run(slm.Graph.from_edges(4, [0, 2], [0, 2], [1.0, 2.0]))
+    np.testing.assert_array_equal(r.hierarchy.flat, [0, 1, 2, 3])
+    # edgeless graph: identity, score 0
+    r = slm.run(slm.Graph.from_edges(3, np.empty(0, np.int64), np.empty(0, np.int64), np.empty(0)))
+    np.testing.assert_array_equal(r.hierarchy.flat, [0, 1, 2])
+    assert r.final_score == 0.0
+
+
+def test_components_random_functional_graphs(slm):
+    """Arbitrary maps (cycles of any length) take the general pointer-doubling path."""
+    rng = np.random.default_rng(3)
+    from oracle import oracle as O
+    for _ in range(40):
+        n = int(rng.integers(1, 300))
+        a = rng.integers(0, n, size=n).astype(np.int64)
+        f = slm.extract_components(a)
+        comm, nc, oc = O.extract_components(a)
+        np.testing.assert_array_equal(f.comm, comm)
+        np.testing.assert_array_equal(f.on_cycle, oc)
+        assert f.n_comms == nc
+
+
+def test_uniform01_device(slm, golden):
+    ids = golden["rng/ids"]
+    np.testing.assert_array_equal(slm.uniform01(0, (0, 0), ids), golden["rng/u_0_0_0"])
+    np.testing.assert_array_equal(slm.uniform01(11, (2, 5), ids), golden["rng/u_11_2_5"])
+
+
+def test_device_generators_match_host(slm):
+    from paper_1702_04645_b200 import _lib, generators as GN
+    for name, over in (("c3_rmat22", dict(scale=12)), ("c5_rmat24", dict(scale=12, edge_factor=8)),
+                       ("c4_rgg24", dict(n=1 << 13))):
+        ctx_d = _lib.Context(0)
+        GN.build_on_device(ctx_d, name, **over)
+        n, s, d, w = GN.generate(name, **over)
+        ctx_h = _lib.Context(0)
+        ctx_h.build_graph(n, s, d, w)
+        for x, y in zip(ctx_d.csr(), ctx_h.csr()):
+            np.testing.assert_array_equal(x, y)
