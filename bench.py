@@ -1,0 +1,336 @@
+"""Bench: SLM local-move sweep (the plan sweep, _best_targets detector.py:367-418) on B200.
+
+Contract (one JSON line from rank 0):
+  * step    = one local-move plan sweep over the whole graph of the workload (default:
+              BASELINE config 5, R-MAT scale 24, edge factor 32, integer weights U[1,100],
+              ~1.02e9 directed union entries), on the snapshot the first MAXIMAL sweep of
+              level 0 sees (after ASSIGN, COMPONENTS and POSITIVE).
+  * value   = local-move GTEPS = union entries scanned per second, whole job (sum over ranks
+              of entries / max over ranks of the device time of K sweeps; CUDA events on the
+              library's own stream; inputs resident in HBM).  Inputs (12+ GB union) exceed
+              the 126 MB L2, so no flush is needed between sweeps.
+  * e2e     = the same metric through the reference-facing C ABI call with host buffers:
+              slm_plan_sweep(labels from pinned host memory -> targets to host), H2D and D2H
+              inside the timed region.
+  * roofline: algorithmic bytes per sweep B = E*12 + n*32 + G*16 over the
+              sweep's average device time, against MEASURED_PEAKS.json hbm_gbs.
+  * cpu_baseline: the C oracle port of _best_targets on the host's cores over a bounded
+              contiguous row sample of the same snapshot (also checked for equal targets).
+  * --impl reference: the oracle port alone (the reference's CPU path), same metric.
+  * N > 1 (torchrun): replicas only: every rank runs the same sweep on
+    its own GPU; rank 0 prints.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, device):
+        self.device = device
+        self.lines = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def _traffic():
+    p = os.path.join(ROOT, "profiles", "plan_sweep_traffic.json")
+    try:
+        return json.load(open(p)).get("dram_bytes_per_sweep")
+    except (OSError, ValueError):
+        return None
+
+
+def setup_snapshot(ctx, cfgname, over):
+    """Build the workload in HBM and produce the first MAXIMAL sweep's snapshot."""
+    from paper_1702_04645_b200 import RunConfig, generators as GN
+    t0 = time.perf_counter()
+    GN.build_on_device(ctx, cfgname, **over)
+    t1 = time.perf_counter()
+    ctx.assign(want=False)
+    ctx.components(want=False)
+    ctx.positive(RunConfig()._c())
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1
+
+
+def snapshot_arrays(ctx):
+    _, comm, nc, _ = ctx.forest(want_a=False, want_cycle=False)
+    so, si, _ = ctx.aggregates(nc)
+    return comm, so, si
+
+
+def cpu_sample(ctx, info, target_entries, snap):
+    """Download a contiguous row sample of the snapshot for the oracle port."""
+    n = info["n"]
+    # rows [0, R) with about target_entries union entries
+    lo, hi = 0, n
+    probe = ctx.union_rows(0, min(n, 1 << 16))[0]
+    avg = max(1.0, probe[-1] / max(1, probe.size - 1))
+    R = int(min(n, max(1024, target_entries / avg)))
+    uptr, unbr, uu = ctx.union_rows(0, R)
+    comm, so, si = snap
+    s_out, s_in, m = ctx.strengths()
+    return dict(R=R, uptr=uptr, unbr=unbr, uu=uu, comm=comm, S_out=so, S_in=si, s_out=s_out,
+                s_in=s_in, m=m, entries=int(uptr[-1]))
+
+
+def time_oracle(sample, threads, reps=1):
+    from oracle import oracle as O
+    O.build()
+    O.set_threads(threads)
+    ts = []
+    out = None
+    for _ in range(reps):
+        t = time.perf_counter()
+        out = O.plan_sample(sample["uptr"], sample["unbr"], sample["uu"], sample["s_out"],
+                            sample["s_in"], sample["m"], sample["comm"], sample["S_out"],
+                            sample["S_in"], 0, sample["R"])
+        ts.append(time.perf_counter() - t)
+    return min(ts), out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c5_rmat24")
+    ap.add_argument("--scale", type=int, default=None, help="override R-MAT scale (dev)")
+    ap.add_argument("--cpu-entries", type=float, default=6e7,
+                    help="union entries in the CPU-baseline row sample")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    ws, rank, local = _dist()
+    import torch
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group(backend="nccl" if args.impl == "ours" else "gloo")
+    torch.cuda.set_device(local)
+    from paper_1702_04645_b200 import _lib
+    from paper_1702_04645_b200.generators import CONFIGS
+
+    over = {}
+    if args.scale is not None:
+        over["scale"] = args.scale
+    spec = dict(CONFIGS[args.config])
+    spec.update(over)
+    workload = {"workload": args.config, **{k: v for k, v in spec.items()}}
+    threads = os.cpu_count() or 1
+
+    ctx = _lib.Context(local)
+    build_s, setup_s = setup_snapshot(ctx, args.config, over)
+    info = ctx.info()
+    snap = snapshot_arrays(ctx)
+    E, n = info["ue"], info["n"]
+
+    if args.impl == "reference":
+        if rank != 0:
+            if ws > 1:
+                import torch.distributed as dist
+                dist.barrier()
+            return
+        sample = cpu_sample(ctx, info, args.cpu_entries, snap)
+        times = []
+        for i in range(args.warmup + args.steps):
+            t, _ = time_oracle(sample, threads)
+            if i >= args.warmup:
+                times.append(t)
+        tot = sum(times)
+        val = sample["entries"] * len(times) / tot / 1e9
+        line = {"impl": "reference", "metric": "local-move GTEPS", "value": val, "unit": "GTEPS",
+                "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": tot / len(times) * 1e3, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": workload,
+                "cpu_baseline": {"value": val, "unit": "GTEPS", "cores": threads, "kind": "port",
+                                 "sample": f"_best_targets over rows [0,{sample['R']}) "
+                                           f"({sample['entries']} union entries) of the "
+                                           f"{args.config} first-sweep snapshot"},
+                "e2e": {"value": val, "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        return
+
+    groups, bin_rows, bin_entries = ctx.plan_groups()
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=local)
+    bins_used = int((bin_rows > 0).sum())
+    launches_per_sweep = 1 + bins_used
+
+    def timed(mask, iters):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(iters):
+            ctx.plan_async(mask)
+        b.record(stream)
+        b.synchronize()
+        return a.elapsed_time(b)
+
+    for _ in range(args.warmup):
+        ctx.plan_async(15)
+    ctx.sync()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    ctx.sync()
+    with Clocks(local) as clk:
+        ms = timed(15, args.steps)
+    ctx.sync()
+    torch.cuda.synchronize()
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    gpu_cstar = ctx.get_cstar()
+    ms_step = ms_max / args.steps
+    value = E * args.steps * ws / (ms_max / 1e3) / 1e9
+
+    # per-bin device times (explanation only)
+    per_bin = {}
+    for mask, name in ((1, "small_warp"), (2, "mid_cta_smem_hash"), (4, "hub_cta_global_hash"),
+                       (8, "label_copy")):
+        per_bin[name] = round(timed(mask, max(3, args.steps // 4)) / max(3, args.steps // 4), 4)
+
+    # e2e through the C ABI with pinned host buffers
+    comm = snap[0]
+    lab_pin = torch.from_numpy(comm).pin_memory().numpy()
+    out_pin = torch.empty(n, dtype=torch.int64).pin_memory().numpy()
+    from paper_1702_04645_b200._lib import ptr
+    ke = max(3, min(args.steps, 5))
+    ctx.call("slm_plan_sweep", ptr(lab_pin), ptr(out_pin))
+    t0 = time.perf_counter()
+    for _ in range(ke):
+        ctx.call("slm_plan_sweep", ptr(lab_pin), ptr(out_pin))
+    e2e_s = (time.perf_counter() - t0) / ke
+    e2e_val = E * ws / e2e_s / 1e9
+
+    # roofline of the sweep (SURVEY §8(d) algorithmic bytes)
+    B = E * 12 + n * 32 + groups * 16
+    peak, peak_kind = _peaks()
+    achieved = B / (ms_step / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": _traffic(),
+            "peak_kind": peak_kind, "algorithmic_bytes_per_sweep": int(B),
+            "groups_G": int(groups), "G_over_E": round(groups / E, 4)}
+
+    line = {"metric": "local-move GTEPS", "value": round(value, 3), "unit": "GTEPS",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {**workload, "n": n, "union_entries": E, "l2": "inputs > L2 (no flush)",
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
+            "roofline": roof,
+            "e2e": {"value": round(e2e_val, 3), "unit": "GTEPS", "h2d_bytes_per_step": n * 8,
+                    "d2h_bytes_per_step": n * 8, "ms_per_step": round(e2e_s * 1e3, 3)},
+            "gpu_launches": launches_per_sweep * args.steps,
+            "clocks": clk.summary(),
+            "per_kernel_ms": per_bin,
+            "bins": {"rows": bin_rows.tolist(), "entries": bin_entries.tolist()},
+            "setup_s": {"build_csr_union": round(build_s, 3),
+                        "assign_components_positive": round(setup_s, 3)}}
+    if rank == 0 and not args.no_cpu:
+        sample = cpu_sample(ctx, info, args.cpu_entries, snap)
+        t_cpu, cst = time_oracle(sample, threads)
+        ok = bool(np.array_equal(cst, gpu_cstar[:sample["R"]]))
+        line["cpu_baseline"] = {
+            "value": round(sample["entries"] / t_cpu / 1e9, 5), "unit": "GTEPS",
+            "cores": threads, "kind": "port",
+            "sample": f"_best_targets over rows [0,{sample['R']}) ({sample['entries']} union "
+                      f"entries) of the same snapshot; targets equal to the GPU's: {ok}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -77,6 +77,10 @@ SLM_API int slm_get_csr(slm_ctx *ctx, int64_t *out_ptr, int64_t *out_dst, double
 /* NeighborUnion ptr/nbr and w_out + w_in (graph.py:46-60) */
 SLM_API int slm_get_union(slm_ctx *ctx, int64_t *ptr, int64_t *nbr, double *u);
 SLM_API int slm_get_strengths(slm_ctx *ctx, double *s_out, double *s_in);
+/* Union rows [r0, r1): ptr_out has r1-r0+1 offsets relative to row r0; nbr_out / u_out
+ * nullable (call once with NULL to size them from ptr_out[r1-r0]). */
+SLM_API int slm_get_union_rows(slm_ctx *ctx, int64_t r0, int64_t r1, int64_t *ptr_out,
+                               int64_t *nbr_out, double *u_out);
 SLM_API int slm_set_resolution(slm_ctx *ctx, double gamma);
 
 /* ---- phases (current level) ----------------------------------------------------- */
@@ -101,6 +105,13 @@ SLM_API int slm_positive(slm_ctx *ctx, const slm_config *cfg, int64_t *splits, i
  * (nullable) replaces the forest labels as the snapshot (must be dense, with the
  * aggregates recomputed from it); cstar_out nullable. */
 SLM_API int slm_plan_sweep(slm_ctx *ctx, const int64_t *comm_in, int64_t *cstar_out);
+/* Bench helpers: enqueue one plan sweep on the context stream without synchronising or
+ * copying (bin_mask: 1 small rows, 2 mid rows, 4 hub rows, 8 label copy for empty rows;
+ * 15 = the full sweep); count distinct (node, community) groups G of the last snapshot and
+ * the rows / union entries of each degree bin; read the last plan's targets. */
+SLM_API int slm_plan_sweep_async(slm_ctx *ctx, int32_t bin_mask);
+SLM_API int slm_plan_groups(slm_ctx *ctx, int64_t *groups, int64_t *bin_rows, int64_t *bin_entries);
+SLM_API int slm_get_cstar(slm_ctx *ctx, int64_t *cstar_out);
 /* maximal_correction (detector.py:457-521) for (level, sweep); gains_out nullable. */
 SLM_API int slm_maximal(slm_ctx *ctx, const slm_config *cfg, int64_t level, int64_t sweep,
                 int32_t *improved, int64_t *applied, double *gains_out, int64_t gains_cap);

@@ -71,6 +71,8 @@ def lib():
                                    C.POINTER(i64), C.POINTER(i64), _f64p, i64, C.POINTER(i64)]
         L.orc_plan.argtypes = [vp, C.c_double, _i64p, i64, _i64p]
         L.orc_plan_rows.argtypes = [vp, C.c_double, _i64p, _f64p, _f64p, i64, i64, _i64p]
+        L.orc_plan_sample.argtypes = [_i64p, _i64p, _f64p, _f64p, _f64p, C.c_double, _i64p,
+                                      _f64p, _f64p, i64, i64, _i64p]
         L.orc_mix_key.restype = C.c_uint64
         L.orc_mix_key.argtypes = [C.c_uint64, i64, i64]
         L.orc_uniform01.argtypes = [C.c_uint64, i64, i64, _i64p, i64, _f64p]
@@ -192,6 +194,19 @@ def best_targets(g: OGraph, labels, n_comms, m=None):
     cstar = np.empty(g.n, np.int64)
     lib().orc_plan(g._h, g.m_w if m is None else m, _i64(labels), n_comms, cstar)
     return cstar
+
+
+def plan_sample(uptr, unbr, uu, s_out, s_in, m, labels, S_out, S_in, r0, r1):
+    """_best_targets for rows [r0, r1) from raw arrays (uptr relative to r0); returns cstar
+    for those rows (bench CPU baseline, all threads set by set_threads)."""
+    n = labels.size
+    cstar = np.zeros(n, np.int64)
+    lib().orc_plan_sample(_i64(uptr), _i64(unbr), np.ascontiguousarray(uu, np.float64),
+                          np.ascontiguousarray(s_out, np.float64),
+                          np.ascontiguousarray(s_in, np.float64), float(m), _i64(labels),
+                          np.ascontiguousarray(S_out, np.float64),
+                          np.ascontiguousarray(S_in, np.float64), int(r0), int(r1), cstar)
+    return cstar[r0:r1]
 
 
 def mix_key(seed, level, sweep):

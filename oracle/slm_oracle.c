@@ -699,8 +699,11 @@ EXPORT int orc_positive(const orc_graph *g, double m, int64_t *a, const int64_t 
 
 /* _best_targets (detector.py:367-418): synchronous best community per node from a
  * frozen snapshot.  S_* are the snapshot aggregates (quality.py:71-79). */
-static void plan_rows(const orc_graph *g, double m, const int64_t *lab, const double *S_out,
-                      const double *S_in, int64_t r0, int64_t r1, int64_t *cstar) {
+static void plan_rows_raw(const int64_t *uptr, const int64_t *unbr, const double *uu,
+                          const double *s_out, const double *s_in, double m, const int64_t *lab,
+                          const double *S_out, const double *S_in, int64_t r0, int64_t r1,
+                          int64_t row_base, int64_t *cstar) {
+    /* rows r0..r1 (global ids); uptr/unbr/uu hold rows row_base.. ; cstar indexed by row */
     const double m2 = m * m;
     int64_t cap = 0;
     int64_t *idx = NULL;
@@ -708,9 +711,9 @@ static void plan_rows(const orc_graph *g, double m, const int64_t *lab, const do
     double *wbuf = NULL;
     for (int64_t r = r0; r < r1; r++) {
         int64_t L = lab[r];
-        double so = g->s_out[r], si = g->s_in[r];
+        double so = s_out[r], si = s_in[r];
         cstar[r] = L;
-        int64_t e0 = g->uptr[r], e1 = g->uptr[r + 1], d = e1 - e0;
+        int64_t e0 = uptr[r - row_base], e1 = uptr[r - row_base + 1], d = e1 - e0;
         if (d == 0) continue;
         double t_stay = -(so * (S_in[L] - si) + si * (S_out[L] - so)) / m2;
         if (cap < d) {
@@ -720,7 +723,7 @@ static void plan_rows(const orc_graph *g, double m, const int64_t *lab, const do
             wbuf = (double *)realloc(wbuf, (size_t)cap * sizeof(double));
         }
         /* stable sort entries of the row by community (insertion sort for short rows) */
-        for (int64_t k = 0; k < d; k++) { key[k] = (uint64_t)lab[g->unbr[e0 + k]]; idx[k] = k; }
+        for (int64_t k = 0; k < d; k++) { key[k] = (uint64_t)lab[unbr[e0 + k]]; idx[k] = k; }
         if (d <= 32) {
             for (int64_t k = 1; k < d; k++) {
                 int64_t v = idx[k]; uint64_t kv = key[v]; int64_t q = k - 1;
@@ -733,11 +736,10 @@ static void plan_rows(const orc_graph *g, double m, const int64_t *lab, const do
         double mx = -INFINITY;
         int64_t best_c = -1;
         int64_t k = 0;
-        /* first pass: group sums and t; track own t and max over non-own */
         while (k < d) {
             int64_t c = (int64_t)key[idx[k]];
             int64_t q = k, nn = 0;
-            while (q < d && (int64_t)key[idx[q]] == c) { wbuf[nn++] = g->uu[e0 + idx[q]]; q++; }
+            while (q < d && (int64_t)key[idx[q]] == c) { wbuf[nn++] = uu[e0 + idx[q]]; q++; }
             double gsum = reduceat_seg(wbuf, nn);
             int own = (c == L);
             double sin_c = S_in[c] - (own ? si : 0.0);
@@ -750,6 +752,30 @@ static void plan_rows(const orc_graph *g, double m, const int64_t *lab, const do
         if (best_c >= 0 && mx > t_stay) cstar[r] = best_c;
     }
     free(idx); free(key); free(wbuf);
+}
+
+/* _best_targets (detector.py:367-418): synchronous best community per node from a
+ * frozen snapshot.  S_* are the snapshot aggregates (quality.py:71-79). */
+static void plan_rows(const orc_graph *g, double m, const int64_t *lab, const double *S_out,
+                      const double *S_in, int64_t r0, int64_t r1, int64_t *cstar) {
+    plan_rows_raw(g->uptr, g->unbr, g->uu, g->s_out, g->s_in, m, lab, S_out, S_in, r0, r1, 0,
+                  cstar);
+}
+
+/* Bounded-sample plan over raw arrays (the bench's CPU baseline): rows [r0, r1) whose union
+ * rows are given relative to r0. */
+EXPORT void orc_plan_sample(const int64_t *uptr, const int64_t *unbr, const double *uu,
+                            const double *s_out, const double *s_in, double m, const int64_t *lab,
+                            const double *S_out, const double *S_in, int64_t r0, int64_t r1,
+                            int64_t *cstar) {
+    int64_t n = r1 - r0;
+    const int64_t chunk = 2048;
+    int64_t nch = (n + chunk - 1) / chunk;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(g_threads)
+    for (int64_t c = 0; c < nch; c++) {
+        int64_t a0 = r0 + c * chunk, a1 = a0 + chunk < r1 ? a0 + chunk : r1;
+        plan_rows_raw(uptr, unbr, uu, s_out, s_in, m, lab, S_out, S_in, a0, a1, r0, cstar);
+    }
 }
 
 EXPORT void orc_plan(const orc_graph *g, double m, const int64_t *lab, int64_t nc, int64_t *cstar) {

@@ -48,6 +48,7 @@ SIGNATURES = {
     "slm_get_csr": (C.c_int, [_VP, _VP, _VP, _VP]),
     "slm_get_union": (C.c_int, [_VP, _VP, _VP, _VP]),
     "slm_get_strengths": (C.c_int, [_VP, _VP, _VP]),
+    "slm_get_union_rows": (C.c_int, [_VP, _I64, _I64, _VP, _VP, _VP]),
     "slm_set_resolution": (C.c_int, [_VP, C.c_double]),
     "slm_assign": (C.c_int, [_VP, _VP]),
     "slm_set_assignment": (C.c_int, [_VP, _VP]),
@@ -62,6 +63,9 @@ SIGNATURES = {
     "slm_score": (C.c_int, [_VP, C.c_int32, _VP, C.c_double, _PD]),
     "slm_uniform01": (C.c_int, [_VP, C.c_uint64, _I64, _I64, _VP, _I64, _VP]),
     "slm_last_commit_stats": (C.c_int, [_VP, _PI64, _PI64]),
+    "slm_plan_sweep_async": (C.c_int, [_VP, C.c_int32]),
+    "slm_plan_groups": (C.c_int, [_VP, _PI64, _VP, _VP]),
+    "slm_get_cstar": (C.c_int, [_VP, _VP]),
     "slm_gen_rmat_host": (C.c_int, [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                     C.c_uint64, C.c_int, _VP, _VP, _VP, _PI64]),
     "slm_gen_rgg_host": (C.c_int, [_I64, C.c_double, C.c_uint64, _VP, _VP, _VP, _PI64]),
@@ -177,6 +181,14 @@ class Context:
         self.call("slm_get_union", ptr(p), ptr(nb), ptr(u))
         return p, nb, u
 
+    def union_rows(self, r0, r1):
+        p = np.empty(r1 - r0 + 1, np.int64)
+        self.call("slm_get_union_rows", int(r0), int(r1), ptr(p), None, None)
+        nb = np.empty(int(p[-1]), np.int64)
+        u = np.empty(int(p[-1]), np.float64)
+        self.call("slm_get_union_rows", int(r0), int(r1), ptr(p), ptr(nb), ptr(u))
+        return p, nb, u
+
     def strengths(self):
         d = self.info()
         so = np.empty(d["n"], np.float64)
@@ -268,6 +280,24 @@ class Context:
         self.call("slm_uniform01", int(seed) & ((1 << 64) - 1), int(level), int(sweep), ptr(ids),
                   ids.size, ptr(out))
         return out
+
+    def plan_async(self, bin_mask=15):
+        self.call("slm_plan_sweep_async", int(bin_mask))
+
+    def plan_groups(self):
+        g = C.c_int64()
+        rows = np.zeros(3, np.int64)
+        ents = np.zeros(3, np.int64)
+        self.call("slm_plan_groups", C.byref(g), ptr(rows), ptr(ents))
+        return g.value, rows, ents
+
+    def get_cstar(self):
+        cstar = np.empty(self.info()["n"], np.int64)
+        self.call("slm_get_cstar", ptr(cstar))
+        return cstar
+
+    def sync(self):
+        self.call("slm_sync")
 
     def last_commit_stats(self):
         c, r = C.c_int64(), C.c_int64()

@@ -203,6 +203,26 @@ int slm_get_union(slm_ctx *ctx, int64_t *ptr, int64_t *nbr, double *u) {
     API_END
 }
 
+int slm_get_union_rows(slm_ctx *ctx, int64_t r0, int64_t r1, int64_t *ptr_out, int64_t *nbr_out,
+                       double *u_out) {
+    API_BEGIN
+    require_graph(ctx);
+    const LevelGraph &G = *ctx->g;
+    SLM_REQUIRE(r0 >= 0 && r0 <= r1 && r1 <= G.n, SLM_EINVAL, "row range out of bounds");
+    std::vector<int64_t> p(r1 - r0 + 1);
+    CUDA_TRY(cudaMemcpy(p.data(), G.uptr.p + r0, (r1 - r0 + 1) * 8, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i <= r1 - r0; i++) ptr_out[i] = p[i] - p[0];
+    const int64_t cnt = p[r1 - r0] - p[0];
+    if (nbr_out && cnt) {
+        std::vector<int32_t> tmp(cnt);
+        CUDA_TRY(cudaMemcpy(tmp.data(), G.unbr.p + p[0], cnt * 4, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < cnt; i++) nbr_out[i] = tmp[i];
+    }
+    if (u_out && cnt)
+        CUDA_TRY(cudaMemcpy(u_out, G.uu.p + p[0], cnt * 8, cudaMemcpyDeviceToHost));
+    API_END
+}
+
 int slm_get_strengths(slm_ctx *ctx, double *s_out, double *s_in) {
     API_BEGIN
     require_graph(ctx);
@@ -356,6 +376,55 @@ int slm_plan_sweep(slm_ctx *ctx, const int64_t *comm_in, int64_t *cstar_out) {
     ctx->cstar.resize(G.n);
     run_plan(ctx, G, F, gain_m(ctx), ctx->cstar.p);
     download_i32_as_i64(ctx, ctx->cstar.p, G.n, cstar_out);
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    API_END
+}
+
+int slm_plan_sweep_async(slm_ctx *ctx, int32_t bin_mask) {
+    API_BEGIN
+    require_agg(ctx);
+    const LevelGraph &G = *ctx->g;
+    ctx->cstar.resize(G.n);
+    run_plan(ctx, G, ctx->f, gain_m(ctx), ctx->cstar.p, bin_mask, nullptr);
+    API_END
+}
+
+int slm_plan_groups(slm_ctx *ctx, int64_t *groups, int64_t *bin_rows, int64_t *bin_entries) {
+    API_BEGIN
+    require_agg(ctx);
+    const LevelGraph &G = *ctx->g;
+    DBuf<unsigned long long> d;
+    d.resize(1);
+    CUDA_TRY(cudaMemsetAsync(d.p, 0, 8, ctx->stream));
+    ctx->cstar.resize(G.n);
+    run_plan(ctx, G, ctx->f, gain_m(ctx), ctx->cstar.p, 15, d.p);
+    unsigned long long h = 0;
+    CUDA_TRY(cudaMemcpyAsync(&h, d.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (groups) *groups = (int64_t)h;
+    if (bin_rows)
+        for (int b = 0; b < NBINS; b++) bin_rows[b] = G.bin_off[b + 1] - G.bin_off[b];
+    if (bin_entries) {
+        // entries per bin: sum of degrees of the rows in each bin (host reduction)
+        std::vector<int64_t> up(G.n + 1);
+        std::vector<int32_t> rows(G.bin_off[NBINS]);
+        CUDA_TRY(cudaMemcpy(up.data(), G.uptr.p, (G.n + 1) * 8, cudaMemcpyDeviceToHost));
+        if (!rows.empty())
+            CUDA_TRY(cudaMemcpy(rows.data(), G.bin_rows.p, rows.size() * 4, cudaMemcpyDeviceToHost));
+        for (int b = 0; b < NBINS; b++) {
+            int64_t e = 0;
+            for (int64_t k = G.bin_off[b]; k < G.bin_off[b + 1]; k++) e += up[rows[k] + 1] - up[rows[k]];
+            bin_entries[b] = e;
+        }
+    }
+    API_END
+}
+
+int slm_get_cstar(slm_ctx *ctx, int64_t *cstar_out) {
+    API_BEGIN
+    require_graph(ctx);
+    SLM_REQUIRE(ctx->cstar.n == (size_t)ctx->g->n, SLM_ESTATE, "no plan computed");
+    download_i32_as_i64(ctx, ctx->cstar.p, ctx->g->n, cstar_out);
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     API_END
 }

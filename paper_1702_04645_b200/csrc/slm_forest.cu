@@ -96,8 +96,12 @@ __global__ void k_head_flag(const int32_t *key, const int32_t *first, int64_t n,
     GS_LOOP(i, n) h[i] = (first[key[i]] == (int32_t)i) ? 1 : 0;
 }
 __global__ void k_assign_label(const int32_t *key, const int32_t *first, const int32_t *lab,
-                               int64_t n, int32_t *comm) {
-    GS_LOOP(i, n) comm[i] = lab[first[key[i]]];
+                               int64_t n, int32_t *comm, int32_t *croot) {
+    GS_LOOP(i, n) {
+        int32_t c = lab[first[key[i]]];
+        comm[i] = c;
+        if (key[i] == (int32_t)i) croot[c] = (int32_t)i;   // the smallest cycle node
+    }
 }
 
 __global__ void k_iota(int32_t *x, int64_t n) { GS_LOOP(i, n) x[i] = (int32_t)i; }
@@ -173,6 +177,58 @@ __global__ void k_dfs_layout(const int32_t *cptr, const int32_t *members, const 
                 sp--;
             }
         }
+    }
+}
+
+// ---- depth-parallel DFS layout (any community size; O(n * depth) work, depth is small)
+
+__global__ void k_depth(const int32_t *a, const int32_t *comm, const int32_t *croot, int64_t n,
+                        int cap, uint32_t *depth, int32_t *iota, int32_t *flags) {
+    GS_LOOP(x, n) {
+        const int32_t r = croot[comm[x]];
+        int32_t y = (int32_t)x;
+        int d = 0;
+        while (y != r && d < cap) {
+            y = a[y];
+            d++;
+        }
+        if (y != r) atomicOr(&flags[0], 1);
+        depth[x] = (uint32_t)d;
+        iota[x] = (int32_t)x;
+        atomicMax(&flags[1], d);
+    }
+}
+__global__ void k_ones(int32_t *x, int64_t n) { GS_LOOP(i, n) x[i] = 1; }
+__global__ void k_size_level(const int32_t *nodes, int64_t lo, int64_t hi, const int32_t *a,
+                             int32_t *sz) {
+    for (int64_t k = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < hi;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        int32_t x = nodes[k];
+        atomicAdd(&sz[a[x]], sz[x]);
+    }
+}
+__global__ void k_kid_vals(const int32_t *kids, int64_t nk, const int32_t *comm,
+                           const int32_t *croot, const int32_t *sz, int32_t *val) {
+    GS_LOOP(j, nk) {
+        int32_t k = kids[j];
+        val[j] = (croot[comm[k]] == k) ? 0 : sz[k];
+    }
+}
+__global__ void k_kid_off(const int32_t *kids, const int32_t *ex, int64_t nk, int32_t *offp) {
+    GS_LOOP(j, nk) offp[kids[j]] = 1 + ex[j];
+}
+__global__ void k_positions(const int32_t *a, const int32_t *comm, const int32_t *croot,
+                            const int32_t *offp, const int32_t *cptr, int64_t n, int32_t *pos,
+                            int32_t *order) {
+    GS_LOOP(x, n) {
+        const int32_t c = comm[x], r = croot[c];
+        int32_t y = (int32_t)x, p = 0;
+        while (y != r) {
+            p += offp[y];
+            y = a[y];
+        }
+        pos[x] = p;
+        order[cptr[c] + p] = (int32_t)x;
     }
 }
 
@@ -261,7 +317,8 @@ void run_components(slm_ctx *ctx, Forest &F, int64_t n) {
     CUDA_TRY(cudaMemsetAsync(h.p + n, 0, 4, s));
     k_head_flag<<<G, 256, 0, s>>>(key, first, n, h.p);
     cub_exclusive_sum<int32_t>(ctx, h.p, lab.p, n + 1);
-    k_assign_label<<<G, 256, 0, s>>>(key, first, lab.p, n, F.comm.p);
+    F.croot.resize(n);
+    k_assign_label<<<G, 256, 0, s>>>(key, first, lab.p, n, F.comm.p, F.croot.p);
     int32_t nc = 0;
     CUDA_TRY(cudaMemcpyAsync(&nc, lab.p + n, 4, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -305,11 +362,73 @@ void build_layout(slm_ctx *ctx, Forest &F) {
     k_iota<<<grid_for(n, 256), 256, 0, s>>>(iota, n);
     if (n > 0) sort_pairs_u32_i32(ctx, kk, ks, iota, F.kids.p, n, bits_for(n + 1));
     k_lb_ptr32<<<grid_for(n + 1, 256), 256, 0, s>>>((const int32_t *)ks, n, n, F.kptr.p);
-    int32_t *stk_node = ctx->i32a.resize(n);
-    int32_t *stk_it = ctx->i32b.resize(n);
-    k_dfs_layout<<<grid_for(nc, 64), 64, 0, s>>>(F.cptr.p, F.members.p, F.on_cycle.p, F.kptr.p,
-                                                 F.kids.p, nc, F.order.p, F.pos.p, F.sz.p,
-                                                 stk_node, stk_it);
+    // depth of every node below its community root (parent = a[x])
+    int32_t *flags = ctx->i32d.resize(2);
+    CUDA_TRY(cudaMemsetAsync(flags, 0, 8, s));
+    DBuf<uint32_t> depth, depth_sorted;
+    DBuf<int32_t> by_depth;
+    depth.resize(n);
+    depth_sorted.resize(n);
+    by_depth.resize(n);
+    int32_t *iota2 = ctx->i32a.resize(n);
+    k_depth<<<grid_for(n, 256), 256, 0, s>>>(F.a.p, F.comm.p, F.croot.p, n, 4096, depth.p,
+                                              iota2, flags);
+    int32_t hf[2];
+    CUDA_TRY(cudaMemcpyAsync(hf, flags, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    const int maxd = hf[1];
+    if (hf[0]) {
+        // pathological depth (> 4096): sequential DFS per community
+        int32_t *stk_node = ctx->i32a.resize(n);
+        DBuf<int32_t> stk_it;
+        stk_it.resize(n);
+        k_dfs_layout<<<grid_for(nc, 64), 64, 0, s>>>(F.cptr.p, F.members.p, F.on_cycle.p, F.kptr.p,
+                                                     F.kids.p, nc, F.order.p, F.pos.p, F.sz.p,
+                                                     stk_node, stk_it.p);
+        CUDA_TRY(cudaGetLastError());
+        F.layout_valid = true;
+        return;
+    }
+    // subtree sizes bottom-up, one launch per depth level
+    if (n > 0)
+        sort_pairs_u32_i32(ctx, depth.p, depth_sorted.p, iota2, by_depth.p, n, bits_for(maxd + 2));
+    std::vector<int64_t> lvl(maxd + 2, 0);
+    {
+        DBuf<int32_t> lb;
+        lb.resize(maxd + 2);
+        k_lb_ptr32<<<1, 128, 0, s>>>((const int32_t *)depth_sorted.p, n, maxd + 1, lb.p);
+        std::vector<int32_t> h(maxd + 2);
+        CUDA_TRY(cudaMemcpyAsync(h.data(), lb.p, (maxd + 2) * 4, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        for (int d = 0; d <= maxd + 1; d++) lvl[d] = h[d];
+    }
+    k_ones<<<grid_for(n, 256), 256, 0, s>>>(F.sz.p, n);
+    for (int d = maxd; d >= 1; d--) {
+        int64_t lo = lvl[d], hi = lvl[d + 1];
+        if (hi > lo)
+            k_size_level<<<grid_for(hi - lo, 256), 256, 0, s>>>(by_depth.p, lo, hi, F.a.p, F.sz.p);
+    }
+    // offsets among siblings (kids ascending, the root never a kid) and pre-order positions
+    int32_t nk = 0;
+    CUDA_TRY(cudaMemcpyAsync(&nk, F.kptr.p + n, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    DBuf<int32_t> val, ex, offp;
+    val.resize(nk);
+    ex.resize(nk);
+    offp.resize(n);
+    if (nk > 0) {
+        k_kid_vals<<<grid_for(nk, 256), 256, 0, s>>>(F.kids.p, nk, F.comm.p, F.croot.p, F.sz.p, val.p);
+        size_t tb = 0;
+        CUDA_TRY(cub::DeviceScan::ExclusiveSumByKey(nullptr, tb, (const uint32_t *)ks, val.p, ex.p,
+                                                    (int64_t)nk, cub::Equality(), s));
+        ctx->tmp.resize(tb);
+        CUDA_TRY(cub::DeviceScan::ExclusiveSumByKey(ctx->tmp.p, tb, (const uint32_t *)ks, val.p,
+                                                    ex.p, (int64_t)nk, cub::Equality(), s));
+        k_kid_off<<<grid_for(nk, 256), 256, 0, s>>>(F.kids.p, ex.p, nk, offp.p);
+    }
+    k_positions<<<grid_for(n, 256), 256, 0, s>>>(F.a.p, F.comm.p, F.croot.p, offp.p, F.cptr.p, n,
+                                                  F.pos.p, F.order.p);
+    CUDA_TRY(cudaGetLastError());
     F.layout_valid = true;
 }
 

@@ -106,6 +106,7 @@ struct Forest {
     DBuf<int32_t> a, comm;
     DBuf<uint8_t> on_cycle;
     DBuf<int32_t> cptr, members;        // members sorted by (comm, node)
+    DBuf<int32_t> croot;                // per community: smallest cycle node (DFS root)
     DBuf<double> S_out, S_in;
     DBuf<int32_t> count;
     // DFS pre-order layout per community (root = smallest cycle node)
@@ -244,7 +245,8 @@ void run_assign(slm_ctx *ctx, const LevelGraph &G, double m, int32_t *d_a);
 void run_components(slm_ctx *ctx, Forest &F, int64_t n);
 void build_members_and_aggregates(slm_ctx *ctx, const LevelGraph &G, Forest &F);
 void build_layout(slm_ctx *ctx, Forest &F);
-void run_plan(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_t *d_cstar);
+void run_plan(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_t *d_cstar,
+              int bin_mask = 15, unsigned long long *d_groups = nullptr);
 void run_local_gains(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, double *d_lg,
                      uint8_t *d_bad);
 void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_t scc_cap,

@@ -26,6 +26,7 @@ struct PlanArgs {
     const double *s_out, *s_in;
     double m, m2;
     int32_t *cstar;
+    unsigned long long *groups;   // distinct (node, community) groups seen (roofline G)
 };
 
 __device__ __forceinline__ bool better(double t1, int32_t c1, double t2, int32_t c2) {
@@ -79,6 +80,10 @@ __global__ void __launch_bounds__(256) k_plan_small(PlanArgs A, const int32_t *r
         }
         const bool leader = valid && (lane == __ffs(mask) - 1);
         const bool own = (c == L);
+        if (A.groups) {
+            unsigned lm = __ballot_sync(0xffffffffu, leader);
+            if (lane == 0) atomicAdd(A.groups, (unsigned long long)__popc(lm));
+        }
         double t = -INFINITY;
         if (leader) t = plan_gain(gs, own, so, si, A.S_in[c], A.S_out[c], A.m, A.m2);
         const unsigned ownmask = __ballot_sync(0xffffffffu, leader && own);
@@ -147,9 +152,11 @@ __device__ void plan_row_hash(const PlanArgs &A, int32_t r, int32_t *hk, double 
     __syncthreads();
     double bt = -INFINITY;
     int32_t bc = 0x7fffffff;
+    unsigned ng = 0;
     for (uint32_t k = threadIdx.x; k < H; k += BLOCK) {
         int32_t c = hk[k];
         if (c < 0) continue;
+        ng++;
         bool own = (c == L);
         double t = plan_gain(hv[k], own, so, si, A.S_in[c], A.S_out[c], A.m, A.m2);
         if (own) *sh_stay = t;
@@ -157,6 +164,11 @@ __device__ void plan_row_hash(const PlanArgs &A, int32_t r, int32_t *hk, double 
             bt = t;
             bc = c;
         }
+    }
+    if (A.groups) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) ng += __shfl_xor_sync(0xffffffffu, ng, off);
+        if ((threadIdx.x & 31) == 0 && ng) atomicAdd(A.groups, (unsigned long long)ng);
     }
     __syncthreads();
     block_argmax<BLOCK>(bt, bc, sh_t, sh_c);
@@ -204,6 +216,7 @@ __global__ void __launch_bounds__(LARGE_BLOCK) k_plan_large(PlanArgs A, const in
 
 static PlanArgs make_args(const LevelGraph &G, const Forest &F, double m, int32_t *cstar) {
     PlanArgs A;
+    A.groups = nullptr;
     A.uptr = G.uptr.p;
     A.unbr = G.unbr.p;
     A.uu = G.uu.p;
@@ -224,18 +237,20 @@ __global__ void k_copy_labels(const int32_t *label, int64_t n, int32_t *out) {
         out[i] = label[i];
 }
 
-void run_plan(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_t *d_cstar) {
+void run_plan(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_t *d_cstar,
+              int bin_mask, unsigned long long *d_groups) {
     cudaStream_t s = ctx->stream;
     int64_t n = G.n;
     // rows without entries keep their label (detector.py:379-382)
-    k_copy_labels<<<grid_for(n, 256), 256, 0, s>>>(F.comm.p, n, d_cstar);
+    if (bin_mask & 8) k_copy_labels<<<grid_for(n, 256), 256, 0, s>>>(F.comm.p, n, d_cstar);
     PlanArgs A = make_args(G, F, m, d_cstar);
+    A.groups = d_groups;
     int64_t ns = G.bin_off[1] - G.bin_off[0];
     int64_t nm = G.bin_off[2] - G.bin_off[1];
     int64_t nl = G.bin_off[3] - G.bin_off[2];
-    if (ns)
+    if (ns && (bin_mask & 1))
         k_plan_small<<<grid_for(ns * 32, 256, 148LL * 64), 256, 0, s>>>(A, G.bin_rows.p + G.bin_off[0], ns);
-    if (nm) {
+    if (nm && (bin_mask & 2)) {
         size_t sm = MID_H * (sizeof(double) + sizeof(int32_t));
         static bool attr = false;
         if (!attr) {
@@ -244,7 +259,7 @@ void run_plan(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_t *d
         }
         k_plan_mid<<<(unsigned)std::min<int64_t>(nm, 148 * 2 * 8), MID_BLOCK, sm, s>>>(A, G.bin_rows.p + G.bin_off[1], nm);
     }
-    if (nl) {
+    if (nl && (bin_mask & 4)) {
         ctx->hash_keys.resize(G.large_hash_total);
         ctx->hash_vals.resize(G.large_hash_total);
         k_plan_large<<<(unsigned)std::min<int64_t>(nl, 148 * 2), LARGE_BLOCK, 0, s>>>(

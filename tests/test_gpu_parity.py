@@ -238,3 +238,43 @@ def test_device_generators_match_host(slm):
         ctx_h.build_graph(n, s, d, w)
         for x, y in zip(ctx_d.csr(), ctx_h.csr()):
             np.testing.assert_array_equal(x, y)
+
+
+def test_giant_part_executor_parity(slm, golden, oracle, monkeypatch):
+    """Force the incremental grid executor (normally for parts > 4096 members) onto every
+    bad community and check the same bit-exact outcomes."""
+    from paper_1702_04645_b200 import generators as GN
+    monkeypatch.setenv("SLM_SMALL_PART", "3")
+    for key in case_names(golden):
+        if not exact_sums(key):
+            continue
+        n, s, d, w = case_edges(golden, key)
+        seed, p = int(golden[f"{key}/seed"]), float(golden[f"{key}/p"])
+        g = slm.Graph.from_edges(n, s, d, w)
+        cfg = slm.RunConfig(seed=seed, accept_prob=p)
+        f = slm.extract_components(golden[f"{key}/assign"])
+        f2, sp, un, gains = slm.positive_correction(g, None, f, cfg)
+        np.testing.assert_array_equal(f2.a, golden[f"{key}/pos_a"], err_msg=key)
+        assert [sp, un] == list(golden[f"{key}/pos_stats"]), key
+        np.testing.assert_array_equal(gains, golden[f"{key}/pos_gains"], err_msg=key)
+    for n, s, d, w in (GN.rmat(12, 16, 1, 4), GN.generate("c1_sbm")):
+        _vs_oracle(slm, oracle, n, s, d, w)
+    monkeypatch.setenv("SLM_SMALL_PART", "64")
+    n, s, d, w = GN.rmat(13, 16, 1, 5)
+    _vs_oracle(slm, oracle, n, s, d, w)
+
+
+def test_positive_large_rmat_vs_oracle(slm, oracle):
+    """Hub communities well beyond the warp executor (R-MAT 16): one POSITIVE call."""
+    from paper_1702_04645_b200 import generators as GN
+    n, s, d, w = GN.rmat(16, 16, 1, 4)
+    g = slm.Graph.from_edges(n, s, d, w)
+    a = slm.find_assignment(g)
+    f = slm.extract_components(a)
+    f2, sp, un, gains = slm.positive_correction(g, None, f, slm.RunConfig())
+    og = oracle.OGraph.from_edges(n, s, d, w)
+    comm, nc, _ = oracle.extract_components(a)
+    a2, ch, osp, oun, ogains, _ = oracle.positive_correction(og, a, comm, nc)
+    np.testing.assert_array_equal(f2.a, a2)
+    assert (sp, un) == (osp, oun)
+    np.testing.assert_array_equal(gains, ogains)
