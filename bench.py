@@ -251,7 +251,7 @@ def main():
         return a.elapsed_time(b)
 
     for _ in range(args.warmup):
-        ctx.plan_async(15)
+        ctx.plan_async(127)
     ctx.sync()
     if ws > 1:
         import torch.distributed as dist
@@ -259,7 +259,7 @@ def main():
     torch.cuda.synchronize()
     ctx.sync()
     with Clocks(local) as clk:
-        ms = timed(15, args.steps)
+        ms = timed(127, args.steps)
     ctx.sync()
     torch.cuda.synchronize()
     ms_t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
@@ -274,8 +274,12 @@ def main():
 
     # per-bin device times (explanation only)
     per_bin = {}
-    for mask, name in ((1, "small_warp"), (2, "mid_cta_smem_hash"), (4, "hub_cta_global_hash"),
-                       (8, "label_copy")):
+    for mask, name in ((1, "bin0_packed_warp"), (2, "bin1_warp_hash512"),
+                       (4, "bin2_warp_hash2048"), (8, "bin3_cta_hash8192"),
+                       (16, "bin4_cta_hash16384"), (32, "bin5_cta_global_hash"),
+                       (64, "label_copy")):
+        if mask < 64 and bin_rows[mask.bit_length() - 1] == 0:
+            continue
         per_bin[name] = round(timed(mask, max(3, args.steps // 4)) / max(3, args.steps // 4), 4)
 
     # e2e through the C ABI with pinned host buffers

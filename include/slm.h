@@ -106,9 +106,10 @@ SLM_API int slm_positive(slm_ctx *ctx, const slm_config *cfg, int64_t *splits, i
  * aggregates recomputed from it); cstar_out nullable. */
 SLM_API int slm_plan_sweep(slm_ctx *ctx, const int64_t *comm_in, int64_t *cstar_out);
 /* Bench helpers: enqueue one plan sweep on the context stream without synchronising or
- * copying (bin_mask: 1 small rows, 2 mid rows, 4 hub rows, 8 label copy for empty rows;
- * 15 = the full sweep); count distinct (node, community) groups G of the last snapshot and
- * the rows / union entries of each degree bin; read the last plan's targets. */
+ * copying (bin_mask bit b = degree bin b of 6 (<=32, <=256, <=1024, <=4096, <=16383,
+ * larger), bit 6 = label copy for rows without entries; 127 = the full sweep); count the
+ * distinct (node, community) groups G of the snapshot and the rows / union entries of each
+ * of the 6 degree bins; read the last plan's targets. */
 SLM_API int slm_plan_sweep_async(slm_ctx *ctx, int32_t bin_mask);
 SLM_API int slm_plan_groups(slm_ctx *ctx, int64_t *groups, int64_t *bin_rows, int64_t *bin_entries);
 SLM_API int slm_get_cstar(slm_ctx *ctx, int64_t *cstar_out);

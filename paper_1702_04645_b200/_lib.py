@@ -281,13 +281,13 @@ class Context:
                   ids.size, ptr(out))
         return out
 
-    def plan_async(self, bin_mask=15):
+    def plan_async(self, bin_mask=127):
         self.call("slm_plan_sweep_async", int(bin_mask))
 
     def plan_groups(self):
         g = C.c_int64()
-        rows = np.zeros(3, np.int64)
-        ents = np.zeros(3, np.int64)
+        rows = np.zeros(6, np.int64)
+        ents = np.zeros(6, np.int64)
         self.call("slm_plan_groups", C.byref(g), ptr(rows), ptr(ents))
         return g.value, rows, ents
 

@@ -218,15 +218,33 @@ __global__ void k_pw_segments(const double *a, const int64_t *off, const int64_t
         out[i] = pw_sum_seq(a + off[i], len[i]);
 }
 
-__global__ void k_degree_bins(const int64_t *uptr, int64_t n, int64_t *flag_small,
-                              int64_t *flag_mid, int64_t *flag_large, int32_t *maxdeg) {
+__global__ void k_degree_bins(const int64_t *uptr, int64_t n, int64_t *flags, int32_t *maxdeg) {
+    // flags: NBINS arrays of n+1 entries
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
          r += (int64_t)gridDim.x * blockDim.x) {
         int64_t d = uptr[r + 1] - uptr[r];
-        flag_small[r] = (d >= 1 && d <= SMALL_MAX);
-        flag_mid[r] = (d > SMALL_MAX && d <= MID_MAX);
-        flag_large[r] = (d > MID_MAX);
+        int bin = -1;
+        if (d > 0) {
+            bin = 0;
+            while (d > bin_hi(bin)) bin++;
+        }
+        for (int b = 0; b < NBINS; b++) flags[b * (n + 1) + r] = (b == bin);
         if (d > 0) atomicMax(maxdeg, (int32_t)(d > 0x7fffffff ? 0x7fffffff : d));
+    }
+}
+
+__global__ void k_make_u32(const double *uu, int64_t ue, const double *s_out, const double *s_in,
+                           int64_t n, uint32_t *u32, int32_t *bad, double2 *s2) {
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = t; e < ue; e += stride) {
+        double x = uu[e];
+        if (!(x >= 0.0 && x < 4294967296.0 && x == floor(x))) atomicOr(bad, 1);
+        else u32[e] = (uint32_t)x;
+    }
+    for (int64_t r = t; r < n; r += stride) {
+        if (!(s_out[r] + s_in[r] < 4294967296.0)) atomicOr(bad, 1);
+        s2[r] = make_double2(s_out[r], s_in[r]);
     }
 }
 
@@ -287,52 +305,85 @@ double device_pairwise_sum(slm_ctx *ctx, const double *d_a, int64_t n) {
 static void build_bins(slm_ctx *ctx, LevelGraph &G) {
     int64_t n = G.n;
     cudaStream_t s = ctx->stream;
-    DBuf<int64_t> f[3], p[3];
-    for (int b = 0; b < 3; b++) {
-        f[b].resize(n + 1);
-        p[b].resize(n + 1);
-    }
+    DBuf<int64_t> f, p;
+    f.resize((n + 1) * NBINS);
+    p.resize(n + 1);
     int32_t *d_max = ctx->i32d.resize(1);
     CUDA_TRY(cudaMemsetAsync(d_max, 0, 4, s));
-    k_degree_bins<<<grid_for(n, 256), 256, 0, s>>>(G.uptr.p, n, f[0].p, f[1].p, f[2].p, d_max);
-    int64_t tot[3];
-    for (int b = 0; b < 3; b++) {
-        CUDA_TRY(cudaMemsetAsync(f[b].p + n, 0, 8, s));
-        cub_exclusive_sum<int64_t>(ctx, f[b].p, p[b].p, n + 1);
-        CUDA_TRY(cudaMemcpyAsync(&tot[b], p[b].p + n, 8, cudaMemcpyDeviceToHost, s));
+    k_degree_bins<<<grid_for(n, 256), 256, 0, s>>>(G.uptr.p, n, f.p, d_max);
+    int64_t tot[NBINS];
+    G.bin_rows.resize(n > 0 ? n : 1);
+    G.bin_off[0] = 0;
+    for (int b = 0; b < NBINS; b++) {
+        int64_t *fb = f.p + b * (n + 1);
+        CUDA_TRY(cudaMemsetAsync(fb + n, 0, 8, s));
+        cub_exclusive_sum<int64_t>(ctx, fb, p.p, n + 1);
+        CUDA_TRY(cudaMemcpyAsync(&tot[b], p.p + n, 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        G.bin_off[b + 1] = G.bin_off[b] + tot[b];
+        if (tot[b])
+            k_scatter_bin<<<grid_for(n, 256), 256, 0, s>>>(fb, p.p, n, G.bin_off[b], G.bin_rows.p);
     }
     int32_t mx = 0;
     CUDA_TRY(cudaMemcpyAsync(&mx, d_max, 4, cudaMemcpyDeviceToHost, s));
+    std::vector<int32_t> rows(G.bin_off[NBINS]);
+    std::vector<int64_t> up(n + 1);
+    if (!rows.empty())
+        CUDA_TRY(cudaMemcpyAsync(rows.data(), G.bin_rows.p, rows.size() * 4,
+                                 cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(up.data(), G.uptr.p, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     G.max_deg = mx;
-    G.bin_off[0] = 0;
-    for (int b = 0; b < 3; b++) G.bin_off[b + 1] = G.bin_off[b] + tot[b];
-    G.bin_rows.resize(G.bin_off[3] > 0 ? G.bin_off[3] : 1);
-    for (int b = 0; b < 3; b++)
-        if (tot[b])
-            k_scatter_bin<<<grid_for(n, 256), 256, 0, s>>>(f[b].p, p[b].p, n, G.bin_off[b],
-                                                            G.bin_rows.p);
-    // global hash scratch offsets for large rows (capacity next pow2 >= 2*deg)
-    int64_t nl = tot[2];
+    for (int b = 0; b < NBINS; b++) {
+        int64_t e = 0;
+        for (int64_t k = G.bin_off[b]; k < G.bin_off[b + 1]; k++) e += up[rows[k] + 1] - up[rows[k]];
+        G.bin_entries[b] = e;
+    }
+    // global hash scratch offsets for rows with d > MID_MAX (capacity next pow2 > d)
+    const int64_t b0 = G.bin_off[4], nl = G.bin_off[NBINS] - b0;
     G.large_hash_total = 0;
     if (nl) {
-        std::vector<int32_t> rows(nl);
-        std::vector<int64_t> up(n + 1);
-        CUDA_TRY(cudaMemcpyAsync(rows.data(), G.bin_rows.p + G.bin_off[2], nl * 4,
-                                 cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaMemcpyAsync(up.data(), G.uptr.p, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaStreamSynchronize(s));
         std::vector<int64_t> hoff(nl + 1);
         int64_t acc = 0;
         for (int64_t i = 0; i < nl; i++) {
-            int64_t d = up[rows[i] + 1] - up[rows[i]];
-            int64_t cap = 1;
-            while (cap < 2 * d) cap <<= 1;
+            int64_t d = up[rows[b0 + i] + 1] - up[rows[b0 + i]];
+            int64_t cap = 32;
+            while (cap <= d) cap <<= 1;   // > d >= distinct communities of the row
             hoff[i] = acc;
             acc += cap;
         }
         hoff[nl] = acc;
         G.large_hash_total = acc;
+        // hub rows (bin 5): (row << 20 | segment) items of 8192 entries, grouped in waves
+        // whose tables (12 B per slot) fit in ~48 MB of L2
+        const int64_t nb4 = G.bin_off[5] - G.bin_off[4];
+        const int64_t budget = 4 << 20;   // slots per wave
+        std::vector<int64_t> segs;
+        G.hub_waves.clear();
+        G.hub_wave_slots = 0;
+        int64_t wbase = -1, wslots = 0;
+        for (int64_t i = nb4; i < nl; i++) {
+            const int64_t H = hoff[i + 1] - hoff[i];
+            if (wbase < 0 || wslots + H > budget) {
+                if (wbase >= 0) G.hub_wave_slots = std::max(G.hub_wave_slots, wslots);
+                G.hub_waves.push_back({i - nb4, (int64_t)segs.size(), hoff[i]});
+                wbase = hoff[i];
+                wslots = 0;
+            }
+            wslots += H;
+            int64_t d = up[rows[b0 + i] + 1] - up[rows[b0 + i]];
+            for (int64_t q = 0; q * 8192 < d; q++) segs.push_back(((i - nb4) << 20) | q);
+        }
+        if (wbase >= 0) {
+            G.hub_wave_slots = std::max(G.hub_wave_slots, wslots);
+            G.hub_waves.push_back({nl - nb4, (int64_t)segs.size(), hoff[nl]});
+        }
+        G.hub_nseg = (int64_t)segs.size();
+        if (!segs.empty()) {
+            G.hub_seg.resize(segs.size());
+            CUDA_TRY(cudaMemcpyAsync(G.hub_seg.p, segs.data(), segs.size() * 8,
+                                     cudaMemcpyHostToDevice, s));
+        }
         G.large_hoff.resize(nl + 1);
         CUDA_TRY(cudaMemcpyAsync(G.large_hoff.p, hoff.data(), (nl + 1) * 8,
                                  cudaMemcpyHostToDevice, s));
@@ -455,6 +506,25 @@ void build_level_from_keys(slm_ctx *ctx, LevelGraph &G, int64_t n, DBuf<uint64_t
     G.m_w = device_pairwise_sum(ctx, G.csr_w.p, ng);
     G.integral = (intbad[0] == 0) && (G.m_w < 9007199254740992.0);
     build_bins(ctx, G);
+    // compact integer weights for the plan sweep's fast path, interleaved strengths
+    G.s2.resize(n);
+    G.u32_ok = false;
+    if (G.integral) {
+        G.uu32.resize(G.ue);
+        int32_t *d_bad = ctx->i32c.resize(1);
+        CUDA_TRY(cudaMemsetAsync(d_bad, 0, 4, s));
+        k_make_u32<<<grid_for(std::max<int64_t>(G.ue, n), 256), 256, 0, s>>>(
+            G.uu.p, G.ue, G.s_out.p, G.s_in.p, n, G.uu32.p, d_bad, G.s2.p);
+        int32_t hb = 0;
+        CUDA_TRY(cudaMemcpyAsync(&hb, d_bad, 4, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        G.u32_ok = (hb == 0);
+        if (!G.u32_ok) G.uu32.release();
+    } else {
+        int32_t *d_bad = ctx->i32c.resize(1);
+        k_make_u32<<<grid_for(n, 256), 256, 0, s>>>(G.uu.p, 0, G.s_out.p, G.s_in.p, n, nullptr,
+                                                      d_bad, G.s2.p);
+    }
     CUDA_TRY(cudaStreamSynchronize(s));
 }
 

@@ -397,26 +397,15 @@ int slm_plan_groups(slm_ctx *ctx, int64_t *groups, int64_t *bin_rows, int64_t *b
     d.resize(1);
     CUDA_TRY(cudaMemsetAsync(d.p, 0, 8, ctx->stream));
     ctx->cstar.resize(G.n);
-    run_plan(ctx, G, ctx->f, gain_m(ctx), ctx->cstar.p, 15, d.p);
+    run_plan(ctx, G, ctx->f, gain_m(ctx), ctx->cstar.p, 127, d.p);
     unsigned long long h = 0;
     CUDA_TRY(cudaMemcpyAsync(&h, d.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     if (groups) *groups = (int64_t)h;
     if (bin_rows)
         for (int b = 0; b < NBINS; b++) bin_rows[b] = G.bin_off[b + 1] - G.bin_off[b];
-    if (bin_entries) {
-        // entries per bin: sum of degrees of the rows in each bin (host reduction)
-        std::vector<int64_t> up(G.n + 1);
-        std::vector<int32_t> rows(G.bin_off[NBINS]);
-        CUDA_TRY(cudaMemcpy(up.data(), G.uptr.p, (G.n + 1) * 8, cudaMemcpyDeviceToHost));
-        if (!rows.empty())
-            CUDA_TRY(cudaMemcpy(rows.data(), G.bin_rows.p, rows.size() * 4, cudaMemcpyDeviceToHost));
-        for (int b = 0; b < NBINS; b++) {
-            int64_t e = 0;
-            for (int64_t k = G.bin_off[b]; k < G.bin_off[b + 1]; k++) e += up[rows[k] + 1] - up[rows[k]];
-            bin_entries[b] = e;
-        }
-    }
+    if (bin_entries)
+        for (int b = 0; b < NBINS; b++) bin_entries[b] = G.bin_entries[b];
     API_END
 }
 

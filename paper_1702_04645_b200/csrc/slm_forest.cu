@@ -122,7 +122,7 @@ __global__ void k_lb_ptr32(const int32_t *sorted, int64_t m, int64_t nrows, int3
 // per-community sums in ascending member order (bincount order, quality.py:76-78)
 __global__ void k_comm_sums(const int32_t *cptr, const int32_t *members, const double *s_out,
                             const double *s_in, int64_t nc, double *S_out, double *S_in,
-                            int32_t *count) {
+                            int32_t *count, double2 *S2, float *S1f, float2 *S2f) {
     GS_LOOP(c, nc) {
         double so = 0.0, si = 0.0;
         for (int32_t k = cptr[c]; k < cptr[c + 1]; k++) {
@@ -132,6 +132,9 @@ __global__ void k_comm_sums(const int32_t *cptr, const int32_t *members, const d
         }
         S_out[c] = so;
         S_in[c] = si;
+        S2[c] = make_double2(so, si);
+        S1f[c] = (float)so;
+        S2f[c] = make_float2((float)so, (float)si);
         count[c] = cptr[c + 1] - cptr[c];
     }
 }
@@ -334,6 +337,9 @@ void build_members_and_aggregates(slm_ctx *ctx, const LevelGraph &G, Forest &F) 
     F.cptr.resize(nc + 1);
     F.S_out.resize(nc);
     F.S_in.resize(nc);
+    F.S2.resize(nc);
+    F.S1f.resize(nc);
+    F.S2f.resize(nc);
     F.count.resize(nc);
     int32_t *iota = ctx->i32a.resize(n);
     int32_t *ksorted = ctx->i32b.resize(n);
@@ -343,7 +349,7 @@ void build_members_and_aggregates(slm_ctx *ctx, const LevelGraph &G, Forest &F) 
                            bits_for(nc + 1));
     k_lb_ptr32<<<grid_for(nc + 1, 256), 256, 0, s>>>(ksorted, n, nc, F.cptr.p);
     k_comm_sums<<<grid_for(nc, 128), 128, 0, s>>>(F.cptr.p, F.members.p, G.s_out.p, G.s_in.p, nc,
-                                                  F.S_out.p, F.S_in.p, F.count.p);
+                                                  F.S_out.p, F.S_in.p, F.count.p, F.S2.p, F.S1f.p, F.S2f.p);
     F.agg_valid = true;
 }
 

@@ -74,9 +74,17 @@ struct DBuf {
 
 // --------------------------------------------------------------- level graph state
 
-enum { BIN_SMALL = 0, BIN_MID = 1, BIN_LARGE = 2, NBINS = 3 };
-constexpr int SMALL_MAX = 32;     // warp-per-row, lanes = entries
-constexpr int MID_MAX = 4096;     // CTA-per-row, shared-memory hash
+// union rows are binned by degree d; bin b holds BIN_LO[b] <= d <= BIN_HI[b]
+constexpr int NBINS = 6;
+__host__ __device__ constexpr int64_t bin_hi(int b) {
+    return b == 0 ? 32 : b == 1 ? 256 : b == 2 ? 1024 : b == 3 ? 4096 : b == 4 ? 16383 : INT64_MAX;
+}
+constexpr int SMALL_MAX = 32;     // warp lanes = entries (packed rows)
+constexpr int MID_MAX = 4096;     // generic path: CTA-per-row shared-memory hash up to here
+
+struct HubWave {            // a set of hub rows whose global tables fit in L2 together
+    int64_t row, seg, base;  // first hub row (bin-5 index), first segment, table base
+};
 
 // Canonical directed CSR + neighbour union + strengths of one hierarchy level
 // (graph.py:63-175, 257-263).  Node ids int32, entry offsets int64.
@@ -88,15 +96,24 @@ struct LevelGraph {
     DBuf<int64_t> uptr;
     DBuf<int32_t> unbr;
     DBuf<double> uu;          // w_out + w_in (F6)
+    DBuf<uint32_t> uu32;      // compact u when integral and every row total < 2^32
+    bool u32_ok = false;
     DBuf<double> s_out, s_in;
+    DBuf<double2> s2;         // {s_out, s_in} interleaved (one sector per node)
     double m_w = 0.0;
     bool sym = false;         // W == W^T (then s_in == s_out bitwise)
     bool integral = false;    // all weights integer-valued, m_w < 2^53
     // degree bins of union rows (ascending row ids inside each bin)
     DBuf<int32_t> bin_rows;
-    int64_t bin_off[NBINS + 1] = {0, 0, 0, 0};
-    DBuf<int64_t> large_hoff;  // per large row: offset into the global hash scratch
+    int64_t bin_off[NBINS + 1] = {0, 0, 0, 0, 0, 0, 0};
+    int64_t bin_entries[NBINS] = {0, 0, 0, 0, 0, 0};
+    DBuf<int64_t> large_hoff;  // per row with d > MID_MAX (bins 4, 5): global hash offset
     int64_t large_hash_total = 0;
+    // bin-5 (hub) rows: (row index << 20 | segment) work items of the global-table sweep
+    DBuf<int64_t> hub_seg;
+    int64_t hub_nseg = 0, hub_hash_total = 0, hub_hoff_base = 0;
+    std::vector<HubWave> hub_waves;   // bin-5 waves (+ sentinel)
+    int64_t hub_wave_slots = 0;       // largest wave's table slots
     int32_t max_deg = 0;
 };
 
@@ -108,6 +125,9 @@ struct Forest {
     DBuf<int32_t> cptr, members;        // members sorted by (comm, node)
     DBuf<int32_t> croot;                // per community: smallest cycle node (DFS root)
     DBuf<double> S_out, S_in;
+    DBuf<double2> S2;                   // {S_out, S_in} interleaved
+    DBuf<float> S1f;                    // float(S_out) (approximate pass of the sweep)
+    DBuf<float2> S2f;                   // float {S_out, S_in}
     DBuf<int32_t> count;
     // DFS pre-order layout per community (root = smallest cycle node)
     DBuf<int32_t> order, pos, sz, kptr, kids;
@@ -135,6 +155,8 @@ struct slm_ctx {
     DBuf<uint64_t> u64a, u64b;
     DBuf<double> hash_vals;
     DBuf<int32_t> hash_keys;
+    DBuf<int32_t> hk32;          // hub tables of the integer sweep (kept empty between rows)
+    DBuf<uint32_t> hv32, hocc32, hnocc32;
     int32_t *h_flag = nullptr;   // pinned host scalars
     int64_t *h_i64 = nullptr;
     double *h_f64 = nullptr;
@@ -246,7 +268,9 @@ void run_components(slm_ctx *ctx, Forest &F, int64_t n);
 void build_members_and_aggregates(slm_ctx *ctx, const LevelGraph &G, Forest &F);
 void build_layout(slm_ctx *ctx, Forest &F);
 void run_plan(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_t *d_cstar,
-              int bin_mask = 15, unsigned long long *d_groups = nullptr);
+              int bin_mask = 127, unsigned long long *d_groups = nullptr);
+void run_plan_u32(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_t *d_cstar,
+                  int bin_mask, unsigned long long *d_groups);
 void run_local_gains(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, double *d_lg,
                      uint8_t *d_bad);
 void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_t scc_cap,

@@ -239,18 +239,23 @@ __global__ void k_copy_labels(const int32_t *label, int64_t n, int32_t *out) {
 
 void run_plan(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_t *d_cstar,
               int bin_mask, unsigned long long *d_groups) {
+    if (G.u32_ok) {
+        run_plan_u32(ctx, G, F, m, d_cstar, bin_mask, d_groups);
+        return;
+    }
+    // generic fp64 path (non-integer weights or row totals >= 2^32)
     cudaStream_t s = ctx->stream;
     int64_t n = G.n;
     // rows without entries keep their label (detector.py:379-382)
-    if (bin_mask & 8) k_copy_labels<<<grid_for(n, 256), 256, 0, s>>>(F.comm.p, n, d_cstar);
+    if (bin_mask & 64) k_copy_labels<<<grid_for(n, 256), 256, 0, s>>>(F.comm.p, n, d_cstar);
     PlanArgs A = make_args(G, F, m, d_cstar);
     A.groups = d_groups;
     int64_t ns = G.bin_off[1] - G.bin_off[0];
-    int64_t nm = G.bin_off[2] - G.bin_off[1];
-    int64_t nl = G.bin_off[3] - G.bin_off[2];
+    int64_t nm = G.bin_off[4] - G.bin_off[1];
+    int64_t nl = G.bin_off[6] - G.bin_off[4];
     if (ns && (bin_mask & 1))
         k_plan_small<<<grid_for(ns * 32, 256, 148LL * 64), 256, 0, s>>>(A, G.bin_rows.p + G.bin_off[0], ns);
-    if (nm && (bin_mask & 2)) {
+    if (nm && (bin_mask & 14)) {
         size_t sm = MID_H * (sizeof(double) + sizeof(int32_t));
         static bool attr = false;
         if (!attr) {
@@ -259,11 +264,11 @@ void run_plan(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_t *d
         }
         k_plan_mid<<<(unsigned)std::min<int64_t>(nm, 148 * 2 * 8), MID_BLOCK, sm, s>>>(A, G.bin_rows.p + G.bin_off[1], nm);
     }
-    if (nl && (bin_mask & 4)) {
+    if (nl && (bin_mask & 48)) {
         ctx->hash_keys.resize(G.large_hash_total);
         ctx->hash_vals.resize(G.large_hash_total);
         k_plan_large<<<(unsigned)std::min<int64_t>(nl, 148 * 2), LARGE_BLOCK, 0, s>>>(
-            A, G.bin_rows.p + G.bin_off[2], nl, G.large_hoff.p, ctx->hash_keys.p, ctx->hash_vals.p);
+            A, G.bin_rows.p + G.bin_off[4], nl, G.large_hoff.p, ctx->hash_keys.p, ctx->hash_vals.p);
     }
     CUDA_TRY(cudaGetLastError());
 }

@@ -1,0 +1,779 @@
+// slm_sweep.cu -- the local-move plan sweep (_best_targets, detector.py:367-418), fast path
+// for integer weights.
+//
+// Exactness.  When every weight is an integer and every row's total stays below 2^32 (level
+// 0 of all BASELINE configs), u = w_out + w_in is stored as uint32 and each (node,
+// community) group sum is accumulated in uint32 -- exact, so any accumulation order
+// reproduces the reference's fp64 sums bit for bit.  The reference then evaluates
+//     t_c = fl( fl(gsum / m) - fl(P_c / m2) ),  P_c = fl(fl(s_out*S_in') + fl(s_in*S_out'))
+// for every group and takes the lowest c attaining max t_c.  Here every group is first
+// scored with reciprocal multiplies, t~_c = gsum*(1/m) - P_c*(1/m2), which is within
+// err_c = 2^-48 (|gsum/m| + |P_c/m2|) of t_c (a few ulps; the bound is generous).  A group
+// can only be the exact argmax if t~_c + err_c >= max_c' (t~_c' - err_c'); when a single
+// group passes that test (the common case) only it is evaluated with the reference's two
+// IEEE divisions, otherwise every passing group is.  The staying score is always exact.
+// The decisions are therefore bit-identical to the reference's while the division work
+// drops from two per group to a handful per row.
+//
+// Memory.  Symmetric graphs (W == W^T, all BASELINE configs) have s_in == s_out and
+// S_in == S_out bitwise, so one fp64 per node / community is gathered (8 B, a quarter of
+// the random-gather footprint of separate S_out / S_in); adjacency streams are loaded with
+// evict-first hints so they do not push labels and S out of L2.
+//
+// Degree bins (slm_internal.cuh bin_hi):
+//   0: d <= 32      rows packed into warps (lanes = entries of several rows),
+//                   __match_any_sync on (row, community) + __reduce_add_sync group sums,
+//                   segmented argmax by shuffles
+//   1: d <= 256     warp per row, per-warp shared hash (512 slots) + occupied-slot list
+//   2: d <= 1024    warp per row, per-warp shared hash (2048 slots) + occupied-slot list
+//   3: d <= 4096    CTA per row, shared hash (8192 slots) + occupied-slot list
+//   4, 5: larger    (row, segment) CTAs insert into per-row global tables, then one CTA
+//                   per row walks the row's occupied list
+#include "slm_internal.cuh"
+
+constexpr double ERR_REL = 0x1.0p-48;
+
+template <bool SYM>
+struct SweepArgs {
+    const int64_t *uptr;
+    const int32_t *unbr;
+    const uint32_t *u32;
+    const int32_t *label;
+    const double *S1;      // SYM: S per community
+    const double2 *S2;     // !SYM: {S_out, S_in} per community
+    const float *S1f;      // SYM: float(S) for the approximate pass (half the gather bytes)
+    const float2 *S2f;     // !SYM: float {S_out, S_in}
+    const double *s1;      // SYM: s per node
+    const double2 *s2;     // !SYM: {s_out, s_in} per node
+    double m, m2, inv_m, inv_m2;
+    int32_t *cstar;
+    unsigned long long *groups;
+};
+
+// per-node and per-community strength views
+template <bool SYM>
+__device__ __forceinline__ double2 node_s(const SweepArgs<SYM> &A, int32_t r) {
+    if (SYM) {
+        const double v = A.s1[r];
+        return make_double2(v, v);
+    }
+    return A.s2[r];
+}
+template <bool SYM>
+__device__ __forceinline__ double2 comm_S(const SweepArgs<SYM> &A, int32_t c) {
+    if (SYM) {
+        const double v = A.S1[c];
+        return make_double2(v, v);
+    }
+    return A.S2[c];
+}
+
+template <bool SYM>
+__device__ __forceinline__ double2 comm_Sf(const SweepArgs<SYM> &A, int32_t c) {
+    if (SYM) {
+        const double v = (double)A.S1f[c];
+        return make_double2(v, v);
+    }
+    const float2 f = A.S2f[c];
+    return make_double2((double)f.x, (double)f.y);
+}
+
+// P_c of detector.py:400-402 (S.x = S_out, S.y = S_in; sr.x = s_out, sr.y = s_in)
+__device__ __forceinline__ double null_P(bool own, double2 sr, double2 Sc) {
+    const double so = sr.x, si = sr.y;
+    const double sin_c = Sc.y - (own ? si : 0.0);
+    const double sout_c = Sc.x - (own ? so : 0.0);
+    return so * sin_c + si * sout_c;
+}
+__device__ __forceinline__ double exact_t(uint32_t g, double P, double m, double m2) {
+    return (double)g / m - P / m2;
+}
+// staying score without a neighbour in the own community (detector.py:377-378)
+__device__ __forceinline__ double stay_default(double2 sr, double2 SL, double m2) {
+    const double so = sr.x, si = sr.y;
+    return -(so * (SL.y - si) + si * (SL.x - so)) / m2;
+}
+
+// Running selection state of one thread / warp / CTA over the non-own groups.
+struct Sel {
+    double up1;    // largest upper bound and its group
+    int32_t c1;
+    uint32_t g1;
+    double P1;
+    double up2;    // second largest upper bound (any other group)
+    double lo;     // largest lower bound
+    // own group
+    uint32_t gown;
+    double Pown;
+    int hown;
+};
+__device__ __forceinline__ void sel_init(Sel &S) {
+    S.up1 = -INFINITY;
+    S.c1 = 0x7fffffff;
+    S.g1 = 0;
+    S.P1 = 0.0;
+    S.up2 = -INFINITY;
+    S.lo = -INFINITY;
+    S.gown = 0;
+    S.Pown = 0.0;
+    S.hown = 0;
+}
+// P is computed from float(S) (relative error <= 2^-24 on a non-own group, where no
+// cancellation occurs), hence the extra 2^-23 |b| in the bound.
+__device__ __forceinline__ void sel_add(Sel &S, int32_t c, uint32_t g, double P, bool own,
+                                        double inv_m, double inv_m2) {
+    if (own) {           // the own group is always evaluated exactly (P recomputed in fp64)
+        S.gown = g;
+        S.hown = 1;
+        return;
+    }
+    const double a = (double)g * inv_m, b = P * inv_m2;
+    const double t = a - b;
+    const double e = ERR_REL * (fabs(a) + fabs(b)) + 0x1.0p-23 * fabs(b) + 1e-300;
+    const double up = t + e, lo = t - e;
+    if (lo > S.lo) S.lo = lo;
+    if (up > S.up1 || (up == S.up1 && c < S.c1)) {
+        S.up2 = fmax(S.up2, S.up1);
+        S.up1 = up;
+        S.c1 = c;
+        S.g1 = g;
+        S.P1 = P;
+    } else {
+        S.up2 = fmax(S.up2, up);
+    }
+}
+__device__ __forceinline__ void sel_merge(Sel &S, const Sel &O) {
+    if (O.up1 > S.up1 || (O.up1 == S.up1 && O.c1 < S.c1)) {
+        S.up2 = fmax(fmax(S.up2, O.up2), S.up1);
+        S.up1 = O.up1;
+        S.c1 = O.c1;
+        S.g1 = O.g1;
+        S.P1 = O.P1;
+    } else {
+        S.up2 = fmax(fmax(S.up2, O.up2), O.up1);
+    }
+    S.lo = fmax(S.lo, O.lo);
+    if (O.hown) {
+        S.gown = O.gown;
+        S.Pown = O.Pown;
+        S.hown = 1;
+    }
+}
+__device__ __forceinline__ Sel sel_shfl_xor(const Sel &S, int off) {
+    Sel O;
+    O.up1 = __shfl_xor_sync(0xffffffffu, S.up1, off);
+    O.c1 = __shfl_xor_sync(0xffffffffu, S.c1, off);
+    O.g1 = __shfl_xor_sync(0xffffffffu, S.g1, off);
+    O.P1 = __shfl_xor_sync(0xffffffffu, S.P1, off);
+    O.up2 = __shfl_xor_sync(0xffffffffu, S.up2, off);
+    O.lo = __shfl_xor_sync(0xffffffffu, S.lo, off);
+    O.gown = __shfl_xor_sync(0xffffffffu, S.gown, off);
+    O.Pown = __shfl_xor_sync(0xffffffffu, S.Pown, off);
+    O.hown = __shfl_xor_sync(0xffffffffu, S.hown, off);
+    return O;
+}
+__device__ __forceinline__ void sel_warp(Sel &S) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sel_merge(S, sel_shfl_xor(S, off));
+}
+// unique candidate?  (else the exact fallback must scan every group with up >= lo)
+__device__ __forceinline__ bool sel_unique(const Sel &S) { return S.up2 < S.lo; }
+
+// final decision given the exact best (tb, cb) (cb == INT_MAX: no other community)
+template <bool SYM>
+__device__ __forceinline__ int32_t decide(const SweepArgs<SYM> &A, const Sel &S, double tb,
+                                          int32_t cb, double2 sr, int32_t L) {
+    if (cb == 0x7fffffff) return L;
+    const double2 SL = comm_S(A, L);
+    const double t_stay = S.hown ? exact_t(S.gown, null_P(true, sr, SL), A.m, A.m2)
+                                 : stay_default(sr, SL, A.m2);
+    return tb > t_stay ? cb : L;
+}
+// exact t of the unique approximate winner (fp64 S gathered once)
+template <bool SYM>
+__device__ __forceinline__ double winner_t(const SweepArgs<SYM> &A, const Sel &S, double2 sr) {
+    return exact_t(S.g1, null_P(false, sr, comm_S(A, S.c1)), A.m, A.m2);
+}
+
+__device__ __forceinline__ bool better2(double t1, int32_t c1, double t2, int32_t c2) {
+    return t1 > t2 || (t1 == t2 && c1 < c2);
+}
+
+__device__ __forceinline__ int32_t ld_stream_i32(const int32_t *p) { return __ldcs(p); }
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t *p) { return __ldcs(p); }
+
+// ------------------------------------------------------------------- bin 0
+
+template <bool SYM>
+__global__ void __launch_bounds__(256) k_sweep_small(SweepArgs<SYM> A, const int32_t *rows,
+                                                      int64_t nrows, int64_t rows_per_warp) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t base = w * rows_per_warp; base < nrows; base += nw * rows_per_warp) {
+        const int64_t rend = min(base + rows_per_warp, nrows);
+        int64_t rcur = base;
+        while (rcur < rend) {
+            // lane j describes row rcur + j
+            const int64_t j = rcur + lane;
+            int32_t r = 0, L = 0;
+            int64_t e0 = 0;
+            int deg = 0;
+            if (j < rend) {
+                r = rows[j];
+                e0 = A.uptr[r];
+                deg = (int)(A.uptr[r + 1] - e0);
+                L = A.label[r];
+            }
+            int inc = deg;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                int v = __shfl_up_sync(0xffffffffu, inc, off);
+                if (lane >= off) inc += v;
+            }
+            const unsigned fit = __ballot_sync(0xffffffffu, j < rend && inc <= 32);
+            const int k = __popc(fit);
+            const int start = inc - deg;
+            const int total = __shfl_sync(0xffffffffu, inc, k - 1);
+            // entry lane -> row slot: largest s < k with start_s <= lane
+            int s = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                int cand = s + step;
+                int st = __shfl_sync(0xffffffffu, start, cand & 31);
+                if (cand < k && st <= lane) s = cand;
+            }
+            const bool valid = lane < total;
+            const int32_t rr = __shfl_sync(0xffffffffu, r, s);
+            const int64_t re0 = __shfl_sync(0xffffffffu, e0, s);
+            const int rst = __shfl_sync(0xffffffffu, start, s);
+            const int32_t Lr = __shfl_sync(0xffffffffu, L, s);
+            int32_t c = -1;
+            uint32_t wt = 0;
+            if (valid) {
+                const int64_t e = re0 + (lane - rst);
+                c = A.label[ld_stream_i32(A.unbr + e)];
+                wt = ld_stream_u32(A.u32 + e);
+            }
+            const unsigned long long key =
+                valid ? (((unsigned long long)s << 32) | (uint32_t)c) : ~0ull;
+            const unsigned gm = __match_any_sync(0xffffffffu, key);
+            // group sums by a uniform shuffle loop (a REDUX with per-group masks would be
+            // serialised per group)
+            uint32_t gs = 0;
+            for (int q = 0; q < total; q++) {
+                const uint32_t v = __shfl_sync(0xffffffffu, wt, q);
+                if ((gm >> q) & 1u) gs += v;
+            }
+            const bool leader = valid && lane == __ffs(gm) - 1;
+            if (A.groups) {
+                unsigned lm = __ballot_sync(0xffffffffu, leader);
+                if (lane == 0 && lm) atomicAdd(A.groups, (unsigned long long)__popc(lm));
+            }
+            const bool own = (c == Lr);
+            double bt = -INFINITY, ts = -INFINITY;
+            int32_t bc = 0x7fffffff;
+            int hs = 0;
+            if (leader) {
+                const double2 srr = node_s(A, rr);
+                const double t = exact_t(gs, null_P(own, srr, comm_S(A, c)), A.m, A.m2);
+                if (own) {
+                    ts = t;
+                    hs = 1;
+                } else {
+                    bt = t;
+                    bc = c;
+                }
+            }
+            // segmented inclusive scan over the lanes of one row
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const double obt = __shfl_up_sync(0xffffffffu, bt, off);
+                const int32_t obc = __shfl_up_sync(0xffffffffu, bc, off);
+                const double ots = __shfl_up_sync(0xffffffffu, ts, off);
+                const int ohs = __shfl_up_sync(0xffffffffu, hs, off);
+                const int os = __shfl_up_sync(0xffffffffu, s, off);
+                if (lane >= off && os == s) {
+                    if (better2(obt, obc, bt, bc)) {
+                        bt = obt;
+                        bc = obc;
+                    }
+                    if (ohs) {
+                        ts = ots;
+                        hs = 1;
+                    }
+                }
+            }
+            const int nxt = __shfl_down_sync(0xffffffffu, s, 1);
+            const bool last = valid && (lane == total - 1 || nxt != s);
+            if (last) {
+                const double t_stay =
+                    hs ? ts : stay_default(node_s(A, rr), comm_S(A, Lr), A.m2);
+                A.cstar[rr] = (bc != 0x7fffffff && bt > t_stay) ? bc : Lr;
+            }
+            rcur += k;
+        }
+    }
+}
+
+// -------------------------------------------------------------- hash tables
+
+__device__ __forceinline__ uint32_t hslot32(int32_t c, uint32_t hmask) {
+    return ((uint32_t)c * 2654435761u) & hmask;
+}
+
+// claim (CAS) the entry's community slot and add its weight; lanes that hit the same
+// slot in one instruction are serialised by the shared-memory atomic unit (cheaper than a
+// warp-level pre-combine, whose per-group REDUX masks compile to a serial loop).  Newly
+// claimed slots are appended to the occupied list.
+template <class IDX>
+__device__ __forceinline__ void hash_insert_warp(int32_t *hk, uint32_t *hv, uint32_t hmask,
+                                                 IDX *occ, uint32_t *nocc, bool valid, int32_t c,
+                                                 uint32_t wt) {
+    const int lane = threadIdx.x & 31;
+    bool fresh = false;
+    uint32_t sl = 0;
+    if (valid) {
+        sl = hslot32(c, hmask);
+        for (;;) {
+            int32_t prev = atomicCAS(&hk[sl], -1, c);
+            if (prev == -1 || prev == c) {
+                fresh = (prev == -1);
+                break;
+            }
+            sl = (sl + 1) & hmask;
+        }
+        atomicAdd(&hv[sl], wt);
+    }
+    const unsigned fm = __ballot_sync(0xffffffffu, fresh);
+    if (fm) {
+        uint32_t base = 0;
+        if (lane == __ffs(fm) - 1) base = atomicAdd(nocc, (uint32_t)__popc(fm));
+        base = __shfl_sync(0xffffffffu, base, __ffs(fm) - 1);
+        if (fresh) occ[base + __popc(fm & ((1u << lane) - 1))] = (IDX)sl;
+    }
+}
+
+// walk the occupied slots [lo, hi) of a table: approximate selection (+ own group)
+template <bool SYM, class IDX>
+__device__ __forceinline__ void occ_scan(const SweepArgs<SYM> &A, const int32_t *hk,
+                                         const uint32_t *hv, const IDX *occ, uint32_t lo,
+                                         uint32_t hi, uint32_t stride, int32_t L, double2 sr,
+                                         Sel &S) {
+    constexpr int U = 4;
+    for (uint32_t k0 = lo; k0 < hi; k0 += stride * U) {
+        int32_t c[U];
+        uint32_t g[U];
+        double2 Sc[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const uint32_t k = k0 + u * stride;
+            c[u] = -1;
+            g[u] = 0;
+            if (k < hi) {
+                const uint32_t sl = occ[k];
+                c[u] = hk[sl];
+                g[u] = hv[sl];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++)
+            if (c[u] >= 0 && c[u] != L) Sc[u] = comm_Sf(A, c[u]);
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            if (c[u] < 0) continue;
+            const bool own = (c[u] == L);
+            sel_add(S, c[u], g[u], own ? 0.0 : null_P(false, sr, Sc[u]), own, A.inv_m, A.inv_m2);
+        }
+    }
+}
+
+// exact fallback: best (t, c) over groups whose upper bound reaches lo
+template <bool SYM, class IDX>
+__device__ __forceinline__ void occ_exact(const SweepArgs<SYM> &A, const int32_t *hk,
+                                          const uint32_t *hv, const IDX *occ, uint32_t lo,
+                                          uint32_t hi, uint32_t stride, int32_t L, double2 sr,
+                                          double lob, double &bt, int32_t &bc) {
+    for (uint32_t k = lo; k < hi; k += stride) {
+        const uint32_t sl = occ[k];
+        const int32_t c = hk[sl];
+        if (c == L) continue;
+        const uint32_t g = hv[sl];
+        const double Pf = null_P(false, sr, comm_Sf(A, c));
+        const double a = (double)g * A.inv_m, b = Pf * A.inv_m2;
+        const double up = (a - b) + (ERR_REL * (fabs(a) + fabs(b)) + 0x1.0p-23 * fabs(b) + 1e-300);
+        if (up < lob) continue;
+        const double t = exact_t(g, null_P(false, sr, comm_S(A, c)), A.m, A.m2);
+        if (better2(t, c, bt, bc)) {
+            bt = t;
+            bc = c;
+        }
+    }
+}
+
+// clear the occupied slots [lo, hi)
+template <class IDX>
+__device__ __forceinline__ void occ_clear(int32_t *hk, uint32_t *hv, const IDX *occ, uint32_t lo,
+                                          uint32_t hi, uint32_t stride) {
+    for (uint32_t k = lo; k < hi; k += stride) {
+        const uint32_t sl = occ[k];
+        hk[sl] = -1;
+        hv[sl] = 0;
+    }
+}
+
+// stride-`stride` unrolled load of entries of a row: neighbour labels + weights
+template <int U, bool SYM>
+__device__ __forceinline__ void load_entries(const SweepArgs<SYM> &A, int64_t e0, int64_t d,
+                                             int64_t base, int64_t stride, int32_t (&c)[U],
+                                             uint32_t (&w)[U], bool (&v)[U]) {
+    int32_t z[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        const int64_t idx = base + u * stride;
+        v[u] = idx < d;
+        z[u] = 0;
+        w[u] = 0;
+        if (v[u]) {
+            z[u] = ld_stream_i32(A.unbr + e0 + idx);
+            w[u] = ld_stream_u32(A.u32 + e0 + idx);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) c[u] = v[u] ? A.label[z[u]] : -1;
+}
+
+__device__ __forceinline__ uint32_t table_size(int64_t d) {
+    uint32_t H = 32;
+    while (H <= (uint32_t)d) H <<= 1;   // H > d >= distinct communities
+    return H;
+}
+
+// bins 1, 2: one warp per row, per-warp table of HMAX slots + occupied list (dynamic smem)
+template <int HMAX, int WARPS, bool SYM>
+__global__ void __launch_bounds__(WARPS * 32) k_sweep_warp(SweepArgs<SYM> A, const int32_t *rows,
+                                                            int64_t nrows) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint32_t s_nocc[WARPS];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int32_t *hk = (int32_t *)smem + wid * HMAX;
+    uint32_t *hv = (uint32_t *)((int32_t *)smem + WARPS * HMAX) + wid * HMAX;
+    uint16_t *occ = (uint16_t *)((int32_t *)smem + 2 * WARPS * HMAX) + wid * HMAX;
+    uint32_t *nocc = &s_nocc[wid];
+    for (int k = lane; k < HMAX; k += 32) {
+        hk[k] = -1;
+        hv[k] = 0;
+    }
+    if (lane == 0) *nocc = 0;
+    __syncwarp();
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = w; i < nrows; i += nw) {
+        const int32_t r = rows[i];
+        const int64_t e0 = A.uptr[r], d = A.uptr[r + 1] - e0;
+        const uint32_t hmask = table_size(d) - 1;
+        const int32_t L = A.label[r];
+        const double2 sr = node_s(A, r);
+        constexpr int U = 4;
+        for (int64_t cb = 0; cb < d; cb += 32 * U) {
+            int32_t c[U];
+            uint32_t wt[U];
+            bool v[U];
+            load_entries<U>(A, e0, d, cb + lane, 32, c, wt, v);
+#pragma unroll
+            for (int u = 0; u < U; u++) hash_insert_warp(hk, hv, hmask, occ, nocc, v[u], c[u], wt[u]);
+        }
+        __syncwarp();
+        const uint32_t no = *nocc;
+        Sel S;
+        sel_init(S);
+        occ_scan(A, hk, hv, occ, lane, no, 32, L, sr, S);
+        sel_warp(S);
+        double bt = -INFINITY;
+        int32_t bc = 0x7fffffff;
+        if (S.c1 != 0x7fffffff) {
+            if (sel_unique(S)) {
+                bt = winner_t(A, S, sr);
+                bc = S.c1;
+            } else {
+                occ_exact(A, hk, hv, occ, lane, no, 32, L, sr, S.lo, bt, bc);
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    const double obt = __shfl_xor_sync(0xffffffffu, bt, off);
+                    const int32_t obc = __shfl_xor_sync(0xffffffffu, bc, off);
+                    if (better2(obt, obc, bt, bc)) {
+                        bt = obt;
+                        bc = obc;
+                    }
+                }
+            }
+        }
+        if (A.groups && lane == 0) atomicAdd(A.groups, (unsigned long long)no);
+        if (lane == 0) A.cstar[r] = decide(A, S, bt, bc, sr, L);
+        occ_clear(hk, hv, occ, lane, no, 32);
+        __syncwarp();
+        if (lane == 0) *nocc = 0;
+        __syncwarp();
+    }
+}
+
+// block-wide selection reduce (warp then shared)
+template <int BLOCK>
+__device__ __forceinline__ void sel_block(Sel &S, Sel *sh) {
+    sel_warp(S);
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) sh[wid] = S;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int q = 1; q < BLOCK / 32; q++) sel_merge(S, sh[q]);
+        sh[0] = S;
+    }
+    __syncthreads();
+    S = sh[0];
+    __syncthreads();
+}
+
+template <int BLOCK>
+__device__ __forceinline__ void best_block(double &bt, int32_t &bc, double *sbt, int32_t *sbc) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double obt = __shfl_xor_sync(0xffffffffu, bt, off);
+        const int32_t obc = __shfl_xor_sync(0xffffffffu, bc, off);
+        if (better2(obt, obc, bt, bc)) {
+            bt = obt;
+            bc = obc;
+        }
+    }
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        sbt[wid] = bt;
+        sbc[wid] = bc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int q = 0; q < BLOCK / 32; q++)
+            if (better2(sbt[q], sbc[q], bt, bc)) {
+                bt = sbt[q];
+                bc = sbc[q];
+            }
+    __syncthreads();
+}
+
+// bin 3 (shared table of HMAX slots) and bins 4, 5 (global tables, GLOBAL): one CTA per row
+// scans the occupied list; the shared variant also inserts
+template <int BLOCK, int HMAX, bool GLOBAL, bool SYM>
+__global__ void __launch_bounds__(BLOCK) k_sweep_cta(SweepArgs<SYM> A, const int32_t *rows,
+                                                      int64_t nrows, const int64_t *hoff,
+                                                      int32_t *gk, uint32_t *gv, uint32_t *gocc,
+                                                      uint32_t *gnocc) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ Sel sh[BLOCK / 32];
+    __shared__ double sbt[BLOCK / 32];
+    __shared__ int32_t sbc[BLOCK / 32];
+    __shared__ uint32_t s_nocc;
+    int32_t *hk = (int32_t *)smem;
+    uint32_t *hv = (uint32_t *)(hk + HMAX);
+    uint16_t *socc = (uint16_t *)(hv + HMAX);
+    if (!GLOBAL) {
+        for (int k = threadIdx.x; k < HMAX; k += BLOCK) {
+            hk[k] = -1;
+            hv[k] = 0;
+        }
+        if (threadIdx.x == 0) s_nocc = 0;
+        __syncthreads();
+    }
+    for (int64_t i = blockIdx.x; i < nrows; i += gridDim.x) {
+        const int32_t r = rows[i];
+        const int64_t e0 = A.uptr[r], d = A.uptr[r + 1] - e0;
+        const int32_t L = A.label[r];
+        const double2 sr = node_s(A, r);
+        int32_t *tk = hk;
+        uint32_t *tv = hv;
+        uint32_t no;
+        if (GLOBAL) {
+            tk = gk + hoff[i];
+            tv = gv + hoff[i];
+            no = gnocc[i];
+        } else {
+            const uint32_t hmask = table_size(d) - 1;
+            constexpr int U = 4;
+            for (int64_t cb = 0; cb < d; cb += BLOCK * U) {
+                int32_t c[U];
+                uint32_t wt[U];
+                bool v[U];
+                load_entries<U>(A, e0, d, cb + threadIdx.x, BLOCK, c, wt, v);
+#pragma unroll
+                for (int u = 0; u < U; u++)
+                    hash_insert_warp(tk, tv, hmask, socc, &s_nocc, v[u], c[u], wt[u]);
+            }
+            __syncthreads();
+            no = s_nocc;
+        }
+        Sel S;
+        sel_init(S);
+        if (GLOBAL) occ_scan(A, tk, tv, gocc + hoff[i], threadIdx.x, no, BLOCK, L, sr, S);
+        else occ_scan(A, tk, tv, socc, threadIdx.x, no, BLOCK, L, sr, S);
+        sel_block<BLOCK>(S, sh);
+        double bt = -INFINITY;
+        int32_t bc = 0x7fffffff;
+        if (S.c1 != 0x7fffffff) {
+            if (sel_unique(S)) {
+                bt = winner_t(A, S, sr);
+                bc = S.c1;
+            } else {
+                if (GLOBAL)
+                    occ_exact(A, tk, tv, gocc + hoff[i], threadIdx.x, no, BLOCK, L, sr, S.lo, bt, bc);
+                else
+                    occ_exact(A, tk, tv, socc, threadIdx.x, no, BLOCK, L, sr, S.lo, bt, bc);
+                best_block<BLOCK>(bt, bc, sbt, sbc);
+            }
+        }
+        if (threadIdx.x == 0) {
+            if (A.groups) atomicAdd(A.groups, (unsigned long long)no);
+            A.cstar[r] = decide(A, S, bt, bc, sr, L);
+        }
+        if (GLOBAL) {
+            occ_clear(tk, tv, gocc + hoff[i], threadIdx.x, no, BLOCK);
+            if (threadIdx.x == 0) gnocc[i] = 0;
+        } else {
+            occ_clear(tk, tv, socc, threadIdx.x, no, BLOCK);
+            __syncthreads();
+            if (threadIdx.x == 0) s_nocc = 0;
+        }
+        __syncthreads();
+    }
+}
+
+// bins 4, 5 insert phase: one CTA per (row, segment of HUB_SEG entries), global tables
+constexpr int HUB_SEG = 8192;
+template <bool SYM>
+__global__ void __launch_bounds__(256) k_sweep_hub_insert(SweepArgs<SYM> A, const int32_t *rows,
+                                                          const int64_t *seg_row, int64_t nseg,
+                                                          const int64_t *hoff, int32_t *gk,
+                                                          uint32_t *gv, uint32_t *gocc,
+                                                          uint32_t *gnocc) {
+    // hoff here is already rebased onto the wave's table window (gk/gv/gocc)
+    constexpr int U = 8;
+    for (int64_t q = blockIdx.x; q < nseg; q += gridDim.x) {
+        const int64_t i = seg_row[q] >> 20, sgi = seg_row[q] & 0xFFFFF;
+        const int32_t r = rows[i];
+        const int64_t e0 = A.uptr[r], d = A.uptr[r + 1] - e0;
+        const uint32_t hmask = (uint32_t)(hoff[i + 1] - hoff[i]) - 1;
+        int32_t *tk = gk + hoff[i];
+        uint32_t *tv = gv + hoff[i];
+        uint32_t *to = gocc + hoff[i];
+        const int64_t lo = sgi * HUB_SEG, hi = min(d, lo + HUB_SEG);
+        for (int64_t cb = lo; cb < hi; cb += 256 * U) {
+            int32_t c[U];
+            uint32_t wt[U];
+            bool v[U];
+            load_entries<U>(A, e0, hi, cb + threadIdx.x, 256, c, wt, v);
+#pragma unroll
+            for (int u = 0; u < U; u++) hash_insert_warp(tk, tv, hmask, to, &gnocc[i], v[u], c[u], wt[u]);
+        }
+    }
+}
+
+__global__ void k_copy_labels32(const int32_t *label, int64_t n, int32_t *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = label[i];
+}
+
+template <class K>
+static void set_smem(K kern, size_t bytes) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+constexpr size_t warp_smem(int hmax, int warps) { return (size_t)warps * hmax * 10; }
+
+template <bool SYM>
+static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_t *d_cstar,
+                         int bin_mask, unsigned long long *d_groups) {
+    cudaStream_t s = ctx->stream;
+    SweepArgs<SYM> A;
+    A.uptr = G.uptr.p;
+    A.unbr = G.unbr.p;
+    A.u32 = G.uu32.p;
+    A.label = F.comm.p;
+    A.S1 = F.S_out.p;
+    A.S2 = F.S2.p;
+    A.S1f = F.S1f.p;
+    A.S2f = F.S2f.p;
+    A.s1 = G.s_out.p;
+    A.s2 = G.s2.p;
+    A.m = m;
+    A.m2 = m * m;
+    A.inv_m = 1.0 / m;
+    A.inv_m2 = 1.0 / (m * m);
+    A.cstar = d_cstar;
+    A.groups = d_groups;
+    auto nb = [&](int b) { return G.bin_off[b + 1] - G.bin_off[b]; };
+    auto rows = [&](int b) { return G.bin_rows.p + G.bin_off[b]; };
+    static bool attrs[2] = {false, false};
+    if (!attrs[SYM]) {
+        set_smem(k_sweep_warp<512, 8, SYM>, warp_smem(512, 8));
+        set_smem(k_sweep_cta<128, 2048, false, SYM>, (size_t)2048 * 10);
+        set_smem(k_sweep_cta<512, 8192, false, SYM>, (size_t)8192 * 10);
+        set_smem(k_sweep_cta<1024, 16384, false, SYM>, (size_t)16384 * 10);
+        attrs[SYM] = true;
+    }
+    if (nb(0) && (bin_mask & 1)) {
+        const int64_t warps = 148LL * 64;
+        int64_t rpw = std::max<int64_t>(64, (nb(0) + warps - 1) / warps);
+        int64_t nw = (nb(0) + rpw - 1) / rpw;
+        k_sweep_small<SYM><<<grid_for(nw * 32, 256), 256, 0, s>>>(A, rows(0), nb(0), rpw);
+    }
+    if (nb(1) && (bin_mask & 2))
+        k_sweep_warp<512, 8, SYM><<<grid_for(nb(1) * 32, 256, 148LL * 5), 256,
+                                    warp_smem(512, 8), s>>>(A, rows(1), nb(1));
+    if (nb(2) && (bin_mask & 4))
+        k_sweep_cta<128, 2048, false, SYM><<<(unsigned)std::min<int64_t>(nb(2), 148 * 11), 128,
+                                             (size_t)2048 * 10, s>>>(
+            A, rows(2), nb(2), nullptr, nullptr, nullptr, nullptr, nullptr);
+    if (nb(3) && (bin_mask & 8))
+        k_sweep_cta<512, 8192, false, SYM><<<(unsigned)std::min<int64_t>(nb(3), 148 * 2), 512,
+                                             (size_t)8192 * 10, s>>>(
+            A, rows(3), nb(3), nullptr, nullptr, nullptr, nullptr, nullptr);
+    if (nb(4) && (bin_mask & 16))
+        k_sweep_cta<1024, 16384, false, SYM><<<(unsigned)std::min<int64_t>(nb(4), 148), 1024,
+                                               (size_t)16384 * 10, s>>>(
+            A, rows(4), nb(4), nullptr, nullptr, nullptr, nullptr, nullptr);
+    if (nb(5) && (bin_mask & 32)) {
+        // hub rows: global tables processed in waves whose tables fit in L2
+        const int64_t tot = G.hub_wave_slots;
+        if (ctx->hk32.n < (size_t)tot) {
+            ctx->hk32.resize(tot);
+            ctx->hv32.resize(tot);
+            ctx->hocc32.resize(tot);
+            // tables are left empty by every scan, so clearing once per allocation suffices
+            CUDA_TRY(cudaMemsetAsync(ctx->hk32.p, 0xff, tot * 4, s));
+            CUDA_TRY(cudaMemsetAsync(ctx->hv32.p, 0, tot * 4, s));
+        }
+        if (ctx->hnocc32.n < (size_t)nb(5)) {
+            ctx->hnocc32.resize(nb(5));
+            CUDA_TRY(cudaMemsetAsync(ctx->hnocc32.p, 0, nb(5) * 4, s));
+        }
+        const int64_t *hoff5 = G.large_hoff.p + nb(4);
+        for (size_t wv = 0; wv + 1 < G.hub_waves.size(); wv++) {
+            const HubWave &W0 = G.hub_waves[wv], &W1 = G.hub_waves[wv + 1];
+            const int64_t nr = W1.row - W0.row, ns = W1.seg - W0.seg;
+            int32_t *gk = ctx->hk32.p - W0.base;
+            uint32_t *gv = ctx->hv32.p - W0.base, *go = ctx->hocc32.p - W0.base;
+            // segment items carry bin-5 row indices
+            k_sweep_hub_insert<SYM><<<(unsigned)std::min<int64_t>(ns, 148 * 8), 256, 0, s>>>(
+                A, rows(5), G.hub_seg.p + W0.seg, ns, hoff5, gk, gv, go, ctx->hnocc32.p);
+            k_sweep_cta<1024, 1, true, SYM><<<(unsigned)std::min<int64_t>(nr, 148), 1024, 16, s>>>(
+                A, rows(5) + W0.row, nr, hoff5 + W0.row, gk, gv, go, ctx->hnocc32.p + W0.row);
+        }
+    }
+    CUDA_TRY(cudaGetLastError());
+}
+
+void run_plan_u32(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_t *d_cstar,
+                  int bin_mask, unsigned long long *d_groups) {
+    if (bin_mask & 64)
+        k_copy_labels32<<<grid_for(G.n, 256), 256, 0, ctx->stream>>>(F.comm.p, G.n, d_cstar);
+    if (G.sym) launch_sweep<true>(ctx, G, F, m, d_cstar, bin_mask, d_groups);
+    else launch_sweep<false>(ctx, G, F, m, d_cstar, bin_mask, d_groups);
+}

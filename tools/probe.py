@@ -54,7 +54,7 @@ def main():
     t = time.perf_counter(); r = ctx.positive(cfg); print("positive_s", time.perf_counter() - t, r[:3])
     g, rows, ents = ctx.plan_groups()
     print("G", g, "G/E", g / info["ue"], "bin rows", rows.tolist(), "bin entries", ents.tolist())
-    for mask, name in ((15, "sweep"), (1, "small"), (2, "mid"), (4, "large"), (8, "copy")):
+    for mask, name in ((127, "sweep"), (1, "b0"), (2, "b1"), (4, "b2"), (8, "b3"), (16, "b4"), (32, "b5"), (64, "copy")):
         ms = ev_time(ctx, lambda: ctx.plan_async(mask))
         print(f"plan[{name}] ms {ms:.3f}  GTEPS(full E) {info['ue'] / ms / 1e6:.1f}")
     t = time.perf_counter(); imp, app, _ = ctx.maximal(cfg, 0, 0); el = time.perf_counter() - t
