@@ -66,6 +66,7 @@ SIGNATURES = {
     "slm_plan_sweep_async": (C.c_int, [_VP, C.c_int32]),
     "slm_plan_groups": (C.c_int, [_VP, _PI64, _VP, _VP]),
     "slm_get_cstar": (C.c_int, [_VP, _VP]),
+    "slm_debug_sweep_floor": (C.c_int, [_VP, C.c_int32, _PD]),
     "slm_gen_rmat_host": (C.c_int, [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                     C.c_uint64, C.c_int, _VP, _VP, _VP, _PI64]),
     "slm_gen_rgg_host": (C.c_int, [_I64, C.c_double, C.c_uint64, _VP, _VP, _VP, _PI64]),
@@ -295,6 +296,11 @@ class Context:
         cstar = np.empty(self.info()["n"], np.int64)
         self.call("slm_get_cstar", ptr(cstar))
         return cstar
+
+    def sweep_floor(self, mode):
+        ms = C.c_double()
+        self.call("slm_debug_sweep_floor", int(mode), C.byref(ms))
+        return ms.value
 
     def sync(self):
         self.call("slm_sync")

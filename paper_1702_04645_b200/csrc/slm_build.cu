@@ -357,7 +357,7 @@ static void build_bins(slm_ctx *ctx, LevelGraph &G) {
         // hub rows (bin 5): (row << 20 | segment) items of 8192 entries, grouped in waves
         // whose tables (12 B per slot) fit in ~48 MB of L2
         const int64_t nb4 = G.bin_off[5] - G.bin_off[4];
-        const int64_t budget = 4 << 20;   // slots per wave
+        const int64_t budget = 6 << 20;   // slots per wave (72 MB of tables)
         std::vector<int64_t> segs;
         G.hub_waves.clear();
         G.hub_wave_slots = 0;
@@ -372,7 +372,7 @@ static void build_bins(slm_ctx *ctx, LevelGraph &G) {
             }
             wslots += H;
             int64_t d = up[rows[b0 + i] + 1] - up[rows[b0 + i]];
-            for (int64_t q = 0; q * 8192 < d; q++) segs.push_back(((i - nb4) << 20) | q);
+            for (int64_t q = 0; q * 4096 < d; q++) segs.push_back(((i - nb4) << 20) | q);
         }
         if (wbase >= 0) {
             G.hub_wave_slots = std::max(G.hub_wave_slots, wslots);

@@ -409,6 +409,14 @@ int slm_plan_groups(slm_ctx *ctx, int64_t *groups, int64_t *bin_rows, int64_t *b
     API_END
 }
 
+int slm_debug_sweep_floor(slm_ctx *ctx, int32_t mode, double *ms) {
+    API_BEGIN
+    require_agg(ctx);
+    SLM_REQUIRE(ctx->g->u32_ok, SLM_EUNSUP, "needs the integer fast path");
+    *ms = sweep_floor_ms(ctx, *ctx->g, ctx->f, mode);
+    API_END
+}
+
 int slm_get_cstar(slm_ctx *ctx, int64_t *cstar_out) {
     API_BEGIN
     require_graph(ctx);

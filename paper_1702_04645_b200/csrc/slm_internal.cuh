@@ -269,6 +269,7 @@ void build_members_and_aggregates(slm_ctx *ctx, const LevelGraph &G, Forest &F);
 void build_layout(slm_ctx *ctx, Forest &F);
 void run_plan(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_t *d_cstar,
               int bin_mask = 127, unsigned long long *d_groups = nullptr);
+double sweep_floor_ms(slm_ctx *ctx, const LevelGraph &G, Forest &F, int mode);
 void run_plan_u32(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_t *d_cstar,
                   int bin_mask, unsigned long long *d_groups);
 void run_local_gains(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, double *d_lg,

@@ -468,13 +468,26 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep_warp(SweepArgs<SYM> A, con
     __syncwarp();
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    // row metadata is fetched one row ahead (lane 0..3 carry r, e0, d, L of the next row)
+    int32_t nr = 0;
+    int64_t ne0 = 0, nd = 0;
+    if (w < nrows) {
+        nr = rows[w];
+        ne0 = A.uptr[nr];
+        nd = A.uptr[nr + 1] - ne0;
+    }
     for (int64_t i = w; i < nrows; i += nw) {
-        const int32_t r = rows[i];
-        const int64_t e0 = A.uptr[r], d = A.uptr[r + 1] - e0;
+        const int32_t r = nr;
+        const int64_t e0 = ne0, d = nd;
+        if (i + nw < nrows) {
+            nr = rows[i + nw];
+            ne0 = A.uptr[nr];
+            nd = A.uptr[nr + 1] - ne0;
+        }
         const uint32_t hmask = table_size(d) - 1;
         const int32_t L = A.label[r];
         const double2 sr = node_s(A, r);
-        constexpr int U = 4;
+        constexpr int U = 8;
         for (int64_t cb = 0; cb < d; cb += 32 * U) {
             int32_t c[U];
             uint32_t wt[U];
@@ -517,20 +530,22 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep_warp(SweepArgs<SYM> A, con
     }
 }
 
-// block-wide selection reduce (warp then shared)
+// block-wide selection reduce: warps reduce by shuffles, warp 0 merges the per-warp
+// partials by shuffles, one barrier pair
 template <int BLOCK>
 __device__ __forceinline__ void sel_block(Sel &S, Sel *sh) {
     sel_warp(S);
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (lane == 0) sh[wid] = S;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int q = 1; q < BLOCK / 32; q++) sel_merge(S, sh[q]);
-        sh[0] = S;
+    if (wid == 0) {
+        if (lane < BLOCK / 32) S = sh[lane];
+        else sel_init(S);
+        sel_warp(S);
+        if (lane == 0) sh[0] = S;
     }
     __syncthreads();
     S = sh[0];
-    __syncthreads();
 }
 
 template <int BLOCK>
@@ -550,12 +565,19 @@ __device__ __forceinline__ void best_block(double &bt, int32_t &bc, double *sbt,
         sbc[wid] = bc;
     }
     __syncthreads();
-    if (threadIdx.x == 0)
-        for (int q = 0; q < BLOCK / 32; q++)
-            if (better2(sbt[q], sbc[q], bt, bc)) {
-                bt = sbt[q];
-                bc = sbc[q];
+    if (wid == 0) {
+        bt = lane < BLOCK / 32 ? sbt[lane] : -INFINITY;
+        bc = lane < BLOCK / 32 ? sbc[lane] : 0x7fffffff;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double obt = __shfl_xor_sync(0xffffffffu, bt, off);
+            const int32_t obc = __shfl_xor_sync(0xffffffffu, bc, off);
+            if (better2(obt, obc, bt, bc)) {
+                bt = obt;
+                bc = obc;
             }
+        }
+    }
     __syncthreads();
 }
 
@@ -637,40 +659,74 @@ __global__ void __launch_bounds__(BLOCK) k_sweep_cta(SweepArgs<SYM> A, const int
             if (threadIdx.x == 0) gnocc[i] = 0;
         } else {
             occ_clear(tk, tv, socc, threadIdx.x, no, BLOCK);
-            __syncthreads();
-            if (threadIdx.x == 0) s_nocc = 0;
+            if (threadIdx.x == 0) s_nocc = 0;   // read by all threads before the sel barriers
         }
         __syncthreads();
     }
 }
 
-// bins 4, 5 insert phase: one CTA per (row, segment of HUB_SEG entries), global tables
-constexpr int HUB_SEG = 8192;
+// hub rows (bin 5) insert phase: one CTA per (row, segment of HUB_SEG entries).  The
+// segment is combined in a shared table first, then each distinct community of the segment
+// is merged into the row's global table (L2-resident within a wave) with one claim + add.
+constexpr int HUB_SEG = 4096;
+constexpr int HUB_BLOCK = 512;
+constexpr int HUB_H = 8192;
 template <bool SYM>
-__global__ void __launch_bounds__(256) k_sweep_hub_insert(SweepArgs<SYM> A, const int32_t *rows,
-                                                          const int64_t *seg_row, int64_t nseg,
-                                                          const int64_t *hoff, int32_t *gk,
-                                                          uint32_t *gv, uint32_t *gocc,
-                                                          uint32_t *gnocc) {
-    // hoff here is already rebased onto the wave's table window (gk/gv/gocc)
-    constexpr int U = 8;
+__global__ void __launch_bounds__(HUB_BLOCK) k_sweep_hub_insert(SweepArgs<SYM> A,
+                                                                const int32_t *rows,
+                                                                const int64_t *seg_row,
+                                                                int64_t nseg, const int64_t *hoff,
+                                                                int32_t *gk, uint32_t *gv,
+                                                                uint32_t *gocc, uint32_t *gnocc) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint32_t s_nocc;
+    int32_t *hk = (int32_t *)smem;
+    uint32_t *hv = (uint32_t *)(hk + HUB_H);
+    uint16_t *socc = (uint16_t *)(hv + HUB_H);
+    for (int k = threadIdx.x; k < HUB_H; k += HUB_BLOCK) {
+        hk[k] = -1;
+        hv[k] = 0;
+    }
+    if (threadIdx.x == 0) s_nocc = 0;
+    __syncthreads();
+    constexpr int U = HUB_SEG / HUB_BLOCK;
     for (int64_t q = blockIdx.x; q < nseg; q += gridDim.x) {
         const int64_t i = seg_row[q] >> 20, sgi = seg_row[q] & 0xFFFFF;
         const int32_t r = rows[i];
         const int64_t e0 = A.uptr[r], d = A.uptr[r + 1] - e0;
-        const uint32_t hmask = (uint32_t)(hoff[i + 1] - hoff[i]) - 1;
-        int32_t *tk = gk + hoff[i];
-        uint32_t *tv = gv + hoff[i];
-        uint32_t *to = gocc + hoff[i];
         const int64_t lo = sgi * HUB_SEG, hi = min(d, lo + HUB_SEG);
-        for (int64_t cb = lo; cb < hi; cb += 256 * U) {
+        {
             int32_t c[U];
             uint32_t wt[U];
             bool v[U];
-            load_entries<U>(A, e0, hi, cb + threadIdx.x, 256, c, wt, v);
+            load_entries<U>(A, e0, hi, lo + threadIdx.x, HUB_BLOCK, c, wt, v);
 #pragma unroll
-            for (int u = 0; u < U; u++) hash_insert_warp(tk, tv, hmask, to, &gnocc[i], v[u], c[u], wt[u]);
+            for (int u = 0; u < U; u++)
+                hash_insert_warp(hk, hv, (uint32_t)(HUB_H - 1), socc, &s_nocc, v[u], c[u], wt[u]);
         }
+        __syncthreads();
+        const uint32_t no = s_nocc;
+        const uint32_t gmask = (uint32_t)(hoff[i + 1] - hoff[i]) - 1;
+        int32_t *tk = gk + hoff[i];
+        uint32_t *tv = gv + hoff[i];
+        uint32_t *to = gocc + hoff[i];
+        for (uint32_t k0 = 0; k0 < no; k0 += HUB_BLOCK) {
+            const uint32_t k = k0 + threadIdx.x;
+            const bool valid = k < no;
+            int32_t c = -1;
+            uint32_t g = 0;
+            if (valid) {
+                const uint32_t sl = socc[k];
+                c = hk[sl];
+                g = hv[sl];
+                hk[sl] = -1;
+                hv[sl] = 0;
+            }
+            hash_insert_warp(tk, tv, gmask, to, &gnocc[i], valid, c, g);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_nocc = 0;
+        __syncthreads();
     }
 }
 
@@ -716,6 +772,7 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
         set_smem(k_sweep_cta<128, 2048, false, SYM>, (size_t)2048 * 10);
         set_smem(k_sweep_cta<512, 8192, false, SYM>, (size_t)8192 * 10);
         set_smem(k_sweep_cta<1024, 16384, false, SYM>, (size_t)16384 * 10);
+        set_smem(k_sweep_hub_insert<SYM>, (size_t)HUB_H * 10);
         attrs[SYM] = true;
     }
     if (nb(0) && (bin_mask & 1)) {
@@ -761,7 +818,8 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
             int32_t *gk = ctx->hk32.p - W0.base;
             uint32_t *gv = ctx->hv32.p - W0.base, *go = ctx->hocc32.p - W0.base;
             // segment items carry bin-5 row indices
-            k_sweep_hub_insert<SYM><<<(unsigned)std::min<int64_t>(ns, 148 * 8), 256, 0, s>>>(
+            k_sweep_hub_insert<SYM><<<(unsigned)std::min<int64_t>(ns, 148 * 2), HUB_BLOCK,
+                                      (size_t)HUB_H * 10, s>>>(
                 A, rows(5), G.hub_seg.p + W0.seg, ns, hoff5, gk, gv, go, ctx->hnocc32.p);
             k_sweep_cta<1024, 1, true, SYM><<<(unsigned)std::min<int64_t>(nr, 148), 1024, 16, s>>>(
                 A, rows(5) + W0.row, nr, hoff5 + W0.row, gk, gv, go, ctx->hnocc32.p + W0.row);
@@ -776,4 +834,55 @@ void run_plan_u32(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_
         k_copy_labels32<<<grid_for(G.n, 256), 256, 0, ctx->stream>>>(F.comm.p, G.n, d_cstar);
     if (G.sym) launch_sweep<true>(ctx, G, F, m, d_cstar, bin_mask, d_groups);
     else launch_sweep<false>(ctx, G, F, m, d_cstar, bin_mask, d_groups);
+}
+
+// ---------------------------------------------------------------- diagnostics
+// Memory-system floor of the sweep: stream the union (mode 0), + gather labels of the
+// neighbours (1), + gather float S of those labels (2).  Used by tools/probe.py only.
+__global__ void __launch_bounds__(256) k_floor(const int32_t *unbr, const uint32_t *u32,
+                                               const int32_t *label, const float *S1f, int64_t E,
+                                               int mode, unsigned long long *out) {
+    constexpr int U = 8;
+    unsigned long long acc = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < E; b += stride * U) {
+        int32_t z[U];
+        uint32_t w[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t e = b + u * stride;
+            z[u] = e < E ? __ldcs(unbr + e) : 0;
+            w[u] = e < E ? __ldcs(u32 + e) : 0;
+        }
+        if (mode >= 1) {
+#pragma unroll
+            for (int u = 0; u < U; u++) z[u] = label[z[u]];
+        }
+        if (mode >= 2) {
+#pragma unroll
+            for (int u = 0; u < U; u++) w[u] += (uint32_t)S1f[z[u]];
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) acc += (unsigned long long)(z[u] ^ w[u]);
+    }
+    if (acc == 0x123456789ull) *out = acc;
+}
+
+double sweep_floor_ms(slm_ctx *ctx, const LevelGraph &G, Forest &F, int mode) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    DBuf<unsigned long long> o;
+    o.resize(1);
+    k_floor<<<148 * 8, 256, 0, ctx->stream>>>(G.unbr.p, G.uu32.p, F.comm.p, F.S1f.p, G.ue, mode, o.p);
+    cudaEventRecord(a, ctx->stream);
+    for (int it = 0; it < 5; it++)
+        k_floor<<<148 * 8, 256, 0, ctx->stream>>>(G.unbr.p, G.uu32.p, F.comm.p, F.S1f.p, G.ue, mode, o.p);
+    cudaEventRecord(b, ctx->stream);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return ms / 5;
 }

@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--full", action="store_true")
     ap.add_argument("--scale", type=int, default=None)
     ap.add_argument("--max-sweeps", type=int, default=100)
+    ap.add_argument("--no-maximal", action="store_true")
     a = ap.parse_args()
     over = {}
     if a.scale is not None:
@@ -57,6 +58,10 @@ def main():
     for mask, name in ((127, "sweep"), (1, "b0"), (2, "b1"), (4, "b2"), (8, "b3"), (16, "b4"), (32, "b5"), (64, "copy")):
         ms = ev_time(ctx, lambda: ctx.plan_async(mask))
         print(f"plan[{name}] ms {ms:.3f}  GTEPS(full E) {info['ue'] / ms / 1e6:.1f}")
+    for mode in (0, 1, 2):
+        print("floor mode", mode, "ms", round(ctx.sweep_floor(mode), 3))
+    if a.no_maximal:
+        return
     t = time.perf_counter(); imp, app, _ = ctx.maximal(cfg, 0, 0); el = time.perf_counter() - t
     print("maximal0_s", el, "improved", imp, "applied", app, "cand/rounds", ctx.last_commit_stats())
     if a.full:
