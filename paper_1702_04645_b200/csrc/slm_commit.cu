@@ -6,14 +6,18 @@
 // an attach target (detector.py:440-454); a commit drags the node's assignment tail
 // (detector.py:421-437) into the target community.
 //
-// Exact parallel replay by rounds.  A candidate's outcome depends on earlier commits only
-// through its two communities.  Each round evaluates every unresolved candidate against
-// the live state ("tentative outcome"), then computes by fixpoint the set of candidates that
-// an earlier *possible* commit could still influence (sharing a community with an earlier
-// tentative commit, transitively); every other candidate's tentative outcome is final.
-// Final commits of one round are pairwise community-disjoint, so they apply in parallel
-// with plain stores.  The earliest unresolved candidate is always final, so rounds make
-// progress; rounds track chains of dependent *commits*, not of skips.
+// Exact parallel replay by community timelines.  A candidate's outcome depends on earlier
+// commits only through its two communities (frm, to).  Every community C gets the ordered
+// list of accepted candidates touching it (its timeline) and one warp that walks it: the
+// walker evaluates the candidates that move INTO C (C owns its target-side state: S[C],
+// count[C], labels of nodes moving in), and parks at a candidate that moves OUT of C until
+// that candidate's target walker has evaluated it.  Evaluating candidate k therefore only
+// waits for frm_k's walker to have reached k -- so a long chain of candidates into one hub
+// community is walked in a single pass, with per-candidate data prefetched 32 at a time.
+// Rounds (kernel relaunches) hand parked walkers over; the earliest unresolved candidate is
+// always evaluable, so every round makes progress.  Candidates whose tail has no neighbour
+// that can move keep their snapshot w_to / attach target even when `to` has changed
+// (only S[to] is re-read); the others are re-priced against the live labels.
 //
 // Tails are contiguous ranges of the community DFS layout (slm_forest.cu): a cycle node's
 // tail is its whole community, any other node's tail is its DFS subtree.
@@ -40,7 +44,7 @@ __global__ void k_cand_scatter(const int32_t *f, const int32_t *pos, int64_t n, 
     GS_LOOP(i, n) if (f[i]) cand[pos[i]] = (int32_t)i;
 }
 
-__global__ void k_coins(const int32_t *cand, int64_t K, uint64_t base, double p, uint8_t *status) {
+__global__ void k_coins(const int32_t *cand, int64_t K, uint64_t base, double p, int32_t *status) {
     GS_LOOP(k, K) status[k] = (uniform01_at(base, cand[k]) < p) ? ST_UNRES : ST_COIN;
 }
 
@@ -100,7 +104,7 @@ struct CommitArgs {
 };
 
 // speculative evaluation against the snapshot (one warp per accepted candidate)
-__global__ void k_spec(CommitArgs A, int64_t K, const uint8_t *status, CandSpec *spec) {
+__global__ void k_spec(CommitArgs A, int64_t K, const int32_t *status, CandSpec *spec) {
     const int lane = threadIdx.x & 31;
     int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -156,133 +160,258 @@ __global__ void k_spec(CommitArgs A, int64_t K, const uint8_t *status, CandSpec 
     }
 }
 
-struct LiveState {
+
+// mark every node of an accepted candidate's tail (a node that may move this sweep)
+__global__ void k_mark_moving(const int32_t *cand, const int32_t *comm, const uint8_t *on_cycle,
+                              const int32_t *cptr, const int32_t *pos, const int32_t *sz,
+                              const int32_t *order, int64_t K, const int32_t *status,
+                              uint8_t *moving) {
+    const int lane = threadIdx.x & 31;
+    int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t k = w; k < K; k += nw) {
+        if (status[k] != ST_UNRES) continue;
+        const int32_t i = cand[k], frm = comm[i], base = cptr[frm];
+        int32_t lo, hi;
+        if (on_cycle[i]) {
+            lo = base;
+            hi = cptr[frm + 1];
+        } else {
+            lo = base + pos[i];
+            hi = lo + sz[i];
+        }
+        for (int32_t q = lo + lane; q < hi; q += 32) moving[order[q]] = 1;
+    }
+}
+
+// re-price flag: a tail node has a neighbour outside `frm` that may move this sweep
+__global__ void k_reprice_flags(CommitArgs A, int64_t K, const int32_t *status,
+                                const CandSpec *spec, const uint8_t *moving, uint8_t *reprice) {
+    const int lane = threadIdx.x & 31;
+    int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t k = w; k < K; k += nw) {
+        if (status[k] != ST_UNRES) continue;
+        const int32_t frm = A.comm[A.cand[k]];
+        const CandSpec c = spec[k];
+        bool hit = false;
+        for (int32_t q = c.tail_lo; q < c.tail_hi && !hit; q++) {
+            const int32_t x = A.order[q];
+            bool h = false;
+            for (int64_t e = A.uptr[x] + lane; e < A.uptr[x + 1]; e += 32) {
+                const int32_t z = A.unbr[e];
+                if (moving[z] && A.comm[z] != frm) h = true;
+            }
+            hit = __any_sync(0xffffffffu, h);
+        }
+        if (lane == 0) reprice[k] = hit;
+    }
+}
+
+__global__ void k_acc_flags(int64_t K, const int32_t *status, int32_t *f) {
+    GS_LOOP(k, K) f[k] = status[k] == ST_UNRES ? 1 : 0;
+}
+__global__ void k_acc_pairs(const int32_t *cand, const int32_t *comm, const int32_t *cstar,
+                            int64_t K, const int32_t *f, const int32_t *pos, uint32_t *key,
+                            int32_t *val) {
+    GS_LOOP(k, K) {
+        if (!f[k]) continue;
+        const int32_t i = cand[k];
+        const int64_t t = 2 * (int64_t)pos[k];
+        key[t] = (uint32_t)comm[i];
+        val[t] = (int32_t)k;
+        key[t + 1] = (uint32_t)cstar[i];
+        val[t + 1] = (int32_t)k;
+    }
+}
+__global__ void k_lb32c(const uint32_t *sorted, int64_t m, int64_t nrows, int32_t *ptr) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= nrows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = m;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            if ((int64_t)sorted[mid] < r) lo = mid + 1;
+            else hi = mid;
+        }
+        ptr[r] = (int32_t)lo;
+    }
+}
+__global__ void k_walker_list(const int32_t *tl_ptr, int64_t nc, int32_t *f) {
+    GS_LOOP(c, nc) f[c] = tl_ptr[c + 1] > tl_ptr[c] ? 1 : 0;
+}
+__global__ void k_walker_scatter(const int32_t *f, const int32_t *pos, const int32_t *tl_ptr,
+                                 int64_t nc, int32_t *wl, int32_t *wpos, int32_t *atk) {
+    GS_LOOP(c, nc) {
+        if (f[c]) wl[pos[c]] = (int32_t)c;
+        wpos[c] = tl_ptr[c];
+        atk[c] = 0x7fffffff;
+    }
+}
+
+struct Live {
     int32_t *lab;
     double *S_out, *S_in;
     int32_t *cnt;
     uint8_t *dirty;
     int32_t *first_commit;
     int32_t *a;
+    int32_t *wpos, *atk;
+    const int32_t *tl_ptr, *tl_ev;
+    const uint8_t *reprice;
+    double *gain;
+    int32_t *remaining;
 };
 
-// tentative evaluation of every unresolved candidate against the live state
-__global__ void k_tentative(CommitArgs A, LiveState S, int64_t K, uint8_t *status,
-                            const CandSpec *spec, uint8_t *tent, double *tgain, int32_t *tj) {
+__device__ __forceinline__ int32_t vload(const int32_t *p) { return *(volatile const int32_t *)p; }
+// resolve an accepted candidate as skipped exactly once (both of its walkers may try)
+__device__ __forceinline__ void resolve_skip(int32_t *status, int32_t k, int32_t *remaining) {
+    if (atomicCAS(status + k, ST_UNRES, ST_SKIP) == ST_UNRES) atomicSub(remaining, 1);
+}
+__device__ __forceinline__ uint8_t vload8(const uint8_t *p) { return *(volatile const uint8_t *)p; }
+
+// one warp per community timeline (see header comment)
+__global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_t *wl, int64_t nw_,
+                                              int32_t *status, const CandSpec *spec) {
     const int lane = threadIdx.x & 31;
     int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t k = w; k < K; k += nw) {
-        if (status[k] != ST_UNRES) continue;
-        const int32_t i = A.cand[k];
-        const int32_t frm = A.comm[i], to = A.cstar[i];
-        if (S.dirty[frm]) {                 // detector.py:489-490
-            if (lane == 0) status[k] = ST_SKIP;
-            continue;
-        }
-        const CandSpec c = spec[k];
-        double wt = c.w_to;
-        int32_t j = c.j;
-        bool ok = S.cnt[to] != 0;           // detector.py:494-495
-        if (ok && S.dirty[to])
-            eval_to_side(A.uptr, A.unbr, A.uu, A.s_out, A.s_in, S.lab, A.order, c.tail_lo,
-                         c.tail_hi, i, to, A.m, A.m2, wt, j);
-        if (lane == 0) {
-            double g = 0.0;
-            if (ok) {
-                const double so_b = c.so_b, si_b = c.si_b;
-                const double so_t = S.S_out[to], si_t = S.S_in[to];
-                // gain_switch d_null, quality.py:216-219, exact operand order
-                double d_null = -S.S_out[frm] * si_b - so_b * S.S_in[frm] + so_t * si_b +
-                                so_b * si_t + 2.0 * so_b * si_b;
-                g = (wt - c.w_from) / A.m - d_null / (A.m * A.m);
-                ok = (g > 0.0) && (j >= 0);  // detector.py:498-502
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t wi = w; wi < nw_; wi += nwarps) {
+        const int32_t C = wl[wi];
+        int32_t p = V.wpos[C];
+        const int32_t end = V.tl_ptr[C + 1];
+        if (p >= end) continue;
+        __threadfence();
+        double SoC = V.S_out[C], SiC = V.S_in[C];
+        int32_t cntC = V.cnt[C];
+        bool parked = false;
+        while (p < end && !parked) {
+            // prefetch up to 32 events
+            const int nb = min(32, end - p);
+            int32_t k = -1, i = 0, frm = 0, to = 0, atF = -1;
+            int32_t st = ST_SKIP;
+            if (lane < nb) {
+                k = V.tl_ev[p + lane];
+                st = vload(status + k);
+                i = A.cand[k];
+                frm = A.comm[i];
+                to = A.cstar[i];
+                if (to == C) atF = vload(V.atk + frm);
             }
-            tent[k] = ok ? 1 : 0;
-            tgain[k] = g;
-            tj[k] = j;
+            for (int q = 0; q < nb; q++) {
+                const int32_t kq = __shfl_sync(0xffffffffu, k, q);
+                const int32_t fq = __shfl_sync(0xffffffffu, frm, q);
+                const int32_t tq = __shfl_sync(0xffffffffu, to, q);
+                const int32_t iq = __shfl_sync(0xffffffffu, i, q);
+                int32_t sq = __shfl_sync(0xffffffffu, st, q);
+                if (tq != C) {
+                    // C is the source side: resolved already, or a certain skip (C touched by
+                    // an earlier commit: dirty is final here since C's timeline is at kq), or
+                    // wait for the target walker's verdict
+                    if (sq == ST_UNRES) sq = vload(status + kq);
+                    // short-circuit only if C never offered kq to its target walker
+                    if (sq == ST_UNRES && vload(V.atk + C) != kq && vload8(V.dirty + C)) {
+                        if (lane == 0) resolve_skip(status, kq, V.remaining);
+                        continue;
+                    }
+                    if (sq == ST_UNRES) {
+                        if (lane == 0) {
+                            __threadfence();
+                            *(volatile int32_t *)(V.atk + C) = kq;
+                        }
+                        parked = true;
+                        p += q;
+                        break;
+                    }
+                    if (sq == ST_COMMIT) {   // our state was changed by that commit
+                        __threadfence();
+                        SoC = V.S_out[C];
+                        SiC = V.S_in[C];
+                        cntC = V.cnt[C];
+                    }
+                    continue;
+                }
+                // C evaluates kq.  Already resolved by the source side, or a certain skip
+                // (source dirty -- dirty flags are monotone and only commits before kq can
+                // have set it -- or target empty), or frm's walker must have reached kq.
+                if (sq == ST_UNRES) sq = vload(status + kq);
+                if (sq != ST_UNRES) continue;
+                if (cntC == 0 || vload8(V.dirty + fq)) {
+                    if (lane == 0) resolve_skip(status, kq, V.remaining);
+                    continue;
+                }
+                int32_t aq = __shfl_sync(0xffffffffu, atF, q);
+                if (aq != kq) aq = vload(V.atk + fq);
+                if (aq != kq) {
+                    if (lane == 0) {
+                        __threadfence();
+                        *(volatile int32_t *)(V.atk + C) = kq;
+                    }
+                    parked = true;
+                    p += q;
+                    break;
+                }
+                __threadfence();
+                uint8_t verdict = ST_SKIP;
+                double g = 0.0;
+                int32_t j = -1;
+                const CandSpec c = spec[kq];
+                if (!vload8(V.dirty + fq) && cntC != 0) {       // detector.py:489-495
+                    double wt = c.w_to;
+                    j = c.j;
+                    if (vload8(V.dirty + C) && V.reprice[kq])
+                        eval_to_side(A.uptr, A.unbr, A.uu, A.s_out, A.s_in, V.lab, A.order,
+                                     c.tail_lo, c.tail_hi, iq, C, A.m, A.m2, wt, j);
+                    const double SoF = V.S_out[fq], SiF = V.S_in[fq];
+                    const double so_b = c.so_b, si_b = c.si_b;
+                    // gain_switch d_null (quality.py:216-219), exact operand order
+                    const double d_null = -SoF * si_b - so_b * SiF + SoC * si_b + so_b * SiC +
+                                          2.0 * so_b * si_b;
+                    g = (wt - c.w_from) / A.m - d_null / (A.m * A.m);
+                    if (g > 0.0 && j >= 0) verdict = ST_COMMIT;   // detector.py:498-502
+                }
+                if (verdict == ST_COMMIT) {
+                    const int32_t len = c.tail_hi - c.tail_lo;
+                    for (int32_t t = c.tail_lo + lane; t < c.tail_hi; t += 32) V.lab[A.order[t]] = C;
+                    SoC += c.so_b;
+                    SiC += c.si_b;
+                    cntC += len;
+                    if (lane == 0) {
+                        V.a[iq] = j;
+                        // move_nodes (quality.py:87-95)
+                        V.S_out[fq] -= c.so_b;
+                        V.S_in[fq] -= c.si_b;
+                        V.cnt[fq] -= len;
+                        V.S_out[C] = SoC;
+                        V.S_in[C] = SiC;
+                        V.cnt[C] = cntC;
+                        V.dirty[fq] = 1;
+                        V.dirty[C] = 1;
+                        atomicMin(&V.first_commit[fq], kq);
+                        atomicMin(&V.first_commit[C], kq);
+                        V.gain[kq] = g;
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    __threadfence();
+                    if (atomicCAS(status + kq, ST_UNRES, (int32_t)verdict) == ST_UNRES)
+                        atomicSub(V.remaining, 1);
+                }
+            }
+            if (!parked) p += nb;
         }
-    }
-}
-
-__global__ void k_src_init(int64_t K, const uint8_t *status, const uint8_t *tent, uint8_t *srcf) {
-    GS_LOOP(k, K) srcf[k] = (status[k] == ST_UNRES && tent[k]) ? 1 : 0;
-}
-__global__ void k_minsrc_reset(const int32_t *cand, const int32_t *comm, const int32_t *cstar,
-                               int64_t K, const uint8_t *status, int32_t *minsrc) {
-    GS_LOOP(k, K) {
-        if (status[k] != ST_UNRES) continue;
-        int32_t i = cand[k];
-        minsrc[comm[i]] = 0x7fffffff;
-        minsrc[cstar[i]] = 0x7fffffff;
-    }
-}
-__global__ void k_minsrc(const int32_t *cand, const int32_t *comm, const int32_t *cstar, int64_t K,
-                         const uint8_t *status, const uint8_t *srcf, int32_t *minsrc) {
-    GS_LOOP(k, K) {
-        if (status[k] != ST_UNRES || !srcf[k]) continue;
-        int32_t i = cand[k];
-        atomicMin(&minsrc[comm[i]], (int32_t)k);
-        atomicMin(&minsrc[cstar[i]], (int32_t)k);
-    }
-}
-__global__ void k_unstable_update(const int32_t *cand, const int32_t *comm, const int32_t *cstar,
-                                  int64_t K, const uint8_t *status, const uint8_t *tent,
-                                  const int32_t *minsrc, uint8_t *srcf, uint8_t *unst,
-                                  int32_t *changed) {
-    GS_LOOP(k, K) {
-        if (status[k] != ST_UNRES) continue;
-        int32_t i = cand[k];
-        bool u = minsrc[comm[i]] < (int32_t)k || minsrc[cstar[i]] < (int32_t)k;
-        unst[k] = u;
-        uint8_t sf = (tent[k] || u) ? 1 : 0;
-        if (sf != srcf[k]) {
-            srcf[k] = sf;
-            *changed = 1;
-        }
-    }
-}
-
-// apply final outcomes: stable tentative commits commit, stable skips resolve
-__global__ void k_apply(CommitArgs A, LiveState S, int64_t K, uint8_t *status, const uint8_t *tent,
-                        const uint8_t *unst, const CandSpec *spec, const int32_t *tj,
-                        int32_t *remaining) {
-    const int lane = threadIdx.x & 31;
-    int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t k = w; k < K; k += nw) {
-        if (status[k] != ST_UNRES) continue;
-        if (unst[k]) {
-            if (lane == 0) atomicAdd(remaining, 1);
-            continue;
-        }
-        if (!tent[k]) {
-            if (lane == 0) status[k] = ST_SKIP;
-            continue;
-        }
-        const int32_t i = A.cand[k];
-        const int32_t frm = A.comm[i], to = A.cstar[i];
-        const CandSpec c = spec[k];
-        for (int32_t q = c.tail_lo + lane; q < c.tail_hi; q += 32) S.lab[A.order[q]] = to;
         if (lane == 0) {
-            S.a[i] = tj[k];
-            // move_nodes (quality.py:87-95)
-            S.S_out[frm] -= c.so_b;
-            S.S_in[frm] -= c.si_b;
-            S.cnt[frm] -= (c.tail_hi - c.tail_lo);
-            S.S_out[to] += c.so_b;
-            S.S_in[to] += c.si_b;
-            S.cnt[to] += (c.tail_hi - c.tail_lo);
-            S.dirty[frm] = 1;
-            S.dirty[to] = 1;
-            atomicMin(&S.first_commit[frm], (int32_t)k);
-            atomicMin(&S.first_commit[to], (int32_t)k);
-            status[k] = ST_COMMIT;
+            V.wpos[C] = p;
+            if (p >= end) {
+                __threadfence();
+                *(volatile int32_t *)(V.atk + C) = 0x7fffffff;
+            }
         }
     }
 }
 
 __global__ void k_coin_blocked(const int32_t *cand, const int32_t *comm, int64_t K,
-                               const uint8_t *status, const int32_t *first_commit,
+                               const int32_t *status, const int32_t *first_commit,
                                int32_t *out) {
     GS_LOOP(k, K) {
         if (status[k] != ST_COIN) continue;
@@ -291,7 +420,7 @@ __global__ void k_coin_blocked(const int32_t *cand, const int32_t *comm, int64_t
     }
 }
 
-__global__ void k_commit_flags(int64_t K, const uint8_t *status, int32_t *f) {
+__global__ void k_commit_flags(int64_t K, const int32_t *status, int32_t *f) {
     GS_LOOP(k, K) f[k] = status[k] == ST_COMMIT ? 1 : 0;
 }
 __global__ void k_gather_gains(int64_t K, const int32_t *f, const int32_t *pos, const double *g,
@@ -321,11 +450,11 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     if (K == 0) return;
     cand.resize(K);
     k_cand_scatter<<<grid_for(n, 256), 256, 0, s>>>(flag.p, pos.p, n, cand.p);
-    DBuf<uint8_t> status, tent, srcf, unst;
+    DBuf<int32_t> status;
+    DBuf<uint8_t> moving, reprice;
     status.resize(K);
-    tent.resize(K);
-    srcf.resize(K);
-    unst.resize(K);
+    reprice.resize(K);
+    moving.resize(n);
     k_coins<<<grid_for(K, 256), 256, 0, s>>>(cand.p, K, mix_key2(seed, level, sweep), accept_prob,
                                              status.p);
     CommitArgs A;
@@ -348,60 +477,97 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     spec.resize(K);
     unsigned GW = grid_for((int64_t)K * 32, 256, 148LL * 32);
     k_spec<<<GW, 256, 0, s>>>(A, K, status.p, spec.p);
+    CUDA_TRY(cudaMemsetAsync(moving.p, 0, n, s));
+    k_mark_moving<<<GW, 256, 0, s>>>(cand.p, F.comm.p, F.on_cycle.p, F.cptr.p, F.pos.p, F.sz.p,
+                                     F.order.p, K, status.p, moving.p);
+    k_reprice_flags<<<GW, 256, 0, s>>>(A, K, status.p, spec.p, moving.p, reprice.p);
+    // accepted candidates -> (community, k) pairs -> timelines
+    DBuf<int32_t> af, apos;
+    af.resize(K + 1);
+    apos.resize(K + 1);
+    CUDA_TRY(cudaMemsetAsync(af.p + K, 0, 4, s));
+    k_acc_flags<<<grid_for(K, 256), 256, 0, s>>>(K, status.p, af.p);
+    cub_exclusive_sum<int32_t>(ctx, af.p, apos.p, K + 1);
+    int32_t NA = 0;
+    CUDA_TRY(cudaMemcpyAsync(&NA, apos.p + K, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    ctx->last_accepted = NA;
     // live state
-    DBuf<int32_t> lab, cnt, first_commit, minsrc, tj;
-    DBuf<double> So, Si, tgain;
+    DBuf<int32_t> lab, cnt, first_commit, wpos, atk, tl_ptr, tl_ev, wl, remaining;
+    DBuf<double> So, Si, gbuf;
     DBuf<uint8_t> dirty;
     lab.resize(n);
     cnt.resize(nc);
     first_commit.resize(nc);
-    minsrc.resize(nc);
     So.resize(nc);
     Si.resize(nc);
     dirty.resize(nc);
-    tgain.resize(K);
-    tj.resize(K);
+    gbuf.resize(K);
+    remaining.resize(1);
     CUDA_TRY(cudaMemcpyAsync(lab.p, F.comm.p, n * 4, cudaMemcpyDeviceToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(cnt.p, F.count.p, nc * 4, cudaMemcpyDeviceToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(So.p, F.S_out.p, nc * 8, cudaMemcpyDeviceToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(Si.p, F.S_in.p, nc * 8, cudaMemcpyDeviceToDevice, s));
     CUDA_TRY(cudaMemsetAsync(dirty.p, 0, nc, s));
     CUDA_TRY(cudaMemsetAsync(first_commit.p, 0x7f, nc * 4, s));   // 0x7f7f7f7f > any k
-    LiveState S;
-    S.lab = lab.p;
-    S.S_out = So.p;
-    S.S_in = Si.p;
-    S.cnt = cnt.p;
-    S.dirty = dirty.p;
-    S.first_commit = first_commit.p;
-    S.a = F.a.p;   // committed pointers are written in place (forest.a copy semantics:
-                   // the static tails come from the layout built before this call)
-    int32_t *dflags = ctx->i32d.resize(4);
-    unsigned GK = grid_for(K, 256);
-    for (int round = 0;; round++) {
-        k_tentative<<<GW, 256, 0, s>>>(A, S, K, status.p, spec.p, tent.p, tgain.p, tj.p);
-        k_src_init<<<GK, 256, 0, s>>>(K, status.p, tent.p, srcf.p);
-        for (int it = 0;; it++) {
-            k_minsrc_reset<<<GK, 256, 0, s>>>(cand.p, F.comm.p, d_cstar, K, status.p, minsrc.p);
-            k_minsrc<<<GK, 256, 0, s>>>(cand.p, F.comm.p, d_cstar, K, status.p, srcf.p, minsrc.p);
-            CUDA_TRY(cudaMemsetAsync(dflags, 0, 4, s));
-            k_unstable_update<<<GK, 256, 0, s>>>(cand.p, F.comm.p, d_cstar, K, status.p, tent.p,
-                                                 minsrc.p, srcf.p, unst.p, dflags);
-            int32_t ch = 0;
-            CUDA_TRY(cudaMemcpyAsync(&ch, dflags, 4, cudaMemcpyDeviceToHost, s));
-            CUDA_TRY(cudaStreamSynchronize(s));
-            if (!ch) break;
-        }
-        CUDA_TRY(cudaMemsetAsync(dflags + 1, 0, 4, s));
-        k_apply<<<GW, 256, 0, s>>>(A, S, K, status.p, tent.p, unst.p, spec.p, tj.p, dflags + 1);
-        int32_t rem = 0;
-        CUDA_TRY(cudaMemcpyAsync(&rem, dflags + 1, 4, cudaMemcpyDeviceToHost, s));
+    if (NA > 0) {
+        DBuf<uint32_t> keys, keys_sorted;
+        DBuf<int32_t> vals;
+        keys.resize(2 * (int64_t)NA);
+        keys_sorted.resize(2 * (int64_t)NA);
+        vals.resize(2 * (int64_t)NA);
+        tl_ev.resize(2 * (int64_t)NA);
+        k_acc_pairs<<<grid_for(K, 256), 256, 0, s>>>(cand.p, F.comm.p, d_cstar, K, af.p, apos.p,
+                                                     keys.p, vals.p);
+        sort_pairs_u32_i32(ctx, keys.p, keys_sorted.p, vals.p, tl_ev.p, 2 * (int64_t)NA,
+                           bits_for(nc + 1));
+        tl_ptr.resize(nc + 1);
+        k_lb32c<<<grid_for(nc + 1, 256), 256, 0, s>>>(keys_sorted.p, 2 * (int64_t)NA, nc, tl_ptr.p);
+        // walkers: communities with a non-empty timeline
+        DBuf<int32_t> wf, wp;
+        wf.resize(nc + 1);
+        wp.resize(nc + 1);
+        wpos.resize(nc);
+        atk.resize(nc);
+        CUDA_TRY(cudaMemsetAsync(wf.p + nc, 0, 4, s));
+        k_walker_list<<<grid_for(nc, 256), 256, 0, s>>>(tl_ptr.p, nc, wf.p);
+        cub_exclusive_sum<int32_t>(ctx, wf.p, wp.p, nc + 1);
+        int32_t NW = 0;
+        CUDA_TRY(cudaMemcpyAsync(&NW, wp.p + nc, 4, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
-        ctx->last_rounds = round + 1;
-        if (rem == 0) break;
+        wl.resize(NW);
+        k_walker_scatter<<<grid_for(nc, 256), 256, 0, s>>>(wf.p, wp.p, tl_ptr.p, nc, wl.p, wpos.p,
+                                                           atk.p);
+        CUDA_TRY(cudaMemcpyAsync(remaining.p, &NA, 4, cudaMemcpyHostToDevice, s));
+        Live V;
+        V.lab = lab.p;
+        V.S_out = So.p;
+        V.S_in = Si.p;
+        V.cnt = cnt.p;
+        V.dirty = dirty.p;
+        V.first_commit = first_commit.p;
+        V.a = F.a.p;   // committed pointers are written in place (tails come from the layout)
+        V.wpos = wpos.p;
+        V.atk = atk.p;
+        V.tl_ptr = tl_ptr.p;
+        V.tl_ev = tl_ev.p;
+        V.reprice = reprice.p;
+        V.gain = gbuf.p;
+        V.remaining = remaining.p;
+        const unsigned GWK = grid_for((int64_t)NW * 32, 256, 148LL * 64);
+        int32_t rem = NA;
+        for (int round = 0; rem > 0; round++) {
+            k_walk<<<GWK, 256, 0, s>>>(A, V, wl.p, NW, status.p, spec.p);
+            CUDA_TRY(cudaMemcpyAsync(&rem, remaining.p, 4, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            ctx->last_rounds = round + 1;
+            SLM_REQUIRE(round < 10000000, SLM_ESTATE, "commit walkers made no progress");
+        }
     }
-    CUDA_TRY(cudaMemsetAsync(dflags + 2, 0, 4, s));
-    k_coin_blocked<<<GK, 256, 0, s>>>(cand.p, F.comm.p, K, status.p, first_commit.p, dflags + 2);
+    int32_t *dflags = ctx->i32d.resize(4);
+    CUDA_TRY(cudaMemsetAsync(dflags, 0, 4, s));
+    const unsigned GK = grid_for(K, 256);
+    k_coin_blocked<<<GK, 256, 0, s>>>(cand.p, F.comm.p, K, status.p, first_commit.p, dflags);
     // applied + gains in ascending candidate order
     DBuf<int32_t> cf, cpos;
     cf.resize(K + 1);
@@ -411,14 +577,14 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     cub_exclusive_sum<int32_t>(ctx, cf.p, cpos.p, K + 1);
     int32_t hv[2] = {0, 0};
     CUDA_TRY(cudaMemcpyAsync(&hv[0], cpos.p + K, 4, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaMemcpyAsync(&hv[1], dflags + 2, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(&hv[1], dflags, 4, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     *applied = hv[0];
     *improved = (hv[0] > 0) || hv[1];
     if (gains && hv[0] > 0) {
         DBuf<double> gg;
         gg.resize(hv[0]);
-        k_gather_gains<<<GK, 256, 0, s>>>(K, cf.p, cpos.p, tgain.p, gg.p);
+        k_gather_gains<<<GK, 256, 0, s>>>(K, cf.p, cpos.p, gbuf.p, gg.p);
         gains->resize(hv[0]);
         CUDA_TRY(cudaMemcpyAsync(gains->data(), gg.p, hv[0] * 8, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
