@@ -129,6 +129,10 @@ SLM_API int slm_score(slm_ctx *ctx, int32_t on_original, const int64_t *labels, 
 /* uniform01 (rng.py:34-43) with parts = (level, sweep), computed on the device. */
 SLM_API int slm_uniform01(slm_ctx *ctx, uint64_t seed, int64_t level, int64_t sweep, const int64_t *ids,
                   int64_t k, double *out);
+/* Phase timers (enabled by SLM_PROFILE=1, which synchronises at phase boundaries): ms per
+ * phase in the order plan, candidates, spec, walk, components, aggregates, layout,
+ * positive-local-gains, positive-small, positive-giant, assign, aggregate. */
+SLM_API int slm_phase_times(slm_ctx *ctx, double *ms, int32_t nmax, int32_t reset);
 /* Diagnostics of the last slm_maximal: candidates, commit rounds. */
 SLM_API int slm_last_commit_stats(slm_ctx *ctx, int64_t *candidates, int64_t *rounds);
 

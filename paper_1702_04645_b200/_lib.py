@@ -63,6 +63,7 @@ SIGNATURES = {
     "slm_score": (C.c_int, [_VP, C.c_int32, _VP, C.c_double, _PD]),
     "slm_uniform01": (C.c_int, [_VP, C.c_uint64, _I64, _I64, _VP, _I64, _VP]),
     "slm_last_commit_stats": (C.c_int, [_VP, _PI64, _PI64]),
+    "slm_phase_times": (C.c_int, [_VP, _VP, C.c_int32, C.c_int32]),
     "slm_plan_sweep_async": (C.c_int, [_VP, C.c_int32]),
     "slm_plan_groups": (C.c_int, [_VP, _PI64, _VP, _VP]),
     "slm_get_cstar": (C.c_int, [_VP, _VP]),
@@ -304,6 +305,14 @@ class Context:
 
     def sync(self):
         self.call("slm_sync")
+
+    PHASES = ("plan", "candidates", "spec", "walk", "components", "aggregates", "layout",
+              "positive_lg", "positive_small", "positive_giant", "assign", "aggregate")
+
+    def phase_times(self, reset=False):
+        ms = np.zeros(len(self.PHASES), np.float64)
+        self.call("slm_phase_times", ptr(ms), len(self.PHASES), 1 if reset else 0)
+        return {k: round(float(v), 1) for k, v in zip(self.PHASES, ms)}
 
     def last_commit_stats(self):
         c, r = C.c_int64(), C.c_int64()

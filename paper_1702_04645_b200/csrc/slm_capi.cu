@@ -82,6 +82,8 @@ extern "C" {
 slm_ctx *slm_create(int device) {
     slm_ctx *ctx = new slm_ctx();
     ctx->device = device;
+    const char *pe = getenv("SLM_PROFILE");
+    ctx->prof = pe && pe[0] == '1';
     if (cudaSetDevice(device) != cudaSuccess ||
         cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
         cudaGetLastError();
@@ -438,7 +440,9 @@ int slm_maximal(slm_ctx *ctx, const slm_config *cfg, int64_t level, int64_t swee
     // the plan depends only on the forest: reuse it across coin-only sweeps (F7)
     if (ctx->plan_version != F.version || ctx->cstar.n != (size_t)G.n) {
         ctx->cstar.resize(G.n);
+        phase_mark(ctx, -1);
         run_plan(ctx, G, F, m, ctx->cstar.p);
+        phase_mark(ctx, PH_PLAN);
         ctx->plan_version = F.version;
     }
     int imp = 0;
@@ -501,6 +505,14 @@ int slm_uniform01(slm_ctx *ctx, uint64_t seed, int64_t level, int64_t sweep, con
     k_uniform<<<grid_for(k, 256), 256, 0, ctx->stream>>>(mix_key2(seed, level, sweep), d.p, k, o.p);
     CUDA_TRY(cudaMemcpyAsync(out, o.p, k * 8, cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    API_END
+}
+
+int slm_phase_times(slm_ctx *ctx, double *ms, int32_t nmax, int32_t reset) {
+    API_BEGIN
+    for (int i = 0; i < NPHASE && i < nmax; i++) ms[i] = ctx->ph_ms[i];
+    if (reset)
+        for (int i = 0; i < NPHASE; i++) ctx->ph_ms[i] = 0.0;
     API_END
 }
 

@@ -30,9 +30,12 @@
 
 struct CandSpec {
     double w_to, w_from, so_b, si_b;
+    double pgj;          // pairwise gain of the snapshot attach target j
+    int64_t je;          // its union entry index (row order = tie-break order), -1 if none
+    int64_t mv_off;      // moving-neighbour entries of the tail: [mv_off, mv_off + mv_cnt)
     int32_t j;
     int32_t tail_lo, tail_hi;   // range in F.order
-    int32_t pad;
+    int32_t mv_cnt;
 };
 
 enum { ST_UNRES = 0, ST_SKIP = 1, ST_COMMIT = 2, ST_COIN = 3 };
@@ -58,7 +61,8 @@ __device__ __forceinline__ double warp_sum(double v) {
 __device__ void eval_to_side(const int64_t *uptr, const int32_t *unbr, const double *uu,
                              const double *s_out, const double *s_in, const int32_t *lab,
                              const int32_t *order, int32_t lo, int32_t hi, int32_t i, int32_t to,
-                             double m, double m2, double &w_to, int32_t &j) {
+                             double m, double m2, double &w_to, int32_t &j, int64_t *je = nullptr,
+                             double *pgj = nullptr) {
     const int lane = threadIdx.x & 31;
     double acc = 0.0;
     for (int32_t q = lo; q < hi; q++) {
@@ -67,6 +71,37 @@ __device__ void eval_to_side(const int64_t *uptr, const int32_t *unbr, const dou
             if (lab[unbr[e]] == to) acc += uu[e];
     }
     w_to = warp_sum(acc);
+    const double soi = s_out[i], sii = s_in[i];
+    double bt = -INFINITY;
+    int64_t be = INT64_MAX;
+    for (int64_t e = uptr[i] + lane; e < uptr[i + 1]; e += 32) {
+        int32_t z = unbr[e];
+        if (lab[z] != to) continue;
+        double pg = uu[e] / m - (soi * s_in[z] + sii * s_out[z]) / m2;
+        if (pg > bt) {
+            bt = pg;
+            be = e;
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        double ot = __shfl_xor_sync(0xffffffffu, bt, off);
+        int64_t oe = __shfl_xor_sync(0xffffffffu, be, off);
+        if (ot > bt || (ot == bt && oe < be)) {
+            bt = ot;
+            be = oe;
+        }
+    }
+    j = (be != INT64_MAX) ? unbr[be] : -1;
+    if (je) *je = (be != INT64_MAX) ? be : -1;
+    if (pgj) *pgj = bt;
+}
+
+// attach target of i among the entries of its own row only (live labels)
+__device__ void attach_only(const int64_t *uptr, const int32_t *unbr, const double *uu,
+                            const double *s_out, const double *s_in, const int32_t *lab, int32_t i,
+                            int32_t to, double m, double m2, int32_t &j) {
+    const int lane = threadIdx.x & 31;
     const double soi = s_out[i], sii = s_in[i];
     double bt = -INFINITY;
     int64_t be = INT64_MAX;
@@ -141,20 +176,24 @@ __global__ void k_spec(CommitArgs A, int64_t K, const int32_t *status, CandSpec 
         so = warp_sum(so);
         si = warp_sum(si);
         wf = warp_sum(wf);
-        double wt;
+        double wt, pgj;
         int32_t j;
+        int64_t je;
         eval_to_side(A.uptr, A.unbr, A.uu, A.s_out, A.s_in, A.comm, A.order, lo, hi, i, to, A.m,
-                     A.m2, wt, j);
+                     A.m2, wt, j, &je, &pgj);
         if (lane == 0) {
             CandSpec c;
             c.w_to = wt;
             c.w_from = wf;
             c.so_b = so;
             c.si_b = si;
+            c.pgj = pgj;
+            c.je = je;
+            c.mv_off = 0;
             c.j = j;
             c.tail_lo = lo;
             c.tail_hi = hi;
-            c.pad = 0;
+            c.mv_cnt = 0;
             spec[k] = c;
         }
     }
@@ -184,28 +223,103 @@ __global__ void k_mark_moving(const int32_t *cand, const int32_t *comm, const ui
     }
 }
 
-// re-price flag: a tail node has a neighbour outside `frm` that may move this sweep
-__global__ void k_reprice_flags(CommitArgs A, int64_t K, const int32_t *status,
-                                const CandSpec *spec, const uint8_t *moving, uint8_t *reprice) {
+// moving-neighbour entries of each accepted candidate's tail: entries (x in tail, z) with z
+// outside `frm` and in some accepted tail.  Only these can change w_to / the attach target
+// when `to` changes during the sweep, so re-pricing is an exact delta over this list.
+__global__ void k_mv_scan(CommitArgs A, int64_t K, const int32_t *status, CandSpec *spec,
+                          const uint8_t *moving, int fill, int64_t *cnt, int32_t *mv_z,
+                          double *mv_u, int64_t *mv_e, uint8_t *mv_i) {
     const int lane = threadIdx.x & 31;
     int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t k = w; k < K; k += nw) {
         if (status[k] != ST_UNRES) continue;
-        const int32_t frm = A.comm[A.cand[k]];
+        const int32_t i = A.cand[k], frm = A.comm[i];
         const CandSpec c = spec[k];
-        bool hit = false;
-        for (int32_t q = c.tail_lo; q < c.tail_hi && !hit; q++) {
+        int64_t base = fill ? c.mv_off : 0, total = 0;
+        for (int32_t q = c.tail_lo; q < c.tail_hi; q++) {
             const int32_t x = A.order[q];
-            bool h = false;
-            for (int64_t e = A.uptr[x] + lane; e < A.uptr[x + 1]; e += 32) {
-                const int32_t z = A.unbr[e];
-                if (moving[z] && A.comm[z] != frm) h = true;
+            for (int64_t e0 = A.uptr[x]; e0 < A.uptr[x + 1]; e0 += 32) {
+                const int64_t e = e0 + lane;
+                bool hit = false;
+                int32_t z = 0;
+                if (e < A.uptr[x + 1]) {
+                    z = A.unbr[e];
+                    hit = moving[z] && A.comm[z] != frm;
+                }
+                const unsigned hm = __ballot_sync(0xffffffffu, hit);
+                if (fill && hit) {
+                    const int64_t at = base + total + __popc(hm & ((1u << lane) - 1));
+                    mv_z[at] = z;
+                    mv_u[at] = A.uu[e];
+                    mv_e[at] = e;
+                    mv_i[at] = (x == i);
+                }
+                total += __popc(hm);
             }
-            hit = __any_sync(0xffffffffu, h);
         }
-        if (lane == 0) reprice[k] = hit;
+        if (lane == 0) {
+            if (fill) spec[k].mv_cnt = (int32_t)total;
+            else cnt[k] = total;
+        }
     }
+}
+__global__ void k_mv_offsets(int64_t K, const int32_t *status, const int64_t *off, CandSpec *spec) {
+    GS_LOOP(k, K) if (status[k] == ST_UNRES) spec[k].mv_off = off[k];
+}
+
+struct MvList {
+    const int32_t *z;
+    const double *u;
+    const int64_t *e;
+    const uint8_t *is_i;
+};
+
+// exact re-pricing of candidate (i -> C) against the live labels: w_to and the attach target
+__device__ void reprice(const CommitArgs &A, const MvList &M, const int32_t *lab, const CandSpec &c,
+                        int32_t i, int32_t C, double &wt, int32_t &j) {
+    const int lane = threadIdx.x & 31;
+    double dw = 0.0;
+    double bt = -INFINITY;
+    int64_t be = INT64_MAX;
+    int lost = 0;
+    const double soi = A.s_out[i], sii = A.s_in[i];
+    for (int32_t t = lane; t < c.mv_cnt; t += 32) {
+        const int64_t q = c.mv_off + t;
+        const int32_t z = M.z[q];
+        const bool now = lab[z] == C, was = A.comm[z] == C;
+        if (now != was) dw += now ? M.u[q] : -M.u[q];
+        if (M.is_i[q]) {
+            if (now) {
+                const double pg = M.u[q] / A.m - (soi * A.s_in[z] + sii * A.s_out[z]) / A.m2;
+                const int64_t e = M.e[q];
+                if (pg > bt || (pg == bt && e < be)) {
+                    bt = pg;
+                    be = e;
+                }
+            } else if (was && z == c.j) {
+                lost = 1;
+            }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        dw += __shfl_xor_sync(0xffffffffu, dw, off);
+        lost |= __shfl_xor_sync(0xffffffffu, lost, off);
+        const double ot = __shfl_xor_sync(0xffffffffu, bt, off);
+        const int64_t oe = __shfl_xor_sync(0xffffffffu, be, off);
+        if (ot > bt || (ot == bt && oe < be)) {
+            bt = ot;
+            be = oe;
+        }
+    }
+    wt = c.w_to + dw;
+    if (lost) {   // the snapshot attach target itself left C: rescan i's row
+        attach_only(A.uptr, A.unbr, A.uu, A.s_out, A.s_in, lab, i, C, A.m, A.m2, j);
+        return;
+    }
+    j = c.j;
+    if (be != INT64_MAX && (c.j < 0 || bt > c.pgj || (bt == c.pgj && be < c.je))) j = A.unbr[be];
 }
 
 __global__ void k_acc_flags(int64_t K, const int32_t *status, int32_t *f) {
@@ -257,7 +371,7 @@ struct Live {
     int32_t *a;
     int32_t *wpos, *atk;
     const int32_t *tl_ptr, *tl_ev;
-    const uint8_t *reprice;
+    MvList mv;
     double *gain;
     int32_t *remaining;
 };
@@ -269,7 +383,11 @@ __device__ __forceinline__ void resolve_skip(int32_t *status, int32_t k, int32_t
 }
 __device__ __forceinline__ uint8_t vload8(const uint8_t *p) { return *(volatile const uint8_t *)p; }
 
-// one warp per community timeline (see header comment)
+// one warp per community timeline (see header comment).  Up to 32 upcoming events are
+// prefetched by the lanes (their static data, and for events C evaluates the source's
+// position / dirty flag / strengths -- final once the source is parked at the event), then
+// walked in order with shuffles; a long chain into C therefore costs no global round trip
+// per event unless its source has not reached it yet.
 __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_t *wl, int64_t nw_,
                                               int32_t *status, const CandSpec *spec) {
     const int lane = threadIdx.x & 31;
@@ -285,23 +403,33 @@ __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_
         int32_t cntC = V.cnt[C];
         bool parked = false;
         while (p < end && !parked) {
-            // prefetch up to 32 events
             const int nb = min(32, end - p);
-            int32_t k = -1, i = 0, frm = 0, to = 0, atF = -1;
-            int32_t st = ST_SKIP;
+            int32_t k = -1, i = 0, frm = 0, to = 0, atF = -1, st = ST_SKIP;
+            int dF = 0;
+            double SoF = 0.0, SiF = 0.0;
+            CandSpec cs;
+            cs.w_to = cs.w_from = cs.so_b = cs.si_b = 0.0;
+            cs.j = -1;
+            cs.tail_lo = cs.tail_hi = 0;
             if (lane < nb) {
                 k = V.tl_ev[p + lane];
                 st = vload(status + k);
                 i = A.cand[k];
                 frm = A.comm[i];
                 to = A.cstar[i];
-                if (to == C) atF = vload(V.atk + frm);
+                if (to == C) {
+                    atF = vload(V.atk + frm);
+                    __threadfence();
+                    dF = vload8(V.dirty + frm);
+                    SoF = V.S_out[frm];
+                    SiF = V.S_in[frm];
+                    cs = spec[k];
+                }
             }
             for (int q = 0; q < nb; q++) {
                 const int32_t kq = __shfl_sync(0xffffffffu, k, q);
                 const int32_t fq = __shfl_sync(0xffffffffu, frm, q);
                 const int32_t tq = __shfl_sync(0xffffffffu, to, q);
-                const int32_t iq = __shfl_sync(0xffffffffu, i, q);
                 int32_t sq = __shfl_sync(0xffffffffu, st, q);
                 if (tq != C) {
                     // C is the source side: resolved already, or a certain skip (C touched by
@@ -333,42 +461,62 @@ __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_
                 // C evaluates kq.  Already resolved by the source side, or a certain skip
                 // (source dirty -- dirty flags are monotone and only commits before kq can
                 // have set it -- or target empty), or frm's walker must have reached kq.
-                if (sq == ST_UNRES) sq = vload(status + kq);
                 if (sq != ST_UNRES) continue;
-                if (cntC == 0 || vload8(V.dirty + fq)) {
+                int32_t aq = __shfl_sync(0xffffffffu, atF, q);
+                int dq = __shfl_sync(0xffffffffu, dF, q);
+                double SoFq = __shfl_sync(0xffffffffu, SoF, q);
+                double SiFq = __shfl_sync(0xffffffffu, SiF, q);
+                if (cntC == 0 || dq) {
                     if (lane == 0) resolve_skip(status, kq, V.remaining);
                     continue;
                 }
-                int32_t aq = __shfl_sync(0xffffffffu, atF, q);
-                if (aq != kq) aq = vload(V.atk + fq);
-                if (aq != kq) {
-                    if (lane == 0) {
-                        __threadfence();
-                        *(volatile int32_t *)(V.atk + C) = kq;
+                if (aq != kq) {   // not parked at kq when prefetched: look again
+                    aq = vload(V.atk + fq);
+                    if (aq != kq) {
+                        if (vload8(V.dirty + fq)) {
+                            if (lane == 0) resolve_skip(status, kq, V.remaining);
+                            continue;
+                        }
+                        if (lane == 0) {
+                            __threadfence();
+                            *(volatile int32_t *)(V.atk + C) = kq;
+                        }
+                        parked = true;
+                        p += q;
+                        break;
                     }
-                    parked = true;
-                    p += q;
-                    break;
+                    __threadfence();
+                    if (vload8(V.dirty + fq)) {
+                        if (lane == 0) resolve_skip(status, kq, V.remaining);
+                        continue;
+                    }
+                    SoFq = V.S_out[fq];
+                    SiFq = V.S_in[fq];
                 }
-                __threadfence();
+                const int32_t iq = __shfl_sync(0xffffffffu, i, q);
+                CandSpec c;
+                c.w_to = __shfl_sync(0xffffffffu, cs.w_to, q);
+                c.w_from = __shfl_sync(0xffffffffu, cs.w_from, q);
+                c.so_b = __shfl_sync(0xffffffffu, cs.so_b, q);
+                c.si_b = __shfl_sync(0xffffffffu, cs.si_b, q);
+                c.j = __shfl_sync(0xffffffffu, cs.j, q);
+                c.tail_lo = __shfl_sync(0xffffffffu, cs.tail_lo, q);
+                c.tail_hi = __shfl_sync(0xffffffffu, cs.tail_hi, q);
+                c.pgj = __shfl_sync(0xffffffffu, cs.pgj, q);
+                c.je = __shfl_sync(0xffffffffu, cs.je, q);
+                c.mv_off = __shfl_sync(0xffffffffu, cs.mv_off, q);
+                c.mv_cnt = __shfl_sync(0xffffffffu, cs.mv_cnt, q);
                 uint8_t verdict = ST_SKIP;
-                double g = 0.0;
-                int32_t j = -1;
-                const CandSpec c = spec[kq];
-                if (!vload8(V.dirty + fq) && cntC != 0) {       // detector.py:489-495
-                    double wt = c.w_to;
-                    j = c.j;
-                    if (vload8(V.dirty + C) && V.reprice[kq])
-                        eval_to_side(A.uptr, A.unbr, A.uu, A.s_out, A.s_in, V.lab, A.order,
-                                     c.tail_lo, c.tail_hi, iq, C, A.m, A.m2, wt, j);
-                    const double SoF = V.S_out[fq], SiF = V.S_in[fq];
-                    const double so_b = c.so_b, si_b = c.si_b;
-                    // gain_switch d_null (quality.py:216-219), exact operand order
-                    const double d_null = -SoF * si_b - so_b * SiF + SoC * si_b + so_b * SiC +
-                                          2.0 * so_b * si_b;
-                    g = (wt - c.w_from) / A.m - d_null / (A.m * A.m);
-                    if (g > 0.0 && j >= 0) verdict = ST_COMMIT;   // detector.py:498-502
-                }
+                double wt = c.w_to;
+                int32_t j = c.j;
+                if (c.mv_cnt > 0 && vload8(V.dirty + C))
+                    reprice(A, V.mv, V.lab, c, iq, C, wt, j);
+                const double so_b = c.so_b, si_b = c.si_b;
+                // gain_switch d_null (quality.py:216-219), exact operand order
+                const double d_null = -SoFq * si_b - so_b * SiFq + SoC * si_b + so_b * SiC +
+                                      2.0 * so_b * si_b;
+                const double g = (wt - c.w_from) / A.m - d_null / (A.m * A.m);
+                if (g > 0.0 && j >= 0) verdict = ST_COMMIT;   // detector.py:498-502
                 if (verdict == ST_COMMIT) {
                     const int32_t len = c.tail_hi - c.tail_lo;
                     for (int32_t t = c.tail_lo + lane; t < c.tail_hi; t += 32) V.lab[A.order[t]] = C;
@@ -436,6 +584,7 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     *improved = 0;
     *applied = 0;
     ctx->last_rounds = 0;
+    phase_mark(ctx, -1);
     // candidates: cstar != label, ascending (detector.py:473)
     DBuf<int32_t> flag, pos, cand;
     flag.resize(n + 1);
@@ -451,9 +600,8 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     cand.resize(K);
     k_cand_scatter<<<grid_for(n, 256), 256, 0, s>>>(flag.p, pos.p, n, cand.p);
     DBuf<int32_t> status;
-    DBuf<uint8_t> moving, reprice;
+    DBuf<uint8_t> moving;
     status.resize(K);
-    reprice.resize(K);
     moving.resize(n);
     k_coins<<<grid_for(K, 256), 256, 0, s>>>(cand.p, K, mix_key2(seed, level, sweep), accept_prob,
                                              status.p);
@@ -475,12 +623,33 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     A.m2 = m * m;
     DBuf<CandSpec> spec;
     spec.resize(K);
+    phase_mark(ctx, PH_CAND);
     unsigned GW = grid_for((int64_t)K * 32, 256, 148LL * 32);
     k_spec<<<GW, 256, 0, s>>>(A, K, status.p, spec.p);
     CUDA_TRY(cudaMemsetAsync(moving.p, 0, n, s));
     k_mark_moving<<<GW, 256, 0, s>>>(cand.p, F.comm.p, F.on_cycle.p, F.cptr.p, F.pos.p, F.sz.p,
                                      F.order.p, K, status.p, moving.p);
-    k_reprice_flags<<<GW, 256, 0, s>>>(A, K, status.p, spec.p, moving.p, reprice.p);
+    DBuf<int64_t> mvcnt, mvoff;
+    DBuf<int32_t> mv_z;
+    DBuf<double> mv_u;
+    DBuf<int64_t> mv_e;
+    DBuf<uint8_t> mv_i;
+    mvcnt.resize(K + 1);
+    mvoff.resize(K + 1);
+    CUDA_TRY(cudaMemsetAsync(mvcnt.p, 0, (K + 1) * 8, s));
+    k_mv_scan<<<GW, 256, 0, s>>>(A, K, status.p, spec.p, moving.p, 0, mvcnt.p, nullptr, nullptr,
+                                 nullptr, nullptr);
+    cub_exclusive_sum<int64_t>(ctx, mvcnt.p, mvoff.p, K + 1);
+    int64_t NMV = 0;
+    CUDA_TRY(cudaMemcpyAsync(&NMV, mvoff.p + K, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    mv_z.resize(NMV);
+    mv_u.resize(NMV);
+    mv_e.resize(NMV);
+    mv_i.resize(NMV);
+    k_mv_offsets<<<grid_for(K, 256), 256, 0, s>>>(K, status.p, mvoff.p, spec.p);
+    k_mv_scan<<<GW, 256, 0, s>>>(A, K, status.p, spec.p, moving.p, 1, nullptr, mv_z.p, mv_u.p,
+                                 mv_e.p, mv_i.p);
     // accepted candidates -> (community, k) pairs -> timelines
     DBuf<int32_t> af, apos;
     af.resize(K + 1);
@@ -551,19 +720,34 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
         V.atk = atk.p;
         V.tl_ptr = tl_ptr.p;
         V.tl_ev = tl_ev.p;
-        V.reprice = reprice.p;
+        V.mv.z = mv_z.p;
+        V.mv.u = mv_u.p;
+        V.mv.e = mv_e.p;
+        V.mv.is_i = mv_i.p;
         V.gain = gbuf.p;
         V.remaining = remaining.p;
+        phase_mark(ctx, PH_SPEC);
         const unsigned GWK = grid_for((int64_t)NW * 32, 256, 148LL * 64);
         int32_t rem = NA;
+        std::vector<double> rt;
         for (int round = 0; rem > 0; round++) {
+            const double t0 = ctx->prof ? now_ms() : 0.0;
             k_walk<<<GWK, 256, 0, s>>>(A, V, wl.p, NW, status.p, spec.p);
             CUDA_TRY(cudaMemcpyAsync(&rem, remaining.p, 4, cudaMemcpyDeviceToHost, s));
             CUDA_TRY(cudaStreamSynchronize(s));
+            if (ctx->prof) rt.push_back(now_ms() - t0);
             ctx->last_rounds = round + 1;
             SLM_REQUIRE(round < 10000000, SLM_ESTATE, "commit walkers made no progress");
         }
+        if (ctx->prof && getenv("SLM_PROFILE_WALK")) {
+            fprintf(stderr, "walk K=%d NA=%d NW=%d rounds=%zu ms:", K, NA, NW, rt.size());
+            for (size_t q = 0; q < rt.size() && q < 8; q++) fprintf(stderr, " %.2f", rt[q]);
+            double tot = 0;
+            for (double x : rt) tot += x;
+            fprintf(stderr, " total %.2f\n", tot);
+        }
     }
+    phase_mark(ctx, PH_WALK);
     int32_t *dflags = ctx->i32d.resize(4);
     CUDA_TRY(cudaMemsetAsync(dflags, 0, 4, s));
     const unsigned GK = grid_for(K, 256);

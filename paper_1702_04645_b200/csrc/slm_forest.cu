@@ -119,6 +119,61 @@ __global__ void k_lb_ptr32(const int32_t *sorted, int64_t m, int64_t nrows, int3
     }
 }
 
+// per-community sums of integer strengths: runs of equal community inside a warp's 32
+// consecutive members are combined by a segmented shuffle scan, one atomic per run (exact:
+// every partial sum is an integer below 2^53)
+__global__ void k_comm_sums_runs(const int32_t *members, const int32_t *comm, const double *s_out,
+                                 const double *s_in, int64_t n, double *S_out, double *S_in) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31LL; b < n;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = b + lane;
+        int32_t c = -1;
+        double so = 0.0, si = 0.0;
+        if (k < n) {
+            const int32_t x = members[k];
+            c = comm[x];
+            so = s_out[x];
+            si = s_in[x];
+        }
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int32_t oc = __shfl_up_sync(0xffffffffu, c, off);
+            const double oso = __shfl_up_sync(0xffffffffu, so, off);
+            const double osi = __shfl_up_sync(0xffffffffu, si, off);
+            if (lane >= off && oc == c) {
+                so += oso;
+                si += osi;
+            }
+        }
+        const int32_t nc = __shfl_down_sync(0xffffffffu, c, 1);
+        if (c >= 0 && (lane == 31 || nc != c)) {
+            atomicAdd(&S_out[c], so);
+            atomicAdd(&S_in[c], si);
+        }
+    }
+}
+
+// gather node strengths in member order (input of the segmented sums)
+__global__ void k_gather_members(const int32_t *members, const double *s_out, const double *s_in,
+                                 int64_t n, double *vo, double *vi) {
+    GS_LOOP(k, n) {
+        const int32_t x = members[k];
+        vo[k] = s_out[x];
+        vi[k] = s_in[x];
+    }
+}
+__global__ void k_comm_finish(const int32_t *cptr, const double *S_out, const double *S_in,
+                              int64_t nc, int32_t *count, double2 *S2, float *S1f, float2 *S2f) {
+    GS_LOOP(c, nc) {
+        const double so = S_out[c], si = S_in[c];
+        S2[c] = make_double2(so, si);
+        S1f[c] = (float)so;
+        S2f[c] = make_float2((float)so, (float)si);
+        count[c] = cptr[c + 1] - cptr[c];
+    }
+}
+
 // per-community sums in ascending member order (bincount order, quality.py:76-78)
 __global__ void k_comm_sums(const int32_t *cptr, const int32_t *members, const double *s_out,
                             const double *s_in, int64_t nc, double *S_out, double *S_in,
@@ -348,8 +403,22 @@ void build_members_and_aggregates(slm_ctx *ctx, const LevelGraph &G, Forest &F) 
         sort_pairs_u32_i32(ctx, (uint32_t *)F.comm.p, (uint32_t *)ksorted, iota, F.members.p, n,
                            bits_for(nc + 1));
     k_lb_ptr32<<<grid_for(nc + 1, 256), 256, 0, s>>>(ksorted, n, nc, F.cptr.p);
-    k_comm_sums<<<grid_for(nc, 128), 128, 0, s>>>(F.cptr.p, F.members.p, G.s_out.p, G.s_in.p, nc,
-                                                  F.S_out.p, F.S_in.p, F.count.p, F.S2.p, F.S1f.p, F.S2f.p);
+    // segmented sums over the member-ordered strengths (exact for integer weights in any
+    // order; CUB's fixed reduction tree keeps real-valued sums deterministic)
+    if (!G.integral) {
+        // real weights: sequential per-community sums in node order (numpy bincount order)
+        k_comm_sums<<<grid_for(nc, 128), 128, 0, s>>>(F.cptr.p, F.members.p, G.s_out.p, G.s_in.p,
+                                                      nc, F.S_out.p, F.S_in.p, F.count.p, F.S2.p,
+                                                      F.S1f.p, F.S2f.p);
+        F.agg_valid = true;
+        return;
+    }
+    CUDA_TRY(cudaMemsetAsync(F.S_out.p, 0, nc * 8, s));
+    CUDA_TRY(cudaMemsetAsync(F.S_in.p, 0, nc * 8, s));
+    k_comm_sums_runs<<<grid_for(n, 256), 256, 0, s>>>(F.members.p, F.comm.p, G.s_out.p, G.s_in.p,
+                                                       n, F.S_out.p, F.S_in.p);
+    k_comm_finish<<<grid_for(nc, 256), 256, 0, s>>>(F.cptr.p, F.S_out.p, F.S_in.p, nc, F.count.p,
+                                                    F.S2.p, F.S1f.p, F.S2f.p);
     F.agg_valid = true;
 }
 
@@ -439,8 +508,12 @@ void build_layout(slm_ctx *ctx, Forest &F) {
 }
 
 void forest_refresh(slm_ctx *ctx, const LevelGraph &G, Forest &F) {
+    phase_mark(ctx, -1);
     run_components(ctx, F, G.n);
+    phase_mark(ctx, PH_REFRESH_COMP);
     build_members_and_aggregates(ctx, G, F);
+    phase_mark(ctx, PH_REFRESH_AGG);
     build_layout(ctx, F);
+    phase_mark(ctx, PH_REFRESH_LAYOUT);
     F.version++;
 }

@@ -136,7 +136,14 @@ struct Forest {
     uint64_t version = 0;
 };
 
+enum Phase { PH_PLAN, PH_CAND, PH_SPEC, PH_WALK, PH_REFRESH_COMP, PH_REFRESH_AGG, PH_REFRESH_LAYOUT,
+             PH_POS_LG, PH_POS_SMALL, PH_POS_GIANT, PH_ASSIGN, PH_AGGREGATE, NPHASE };
+
 struct slm_ctx {
+    // optional phase timing (SLM_PROFILE=1): synchronises at phase boundaries
+    bool prof = false;
+    double ph_ms[NPHASE] = {};
+    double ph_t0 = 0.0;
     int device = 0;
     cudaStream_t stream = nullptr;
     std::string err;
@@ -165,6 +172,20 @@ struct slm_ctx {
 };
 
 // ------------------------------------------------------------------------- helpers
+
+#include <chrono>
+static inline double now_ms() {
+    return std::chrono::duration<double, std::milli>(
+               std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+// mark the end of a phase (no-op unless profiling)
+static inline void phase_mark(slm_ctx *ctx, int ph) {
+    if (!ctx->prof) return;
+    cudaStreamSynchronize(ctx->stream);
+    double t = now_ms();
+    if (ph >= 0) ctx->ph_ms[ph] += t - ctx->ph_t0;
+    ctx->ph_t0 = t;
+}
 
 static inline unsigned grid_for(int64_t work, int block, int64_t cap = 148LL * 64) {
     int64_t g = (work + block - 1) / block;

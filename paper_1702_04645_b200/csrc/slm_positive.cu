@@ -849,6 +849,7 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     if (gains) gains->clear();
     if (m == 0.0 || n == 0) return;
     read_small_part();
+    phase_mark(ctx, -1);
     DBuf<uint8_t> bad;
     bad.resize(nc);
     CUDA_TRY(cudaMemsetAsync(bad.p, 0, nc, s));
@@ -865,6 +866,7 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     if (nbad == 0) return;
     list.resize(nbad);
     k_bad_scatter<<<grid_for(nc, 256), 256, 0, s>>>(f.p, pos.p, nc, list.p);
+    phase_mark(ctx, PH_POS_LG);
     std::vector<int32_t> hbad(nbad), hcptr(nc + 1);
     CUDA_TRY(cudaMemcpyAsync(hbad.data(), list.p, nbad * 4, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(hcptr.data(), F.cptr.p, (nc + 1) * 4, cudaMemcpyDeviceToHost, s));
@@ -934,6 +936,7 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     DBuf<int32_t> ngains, nunres;
     std::vector<int32_t> hng1, hun1, hng2, hun2;
     launch_small(ctx, A, small1, dparts, ngains, nunres, hng1, hun1);
+    phase_mark(ctx, PH_POS_SMALL);
     int64_t tot = 0, un = 0;
     for (size_t i = 0; i < small1.size(); i++) {
         tot += hng1[i];
@@ -996,6 +999,7 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     int32_t hflags[2];
     CUDA_TRY(cudaMemcpyAsync(hflags, flags.p, 8, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
+    phase_mark(ctx, PH_POS_GIANT);
     SLM_REQUIRE(!hflags[1], SLM_EUNSUP, "assignment cycle longer than 2 in POSITIVE");
     *splits = tot;
     *unresolved = un;

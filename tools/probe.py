@@ -47,6 +47,7 @@ def main():
     ctx = _lib.Context(0)
     t = time.perf_counter()
     GN.build_on_device(ctx, a.config, **over)
+    ctx.phase_times(reset=True)
     info = ctx.info()
     print("build_s", round(time.perf_counter() - t, 3), json.dumps(info))
     t = time.perf_counter(); ctx.assign(want=False); print("assign_s", time.perf_counter() - t)
@@ -70,6 +71,7 @@ def main():
         g = Graph(info["n"], None, None, None)
         g._ctx = ctx
         ctx.level = 0
+        ctx.phase_times(reset=True)
         t = time.perf_counter()
         res = _run(g, RunConfig(max_outer_iters=a.max_sweeps))
         el = time.perf_counter() - t
@@ -77,6 +79,7 @@ def main():
         print("full_run_s", round(el, 3), "levels", st.levels, "sweeps", st.sweeps_per_level,
               "Q", res.final_score, "phase_s", {k: round(v, 3) for k, v in st.phase_seconds.items()},
               "moves", st.accepted_moves, "splits", st.accepted_splits, "skipped_pos", st.skipped_positive_calls)
+        print("phase_ms", ctx.phase_times())
 
 
 if __name__ == "__main__":
