@@ -28,6 +28,8 @@
 #include <algorithm>
 #include <cstring>
 #include <cstdlib>
+#include <functional>
+#include <map>
 
 // parts up to this size use the warp executor; SLM_SMALL_PART overrides it (tests force the
 // giant executor onto small graphs with it)
@@ -415,208 +417,9 @@ __global__ void k_g_subsums(GiantArgs A, int64_t lo, int64_t hi, int64_t cbase, 
         A.sib[x] = psi[i1] - psi[i0];
         A.xw[x] = pdp[i1] - pdp[i0];
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (S && blockIdx.x == 0 && threadIdx.x == 0) {
         S->so_c = pso[hi - lo];
         S->si_c = psi[hi - lo];
-    }
-}
-
-constexpr int GE_BLOCK = 256;
-
-__global__ void __launch_bounds__(GE_BLOCK) k_g_eval(GiantArgs A, int64_t lo, int64_t hi,
-                                                     const GiantState *S, int32_t *blk_neg,
-                                                     double *blk_g, int32_t *blk_x) {
-    __shared__ double sg[GE_BLOCK / 32];
-    __shared__ int32_t sx[GE_BLOCK / 32];
-    __shared__ int32_t sn[GE_BLOCK / 32];
-    const double m = A.m, m2 = A.m2;
-    const double so_c = S->so_c, si_c = S->si_c;
-    const int32_t pid = S->pid, r = S->root, q = S->q;
-    const bool two = S->two;
-    double bg = -INFINITY;
-    int32_t bx = 0x7fffffff;
-    int neg = 0;
-    for (int64_t k = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < hi;
-         k += (int64_t)gridDim.x * blockDim.x) {
-        int32_t x = A.order[k];
-        if (A.gmark[x] != pid) continue;
-        const double sox = A.s_out[x], six = A.s_in[x];
-        double g = A.wpart[x] / m - (sox * (si_c - six) + six * (so_c - sox)) / m2;
-        if (g < 0.0) neg++;
-        if (x == r || (two && x == q)) continue;
-        double so_b = A.sob[x], si_b = A.sib[x];
-        double null = -so_c * si_b - so_b * si_c + 2.0 * so_b * si_b;
-        double gain = -A.xw[x] / m - null / (m * m);
-        if (gain > bg || (gain == bg && x < bx)) {
-            bg = gain;
-            bx = x;
-        }
-    }
-    neg = wsum_i(neg);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        double og = __shfl_xor_sync(0xffffffffu, bg, o);
-        int32_t ox = __shfl_xor_sync(0xffffffffu, bx, o);
-        if (og > bg || (og == bg && ox < bx)) {
-            bg = og;
-            bx = ox;
-        }
-    }
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) {
-        sg[wid] = bg;
-        sx[wid] = bx;
-        sn[wid] = neg;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double g0 = sg[0];
-        int32_t x0 = sx[0];
-        int nn = sn[0];
-        for (int i = 1; i < GE_BLOCK / 32; i++) {
-            nn += sn[i];
-            if (sg[i] > g0 || (sg[i] == g0 && sx[i] < x0)) {
-                g0 = sg[i];
-                x0 = sx[i];
-            }
-        }
-        blk_g[blockIdx.x] = g0;
-        blk_x[blockIdx.x] = x0;
-        blk_neg[blockIdx.x] = nn;
-    }
-}
-
-__global__ void k_g_reduce(GiantArgs A, int nb, const int32_t *blk_neg, const double *blk_g,
-                           const int32_t *blk_x, GiantState *S) {
-    if (threadIdx.x != 0) return;
-    double g0 = -INFINITY;
-    int32_t x0 = 0x7fffffff;
-    int nn = 0;
-    for (int i = 0; i < nb; i++) {
-        nn += blk_neg[i];
-        if (blk_g[i] > g0 || (blk_g[i] == g0 && blk_x[i] < x0)) {
-            g0 = blk_g[i];
-            x0 = blk_x[i];
-        }
-    }
-    S->neg = nn;
-    S->best_gain = g0;
-    S->best_x = x0;
-    S->pair_gain = -INFINITY;
-    if (S->two) {
-        const double m = A.m, m2 = A.m2;
-        const int32_t q = S->q;
-        double so_b = A.sob[q], si_b = A.sib[q];
-        double so_c = S->so_c, si_c = S->si_c;
-        double null = -so_c * si_b - so_b * si_c + 2.0 * so_b * si_b;
-        S->pair_gain = -A.xw[q] / m - null / m2;
-    }
-}
-
-// re-mark the cut subtree as part pid_b and count it
-__global__ void k_g_cut_mark(GiantArgs A, int64_t cbase, int32_t xc, int32_t pid, int32_t pid_b,
-                             GiantState *S) {
-    const int64_t lo = cbase + A.pos[xc], hi = lo + A.sz[xc];
-    int cnt = 0;
-    for (int64_t k = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < hi;
-         k += (int64_t)gridDim.x * blockDim.x) {
-        int32_t x = A.order[k];
-        if (A.gmark[x] == pid) {
-            A.gmark[x] = pid_b;
-            cnt++;
-        }
-    }
-    cnt = wsum_i(cnt);
-    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&S->bsize, cnt);
-}
-
-// one thread: apply the cut to a, the part totals and the ancestors' subtree sums
-__global__ void k_g_apply(GiantArgs A, int32_t xc, int32_t pair, GiantState *S) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    const int32_t r = S->root;
-    const double sb = A.sob[xc], ib = A.sib[xc];
-    S->so_c -= sb;
-    S->si_c -= ib;
-    if (pair) {
-        A.sob[r] -= sb;
-        A.sib[r] -= ib;
-        A.a[r] = r;
-        A.a[xc] = xc;
-        S->two = 0;
-    } else {
-        int32_t y = A.a[xc];
-        A.a[xc] = xc;
-        for (;;) {
-            A.sob[y] -= sb;
-            A.sib[y] -= ib;
-            if (y == r) break;
-            y = A.a[y];
-        }
-    }
-}
-
-// edges between the cut subtree b and the rest R: drop them from w_part (R side) and from
-// x_w along the tree path between their endpoints (strictly below the LCA, R nodes only)
-__global__ void k_g_cross(GiantArgs A, int64_t cbase, int32_t xc, int32_t xc_parent, int32_t pid,
-                          int32_t pid_b) {
-    const int lane = threadIdx.x & 31;
-    int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int64_t lo = cbase + A.pos[xc], hi = lo + A.sz[xc];
-    for (int64_t k = lo + w; k < hi; k += nw) {
-        int32_t z = A.order[k];
-        if (A.gmark[z] != pid_b) continue;
-        const int32_t pz = A.pos[z];
-        for (int64_t e = A.uptr[z] + lane; e < A.uptr[z + 1]; e += 32) {
-            int32_t v = A.unbr[e];
-            if (A.gmark[v] != pid) continue;
-            const double u = A.uu[e];
-            atomicAdd(&A.wpart[v], -u);
-            int32_t y = v;
-            while (!in_range(A, y, pz)) {
-                atomicAdd(&A.xw[y], -u);
-                y = A.a[y];
-            }
-            const int32_t lca = y;
-            y = xc_parent;
-            while (y != lca) {
-                atomicAdd(&A.xw[y], -u);
-                y = A.a[y];
-            }
-        }
-    }
-}
-
-// compact a (small) cut subtree into its own descriptor region with in-part subtree sizes
-__global__ void k_g_compact_flags(const int32_t *order, const int32_t *gmark, int64_t lo,
-                                  int64_t hi, int32_t pid_b, int32_t *flag) {
-    for (int64_t k = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < hi;
-         k += (int64_t)gridDim.x * blockDim.x)
-        flag[k - lo] = gmark[order[k]] == pid_b ? 1 : 0;
-}
-__global__ void k_g_compact_fill(const int32_t *order, const int32_t *pos, const int32_t *flag,
-                                 const int32_t *idx, int64_t lo, int64_t hi, int32_t dst_off,
-                                 int32_t *pbuf, int32_t *posb) {
-    for (int64_t k = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < hi;
-         k += (int64_t)gridDim.x * blockDim.x)
-        if (flag[k - lo]) {
-            pbuf[dst_off + idx[k - lo]] = order[k];
-            posb[idx[k - lo]] = pos[order[k]];
-        }
-}
-__global__ void k_g_compact_psz(const int32_t *pbuf, const int32_t *posb, const int32_t *sz,
-                                int32_t dst_off, int32_t len, int32_t *psz) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        int32_t y = pbuf[dst_off + i];
-        int32_t endp = posb[i] + sz[y];
-        int32_t lo = (int32_t)i, hi = len;   // first index with posb >= endp
-        while (lo < hi) {
-            int32_t mid = (lo + hi) >> 1;
-            if (posb[mid] < endp) lo = mid + 1;
-            else hi = mid;
-        }
-        psz[y] = lo - (int32_t)i;
     }
 }
 
@@ -630,190 +433,475 @@ __global__ void k_init_i32(int32_t *x, int64_t n, int32_t v) { GS_LOOP(i, n) x[i
 
 static DBuf<uint32_t> g_stamp;   // monotone part stamps (never reset)
 
-namespace {
+// ------------------------------------------------ giant parts: one CTA per part
 
-struct Split {              // one cut of a giant part
-    double gain;
-    int kind;               // 0: small child (descriptor index), 1: giant child (giant id)
-    int64_t child;
-};
-struct GiantRec {
-    std::vector<Split> splits;
-};
+constexpr int GB = 1024;              // threads per giant-part CTA
+constexpr int GT = 128;               // top candidate list kept between full passes
+constexpr int GLOC = 2;               // per-thread candidates of a full pass
+constexpr int GSORT = GB * GLOC;      // sorted in shared memory
+constexpr int DIRTY_CAP = 1 << 16;    // locally updated nodes before a forced full pass
 
-struct PosCtx {
-    slm_ctx *ctx;
-    const LevelGraph *G;
-    Forest *F;
-    double m;
-    GiantArgs GA;
-    DBuf<GiantState> S;
-    DBuf<int32_t> blk_neg, blk_x, cflag, cidx;
-    DBuf<double> blk_g, vso, vsi, vdp, pso, psi, pdp;
-    int32_t next_pid = 1;
-    int32_t alloc_off = 0;             // descriptor region allocator (pbuf2 / sstk)
-    std::vector<PartDesc> small2;      // small parts cut from giant parts
-    std::vector<GiantRec> giants;
-    int64_t unresolved = 0, splits = 0;
-    bool changed = false;
-    int32_t *pbuf2 = nullptr, *psz = nullptr;
+struct GPart {
+    int64_t lo, hi, cbase;   // member slice (community DFS coordinates) and community base
+    int32_t pid, root;
+    double so_c, si_c;
+    int64_t neg_off;         // region of hi-lo entries in the negative-member pool
+    int64_t dirty_off;       // region of DIRTY_CAP entries in the dirty pool
 };
 
-// process one giant part (members: order[lo..hi) with gmark == pid), recursively
-int64_t giant_process(PosCtx &P, int64_t cbase, int64_t lo, int64_t hi, int32_t pid,
-                      int32_t root) {
-    slm_ctx *ctx = P.ctx;
-    cudaStream_t s = ctx->stream;
-    GiantArgs &A = P.GA;
-    const int64_t N = hi - lo;
-    const int64_t gid = (int64_t)P.giants.size();
-    P.giants.emplace_back();
-    // state
-    GiantState h0;
-    memset(&h0, 0, sizeof(h0));
-    h0.pid = pid;
-    h0.root = root;
-    int32_t ar = 0, aq = 0;
-    CUDA_TRY(cudaMemcpyAsync(&ar, A.a + root, 4, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    if (ar != root) {
-        CUDA_TRY(cudaMemcpyAsync(&aq, A.a + ar, 4, cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaStreamSynchronize(s));
-        SLM_REQUIRE(aq == root, SLM_EUNSUP, "assignment cycle longer than 2 in POSITIVE");
-        h0.q = ar;
-        h0.two = 1;
-    } else {
-        h0.q = root;
-        h0.two = 0;
+struct GOut {
+    // split log: (part pid, sequence, gain, child kind 0 small / 1 giant, child id)
+    int32_t *log_pid, *log_seq, *log_kind, *log_child;
+    double *log_gain;
+    int32_t *nlog;
+    // small children: descriptors + compacted members (warp executor, second batch)
+    PartDesc *desc;
+    int32_t *ndesc;
+    int32_t *pbuf2, *posb, *psz;
+    int32_t *alloc;
+    // giant children: next wave
+    int64_t *nx_lo, *nx_hi;
+    int32_t *nx_pid, *nx_root, *nx_size;
+    int32_t *nnext;
+    int32_t *pid_ctr;
+    unsigned long long *unresolved;
+    int32_t *flags;          // [0] changed, [1] unsupported cycle
+    int32_t small_part;      // cut subtrees up to this size go to the warp executor
+};
+
+__device__ __forceinline__ double g_member(const GiantArgs &A, int32_t x, double so_c, double si_c) {
+    const double sox = A.s_out[x], six = A.s_in[x];
+    return A.wpart[x] / A.m - (sox * (si_c - six) + six * (so_c - sox)) / A.m2;
+}
+__device__ __forceinline__ double g_branch(const GiantArgs &A, int32_t x, double so_c, double si_c) {
+    const double so_b = A.sob[x], si_b = A.sib[x];
+    const double null = -so_c * si_b - so_b * si_c + 2.0 * so_b * si_b;
+    return -A.xw[x] / A.m - null / (A.m * A.m);
+}
+__device__ __forceinline__ bool gbetter(double g1, int32_t x1, double g2, int32_t x2) {
+    return g1 > g2 || (g1 == g2 && x1 < x2);
+}
+
+// block argmax of (g desc, x asc); result valid in every thread
+__device__ void block_best(double &g, int32_t &x, double *sg, int32_t *sx) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double og = __shfl_xor_sync(0xffffffffu, g, o);
+        const int32_t ox = __shfl_xor_sync(0xffffffffu, x, o);
+        if (gbetter(og, ox, g, x)) {
+            g = og;
+            x = ox;
+        }
     }
-    CUDA_TRY(cudaMemcpyAsync(P.S.p, &h0, sizeof(h0), cudaMemcpyHostToDevice, s));
-    // full pass: w_part, LCA deposits, subtree sums
-    unsigned GW = grid_for(N * 32, 256, 148LL * 32);
-    unsigned GN = grid_for(N, 256);
-    k_g_wpart<<<GW, 256, 0, s>>>(A, lo, hi, pid);
-    k_g_lca<<<GW, 256, 0, s>>>(A, lo, hi, pid);
-    P.vso.resize(N + 1);
-    P.vsi.resize(N + 1);
-    P.vdp.resize(N + 1);
-    P.pso.resize(N + 1);
-    P.psi.resize(N + 1);
-    P.pdp.resize(N + 1);
-    k_g_gather<<<GN, 256, 0, s>>>(A, lo, hi, pid, P.vso.p, P.vsi.p, P.vdp.p);
-    CUDA_TRY(cudaMemsetAsync(P.vso.p + N, 0, 8, s));
-    CUDA_TRY(cudaMemsetAsync(P.vsi.p + N, 0, 8, s));
-    CUDA_TRY(cudaMemsetAsync(P.vdp.p + N, 0, 8, s));
-    {
-        size_t tb = 0;
-        CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, P.vso.p, P.pso.p, N + 1, s));
-        ctx->tmp.resize(tb);
-        CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx->tmp.p, tb, P.vso.p, P.pso.p, N + 1, s));
-        CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx->tmp.p, tb, P.vsi.p, P.psi.p, N + 1, s));
-        CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx->tmp.p, tb, P.vdp.p, P.pdp.p, N + 1, s));
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        sg[wid] = g;
+        sx[wid] = x;
     }
-    k_g_subsums<<<GN, 256, 0, s>>>(A, lo, hi, cbase, pid, P.pso.p, P.psi.p, P.pdp.p, P.S.p);
-    // split loop
-    const unsigned GE = std::min<unsigned>(GN, 148 * 8);
-    P.blk_neg.resize(GE);
-    P.blk_g.resize(GE);
-    P.blk_x.resize(GE);
-    int64_t neg_left = 0;
+    __syncthreads();
+    if (wid == 0) {
+        g = lane < GB / 32 ? sg[lane] : -INFINITY;
+        x = lane < GB / 32 ? sx[lane] : 0x7fffffff;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double og = __shfl_xor_sync(0xffffffffu, g, o);
+            const int32_t ox = __shfl_xor_sync(0xffffffffu, x, o);
+            if (gbetter(og, ox, g, x)) {
+                g = og;
+                x = ox;
+            }
+        }
+        if (lane == 0) {
+            sg[0] = g;
+            sx[0] = x;
+        }
+    }
+    __syncthreads();
+    g = sg[0];
+    x = sx[0];
+    __syncthreads();
+}
+
+__device__ int block_sum_i(int v, int *si) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) si[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        v = lane < GB / 32 ? si[lane] : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) si[0] = v;
+    }
+    __syncthreads();
+    v = si[0];
+    __syncthreads();
+    return v;
+}
+
+__device__ __forceinline__ void mark_dirty(int32_t y, uint8_t *gflag, int32_t *dirty, int *ndirty,
+                                           int *overflow) {
+    // byte flag with a CAS on its aligned word
+    unsigned int *wp = (unsigned int *)(gflag + (y & ~3));
+    const unsigned int bit = 1u << ((y & 3) * 8);
+    const unsigned int old = atomicOr(wp, bit);
+    if (!(old & bit)) {
+        const int at = atomicAdd(ndirty, 1);
+        if (at < DIRTY_CAP) dirty[at] = y;
+        else *overflow = 1;
+    }
+}
+
+// one CTA per giant part: the reference's repeated best single cut (detector.py:210-284)
+// with incremental state.  Between full passes every non-dirty candidate's branch gain
+// can only decrease (the part totals shrink; its own subtree sums and crossing weight are
+// unchanged), and every non-dirty member's gain can only increase, so the top list plus the
+// bound tau decide most splits exactly without rescanning the part.
+__global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *parts, GOut O,
+                                                  int32_t *neg_pool, int32_t *dirty_pool,
+                                                  uint8_t *gflag, uint8_t *negflag) {
+    __shared__ double tg[GSORT];
+    __shared__ int32_t tx[GSORT];
+    __shared__ double sg[32];
+    __shared__ int32_t sxx[32];
+    __shared__ int si[32];
+    __shared__ int s_nneg, s_ndirty, s_overflow;
+    __shared__ double s_tau, s_so, s_si;
+    __shared__ int s_ntop, s_two;
+    const GPart P = parts[blockIdx.x];
+    const int tid = threadIdx.x;
+    const int32_t pid = P.pid, r = P.root;
+    int32_t *negl = neg_pool + P.neg_off;
+    int32_t *dirty = dirty_pool + P.dirty_off;
+    const int32_t q = A.a[r];
+    if (tid == 0) {
+        s_two = (q != r);
+        if (q != r && A.a[q] != r) atomicOr(&O.flags[1], 1);
+        s_so = P.so_c;
+        s_si = P.si_c;
+        s_nneg = 0;
+        s_ndirty = 0;
+        s_overflow = 0;
+    }
+    __syncthreads();
+    if (s_two && A.a[q] != r) return;
+    bool need_full = true;
+    int seq = 0;
     for (;;) {
-        k_g_eval<<<GE, GE_BLOCK, 0, s>>>(A, lo, hi, P.S.p, P.blk_neg.p, P.blk_g.p, P.blk_x.p);
-        k_g_reduce<<<1, 32, 0, s>>>(A, GE, P.blk_neg.p, P.blk_g.p, P.blk_x.p, P.S.p);
-        GiantState h;
-        CUDA_TRY(cudaMemcpyAsync(&h, P.S.p, sizeof(h), cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaStreamSynchronize(s));
-        if (h.neg == 0) break;
+        double so_c = s_so, si_c = s_si;
+        const bool two = s_two;
+        double bg = -INFINITY;
+        int32_t bx = 0x7fffffff;
+        int negc = 0;
+        if (!need_full) {
+            // incremental: re-evaluate the top list and the dirty nodes
+            const int ntop = s_ntop, nd = min(s_ndirty, DIRTY_CAP);
+            for (int t = tid; t < ntop + nd; t += GB) {
+                const int32_t x = t < ntop ? tx[t] : dirty[t - ntop];
+                if (A.gmark[x] != pid || x == r || (two && x == q)) continue;
+                const double g = g_branch(A, x, so_c, si_c);
+                if (gbetter(g, x, bg, bx)) {
+                    bg = g;
+                    bx = x;
+                }
+            }
+            block_best(bg, bx, sg, sxx);
+            if (!(bg > s_tau) || s_overflow) need_full = true;
+        }
+        if (need_full) {
+            // reset the incremental state
+            for (int t = tid; t < min(s_ndirty, DIRTY_CAP); t += GB) gflag[dirty[t]] = 0;
+            for (int t = tid; t < s_nneg; t += GB) negflag[negl[t]] = 0;
+            __syncthreads();
+            if (tid == 0) {
+                s_ndirty = 0;
+                s_overflow = 0;
+                s_nneg = 0;
+            }
+            __syncthreads();
+            double lg[GLOC];
+            int32_t lx[GLOC];
+#pragma unroll
+            for (int u = 0; u < GLOC; u++) {
+                lg[u] = -INFINITY;
+                lx[u] = 0x7fffffff;
+            }
+            double drop = -INFINITY;
+            for (int64_t k = P.lo + tid; k < P.hi; k += GB) {
+                const int32_t x = A.order[k];
+                if (A.gmark[x] != pid) continue;
+                if (g_member(A, x, so_c, si_c) < 0.0) {
+                    negl[atomicAdd(&s_nneg, 1)] = x;
+                    negflag[x] = 1;
+                }
+                if (x == r || (two && x == q)) continue;
+                double g = g_branch(A, x, so_c, si_c);
+                int32_t xx = x;
+#pragma unroll
+                for (int u = 0; u < GLOC; u++) {   // insertion into the local top list
+                    if (gbetter(g, xx, lg[u], lx[u])) {
+                        const double tgv = lg[u];
+                        const int32_t txv = lx[u];
+                        lg[u] = g;
+                        lx[u] = xx;
+                        g = tgv;
+                        xx = txv;
+                    }
+                }
+                drop = fmax(drop, g);   // best candidate not kept locally
+            }
+#pragma unroll
+            for (int u = 0; u < GLOC; u++) {
+                tg[tid * GLOC + u] = lg[u];
+                tx[tid * GLOC + u] = lx[u];
+            }
+            // bitonic sort of the GSORT candidates, best first
+            for (int kk = 2; kk <= GSORT; kk <<= 1) {
+                for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+                    __syncthreads();
+                    for (int idx = tid; idx < GSORT; idx += GB) {
+                        const int ixj = idx ^ jj;
+                        if (ixj > idx) {
+                            const bool up = (idx & kk) == 0;
+                            const bool swap = up ? gbetter(tg[ixj], tx[ixj], tg[idx], tx[idx])
+                                                 : gbetter(tg[idx], tx[idx], tg[ixj], tx[ixj]);
+                            if (swap) {
+                                const double a1 = tg[idx];
+                                tg[idx] = tg[ixj];
+                                tg[ixj] = a1;
+                                const int32_t b1 = tx[idx];
+                                tx[idx] = tx[ixj];
+                                tx[ixj] = b1;
+                            }
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            // tau: best candidate outside the kept list
+            double dmax = drop;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+            if ((tid & 31) == 0) sg[tid >> 5] = dmax;
+            __syncthreads();
+            if (tid == 0) {
+                double t = tg[GT];
+                for (int w = 0; w < GB / 32; w++) t = fmax(t, sg[w]);
+                s_tau = t;
+                int nt = 0;
+                while (nt < GT && tx[nt] != 0x7fffffff) nt++;
+                s_ntop = nt;
+            }
+            __syncthreads();
+            bg = tg[0];
+            bx = tx[0];
+            need_full = false;
+        }
+        // negative members: the previous ones (re-evaluated) plus the dirty ones
+        {
+            const int nn = s_nneg, nd = min(s_ndirty, DIRTY_CAP);
+            int c = 0;
+            for (int t = tid; t < nn; t += GB) {
+                const int32_t x = negl[t];
+                if (A.gmark[x] == pid && g_member(A, x, so_c, si_c) < 0.0) c++;
+            }
+            for (int t = tid; t < nd; t += GB) {
+                const int32_t x = dirty[t];
+                if (A.gmark[x] == pid && !negflag[x] && g_member(A, x, so_c, si_c) < 0.0) {
+                    c++;
+                    negflag[x] = 1;
+                    negl[atomicAdd(&s_nneg, 1)] = x;
+                }
+            }
+            negc = block_sum_i(c, si);
+        }
+        if (negc == 0) break;   // no member with negative gain left (detector.py:224-225)
         int32_t xc = -1;
         int pair = 0;
         double gain = 0.0;
-        if (h.best_x != 0x7fffffff && h.best_gain > 0.0) {
-            xc = h.best_x;
-            gain = h.best_gain;
-        } else if (h.two && h.pair_gain > 0.0) {
-            xc = h.q;
-            pair = 1;
-            gain = h.pair_gain;
+        if (bx != 0x7fffffff && bg > 0.0) {
+            xc = bx;
+            gain = bg;
+        } else if (two) {
+            const double pg = [&] {   // pair cut (detector.py:254-274, 288-335 with s = 2)
+                const double so_b = A.sob[q], si_b = A.sib[q];
+                const double null = -so_c * si_b - so_b * si_c + 2.0 * so_b * si_b;
+                return -A.xw[q] / A.m - null / A.m2;
+            }();
+            if (pg > 0.0) {
+                xc = q;
+                pair = 1;
+                gain = pg;
+            }
         }
         if (xc < 0) {
-            neg_left = h.neg;
+            if (tid == 0) atomicAdd(O.unresolved, (unsigned long long)negc);   // 275-277
             break;
         }
-        int32_t xpar = 0;
-        CUDA_TRY(cudaMemcpyAsync(&xpar, A.a + xc, 4, cudaMemcpyDeviceToHost, s));
-        const int32_t pid_b = P.next_pid++;
-        CUDA_TRY(cudaMemsetAsync(&P.S.p->bsize, 0, 4, s));
-        int32_t pxc = 0, sxc = 0;
-        CUDA_TRY(cudaMemcpyAsync(&pxc, A.pos + xc, 4, cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaMemcpyAsync(&sxc, A.sz + xc, 4, cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaStreamSynchronize(s));
-        const int64_t blo = cbase + pxc, bhi = blo + sxc;
-        k_g_cut_mark<<<grid_for(sxc, 256), 256, 0, s>>>(A, cbase, xc, pid, pid_b, P.S.p);
-        k_g_apply<<<1, 32, 0, s>>>(A, xc, pair, P.S.p);
-        k_g_cross<<<grid_for((int64_t)sxc * 32, 256, 148LL * 32), 256, 0, s>>>(A, cbase, xc, xpar,
-                                                                              pid, pid_b);
-        int32_t bsize = 0;
-        CUDA_TRY(cudaMemcpyAsync(&bsize, &P.S.p->bsize, 4, cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaStreamSynchronize(s));
-        P.changed = true;
-        P.splits++;
-        Split sp;
-        sp.gain = gain;
-        if (bsize <= SMALL_PART) {
-            // compact b into its own region for the warp executor
-            const int32_t off = P.alloc_off;
-            P.alloc_off += bsize;
-            const int64_t L = bhi - blo;
-            P.cflag.resize(L + 1);
-            P.cidx.resize(L + 1);
-            DBuf<int32_t> posb;
-            posb.resize(bsize);
-            k_g_compact_flags<<<grid_for(L, 256), 256, 0, s>>>(A.order, A.gmark, blo, bhi, pid_b,
-                                                               P.cflag.p);
-            CUDA_TRY(cudaMemsetAsync(P.cflag.p + L, 0, 4, s));
-            cub_exclusive_sum<int32_t>(ctx, P.cflag.p, P.cidx.p, L + 1);
-            k_g_compact_fill<<<grid_for(L, 256), 256, 0, s>>>(A.order, A.pos, P.cflag.p,
-                                                              P.cidx.p, blo, bhi, off, P.pbuf2,
-                                                              posb.p);
-            k_g_compact_psz<<<grid_for(bsize, 256), 256, 0, s>>>(P.pbuf2, posb.p, A.sz, off,
-                                                                 bsize, P.psz);
-            CUDA_TRY(cudaStreamSynchronize(s));
-            PartDesc d;
-            d.off = off;
-            d.len = bsize;
-            d.from_layout = 0;
-            d.pad = 0;
-            sp.kind = 0;
-            sp.child = (int64_t)P.small2.size();
-            P.small2.push_back(d);
-        } else {
-            GiantState saved;
-            CUDA_TRY(cudaMemcpyAsync(&saved, P.S.p, sizeof(saved), cudaMemcpyDeviceToHost, s));
-            CUDA_TRY(cudaStreamSynchronize(s));
-            sp.kind = 1;
-            sp.child = giant_process(P, cbase, blo, bhi, pid_b, xc);
-            CUDA_TRY(cudaMemcpyAsync(P.S.p, &saved, sizeof(saved), cudaMemcpyHostToDevice, s));
-            // the child used the shared scratch: recompute this part's block buffers lazily
-            P.blk_neg.resize(GE);
-            P.blk_g.resize(GE);
-            P.blk_x.resize(GE);
+        // ---- apply the cut: a, part totals, ancestors' subtree sums
+        const int32_t xpar = A.a[xc];
+        const double sb = A.sob[xc], ib = A.sib[xc];
+        const int64_t blo = P.cbase + A.pos[xc], bhi = blo + A.sz[xc];
+        int32_t pid_b = 0;
+        __syncthreads();   // everyone has read a[xc] before it changes
+        if (tid == 0) {
+            pid_b = atomicAdd(O.pid_ctr, 1);
+            sxx[0] = pid_b;
+            s_so = so_c - sb;
+            s_si = si_c - ib;
+            O.flags[0] = 1;
+            if (pair) {
+                A.sob[r] -= sb;
+                A.sib[r] -= ib;
+                mark_dirty(r, gflag, dirty, &s_ndirty, &s_overflow);
+                A.a[r] = r;
+                A.a[xc] = xc;
+                s_two = 0;
+            } else {
+                A.a[xc] = xc;
+                int32_t y = xpar;
+                for (;;) {
+                    A.sob[y] -= sb;
+                    A.sib[y] -= ib;
+                    mark_dirty(y, gflag, dirty, &s_ndirty, &s_overflow);
+                    if (y == r) break;
+                    y = A.a[y];
+                }
+            }
         }
-        P.giants[gid].splits.push_back(sp);
+        __syncthreads();
+        pid_b = sxx[0];
+        // re-mark the cut subtree
+        int cb = 0;
+        for (int64_t k = blo + tid; k < bhi; k += GB) {
+            const int32_t x = A.order[k];
+            if (A.gmark[x] == pid) {
+                A.gmark[x] = pid_b;
+                cb++;
+            }
+        }
+        const int bsize = block_sum_i(cb, si);
+        // edges between b and the rest: w_part of the rest side, x_w along the tree paths
+        {
+            const int lane = tid & 31, wid = tid >> 5;
+            for (int64_t k = blo + wid; k < bhi; k += GB / 32) {
+                const int32_t z = A.order[k];
+                if (A.gmark[z] != pid_b) continue;
+                const int32_t pz = A.pos[z];
+                for (int64_t e = A.uptr[z] + lane; e < A.uptr[z + 1]; e += 32) {
+                    const int32_t v = A.unbr[e];
+                    if (A.gmark[v] != pid) continue;
+                    const double u = A.uu[e];
+                    atomicAdd(&A.wpart[v], -u);
+                    mark_dirty(v, gflag, dirty, &s_ndirty, &s_overflow);
+                    int32_t y = v;
+                    for (;;) {
+                        const int32_t pa = A.pos[y];
+                        if (pz >= pa && pz < pa + A.sz[y]) break;
+                        atomicAdd(&A.xw[y], -u);
+                        mark_dirty(y, gflag, dirty, &s_ndirty, &s_overflow);
+                        y = A.a[y];
+                    }
+                    const int32_t lca = y;
+                    y = xpar;
+                    while (y != lca) {
+                        atomicAdd(&A.xw[y], -u);
+                        mark_dirty(y, gflag, dirty, &s_ndirty, &s_overflow);
+                        y = A.a[y];
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // ---- record the split and its child part
+        if (bsize <= O.small_part) {
+            // ordered compaction of b's members (DFS order) + in-part subtree sizes
+            __shared__ int s_off;
+            if (tid == 0) s_off = atomicAdd(O.alloc, bsize);
+            __syncthreads();
+            const int off = s_off;
+            int base = 0;
+            for (int64_t k0 = blo; k0 < bhi; k0 += GB) {
+                const int64_t k = k0 + tid;
+                const int32_t x = k < bhi ? A.order[k] : 0;
+                const int f = (k < bhi && A.gmark[x] == pid_b) ? 1 : 0;
+                // block exclusive scan of f
+                int inc = f;
+                const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += v;
+                }
+                if (lane == 31) si[wid] = inc;
+                __syncthreads();
+                if (wid == 0) {
+                    int v = si[lane];
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int w2 = __shfl_up_sync(0xffffffffu, v, o);
+                        if (lane >= o) v += w2;
+                    }
+                    si[lane] = v;   // inclusive warp totals
+                }
+                __syncthreads();
+                const int before = (wid ? si[wid - 1] : 0) + inc - f;
+                if (f) {
+                    O.pbuf2[off + base + before] = x;
+                    O.posb[off + base + before] = A.pos[x];
+                }
+                base += si[GB / 32 - 1];
+                __syncthreads();
+            }
+            for (int t = tid; t < bsize; t += GB) {
+                const int32_t y = O.pbuf2[off + t];
+                const int32_t endp = O.posb[off + t] + A.sz[y];
+                int lo2 = t, hi2 = bsize;
+                while (lo2 < hi2) {
+                    const int mid = (lo2 + hi2) >> 1;
+                    if (O.posb[off + mid] < endp) lo2 = mid + 1;
+                    else hi2 = mid;
+                }
+                O.psz[y] = lo2 - t;
+            }
+            if (tid == 0) {
+                const int di = atomicAdd(O.ndesc, 1);
+                PartDesc d;
+                d.off = off;
+                d.len = bsize;
+                d.from_layout = 0;
+                d.pad = 0;
+                O.desc[di] = d;
+                const int li = atomicAdd(O.nlog, 1);
+                O.log_pid[li] = pid;
+                O.log_seq[li] = seq;
+                O.log_gain[li] = gain;
+                O.log_kind[li] = 0;
+                O.log_child[li] = di;
+            }
+        } else if (tid == 0) {
+            const int ni = atomicAdd(O.nnext, 1);
+            O.nx_lo[ni] = blo;
+            O.nx_hi[ni] = bhi;
+            O.nx_pid[ni] = pid_b;
+            O.nx_root[ni] = xc;
+            O.nx_size[ni] = bsize;
+            const int li = atomicAdd(O.nlog, 1);
+            O.log_pid[li] = pid;
+            O.log_seq[li] = seq;
+            O.log_gain[li] = gain;
+            O.log_kind[li] = 1;
+            O.log_child[li] = pid_b;
+        }
+        seq++;
+        __syncthreads();
     }
-    P.unresolved += neg_left;
-    return gid;
+    // leave the flag arrays clean for the next part on this SM
+    __syncthreads();
+    for (int t = tid; t < min(s_ndirty, DIRTY_CAP); t += GB) gflag[dirty[t]] = 0;
+    for (int t = tid; t < s_nneg; t += GB) negflag[negl[t]] = 0;
 }
-
-void append_giant_gains(const PosCtx &P, int64_t gid, const std::vector<std::vector<double>> &sg,
-                        std::vector<double> &out) {
-    for (const Split &sp : P.giants[gid].splits) {
-        out.push_back(sp.gain);
-        if (sp.kind == 0) out.insert(out.end(), sg[sp.child].begin(), sg[sp.child].end());
-        else append_giant_gains(P, sp.child, sg, out);
-    }
-}
-
-}  // namespace
 
 static void launch_small(slm_ctx *ctx, PosArgs &A, const std::vector<PartDesc> &parts,
                          DBuf<PartDesc> &dparts, DBuf<int32_t> &ngains, DBuf<int32_t> &nunres,
@@ -942,21 +1030,20 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
         tot += hng1[i];
         un += hun1[i];
     }
-    // 2. giant communities: incremental grid executor; small cut subtrees -> batch 2
-    PosCtx P;
-    P.ctx = ctx;
-    P.G = &G;
-    P.F = &F;
-    P.m = m;
-    P.S.resize(1);
-    P.pbuf2 = pbuf2.p;
-    P.psz = psz.p;
-    std::vector<int64_t> giant_ids;
+    // 2. giant communities: one CTA per part with incremental state (k_giant_cta), in waves
+    //    (a cut subtree larger than SMALL_PART becomes a part of the next wave); small cut
+    //    subtrees are collected for a second warp-executor batch
+    std::vector<PartDesc> small2;
+    std::vector<int32_t> l_pid, l_seq, l_kind, l_child;
+    std::vector<double> l_gain;
+    std::vector<int32_t> giant_pid;   // per giant community (in bad-list order)
+    bool gchanged = false;
+    int64_t gunres = 0;
     if (!giant_comm.empty()) {
         xw.resize(n);
         sob.resize(n);
         sib.resize(n);
-        GiantArgs &GA = P.GA;
+        GiantArgs GA;
         GA.uptr = G.uptr.p;
         GA.unbr = G.unbr.p;
         GA.uu = G.uu.p;
@@ -975,23 +1062,187 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
         GA.m = m;
         GA.m2 = m * m;
         k_init_i32<<<grid_for(n, 256), 256, 0, s>>>(gmark.p, n, 0);
+        // pools
+        DBuf<int32_t> neg_pool, log_pid, log_seq, log_kind, log_child, cnt6, nx_pid, nx_root,
+            nx_size, posb;
+        DBuf<double> log_gain, vso, vsi, vdp, pso2, psi2, pdp2;
+        DBuf<int64_t> nx_lo, nx_hi;
+        DBuf<PartDesc> desc;
+        DBuf<uint8_t> gflag, negflag;
+        DBuf<unsigned long long> unres_d;
+        neg_pool.resize(n);
+        log_pid.resize(n);
+        log_seq.resize(n);
+        log_kind.resize(n);
+        log_child.resize(n);
+        log_gain.resize(n);
+        desc.resize(n);
+        nx_lo.resize(n);
+        nx_hi.resize(n);
+        nx_pid.resize(n);
+        nx_root.resize(n);
+        nx_size.resize(n);
+        posb.resize(n);
+        gflag.resize(n + 4);
+        negflag.resize(n + 4);
+        cnt6.resize(6);   // nlog, ndesc, alloc, nnext, pid_ctr, pad
+        unres_d.resize(1);
+        CUDA_TRY(cudaMemsetAsync(gflag.p, 0, n + 4, s));
+        CUDA_TRY(cudaMemsetAsync(negflag.p, 0, n + 4, s));
+        CUDA_TRY(cudaMemsetAsync(cnt6.p, 0, 24, s));
+        CUDA_TRY(cudaMemsetAsync(unres_d.p, 0, 8, s));
+        GOut O;
+        O.log_pid = log_pid.p;
+        O.log_seq = log_seq.p;
+        O.log_kind = log_kind.p;
+        O.log_child = log_child.p;
+        O.log_gain = log_gain.p;
+        O.nlog = cnt6.p + 0;
+        O.desc = desc.p;
+        O.ndesc = cnt6.p + 1;
+        O.pbuf2 = pbuf2.p;
+        O.posb = posb.p;
+        O.psz = psz.p;
+        O.alloc = cnt6.p + 2;
+        O.nx_lo = nx_lo.p;
+        O.nx_hi = nx_hi.p;
+        O.nx_pid = nx_pid.p;
+        O.nx_root = nx_root.p;
+        O.nx_size = nx_size.p;
+        O.nnext = cnt6.p + 3;
+        O.pid_ctr = cnt6.p + 4;
+        O.unresolved = unres_d.p;
+        O.flags = flags.p;
+        O.small_part = SMALL_PART;
+        // wave 0: the giant bad communities
+        std::vector<GPart> wave;
+        int32_t next_pid = 1;
+        int64_t neg_alloc = 0;
         for (int32_t c : giant_comm) {
-            const int64_t lo = hcptr[c], hi = hcptr[c + 1];
-            const int32_t pid = P.next_pid++;
-            k_g_mark<<<grid_for(hi - lo, 256), 256, 0, s>>>(F.order.p, lo, hi, pid, gmark.p);
-            int32_t root = 0;
-            CUDA_TRY(cudaMemcpyAsync(&root, F.order.p + lo, 4, cudaMemcpyDeviceToHost, s));
+            GPart gp;
+            gp.lo = hcptr[c];
+            gp.hi = hcptr[c + 1];
+            gp.cbase = hcptr[c];
+            gp.pid = next_pid++;
+            gp.neg_off = neg_alloc;
+            neg_alloc += gp.hi - gp.lo;
+            giant_pid.push_back(gp.pid);
+            k_g_mark<<<grid_for(gp.hi - gp.lo, 256), 256, 0, s>>>(F.order.p, gp.lo, gp.hi, gp.pid,
+                                                                   gmark.p);
+            CUDA_TRY(cudaMemcpyAsync(&gp.root, F.order.p + gp.lo, 4, cudaMemcpyDeviceToHost, s));
             CUDA_TRY(cudaStreamSynchronize(s));
-            giant_ids.push_back(giant_process(P, lo, lo, hi, pid, root));
+            wave.push_back(gp);
         }
-        tot += P.splits;
-        un += P.unresolved;
+        CUDA_TRY(cudaMemcpyAsync(cnt6.p + 4, &next_pid, 4, cudaMemcpyHostToDevice, s));
+        DBuf<GPart> dparts2;
+        DBuf<int32_t> dirty_pool;
+        while (!wave.empty()) {
+            // init pass of every part: w_part, LCA deposits, subtree sums, part totals
+            for (GPart &gp : wave) {
+                const int64_t lo = gp.lo, hi = gp.hi, N = hi - lo;
+                const unsigned GW = grid_for(N * 32, 256, 148LL * 32);
+                const unsigned GN = grid_for(N, 256);
+                k_g_wpart<<<GW, 256, 0, s>>>(GA, lo, hi, gp.pid);
+                k_g_lca<<<GW, 256, 0, s>>>(GA, lo, hi, gp.pid);
+                vso.resize(N + 1);
+                vsi.resize(N + 1);
+                vdp.resize(N + 1);
+                pso2.resize(N + 1);
+                psi2.resize(N + 1);
+                pdp2.resize(N + 1);
+                k_g_gather<<<GN, 256, 0, s>>>(GA, lo, hi, gp.pid, vso.p, vsi.p, vdp.p);
+                CUDA_TRY(cudaMemsetAsync(vso.p + N, 0, 8, s));
+                CUDA_TRY(cudaMemsetAsync(vsi.p + N, 0, 8, s));
+                CUDA_TRY(cudaMemsetAsync(vdp.p + N, 0, 8, s));
+                size_t tb = 0;
+                CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, vso.p, pso2.p, N + 1, s));
+                ctx->tmp.resize(tb);
+                CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx->tmp.p, tb, vso.p, pso2.p, N + 1, s));
+                CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx->tmp.p, tb, vsi.p, psi2.p, N + 1, s));
+                CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx->tmp.p, tb, vdp.p, pdp2.p, N + 1, s));
+                k_g_subsums<<<GN, 256, 0, s>>>(GA, lo, hi, gp.cbase, gp.pid, pso2.p, psi2.p, pdp2.p,
+                                                nullptr);
+                CUDA_TRY(cudaMemcpyAsync(&gp.so_c, pso2.p + N, 8, cudaMemcpyDeviceToHost, s));
+                CUDA_TRY(cudaMemcpyAsync(&gp.si_c, psi2.p + N, 8, cudaMemcpyDeviceToHost, s));
+                CUDA_TRY(cudaStreamSynchronize(s));
+            }
+            const int64_t np = (int64_t)wave.size();
+            dirty_pool.resize(np * DIRTY_CAP);
+            for (int64_t i = 0; i < np; i++) wave[i].dirty_off = i * DIRTY_CAP;
+            dparts2.resize(np);
+            CUDA_TRY(cudaMemcpyAsync(dparts2.p, wave.data(), np * sizeof(GPart),
+                                     cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaMemsetAsync(cnt6.p + 3, 0, 4, s));
+            k_giant_cta<<<(unsigned)np, GB, 0, s>>>(GA, dparts2.p, O, neg_pool.p, dirty_pool.p,
+                                                    gflag.p, negflag.p);
+            CUDA_TRY(cudaGetLastError());
+            int32_t nnext = 0;
+            CUDA_TRY(cudaMemcpyAsync(&nnext, cnt6.p + 3, 4, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            wave.clear();
+            if (nnext > 0) {
+                std::vector<int64_t> hlo(nnext), hhi(nnext);
+                std::vector<int32_t> hpid(nnext), hroot(nnext), hsize(nnext);
+                CUDA_TRY(cudaMemcpyAsync(hlo.data(), nx_lo.p, nnext * 8, cudaMemcpyDeviceToHost, s));
+                CUDA_TRY(cudaMemcpyAsync(hhi.data(), nx_hi.p, nnext * 8, cudaMemcpyDeviceToHost, s));
+                CUDA_TRY(cudaMemcpyAsync(hpid.data(), nx_pid.p, nnext * 4, cudaMemcpyDeviceToHost, s));
+                CUDA_TRY(cudaMemcpyAsync(hroot.data(), nx_root.p, nnext * 4, cudaMemcpyDeviceToHost, s));
+                CUDA_TRY(cudaMemcpyAsync(hsize.data(), nx_size.p, nnext * 4, cudaMemcpyDeviceToHost, s));
+                CUDA_TRY(cudaStreamSynchronize(s));
+                neg_alloc = 0;
+                for (int32_t i = 0; i < nnext; i++) {
+                    GPart gp;
+                    gp.lo = hlo[i];
+                    gp.hi = hhi[i];
+                    gp.cbase = hlo[i] - 0;   // slice start in community coordinates below
+                    gp.pid = hpid[i];
+                    gp.root = hroot[i];
+                    gp.neg_off = neg_alloc;
+                    neg_alloc += hsize[i];
+                    wave.push_back(gp);
+                }
+                // cbase: the community layout base of the part (pos[] is community-relative)
+                for (GPart &gp : wave) {
+                    int32_t pr = 0;
+                    CUDA_TRY(cudaMemcpyAsync(&pr, F.pos.p + gp.root, 4, cudaMemcpyDeviceToHost, s));
+                    CUDA_TRY(cudaStreamSynchronize(s));
+                    gp.cbase = gp.lo - pr;
+                }
+            }
+        }
+        int32_t hc[4];
+        unsigned long long hun = 0;
+        CUDA_TRY(cudaMemcpyAsync(hc, cnt6.p, 16, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(&hun, unres_d.p, 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        const int32_t nlog = hc[0], ndesc = hc[1];
+        gunres = (int64_t)hun;
+        gchanged = nlog > 0;
+        small2.resize(ndesc);
+        if (ndesc)
+            CUDA_TRY(cudaMemcpyAsync(small2.data(), desc.p, ndesc * sizeof(PartDesc),
+                                     cudaMemcpyDeviceToHost, s));
+        l_pid.resize(nlog);
+        l_seq.resize(nlog);
+        l_kind.resize(nlog);
+        l_child.resize(nlog);
+        l_gain.resize(nlog);
+        if (nlog) {
+            CUDA_TRY(cudaMemcpyAsync(l_pid.data(), log_pid.p, nlog * 4, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaMemcpyAsync(l_seq.data(), log_seq.p, nlog * 4, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaMemcpyAsync(l_kind.data(), log_kind.p, nlog * 4, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaMemcpyAsync(l_child.data(), log_child.p, nlog * 4, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaMemcpyAsync(l_gain.data(), log_gain.p, nlog * 8, cudaMemcpyDeviceToHost, s));
+        }
+        CUDA_TRY(cudaStreamSynchronize(s));
+        tot += nlog;
+        un += gunres;
         // small parts cut from giants (their own regions in pbuf2 / sstk2 / gbuf2)
         A.pbuf = pbuf2.p;
         A.sstk = sstk2.p;
         A.gains = gbuf2.p;
-        launch_small(ctx, A, P.small2, dparts, ngains, nunres, hng2, hun2);
-        for (size_t i = 0; i < P.small2.size(); i++) {
+        launch_small(ctx, A, small2, dparts, ngains, nunres, hng2, hun2);
+        for (size_t i = 0; i < small2.size(); i++) {
             tot += hng2[i];
             un += hun2[i];
         }
@@ -1003,24 +1254,39 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     SLM_REQUIRE(!hflags[1], SLM_EUNSUP, "assignment cycle longer than 2 in POSITIVE");
     *splits = tot;
     *unresolved = un;
-    *changed = hflags[0] || P.changed;
+    *changed = hflags[0] || gchanged;
     if (gains && tot > 0) {
         // the reference's order: communities ascending; within a community its LIFO stack,
         // i.e. a cut's gain, then the cut subtree's gains, then the rest's
         std::vector<double> hg1(n), hg2(n);
         CUDA_TRY(cudaMemcpyAsync(hg1.data(), gbuf.p, n * 8, cudaMemcpyDeviceToHost, s));
-        if (!P.small2.empty())
+        if (!small2.empty())
             CUDA_TRY(cudaMemcpyAsync(hg2.data(), gbuf2.p, n * 8, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
-        std::vector<std::vector<double>> sg2(P.small2.size());
-        for (size_t i = 0; i < P.small2.size(); i++)
-            sg2[i].assign(hg2.begin() + P.small2[i].off, hg2.begin() + P.small2[i].off + hng2[i]);
+        // split logs per giant part, in sequence order
+        std::map<int32_t, std::vector<std::pair<int32_t, size_t>>> by_pid;
+        for (size_t li = 0; li < l_pid.size(); li++) by_pid[l_pid[li]].push_back({l_seq[li], li});
+        for (auto &kv : by_pid) std::sort(kv.second.begin(), kv.second.end());
+        std::function<void(int32_t)> emit = [&](int32_t pid) {
+            auto it = by_pid.find(pid);
+            if (it == by_pid.end()) return;
+            for (auto &sl : it->second) {
+                const size_t li = sl.second;
+                gains->push_back(l_gain[li]);
+                if (l_kind[li] == 0) {
+                    const PartDesc &d = small2[l_child[li]];
+                    for (int k = 0; k < hng2[l_child[li]]; k++) gains->push_back(hg2[d.off + k]);
+                } else {
+                    emit(l_child[li]);
+                }
+            }
+        };
         for (int32_t i = 0; i < nbad; i++) {
             if (order_kind[i] >= 0) {
                 const PartDesc &d = small1[order_kind[i]];
                 for (int k = 0; k < hng1[order_kind[i]]; k++) gains->push_back(hg1[d.off + k]);
             } else {
-                append_giant_gains(P, giant_ids[-1 - order_kind[i]], sg2, *gains);
+                emit(giant_pid[-1 - order_kind[i]]);
             }
         }
     }
