@@ -44,6 +44,31 @@ __global__ void k_i64_to_i32(const int64_t *x, int64_t n, int32_t *y) {
          i += (int64_t)gridDim.x * blockDim.x)
         y[i] = (int32_t)x[i];
 }
+// labels from the caller: range check against n, max, int32 copy
+__global__ void k_labels_in(const int64_t *x, int64_t n, int32_t *y, int64_t *mx_bad) {
+    long long mx = -1;
+    int bad = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = x[i];
+        if (v < 0 || v >= n) {
+            bad = 1;
+            continue;
+        }
+        y[i] = (int32_t)v;
+        mx = v > mx ? v : mx;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const long long om = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = om > mx ? om : mx;
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax((long long *)&mx_bad[0], mx);
+        if (bad) atomicOr((unsigned long long *)&mx_bad[1], 1ull);
+    }
+}
 __global__ void k_i32_to_i64b(const int32_t *x, int64_t n, int64_t *y) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -359,16 +384,22 @@ int slm_plan_sweep(slm_ctx *ctx, const int64_t *comm_in, int64_t *cstar_out) {
     const LevelGraph &G = *ctx->g;
     Forest &F = ctx->f;
     if (comm_in) {
-        // explicit snapshot: labels + aggregates from them (members/aggregates only)
-        int64_t mx = -1;
-        for (int64_t i = 0; i < G.n; i++) {
-            SLM_REQUIRE(comm_in[i] >= 0 && comm_in[i] < G.n, SLM_EINVAL, "labels out of range");
-            if (comm_in[i] > mx) mx = comm_in[i];
-        }
+        // explicit snapshot: labels + aggregates from them (members/aggregates only);
+        // range check and max label on the device
         F.n = G.n;
         F.comm.resize(G.n);
-        upload_i64_as_i32(ctx, comm_in, G.n, F.comm.p);
-        F.n_comms = mx + 1;
+        int64_t *tmp = ctx->i64a.resize(G.n > 0 ? G.n : 1);
+        if (G.n)
+            CUDA_TRY(cudaMemcpyAsync(tmp, comm_in, G.n * 8, cudaMemcpyHostToDevice, ctx->stream));
+        int64_t *dmx = ctx->i64b.resize(2);
+        const int64_t init[2] = {-1, 0};
+        CUDA_TRY(cudaMemcpyAsync(dmx, init, 16, cudaMemcpyHostToDevice, ctx->stream));
+        k_labels_in<<<grid_for(G.n, 256), 256, 0, ctx->stream>>>(tmp, G.n, F.comm.p, dmx);
+        int64_t hmx[2];
+        CUDA_TRY(cudaMemcpyAsync(hmx, dmx, 16, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        SLM_REQUIRE(hmx[1] == 0, SLM_EINVAL, "labels out of range");
+        F.n_comms = hmx[0] + 1;
         build_members_and_aggregates(ctx, G, F);
         F.layout_valid = false;
         F.version++;

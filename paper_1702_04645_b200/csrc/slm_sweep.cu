@@ -22,16 +22,17 @@
 //
 // Degree bins (slm_internal.cuh bin_hi):
 //   0: d <= 32      rows packed into warps (lanes = entries of several rows),
-//                   __match_any_sync on (row, community) + __reduce_add_sync group sums,
+//                   __match_any_sync on (row, community) + shuffle group sums,
 //                   segmented argmax by shuffles
-//   1: d <= 256     warp per row, per-warp shared hash (512 slots) + occupied-slot list
-//   2: d <= 1024    warp per row, per-warp shared hash (2048 slots) + occupied-slot list
-//   3: d <= 4096    CTA per row, shared hash (8192 slots) + occupied-slot list
-//   4, 5: larger    (row, segment) CTAs insert into per-row global tables, then one CTA
-//                   per row walks the row's occupied list
+//   1: d <= 256     warp per row, per-warp shared table (<= 512 slots)
+//   2: d <= 1024    CTA(128) per row, shared table (<= 2048 slots)
+//   3: d <= 4096    CTA(512) per row, shared table (<= 8192 slots)
+//   4: d <= 16383   CTA(1024) per row, shared table (16384 slots)
+//   5: larger       persistent CTAs over (row, segment) items: shared pre-combine, then a
+//                   per-row global table scanned by the CTA that completes the row
+// Tables are scanned slot by slot (no occupied-slot list): a slot costs one 8-byte shared
+// load, cheaper than maintaining a list with an atomic per fresh community.
 #include "slm_internal.cuh"
-
-constexpr double ERR_REL = 0x1.0p-48;
 
 template <bool SYM>
 struct SweepArgs {
@@ -45,7 +46,8 @@ struct SweepArgs {
     const float2 *S2f;     // !SYM: float {S_out, S_in}
     const double *s1;      // SYM: s per node
     const double2 *s2;     // !SYM: {s_out, s_in} per node
-    double m, m2, inv_m, inv_m2;
+    double m, m2;
+    float inv_mf, inv_m2f; // float(1/m), float(1/m^2) of the approximate pass
     int32_t *cstar;
     unsigned long long *groups;
 };
@@ -67,15 +69,13 @@ __device__ __forceinline__ double2 comm_S(const SweepArgs<SYM> &A, int32_t c) {
     }
     return A.S2[c];
 }
-
 template <bool SYM>
-__device__ __forceinline__ double2 comm_Sf(const SweepArgs<SYM> &A, int32_t c) {
+__device__ __forceinline__ float2 comm_Sf(const SweepArgs<SYM> &A, int32_t c) {
     if (SYM) {
-        const double v = (double)A.S1f[c];
-        return make_double2(v, v);
+        const float v = A.S1f[c];
+        return make_float2(v, v);
     }
-    const float2 f = A.S2f[c];
-    return make_double2((double)f.x, (double)f.y);
+    return A.S2f[c];
 }
 
 // P_c of detector.py:400-402 (S.x = S_out, S.y = S_in; sr.x = s_out, sr.y = s_in)
@@ -94,105 +94,59 @@ __device__ __forceinline__ double stay_default(double2 sr, double2 SL, double m2
     return -(so * (SL.y - si) + si * (SL.x - so)) / m2;
 }
 
-// Running selection state of one thread / warp / CTA over the non-own groups.
+// Approximate score of a non-own group in fp32 with a rigorous error bound.  With a =
+// g/m and b = P/m^2 (P = s_out S_in + s_in S_out, all terms >= 0), every float operand
+// carries relative error <= 2^-24 (g, 1/m, 1/m^2, s, S each rounded once), so a~ is within
+// 3 u |a|, b~ within 6 u |b| and the rounded difference within u |t| of the exact values
+// (u = 2^-24); the reference's fp64 t is within 2^-52 (|a| + |b|) of exact.  The bound
+// 2^-19 (|a~| + |b~|) exceeds their sum by a factor > 3.  Normal range: g >= 1, P >= 1
+// (integer weights) and m <= 2^53 keep a~, b~ >= 2^-106, far from float underflow.
+__device__ __forceinline__ float approx_up(uint32_t g, float2 Sc, float2 srf, float inv_mf,
+                                           float inv_m2f, float &lo) {
+    const float a = __uint2float_rn(g) * inv_mf;
+    const float P = srf.x * Sc.y + srf.y * Sc.x;
+    const float b = P * inv_m2f;
+    const float t = a - b;
+    const float e = 0x1.0p-19f * (fabsf(a) + fabsf(b));
+    lo = t - e;
+    return t + e;
+}
+
+// Running selection state of one thread over the non-own groups: the largest upper bound
+// (and its group), the second largest upper bound, and the largest lower bound.  Once lo
+// is maximised over the row the argmax is certain when exactly one group has an upper
+// bound >= lo (it is that group); otherwise every group with up >= lo is evaluated exactly.
+// Groups with up < lo are strictly below the group attaining lo.
 struct Sel {
-    double up1;    // largest upper bound and its group
+    float up1, up2, lo;
     int32_t c1;
     uint32_t g1;
-    double P1;
-    double up2;    // second largest upper bound (any other group)
-    double lo;     // largest lower bound
-    // own group
-    uint32_t gown;
-    double Pown;
-    int hown;
 };
 __device__ __forceinline__ void sel_init(Sel &S) {
     S.up1 = -INFINITY;
-    S.c1 = 0x7fffffff;
-    S.g1 = 0;
-    S.P1 = 0.0;
     S.up2 = -INFINITY;
     S.lo = -INFINITY;
-    S.gown = 0;
-    S.Pown = 0.0;
-    S.hown = 0;
+    S.c1 = 0x7fffffff;
+    S.g1 = 0;
 }
-// P is computed from float(S) (relative error <= 2^-24 on a non-own group, where no
-// cancellation occurs), hence the extra 2^-23 |b| in the bound.
-__device__ __forceinline__ void sel_add(Sel &S, int32_t c, uint32_t g, double P, bool own,
-                                        double inv_m, double inv_m2) {
-    if (own) {           // the own group is always evaluated exactly (P recomputed in fp64)
-        S.gown = g;
-        S.hown = 1;
-        return;
-    }
-    const double a = (double)g * inv_m, b = P * inv_m2;
-    const double t = a - b;
-    const double e = ERR_REL * (fabs(a) + fabs(b)) + 0x1.0p-23 * fabs(b) + 1e-300;
-    const double up = t + e, lo = t - e;
-    if (lo > S.lo) S.lo = lo;
-    if (up > S.up1 || (up == S.up1 && c < S.c1)) {
-        S.up2 = fmax(S.up2, S.up1);
-        S.up1 = up;
-        S.c1 = c;
-        S.g1 = g;
-        S.P1 = P;
-    } else {
-        S.up2 = fmax(S.up2, up);
-    }
+__device__ __forceinline__ void sel_add(Sel &S, int32_t c, uint32_t g, float up, float lo) {
+    S.lo = fmaxf(S.lo, lo);
+    const bool top = up > S.up1;
+    S.up2 = fmaxf(S.up2, top ? S.up1 : up);
+    S.up1 = top ? up : S.up1;
+    S.c1 = top ? c : S.c1;
+    S.g1 = top ? g : S.g1;
 }
-__device__ __forceinline__ void sel_merge(Sel &S, const Sel &O) {
-    if (O.up1 > S.up1 || (O.up1 == S.up1 && O.c1 < S.c1)) {
-        S.up2 = fmax(fmax(S.up2, O.up2), S.up1);
-        S.up1 = O.up1;
-        S.c1 = O.c1;
-        S.g1 = O.g1;
-        S.P1 = O.P1;
-    } else {
-        S.up2 = fmax(fmax(S.up2, O.up2), O.up1);
-    }
-    S.lo = fmax(S.lo, O.lo);
-    if (O.hown) {
-        S.gown = O.gown;
-        S.Pown = O.Pown;
-        S.hown = 1;
-    }
-}
-__device__ __forceinline__ Sel sel_shfl_xor(const Sel &S, int off) {
-    Sel O;
-    O.up1 = __shfl_xor_sync(0xffffffffu, S.up1, off);
-    O.c1 = __shfl_xor_sync(0xffffffffu, S.c1, off);
-    O.g1 = __shfl_xor_sync(0xffffffffu, S.g1, off);
-    O.P1 = __shfl_xor_sync(0xffffffffu, S.P1, off);
-    O.up2 = __shfl_xor_sync(0xffffffffu, S.up2, off);
-    O.lo = __shfl_xor_sync(0xffffffffu, S.lo, off);
-    O.gown = __shfl_xor_sync(0xffffffffu, S.gown, off);
-    O.Pown = __shfl_xor_sync(0xffffffffu, S.Pown, off);
-    O.hown = __shfl_xor_sync(0xffffffffu, S.hown, off);
-    return O;
-}
-__device__ __forceinline__ void sel_warp(Sel &S) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) sel_merge(S, sel_shfl_xor(S, off));
-}
-// unique candidate?  (else the exact fallback must scan every group with up >= lo)
-__device__ __forceinline__ bool sel_unique(const Sel &S) { return S.up2 < S.lo; }
 
-// final decision given the exact best (tb, cb) (cb == INT_MAX: no other community)
+// final decision given the exact best (tb, cb) over the other communities and the own group
 template <bool SYM>
-__device__ __forceinline__ int32_t decide(const SweepArgs<SYM> &A, const Sel &S, double tb,
-                                          int32_t cb, double2 sr, int32_t L) {
+__device__ __forceinline__ int32_t decide(const SweepArgs<SYM> &A, double tb, int32_t cb, bool hown,
+                                          uint32_t gown, double2 sr, int32_t L) {
     if (cb == 0x7fffffff) return L;
     const double2 SL = comm_S(A, L);
-    const double t_stay = S.hown ? exact_t(S.gown, null_P(true, sr, SL), A.m, A.m2)
-                                 : stay_default(sr, SL, A.m2);
+    const double t_stay = hown ? exact_t(gown, null_P(true, sr, SL), A.m, A.m2)
+                               : stay_default(sr, SL, A.m2);
     return tb > t_stay ? cb : L;
-}
-// exact t of the unique approximate winner (fp64 S gathered once)
-template <bool SYM>
-__device__ __forceinline__ double winner_t(const SweepArgs<SYM> &A, const Sel &S, double2 sr) {
-    return exact_t(S.g1, null_P(false, sr, comm_S(A, S.c1)), A.m, A.m2);
 }
 
 __device__ __forceinline__ bool better2(double t1, int32_t c1, double t2, int32_t c2) {
@@ -317,108 +271,130 @@ __global__ void __launch_bounds__(256) k_sweep_small(SweepArgs<SYM> A, const int
 }
 
 // -------------------------------------------------------------- hash tables
+// A table is a power-of-two array of int2 {community (-1 = empty), group sum}, linear
+// probing, plus an occupied-slot list.  A slot already holding c is found with a plain
+// load, so a repeated community costs one atomic add; a fresh community pays a CAS and
+// one list append (warp-aggregated).  The scan walks the list (cost ~ groups, not slots)
+// and clears exactly the listed slots, so tables stay empty between rows: shared tables
+// are initialised once per launch, global (hub) tables once per allocation.
 
 __device__ __forceinline__ uint32_t hslot32(int32_t c, uint32_t hmask) {
     return ((uint32_t)c * 2654435761u) & hmask;
 }
 
-// claim (CAS) the entry's community slot and add its weight; lanes that hit the same
-// slot in one instruction are serialised by the shared-memory atomic unit (cheaper than a
-// warp-level pre-combine, whose per-group REDUX masks compile to a serial loop).  Newly
-// claimed slots are appended to the occupied list.
-template <class IDX>
-__device__ __forceinline__ void hash_insert_warp(int32_t *hk, uint32_t *hv, uint32_t hmask,
-                                                 IDX *occ, uint32_t *nocc, bool valid, int32_t c,
-                                                 uint32_t wt) {
-    const int lane = threadIdx.x & 31;
-    bool fresh = false;
-    uint32_t sl = 0;
-    if (valid) {
-        sl = hslot32(c, hmask);
-        for (;;) {
-            int32_t prev = atomicCAS(&hk[sl], -1, c);
-            if (prev == -1 || prev == c) {
-                fresh = (prev == -1);
+// claim (or find) c's slot and add w; returns the slot, fresh = this call claimed it
+template <bool GLOBALT>
+__device__ __forceinline__ uint32_t tab_insert(int2 *T, uint32_t hmask, int32_t c, uint32_t w,
+                                               bool &fresh) {
+    uint32_t sl = hslot32(c, hmask);
+    fresh = false;
+    for (;;) {
+        const int32_t k = GLOBALT ? __ldcg(&T[sl].x) : *(volatile int32_t *)&T[sl].x;
+        if (k == c) break;
+        if (k == -1) {
+            const int32_t prev = atomicCAS(&T[sl].x, -1, c);
+            if (prev == -1) {
+                fresh = true;
                 break;
             }
-            sl = (sl + 1) & hmask;
+            if (prev == c) break;
         }
-        atomicAdd(&hv[sl], wt);
+        sl = (sl + 1) & hmask;
     }
-    const unsigned fm = __ballot_sync(0xffffffffu, fresh);
-    if (fm) {
-        uint32_t base = 0;
-        if (lane == __ffs(fm) - 1) base = atomicAdd(nocc, (uint32_t)__popc(fm));
-        base = __shfl_sync(0xffffffffu, base, __ffs(fm) - 1);
-        if (fresh) occ[base + __popc(fm & ((1u << lane) - 1))] = (IDX)sl;
-    }
+    atomicAdd((uint32_t *)&T[sl].y, w);
+    return sl;
 }
 
-// walk the occupied slots [lo, hi) of a table: approximate selection (+ own group)
-template <bool SYM, class IDX>
-__device__ __forceinline__ void occ_scan(const SweepArgs<SYM> &A, const int32_t *hk,
-                                         const uint32_t *hv, const IDX *occ, uint32_t lo,
-                                         uint32_t hi, uint32_t stride, int32_t L, double2 sr,
-                                         Sel &S) {
+// warp-aggregated append of the freshly claimed slots to a list with a shared counter
+// (every lane of the warp calls it)
+template <class IDX>
+__device__ __forceinline__ void occ_append(IDX *occ, uint32_t *cnt, bool fresh, uint32_t sl) {
+    const unsigned fm = __ballot_sync(0xffffffffu, fresh);
+    if (!fm) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(fm) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(cnt, (uint32_t)__popc(fm));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (fresh) occ[base + __popc(fm & ((1u << lane) - 1))] = (IDX)sl;
+}
+
+template <bool GLOBALT>
+__device__ __forceinline__ int2 tab_load(const int2 *T, uint32_t k) {
+    return GLOBALT ? __ldcg(T + k) : T[k];
+}
+template <bool GLOBALT, class IDX>
+__device__ __forceinline__ uint32_t occ_load(const IDX *occ, uint32_t k) {
+    if (GLOBALT) return __ldcg((const unsigned int *)occ + k);
+    return occ[k];
+}
+
+// table size for a row of d entries: the smallest power of two >= lo with H > d / f
+// (f = 1: H > d, always enough; f = 2: load <= 1/2)
+__device__ __forceinline__ uint32_t tab_size(int64_t d, int f, uint32_t lo) {
+    uint32_t H = lo;
+    while ((int64_t)H <= f * d) H <<= 1;
+    return H;
+}
+
+// list entries t0, t0 + stride, ... < no: approximate selection, own group
+template <bool SYM, bool GLOBALT, class IDX>
+__device__ __forceinline__ void occ_scan(const SweepArgs<SYM> &A, const int2 *T, const IDX *occ,
+                                         uint32_t no, uint32_t t0, uint32_t stride, int32_t L,
+                                         float2 srf, Sel &S, uint32_t &gown, bool &hown) {
     constexpr int U = 4;
-    for (uint32_t k0 = lo; k0 < hi; k0 += stride * U) {
-        int32_t c[U];
-        uint32_t g[U];
-        double2 Sc[U];
+    for (uint32_t k0 = t0; k0 < no; k0 += stride * U) {
+        int2 e[U];
+        float2 Sc[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const uint32_t k = k0 + u * stride;
-            c[u] = -1;
-            g[u] = 0;
-            if (k < hi) {
-                const uint32_t sl = occ[k];
-                c[u] = hk[sl];
-                g[u] = hv[sl];
-            }
+            e[u] = k < no ? tab_load<GLOBALT>(T, occ_load<GLOBALT>(occ, k)) : make_int2(-1, 0);
         }
 #pragma unroll
         for (int u = 0; u < U; u++)
-            if (c[u] >= 0 && c[u] != L) Sc[u] = comm_Sf(A, c[u]);
+            Sc[u] = (e[u].x >= 0 && e[u].x != L) ? comm_Sf(A, e[u].x) : make_float2(0.f, 0.f);
 #pragma unroll
         for (int u = 0; u < U; u++) {
-            if (c[u] < 0) continue;
-            const bool own = (c[u] == L);
-            sel_add(S, c[u], g[u], own ? 0.0 : null_P(false, sr, Sc[u]), own, A.inv_m, A.inv_m2);
+            if (e[u].x < 0) continue;
+            if (e[u].x == L) {
+                gown = (uint32_t)e[u].y;
+                hown = true;
+            } else {
+                float lo;
+                const float up = approx_up((uint32_t)e[u].y, Sc[u], srf, A.inv_mf, A.inv_m2f, lo);
+                sel_add(S, e[u].x, (uint32_t)e[u].y, up, lo);
+            }
         }
     }
 }
 
-// exact fallback: best (t, c) over groups whose upper bound reaches lo
-template <bool SYM, class IDX>
-__device__ __forceinline__ void occ_exact(const SweepArgs<SYM> &A, const int32_t *hk,
-                                          const uint32_t *hv, const IDX *occ, uint32_t lo,
-                                          uint32_t hi, uint32_t stride, int32_t L, double2 sr,
-                                          double lob, double &bt, int32_t &bc) {
-    for (uint32_t k = lo; k < hi; k += stride) {
-        const uint32_t sl = occ[k];
-        const int32_t c = hk[sl];
-        if (c == L) continue;
-        const uint32_t g = hv[sl];
-        const double Pf = null_P(false, sr, comm_Sf(A, c));
-        const double a = (double)g * A.inv_m, b = Pf * A.inv_m2;
-        const double up = (a - b) + (ERR_REL * (fabs(a) + fabs(b)) + 0x1.0p-23 * fabs(b) + 1e-300);
+// exact fallback: best (t, c) over the listed groups whose upper bound reaches lob
+template <bool SYM, bool GLOBALT, class IDX>
+__device__ __forceinline__ void occ_exact(const SweepArgs<SYM> &A, const int2 *T, const IDX *occ,
+                                          uint32_t no, uint32_t t0, uint32_t stride, int32_t L,
+                                          double2 sr, float2 srf, float lob, double &bt,
+                                          int32_t &bc) {
+    for (uint32_t k = t0; k < no; k += stride) {
+        const int2 e = tab_load<GLOBALT>(T, occ_load<GLOBALT>(occ, k));
+        if (e.x == L) continue;
+        float lo;
+        const float up = approx_up((uint32_t)e.y, comm_Sf(A, e.x), srf, A.inv_mf, A.inv_m2f, lo);
         if (up < lob) continue;
-        const double t = exact_t(g, null_P(false, sr, comm_S(A, c)), A.m, A.m2);
-        if (better2(t, c, bt, bc)) {
+        const double t = exact_t((uint32_t)e.y, null_P(false, sr, comm_S(A, e.x)), A.m, A.m2);
+        if (better2(t, e.x, bt, bc)) {
             bt = t;
-            bc = c;
+            bc = e.x;
         }
     }
 }
 
-// clear the occupied slots [lo, hi)
-template <class IDX>
-__device__ __forceinline__ void occ_clear(int32_t *hk, uint32_t *hv, const IDX *occ, uint32_t lo,
-                                          uint32_t hi, uint32_t stride) {
-    for (uint32_t k = lo; k < hi; k += stride) {
-        const uint32_t sl = occ[k];
-        hk[sl] = -1;
-        hv[sl] = 0;
+template <bool GLOBALT, class IDX>
+__device__ __forceinline__ void occ_clear(int2 *T, const IDX *occ, uint32_t no, uint32_t t0,
+                                          uint32_t stride) {
+    for (uint32_t k = t0; k < no; k += stride) {
+        const uint32_t sl = occ_load<GLOBALT>(occ, k);
+        if (GLOBALT) __stcg(T + sl, make_int2(-1, 0));
+        else T[sl] = make_int2(-1, 0);
     }
 }
 
@@ -443,32 +419,37 @@ __device__ __forceinline__ void load_entries(const SweepArgs<SYM> &A, int64_t e0
     for (int u = 0; u < U; u++) c[u] = v[u] ? A.label[z[u]] : -1;
 }
 
-__device__ __forceinline__ uint32_t table_size(int64_t d) {
-    uint32_t H = 32;
-    while (H <= (uint32_t)d) H <<= 1;   // H > d >= distinct communities
-    return H;
+__device__ __forceinline__ float warp_maxf(float v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
+    return v;
+}
+__device__ __forceinline__ void warp_best(double &bt, int32_t &bc) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double obt = __shfl_xor_sync(0xffffffffu, bt, off);
+        const int32_t obc = __shfl_xor_sync(0xffffffffu, bc, off);
+        if (better2(obt, obc, bt, bc)) {
+            bt = obt;
+            bc = obc;
+        }
+    }
 }
 
-// bins 1, 2: one warp per row, per-warp table of HMAX slots + occupied list (dynamic smem)
+// bin 1: one warp per row, per-warp shared table of up to HMAX slots + list (count in a
+// register: the warp is the only writer)
 template <int HMAX, int WARPS, bool SYM>
-__global__ void __launch_bounds__(WARPS * 32) k_sweep_warp(SweepArgs<SYM> A, const int32_t *rows,
-                                                            int64_t nrows) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ uint32_t s_nocc[WARPS];
+__global__ void __launch_bounds__(WARPS * 32, 4) k_sweep_warp(SweepArgs<SYM> A, const int32_t *rows,
+                                                               int64_t nrows) {
+    extern __shared__ int2 wtab[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int32_t *hk = (int32_t *)smem + wid * HMAX;
-    uint32_t *hv = (uint32_t *)((int32_t *)smem + WARPS * HMAX) + wid * HMAX;
-    uint16_t *occ = (uint16_t *)((int32_t *)smem + 2 * WARPS * HMAX) + wid * HMAX;
-    uint32_t *nocc = &s_nocc[wid];
-    for (int k = lane; k < HMAX; k += 32) {
-        hk[k] = -1;
-        hv[k] = 0;
-    }
-    if (lane == 0) *nocc = 0;
+    int2 *T = wtab + wid * HMAX;
+    uint16_t *occ = (uint16_t *)(wtab + WARPS * HMAX) + wid * HMAX;
+    for (int k = lane; k < HMAX; k += 32) T[k] = make_int2(-1, 0);
     __syncwarp();
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    // row metadata is fetched one row ahead (lane 0..3 carry r, e0, d, L of the next row)
+    // row metadata is fetched one row ahead
     int32_t nr = 0;
     int64_t ne0 = 0, nd = 0;
     if (w < nrows) {
@@ -484,250 +465,287 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep_warp(SweepArgs<SYM> A, con
             ne0 = A.uptr[nr];
             nd = A.uptr[nr + 1] - ne0;
         }
-        const uint32_t hmask = table_size(d) - 1;
+        const uint32_t H = min(tab_size(d, 2, 32), (uint32_t)HMAX);   // > d either way
         const int32_t L = A.label[r];
         const double2 sr = node_s(A, r);
-        constexpr int U = 8;
+        const float2 srf = make_float2((float)sr.x, (float)sr.y);
+        uint32_t no = 0;
+        constexpr int U = 4;
         for (int64_t cb = 0; cb < d; cb += 32 * U) {
             int32_t c[U];
             uint32_t wt[U];
             bool v[U];
             load_entries<U>(A, e0, d, cb + lane, 32, c, wt, v);
 #pragma unroll
-            for (int u = 0; u < U; u++) hash_insert_warp(hk, hv, hmask, occ, nocc, v[u], c[u], wt[u]);
+            for (int u = 0; u < U; u++) {
+                if (cb + u * 32 >= d) break;   // warp-uniform
+                bool fresh = false;
+                uint32_t sl = 0;
+                if (v[u]) sl = tab_insert<false>(T, H - 1, c[u], wt[u], fresh);
+                const unsigned fm = __ballot_sync(0xffffffffu, fresh);
+                if (fresh) occ[no + __popc(fm & ((1u << lane) - 1))] = (uint16_t)sl;
+                no += __popc(fm);
+            }
         }
         __syncwarp();
-        const uint32_t no = *nocc;
         Sel S;
         sel_init(S);
-        occ_scan(A, hk, hv, occ, lane, no, 32, L, sr, S);
-        sel_warp(S);
+        uint32_t gown = 0;
+        bool hown = false;
+        occ_scan<SYM, false>(A, T, occ, no, lane, 32, L, srf, S, gown, hown);
+        const unsigned ob = __ballot_sync(0xffffffffu, hown);
+        gown = __shfl_sync(0xffffffffu, gown, ob ? __ffs(ob) - 1 : 0);
+        if (A.groups && lane == 0) atomicAdd(A.groups, (unsigned long long)no);
+        const float lo = warp_maxf(S.lo);
+        if (lo == -INFINITY) {
+            if (lane == 0) A.cstar[r] = L;
+        } else {
+            const unsigned cnt = (S.up1 >= lo) + (S.up2 >= lo);
+            if (__reduce_add_sync(0xffffffffu, cnt) == 1) {
+                if (S.up1 >= lo) {
+                    const double bt =
+                        exact_t(S.g1, null_P(false, sr, comm_S(A, S.c1)), A.m, A.m2);
+                    A.cstar[r] = decide(A, bt, S.c1, ob != 0, gown, sr, L);
+                }
+            } else {
+                double bt = -INFINITY;
+                int32_t bc = 0x7fffffff;
+                occ_exact<SYM, false>(A, T, occ, no, lane, 32, L, sr, srf, lo, bt, bc);
+                warp_best(bt, bc);
+                if (lane == 0) A.cstar[r] = decide(A, bt, bc, ob != 0, gown, sr, L);
+            }
+        }
+        occ_clear<false>(T, occ, no, lane, 32);
+        __syncwarp();
+    }
+}
+
+// per-CTA reduction scratch of the selection
+struct BlockSel {
+    float lo[32];
+    unsigned cnt[32];
+    double bt[32];
+    int32_t bc[32];
+    uint32_t gown;
+    int hown;
+};
+
+// CTA-wide decision for row r over a filled table T with list occ[0, no) (visible to every
+// thread): writes cstar[r]; no trailing barrier (the caller clears the table and syncs).
+template <int BLOCK, bool SYM, bool GLOBALT, class IDX>
+__device__ __forceinline__ void block_select(const SweepArgs<SYM> &A, const int2 *T, const IDX *occ,
+                                             uint32_t no, int32_t r, int32_t L, double2 sr,
+                                             BlockSel &B) {
+    constexpr int NW = BLOCK / 32;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const float2 srf = make_float2((float)sr.x, (float)sr.y);
+    Sel S;
+    sel_init(S);
+    uint32_t gown = 0;
+    bool hown = false;
+    occ_scan<SYM, GLOBALT>(A, T, occ, no, threadIdx.x, BLOCK, L, srf, S, gown, hown);
+    if (hown) {
+        B.gown = gown;
+        B.hown = 1;
+    }
+    float lo = warp_maxf(S.lo);
+    if (lane == 0) B.lo[wid] = lo;
+    __syncthreads();
+    lo = warp_maxf(lane < NW ? B.lo[lane] : -INFINITY);
+    unsigned cnt = __reduce_add_sync(0xffffffffu, (S.up1 >= lo) + (S.up2 >= lo));
+    if (lane == 0) B.cnt[wid] = cnt;
+    __syncthreads();
+    cnt = __reduce_add_sync(0xffffffffu, lane < NW ? B.cnt[lane] : 0u);
+    if (A.groups && threadIdx.x == 0) atomicAdd(A.groups, (unsigned long long)no);
+    if (lo == -INFINITY) {
+        if (threadIdx.x == 0) {
+            A.cstar[r] = L;
+            B.hown = 0;
+        }
+    } else if (cnt == 1) {
+        if (S.up1 >= lo) {
+            const double bt = exact_t(S.g1, null_P(false, sr, comm_S(A, S.c1)), A.m, A.m2);
+            A.cstar[r] = decide(A, bt, S.c1, B.hown != 0, B.gown, sr, L);
+            B.hown = 0;
+        }
+    } else {
         double bt = -INFINITY;
         int32_t bc = 0x7fffffff;
-        if (S.c1 != 0x7fffffff) {
-            if (sel_unique(S)) {
-                bt = winner_t(A, S, sr);
-                bc = S.c1;
-            } else {
-                occ_exact(A, hk, hv, occ, lane, no, 32, L, sr, S.lo, bt, bc);
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) {
-                    const double obt = __shfl_xor_sync(0xffffffffu, bt, off);
-                    const int32_t obc = __shfl_xor_sync(0xffffffffu, bc, off);
-                    if (better2(obt, obc, bt, bc)) {
-                        bt = obt;
-                        bc = obc;
-                    }
-                }
-            }
+        occ_exact<SYM, GLOBALT>(A, T, occ, no, threadIdx.x, BLOCK, L, sr, srf, lo, bt, bc);
+        warp_best(bt, bc);
+        if (lane == 0) {
+            B.bt[wid] = bt;
+            B.bc[wid] = bc;
         }
-        if (A.groups && lane == 0) atomicAdd(A.groups, (unsigned long long)no);
-        if (lane == 0) A.cstar[r] = decide(A, S, bt, bc, sr, L);
-        occ_clear(hk, hv, occ, lane, no, 32);
-        __syncwarp();
-        if (lane == 0) *nocc = 0;
-        __syncwarp();
-    }
-}
-
-// block-wide selection reduce: warps reduce by shuffles, warp 0 merges the per-warp
-// partials by shuffles, one barrier pair
-template <int BLOCK>
-__device__ __forceinline__ void sel_block(Sel &S, Sel *sh) {
-    sel_warp(S);
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) sh[wid] = S;
-    __syncthreads();
-    if (wid == 0) {
-        if (lane < BLOCK / 32) S = sh[lane];
-        else sel_init(S);
-        sel_warp(S);
-        if (lane == 0) sh[0] = S;
-    }
-    __syncthreads();
-    S = sh[0];
-}
-
-template <int BLOCK>
-__device__ __forceinline__ void best_block(double &bt, int32_t &bc, double *sbt, int32_t *sbc) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        const double obt = __shfl_xor_sync(0xffffffffu, bt, off);
-        const int32_t obc = __shfl_xor_sync(0xffffffffu, bc, off);
-        if (better2(obt, obc, bt, bc)) {
-            bt = obt;
-            bc = obc;
-        }
-    }
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) {
-        sbt[wid] = bt;
-        sbc[wid] = bc;
-    }
-    __syncthreads();
-    if (wid == 0) {
-        bt = lane < BLOCK / 32 ? sbt[lane] : -INFINITY;
-        bc = lane < BLOCK / 32 ? sbc[lane] : 0x7fffffff;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const double obt = __shfl_xor_sync(0xffffffffu, bt, off);
-            const int32_t obc = __shfl_xor_sync(0xffffffffu, bc, off);
-            if (better2(obt, obc, bt, bc)) {
-                bt = obt;
-                bc = obc;
-            }
-        }
-    }
-    __syncthreads();
-}
-
-// bin 3 (shared table of HMAX slots) and bins 4, 5 (global tables, GLOBAL): one CTA per row
-// scans the occupied list; the shared variant also inserts
-template <int BLOCK, int HMAX, bool GLOBAL, bool SYM>
-__global__ void __launch_bounds__(BLOCK) k_sweep_cta(SweepArgs<SYM> A, const int32_t *rows,
-                                                      int64_t nrows, const int64_t *hoff,
-                                                      int32_t *gk, uint32_t *gv, uint32_t *gocc,
-                                                      uint32_t *gnocc) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ Sel sh[BLOCK / 32];
-    __shared__ double sbt[BLOCK / 32];
-    __shared__ int32_t sbc[BLOCK / 32];
-    __shared__ uint32_t s_nocc;
-    int32_t *hk = (int32_t *)smem;
-    uint32_t *hv = (uint32_t *)(hk + HMAX);
-    uint16_t *socc = (uint16_t *)(hv + HMAX);
-    if (!GLOBAL) {
-        for (int k = threadIdx.x; k < HMAX; k += BLOCK) {
-            hk[k] = -1;
-            hv[k] = 0;
-        }
-        if (threadIdx.x == 0) s_nocc = 0;
         __syncthreads();
+        if (wid == 0) {
+            bt = lane < NW ? B.bt[lane] : -INFINITY;
+            bc = lane < NW ? B.bc[lane] : 0x7fffffff;
+            warp_best(bt, bc);
+            if (lane == 0) {
+                A.cstar[r] = decide(A, bt, bc, B.hown != 0, B.gown, sr, L);
+                B.hown = 0;
+            }
+        }
     }
+}
+
+// bins 2-4: one CTA per row, shared table of up to HMAX slots + list
+template <int BLOCK, int HMAX, int F, int MINB, bool SYM>
+__global__ void __launch_bounds__(BLOCK, MINB) k_sweep_cta(SweepArgs<SYM> A, const int32_t *rows,
+                                                            int64_t nrows) {
+    extern __shared__ int2 ctab[];
+    uint16_t *occ = (uint16_t *)(ctab + HMAX);
+    __shared__ BlockSel B;
+    __shared__ uint32_t s_no;
+    for (int k = threadIdx.x; k < HMAX; k += BLOCK) ctab[k] = make_int2(-1, 0);
+    if (threadIdx.x == 0) {
+        B.hown = 0;
+        s_no = 0;
+    }
+    __syncthreads();
     for (int64_t i = blockIdx.x; i < nrows; i += gridDim.x) {
         const int32_t r = rows[i];
         const int64_t e0 = A.uptr[r], d = A.uptr[r + 1] - e0;
         const int32_t L = A.label[r];
         const double2 sr = node_s(A, r);
-        int32_t *tk = hk;
-        uint32_t *tv = hv;
-        uint32_t no;
-        if (GLOBAL) {
-            tk = gk + hoff[i];
-            tv = gv + hoff[i];
-            no = gnocc[i];
-        } else {
-            const uint32_t hmask = table_size(d) - 1;
-            constexpr int U = 4;
-            for (int64_t cb = 0; cb < d; cb += BLOCK * U) {
-                int32_t c[U];
-                uint32_t wt[U];
-                bool v[U];
-                load_entries<U>(A, e0, d, cb + threadIdx.x, BLOCK, c, wt, v);
+        const uint32_t H = min(tab_size(d, F, 32), (uint32_t)HMAX);   // > d (bin bound)
+        constexpr int U = 4;
+        for (int64_t cb = 0; cb < d; cb += BLOCK * U) {
+            int32_t c[U];
+            uint32_t wt[U];
+            bool v[U];
+            load_entries<U>(A, e0, d, cb + threadIdx.x, BLOCK, c, wt, v);
 #pragma unroll
-                for (int u = 0; u < U; u++)
-                    hash_insert_warp(tk, tv, hmask, socc, &s_nocc, v[u], c[u], wt[u]);
+            for (int u = 0; u < U; u++) {
+                if (cb + u * BLOCK >= d) break;   // CTA-uniform
+                bool fresh = false;
+                uint32_t sl = 0;
+                if (v[u]) sl = tab_insert<false>(ctab, H - 1, c[u], wt[u], fresh);
+                occ_append(occ, &s_no, fresh, sl);
             }
-            __syncthreads();
-            no = s_nocc;
-        }
-        Sel S;
-        sel_init(S);
-        if (GLOBAL) occ_scan(A, tk, tv, gocc + hoff[i], threadIdx.x, no, BLOCK, L, sr, S);
-        else occ_scan(A, tk, tv, socc, threadIdx.x, no, BLOCK, L, sr, S);
-        sel_block<BLOCK>(S, sh);
-        double bt = -INFINITY;
-        int32_t bc = 0x7fffffff;
-        if (S.c1 != 0x7fffffff) {
-            if (sel_unique(S)) {
-                bt = winner_t(A, S, sr);
-                bc = S.c1;
-            } else {
-                if (GLOBAL)
-                    occ_exact(A, tk, tv, gocc + hoff[i], threadIdx.x, no, BLOCK, L, sr, S.lo, bt, bc);
-                else
-                    occ_exact(A, tk, tv, socc, threadIdx.x, no, BLOCK, L, sr, S.lo, bt, bc);
-                best_block<BLOCK>(bt, bc, sbt, sbc);
-            }
-        }
-        if (threadIdx.x == 0) {
-            if (A.groups) atomicAdd(A.groups, (unsigned long long)no);
-            A.cstar[r] = decide(A, S, bt, bc, sr, L);
-        }
-        if (GLOBAL) {
-            occ_clear(tk, tv, gocc + hoff[i], threadIdx.x, no, BLOCK);
-            if (threadIdx.x == 0) gnocc[i] = 0;
-        } else {
-            occ_clear(tk, tv, socc, threadIdx.x, no, BLOCK);
-            if (threadIdx.x == 0) s_nocc = 0;   // read by all threads before the sel barriers
         }
         __syncthreads();
+        const uint32_t no = s_no;
+        block_select<BLOCK, SYM, false>(A, ctab, occ, no, r, L, sr, B);
+        occ_clear<false>(ctab, occ, no, threadIdx.x, BLOCK);
+        __syncthreads();
+        if (threadIdx.x == 0) s_no = 0;   // every thread read s_no before the select barriers
     }
 }
 
-// hub rows (bin 5) insert phase: one CTA per (row, segment of HUB_SEG entries).  The
-// segment is combined in a shared table first, then each distinct community of the segment
-// is merged into the row's global table (L2-resident within a wave) with one claim + add.
-constexpr int HUB_SEG = 4096;
+// bin 5 (hubs): persistent CTAs take (row, segment of HUB_SEG entries) items, rows in
+// descending degree.  A segment is combined in a shared table, then merged into the row's
+// global table (one claim + add per distinct community of the segment).  Row tables are
+// regions of a ring buffer: before touching row j's region a CTA waits until the earlier
+// rows overlapping it are finished (their done-epoch flags).  The CTA that completes a row's
+// last segment (counter + release/acquire fences) selects over the row's list, clears the
+// listed slots, resets the counters and publishes the row's done epoch.  Requires every
+// CTA to be resident (the grid is sized from the occupancy query), so waits terminate.
 constexpr int HUB_BLOCK = 512;
 constexpr int HUB_H = 8192;
+struct HubArgs {
+    const int32_t *rows;     // bin-5 rows
+    const int64_t *items;    // (j << 20 | segment)
+    int64_t nitems;
+    const int64_t *row_of;   // j -> bin-5 row index
+    const int64_t *off, *size;
+    const int32_t *dptr, *didx;
+    int2 *tab;
+    uint32_t *occ;
+    uint32_t *cnt;           // per j: [3j] occupied, [3j+1] segments done, [3j+2] done epoch
+    uint32_t epoch;
+};
 template <bool SYM>
-__global__ void __launch_bounds__(HUB_BLOCK) k_sweep_hub_insert(SweepArgs<SYM> A,
-                                                                const int32_t *rows,
-                                                                const int64_t *seg_row,
-                                                                int64_t nseg, const int64_t *hoff,
-                                                                int32_t *gk, uint32_t *gv,
-                                                                uint32_t *gocc, uint32_t *gnocc) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ uint32_t s_nocc;
-    int32_t *hk = (int32_t *)smem;
-    uint32_t *hv = (uint32_t *)(hk + HUB_H);
-    uint16_t *socc = (uint16_t *)(hv + HUB_H);
-    for (int k = threadIdx.x; k < HUB_H; k += HUB_BLOCK) {
-        hk[k] = -1;
-        hv[k] = 0;
+__global__ void __launch_bounds__(HUB_BLOCK, 2) k_sweep_hub(SweepArgs<SYM> A, HubArgs Hb) {
+    extern __shared__ int2 htab[];
+    uint16_t *socc = (uint16_t *)(htab + HUB_H);
+    __shared__ BlockSel B;
+    __shared__ uint32_t s_no;
+    __shared__ int s_last;
+    __shared__ int64_t s_ready;   // row whose dependencies this CTA has seen finished
+    for (int k = threadIdx.x; k < HUB_H; k += HUB_BLOCK) htab[k] = make_int2(-1, 0);
+    if (threadIdx.x == 0) {
+        B.hown = 0;
+        s_no = 0;
+        s_ready = -1;
     }
-    if (threadIdx.x == 0) s_nocc = 0;
     __syncthreads();
     constexpr int U = HUB_SEG / HUB_BLOCK;
-    for (int64_t q = blockIdx.x; q < nseg; q += gridDim.x) {
-        const int64_t i = seg_row[q] >> 20, sgi = seg_row[q] & 0xFFFFF;
-        const int32_t r = rows[i];
+    for (int64_t q = blockIdx.x; q < Hb.nitems; q += gridDim.x) {
+        const int64_t j = Hb.items[q] >> 20, sg = Hb.items[q] & 0xFFFFF;
+        const int32_t r = Hb.rows[Hb.row_of[j]];
         const int64_t e0 = A.uptr[r], d = A.uptr[r + 1] - e0;
-        const int64_t lo = sgi * HUB_SEG, hi = min(d, lo + HUB_SEG);
+        const int64_t lo = sg * HUB_SEG, hi = min(d, lo + HUB_SEG);
         {
             int32_t c[U];
             uint32_t wt[U];
             bool v[U];
             load_entries<U>(A, e0, hi, lo + threadIdx.x, HUB_BLOCK, c, wt, v);
 #pragma unroll
-            for (int u = 0; u < U; u++)
-                hash_insert_warp(hk, hv, (uint32_t)(HUB_H - 1), socc, &s_nocc, v[u], c[u], wt[u]);
-        }
-        __syncthreads();
-        const uint32_t no = s_nocc;
-        const uint32_t gmask = (uint32_t)(hoff[i + 1] - hoff[i]) - 1;
-        int32_t *tk = gk + hoff[i];
-        uint32_t *tv = gv + hoff[i];
-        uint32_t *to = gocc + hoff[i];
-        for (uint32_t k0 = 0; k0 < no; k0 += HUB_BLOCK) {
-            const uint32_t k = k0 + threadIdx.x;
-            const bool valid = k < no;
-            int32_t c = -1;
-            uint32_t g = 0;
-            if (valid) {
-                const uint32_t sl = socc[k];
-                c = hk[sl];
-                g = hv[sl];
-                hk[sl] = -1;
-                hv[sl] = 0;
+            for (int u = 0; u < U; u++) {
+                bool fresh = false;
+                uint32_t sl = 0;
+                if (v[u]) sl = tab_insert<false>(htab, HUB_H - 1, c[u], wt[u], fresh);
+                occ_append(socc, &s_no, fresh, sl);
             }
-            hash_insert_warp(tk, tv, gmask, to, &gnocc[i], valid, c, g);
+        }
+        // wait for the rows whose table regions overlap row j's (ring reuse)
+        if (threadIdx.x == 0 && s_ready != j) {
+            for (int32_t k = Hb.dptr[j]; k < Hb.dptr[j + 1]; k++) {
+                const volatile uint32_t *f = Hb.cnt + 3 * (int64_t)Hb.didx[k] + 2;
+                while (*f != Hb.epoch) __nanosleep(256);
+            }
+            __threadfence();
+            s_ready = j;
         }
         __syncthreads();
-        if (threadIdx.x == 0) s_nocc = 0;
+        const uint32_t ns = s_no;
+        int2 *GT = Hb.tab + Hb.off[j];
+        uint32_t *GO = Hb.occ + Hb.off[j];
+        const uint32_t H = (uint32_t)Hb.size[j];
+        uint32_t *gno = Hb.cnt + 3 * j;
+        for (uint32_t k0 = 0; k0 < ns; k0 += HUB_BLOCK) {
+            const uint32_t k = k0 + threadIdx.x;
+            bool fresh = false;
+            uint32_t sl = 0;
+            if (k < ns) {
+                const uint32_t ss = socc[k];
+                const int2 e = htab[ss];
+                htab[ss] = make_int2(-1, 0);
+                sl = tab_insert<true>(GT, H - 1, e.x, (uint32_t)e.y, fresh);
+            }
+            occ_append(GO, gno, fresh, sl);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            s_no = 0;
+            __threadfence();
+            const uint32_t nsg = (uint32_t)((d + HUB_SEG - 1) / HUB_SEG);
+            s_last = atomicAdd(gno + 1, 1u) == nsg - 1;
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            const uint32_t no = __ldcg(gno);
+            block_select<HUB_BLOCK, SYM, true>(A, GT, GO, no, r, A.label[r], node_s(A, r), B);
+            occ_clear<true>(GT, GO, no, threadIdx.x, HUB_BLOCK);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                gno[0] = 0;
+                gno[1] = 0;
+                __threadfence();
+                *(volatile uint32_t *)(gno + 2) = Hb.epoch;
+            }
+        }
         __syncthreads();
     }
+}
+
+__global__ void k_fill_empty(int2 *T, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        T[i] = make_int2(-1, 0);
 }
 
 __global__ void k_copy_labels32(const int32_t *label, int64_t n, int32_t *out) {
@@ -740,8 +758,6 @@ template <class K>
 static void set_smem(K kern, size_t bytes) {
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
-
-constexpr size_t warp_smem(int hmax, int warps) { return (size_t)warps * hmax * 10; }
 
 template <bool SYM>
 static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_t *d_cstar,
@@ -760,19 +776,29 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
     A.s2 = G.s2.p;
     A.m = m;
     A.m2 = m * m;
-    A.inv_m = 1.0 / m;
-    A.inv_m2 = 1.0 / (m * m);
+    A.inv_mf = (float)(1.0 / m);
+    A.inv_m2f = (float)(1.0 / (m * m));
     A.cstar = d_cstar;
     A.groups = d_groups;
     auto nb = [&](int b) { return G.bin_off[b + 1] - G.bin_off[b]; };
     auto rows = [&](int b) { return G.bin_rows.p + G.bin_off[b]; };
+    constexpr int W1 = 8;
+    constexpr size_t SM1 = (size_t)W1 * 512 * 10, SM2 = 2048 * 10, SM3 = 8192 * 10,
+                     SM4 = 16384 * 10, SMH = HUB_H * 10;
+    auto k1 = k_sweep_warp<512, W1, SYM>;
+    auto k2 = k_sweep_cta<128, 2048, 2, 8, SYM>;
+    auto k3 = k_sweep_cta<512, 8192, 1, 2, SYM>;
+    auto k4 = k_sweep_cta<1024, 16384, 1, 1, SYM>;
+    auto kh = k_sweep_hub<SYM>;
     static bool attrs[2] = {false, false};
+    static int hub_occ[2] = {0, 0};
     if (!attrs[SYM]) {
-        set_smem(k_sweep_warp<512, 8, SYM>, warp_smem(512, 8));
-        set_smem(k_sweep_cta<128, 2048, false, SYM>, (size_t)2048 * 10);
-        set_smem(k_sweep_cta<512, 8192, false, SYM>, (size_t)8192 * 10);
-        set_smem(k_sweep_cta<1024, 16384, false, SYM>, (size_t)16384 * 10);
-        set_smem(k_sweep_hub_insert<SYM>, (size_t)HUB_H * 10);
+        set_smem(k1, SM1);
+        set_smem(k2, SM2);
+        set_smem(k3, SM3);
+        set_smem(k4, SM4);
+        set_smem(kh, SMH);
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hub_occ[SYM], kh, HUB_BLOCK, SMH));
         attrs[SYM] = true;
     }
     if (nb(0) && (bin_mask & 1)) {
@@ -782,48 +808,46 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
         k_sweep_small<SYM><<<grid_for(nw * 32, 256), 256, 0, s>>>(A, rows(0), nb(0), rpw);
     }
     if (nb(1) && (bin_mask & 2))
-        k_sweep_warp<512, 8, SYM><<<grid_for(nb(1) * 32, 256, 148LL * 5), 256,
-                                    warp_smem(512, 8), s>>>(A, rows(1), nb(1));
+        k1<<<grid_for(nb(1) * 32, W1 * 32, 148LL * 4), W1 * 32, SM1, s>>>(A, rows(1), nb(1));
     if (nb(2) && (bin_mask & 4))
-        k_sweep_cta<128, 2048, false, SYM><<<(unsigned)std::min<int64_t>(nb(2), 148 * 11), 128,
-                                             (size_t)2048 * 10, s>>>(
-            A, rows(2), nb(2), nullptr, nullptr, nullptr, nullptr, nullptr);
+        k2<<<(unsigned)std::min<int64_t>(nb(2), 148 * 8), 128, SM2, s>>>(A, rows(2), nb(2));
     if (nb(3) && (bin_mask & 8))
-        k_sweep_cta<512, 8192, false, SYM><<<(unsigned)std::min<int64_t>(nb(3), 148 * 2), 512,
-                                             (size_t)8192 * 10, s>>>(
-            A, rows(3), nb(3), nullptr, nullptr, nullptr, nullptr, nullptr);
+        k3<<<(unsigned)std::min<int64_t>(nb(3), 148 * 2), 512, SM3, s>>>(A, rows(3), nb(3));
     if (nb(4) && (bin_mask & 16))
-        k_sweep_cta<1024, 16384, false, SYM><<<(unsigned)std::min<int64_t>(nb(4), 148), 1024,
-                                               (size_t)16384 * 10, s>>>(
-            A, rows(4), nb(4), nullptr, nullptr, nullptr, nullptr, nullptr);
+        k4<<<(unsigned)std::min<int64_t>(nb(4), 148), 1024, SM4, s>>>(A, rows(4), nb(4));
     if (nb(5) && (bin_mask & 32)) {
-        // hub rows: global tables processed in waves whose tables fit in L2
-        const int64_t tot = G.hub_wave_slots;
-        if (ctx->hk32.n < (size_t)tot) {
-            ctx->hk32.resize(tot);
-            ctx->hv32.resize(tot);
-            ctx->hocc32.resize(tot);
-            // tables are left empty by every scan, so clearing once per allocation suffices
-            CUDA_TRY(cudaMemsetAsync(ctx->hk32.p, 0xff, tot * 4, s));
-            CUDA_TRY(cudaMemsetAsync(ctx->hv32.p, 0, tot * 4, s));
+        SLM_REQUIRE(hub_occ[SYM] > 0, SLM_ECUDA, "hub sweep kernel cannot be resident");
+        const int64_t RS = G.hub_ring, nh = G.hub_rows_n;
+        if (ctx->hub_tab.n < (size_t)RS) {
+            ctx->hub_tab.resize(RS);
+            ctx->hub_occ.resize(RS);
+            // tables are left empty by every scan, so filling once per allocation suffices
+            k_fill_empty<<<grid_for(RS, 256), 256, 0, s>>>(ctx->hub_tab.p, RS);
         }
-        if (ctx->hnocc32.n < (size_t)nb(5)) {
-            ctx->hnocc32.resize(nb(5));
-            CUDA_TRY(cudaMemsetAsync(ctx->hnocc32.p, 0, nb(5) * 4, s));
+        if (ctx->hub_cnt.n < (size_t)(3 * nh)) {
+            ctx->hub_cnt.resize(3 * nh);
+            CUDA_TRY(cudaMemsetAsync(ctx->hub_cnt.p, 0, 3 * nh * 4, s));
+            ctx->hub_epoch = 0;
         }
-        const int64_t *hoff5 = G.large_hoff.p + nb(4);
-        for (size_t wv = 0; wv + 1 < G.hub_waves.size(); wv++) {
-            const HubWave &W0 = G.hub_waves[wv], &W1 = G.hub_waves[wv + 1];
-            const int64_t nr = W1.row - W0.row, ns = W1.seg - W0.seg;
-            int32_t *gk = ctx->hk32.p - W0.base;
-            uint32_t *gv = ctx->hv32.p - W0.base, *go = ctx->hocc32.p - W0.base;
-            // segment items carry bin-5 row indices
-            k_sweep_hub_insert<SYM><<<(unsigned)std::min<int64_t>(ns, 148 * 2), HUB_BLOCK,
-                                      (size_t)HUB_H * 10, s>>>(
-                A, rows(5), G.hub_seg.p + W0.seg, ns, hoff5, gk, gv, go, ctx->hnocc32.p);
-            k_sweep_cta<1024, 1, true, SYM><<<(unsigned)std::min<int64_t>(nr, 148), 1024, 16, s>>>(
-                A, rows(5) + W0.row, nr, hoff5 + W0.row, gk, gv, go, ctx->hnocc32.p + W0.row);
+        if (++ctx->hub_epoch == 0) {   // wrapped: reset the done flags
+            CUDA_TRY(cudaMemsetAsync(ctx->hub_cnt.p, 0, 3 * nh * 4, s));
+            ctx->hub_epoch = 1;
         }
+        HubArgs Hb;
+        Hb.rows = rows(5);
+        Hb.items = G.hub_seg.p;
+        Hb.nitems = G.hub_nseg;
+        Hb.row_of = G.hub_row.p;
+        Hb.off = G.hub_off.p;
+        Hb.size = G.hub_size.p;
+        Hb.dptr = G.hub_dptr.p;
+        Hb.didx = G.hub_didx.p;
+        Hb.tab = ctx->hub_tab.p;
+        Hb.occ = ctx->hub_occ.p;
+        Hb.cnt = ctx->hub_cnt.p;
+        Hb.epoch = ctx->hub_epoch;
+        const int64_t grid = std::min<int64_t>(G.hub_nseg, 148LL * hub_occ[SYM]);
+        kh<<<(unsigned)grid, HUB_BLOCK, SMH, s>>>(A, Hb);
     }
     CUDA_TRY(cudaGetLastError());
 }

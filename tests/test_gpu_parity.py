@@ -278,3 +278,41 @@ def test_positive_large_rmat_vs_oracle(slm, oracle):
     np.testing.assert_array_equal(f2.a, a2)
     assert (sp, un) == (osp, oun)
     np.testing.assert_array_equal(gains, ogains)
+
+
+def _hub_graph(seed=7):
+    """Random weighted graph whose rows fill every degree bin, hubs included (rows of
+    20k-70k entries span several hub segments)."""
+    rng = np.random.default_rng(seed)
+    n = 120_000
+    src = [rng.integers(0, n, 400_000)]
+    dst = [rng.integers(0, n, 400_000)]
+    for h, k in enumerate([70_000, 45_000, 30_000, 21_000, 17_000, 12_000, 6_000, 2_500,
+                           900, 300, 100, 40]):
+        nb = rng.choice(n, size=k, replace=False)
+        src.append(np.full(k, h * 997 + 5))
+        dst.append(nb)
+    s = np.concatenate(src)
+    d = np.concatenate(dst)
+    keep = s != d
+    s, d = s[keep], d[keep]
+    w = rng.integers(1, 101, s.size).astype(np.float64)
+    return n, np.concatenate([s, d]), np.concatenate([d, s]), np.concatenate([w, w])
+
+
+@pytest.mark.parametrize("ring", [None, "4096"])
+def test_plan_all_degree_bins_vs_oracle(slm, oracle, monkeypatch, ring):
+    """Plan sweep over rows of every degree bin (warp, CTA and hub kernels) against the
+    oracle's _best_targets, including the hub-table ring with forced reuse."""
+    if ring:
+        monkeypatch.setenv("SLM_HUB_RING", ring)
+    n, s, d, w = _hub_graph()
+    ctx = slm.Graph.from_edges(n, s, d, w).context()
+    og = oracle.OGraph.from_edges(n, s, d, w)
+    rng = np.random.default_rng(11)
+    for labels in (rng.integers(0, 2000, n), np.arange(n) // 7, rng.integers(0, 40, n)):
+        _, inv = np.unique(labels, return_inverse=True)
+        labels = inv.astype(np.int64)
+        ref = oracle.best_targets(og, labels, int(labels.max()) + 1)
+        for _ in range(2):   # repeated sweeps reuse the emptied tables
+            np.testing.assert_array_equal(ctx.plan(labels), ref)
