@@ -355,10 +355,9 @@ static void build_bins(slm_ctx *ctx, LevelGraph &G) {
         }
         hoff[nl] = acc;
         G.large_hash_total = acc;
-        // hub rows (bin 5) for the integer sweep: processing order j = descending degree;
-        // work items (j << 20 | segment) of HUB_SEG entries; each row's table (pow2 > d
-        // slots) is a region of a ring buffer reused row after row (so it stays in L2);
-        // row j waits for the earlier rows whose regions it overlaps (hub_dep CSR).
+        // hub rows (bin 5) for the integer sweep: processing order j = descending degree,
+        // work items (j << 20 | segment) of HUB_SEG entries; row j's global table (pow2 > d
+        // slots) and list are its own region of the hub arena
         const int64_t nb4 = G.bin_off[5] - G.bin_off[4];
         const int64_t nh = nl - nb4;
         std::vector<int64_t> hub(nh);
@@ -366,66 +365,29 @@ static void build_bins(slm_ctx *ctx, LevelGraph &G) {
         auto deg5 = [&](int64_t j) { return up[rows[b0 + nb4 + j] + 1] - up[rows[b0 + nb4 + j]]; };
         std::stable_sort(hub.begin(), hub.end(),
                          [&](int64_t x, int64_t y) { return deg5(x) > deg5(y); });
-        std::vector<int64_t> segs, hrow(nh), hoffr(nh + 1);
-        std::vector<int32_t> dptr(nh + 1, 0), didx;
-        int64_t hmax = 64;
-        for (int64_t j = 0; j < nh; j++) {
-            int64_t H = 64;
-            while (H <= deg5(hub[j])) H <<= 1;
-            hmax = std::max(hmax, H);
-        }
-        const char *ring_env = getenv("SLM_HUB_RING");   // test hook: force ring reuse
-        const int64_t ring_min = ring_env ? std::max<int64_t>(64, atoll(ring_env)) : HUB_RING_MIN;
-        const int64_t RS = std::max<int64_t>(ring_min, 2 * hmax);
+        std::vector<int64_t> segs, hoffr(nh), hsz(nh);
         int64_t cur = 0;
-        std::vector<int64_t> lo_(nh), hi_(nh);
         for (int64_t j = 0; j < nh; j++) {
             const int64_t d = deg5(hub[j]);
             int64_t H = 64;
             while (H <= d) H <<= 1;
-            if (cur + H > RS) cur = 0;
-            lo_[j] = cur;
-            hi_[j] = cur + H;
+            hoffr[j] = cur;
+            hsz[j] = H;
             cur += H;
-            hrow[j] = hub[j];
-            hoffr[j] = lo_[j];
-            // earlier rows whose regions overlap [lo, hi) must be finished first; the scan
-            // back stops once the overlapping rows cover the region (each of them waited
-            // for the older rows below it)
-            std::vector<std::pair<int64_t, int64_t>> cov;
-            for (int64_t k = j - 1; k >= 0; k--) {
-                if (!(lo_[k] < hi_[j] && lo_[j] < hi_[k])) continue;
-                didx.push_back((int32_t)k);
-                cov.push_back({std::max(lo_[k], lo_[j]), std::min(hi_[k], hi_[j])});
-                std::sort(cov.begin(), cov.end());
-                int64_t reach = lo_[j];
-                for (auto &iv : cov)
-                    if (iv.first <= reach) reach = std::max(reach, iv.second);
-                if (reach >= hi_[j]) break;
-            }
-            dptr[j + 1] = (int32_t)didx.size();
             for (int64_t q = 0; q * HUB_SEG < d; q++) segs.push_back((j << 20) | q);
         }
-        hoffr[nh] = 0;
         G.hub_rows_n = nh;
-        G.hub_ring = RS;
+        G.hub_ring = cur;
         G.hub_nseg = (int64_t)segs.size();
         if (nh) {
-            std::vector<int64_t> hsz(nh);
-            for (int64_t j = 0; j < nh; j++) hsz[j] = hi_[j] - lo_[j];
             G.hub_seg.resize(segs.size());
             G.hub_row.resize(nh);
             G.hub_off.resize(nh);
             G.hub_size.resize(nh);
-            G.hub_dptr.resize(nh + 1);
-            G.hub_didx.resize(std::max<size_t>(1, didx.size()));
             CUDA_TRY(cudaMemcpyAsync(G.hub_seg.p, segs.data(), segs.size() * 8, cudaMemcpyHostToDevice, s));
-            CUDA_TRY(cudaMemcpyAsync(G.hub_row.p, hrow.data(), nh * 8, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaMemcpyAsync(G.hub_row.p, hub.data(), nh * 8, cudaMemcpyHostToDevice, s));
             CUDA_TRY(cudaMemcpyAsync(G.hub_off.p, hoffr.data(), nh * 8, cudaMemcpyHostToDevice, s));
             CUDA_TRY(cudaMemcpyAsync(G.hub_size.p, hsz.data(), nh * 8, cudaMemcpyHostToDevice, s));
-            CUDA_TRY(cudaMemcpyAsync(G.hub_dptr.p, dptr.data(), (nh + 1) * 4, cudaMemcpyHostToDevice, s));
-            if (!didx.empty())
-                CUDA_TRY(cudaMemcpyAsync(G.hub_didx.p, didx.data(), didx.size() * 4, cudaMemcpyHostToDevice, s));
             CUDA_TRY(cudaStreamSynchronize(s));
         }
         G.large_hoff.resize(nl + 1);

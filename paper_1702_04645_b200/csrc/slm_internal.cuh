@@ -83,7 +83,6 @@ constexpr int SMALL_MAX = 32;     // warp lanes = entries (packed rows)
 constexpr int MID_MAX = 4096;     // generic path: CTA-per-row shared-memory hash up to here
 
 constexpr int HUB_SEG = 4096;     // entries per hub-row work item of the integer sweep
-constexpr int64_t HUB_RING_MIN = 4 << 20;   // slots of the hub-table ring (32 MB + occ lists)
 
 // Canonical directed CSR + neighbour union + strengths of one hierarchy level
 // (graph.py:63-175, 257-263).  Node ids int32, entry offsets int64.
@@ -109,11 +108,9 @@ struct LevelGraph {
     DBuf<int64_t> large_hoff;  // per row with d > MID_MAX (bins 4, 5): global hash offset
     int64_t large_hash_total = 0;
     // bin-5 (hub) rows of the integer sweep, in processing order j (descending degree):
-    // work items (j << 20 | segment); bin-5 row index, ring-buffer table offset and size of
-    // row j; CSR of the earlier rows whose table regions row j overlaps
+    // work items (j << 20 | segment); bin-5 row index, table offset and size of row j
     DBuf<int64_t> hub_seg, hub_row, hub_off, hub_size;
-    DBuf<int32_t> hub_dptr, hub_didx;
-    int64_t hub_nseg = 0, hub_rows_n = 0, hub_ring = 0;
+    int64_t hub_nseg = 0, hub_rows_n = 0, hub_ring = 0;   // hub_ring: arena slots
     int32_t max_deg = 0;
 };
 
@@ -162,10 +159,9 @@ struct slm_ctx {
     DBuf<uint64_t> u64a, u64b;
     DBuf<double> hash_vals;
     DBuf<int32_t> hash_keys;
-    DBuf<int2> hub_tab;          // hub-table ring {community, sum} of the integer sweep (kept empty)
-    DBuf<uint32_t> hub_occ;      // occupied-slot lists (same ring offsets)
-    DBuf<uint32_t> hub_cnt;      // per hub row: {occupied count, segments done, done epoch}
-    uint32_t hub_epoch = 0;
+    DBuf<int2> hub_tab;          // hub tables {community, sum} of the integer sweep (kept empty)
+    DBuf<uint32_t> hub_occ;      // occupied-slot lists (same offsets)
+    DBuf<uint32_t> hub_cnt;      // per hub row: list length (kept zero between sweeps)
     int32_t *h_flag = nullptr;   // pinned host scalars
     int64_t *h_i64 = nullptr;
     double *h_f64 = nullptr;

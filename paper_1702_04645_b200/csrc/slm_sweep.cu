@@ -28,11 +28,13 @@
 //   2: d <= 1024    CTA(128) per row, shared table (<= 2048 slots)
 //   3: d <= 4096    CTA(512) per row, shared table (<= 8192 slots)
 //   4: d <= 16383   CTA(1024) per row, shared table (16384 slots)
-//   5: larger       persistent CTAs over (row, segment) items: shared pre-combine, then a
-//                   per-row global table scanned by the CTA that completes the row
+//   5: larger       CTAs over (row, segment) items: shared pre-combine merged into a per-row
+//                   global table; then one CTA per row selects over the row's list
 // Tables are scanned slot by slot (no occupied-slot list): a slot costs one 8-byte shared
 // load, cheaper than maintaining a list with an atomic per fresh community.
 #include "slm_internal.cuh"
+#include <algorithm>
+#include <vector>
 
 template <bool SYM>
 struct SweepArgs {
@@ -50,6 +52,7 @@ struct SweepArgs {
     float inv_mf, inv_m2f; // float(1/m), float(1/m^2) of the approximate pass
     int32_t *cstar;
     unsigned long long *groups;
+    unsigned long long *stats;   // development counters (SLM_SWEEP_STATS): fallback rows / groups
 };
 
 // per-node and per-community strength views
@@ -508,6 +511,10 @@ __global__ void __launch_bounds__(WARPS * 32, 4) k_sweep_warp(SweepArgs<SYM> A, 
                     A.cstar[r] = decide(A, bt, S.c1, ob != 0, gown, sr, L);
                 }
             } else {
+                if (A.stats && lane == 0) {
+                    atomicAdd(A.stats + 2, 1ull);
+                    atomicAdd(A.stats + 3, (unsigned long long)no);
+                }
                 double bt = -INFINITY;
                 int32_t bc = 0x7fffffff;
                 occ_exact<SYM, false>(A, T, occ, no, lane, 32, L, sr, srf, lo, bt, bc);
@@ -569,6 +576,10 @@ __device__ __forceinline__ void block_select(const SweepArgs<SYM> &A, const int2
             B.hown = 0;
         }
     } else {
+        if (A.stats && threadIdx.x == 0) {
+            atomicAdd(A.stats + (GLOBALT ? 4 : 0), 1ull);
+            atomicAdd(A.stats + (GLOBALT ? 5 : 1), (unsigned long long)no);
+        }
         double bt = -INFINITY;
         int32_t bc = 0x7fffffff;
         occ_exact<SYM, GLOBALT>(A, T, occ, no, threadIdx.x, BLOCK, L, sr, srf, lo, bt, bc);
@@ -634,44 +645,41 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_sweep_cta(SweepArgs<SYM> A, con
     }
 }
 
-// bin 5 (hubs): persistent CTAs take (row, segment of HUB_SEG entries) items, rows in
-// descending degree.  A segment is combined in a shared table, then merged into the row's
-// global table (one claim + add per distinct community of the segment).  Row tables are
-// regions of a ring buffer: before touching row j's region a CTA waits until the earlier
-// rows overlapping it are finished (their done-epoch flags).  The CTA that completes a row's
-// last segment (counter + release/acquire fences) selects over the row's list, clears the
-// listed slots, resets the counters and publishes the row's done epoch.  Requires every
-// CTA to be resident (the grid is sized from the occupancy query), so waits terminate.
+// bin 5 (hubs), two kernels.  (1) k_sweep_hub_merge: CTAs stride over (row, segment of
+// HUB_SEG entries) items; a segment is combined in a shared table, then merged into the
+// row's global table (its own region, pow2 > d slots): MU independent CAS claims per thread
+// in flight (the CAS returns the occupant, so one L2 round trip finds or claims a slot), the
+// sum a fire-and-forget reduction, fresh slots staged in shared memory and appended to the
+// row's list with one reservation per segment.  (2) k_sweep_hub_select: one CTA per hub row
+// (largest first) selects over the row's list, clears the listed slots and the count.
+// Splitting the phases keeps the selection work off the merge CTAs (a CTA that both merges
+// and selects finishes its segments late, so it keeps completing rows and keeps selecting).
 constexpr int HUB_BLOCK = 512;
 constexpr int HUB_H = 8192;
 struct HubArgs {
     const int32_t *rows;     // bin-5 rows
-    const int64_t *items;    // (j << 20 | segment)
-    int64_t nitems;
+    const int64_t *items;    // (j << 20 | segment), j = processing index
+    int64_t nitems, nrows;
     const int64_t *row_of;   // j -> bin-5 row index
     const int64_t *off, *size;
-    const int32_t *dptr, *didx;
     int2 *tab;
     uint32_t *occ;
-    uint32_t *cnt;           // per j: [3j] occupied, [3j+1] segments done, [3j+2] done epoch
-    uint32_t epoch;
+    uint32_t *cnt;           // per j: occupied count (left zero by the select kernel)
 };
 template <bool SYM>
-__global__ void __launch_bounds__(HUB_BLOCK, 2) k_sweep_hub(SweepArgs<SYM> A, HubArgs Hb) {
+__global__ void __launch_bounds__(HUB_BLOCK, 2) k_sweep_hub_merge(SweepArgs<SYM> A, HubArgs Hb) {
     extern __shared__ int2 htab[];
     uint16_t *socc = (uint16_t *)(htab + HUB_H);
-    __shared__ BlockSel B;
-    __shared__ uint32_t s_no;
-    __shared__ int s_last;
-    __shared__ int64_t s_ready;   // row whose dependencies this CTA has seen finished
+    uint32_t *sfresh = (uint32_t *)(socc + HUB_H);
+    __shared__ uint32_t s_no, s_nf, s_base;
     for (int k = threadIdx.x; k < HUB_H; k += HUB_BLOCK) htab[k] = make_int2(-1, 0);
     if (threadIdx.x == 0) {
-        B.hown = 0;
         s_no = 0;
-        s_ready = -1;
+        s_nf = 0;
     }
     __syncthreads();
     constexpr int U = HUB_SEG / HUB_BLOCK;
+    constexpr int MU = 4;
     for (int64_t q = blockIdx.x; q < Hb.nitems; q += gridDim.x) {
         const int64_t j = Hb.items[q] >> 20, sg = Hb.items[q] & 0xFFFFF;
         const int32_t r = Hb.rows[Hb.row_of[j]];
@@ -690,55 +698,67 @@ __global__ void __launch_bounds__(HUB_BLOCK, 2) k_sweep_hub(SweepArgs<SYM> A, Hu
                 occ_append(socc, &s_no, fresh, sl);
             }
         }
-        // wait for the rows whose table regions overlap row j's (ring reuse)
-        if (threadIdx.x == 0 && s_ready != j) {
-            for (int32_t k = Hb.dptr[j]; k < Hb.dptr[j + 1]; k++) {
-                const volatile uint32_t *f = Hb.cnt + 3 * (int64_t)Hb.didx[k] + 2;
-                while (*f != Hb.epoch) __nanosleep(256);
-            }
-            __threadfence();
-            s_ready = j;
-        }
         __syncthreads();
         const uint32_t ns = s_no;
         int2 *GT = Hb.tab + Hb.off[j];
-        uint32_t *GO = Hb.occ + Hb.off[j];
-        const uint32_t H = (uint32_t)Hb.size[j];
-        uint32_t *gno = Hb.cnt + 3 * j;
-        for (uint32_t k0 = 0; k0 < ns; k0 += HUB_BLOCK) {
-            const uint32_t k = k0 + threadIdx.x;
-            bool fresh = false;
-            uint32_t sl = 0;
-            if (k < ns) {
-                const uint32_t ss = socc[k];
-                const int2 e = htab[ss];
-                htab[ss] = make_int2(-1, 0);
-                sl = tab_insert<true>(GT, H - 1, e.x, (uint32_t)e.y, fresh);
+        const uint32_t gmask = (uint32_t)Hb.size[j] - 1;
+        for (uint32_t k0 = 0; k0 < ns; k0 += HUB_BLOCK * MU) {
+            int2 e[MU];
+            uint32_t sl[MU];
+            int32_t prev[MU];
+#pragma unroll
+            for (int u = 0; u < MU; u++) {
+                const uint32_t k = k0 + u * HUB_BLOCK + threadIdx.x;
+                e[u] = make_int2(-1, 0);
+                if (k < ns) {
+                    const uint32_t ss = socc[k];
+                    e[u] = htab[ss];
+                    htab[ss] = make_int2(-1, 0);
+                }
+                sl[u] = hslot32(e[u].x, gmask);
             }
-            occ_append(GO, gno, fresh, sl);
+#pragma unroll
+            for (int u = 0; u < MU; u++)
+                prev[u] = e[u].x >= 0 ? atomicCAS(&GT[sl[u]].x, -1, e[u].x) : e[u].x;
+#pragma unroll
+            for (int u = 0; u < MU; u++) {
+                if (e[u].x < 0) continue;
+                while (prev[u] != -1 && prev[u] != e[u].x) {
+                    sl[u] = (sl[u] + 1) & gmask;
+                    prev[u] = atomicCAS(&GT[sl[u]].x, -1, e[u].x);
+                }
+                atomicAdd((uint32_t *)&GT[sl[u]].y, (uint32_t)e[u].y);
+                if (prev[u] == -1) sfresh[atomicAdd(&s_nf, 1u)] = sl[u];
+            }
         }
         __syncthreads();
         if (threadIdx.x == 0) {
             s_no = 0;
-            __threadfence();
-            const uint32_t nsg = (uint32_t)((d + HUB_SEG - 1) / HUB_SEG);
-            s_last = atomicAdd(gno + 1, 1u) == nsg - 1;
+            s_base = s_nf ? atomicAdd(Hb.cnt + j, s_nf) : 0;
         }
         __syncthreads();
-        if (s_last) {
-            __threadfence();
-            const uint32_t no = __ldcg(gno);
-            block_select<HUB_BLOCK, SYM, true>(A, GT, GO, no, r, A.label[r], node_s(A, r), B);
-            occ_clear<true>(GT, GO, no, threadIdx.x, HUB_BLOCK);
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                gno[0] = 0;
-                gno[1] = 0;
-                __threadfence();
-                *(volatile uint32_t *)(gno + 2) = Hb.epoch;
-            }
-        }
+        const uint32_t nf = s_nf;
+        uint32_t *GO = Hb.occ + Hb.off[j];
+        for (uint32_t k = threadIdx.x; k < nf; k += HUB_BLOCK) GO[s_base + k] = sfresh[k];
         __syncthreads();
+        if (threadIdx.x == 0) s_nf = 0;
+    }
+}
+
+template <bool SYM>
+__global__ void __launch_bounds__(HUB_BLOCK) k_sweep_hub_select(SweepArgs<SYM> A, HubArgs Hb) {
+    __shared__ BlockSel B;
+    if (threadIdx.x == 0) B.hown = 0;
+    __syncthreads();
+    for (int64_t j = blockIdx.x; j < Hb.nrows; j += gridDim.x) {
+        const int32_t r = Hb.rows[Hb.row_of[j]];
+        const uint32_t no = Hb.cnt[j];
+        int2 *GT = Hb.tab + Hb.off[j];
+        const uint32_t *GO = Hb.occ + Hb.off[j];
+        block_select<HUB_BLOCK, SYM, true>(A, GT, GO, no, r, A.label[r], node_s(A, r), B);
+        occ_clear<true>(GT, GO, no, threadIdx.x, HUB_BLOCK);
+        __syncthreads();
+        if (threadIdx.x == 0) Hb.cnt[j] = 0;
     }
 }
 
@@ -780,25 +800,32 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
     A.inv_m2f = (float)(1.0 / (m * m));
     A.cstar = d_cstar;
     A.groups = d_groups;
+    static DBuf<unsigned long long> stats;
+    A.stats = nullptr;
+    const bool want_stats = getenv("SLM_SWEEP_STATS") != nullptr;
+    if (want_stats) {
+        stats.resize(8);
+        CUDA_TRY(cudaMemsetAsync(stats.p, 0, stats.bytes(), s));
+        A.stats = stats.p;
+    }
     auto nb = [&](int b) { return G.bin_off[b + 1] - G.bin_off[b]; };
     auto rows = [&](int b) { return G.bin_rows.p + G.bin_off[b]; };
     constexpr int W1 = 8;
     constexpr size_t SM1 = (size_t)W1 * 512 * 10, SM2 = 2048 * 10, SM3 = 8192 * 10,
-                     SM4 = 16384 * 10, SMH = HUB_H * 10;
+                     SM4 = 16384 * 10, SMH = HUB_H * 10 + HUB_SEG * 4;
     auto k1 = k_sweep_warp<512, W1, SYM>;
     auto k2 = k_sweep_cta<128, 2048, 2, 8, SYM>;
     auto k3 = k_sweep_cta<512, 8192, 1, 2, SYM>;
     auto k4 = k_sweep_cta<1024, 16384, 1, 1, SYM>;
-    auto kh = k_sweep_hub<SYM>;
+    auto khm = k_sweep_hub_merge<SYM>;
+    auto khs = k_sweep_hub_select<SYM>;
     static bool attrs[2] = {false, false};
-    static int hub_occ[2] = {0, 0};
     if (!attrs[SYM]) {
         set_smem(k1, SM1);
         set_smem(k2, SM2);
         set_smem(k3, SM3);
         set_smem(k4, SM4);
-        set_smem(kh, SMH);
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hub_occ[SYM], kh, HUB_BLOCK, SMH));
+        set_smem(khm, SMH);
         attrs[SYM] = true;
     }
     if (nb(0) && (bin_mask & 1)) {
@@ -816,40 +843,40 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
     if (nb(4) && (bin_mask & 16))
         k4<<<(unsigned)std::min<int64_t>(nb(4), 148), 1024, SM4, s>>>(A, rows(4), nb(4));
     if (nb(5) && (bin_mask & 32)) {
-        SLM_REQUIRE(hub_occ[SYM] > 0, SLM_ECUDA, "hub sweep kernel cannot be resident");
         const int64_t RS = G.hub_ring, nh = G.hub_rows_n;
         if (ctx->hub_tab.n < (size_t)RS) {
             ctx->hub_tab.resize(RS);
             ctx->hub_occ.resize(RS);
-            // tables are left empty by every scan, so filling once per allocation suffices
+            // tables are left empty by every select, so filling once per allocation suffices
             k_fill_empty<<<grid_for(RS, 256), 256, 0, s>>>(ctx->hub_tab.p, RS);
         }
-        if (ctx->hub_cnt.n < (size_t)(3 * nh)) {
-            ctx->hub_cnt.resize(3 * nh);
-            CUDA_TRY(cudaMemsetAsync(ctx->hub_cnt.p, 0, 3 * nh * 4, s));
-            ctx->hub_epoch = 0;
-        }
-        if (++ctx->hub_epoch == 0) {   // wrapped: reset the done flags
-            CUDA_TRY(cudaMemsetAsync(ctx->hub_cnt.p, 0, 3 * nh * 4, s));
-            ctx->hub_epoch = 1;
+        if (ctx->hub_cnt.n < (size_t)nh) {
+            ctx->hub_cnt.resize(nh);
+            CUDA_TRY(cudaMemsetAsync(ctx->hub_cnt.p, 0, nh * 4, s));
         }
         HubArgs Hb;
         Hb.rows = rows(5);
         Hb.items = G.hub_seg.p;
         Hb.nitems = G.hub_nseg;
+        Hb.nrows = nh;
         Hb.row_of = G.hub_row.p;
         Hb.off = G.hub_off.p;
         Hb.size = G.hub_size.p;
-        Hb.dptr = G.hub_dptr.p;
-        Hb.didx = G.hub_didx.p;
         Hb.tab = ctx->hub_tab.p;
         Hb.occ = ctx->hub_occ.p;
         Hb.cnt = ctx->hub_cnt.p;
-        Hb.epoch = ctx->hub_epoch;
-        const int64_t grid = std::min<int64_t>(G.hub_nseg, 148LL * hub_occ[SYM]);
-        kh<<<(unsigned)grid, HUB_BLOCK, SMH, s>>>(A, Hb);
+        khm<<<(unsigned)std::min<int64_t>(G.hub_nseg, 148LL * 2), HUB_BLOCK, SMH, s>>>(A, Hb);
+        khs<<<(unsigned)std::min<int64_t>(nh, 148LL * 4), HUB_BLOCK, 0, s>>>(A, Hb);
     }
     CUDA_TRY(cudaGetLastError());
+    if (want_stats) {
+        unsigned long long h[8];
+        CUDA_TRY(cudaMemcpyAsync(h, stats.p, 64, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        fprintf(stderr, "[sweep stats] mask %d: cta fallback rows %llu groups %llu | warp fallback "
+                "rows %llu groups %llu | hub fallback rows %llu groups %llu\n", bin_mask, h[0], h[1],
+                h[2], h[3], h[4], h[5]);
+    }
 }
 
 void run_plan_u32(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_t *d_cstar,

@@ -300,12 +300,9 @@ def _hub_graph(seed=7):
     return n, np.concatenate([s, d]), np.concatenate([d, s]), np.concatenate([w, w])
 
 
-@pytest.mark.parametrize("ring", [None, "4096"])
-def test_plan_all_degree_bins_vs_oracle(slm, oracle, monkeypatch, ring):
+def test_plan_all_degree_bins_vs_oracle(slm, oracle):
     """Plan sweep over rows of every degree bin (warp, CTA and hub kernels) against the
-    oracle's _best_targets, including the hub-table ring with forced reuse."""
-    if ring:
-        monkeypatch.setenv("SLM_HUB_RING", ring)
+    oracle's _best_targets; repeated sweeps check that the tables are left empty."""
     n, s, d, w = _hub_graph()
     ctx = slm.Graph.from_edges(n, s, d, w).context()
     og = oracle.OGraph.from_edges(n, s, d, w)
