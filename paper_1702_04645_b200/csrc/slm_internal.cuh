@@ -162,6 +162,10 @@ struct slm_ctx {
     DBuf<int2> hub_tab;          // hub tables {community, sum} of the integer sweep (kept empty)
     DBuf<uint32_t> hub_occ;      // occupied-slot lists (same offsets)
     DBuf<uint32_t> hub_cnt;      // per hub row: list length (kept zero between sweeps)
+    DBuf<int32_t> ovf_rows;      // rows of bins 2-4 whose communities overflowed the shared table
+    DBuf<uint32_t> ovf_cnt;      // [0] overflow rows, [1 + b] list length of overflow CTA b
+    DBuf<int2> ovf_tab;          // per overflow CTA: global table (kept empty)
+    DBuf<uint32_t> ovf_occ;
     int32_t *h_flag = nullptr;   // pinned host scalars
     int64_t *h_i64 = nullptr;
     double *h_f64 = nullptr;

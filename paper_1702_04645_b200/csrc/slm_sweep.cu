@@ -152,6 +152,28 @@ __device__ __forceinline__ int32_t decide(const SweepArgs<SYM> &A, double tb, in
     return tb > t_stay ? cb : L;
 }
 
+// Decision for a certain winner cb (group sum gb, approximate bounds [lo_b, up_b]) without
+// division when the bounds separate it from the staying score.  The staying score is
+// bounded in fp32 as well; its null term may cancel (S_L - s), so its error is bounded
+// against Pabs = s_out (S_in + s_in) + s_in (S_out + s_out) instead: each float operand has
+// relative error <= 2^-24 and each difference / product / sum adds one rounding, so
+// |b~ - b| <= 2^-20 Pabs / m^2 and the bound 2^-18 (a~ + Pabs~ / m^2) keeps a factor > 3.
+template <bool SYM>
+__device__ __forceinline__ int32_t decide_fast(const SweepArgs<SYM> &A, uint32_t gb, int32_t cb,
+                                               float lo_b, float up_b, bool hown, uint32_t gown,
+                                               double2 sr, float2 srf, int32_t L) {
+    const float2 SL = comm_Sf(A, L);
+    const float a = hown ? __uint2float_rn(gown) * A.inv_mf : 0.0f;
+    const float P = srf.x * (SL.y - srf.y) + srf.y * (SL.x - srf.x);
+    const float Pabs = srf.x * (SL.y + srf.y) + srf.y * (SL.x + srf.x);
+    const float ts = a - P * A.inv_m2f;
+    const float es = 0x1.0p-18f * (a + Pabs * A.inv_m2f);
+    if (lo_b > ts + es) return cb;
+    if (up_b < ts - es) return L;
+    const double tb = exact_t(gb, null_P(false, sr, comm_S(A, cb)), A.m, A.m2);
+    return decide(A, tb, cb, hown, gown, sr, L);
+}
+
 __device__ __forceinline__ bool better2(double t1, int32_t c1, double t2, int32_t c2) {
     return t1 > t2 || (t1 == t2 && c1 < c2);
 }
@@ -281,8 +303,10 @@ __global__ void __launch_bounds__(256) k_sweep_small(SweepArgs<SYM> A, const int
 // and clears exactly the listed slots, so tables stay empty between rows: shared tables
 // are initialised once per launch, global (hub) tables once per allocation.
 
+// Fibonacci hashing: the HIGH log2(H) bits of c * 2^32/phi (the low bits of the product
+// depend only on the low bits of c, which cluster for community ids)
 __device__ __forceinline__ uint32_t hslot32(int32_t c, uint32_t hmask) {
-    return ((uint32_t)c * 2654435761u) & hmask;
+    return ((uint32_t)c * 2654435769u) >> __clz(hmask);
 }
 
 // claim (or find) c's slot and add w; returns the slot, fresh = this call claimed it
@@ -334,9 +358,8 @@ __device__ __forceinline__ uint32_t occ_load(const IDX *occ, uint32_t k) {
 // table size for a row of d entries: the smallest power of two >= lo with H > d / f
 // (f = 1: H > d, always enough; f = 2: load <= 1/2)
 __device__ __forceinline__ uint32_t tab_size(int64_t d, int f, uint32_t lo) {
-    uint32_t H = lo;
-    while ((int64_t)H <= f * d) H <<= 1;
-    return H;
+    const uint32_t x = (uint32_t)(f * d);   // bins using it have f d < 2^31
+    return max(lo, 1u << (32 - __clz(x)));  // smallest power of two > x
 }
 
 // list entries t0, t0 + stride, ... < no: approximate selection, own group
@@ -505,11 +528,8 @@ __global__ void __launch_bounds__(WARPS * 32, 4) k_sweep_warp(SweepArgs<SYM> A, 
         } else {
             const unsigned cnt = (S.up1 >= lo) + (S.up2 >= lo);
             if (__reduce_add_sync(0xffffffffu, cnt) == 1) {
-                if (S.up1 >= lo) {
-                    const double bt =
-                        exact_t(S.g1, null_P(false, sr, comm_S(A, S.c1)), A.m, A.m2);
-                    A.cstar[r] = decide(A, bt, S.c1, ob != 0, gown, sr, L);
-                }
+                if (S.up1 >= lo)
+                    A.cstar[r] = decide_fast(A, S.g1, S.c1, lo, S.up1, ob != 0, gown, sr, srf, L);
             } else {
                 if (A.stats && lane == 0) {
                     atomicAdd(A.stats + 2, 1ull);
@@ -571,8 +591,7 @@ __device__ __forceinline__ void block_select(const SweepArgs<SYM> &A, const int2
         }
     } else if (cnt == 1) {
         if (S.up1 >= lo) {
-            const double bt = exact_t(S.g1, null_P(false, sr, comm_S(A, S.c1)), A.m, A.m2);
-            A.cstar[r] = decide(A, bt, S.c1, B.hown != 0, B.gown, sr, L);
+            A.cstar[r] = decide_fast(A, S.g1, S.c1, lo, S.up1, B.hown != 0, B.gown, sr, srf, L);
             B.hown = 0;
         }
     } else {
@@ -601,18 +620,59 @@ __device__ __forceinline__ void block_select(const SweepArgs<SYM> &A, const int2
     }
 }
 
-// bins 2-4: one CTA per row, shared table of up to HMAX slots + list
+__global__ void k_fill_empty(int2 *T, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        T[i] = make_int2(-1, 0);
+}
+
+// bounded insert for tables that may be too small for the row (capacity decided from
+// typical group counts): gives up after PROBE_MAX probes (a table near full); the row is
+// then redone by the overflow kernel
+constexpr uint32_t PROBE_MAX = 128;
+__device__ __forceinline__ bool tab_insert_bounded(int2 *T, uint32_t hmask, int32_t c, uint32_t w,
+                                                   bool &fresh, uint32_t &slot) {
+    uint32_t sl = hslot32(c, hmask);
+    fresh = false;
+    for (uint32_t p = 0; p < PROBE_MAX && p <= hmask; p++) {
+        const int32_t k = *(volatile int32_t *)&T[sl].x;
+        if (k == c) {
+            atomicAdd((uint32_t *)&T[sl].y, w);
+            slot = sl;
+            return true;
+        }
+        if (k == -1) {
+            const int32_t prev = atomicCAS(&T[sl].x, -1, c);
+            if (prev == -1 || prev == c) {
+                fresh = prev == -1;
+                atomicAdd((uint32_t *)&T[sl].y, w);
+                slot = sl;
+                return true;
+            }
+        }
+        sl = (sl + 1) & hmask;
+    }
+    return false;
+}
+
+// bins 2-4: one CTA per row over a shared table of min(HMAX, pow2 > F d) slots + list.
+// HMAX is sized for the bin's typical number of distinct communities, not its degree
+// bound, so that several rows are in flight per SM; a row whose communities do not fit
+// (a probe cycle fails) is appended to the overflow list and redone by k_sweep_overflow.
 template <int BLOCK, int HMAX, int F, int MINB, bool SYM>
 __global__ void __launch_bounds__(BLOCK, MINB) k_sweep_cta(SweepArgs<SYM> A, const int32_t *rows,
-                                                            int64_t nrows) {
+                                                            int64_t nrows, int32_t *ovf,
+                                                            uint32_t *novf) {
     extern __shared__ int2 ctab[];
     uint16_t *occ = (uint16_t *)(ctab + HMAX);
     __shared__ BlockSel B;
     __shared__ uint32_t s_no;
+    __shared__ int s_ovf;
     for (int k = threadIdx.x; k < HMAX; k += BLOCK) ctab[k] = make_int2(-1, 0);
     if (threadIdx.x == 0) {
         B.hown = 0;
         s_no = 0;
+        s_ovf = 0;
     }
     __syncthreads();
     for (int64_t i = blockIdx.x; i < nrows; i += gridDim.x) {
@@ -620,7 +680,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_sweep_cta(SweepArgs<SYM> A, con
         const int64_t e0 = A.uptr[r], d = A.uptr[r + 1] - e0;
         const int32_t L = A.label[r];
         const double2 sr = node_s(A, r);
-        const uint32_t H = min(tab_size(d, F, 32), (uint32_t)HMAX);   // > d (bin bound)
+        const uint32_t H = min(tab_size(d, F, 32), (uint32_t)HMAX);
         constexpr int U = 4;
         for (int64_t cb = 0; cb < d; cb += BLOCK * U) {
             int32_t c[U];
@@ -632,16 +692,64 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_sweep_cta(SweepArgs<SYM> A, con
                 if (cb + u * BLOCK >= d) break;   // CTA-uniform
                 bool fresh = false;
                 uint32_t sl = 0;
-                if (v[u]) sl = tab_insert<false>(ctab, H - 1, c[u], wt[u], fresh);
+                if (v[u] && !tab_insert_bounded(ctab, H - 1, c[u], wt[u], fresh, sl)) s_ovf = 1;
                 occ_append(occ, &s_no, fresh, sl);
             }
         }
         __syncthreads();
         const uint32_t no = s_no;
-        block_select<BLOCK, SYM, false>(A, ctab, occ, no, r, L, sr, B);
+        if (s_ovf) {
+            if (threadIdx.x == 0) ovf[atomicAdd(novf, 1u)] = r;
+            if (A.stats && threadIdx.x == 0) atomicAdd(A.stats + 6, 1ull);
+        } else {
+            block_select<BLOCK, SYM, false>(A, ctab, occ, no, r, L, sr, B);
+        }
         occ_clear<false>(ctab, occ, no, threadIdx.x, BLOCK);
         __syncthreads();
-        if (threadIdx.x == 0) s_no = 0;   // every thread read s_no before the select barriers
+        if (threadIdx.x == 0) {   // every thread read s_no / s_ovf before the barriers above
+            s_no = 0;
+            s_ovf = 0;
+        }
+    }
+}
+
+// rows of bins 2-4 whose communities overflowed the shared table: one CTA per row over a
+// per-CTA global table of OVF_H slots (> the largest degree of those bins) + list
+constexpr int OVF_BLOCK = 512;
+constexpr int OVF_H = 32768;
+constexpr int OVF_GRID = 296;
+template <bool SYM>
+__global__ void __launch_bounds__(OVF_BLOCK) k_sweep_overflow(SweepArgs<SYM> A, const int32_t *ovf,
+                                                               const uint32_t *novf, int2 *tabs,
+                                                               uint32_t *occs, uint32_t *nocc) {
+    __shared__ BlockSel B;
+    if (threadIdx.x == 0) B.hown = 0;
+    __syncthreads();
+    int2 *T = tabs + (int64_t)blockIdx.x * OVF_H;
+    uint32_t *O = occs + (int64_t)blockIdx.x * OVF_H;
+    uint32_t *cnt = nocc + blockIdx.x;
+    const uint32_t nrows = *novf;
+    for (uint32_t i = blockIdx.x; i < nrows; i += gridDim.x) {
+        const int32_t r = ovf[i];
+        const int64_t e0 = A.uptr[r], d = A.uptr[r + 1] - e0;
+        const uint32_t H = min(tab_size(d, 1, 32), (uint32_t)OVF_H);   // > d
+        for (int64_t k0 = 0; k0 < d; k0 += OVF_BLOCK) {   // warp-uniform trip count
+            const int64_t k = k0 + threadIdx.x;
+            bool fresh = false;
+            uint32_t sl = 0;
+            if (k < d) {
+                const int32_t c = A.label[A.unbr[e0 + k]];
+                sl = tab_insert<true>(T, H - 1, c, A.u32[e0 + k], fresh);
+            }
+            occ_append(O, cnt, fresh, sl);
+        }
+        __syncthreads();
+        const uint32_t no = __ldcg(cnt);
+        block_select<OVF_BLOCK, SYM, true>(A, T, O, no, r, A.label[r], node_s(A, r), B);
+        occ_clear<true>(T, O, no, threadIdx.x, OVF_BLOCK);
+        __syncthreads();
+        if (threadIdx.x == 0) *cnt = 0;
+        __syncthreads();
     }
 }
 
@@ -762,12 +870,6 @@ __global__ void __launch_bounds__(HUB_BLOCK) k_sweep_hub_select(SweepArgs<SYM> A
     }
 }
 
-__global__ void k_fill_empty(int2 *T, int64_t n) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        T[i] = make_int2(-1, 0);
-}
-
 __global__ void k_copy_labels32(const int32_t *label, int64_t n, int32_t *out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -811,12 +913,12 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
     auto nb = [&](int b) { return G.bin_off[b + 1] - G.bin_off[b]; };
     auto rows = [&](int b) { return G.bin_rows.p + G.bin_off[b]; };
     constexpr int W1 = 8;
-    constexpr size_t SM1 = (size_t)W1 * 512 * 10, SM2 = 2048 * 10, SM3 = 8192 * 10,
-                     SM4 = 16384 * 10, SMH = HUB_H * 10 + HUB_SEG * 4;
+    constexpr size_t SM1 = (size_t)W1 * 512 * 10, SM2 = 2048 * 10, SM3 = 2048 * 10,
+                     SM4 = 8192 * 10, SMH = HUB_H * 10 + HUB_SEG * 4;
     auto k1 = k_sweep_warp<512, W1, SYM>;
     auto k2 = k_sweep_cta<128, 2048, 2, 8, SYM>;
-    auto k3 = k_sweep_cta<512, 8192, 1, 2, SYM>;
-    auto k4 = k_sweep_cta<1024, 16384, 1, 1, SYM>;
+    auto k3 = k_sweep_cta<256, 2048, 1, 4, SYM>;
+    auto k4 = k_sweep_cta<512, 8192, 1, 2, SYM>;
     auto khm = k_sweep_hub_merge<SYM>;
     auto khs = k_sweep_hub_select<SYM>;
     static bool attrs[2] = {false, false};
@@ -836,12 +938,34 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
     }
     if (nb(1) && (bin_mask & 2))
         k1<<<grid_for(nb(1) * 32, W1 * 32, 148LL * 4), W1 * 32, SM1, s>>>(A, rows(1), nb(1));
+    if (bin_mask & 28) {
+        const int64_t cap = nb(2) + nb(3) + nb(4);
+        if (ctx->ovf_rows.n < (size_t)std::max<int64_t>(1, cap)) ctx->ovf_rows.resize(std::max<int64_t>(1, cap));
+        if (ctx->ovf_cnt.n < 1 + OVF_GRID) {
+            ctx->ovf_cnt.resize(1 + OVF_GRID);
+            CUDA_TRY(cudaMemsetAsync(ctx->ovf_cnt.p, 0, (1 + OVF_GRID) * 4, s));
+        } else {
+            CUDA_TRY(cudaMemsetAsync(ctx->ovf_cnt.p, 0, 4, s));
+        }
+    }
+    int32_t *ovf = ctx->ovf_rows.p;
+    uint32_t *novf = ctx->ovf_cnt.p;
     if (nb(2) && (bin_mask & 4))
-        k2<<<(unsigned)std::min<int64_t>(nb(2), 148 * 8), 128, SM2, s>>>(A, rows(2), nb(2));
+        k2<<<(unsigned)std::min<int64_t>(nb(2), 148 * 8), 128, SM2, s>>>(A, rows(2), nb(2), ovf, novf);
     if (nb(3) && (bin_mask & 8))
-        k3<<<(unsigned)std::min<int64_t>(nb(3), 148 * 2), 512, SM3, s>>>(A, rows(3), nb(3));
+        k3<<<(unsigned)std::min<int64_t>(nb(3), 148 * 4), 256, SM3, s>>>(A, rows(3), nb(3), ovf, novf);
     if (nb(4) && (bin_mask & 16))
-        k4<<<(unsigned)std::min<int64_t>(nb(4), 148), 1024, SM4, s>>>(A, rows(4), nb(4));
+        k4<<<(unsigned)std::min<int64_t>(nb(4), 148 * 2), 512, SM4, s>>>(A, rows(4), nb(4), ovf, novf);
+    if (bin_mask & 28) {
+        if (ctx->ovf_tab.n < (size_t)OVF_GRID * OVF_H) {
+            ctx->ovf_tab.resize((size_t)OVF_GRID * OVF_H);
+            ctx->ovf_occ.resize((size_t)OVF_GRID * OVF_H);
+            k_fill_empty<<<grid_for((int64_t)OVF_GRID * OVF_H, 256), 256, 0, s>>>(
+                ctx->ovf_tab.p, (int64_t)OVF_GRID * OVF_H);
+        }
+        k_sweep_overflow<SYM><<<OVF_GRID, OVF_BLOCK, 0, s>>>(A, ovf, novf, ctx->ovf_tab.p,
+                                                             ctx->ovf_occ.p, novf + 1);
+    }
     if (nb(5) && (bin_mask & 32)) {
         const int64_t RS = G.hub_ring, nh = G.hub_rows_n;
         if (ctx->hub_tab.n < (size_t)RS) {
@@ -874,8 +998,8 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
         CUDA_TRY(cudaMemcpyAsync(h, stats.p, 64, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
         fprintf(stderr, "[sweep stats] mask %d: cta fallback rows %llu groups %llu | warp fallback "
-                "rows %llu groups %llu | hub fallback rows %llu groups %llu\n", bin_mask, h[0], h[1],
-                h[2], h[3], h[4], h[5]);
+                "rows %llu groups %llu | hub fallback rows %llu groups %llu | overflow rows %llu\n",
+                bin_mask, h[0], h[1], h[2], h[3], h[4], h[5], h[6]);
     }
 }
 
