@@ -445,6 +445,74 @@ __device__ __forceinline__ void load_entries(const SweepArgs<SYM> &A, int64_t e0
     for (int u = 0; u < U; u++) c[u] = v[u] ? A.label[z[u]] : -1;
 }
 
+// unrolled load of entries base + u * stride < d of one row through row-relative 32-bit
+// indices (nb, ub: the row's neighbour and weight arrays): c = label of the neighbour, or -1
+template <int U>
+__device__ __forceinline__ void load_row(const int32_t *nb, const uint32_t *ub, const int32_t *label,
+                                         uint32_t d, uint32_t base, uint32_t stride,
+                                         int32_t (&c)[U], uint32_t (&w)[U]) {
+    int32_t z[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        const uint32_t idx = base + u * stride;
+        z[u] = -1;
+        w[u] = 0;
+        if (idx < d) {
+            z[u] = __ldcs(nb + idx);
+            w[u] = __ldcs(ub + idx);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) c[u] = z[u] >= 0 ? label[z[u]] : -1;
+}
+
+// insert U entries per lane into a shared table and append the freshly claimed slots to
+// the list with one reservation per chunk (scnt: shared counter; else the warp-private
+// register counter rcnt).  BOUNDED: a failed probe sequence sets *ovf.
+template <int U, bool BOUNDED, class IDX>
+__device__ __forceinline__ void insert_chunk(int2 *T, uint32_t hmask, const int32_t (&c)[U],
+                                             const uint32_t (&w)[U], IDX *occ, uint32_t *scnt,
+                                             uint32_t &rcnt, int *ovf) {
+    const int lane = threadIdx.x & 31;
+    bool fr[U];
+    uint32_t sl[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        fr[u] = false;
+        sl[u] = 0;
+        if (c[u] >= 0) {
+            if (BOUNDED) {
+                if (!tab_insert_bounded(T, hmask, c[u], w[u], fr[u], sl[u])) *ovf = 1;
+            } else {
+                sl[u] = tab_insert<false>(T, hmask, c[u], w[u], fr[u]);
+            }
+        }
+    }
+    unsigned m[U];
+    uint32_t tot = 0;
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        m[u] = __ballot_sync(0xffffffffu, fr[u]);
+        tot += __popc(m[u]);
+    }
+    if (tot == 0) return;
+    uint32_t base;
+    if (scnt) {
+        base = 0;
+        if (lane == 0) base = atomicAdd(scnt, tot);
+        base = __shfl_sync(0xffffffffu, base, 0);
+    } else {
+        base = rcnt;
+        rcnt += tot;
+    }
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        if (fr[u]) occ[base + __popc(m[u] & lt)] = (IDX)sl[u];
+        base += __popc(m[u]);
+    }
+}
+
 __device__ __forceinline__ float warp_maxf(float v) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
@@ -497,21 +565,13 @@ __global__ void __launch_bounds__(WARPS * 32, 4) k_sweep_warp(SweepArgs<SYM> A, 
         const float2 srf = make_float2((float)sr.x, (float)sr.y);
         uint32_t no = 0;
         constexpr int U = 4;
-        for (int64_t cb = 0; cb < d; cb += 32 * U) {
+        const int32_t *nb = A.unbr + e0;
+        const uint32_t *ub = A.u32 + e0;
+        for (uint32_t cb = 0; cb < (uint32_t)d; cb += 32 * U) {
             int32_t c[U];
             uint32_t wt[U];
-            bool v[U];
-            load_entries<U>(A, e0, d, cb + lane, 32, c, wt, v);
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                if (cb + u * 32 >= d) break;   // warp-uniform
-                bool fresh = false;
-                uint32_t sl = 0;
-                if (v[u]) sl = tab_insert<false>(T, H - 1, c[u], wt[u], fresh);
-                const unsigned fm = __ballot_sync(0xffffffffu, fresh);
-                if (fresh) occ[no + __popc(fm & ((1u << lane) - 1))] = (uint16_t)sl;
-                no += __popc(fm);
-            }
+            load_row<U>(nb, ub, A.label, (uint32_t)d, cb + lane, 32, c, wt);
+            insert_chunk<U, false>(T, H - 1, c, wt, occ, (uint32_t *)nullptr, no, (int *)nullptr);
         }
         __syncwarp();
         Sel S;
@@ -682,19 +742,14 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_sweep_cta(SweepArgs<SYM> A, con
         const double2 sr = node_s(A, r);
         const uint32_t H = min(tab_size(d, F, 32), (uint32_t)HMAX);
         constexpr int U = 4;
-        for (int64_t cb = 0; cb < d; cb += BLOCK * U) {
+        const int32_t *nb = A.unbr + e0;
+        const uint32_t *ub = A.u32 + e0;
+        uint32_t unused = 0;
+        for (uint32_t cb = 0; cb < (uint32_t)d; cb += BLOCK * U) {
             int32_t c[U];
             uint32_t wt[U];
-            bool v[U];
-            load_entries<U>(A, e0, d, cb + threadIdx.x, BLOCK, c, wt, v);
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                if (cb + u * BLOCK >= d) break;   // CTA-uniform
-                bool fresh = false;
-                uint32_t sl = 0;
-                if (v[u] && !tab_insert_bounded(ctab, H - 1, c[u], wt[u], fresh, sl)) s_ovf = 1;
-                occ_append(occ, &s_no, fresh, sl);
-            }
+            load_row<U>(nb, ub, A.label, (uint32_t)d, cb + threadIdx.x, BLOCK, c, wt);
+            insert_chunk<U, true>(ctab, H - 1, c, wt, occ, &s_no, unused, &s_ovf);
         }
         __syncthreads();
         const uint32_t no = s_no;
@@ -796,15 +851,10 @@ __global__ void __launch_bounds__(HUB_BLOCK, 2) k_sweep_hub_merge(SweepArgs<SYM>
         {
             int32_t c[U];
             uint32_t wt[U];
-            bool v[U];
-            load_entries<U>(A, e0, hi, lo + threadIdx.x, HUB_BLOCK, c, wt, v);
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                bool fresh = false;
-                uint32_t sl = 0;
-                if (v[u]) sl = tab_insert<false>(htab, HUB_H - 1, c[u], wt[u], fresh);
-                occ_append(socc, &s_no, fresh, sl);
-            }
+            uint32_t unused = 0;
+            load_row<U>(A.unbr + e0 + lo, A.u32 + e0 + lo, A.label, (uint32_t)(hi - lo),
+                        threadIdx.x, HUB_BLOCK, c, wt);
+            insert_chunk<U, false>(htab, HUB_H - 1, c, wt, socc, &s_no, unused, (int *)nullptr);
         }
         __syncthreads();
         const uint32_t ns = s_no;
