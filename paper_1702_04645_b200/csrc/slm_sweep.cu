@@ -445,47 +445,90 @@ __device__ __forceinline__ void load_entries(const SweepArgs<SYM> &A, int64_t e0
     for (int u = 0; u < U; u++) c[u] = v[u] ? A.label[z[u]] : -1;
 }
 
-// unrolled load of entries base + u * stride < d of one row through row-relative 32-bit
-// indices (nb, ub: the row's neighbour and weight arrays): c = label of the neighbour, or -1
-template <int U>
+// unrolled load of entries base + u * stride < d of one row (nb, ub: the row's neighbour
+// and weight arrays; one 64-bit lane pointer, immediate offsets): c = label of the
+// neighbour, or -1
+template <int U, int STRIDE>
 __device__ __forceinline__ void load_row(const int32_t *nb, const uint32_t *ub, const int32_t *label,
-                                         uint32_t d, uint32_t base, uint32_t stride,
-                                         int32_t (&c)[U], uint32_t (&w)[U]) {
+                                         uint32_t d, uint32_t base, int32_t (&c)[U],
+                                         uint32_t (&w)[U]) {
+    // opaque moves keep one lane pointer per array (otherwise the 64-bit address is rebuilt
+    // under each load's predicate)
+    const int32_t *pn;
+    const uint32_t *pu;
+    asm("mov.b64 %0, %1;" : "=l"(pn) : "l"(nb + base));
+    asm("mov.b64 %0, %1;" : "=l"(pu) : "l"(ub + base));
     int32_t z[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
-        const uint32_t idx = base + u * stride;
-        z[u] = -1;
-        w[u] = 0;
-        if (idx < d) {
-            z[u] = __ldcs(nb + idx);
-            w[u] = __ldcs(ub + idx);
-        }
+        const bool ok = base + u * STRIDE < d;
+        z[u] = ok ? __ldcs(pn + u * STRIDE) : -1;
+        w[u] = ok ? __ldcs(pu + u * STRIDE) : 0u;
     }
 #pragma unroll
-    for (int u = 0; u < U; u++) c[u] = z[u] >= 0 ? label[z[u]] : -1;
+    for (int u = 0; u < U; u++) c[u] = z[u] >= 0 ? __ldg(label + z[u]) : -1;
 }
 
-// insert U entries per lane into a shared table and append the freshly claimed slots to
-// the list with one reservation per chunk (scnt: shared counter; else the warp-private
-// register counter rcnt).  BOUNDED: a failed probe sequence sets *ovf.
-template <int U, bool BOUNDED, class IDX>
-__device__ __forceinline__ void insert_chunk(int2 *T, uint32_t hmask, const int32_t (&c)[U],
-                                             const uint32_t (&w)[U], IDX *occ, uint32_t *scnt,
+// shared-memory primitives on 32-bit shared addresses (no generic-address conversion)
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ int32_t lds_vol(uint32_t a) {
+    int32_t v;
+    asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ int32_t cas_s(uint32_t a, int32_t cmp, int32_t val) {
+    int32_t old;
+    asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "r"(a), "r"(cmp), "r"(val)
+                 : "memory");
+    return old;
+}
+__device__ __forceinline__ void red_add_s(uint32_t a, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+}
+
+// insert U entries per lane into a shared table (tb: its shared address, 8-byte slots) and
+// append the freshly claimed slots to the u16 list at ob with one reservation per chunk
+// (scnt: shared counter; else the warp-private register counter rcnt).  BOUNDED: give up
+// after PROBE_MAX probes and set *ovf (the row is redone by the overflow kernel).
+constexpr uint32_t PROBE_MAX = 128;
+template <int U, bool BOUNDED>
+__device__ __forceinline__ void insert_chunk(uint32_t tb, uint32_t hmask, const int32_t (&c)[U],
+                                             const uint32_t (&w)[U], uint32_t ob, uint32_t *scnt,
                                              uint32_t &rcnt, int *ovf) {
     const int lane = threadIdx.x & 31;
+    const uint32_t hsh = __clz(hmask);
     bool fr[U];
     uint32_t sl[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
         fr[u] = false;
-        sl[u] = 0;
+        sl[u] = ((uint32_t)c[u] * 2654435769u) >> hsh;
         if (c[u] >= 0) {
-            if (BOUNDED) {
-                if (!tab_insert_bounded(T, hmask, c[u], w[u], fr[u], sl[u])) *ovf = 1;
-            } else {
-                sl[u] = tab_insert<false>(T, hmask, c[u], w[u], fr[u]);
+            uint32_t p = 0;
+            for (;;) {
+                int32_t k = lds_vol(tb + sl[u] * 8);
+                if (k == c[u]) break;
+                if (k == -1) {
+                    k = cas_s(tb + sl[u] * 8, -1, c[u]);
+                    if (k == -1) {
+                        fr[u] = true;
+                        break;
+                    }
+                    if (k == c[u]) break;
+                }
+                sl[u] = (sl[u] + 1) & hmask;
+                if (BOUNDED && ++p == PROBE_MAX) {
+                    *ovf = 1;
+                    break;
+                }
             }
+            red_add_s(tb + sl[u] * 8 + 4, w[u]);   // (after a failed probe: a stray add to a
+                                                    //  slot of a row that is redone anyway)
         }
     }
     unsigned m[U];
@@ -508,7 +551,7 @@ __device__ __forceinline__ void insert_chunk(int2 *T, uint32_t hmask, const int3
     const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
     for (int u = 0; u < U; u++) {
-        if (fr[u]) occ[base + __popc(m[u] & lt)] = (IDX)sl[u];
+        if (fr[u]) sts_u16(ob + 2 * (base + __popc(m[u] & lt)), sl[u]);
         base += __popc(m[u]);
     }
 }
@@ -539,6 +582,7 @@ __global__ void __launch_bounds__(WARPS * 32, 4) k_sweep_warp(SweepArgs<SYM> A, 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int2 *T = wtab + wid * HMAX;
     uint16_t *occ = (uint16_t *)(wtab + WARPS * HMAX) + wid * HMAX;
+    const uint32_t tsa = smem_addr(T), osa = smem_addr(occ);
     for (int k = lane; k < HMAX; k += 32) T[k] = make_int2(-1, 0);
     __syncwarp();
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -570,8 +614,8 @@ __global__ void __launch_bounds__(WARPS * 32, 4) k_sweep_warp(SweepArgs<SYM> A, 
         for (uint32_t cb = 0; cb < (uint32_t)d; cb += 32 * U) {
             int32_t c[U];
             uint32_t wt[U];
-            load_row<U>(nb, ub, A.label, (uint32_t)d, cb + lane, 32, c, wt);
-            insert_chunk<U, false>(T, H - 1, c, wt, occ, (uint32_t *)nullptr, no, (int *)nullptr);
+            load_row<U, 32>(nb, ub, A.label, (uint32_t)d, cb + lane, c, wt);
+            insert_chunk<U, false>(tsa, H - 1, c, wt, osa, (uint32_t *)nullptr, no, (int *)nullptr);
         }
         __syncwarp();
         Sel S;
@@ -686,35 +730,6 @@ __global__ void k_fill_empty(int2 *T, int64_t n) {
         T[i] = make_int2(-1, 0);
 }
 
-// bounded insert for tables that may be too small for the row (capacity decided from
-// typical group counts): gives up after PROBE_MAX probes (a table near full); the row is
-// then redone by the overflow kernel
-constexpr uint32_t PROBE_MAX = 128;
-__device__ __forceinline__ bool tab_insert_bounded(int2 *T, uint32_t hmask, int32_t c, uint32_t w,
-                                                   bool &fresh, uint32_t &slot) {
-    uint32_t sl = hslot32(c, hmask);
-    fresh = false;
-    for (uint32_t p = 0; p < PROBE_MAX && p <= hmask; p++) {
-        const int32_t k = *(volatile int32_t *)&T[sl].x;
-        if (k == c) {
-            atomicAdd((uint32_t *)&T[sl].y, w);
-            slot = sl;
-            return true;
-        }
-        if (k == -1) {
-            const int32_t prev = atomicCAS(&T[sl].x, -1, c);
-            if (prev == -1 || prev == c) {
-                fresh = prev == -1;
-                atomicAdd((uint32_t *)&T[sl].y, w);
-                slot = sl;
-                return true;
-            }
-        }
-        sl = (sl + 1) & hmask;
-    }
-    return false;
-}
-
 // bins 2-4: one CTA per row over a shared table of min(HMAX, pow2 > F d) slots + list.
 // HMAX is sized for the bin's typical number of distinct communities, not its degree
 // bound, so that several rows are in flight per SM; a row whose communities do not fit
@@ -725,6 +740,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_sweep_cta(SweepArgs<SYM> A, con
                                                             uint32_t *novf) {
     extern __shared__ int2 ctab[];
     uint16_t *occ = (uint16_t *)(ctab + HMAX);
+    const uint32_t tsa = smem_addr(ctab), osa = smem_addr(occ);
     __shared__ BlockSel B;
     __shared__ uint32_t s_no;
     __shared__ int s_ovf;
@@ -748,8 +764,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_sweep_cta(SweepArgs<SYM> A, con
         for (uint32_t cb = 0; cb < (uint32_t)d; cb += BLOCK * U) {
             int32_t c[U];
             uint32_t wt[U];
-            load_row<U>(nb, ub, A.label, (uint32_t)d, cb + threadIdx.x, BLOCK, c, wt);
-            insert_chunk<U, true>(ctab, H - 1, c, wt, occ, &s_no, unused, &s_ovf);
+            load_row<U, BLOCK>(nb, ub, A.label, (uint32_t)d, cb + threadIdx.x, c, wt);
+            insert_chunk<U, true>(tsa, H - 1, c, wt, osa, &s_no, unused, &s_ovf);
         }
         __syncthreads();
         const uint32_t no = s_no;
@@ -834,6 +850,7 @@ __global__ void __launch_bounds__(HUB_BLOCK, 2) k_sweep_hub_merge(SweepArgs<SYM>
     extern __shared__ int2 htab[];
     uint16_t *socc = (uint16_t *)(htab + HUB_H);
     uint32_t *sfresh = (uint32_t *)(socc + HUB_H);
+    const uint32_t tsa = smem_addr(htab), osa = smem_addr(socc);
     __shared__ uint32_t s_no, s_nf, s_base;
     for (int k = threadIdx.x; k < HUB_H; k += HUB_BLOCK) htab[k] = make_int2(-1, 0);
     if (threadIdx.x == 0) {
@@ -852,9 +869,9 @@ __global__ void __launch_bounds__(HUB_BLOCK, 2) k_sweep_hub_merge(SweepArgs<SYM>
             int32_t c[U];
             uint32_t wt[U];
             uint32_t unused = 0;
-            load_row<U>(A.unbr + e0 + lo, A.u32 + e0 + lo, A.label, (uint32_t)(hi - lo),
-                        threadIdx.x, HUB_BLOCK, c, wt);
-            insert_chunk<U, false>(htab, HUB_H - 1, c, wt, socc, &s_no, unused, (int *)nullptr);
+            load_row<U, HUB_BLOCK>(A.unbr + e0 + lo, A.u32 + e0 + lo, A.label, (uint32_t)(hi - lo),
+                                   threadIdx.x, c, wt);
+            insert_chunk<U, false>(tsa, HUB_H - 1, c, wt, osa, &s_no, unused, (int *)nullptr);
         }
         __syncthreads();
         const uint32_t ns = s_no;
