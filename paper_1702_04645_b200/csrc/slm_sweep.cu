@@ -446,27 +446,37 @@ __device__ __forceinline__ void load_entries(const SweepArgs<SYM> &A, int64_t e0
 }
 
 // unrolled load of entries base + u * stride < d of one row (nb, ub: the row's neighbour
-// and weight arrays; one 64-bit lane pointer, immediate offsets): c = label of the
-// neighbour, or -1
+// and weight arrays; one 64-bit lane pointer, immediate offsets): z = neighbour or -1
 template <int U, int STRIDE>
-__device__ __forceinline__ void load_row(const int32_t *nb, const uint32_t *ub, const int32_t *label,
-                                         uint32_t d, uint32_t base, int32_t (&c)[U],
-                                         uint32_t (&w)[U]) {
+__device__ __forceinline__ void load_raw(const int32_t *nb, const uint32_t *ub, uint32_t d,
+                                         uint32_t base, int32_t (&z)[U], uint32_t (&w)[U]) {
     // opaque moves keep one lane pointer per array (otherwise the 64-bit address is rebuilt
     // under each load's predicate)
     const int32_t *pn;
     const uint32_t *pu;
     asm("mov.b64 %0, %1;" : "=l"(pn) : "l"(nb + base));
     asm("mov.b64 %0, %1;" : "=l"(pu) : "l"(ub + base));
-    int32_t z[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
         const bool ok = base + u * STRIDE < d;
         z[u] = ok ? __ldcs(pn + u * STRIDE) : -1;
         w[u] = ok ? __ldcs(pu + u * STRIDE) : 0u;
     }
+}
+// neighbour -> community (or -1)
+template <int U>
+__device__ __forceinline__ void gather_labels(const int32_t *label, const int32_t (&z)[U],
+                                              int32_t (&c)[U]) {
 #pragma unroll
     for (int u = 0; u < U; u++) c[u] = z[u] >= 0 ? __ldg(label + z[u]) : -1;
+}
+template <int U, int STRIDE>
+__device__ __forceinline__ void load_row(const int32_t *nb, const uint32_t *ub, const int32_t *label,
+                                         uint32_t d, uint32_t base, int32_t (&c)[U],
+                                         uint32_t (&w)[U]) {
+    int32_t z[U];
+    load_raw<U, STRIDE>(nb, ub, d, base, z, w);
+    gather_labels<U>(label, z, c);
 }
 
 // shared-memory primitives on 32-bit shared addresses (no generic-address conversion)
@@ -734,6 +744,25 @@ __global__ void k_fill_empty(int2 *T, int64_t n) {
 // HMAX is sized for the bin's typical number of distinct communities, not its degree
 // bound, so that several rows are in flight per SM; a row whose communities do not fit
 // (a probe cycle fails) is appended to the overflow list and redone by k_sweep_overflow.
+// row metadata of the CTA kernel's software pipeline
+struct RowMeta {
+    int32_t r, L;
+    int64_t e0;
+    uint32_t d;
+};
+template <bool SYM>
+__device__ __forceinline__ RowMeta row_meta(const SweepArgs<SYM> &A, const int32_t *rows,
+                                            int64_t i, int64_t nrows) {
+    RowMeta m{0, 0, 0, 0};
+    if (i < nrows) {
+        m.r = rows[i];
+        m.e0 = A.uptr[m.r];
+        m.d = (uint32_t)(A.uptr[m.r + 1] - m.e0);
+        m.L = A.label[m.r];
+    }
+    return m;
+}
+
 template <int BLOCK, int HMAX, int F, int MINB, bool SYM>
 __global__ void __launch_bounds__(BLOCK, MINB) k_sweep_cta(SweepArgs<SYM> A, const int32_t *rows,
                                                             int64_t nrows, int32_t *ovf,
@@ -751,29 +780,42 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_sweep_cta(SweepArgs<SYM> A, con
         s_ovf = 0;
     }
     __syncthreads();
-    for (int64_t i = blockIdx.x; i < nrows; i += gridDim.x) {
-        const int32_t r = rows[i];
-        const int64_t e0 = A.uptr[r], d = A.uptr[r + 1] - e0;
-        const int32_t L = A.label[r];
-        const double2 sr = node_s(A, r);
-        const uint32_t H = min(tab_size(d, F, 32), (uint32_t)HMAX);
-        constexpr int U = 4;
-        const int32_t *nb = A.unbr + e0;
-        const uint32_t *ub = A.u32 + e0;
+    // software pipeline: the metadata of the row after next and the first entry chunk of
+    // the next row are loaded while the current row's selection runs
+    constexpr int U = 4;
+    const int64_t step = gridDim.x;
+    RowMeta cur = row_meta(A, rows, blockIdx.x, nrows);
+    RowMeta nxt = row_meta(A, rows, blockIdx.x + step, nrows);
+    int32_t z[U];
+    uint32_t wt[U];
+    load_raw<U, BLOCK>(A.unbr + cur.e0, A.u32 + cur.e0, cur.d, threadIdx.x, z, wt);
+    for (int64_t i = blockIdx.x; i < nrows; i += step) {
+        const double2 sr = node_s(A, cur.r);
+        const uint32_t H = min(tab_size(cur.d, F, 32), (uint32_t)HMAX);
+        const int32_t *nb = A.unbr + cur.e0;
+        const uint32_t *ub = A.u32 + cur.e0;
         uint32_t unused = 0;
-        for (uint32_t cb = 0; cb < (uint32_t)d; cb += BLOCK * U) {
+        {
             int32_t c[U];
-            uint32_t wt[U];
-            load_row<U, BLOCK>(nb, ub, A.label, (uint32_t)d, cb + threadIdx.x, c, wt);
+            gather_labels<U>(A.label, z, c);
             insert_chunk<U, true>(tsa, H - 1, c, wt, osa, &s_no, unused, &s_ovf);
         }
+        for (uint32_t cb = BLOCK * U; cb < cur.d; cb += BLOCK * U) {
+            int32_t c[U];
+            uint32_t w2[U];
+            load_row<U, BLOCK>(nb, ub, A.label, cur.d, cb + threadIdx.x, c, w2);
+            insert_chunk<U, true>(tsa, H - 1, c, w2, osa, &s_no, unused, &s_ovf);
+        }
         __syncthreads();
+        // prefetch: next row's first chunk, the metadata of the row after it
+        load_raw<U, BLOCK>(A.unbr + nxt.e0, A.u32 + nxt.e0, nxt.d, threadIdx.x, z, wt);
+        const RowMeta nn = row_meta(A, rows, i + 2 * step, nrows);
         const uint32_t no = s_no;
         if (s_ovf) {
-            if (threadIdx.x == 0) ovf[atomicAdd(novf, 1u)] = r;
+            if (threadIdx.x == 0) ovf[atomicAdd(novf, 1u)] = cur.r;
             if (A.stats && threadIdx.x == 0) atomicAdd(A.stats + 6, 1ull);
         } else {
-            block_select<BLOCK, SYM, false>(A, ctab, occ, no, r, L, sr, B);
+            block_select<BLOCK, SYM, false>(A, ctab, occ, no, cur.r, cur.L, sr, B);
         }
         occ_clear<false>(ctab, occ, no, threadIdx.x, BLOCK);
         __syncthreads();
@@ -781,6 +823,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_sweep_cta(SweepArgs<SYM> A, con
             s_no = 0;
             s_ovf = 0;
         }
+        cur = nxt;
+        nxt = nn;
     }
 }
 
