@@ -431,6 +431,117 @@ __global__ void k_bad_scatter(const int32_t *f, const int32_t *pos, int64_t nc, 
 }
 __global__ void k_init_i32(int32_t *x, int64_t n, int32_t v) { GS_LOOP(i, n) x[i] = v; }
 
+// ---- batched init of every part of a giant wave.  Parts are slices [lo, hi) of the layout
+// (members: gmark == pid); their concatenation is indexed by a flat index t.  Member rows are
+// cut into chunks of GCH entries (one warp per chunk), so hub members do not serialise a warp.
+constexpr int GCH = 1024;
+struct GSlice {
+    int64_t lo, hi, cbase, flat;   // flat: start of the slice in the concatenation
+    int32_t pid, pad;
+};
+__device__ __forceinline__ int slice_of(const GSlice *S, int ns, int64_t t) {
+    int a = 0, b = ns - 1;
+    while (a < b) {   // last slice with flat <= t
+        const int mid = (a + b + 1) >> 1;
+        if (S[mid].flat <= t) a = mid;
+        else b = mid - 1;
+    }
+    return a;
+}
+__global__ void k_gb_chunks(GiantArgs A, const GSlice *S, int ns, int64_t N, int32_t *nch) {
+    GS_LOOP(t, N) {
+        const GSlice sl = S[slice_of(S, ns, t)];
+        const int32_t x = A.order[sl.lo + (t - sl.flat)];
+        int32_t c = 0;
+        if (A.gmark[x] == sl.pid) {
+            const int64_t d = A.uptr[x + 1] - A.uptr[x];
+            c = (int32_t)((d + GCH - 1) / GCH);
+            A.wpart[x] = 0.0;
+        }
+        nch[t] = c;
+    }
+}
+__global__ void k_gb_expand(GiantArgs A, const GSlice *S, int ns, int64_t N, const int32_t *nch,
+                            const int64_t *choff, int64_t *chunks) {
+    GS_LOOP(t, N) {
+        const int64_t o = choff[t];
+        for (int32_t c = 0; c < nch[t]; c++) chunks[o + c] = (t << 22) | c;
+    }
+}
+__device__ __forceinline__ int32_t chunk_node(const GiantArgs &A, const GSlice *S, int ns, int64_t ck,
+                                              int64_t &e0, int64_t &e1) {
+    const int64_t t = ck >> 22, c = ck & 0x3FFFFF;
+    const GSlice sl = S[slice_of(S, ns, t)];
+    const int32_t x = A.order[sl.lo + (t - sl.flat)];
+    const int64_t b = A.uptr[x], d = A.uptr[x + 1] - b;
+    e0 = b + c * GCH;
+    e1 = b + min(d, (c + 1) * (int64_t)GCH);
+    return x;
+}
+__global__ void k_gb_wpart(GiantArgs A, const GSlice *S, int ns, const int64_t *chunks, int64_t nck) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t k = w; k < nck; k += nw) {
+        int64_t e0, e1;
+        const int32_t x = chunk_node(A, S, ns, chunks[k], e0, e1);
+        const int32_t pid = A.gmark[x];
+        double wp = 0.0;
+        for (int64_t e = e0 + lane; e < e1; e += 32)
+            if (A.gmark[A.unbr[e]] == pid) wp += A.uu[e];
+        wp = wsum_d(wp);
+        if (lane == 0 && wp != 0.0) atomicAdd(&A.wpart[x], wp);
+    }
+}
+__global__ void k_gb_dep(GiantArgs A, const GSlice *S, int ns, int64_t N) {
+    GS_LOOP(t, N) {
+        const GSlice sl = S[slice_of(S, ns, t)];
+        const int32_t x = A.order[sl.lo + (t - sl.flat)];
+        if (A.gmark[x] == sl.pid) A.dep[x] = A.wpart[x];
+    }
+}
+__global__ void k_gb_lca(GiantArgs A, const GSlice *S, int ns, const int64_t *chunks, int64_t nck) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t k = w; k < nck; k += nw) {
+        int64_t e0, e1;
+        const int32_t y = chunk_node(A, S, ns, chunks[k], e0, e1);
+        const int32_t pid = A.gmark[y];
+        for (int64_t e = e0 + lane; e < e1; e += 32) {
+            const int32_t z = A.unbr[e];
+            if (A.gmark[z] != pid) continue;
+            const int32_t pz = A.pos[z];
+            int32_t anc = y;
+            while (!in_range(A, anc, pz)) anc = A.a[anc];
+            atomicAdd(&A.dep[anc], -A.uu[e]);
+        }
+    }
+}
+__global__ void k_gb_gather(GiantArgs A, const GSlice *S, int ns, int64_t N, double *vso,
+                            double *vsi, double *vdp) {
+    GS_LOOP(t, N) {
+        const GSlice sl = S[slice_of(S, ns, t)];
+        const int32_t x = A.order[sl.lo + (t - sl.flat)];
+        const bool in = A.gmark[x] == sl.pid;
+        vso[t] = in ? A.s_out[x] : 0.0;
+        vsi[t] = in ? A.s_in[x] : 0.0;
+        vdp[t] = in ? A.dep[x] : 0.0;
+    }
+}
+__global__ void k_gb_subsums(GiantArgs A, const GSlice *S, int ns, int64_t N, const double *pso,
+                             const double *psi, const double *pdp) {
+    GS_LOOP(t, N) {
+        const GSlice sl = S[slice_of(S, ns, t)];
+        const int32_t x = A.order[sl.lo + (t - sl.flat)];
+        if (A.gmark[x] != sl.pid) continue;
+        const int64_t i0 = sl.flat + sl.cbase + A.pos[x] - sl.lo, i1 = i0 + A.sz[x];
+        A.sob[x] = pso[i1] - pso[i0];
+        A.sib[x] = psi[i1] - psi[i0];
+        A.xw[x] = pdp[i1] - pdp[i0];
+    }
+}
+
 static DBuf<uint32_t> g_stamp;   // monotone part stamps (never reset)
 
 // ------------------------------------------------ giant parts: one CTA per part
@@ -448,6 +559,17 @@ struct GPart {
     int64_t neg_off;         // region of hi-lo entries in the negative-member pool
     int64_t dirty_off;       // region of DIRTY_CAP entries in the dirty pool
 };
+
+__global__ void k_gb_totals(const GSlice *S, int ns, const double *pso, const double *psi,
+                            GPart *P) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < ns) {
+        const GSlice sl = S[i];
+        const int64_t a = sl.flat, b = sl.flat + (sl.hi - sl.lo);
+        P[i].so_c = pso[b] - pso[a];
+        P[i].si_c = psi[b] - psi[a];
+    }
+}
 
 struct GOut {
     // split log: (part pid, sequence, gain, child kind 0 small / 1 giant, child id)
@@ -926,6 +1048,22 @@ static void launch_small(slm_ctx *ctx, PosArgs &A, const std::vector<PartDesc> &
     CUDA_TRY(cudaStreamSynchronize(s));
 }
 
+struct PosScratch {
+    DBuf<int32_t> pbuf, pbuf2, tbuf, pmark, ppos, psz, gmark, flags;
+    DBuf<int2> sstk, sstk2;
+    DBuf<double> wpart, dep, pso, psi, pdp, gbuf, gbuf2, xw, sob, sib;
+    DBuf<int32_t> neg_pool, log_pid, log_seq, log_kind, log_child, cnt6, nx_pid, nx_root, nx_size,
+        posb, nch;
+    DBuf<double> log_gain, vso, vsi, vdp, pso2, psi2, pdp2;
+    DBuf<int64_t> nx_lo, nx_hi, choff, chunks;
+    DBuf<PartDesc> desc;
+    DBuf<uint8_t> gflag, negflag;
+    DBuf<unsigned long long> unres_d;
+    DBuf<GSlice> slices;
+    DBuf<int32_t> dirty_pool;
+    DBuf<GPart> dparts2;
+};
+
 void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_t scc_cap,
                   int64_t *splits, int64_t *unresolved, int *changed, std::vector<double> *gains) {
     (void)scc_cap;   // the scc_cut_cap branch needs cycles > cap >= 2: unreachable (F5)
@@ -936,6 +1074,14 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     *changed = 0;
     if (gains) gains->clear();
     if (m == 0.0 || n == 0) return;
+    const double t_call = now_ms();
+    const bool plog = getenv("SLM_POS_LOG") != nullptr;
+    double tp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    auto tmark = [&](int k) {
+        if (!plog) return;
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        tp[k] = now_ms();
+    };
     read_small_part();
     phase_mark(ctx, -1);
     DBuf<uint8_t> bad;
@@ -955,6 +1101,7 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     list.resize(nbad);
     k_bad_scatter<<<grid_for(nc, 256), 256, 0, s>>>(f.p, pos.p, nc, list.p);
     phase_mark(ctx, PH_POS_LG);
+    tmark(0);
     std::vector<int32_t> hbad(nbad), hcptr(nc + 1);
     CUDA_TRY(cudaMemcpyAsync(hbad.data(), list.p, nbad * 4, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(hcptr.data(), F.cptr.p, (nc + 1) * 4, cudaMemcpyDeviceToHost, s));
@@ -963,16 +1110,21 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
         CUDA_TRY(cudaMemsetAsync(g_stamp.p, 0, 4, s));
     }
     CUDA_TRY(cudaStreamSynchronize(s));
-    // scratch (n-sized)
-    DBuf<int32_t> pbuf, pbuf2, tbuf, pmark, ppos, psz, gmark, flags;
-    DBuf<int2> sstk, sstk2;
-    DBuf<double> wpart, dep, pso, psi, pdp, gbuf, gbuf2, xw, sob, sib;
+    // n-sized scratch, kept across calls (grow-only; pmark holds monotone stamps, so it is
+    // cleared only when reallocated)
+    static PosScratch SC;
+    DBuf<int32_t> &pbuf = SC.pbuf, &pbuf2 = SC.pbuf2, &tbuf = SC.tbuf, &pmark = SC.pmark,
+                  &ppos = SC.ppos, &psz = SC.psz, &gmark = SC.gmark, &flags = SC.flags;
+    DBuf<int2> &sstk = SC.sstk, &sstk2 = SC.sstk2;
+    DBuf<double> &wpart = SC.wpart, &dep = SC.dep, &pso = SC.pso, &psi = SC.psi, &pdp = SC.pdp,
+                 &gbuf = SC.gbuf, &gbuf2 = SC.gbuf2, &xw = SC.xw, &sob = SC.sob, &sib = SC.sib;
+    const bool fresh_pmark = pmark.cap < (size_t)n;
     pbuf.resize(n); pbuf2.resize(n); tbuf.resize(n); pmark.resize(n); ppos.resize(n);
     psz.resize(n); gmark.resize(n); sstk.resize(n); sstk2.resize(n);
     wpart.resize(n); dep.resize(n); pso.resize(n); psi.resize(n); pdp.resize(n);
     gbuf.resize(n); gbuf2.resize(n);
     flags.resize(2);
-    CUDA_TRY(cudaMemsetAsync(pmark.p, 0, n * 4, s));
+    if (fresh_pmark) CUDA_TRY(cudaMemsetAsync(pmark.p, 0, n * 4, s));
     CUDA_TRY(cudaMemsetAsync(flags.p, 0, 8, s));
     PosArgs A;
     A.uptr = G.uptr.p;
@@ -999,6 +1151,7 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     A.gains = gbuf.p;
     A.stamp_ctr = g_stamp.p;
     A.flags = flags.p;
+    tmark(1);
     // 1. small bad communities straight from the layout
     std::vector<PartDesc> small1;
     std::vector<int64_t> order_kind(nbad);   // >=0: small1 index, <0: -(giant id)-1
@@ -1033,6 +1186,7 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     // 2. giant communities: one CTA per part with incremental state (k_giant_cta), in waves
     //    (a cut subtree larger than SMALL_PART becomes a part of the next wave); small cut
     //    subtrees are collected for a second warp-executor batch
+    tmark(2);
     std::vector<PartDesc> small2;
     std::vector<int32_t> l_pid, l_seq, l_kind, l_child;
     std::vector<double> l_gain;
@@ -1063,13 +1217,16 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
         GA.m2 = m * m;
         k_init_i32<<<grid_for(n, 256), 256, 0, s>>>(gmark.p, n, 0);
         // pools
-        DBuf<int32_t> neg_pool, log_pid, log_seq, log_kind, log_child, cnt6, nx_pid, nx_root,
-            nx_size, posb;
-        DBuf<double> log_gain, vso, vsi, vdp, pso2, psi2, pdp2;
-        DBuf<int64_t> nx_lo, nx_hi;
-        DBuf<PartDesc> desc;
-        DBuf<uint8_t> gflag, negflag;
-        DBuf<unsigned long long> unres_d;
+        DBuf<int32_t> &neg_pool = SC.neg_pool, &log_pid = SC.log_pid, &log_seq = SC.log_seq,
+                      &log_kind = SC.log_kind, &log_child = SC.log_child, &cnt6 = SC.cnt6,
+                      &nx_pid = SC.nx_pid, &nx_root = SC.nx_root, &nx_size = SC.nx_size,
+                      &posb = SC.posb;
+        DBuf<double> &log_gain = SC.log_gain, &vso = SC.vso, &vsi = SC.vsi, &vdp = SC.vdp,
+                     &pso2 = SC.pso2, &psi2 = SC.psi2, &pdp2 = SC.pdp2;
+        DBuf<int64_t> &nx_lo = SC.nx_lo, &nx_hi = SC.nx_hi;
+        DBuf<PartDesc> &desc = SC.desc;
+        DBuf<uint8_t> &gflag = SC.gflag, &negflag = SC.negflag;
+        DBuf<unsigned long long> &unres_d = SC.unres_d;
         neg_pool.resize(n);
         log_pid.resize(n);
         log_seq.resize(n);
@@ -1129,49 +1286,89 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
             giant_pid.push_back(gp.pid);
             k_g_mark<<<grid_for(gp.hi - gp.lo, 256), 256, 0, s>>>(F.order.p, gp.lo, gp.hi, gp.pid,
                                                                    gmark.p);
-            CUDA_TRY(cudaMemcpyAsync(&gp.root, F.order.p + gp.lo, 4, cudaMemcpyDeviceToHost, s));
-            CUDA_TRY(cudaStreamSynchronize(s));
             wave.push_back(gp);
         }
+        {   // roots: the first layout member of each community
+            std::vector<int32_t> roots(wave.size());
+            for (size_t i = 0; i < wave.size(); i++)
+                CUDA_TRY(cudaMemcpyAsync(&roots[i], F.order.p + wave[i].lo, 4,
+                                         cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            for (size_t i = 0; i < wave.size(); i++) wave[i].root = roots[i];
+        }
         CUDA_TRY(cudaMemcpyAsync(cnt6.p + 4, &next_pid, 4, cudaMemcpyHostToDevice, s));
-        DBuf<GPart> dparts2;
-        DBuf<int32_t> dirty_pool;
+        DBuf<GPart> &dparts2 = SC.dparts2;
+        DBuf<int32_t> &dirty_pool = SC.dirty_pool;
+        tmark(6);
         while (!wave.empty()) {
-            // init pass of every part: w_part, LCA deposits, subtree sums, part totals
-            for (GPart &gp : wave) {
-                const int64_t lo = gp.lo, hi = gp.hi, N = hi - lo;
-                const unsigned GW = grid_for(N * 32, 256, 148LL * 32);
-                const unsigned GN = grid_for(N, 256);
-                k_g_wpart<<<GW, 256, 0, s>>>(GA, lo, hi, gp.pid);
-                k_g_lca<<<GW, 256, 0, s>>>(GA, lo, hi, gp.pid);
-                vso.resize(N + 1);
-                vsi.resize(N + 1);
-                vdp.resize(N + 1);
-                pso2.resize(N + 1);
-                psi2.resize(N + 1);
-                pdp2.resize(N + 1);
-                k_g_gather<<<GN, 256, 0, s>>>(GA, lo, hi, gp.pid, vso.p, vsi.p, vdp.p);
-                CUDA_TRY(cudaMemsetAsync(vso.p + N, 0, 8, s));
-                CUDA_TRY(cudaMemsetAsync(vsi.p + N, 0, 8, s));
-                CUDA_TRY(cudaMemsetAsync(vdp.p + N, 0, 8, s));
+            tmark(6);
+            // init pass of every part of the wave, batched: w_part, LCA deposits, subtree
+            // sums (one exclusive scan over the concatenated slices), part totals
+            const int ns = (int)wave.size();
+            std::vector<GSlice> hs(ns);
+            int64_t N = 0;
+            for (int i = 0; i < ns; i++) {
+                hs[i].lo = wave[i].lo;
+                hs[i].hi = wave[i].hi;
+                hs[i].cbase = wave[i].cbase;
+                hs[i].flat = N;
+                hs[i].pid = wave[i].pid;
+                hs[i].pad = 0;
+                N += wave[i].hi - wave[i].lo;
+            }
+            SC.slices.resize(ns);
+            CUDA_TRY(cudaMemcpyAsync(SC.slices.p, hs.data(), ns * sizeof(GSlice),
+                                     cudaMemcpyHostToDevice, s));
+            const GSlice *dsl = SC.slices.p;
+            SC.nch.resize(N + 1);
+            SC.choff.resize(N + 1);
+            CUDA_TRY(cudaMemsetAsync(SC.nch.p + N, 0, 4, s));
+            k_gb_chunks<<<grid_for(N, 256), 256, 0, s>>>(GA, dsl, ns, N, SC.nch.p);
+            {
+                size_t tb = 0;
+                CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, SC.nch.p, SC.choff.p, N + 1, s));
+                ctx->tmp.resize(tb);
+                CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx->tmp.p, tb, SC.nch.p, SC.choff.p, N + 1, s));
+            }
+            int64_t nck = 0;
+            CUDA_TRY(cudaMemcpyAsync(&nck, SC.choff.p + N, 8, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            SC.chunks.resize(std::max<int64_t>(1, nck));
+            k_gb_expand<<<grid_for(N, 256), 256, 0, s>>>(GA, dsl, ns, N, SC.nch.p, SC.choff.p,
+                                                        SC.chunks.p);
+            const unsigned GW = grid_for(nck * 32, 256, 148LL * 32);
+            k_gb_wpart<<<GW, 256, 0, s>>>(GA, dsl, ns, SC.chunks.p, nck);
+            k_gb_dep<<<grid_for(N, 256), 256, 0, s>>>(GA, dsl, ns, N);
+            k_gb_lca<<<GW, 256, 0, s>>>(GA, dsl, ns, SC.chunks.p, nck);
+            vso.resize(N + 1);
+            vsi.resize(N + 1);
+            vdp.resize(N + 1);
+            pso2.resize(N + 1);
+            psi2.resize(N + 1);
+            pdp2.resize(N + 1);
+            k_gb_gather<<<grid_for(N, 256), 256, 0, s>>>(GA, dsl, ns, N, vso.p, vsi.p, vdp.p);
+            CUDA_TRY(cudaMemsetAsync(vso.p + N, 0, 8, s));
+            CUDA_TRY(cudaMemsetAsync(vsi.p + N, 0, 8, s));
+            CUDA_TRY(cudaMemsetAsync(vdp.p + N, 0, 8, s));
+            {
                 size_t tb = 0;
                 CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, vso.p, pso2.p, N + 1, s));
                 ctx->tmp.resize(tb);
                 CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx->tmp.p, tb, vso.p, pso2.p, N + 1, s));
                 CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx->tmp.p, tb, vsi.p, psi2.p, N + 1, s));
                 CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx->tmp.p, tb, vdp.p, pdp2.p, N + 1, s));
-                k_g_subsums<<<GN, 256, 0, s>>>(GA, lo, hi, gp.cbase, gp.pid, pso2.p, psi2.p, pdp2.p,
-                                                nullptr);
-                CUDA_TRY(cudaMemcpyAsync(&gp.so_c, pso2.p + N, 8, cudaMemcpyDeviceToHost, s));
-                CUDA_TRY(cudaMemcpyAsync(&gp.si_c, psi2.p + N, 8, cudaMemcpyDeviceToHost, s));
-                CUDA_TRY(cudaStreamSynchronize(s));
             }
+            k_gb_subsums<<<grid_for(N, 256), 256, 0, s>>>(GA, dsl, ns, N, pso2.p, psi2.p, pdp2.p);
+            tmark(7);
+            tp[3] += tp[7] - tp[6];
             const int64_t np = (int64_t)wave.size();
             dirty_pool.resize(np * DIRTY_CAP);
             for (int64_t i = 0; i < np; i++) wave[i].dirty_off = i * DIRTY_CAP;
             dparts2.resize(np);
             CUDA_TRY(cudaMemcpyAsync(dparts2.p, wave.data(), np * sizeof(GPart),
                                      cudaMemcpyHostToDevice, s));
+            k_gb_totals<<<(unsigned)((np + 127) / 128), 128, 0, s>>>(dsl, ns, pso2.p, psi2.p,
+                                                                     dparts2.p);
             CUDA_TRY(cudaMemsetAsync(cnt6.p + 3, 0, 4, s));
             k_giant_cta<<<(unsigned)np, GB, 0, s>>>(GA, dparts2.p, O, neg_pool.p, dirty_pool.p,
                                                     gflag.p, negflag.p);
@@ -1179,6 +1376,7 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
             int32_t nnext = 0;
             CUDA_TRY(cudaMemcpyAsync(&nnext, cnt6.p + 3, 4, cudaMemcpyDeviceToHost, s));
             CUDA_TRY(cudaStreamSynchronize(s));
+            if (plog) tp[4] += now_ms() - tp[7];
             wave.clear();
             if (nnext > 0) {
                 std::vector<int64_t> hlo(nnext), hhi(nnext);
@@ -1202,12 +1400,12 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
                     wave.push_back(gp);
                 }
                 // cbase: the community layout base of the part (pos[] is community-relative)
-                for (GPart &gp : wave) {
-                    int32_t pr = 0;
-                    CUDA_TRY(cudaMemcpyAsync(&pr, F.pos.p + gp.root, 4, cudaMemcpyDeviceToHost, s));
-                    CUDA_TRY(cudaStreamSynchronize(s));
-                    gp.cbase = gp.lo - pr;
-                }
+                std::vector<int32_t> prs(wave.size());
+                for (size_t i = 0; i < wave.size(); i++)
+                    CUDA_TRY(cudaMemcpyAsync(&prs[i], F.pos.p + wave[i].root, 4,
+                                             cudaMemcpyDeviceToHost, s));
+                CUDA_TRY(cudaStreamSynchronize(s));
+                for (size_t i = 0; i < wave.size(); i++) wave[i].cbase = wave[i].lo - prs[i];
             }
         }
         int32_t hc[4];
@@ -1250,6 +1448,16 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     int32_t hflags[2];
     CUDA_TRY(cudaMemcpyAsync(hflags, flags.p, 8, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
+    if (getenv("SLM_POS_LOG")) {
+        int64_t gm = 0;
+        for (int32_t c : giant_comm) gm += hcptr[c + 1] - hcptr[c];
+        fprintf(stderr, "[positive] bad %d (small %zu) giant %zu members %lld | giant splits %zu "
+                "unresolved %lld small2 %zu | total splits %lld unres %lld | %.1f ms: lg %.1f "
+                "alloc %.1f small1 %.1f ginit %.1f gcta %.1f\n", nbad,
+                small1.size(), giant_comm.size(), (long long)gm, l_pid.size(), (long long)gunres,
+                small2.size(), (long long)tot, (long long)un, now_ms() - t_call, tp[0] - t_call,
+                tp[1] - tp[0], tp[2] - tp[1], tp[3], tp[4]);
+    }
     phase_mark(ctx, PH_POS_GIANT);
     SLM_REQUIRE(!hflags[1], SLM_EUNSUP, "assignment cycle longer than 2 in POSITIVE");
     *splits = tot;
