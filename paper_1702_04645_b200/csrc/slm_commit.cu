@@ -576,17 +576,40 @@ __global__ void k_gather_gains(int64_t K, const int32_t *f, const int32_t *pos, 
     GS_LOOP(k, K) if (f[k]) out[pos[k]] = g[k];
 }
 
+// per-call scratch of run_commit, kept across calls (grow-only)
+struct CommitScratch {
+    DBuf<int32_t> flag, pos, cand;
+    DBuf<int32_t> status;
+    DBuf<uint8_t> moving;
+    DBuf<CandSpec> spec;
+    DBuf<int64_t> mvcnt, mvoff;
+    DBuf<int32_t> mv_z;
+    DBuf<double> mv_u;
+    DBuf<int64_t> mv_e;
+    DBuf<uint8_t> mv_i;
+    DBuf<int32_t> af, apos;
+    DBuf<int32_t> lab, cnt, first_commit, wpos, atk, tl_ptr, tl_ev, wl, remaining;
+    DBuf<double> So, Si, gbuf;
+    DBuf<uint8_t> dirty;
+    DBuf<uint32_t> keys, keys_sorted;
+    DBuf<int32_t> vals;
+    DBuf<int32_t> wf, wp;
+    DBuf<int32_t> cf, cpos;
+    DBuf<double> gg;
+};
+
 void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const int32_t *d_cstar,
                 uint64_t seed, double accept_prob, int64_t level, int64_t sweep, int *improved,
                 int64_t *applied, std::vector<double> *gains) {
     cudaStream_t s = ctx->stream;
+    static CommitScratch CS;
     const int64_t n = G.n, nc = F.n_comms;
     *improved = 0;
     *applied = 0;
     ctx->last_rounds = 0;
     phase_mark(ctx, -1);
     // candidates: cstar != label, ascending (detector.py:473)
-    DBuf<int32_t> flag, pos, cand;
+    DBuf<int32_t> &flag = CS.flag, &pos = CS.pos, &cand = CS.cand;
     flag.resize(n + 1);
     pos.resize(n + 1);
     CUDA_TRY(cudaMemsetAsync(flag.p + n, 0, 4, s));
@@ -599,8 +622,8 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     if (K == 0) return;
     cand.resize(K);
     k_cand_scatter<<<grid_for(n, 256), 256, 0, s>>>(flag.p, pos.p, n, cand.p);
-    DBuf<int32_t> status;
-    DBuf<uint8_t> moving;
+    DBuf<int32_t> &status = CS.status;
+    DBuf<uint8_t> &moving = CS.moving;
     status.resize(K);
     moving.resize(n);
     k_coins<<<grid_for(K, 256), 256, 0, s>>>(cand.p, K, mix_key2(seed, level, sweep), accept_prob,
@@ -621,7 +644,7 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     A.cstar = d_cstar;
     A.m = m;
     A.m2 = m * m;
-    DBuf<CandSpec> spec;
+    DBuf<CandSpec> &spec = CS.spec;
     spec.resize(K);
     phase_mark(ctx, PH_CAND);
     unsigned GW = grid_for((int64_t)K * 32, 256, 148LL * 32);
@@ -629,11 +652,11 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     CUDA_TRY(cudaMemsetAsync(moving.p, 0, n, s));
     k_mark_moving<<<GW, 256, 0, s>>>(cand.p, F.comm.p, F.on_cycle.p, F.cptr.p, F.pos.p, F.sz.p,
                                      F.order.p, K, status.p, moving.p);
-    DBuf<int64_t> mvcnt, mvoff;
-    DBuf<int32_t> mv_z;
-    DBuf<double> mv_u;
-    DBuf<int64_t> mv_e;
-    DBuf<uint8_t> mv_i;
+    DBuf<int64_t> &mvcnt = CS.mvcnt, &mvoff = CS.mvoff;
+    DBuf<int32_t> &mv_z = CS.mv_z;
+    DBuf<double> &mv_u = CS.mv_u;
+    DBuf<int64_t> &mv_e = CS.mv_e;
+    DBuf<uint8_t> &mv_i = CS.mv_i;
     mvcnt.resize(K + 1);
     mvoff.resize(K + 1);
     CUDA_TRY(cudaMemsetAsync(mvcnt.p, 0, (K + 1) * 8, s));
@@ -651,7 +674,7 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     k_mv_scan<<<GW, 256, 0, s>>>(A, K, status.p, spec.p, moving.p, 1, nullptr, mv_z.p, mv_u.p,
                                  mv_e.p, mv_i.p);
     // accepted candidates -> (community, k) pairs -> timelines
-    DBuf<int32_t> af, apos;
+    DBuf<int32_t> &af = CS.af, &apos = CS.apos;
     af.resize(K + 1);
     apos.resize(K + 1);
     CUDA_TRY(cudaMemsetAsync(af.p + K, 0, 4, s));
@@ -662,9 +685,9 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     CUDA_TRY(cudaStreamSynchronize(s));
     ctx->last_accepted = NA;
     // live state
-    DBuf<int32_t> lab, cnt, first_commit, wpos, atk, tl_ptr, tl_ev, wl, remaining;
-    DBuf<double> So, Si, gbuf;
-    DBuf<uint8_t> dirty;
+    DBuf<int32_t> &lab = CS.lab, &cnt = CS.cnt, &first_commit = CS.first_commit, &wpos = CS.wpos, &atk = CS.atk, &tl_ptr = CS.tl_ptr, &tl_ev = CS.tl_ev, &wl = CS.wl, &remaining = CS.remaining;
+    DBuf<double> &So = CS.So, &Si = CS.Si, &gbuf = CS.gbuf;
+    DBuf<uint8_t> &dirty = CS.dirty;
     lab.resize(n);
     cnt.resize(nc);
     first_commit.resize(nc);
@@ -680,8 +703,8 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     CUDA_TRY(cudaMemsetAsync(dirty.p, 0, nc, s));
     CUDA_TRY(cudaMemsetAsync(first_commit.p, 0x7f, nc * 4, s));   // 0x7f7f7f7f > any k
     if (NA > 0) {
-        DBuf<uint32_t> keys, keys_sorted;
-        DBuf<int32_t> vals;
+        DBuf<uint32_t> &keys = CS.keys, &keys_sorted = CS.keys_sorted;
+        DBuf<int32_t> &vals = CS.vals;
         keys.resize(2 * (int64_t)NA);
         keys_sorted.resize(2 * (int64_t)NA);
         vals.resize(2 * (int64_t)NA);
@@ -693,7 +716,7 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
         tl_ptr.resize(nc + 1);
         k_lb32c<<<grid_for(nc + 1, 256), 256, 0, s>>>(keys_sorted.p, 2 * (int64_t)NA, nc, tl_ptr.p);
         // walkers: communities with a non-empty timeline
-        DBuf<int32_t> wf, wp;
+        DBuf<int32_t> &wf = CS.wf, &wp = CS.wp;
         wf.resize(nc + 1);
         wp.resize(nc + 1);
         wpos.resize(nc);
@@ -753,7 +776,7 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     const unsigned GK = grid_for(K, 256);
     k_coin_blocked<<<GK, 256, 0, s>>>(cand.p, F.comm.p, K, status.p, first_commit.p, dflags);
     // applied + gains in ascending candidate order
-    DBuf<int32_t> cf, cpos;
+    DBuf<int32_t> &cf = CS.cf, &cpos = CS.cpos;
     cf.resize(K + 1);
     cpos.resize(K + 1);
     CUDA_TRY(cudaMemsetAsync(cf.p + K, 0, 4, s));
@@ -766,7 +789,7 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     *applied = hv[0];
     *improved = (hv[0] > 0) || hv[1];
     if (gains && hv[0] > 0) {
-        DBuf<double> gg;
+        DBuf<double> &gg = CS.gg;
         gg.resize(hv[0]);
         k_gather_gains<<<GK, 256, 0, s>>>(K, cf.p, cpos.p, gbuf.p, gg.p);
         gains->resize(hv[0]);
