@@ -188,6 +188,8 @@ def main():
     ap.add_argument("--cpu-entries", type=float, default=6e7,
                     help="union entries in the CPU-baseline row sample")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-partition", action="store_true",
+                    help="skip the end-to-end seconds-to-final-partition runs")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -340,12 +342,60 @@ def main():
             "cores": threads, "kind": "port",
             "sample": f"_best_targets over rows [0,{sample['R']}) ({sample['entries']} union "
                       f"entries) of the same snapshot; targets equal to the GPU's: {ok}"}
+    if not args.no_partition:
+        line["partition"] = partition_runs(ctx, args, rank, threads)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
         import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()
+
+
+def partition_runs(ctx, args, rank, threads):
+    """BASELINE's second metric: end-to-end seconds to the final hierarchy.  (1) the workload
+    config, graph already in HBM (device-generated), full level loop through the public
+    run(); (2) C2 (DC-SBM, 10^5 nodes) from host edges through Graph.from_edges + run(),
+    next to the C oracle's full hierarchy on the host cores (same partitions required)."""
+    from paper_1702_04645_b200 import RunConfig, detector, generators as GN
+    from paper_1702_04645_b200.graph import Graph
+    out = {}
+    info = ctx.info()
+    g = Graph(info["n"], None, None, None)
+    g._ctx = ctx
+    ctx.level = 0
+    torch_sync = __import__("torch").cuda.synchronize
+    torch_sync()
+    t0 = time.perf_counter()
+    res = detector.run(g, RunConfig())
+    el = time.perf_counter() - t0
+    out[args.config] = {"seconds": round(el, 3), "levels": len(res.hierarchy.levels),
+                        "sweeps_per_level": res.stats.sweeps_per_level,
+                        "modularity": res.final_score,
+                        "phase_seconds": {k: round(v, 3) for k, v in res.stats.phase_seconds.items()},
+                        "input": "graph resident in HBM (device generator); timed: run()"}
+    if rank == 0:
+        n, s, d, w = GN.generate("c2_dcsbm")
+        t0 = time.perf_counter()
+        g2 = Graph.from_edges(n, s, d, w)
+        r2 = detector.run(g2, RunConfig())
+        gpu_s = time.perf_counter() - t0
+        c2 = {"seconds": round(gpu_s, 3), "levels": len(r2.hierarchy.levels),
+              "modularity": r2.final_score,
+              "input": "host edge list; timed: Graph.from_edges + run()"}
+        if not args.no_cpu:
+            from oracle import oracle as O
+            O.build()
+            O.set_threads(threads)
+            t0 = time.perf_counter()
+            ro = O.run(n, s, d, w)
+            c2["cpu_port_seconds"] = round(time.perf_counter() - t0, 3)
+            c2["cpu_cores"] = threads
+            c2["same_partition"] = bool(
+                len(ro.levels) == len(r2.hierarchy.levels)
+                and all(np.array_equal(a, b) for a, b in zip(ro.levels, r2.hierarchy.levels)))
+        out["c2_dcsbm"] = c2
+    return out
 
 
 if __name__ == "__main__":

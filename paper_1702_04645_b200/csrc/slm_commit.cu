@@ -764,7 +764,7 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
         }
         if (ctx->prof && getenv("SLM_PROFILE_WALK")) {
             fprintf(stderr, "walk K=%d NA=%d NW=%d rounds=%zu ms:", K, NA, NW, rt.size());
-            for (size_t q = 0; q < rt.size() && q < 8; q++) fprintf(stderr, " %.2f", rt[q]);
+            for (size_t q = 0; q < rt.size(); q++) fprintf(stderr, " %.2f", rt[q]);
             double tot = 0;
             for (double x : rt) tot += x;
             fprintf(stderr, " total %.2f\n", tot);
