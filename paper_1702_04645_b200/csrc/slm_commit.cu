@@ -22,6 +22,7 @@
 // Tails are contiguous ranges of the community DFS layout (slm_forest.cu): a cycle node's
 // tail is its whole community, any other node's tail is its DFS subtree.
 #include "slm_internal.cuh"
+#include <string>
 #include <cub/cub.cuh>
 
 #define GS_LOOP(i, n)                                                                      \
@@ -374,6 +375,7 @@ struct Live {
     MvList mv;
     double *gain;
     int32_t *remaining;
+    unsigned long long *wst;   // SLM_PROFILE_WALK counters (else nullptr)
 };
 
 __device__ __forceinline__ int32_t vload(const int32_t *p) { return *(volatile const int32_t *)p; }
@@ -387,7 +389,9 @@ __device__ __forceinline__ uint8_t vload8(const uint8_t *p) { return *(volatile 
 // prefetched by the lanes (their static data, and for events C evaluates the source's
 // position / dirty flag / strengths -- final once the source is parked at the event), then
 // walked in order with shuffles; a long chain into C therefore costs no global round trip
-// per event unless its source has not reached it yet.
+// per event unless its source has not reached it yet.  A candidate's status is written only
+// by its target's walker (plain store; the source side merely moves past a certain skip),
+// so resolutions need no CAS and `remaining` is decremented once per walker visit.
 __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_t *wl, int64_t nw_,
                                               int32_t *status, const CandSpec *spec) {
     const int lane = threadIdx.x & 31;
@@ -401,7 +405,11 @@ __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_
         __threadfence();
         double SoC = V.S_out[C], SiC = V.S_in[C];
         int32_t cntC = V.cnt[C];
+        int32_t my_atk = V.atk[C];          // only this walker writes atk[C]
+        int dirtyC = vload8(V.dirty + C);   // monotone
+        int nres = 0;                       // candidates resolved by this visit
         bool parked = false;
+        const int32_t p_start = p;
         while (p < end && !parked) {
             const int nb = min(32, end - p);
             int32_t k = -1, i = 0, frm = 0, to = 0, atF = -1, st = ST_SKIP;
@@ -432,20 +440,20 @@ __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_
                 const int32_t tq = __shfl_sync(0xffffffffu, to, q);
                 int32_t sq = __shfl_sync(0xffffffffu, st, q);
                 if (tq != C) {
-                    // C is the source side: resolved already, or a certain skip (C touched by
-                    // an earlier commit: dirty is final here since C's timeline is at kq), or
-                    // wait for the target walker's verdict
-                    if (sq == ST_UNRES) sq = vload(status + kq);
-                    // short-circuit only if C never offered kq to its target walker
-                    if (sq == ST_UNRES && vload(V.atk + C) != kq && vload8(V.dirty + C)) {
-                        if (lane == 0) resolve_skip(status, kq, V.remaining);
-                        continue;
+                    // C is the source side: resolved already (COMMIT changed our state), a
+                    // certain skip (C touched by an earlier commit -- final while C's timeline
+                    // is at kq -- and kq never offered), or wait for the target's verdict
+                    if (sq == ST_UNRES && my_atk != kq) {
+                        if (!dirtyC) dirtyC = vload8(V.dirty + C);
+                        if (dirtyC) continue;
                     }
+                    if (sq == ST_UNRES) sq = vload(status + kq);
                     if (sq == ST_UNRES) {
-                        if (lane == 0) {
+                        if (lane == 0 && my_atk != kq) {
                             __threadfence();
                             *(volatile int32_t *)(V.atk + C) = kq;
                         }
+                        my_atk = kq;
                         parked = true;
                         p += q;
                         break;
@@ -455,39 +463,44 @@ __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_
                         SoC = V.S_out[C];
                         SiC = V.S_in[C];
                         cntC = V.cnt[C];
+                        dirtyC = 1;
                     }
                     continue;
                 }
-                // C evaluates kq.  Already resolved by the source side, or a certain skip
-                // (source dirty -- dirty flags are monotone and only commits before kq can
-                // have set it -- or target empty), or frm's walker must have reached kq.
+                // C evaluates kq (only C's walker resolves it).  A certain skip when the
+                // source is dirty (monotone; only commits before kq can have set it) or the
+                // target is empty; otherwise frm's walker must have reached kq.
                 if (sq != ST_UNRES) continue;
                 int32_t aq = __shfl_sync(0xffffffffu, atF, q);
                 int dq = __shfl_sync(0xffffffffu, dF, q);
                 double SoFq = __shfl_sync(0xffffffffu, SoF, q);
                 double SiFq = __shfl_sync(0xffffffffu, SiF, q);
                 if (cntC == 0 || dq) {
-                    if (lane == 0) resolve_skip(status, kq, V.remaining);
+                    if (lane == 0) *(volatile int32_t *)(status + kq) = ST_SKIP;
+                    nres++;
                     continue;
                 }
                 if (aq != kq) {   // not parked at kq when prefetched: look again
                     aq = vload(V.atk + fq);
                     if (aq != kq) {
                         if (vload8(V.dirty + fq)) {
-                            if (lane == 0) resolve_skip(status, kq, V.remaining);
+                            if (lane == 0) *(volatile int32_t *)(status + kq) = ST_SKIP;
+                            nres++;
                             continue;
                         }
-                        if (lane == 0) {
+                        if (lane == 0 && my_atk != kq) {
                             __threadfence();
                             *(volatile int32_t *)(V.atk + C) = kq;
                         }
+                        my_atk = kq;
                         parked = true;
                         p += q;
                         break;
                     }
                     __threadfence();
                     if (vload8(V.dirty + fq)) {
-                        if (lane == 0) resolve_skip(status, kq, V.remaining);
+                        if (lane == 0) *(volatile int32_t *)(status + kq) = ST_SKIP;
+                        nres++;
                         continue;
                     }
                     SoFq = V.S_out[fq];
@@ -509,8 +522,13 @@ __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_
                 uint8_t verdict = ST_SKIP;
                 double wt = c.w_to;
                 int32_t j = c.j;
-                if (c.mv_cnt > 0 && vload8(V.dirty + C))
+                if (c.mv_cnt > 0 && dirtyC) {
                     reprice(A, V.mv, V.lab, c, iq, C, wt, j);
+                    if (V.wst && lane == 0) {
+                        atomicAdd(V.wst + 3, 1ull);
+                        atomicAdd(V.wst + 4, (unsigned long long)c.mv_cnt);
+                    }
+                }
                 const double so_b = c.so_b, si_b = c.si_b;
                 // gain_switch d_null (quality.py:216-219), exact operand order
                 const double d_null = -SoFq * si_b - so_b * SiFq + SoC * si_b + so_b * SiC +
@@ -519,10 +537,12 @@ __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_
                 if (g > 0.0 && j >= 0) verdict = ST_COMMIT;   // detector.py:498-502
                 if (verdict == ST_COMMIT) {
                     const int32_t len = c.tail_hi - c.tail_lo;
+                    if (V.wst && lane == 0) atomicAdd(V.wst + 5, (unsigned long long)len);
                     for (int32_t t = c.tail_lo + lane; t < c.tail_hi; t += 32) V.lab[A.order[t]] = C;
                     SoC += c.so_b;
                     SiC += c.si_b;
                     cntC += len;
+                    dirtyC = 1;
                     if (lane == 0) {
                         V.a[iq] = j;
                         // move_nodes (quality.py:87-95)
@@ -541,14 +561,20 @@ __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_
                 }
                 __syncwarp();
                 if (lane == 0) {
-                    __threadfence();
-                    if (atomicCAS(status + kq, ST_UNRES, (int32_t)verdict) == ST_UNRES)
-                        atomicSub(V.remaining, 1);
+                    if (verdict == ST_COMMIT) __threadfence();   // state, labels before verdict
+                    *(volatile int32_t *)(status + kq) = (int32_t)verdict;
                 }
+                nres++;
             }
             if (!parked) p += nb;
         }
+        if (V.wst && lane == 0 && p > p_start) {
+            atomicAdd(V.wst, (unsigned long long)(p - p_start));
+            atomicMax(V.wst + 1, (unsigned long long)(p - p_start));
+            atomicAdd(V.wst + 2, 1ull);
+        }
         if (lane == 0) {
+            if (nres) atomicSub(V.remaining, nres);
             V.wpos[C] = p;
             if (p >= end) {
                 __threadfence();
@@ -753,18 +779,35 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
         const unsigned GWK = grid_for((int64_t)NW * 32, 256, 148LL * 64);
         int32_t rem = NA;
         std::vector<double> rt;
+        const bool wprof = ctx->prof && getenv("SLM_PROFILE_WALK");
+        static DBuf<unsigned long long> wst;
+        V.wst = nullptr;
+        std::vector<std::string> rinfo;
+        if (wprof) {
+            wst.resize(8);
+            V.wst = wst.p;
+        }
         for (int round = 0; rem > 0; round++) {
+            if (wprof) CUDA_TRY(cudaMemsetAsync(wst.p, 0, 64, s));
             const double t0 = ctx->prof ? now_ms() : 0.0;
             k_walk<<<GWK, 256, 0, s>>>(A, V, wl.p, NW, status.p, spec.p);
             CUDA_TRY(cudaMemcpyAsync(&rem, remaining.p, 4, cudaMemcpyDeviceToHost, s));
             CUDA_TRY(cudaStreamSynchronize(s));
             if (ctx->prof) rt.push_back(now_ms() - t0);
+            if (wprof) {
+                unsigned long long h[8];
+                CUDA_TRY(cudaMemcpy(h, wst.p, 64, cudaMemcpyDeviceToHost));
+                char buf[160];
+                snprintf(buf, sizeof buf, "[%.2fms ev %llu max %llu w %llu rp %llu/%llu tl %llu]",
+                         rt.back(), h[0], h[1], h[2], h[3], h[4], h[5]);
+                rinfo.push_back(buf);
+            }
             ctx->last_rounds = round + 1;
             SLM_REQUIRE(round < 10000000, SLM_ESTATE, "commit walkers made no progress");
         }
         if (ctx->prof && getenv("SLM_PROFILE_WALK")) {
             fprintf(stderr, "walk K=%d NA=%d NW=%d rounds=%zu ms:", K, NA, NW, rt.size());
-            for (size_t q = 0; q < rt.size(); q++) fprintf(stderr, " %.2f", rt[q]);
+            for (size_t q = 0; q < rinfo.size(); q++) fprintf(stderr, " %s", rinfo[q].c_str());
             double tot = 0;
             for (double x : rt) tot += x;
             fprintf(stderr, " total %.2f\n", tot);
