@@ -343,9 +343,16 @@ __global__ void __launch_bounds__(256) k_local_gains(const int64_t *uptr, const 
     }
 }
 
+void run_local_gains_u32(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, double *d_lg,
+                         uint8_t *d_bad);
+
 void run_local_gains(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, double *d_lg,
                      uint8_t *d_bad) {
     int64_t n = G.n;
+    if (G.u32_ok) {
+        run_local_gains_u32(ctx, G, F, m, d_lg, d_bad);
+        return;
+    }
     k_local_gains<<<grid_for(n * 32, 256, 148LL * 64), 256, 0, ctx->stream>>>(
         G.uptr.p, G.unbr.p, G.uu.p, F.comm.p, F.S_out.p, F.S_in.p, G.s_out.p, G.s_in.p, n, m,
         d_lg, d_bad);

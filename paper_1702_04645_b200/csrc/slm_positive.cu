@@ -430,6 +430,9 @@ __global__ void k_bad_scatter(const int32_t *f, const int32_t *pos, int64_t nc, 
     GS_LOOP(c, nc) if (f[c]) list[pos[c]] = (int32_t)c;
 }
 __global__ void k_init_i32(int32_t *x, int64_t n, int32_t v) { GS_LOOP(i, n) x[i] = v; }
+__global__ void k_bad_ranges(const int32_t *list, int64_t nbad, const int32_t *cptr, int2 *out) {
+    GS_LOOP(i, nbad) out[i] = make_int2(cptr[list[i]], cptr[list[i] + 1]);
+}
 
 // ---- batched init of every part of a giant wave.  Parts are slices [lo, hi) of the layout
 // (members: gmark == pid); their concatenation is indexed by a flat index t.  Member rows are
@@ -1084,11 +1087,11 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     };
     read_small_part();
     phase_mark(ctx, -1);
-    DBuf<uint8_t> bad;
+    static DBuf<uint8_t> bad;   // grow-only scratch kept across calls
     bad.resize(nc);
     CUDA_TRY(cudaMemsetAsync(bad.p, 0, nc, s));
     run_local_gains(ctx, G, F, m, nullptr, bad.p);
-    DBuf<int32_t> f, pos, list;
+    static DBuf<int32_t> f, pos, list;
     f.resize(nc + 1);
     pos.resize(nc + 1);
     CUDA_TRY(cudaMemsetAsync(f.p + nc, 0, 4, s));
@@ -1102,9 +1105,16 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     k_bad_scatter<<<grid_for(nc, 256), 256, 0, s>>>(f.p, pos.p, nc, list.p);
     phase_mark(ctx, PH_POS_LG);
     tmark(0);
-    std::vector<int32_t> hbad(nbad), hcptr(nc + 1);
+    // bad community ids and their layout ranges (only those: cptr itself stays on the device)
+    std::vector<int32_t> hbad(nbad);
+    std::vector<int2> hrng(nbad);
+    {
+        static DBuf<int2> drng;
+        drng.resize(nbad);
+        k_bad_ranges<<<grid_for(nbad, 256), 256, 0, s>>>(list.p, nbad, F.cptr.p, drng.p);
+        CUDA_TRY(cudaMemcpyAsync(hrng.data(), drng.p, nbad * 8, cudaMemcpyDeviceToHost, s));
+    }
     CUDA_TRY(cudaMemcpyAsync(hbad.data(), list.p, nbad * 4, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaMemcpyAsync(hcptr.data(), F.cptr.p, (nc + 1) * 4, cudaMemcpyDeviceToHost, s));
     if (g_stamp.p == nullptr) {
         g_stamp.resize(1);
         CUDA_TRY(cudaMemsetAsync(g_stamp.p, 0, 4, s));
@@ -1156,13 +1166,12 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     std::vector<PartDesc> small1;
     std::vector<int64_t> order_kind(nbad);   // >=0: small1 index, <0: -(giant id)-1
     std::vector<int64_t> giant_of;
-    std::vector<int32_t> giant_comm;
+    std::vector<int32_t> giant_comm;   // bad-list indices of the giant communities
     for (int32_t i = 0; i < nbad; i++) {
-        int32_t c = hbad[i];
-        int32_t sz = hcptr[c + 1] - hcptr[c];
+        int32_t sz = hrng[i].y - hrng[i].x;
         if (sz <= SMALL_PART) {
             PartDesc d;
-            d.off = hcptr[c];
+            d.off = hrng[i].x;
             d.len = sz;
             d.from_layout = 1;
             d.pad = 0;
@@ -1170,7 +1179,7 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
             small1.push_back(d);
         } else {
             order_kind[i] = -1 - (int64_t)giant_comm.size();
-            giant_comm.push_back(c);
+            giant_comm.push_back(i);   // index into hbad / hrng
         }
     }
     DBuf<PartDesc> dparts;
@@ -1277,9 +1286,9 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
         int64_t neg_alloc = 0;
         for (int32_t c : giant_comm) {
             GPart gp;
-            gp.lo = hcptr[c];
-            gp.hi = hcptr[c + 1];
-            gp.cbase = hcptr[c];
+            gp.lo = hrng[c].x;
+            gp.hi = hrng[c].y;
+            gp.cbase = hrng[c].x;
             gp.pid = next_pid++;
             gp.neg_off = neg_alloc;
             neg_alloc += gp.hi - gp.lo;
@@ -1450,7 +1459,7 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     CUDA_TRY(cudaStreamSynchronize(s));
     if (getenv("SLM_POS_LOG")) {
         int64_t gm = 0;
-        for (int32_t c : giant_comm) gm += hcptr[c + 1] - hcptr[c];
+        for (int32_t c : giant_comm) gm += hrng[c].y - hrng[c].x;
         fprintf(stderr, "[positive] bad %d (small %zu) giant %zu members %lld | giant splits %zu "
                 "unresolved %lld small2 %zu | total splits %lld unres %lld | %.1f ms: lg %.1f "
                 "alloc %.1f small1 %.1f ginit %.1f gcta %.1f\n", nbad,
