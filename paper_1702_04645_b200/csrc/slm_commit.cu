@@ -385,15 +385,49 @@ __device__ __forceinline__ void resolve_skip(int32_t *status, int32_t k, int32_t
 }
 __device__ __forceinline__ uint8_t vload8(const uint8_t *p) { return *(volatile const uint8_t *)p; }
 
+// per-lane exact re-pricing (serial over the candidate's moving-neighbour entries); false
+// when the snapshot attach target left C (the row must be rescanned cooperatively)
+__device__ bool reprice_lane(const CommitArgs &A, const MvList &M, const int32_t *lab,
+                             const CandSpec &c, int32_t i, int32_t C, double &wt, int32_t &j) {
+    double dw = 0.0, bt = -INFINITY;
+    int64_t be = INT64_MAX;
+    bool lost = false;
+    const double soi = A.s_out[i], sii = A.s_in[i];
+    for (int32_t t = 0; t < c.mv_cnt; t++) {
+        const int64_t q = c.mv_off + t;
+        const int32_t z = M.z[q];
+        const bool now = lab[z] == C, was = A.comm[z] == C;
+        if (now != was) dw += now ? M.u[q] : -M.u[q];
+        if (M.is_i[q]) {
+            if (now) {
+                const double pg = M.u[q] / A.m - (soi * A.s_in[z] + sii * A.s_out[z]) / A.m2;
+                const int64_t e = M.e[q];
+                if (pg > bt || (pg == bt && e < be)) {
+                    bt = pg;
+                    be = e;
+                }
+            } else if (was && z == c.j) {
+                lost = true;
+            }
+        }
+    }
+    wt = c.w_to + dw;
+    if (lost) return false;
+    j = c.j;
+    if (be != INT64_MAX && (c.j < 0 || bt > c.pgj || (bt == c.pgj && be < c.je))) j = A.unbr[be];
+    return true;
+}
+
 // one warp per community timeline (see header comment).  Up to 32 upcoming events are
-// prefetched by the lanes (their static data, and for events C evaluates the source's
-// position / dirty flag / strengths -- final once the source is parked at the event), then
-// walked in order with shuffles; a long chain into C therefore costs no global round trip
-// per event unless its source has not reached it yet.  A candidate's status is written only
-// by its target's walker (plain store; the source side merely moves past a certain skip),
-// so resolutions need no CAS and `remaining` is decremented once per walker visit.
+// loaded by the lanes and classified in parallel against C's current state (speculation:
+// every event up to the first state-changing one -- a commit into C, an observed commit out
+// of C, or a wait -- sees exactly that state); skips before it are written at once, the
+// barrier event is applied, and the rest of the batch is reclassified.  A candidate's
+// status is written only by its target's walker (the source side merely moves past a
+// certain skip), so resolutions need no CAS and `remaining` drops once per walker visit.
 __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_t *wl, int64_t nw_,
                                               int32_t *status, const CandSpec *spec) {
+    enum { C_PASS = 0, C_SKIP = 1, C_COMMIT = 2, C_OUTCOMMIT = 3, C_WAIT = 4, C_COOP = 5 };
     const int lane = threadIdx.x & 31;
     int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -412,20 +446,23 @@ __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_
         const int32_t p_start = p;
         while (p < end && !parked) {
             const int nb = min(32, end - p);
-            int32_t k = -1, i = 0, frm = 0, to = 0, atF = -1, st = ST_SKIP;
+            int32_t k = -1, i = 0, frm = 0, to = -1, atF = -1, st = ST_SKIP;
             int dF = 0;
             double SoF = 0.0, SiF = 0.0;
             CandSpec cs;
-            cs.w_to = cs.w_from = cs.so_b = cs.si_b = 0.0;
+            cs.w_to = cs.w_from = cs.so_b = cs.si_b = cs.pgj = 0.0;
+            cs.je = -1;
+            cs.mv_off = 0;
             cs.j = -1;
             cs.tail_lo = cs.tail_hi = 0;
+            cs.mv_cnt = 0;
             if (lane < nb) {
                 k = V.tl_ev[p + lane];
                 st = vload(status + k);
                 i = A.cand[k];
                 frm = A.comm[i];
                 to = A.cstar[i];
-                if (to == C) {
+                if (to == C && st == ST_UNRES) {
                     atF = vload(V.atk + frm);
                     __threadfence();
                     dF = vload8(V.dirty + frm);
@@ -434,137 +471,154 @@ __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_
                     cs = spec[k];
                 }
             }
-            for (int q = 0; q < nb; q++) {
-                const int32_t kq = __shfl_sync(0xffffffffu, k, q);
-                const int32_t fq = __shfl_sync(0xffffffffu, frm, q);
-                const int32_t tq = __shfl_sync(0xffffffffu, to, q);
-                int32_t sq = __shfl_sync(0xffffffffu, st, q);
-                if (tq != C) {
-                    // C is the source side: resolved already (COMMIT changed our state), a
-                    // certain skip (C touched by an earlier commit -- final while C's timeline
-                    // is at kq -- and kq never offered), or wait for the target's verdict
-                    if (sq == ST_UNRES && my_atk != kq) {
-                        if (!dirtyC) dirtyC = vload8(V.dirty + C);
-                        if (dirtyC) continue;
-                    }
-                    if (sq == ST_UNRES) sq = vload(status + kq);
-                    if (sq == ST_UNRES) {
-                        if (lane == 0 && my_atk != kq) {
-                            __threadfence();
-                            *(volatile int32_t *)(V.atk + C) = kq;
+            int start = 0;
+            while (start < nb) {
+                // ---- classify events [start, nb) against the current state
+                const bool act = lane >= start && lane < nb;
+                int cls = C_PASS;
+                double gq = 0.0, wtq = 0.0;
+                int32_t jq = -1;
+                if (act) {
+                    if (to != C) {   // C is the source
+                        if (st == ST_COMMIT) {
+                            cls = C_OUTCOMMIT;
+                        } else if (st == ST_UNRES && !(my_atk != k && dirtyC)) {
+                            st = vload(status + k);
+                            cls = st == ST_COMMIT ? C_OUTCOMMIT : (st == ST_UNRES ? C_WAIT : C_PASS);
                         }
-                        my_atk = kq;
-                        parked = true;
-                        p += q;
-                        break;
+                    } else if (st == ST_UNRES) {   // C evaluates k
+                        int undecided = 1;
+                        if (cntC == 0 || dF) {
+                            cls = C_SKIP;
+                            undecided = 0;
+                        } else if (atF != k) {
+                            atF = vload(V.atk + frm);
+                            if (atF != k) {
+                                cls = vload8(V.dirty + frm) ? C_SKIP : C_WAIT;
+                                if (cls == C_SKIP) dF = 1;
+                                undecided = 0;
+                            } else {
+                                __threadfence();
+                                if (vload8(V.dirty + frm)) {
+                                    dF = 1;
+                                    cls = C_SKIP;
+                                    undecided = 0;
+                                } else {
+                                    SoF = V.S_out[frm];
+                                    SiF = V.S_in[frm];
+                                }
+                            }
+                        }
+                        if (undecided) {
+                            wtq = cs.w_to;
+                            jq = cs.j;
+                            if (cs.mv_cnt > 0 && dirtyC &&
+                                (cs.mv_cnt > 64 || !reprice_lane(A, V.mv, V.lab, cs, i, C, wtq, jq))) {
+                                cls = C_COOP;   // long list or lost attach target: cooperative
+                            } else {
+                                const double so_b = cs.so_b, si_b = cs.si_b;
+                                // gain_switch d_null (quality.py:216-219), exact operand order
+                                const double d_null = -SoF * si_b - so_b * SiF + SoC * si_b +
+                                                      so_b * SiC + 2.0 * so_b * si_b;
+                                gq = (wtq - cs.w_from) / A.m - d_null / (A.m * A.m);
+                                cls = (gq > 0.0 && jq >= 0) ? C_COMMIT : C_SKIP;   // detector.py:498-502
+                            }
+                        }
                     }
-                    if (sq == ST_COMMIT) {   // our state was changed by that commit
+                }
+                // ---- skips before the first state-changing event
+                const unsigned bar = __ballot_sync(0xffffffffu, act && cls >= C_COMMIT);
+                const int f = bar ? __ffs(bar) - 1 : nb;
+                const bool sk = act && lane < f && cls == C_SKIP;
+                if (sk) *(volatile int32_t *)(status + k) = ST_SKIP;
+                nres += __popc(__ballot_sync(0xffffffffu, sk));
+                if (f >= nb) break;
+                const int cf = __shfl_sync(0xffffffffu, cls, f);
+                const int32_t kf = __shfl_sync(0xffffffffu, k, f);
+                if (cf == C_WAIT) {
+                    if (lane == 0 && my_atk != kf) {
                         __threadfence();
-                        SoC = V.S_out[C];
-                        SiC = V.S_in[C];
-                        cntC = V.cnt[C];
-                        dirtyC = 1;
+                        *(volatile int32_t *)(V.atk + C) = kf;
                     }
-                    continue;
+                    my_atk = kf;
+                    parked = true;
+                    p += f;
+                    break;
                 }
-                // C evaluates kq (only C's walker resolves it).  A certain skip when the
-                // source is dirty (monotone; only commits before kq can have set it) or the
-                // target is empty; otherwise frm's walker must have reached kq.
-                if (sq != ST_UNRES) continue;
-                int32_t aq = __shfl_sync(0xffffffffu, atF, q);
-                int dq = __shfl_sync(0xffffffffu, dF, q);
-                double SoFq = __shfl_sync(0xffffffffu, SoF, q);
-                double SiFq = __shfl_sync(0xffffffffu, SiF, q);
-                if (cntC == 0 || dq) {
-                    if (lane == 0) *(volatile int32_t *)(status + kq) = ST_SKIP;
-                    nres++;
-                    continue;
-                }
-                if (aq != kq) {   // not parked at kq when prefetched: look again
-                    aq = vload(V.atk + fq);
-                    if (aq != kq) {
-                        if (vload8(V.dirty + fq)) {
-                            if (lane == 0) *(volatile int32_t *)(status + kq) = ST_SKIP;
-                            nres++;
-                            continue;
-                        }
-                        if (lane == 0 && my_atk != kq) {
-                            __threadfence();
-                            *(volatile int32_t *)(V.atk + C) = kq;
-                        }
-                        my_atk = kq;
-                        parked = true;
-                        p += q;
-                        break;
-                    }
+                if (cf == C_OUTCOMMIT) {   // our state was changed by that commit
                     __threadfence();
-                    if (vload8(V.dirty + fq)) {
-                        if (lane == 0) *(volatile int32_t *)(status + kq) = ST_SKIP;
-                        nres++;
-                        continue;
-                    }
-                    SoFq = V.S_out[fq];
-                    SiFq = V.S_in[fq];
+                    SoC = V.S_out[C];
+                    SiC = V.S_in[C];
+                    cntC = V.cnt[C];
+                    dirtyC = 1;
+                    start = f + 1;
+                    continue;
                 }
-                const int32_t iq = __shfl_sync(0xffffffffu, i, q);
-                CandSpec c;
-                c.w_to = __shfl_sync(0xffffffffu, cs.w_to, q);
-                c.w_from = __shfl_sync(0xffffffffu, cs.w_from, q);
-                c.so_b = __shfl_sync(0xffffffffu, cs.so_b, q);
-                c.si_b = __shfl_sync(0xffffffffu, cs.si_b, q);
-                c.j = __shfl_sync(0xffffffffu, cs.j, q);
-                c.tail_lo = __shfl_sync(0xffffffffu, cs.tail_lo, q);
-                c.tail_hi = __shfl_sync(0xffffffffu, cs.tail_hi, q);
-                c.pgj = __shfl_sync(0xffffffffu, cs.pgj, q);
-                c.je = __shfl_sync(0xffffffffu, cs.je, q);
-                c.mv_off = __shfl_sync(0xffffffffu, cs.mv_off, q);
-                c.mv_cnt = __shfl_sync(0xffffffffu, cs.mv_cnt, q);
-                uint8_t verdict = ST_SKIP;
-                double wt = c.w_to;
-                int32_t j = c.j;
-                if (c.mv_cnt > 0 && dirtyC) {
+                // ---- evaluated candidate kf into C (commit, or a cooperative re-pricing)
+                const int32_t iq = __shfl_sync(0xffffffffu, i, f);
+                const int32_t fq = __shfl_sync(0xffffffffu, frm, f);
+                const double so_b = __shfl_sync(0xffffffffu, cs.so_b, f);
+                const double si_b = __shfl_sync(0xffffffffu, cs.si_b, f);
+                const int32_t tlo = __shfl_sync(0xffffffffu, cs.tail_lo, f);
+                const int32_t thi = __shfl_sync(0xffffffffu, cs.tail_hi, f);
+                double g = __shfl_sync(0xffffffffu, gq, f);
+                int32_t j = __shfl_sync(0xffffffffu, jq, f);
+                bool commit = cf == C_COMMIT;
+                if (cf == C_COOP) {
+                    CandSpec c;
+                    c.w_to = __shfl_sync(0xffffffffu, cs.w_to, f);
+                    c.w_from = __shfl_sync(0xffffffffu, cs.w_from, f);
+                    c.so_b = so_b;
+                    c.si_b = si_b;
+                    c.j = __shfl_sync(0xffffffffu, cs.j, f);
+                    c.tail_lo = tlo;
+                    c.tail_hi = thi;
+                    c.pgj = __shfl_sync(0xffffffffu, cs.pgj, f);
+                    c.je = __shfl_sync(0xffffffffu, cs.je, f);
+                    c.mv_off = __shfl_sync(0xffffffffu, cs.mv_off, f);
+                    c.mv_cnt = __shfl_sync(0xffffffffu, cs.mv_cnt, f);
+                    const double SoFq = __shfl_sync(0xffffffffu, SoF, f);
+                    const double SiFq = __shfl_sync(0xffffffffu, SiF, f);
+                    double wt = c.w_to;
                     reprice(A, V.mv, V.lab, c, iq, C, wt, j);
-                    if (V.wst && lane == 0) {
-                        atomicAdd(V.wst + 3, 1ull);
-                        atomicAdd(V.wst + 4, (unsigned long long)c.mv_cnt);
-                    }
+                    const double d_null = -SoFq * si_b - so_b * SiFq + SoC * si_b + so_b * SiC +
+                                          2.0 * so_b * si_b;
+                    g = (wt - c.w_from) / A.m - d_null / (A.m * A.m);
+                    commit = g > 0.0 && j >= 0;
                 }
-                const double so_b = c.so_b, si_b = c.si_b;
-                // gain_switch d_null (quality.py:216-219), exact operand order
-                const double d_null = -SoFq * si_b - so_b * SiFq + SoC * si_b + so_b * SiC +
-                                      2.0 * so_b * si_b;
-                const double g = (wt - c.w_from) / A.m - d_null / (A.m * A.m);
-                if (g > 0.0 && j >= 0) verdict = ST_COMMIT;   // detector.py:498-502
-                if (verdict == ST_COMMIT) {
-                    const int32_t len = c.tail_hi - c.tail_lo;
+                if (commit) {
+                    const int32_t len = thi - tlo;
                     if (V.wst && lane == 0) atomicAdd(V.wst + 5, (unsigned long long)len);
-                    for (int32_t t = c.tail_lo + lane; t < c.tail_hi; t += 32) V.lab[A.order[t]] = C;
-                    SoC += c.so_b;
-                    SiC += c.si_b;
+                    for (int32_t t = tlo + lane; t < thi; t += 32) V.lab[A.order[t]] = C;
+                    SoC += so_b;
+                    SiC += si_b;
                     cntC += len;
                     dirtyC = 1;
+                    if (frm == fq) dF = 1;   // later candidates out of the same source skip
                     if (lane == 0) {
                         V.a[iq] = j;
                         // move_nodes (quality.py:87-95)
-                        V.S_out[fq] -= c.so_b;
-                        V.S_in[fq] -= c.si_b;
+                        V.S_out[fq] -= so_b;
+                        V.S_in[fq] -= si_b;
                         V.cnt[fq] -= len;
                         V.S_out[C] = SoC;
                         V.S_in[C] = SiC;
                         V.cnt[C] = cntC;
                         V.dirty[fq] = 1;
                         V.dirty[C] = 1;
-                        atomicMin(&V.first_commit[fq], kq);
-                        atomicMin(&V.first_commit[C], kq);
-                        V.gain[kq] = g;
+                        atomicMin(&V.first_commit[fq], kf);
+                        atomicMin(&V.first_commit[C], kf);
+                        V.gain[kf] = g;
                     }
                 }
                 __syncwarp();
                 if (lane == 0) {
-                    if (verdict == ST_COMMIT) __threadfence();   // state, labels before verdict
-                    *(volatile int32_t *)(status + kq) = (int32_t)verdict;
+                    if (commit) __threadfence();   // state and labels before the verdict
+                    *(volatile int32_t *)(status + kf) = commit ? ST_COMMIT : ST_SKIP;
                 }
+                if (lane == f) st = commit ? ST_COMMIT : ST_SKIP;
                 nres++;
+                start = f + 1;
             }
             if (!parked) p += nb;
         }
