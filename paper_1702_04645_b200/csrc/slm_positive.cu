@@ -328,6 +328,7 @@ struct GiantArgs {
     const int32_t *order, *pos, *sz;   // community layout (original coordinates)
     int32_t *gmark;
     double *wpart, *dep, *xw, *sob, *sib;
+    double *accl;            // per-node deposit scratch of the cut update (kept zero)
     double m, m2;
 };
 
@@ -554,6 +555,9 @@ constexpr int GT = 128;               // top candidate list kept between full pa
 constexpr int GLOC = 2;               // per-thread candidates of a full pass
 constexpr int GSORT = GB * GLOC;      // sorted in shared memory
 constexpr int DIRTY_CAP = 1 << 16;    // locally updated nodes before a forced full pass
+constexpr int CHAIN_CAP = 2048;       // ancestor chain of a cut kept in shared memory
+constexpr int BIG_ROW = 2048;         // cut-subtree members with longer rows: CTA-wide
+constexpr int BIG_CAP = 256;
 
 struct GPart {
     int64_t lo, hi, cbase;   // member slice (community DFS coordinates) and community base
@@ -592,6 +596,7 @@ struct GOut {
     unsigned long long *unresolved;
     int32_t *flags;          // [0] changed, [1] unsupported cycle
     int32_t small_part;      // cut subtrees up to this size go to the warp executor
+    unsigned long long *prof;   // SLM_POS_LOG section cycle counters (else nullptr)
 };
 
 __device__ __forceinline__ double g_member(const GiantArgs &A, int32_t x, double so_c, double si_c) {
@@ -694,6 +699,9 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
     __shared__ int s_nneg, s_ndirty, s_overflow;
     __shared__ double s_tau, s_so, s_si;
     __shared__ int s_ntop, s_two;
+    __shared__ int32_t s_chain[CHAIN_CAP];
+    __shared__ int32_t s_big[BIG_CAP];
+    __shared__ int s_nbig;
     const GPart P = parts[blockIdx.x];
     const int tid = threadIdx.x;
     const int32_t pid = P.pid, r = P.root;
@@ -713,6 +721,15 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
     if (s_two && A.a[q] != r) return;
     bool need_full = true;
     int seq = 0;
+    const long long t_cta = clock64();
+    long long tsec = clock64();
+    auto sec = [&](int k) {
+        if (O.prof && tid == 0) {
+            const long long t = clock64();
+            atomicAdd(O.prof + k, (unsigned long long)(t - tsec));
+            tsec = t;
+        }
+    };
     for (;;) {
         double so_c = s_so, si_c = s_si;
         const bool two = s_two;
@@ -733,8 +750,13 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
             }
             block_best(bg, bx, sg, sxx);
             if (!(bg > s_tau) || s_overflow) need_full = true;
+            sec(0);
         }
         if (need_full) {
+            if (tid == 0) {
+                atomicAdd(O.unresolved + 1, 1ull);
+                atomicAdd(O.unresolved + 2, (unsigned long long)(P.hi - P.lo));
+            }
             // reset the incremental state
             for (int t = tid; t < min(s_ndirty, DIRTY_CAP); t += GB) gflag[dirty[t]] = 0;
             for (int t = tid; t < s_nneg; t += GB) negflag[negl[t]] = 0;
@@ -822,6 +844,7 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
             bg = tg[0];
             bx = tx[0];
             need_full = false;
+            sec(1);
         }
         // negative members: the previous ones (re-evaluated) plus the dirty ones
         {
@@ -840,6 +863,7 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
                 }
             }
             negc = block_sum_i(c, si);
+            sec(2);
         }
         if (negc == 0) break;   // no member with negative gain left (detector.py:224-225)
         int32_t xc = -1;
@@ -907,38 +931,96 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
             }
         }
         const int bsize = block_sum_i(cb, si);
-        // edges between b and the rest: w_part of the rest side, x_w along the tree paths
+        sec(3);
+        // edges between b and the rest: w_part of the rest side, x_w along the tree paths.
+        // Members with short rows: one warp each; long rows (hubs) afterwards with the
+        // whole CTA, so a hub inside b does not serialise one warp.
         {
             const int lane = tid & 31, wid = tid >> 5;
+            if (tid == 0) s_nbig = 0;
+            __syncthreads();
+            auto edge = [&](int64_t e, int32_t pz) {
+                const int32_t v = A.unbr[e];
+                if (A.gmark[v] != pid) return;
+                const double u = A.uu[e];
+                atomicAdd(&A.wpart[v], -u);
+                mark_dirty(v, gflag, dirty, &s_ndirty, &s_overflow);
+                int32_t y = v;
+                for (;;) {
+                    const int32_t pa = A.pos[y];
+                    if (pz >= pa && pz < pa + A.sz[y]) break;
+                    atomicAdd(&A.xw[y], -u);
+                    mark_dirty(y, gflag, dirty, &s_ndirty, &s_overflow);
+                    y = A.a[y];
+                }
+                // b-side: every ancestor of b strictly below lca = y loses u; deposited
+                // at the lca and applied in one walk of b's ancestor chain below
+                atomicAdd(&A.accl[y], u);
+            };
             for (int64_t k = blo + wid; k < bhi; k += GB / 32) {
                 const int32_t z = A.order[k];
                 if (A.gmark[z] != pid_b) continue;
+                const int64_t e0 = A.uptr[z], e1 = A.uptr[z + 1];
+                if (e1 - e0 > BIG_ROW) {
+                    int at = 0;
+                    if (lane == 0) {
+                        at = atomicAdd(&s_nbig, 1);
+                        if (at < BIG_CAP) s_big[at] = z;
+                    }
+                    at = __shfl_sync(0xffffffffu, at, 0);
+                    if (at < BIG_CAP) continue;   // queued for the CTA-wide pass
+                }
                 const int32_t pz = A.pos[z];
-                for (int64_t e = A.uptr[z] + lane; e < A.uptr[z + 1]; e += 32) {
-                    const int32_t v = A.unbr[e];
-                    if (A.gmark[v] != pid) continue;
-                    const double u = A.uu[e];
-                    atomicAdd(&A.wpart[v], -u);
-                    mark_dirty(v, gflag, dirty, &s_ndirty, &s_overflow);
-                    int32_t y = v;
-                    for (;;) {
-                        const int32_t pa = A.pos[y];
-                        if (pz >= pa && pz < pa + A.sz[y]) break;
-                        atomicAdd(&A.xw[y], -u);
+                for (int64_t e = e0 + lane; e < e1; e += 32) edge(e, pz);
+            }
+            __syncthreads();
+            const int nbig = min(s_nbig, BIG_CAP);
+            for (int bi = 0; bi < nbig; bi++) {
+                const int32_t z = s_big[bi];
+                const int32_t pz = A.pos[z];
+                for (int64_t e = A.uptr[z] + tid; e < A.uptr[z + 1]; e += GB) edge(e, pz);
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {   // top-down over b's ancestors: x_w(y) -= sum of deposits above y
+            int nch = 0;
+            for (int32_t y = xpar;; y = A.a[y]) {
+                if (nch < CHAIN_CAP) s_chain[nch] = y;
+                nch++;
+                if (y == r) break;
+            }
+            if (nch <= CHAIN_CAP) {
+                double run = 0.0;
+                for (int c = nch - 1; c >= 0; c--) {
+                    const int32_t y = s_chain[c];
+                    if (run != 0.0) {
+                        A.xw[y] -= run;
                         mark_dirty(y, gflag, dirty, &s_ndirty, &s_overflow);
-                        y = A.a[y];
                     }
-                    const int32_t lca = y;
-                    y = xpar;
-                    while (y != lca) {
-                        atomicAdd(&A.xw[y], -u);
+                    run += A.accl[y];
+                    A.accl[y] = 0.0;
+                }
+            } else {   // very deep chain: per-node suffix via repeated upward walks
+                for (int32_t y = xpar;; y = A.a[y]) {
+                    double above = 0.0;
+                    for (int32_t z2 = A.a[y]; z2 != y; z2 = A.a[z2]) {
+                        above += A.accl[z2];
+                        if (z2 == r) break;
+                    }
+                    if (y != r && above != 0.0) {
+                        A.xw[y] -= above;
                         mark_dirty(y, gflag, dirty, &s_ndirty, &s_overflow);
-                        y = A.a[y];
                     }
+                    if (y == r) break;
+                }
+                for (int32_t y = xpar;; y = A.a[y]) {
+                    A.accl[y] = 0.0;
+                    if (y == r) break;
                 }
             }
         }
         __syncthreads();
+        sec(4);
         // ---- record the split and its child part
         if (bsize <= O.small_part) {
             // ordered compaction of b's members (DFS order) + in-part subtree sizes
@@ -1021,9 +1103,14 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
         }
         seq++;
         __syncthreads();
+        sec(5);
     }
     // leave the flag arrays clean for the next part on this SM
     __syncthreads();
+    if (tid == 0) {
+        atomicMax(O.unresolved + 3, (unsigned long long)seq);
+        atomicMax(O.unresolved + 4, (unsigned long long)(clock64() - t_cta));
+    }
     for (int t = tid; t < min(s_ndirty, DIRTY_CAP); t += GB) gflag[dirty[t]] = 0;
     for (int t = tid; t < s_nneg; t += GB) negflag[negl[t]] = 0;
 }
@@ -1065,6 +1152,7 @@ struct PosScratch {
     DBuf<GSlice> slices;
     DBuf<int32_t> dirty_pool;
     DBuf<GPart> dparts2;
+    DBuf<double> accl;
 };
 
 void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_t scc_cap,
@@ -1222,6 +1310,12 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
         GA.xw = xw.p;
         GA.sob = sob.p;
         GA.sib = sib.p;
+        if (SC.accl.cap < (size_t)n) {
+            SC.accl.resize(n);
+            CUDA_TRY(cudaMemsetAsync(SC.accl.p, 0, n * 8, s));
+        }
+        SC.accl.resize(n);
+        GA.accl = SC.accl.p;
         GA.m = m;
         GA.m2 = m * m;
         k_init_i32<<<grid_for(n, 256), 256, 0, s>>>(gmark.p, n, 0);
@@ -1252,11 +1346,11 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
         gflag.resize(n + 4);
         negflag.resize(n + 4);
         cnt6.resize(6);   // nlog, ndesc, alloc, nnext, pid_ctr, pad
-        unres_d.resize(1);
+        unres_d.resize(8);
         CUDA_TRY(cudaMemsetAsync(gflag.p, 0, n + 4, s));
         CUDA_TRY(cudaMemsetAsync(negflag.p, 0, n + 4, s));
         CUDA_TRY(cudaMemsetAsync(cnt6.p, 0, 24, s));
-        CUDA_TRY(cudaMemsetAsync(unres_d.p, 0, 8, s));
+        CUDA_TRY(cudaMemsetAsync(unres_d.p, 0, 64, s));
         GOut O;
         O.log_pid = log_pid.p;
         O.log_seq = log_seq.p;
@@ -1280,6 +1374,13 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
         O.unresolved = unres_d.p;
         O.flags = flags.p;
         O.small_part = SMALL_PART;
+        static DBuf<unsigned long long> gprof;
+        O.prof = nullptr;
+        if (plog) {
+            gprof.resize(8);
+            CUDA_TRY(cudaMemsetAsync(gprof.p, 0, 64, s));
+            O.prof = gprof.p;
+        }
         // wave 0: the giant bad communities
         std::vector<GPart> wave;
         int32_t next_pid = 1;
@@ -1418,7 +1519,18 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
             }
         }
         int32_t hc[4];
-        unsigned long long hun = 0;
+        unsigned long long hun = 0, hst[8];
+        if (plog) {
+            CUDA_TRY(cudaMemcpyAsync(hst, unres_d.p, 64, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            fprintf(stderr, "[giant] full passes %llu scanned %llu max splits/part %llu max cycles "
+                    "%llu\n", hst[1], hst[2], hst[3], hst[4]);
+            unsigned long long hp[8];
+            CUDA_TRY(cudaMemcpy(hp, O.prof, 64, cudaMemcpyDeviceToHost));
+            fprintf(stderr, "[giant] section cycles: incr %llu full %llu neg %llu cut %llu edges %llu "
+                    "record %llu | cut-subtree entries %llu max row %llu\n", hp[0], hp[1], hp[2],
+                    hp[3], hp[4], hp[5], hp[6], hp[7]);
+        }
         CUDA_TRY(cudaMemcpyAsync(hc, cnt6.p, 16, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaMemcpyAsync(&hun, unres_d.p, 8, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
