@@ -110,6 +110,7 @@ struct LevelGraph {
     // bin-5 (hub) rows of the integer sweep, in processing order j (descending degree):
     // work items (j << 20 | segment); bin-5 row index, table offset and size of row j
     DBuf<int64_t> hub_seg, hub_row, hub_off, hub_size;
+    mutable DBuf<uint32_t> hub_gprev;   // per hub row: groups found by the previous sweep (0: unknown)
     int64_t hub_nseg = 0, hub_rows_n = 0, hub_ring = 0;   // hub_ring: arena slots
     int32_t max_deg = 0;
 };
@@ -162,6 +163,7 @@ struct slm_ctx {
     DBuf<int2> hub_tab;          // hub tables {community, sum} of the integer sweep (kept empty)
     DBuf<uint32_t> hub_occ;      // occupied-slot lists (same offsets)
     DBuf<uint32_t> hub_cnt;      // per hub row: list length (kept zero between sweeps)
+    DBuf<uint32_t> hub_ovf;      // per hub row: overflow flag; fallback row list; its count
     DBuf<int32_t> ovf_rows;      // rows of bins 2-4 whose communities overflowed the shared table
     DBuf<uint32_t> ovf_cnt;      // [0] overflow rows, [1 + b] list length of overflow CTA b
     DBuf<int2> ovf_tab;          // per overflow CTA: global table (kept empty)

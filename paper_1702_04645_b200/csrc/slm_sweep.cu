@@ -888,7 +888,21 @@ struct HubArgs {
     int2 *tab;
     uint32_t *occ;
     uint32_t *cnt;           // per j: occupied count (left zero by the select kernel)
+    uint32_t *gprev;         // per j: groups of the previous sweep of this level (0: unknown)
+    uint32_t *ovf;           // per j: the sized table overflowed this sweep (left zero)
+    int32_t *fb;             // rows to redo with the full table, count in fb_n
+    uint32_t *fb_n;
 };
+
+// slots used by hub row j this sweep: 4x the previous sweep's group count (rounded to a
+// power of two), never more than the row's full region (pow2 > d, always enough).  A row
+// whose groups outgrow it overflows and is redone with the full region (k_sweep_hub_fallback).
+__device__ __forceinline__ uint32_t hub_use(const HubArgs &Hb, int64_t j) {
+    const uint32_t full = (uint32_t)Hb.size[j], g = Hb.gprev[j];
+    if (g == 0) return full;
+    return min(full, max(1024u, 1u << (32 - __clz(4 * g))));
+}
+constexpr int HUB_PROBE_MAX = 64;
 template <bool SYM>
 __global__ void __launch_bounds__(HUB_BLOCK, 2) k_sweep_hub_merge(SweepArgs<SYM> A, HubArgs Hb) {
     extern __shared__ int2 htab[];
@@ -920,7 +934,8 @@ __global__ void __launch_bounds__(HUB_BLOCK, 2) k_sweep_hub_merge(SweepArgs<SYM>
         __syncthreads();
         const uint32_t ns = s_no;
         int2 *GT = Hb.tab + Hb.off[j];
-        const uint32_t gmask = (uint32_t)Hb.size[j] - 1;
+        const uint32_t gmask = hub_use(Hb, j) - 1;
+        bool over = false;
         for (uint32_t k0 = 0; k0 < ns; k0 += HUB_BLOCK * MU) {
             int2 e[MU];
             uint32_t sl[MU];
@@ -942,14 +957,21 @@ __global__ void __launch_bounds__(HUB_BLOCK, 2) k_sweep_hub_merge(SweepArgs<SYM>
 #pragma unroll
             for (int u = 0; u < MU; u++) {
                 if (e[u].x < 0) continue;
+                int probes = 0;
                 while (prev[u] != -1 && prev[u] != e[u].x) {
+                    if (++probes == HUB_PROBE_MAX) break;
                     sl[u] = (sl[u] + 1) & gmask;
                     prev[u] = atomicCAS(&GT[sl[u]].x, -1, e[u].x);
+                }
+                if (prev[u] != -1 && prev[u] != e[u].x) {   // sized table too full: redo row
+                    over = true;
+                    continue;
                 }
                 atomicAdd((uint32_t *)&GT[sl[u]].y, (uint32_t)e[u].y);
                 if (prev[u] == -1) sfresh[atomicAdd(&s_nf, 1u)] = sl[u];
             }
         }
+        if (over) Hb.ovf[j] = 1;
         __syncthreads();
         if (threadIdx.x == 0) {
             s_no = 0;
@@ -974,10 +996,58 @@ __global__ void __launch_bounds__(HUB_BLOCK) k_sweep_hub_select(SweepArgs<SYM> A
         const uint32_t no = Hb.cnt[j];
         int2 *GT = Hb.tab + Hb.off[j];
         const uint32_t *GO = Hb.occ + Hb.off[j];
+        const bool over = Hb.ovf[j] != 0;
+        if (!over)
+            block_select<HUB_BLOCK, SYM, true>(A, GT, GO, no, r, A.label[r], node_s(A, r), B);
+        occ_clear<true>(GT, GO, no, threadIdx.x, HUB_BLOCK);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            Hb.cnt[j] = 0;
+            if (over) {
+                Hb.ovf[j] = 0;
+                Hb.gprev[j] = 0;
+                Hb.fb[atomicAdd(Hb.fb_n, 1u)] = (int32_t)j;
+            } else {
+                Hb.gprev[j] = no;
+            }
+        }
+    }
+}
+
+// rows whose sized table overflowed: one CTA per row rebuilds the row's groups in its full
+// region (pow2 > d slots) straight from the entries, selects, clears
+template <bool SYM>
+__global__ void __launch_bounds__(HUB_BLOCK) k_sweep_hub_fallback(SweepArgs<SYM> A, HubArgs Hb) {
+    __shared__ BlockSel B;
+    if (threadIdx.x == 0) B.hown = 0;
+    __syncthreads();
+    const uint32_t nfb = *Hb.fb_n;
+    for (uint32_t q = blockIdx.x; q < nfb; q += gridDim.x) {
+        const int64_t j = Hb.fb[q];
+        const int32_t r = Hb.rows[Hb.row_of[j]];
+        const int64_t e0 = A.uptr[r], d = A.uptr[r + 1] - e0;
+        int2 *GT = Hb.tab + Hb.off[j];
+        uint32_t *GO = Hb.occ + Hb.off[j];
+        const uint32_t H = (uint32_t)Hb.size[j];
+        for (int64_t k0 = 0; k0 < d; k0 += HUB_BLOCK) {   // CTA-uniform trip count
+            const int64_t k = k0 + threadIdx.x;
+            bool fresh = false;
+            uint32_t sl = 0;
+            if (k < d)
+                sl = tab_insert<true>(GT, H - 1, A.label[A.unbr[e0 + k]], A.u32[e0 + k], fresh);
+            occ_append(GO, Hb.cnt + j, fresh, sl);
+        }
+        __threadfence();
+        __syncthreads();
+        const uint32_t no = __ldcg(Hb.cnt + j);
         block_select<HUB_BLOCK, SYM, true>(A, GT, GO, no, r, A.label[r], node_s(A, r), B);
         occ_clear<true>(GT, GO, no, threadIdx.x, HUB_BLOCK);
         __syncthreads();
-        if (threadIdx.x == 0) Hb.cnt[j] = 0;
+        if (threadIdx.x == 0) {
+            Hb.cnt[j] = 0;
+            Hb.gprev[j] = no;
+        }
+        __syncthreads();
     }
 }
 
@@ -1100,8 +1170,22 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
         Hb.tab = ctx->hub_tab.p;
         Hb.occ = ctx->hub_occ.p;
         Hb.cnt = ctx->hub_cnt.p;
+        if (G.hub_gprev.n < (size_t)nh) {   // per level graph: unknown group counts
+            G.hub_gprev.resize(nh);
+            CUDA_TRY(cudaMemsetAsync(G.hub_gprev.p, 0, nh * 4, s));
+        }
+        if (ctx->hub_ovf.n < (size_t)(2 * nh + 1)) {
+            ctx->hub_ovf.resize(2 * nh + 1);
+            CUDA_TRY(cudaMemsetAsync(ctx->hub_ovf.p, 0, (2 * nh + 1) * 4, s));
+        }
+        CUDA_TRY(cudaMemsetAsync(ctx->hub_ovf.p + 2 * nh, 0, 4, s));
+        Hb.gprev = G.hub_gprev.p;
+        Hb.ovf = ctx->hub_ovf.p;
+        Hb.fb = (int32_t *)(ctx->hub_ovf.p + nh);
+        Hb.fb_n = ctx->hub_ovf.p + 2 * nh;
         khm<<<(unsigned)std::min<int64_t>(G.hub_nseg, 148LL * 2), HUB_BLOCK, SMH, s>>>(A, Hb);
         khs<<<(unsigned)std::min<int64_t>(nh, 148LL * 4), HUB_BLOCK, 0, s>>>(A, Hb);
+        k_sweep_hub_fallback<SYM><<<148, HUB_BLOCK, 0, s>>>(A, Hb);
     }
     CUDA_TRY(cudaGetLastError());
     if (want_stats) {
