@@ -379,6 +379,14 @@ static void build_bins(slm_ctx *ctx, LevelGraph &G) {
         G.hub_rows_n = nh;
         G.hub_ring = cur;
         G.hub_nseg = (int64_t)segs.size();
+        // the largest rows (a prefix in processing order) are spread over CTAs by segment;
+        // the rest are processed one CTA per row
+        G.hub_big_rows = 0;
+        G.hub_big_items = 0;
+        for (int64_t j = 0; j < nh && deg5(hub[j]) > HUB_BIG_DEG; j++) {
+            G.hub_big_rows++;
+            G.hub_big_items += (deg5(hub[j]) + HUB_SEG - 1) / HUB_SEG;
+        }
         if (nh) {
             G.hub_seg.resize(segs.size());
             G.hub_row.resize(nh);

@@ -83,6 +83,7 @@ constexpr int SMALL_MAX = 32;     // warp lanes = entries (packed rows)
 constexpr int MID_MAX = 4096;     // generic path: CTA-per-row shared-memory hash up to here
 
 constexpr int HUB_SEG = 4096;     // entries per hub-row work item of the integer sweep
+constexpr int64_t HUB_BIG_DEG = 32768;   // hub rows spread over CTAs by segment above this
 
 // Canonical directed CSR + neighbour union + strengths of one hierarchy level
 // (graph.py:63-175, 257-263).  Node ids int32, entry offsets int64.
@@ -112,6 +113,7 @@ struct LevelGraph {
     DBuf<int64_t> hub_seg, hub_row, hub_off, hub_size;
     mutable DBuf<uint32_t> hub_gprev;   // per hub row: groups found by the previous sweep (0: unknown)
     int64_t hub_nseg = 0, hub_rows_n = 0, hub_ring = 0;   // hub_ring: arena slots
+    int64_t hub_big_rows = 0, hub_big_items = 0;        // rows with d > HUB_BIG_DEG (prefix)
     int32_t max_deg = 0;
 };
 

@@ -1014,6 +1014,120 @@ __global__ void __launch_bounds__(HUB_BLOCK) k_sweep_hub_select(SweepArgs<SYM> A
     }
 }
 
+// hub rows, one CTA per row (rows fetched largest first from a global counter, so the
+// work is balanced like LPT scheduling): segments of HUB_SEG entries are combined in the
+// shared table and merged into the row's own global table (only this CTA touches it, and
+// it is reused at once, so it stays in L2); the CTA then selects over the row's list and
+// clears it.  (Variant of the merge / select kernels above; SLM_HUB_MODE=1 selects those.)
+template <bool SYM>
+__global__ void __launch_bounds__(HUB_BLOCK, 2) k_sweep_hub_row(SweepArgs<SYM> A, HubArgs Hb,
+                                                                 uint32_t *next) {
+    extern __shared__ int2 htab[];
+    uint16_t *socc = (uint16_t *)(htab + HUB_H);
+    uint32_t *sfresh = (uint32_t *)(socc + HUB_H);
+    const uint32_t tsa = smem_addr(htab), osa = smem_addr(socc);
+    __shared__ uint32_t s_no, s_nf, s_base, s_row;
+    __shared__ int s_over;
+    __shared__ BlockSel B;
+    for (int k = threadIdx.x; k < HUB_H; k += HUB_BLOCK) htab[k] = make_int2(-1, 0);
+    if (threadIdx.x == 0) {
+        s_no = 0;
+        s_nf = 0;
+        s_over = 0;
+        B.hown = 0;
+    }
+    constexpr int U = HUB_SEG / HUB_BLOCK;
+    constexpr int MU = 4;
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_row = atomicAdd(next, 1u);
+        __syncthreads();
+        const int64_t j = s_row;
+        if (j >= Hb.nrows) break;
+        const int32_t r = Hb.rows[Hb.row_of[j]];
+        const int64_t e0 = A.uptr[r], d = A.uptr[r + 1] - e0;
+        int2 *GT = Hb.tab + Hb.off[j];
+        uint32_t *GO = Hb.occ + Hb.off[j];
+        const uint32_t gmask = hub_use(Hb, j) - 1;
+        uint32_t total = 0;   // list length (uniform)
+        for (int64_t lo = 0; lo < d; lo += HUB_SEG) {
+            const int64_t hi = min(d, lo + HUB_SEG);
+            {
+                int32_t c[U];
+                uint32_t wt[U];
+                uint32_t unused = 0;
+                load_row<U, HUB_BLOCK>(A.unbr + e0 + lo, A.u32 + e0 + lo, A.label,
+                                       (uint32_t)(hi - lo), threadIdx.x, c, wt);
+                insert_chunk<U, false>(tsa, HUB_H - 1, c, wt, osa, &s_no, unused, (int *)nullptr);
+            }
+            __syncthreads();
+            const uint32_t ns = s_no;
+            bool over = false;
+            for (uint32_t k0 = 0; k0 < ns; k0 += HUB_BLOCK * MU) {
+                int2 e[MU];
+                uint32_t sl[MU];
+                int32_t prev[MU];
+#pragma unroll
+                for (int u = 0; u < MU; u++) {
+                    const uint32_t k = k0 + u * HUB_BLOCK + threadIdx.x;
+                    e[u] = make_int2(-1, 0);
+                    if (k < ns) {
+                        const uint32_t ss = socc[k];
+                        e[u] = htab[ss];
+                        htab[ss] = make_int2(-1, 0);
+                    }
+                    sl[u] = hslot32(e[u].x, gmask);
+                }
+#pragma unroll
+                for (int u = 0; u < MU; u++)
+                    prev[u] = e[u].x >= 0 ? atomicCAS(&GT[sl[u]].x, -1, e[u].x) : e[u].x;
+#pragma unroll
+                for (int u = 0; u < MU; u++) {
+                    if (e[u].x < 0) continue;
+                    int probes = 0;
+                    while (prev[u] != -1 && prev[u] != e[u].x) {
+                        if (++probes == HUB_PROBE_MAX) break;
+                        sl[u] = (sl[u] + 1) & gmask;
+                        prev[u] = atomicCAS(&GT[sl[u]].x, -1, e[u].x);
+                    }
+                    if (prev[u] != -1 && prev[u] != e[u].x) {
+                        over = true;
+                        continue;
+                    }
+                    atomicAdd((uint32_t *)&GT[sl[u]].y, (uint32_t)e[u].y);
+                    if (prev[u] == -1) sfresh[atomicAdd(&s_nf, 1u)] = sl[u];
+                }
+            }
+            if (over) s_over = 1;
+            __syncthreads();
+            const uint32_t nf = s_nf;
+            for (uint32_t k = threadIdx.x; k < nf; k += HUB_BLOCK) GO[total + k] = sfresh[k];
+            total += nf;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                s_no = 0;
+                s_nf = 0;
+            }
+        }
+        __threadfence_block();
+        __syncthreads();
+        const bool over = s_over != 0;
+        if (!over)
+            block_select<HUB_BLOCK, SYM, true>(A, GT, GO, total, r, A.label[r], node_s(A, r), B);
+        occ_clear<true>(GT, GO, total, threadIdx.x, HUB_BLOCK);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            s_over = 0;
+            if (over) {
+                Hb.gprev[j] = 0;
+                Hb.fb[atomicAdd(Hb.fb_n, 1u)] = (int32_t)j;
+            } else {
+                Hb.gprev[j] = total;
+            }
+        }
+    }
+}
+
 // rows whose sized table overflowed: one CTA per row rebuilds the row's groups in its full
 // region (pow2 > d slots) straight from the entries, selects, clears
 template <bool SYM>
@@ -1102,6 +1216,7 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
     auto k4 = k_sweep_cta<512, 8192, 1, 2, SYM>;
     auto khm = k_sweep_hub_merge<SYM>;
     auto khs = k_sweep_hub_select<SYM>;
+    auto khr = k_sweep_hub_row<SYM>;
     static bool attrs[2] = {false, false};
     if (!attrs[SYM]) {
         set_smem(k1, SM1);
@@ -1109,6 +1224,7 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
         set_smem(k3, SM3);
         set_smem(k4, SM4);
         set_smem(khm, SMH);
+        set_smem(khr, SMH);
         attrs[SYM] = true;
     }
     if (nb(0) && (bin_mask & 1)) {
@@ -1174,17 +1290,38 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
             G.hub_gprev.resize(nh);
             CUDA_TRY(cudaMemsetAsync(G.hub_gprev.p, 0, nh * 4, s));
         }
-        if (ctx->hub_ovf.n < (size_t)(2 * nh + 1)) {
-            ctx->hub_ovf.resize(2 * nh + 1);
-            CUDA_TRY(cudaMemsetAsync(ctx->hub_ovf.p, 0, (2 * nh + 1) * 4, s));
+        if (ctx->hub_ovf.n < (size_t)(2 * nh + 2)) {
+            ctx->hub_ovf.resize(2 * nh + 2);
+            CUDA_TRY(cudaMemsetAsync(ctx->hub_ovf.p, 0, (2 * nh + 2) * 4, s));
         }
         CUDA_TRY(cudaMemsetAsync(ctx->hub_ovf.p + 2 * nh, 0, 4, s));
         Hb.gprev = G.hub_gprev.p;
         Hb.ovf = ctx->hub_ovf.p;
         Hb.fb = (int32_t *)(ctx->hub_ovf.p + nh);
         Hb.fb_n = ctx->hub_ovf.p + 2 * nh;
-        khm<<<(unsigned)std::min<int64_t>(G.hub_nseg, 148LL * 2), HUB_BLOCK, SMH, s>>>(A, Hb);
-        khs<<<(unsigned)std::min<int64_t>(nh, 148LL * 4), HUB_BLOCK, 0, s>>>(A, Hb);
+        static const bool two_kernels = getenv("SLM_HUB_MODE") && atoi(getenv("SLM_HUB_MODE")) == 1;
+        if (two_kernels) {
+            khm<<<(unsigned)std::min<int64_t>(G.hub_nseg, 148LL * 2), HUB_BLOCK, SMH, s>>>(A, Hb);
+            khs<<<(unsigned)std::min<int64_t>(nh, 148LL * 4), HUB_BLOCK, 0, s>>>(A, Hb);
+        } else {
+            // the largest rows by segment (merge + select kernels over their prefix of the
+            // work list), the rest one CTA per row
+            const int64_t nbig = G.hub_big_rows;
+            if (nbig) {
+                HubArgs Hbig = Hb;
+                Hbig.nitems = G.hub_big_items;
+                Hbig.nrows = nbig;
+                khm<<<(unsigned)std::min<int64_t>(Hbig.nitems, 148LL * 2), HUB_BLOCK, SMH, s>>>(A, Hbig);
+                khs<<<(unsigned)std::min<int64_t>(nbig, 148LL * 4), HUB_BLOCK, 0, s>>>(A, Hbig);
+            }
+            if (nh > nbig) {
+                uint32_t *next = ctx->hub_ovf.p + 2 * nh + 1;   // row counter, starts at nbig
+                const uint32_t start = (uint32_t)nbig;
+                CUDA_TRY(cudaMemcpyAsync(next, &start, 4, cudaMemcpyHostToDevice, s));
+                k_sweep_hub_row<SYM><<<(unsigned)std::min<int64_t>(nh - nbig, 148LL * 2), HUB_BLOCK,
+                                       SMH, s>>>(A, Hb, next);
+            }
+        }
         k_sweep_hub_fallback<SYM><<<148, HUB_BLOCK, 0, s>>>(A, Hb);
     }
     CUDA_TRY(cudaGetLastError());
