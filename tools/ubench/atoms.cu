@@ -1,0 +1,59 @@
+// Microbenchmark: shared-memory atomics vs plain shared RMW throughput on this GPU.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 atoms.cu -o atoms && ./atoms
+#include <cstdio>
+#include <cuda_runtime.h>
+
+template <int MODE>
+__global__ void k(unsigned *out, int iters) {
+    __shared__ unsigned t[4096];
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x) t[i] = 0;
+    __syncthreads();
+    unsigned x = threadIdx.x * 2654435761u + blockIdx.x;
+    unsigned acc = 0;
+    for (int it = 0; it < iters; it++) {
+        x = x * 1664525u + 1013904223u;
+        const unsigned a = (x >> 20) & 4095;   // spread addresses
+        if (MODE == 0) atomicAdd(&t[a], 1u);                     // RED.shared
+        else if (MODE == 1) acc += atomicAdd(&t[a], 1u);         // ATOMS with return
+        else if (MODE == 2) acc += atomicCAS(&t[a], 0u, x);      // CAS
+        else if (MODE == 3) { volatile unsigned *v = t; acc += v[a]; }   // LDS
+        else if (MODE == 4) { t[a] = x; }                        // STS
+        else if (MODE == 5) { atomicAdd(&t[threadIdx.x & 4095], 1u); }   // lane-distinct banks
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) out[blockIdx.x] = t[blockIdx.x & 4095] + acc;
+}
+
+int main() {
+    unsigned *o;
+    cudaMalloc(&o, 1 << 20);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int iters = 4096, blocks = sms * 8, threads = 256;
+    const char *names[] = {"RED.shared add (spread)", "ATOMS add w/ return (spread)", "ATOMS CAS (spread)",
+                           "LDS volatile (spread)", "STS (spread)", "RED.shared add (lane-distinct)"};
+    for (int mode = 0; mode < 6; mode++) {
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        for (int rep = 0; rep < 2; rep++) {
+            cudaEventRecord(a);
+            switch (mode) {
+                case 0: k<0><<<blocks, threads>>>(o, iters); break;
+                case 1: k<1><<<blocks, threads>>>(o, iters); break;
+                case 2: k<2><<<blocks, threads>>>(o, iters); break;
+                case 3: k<3><<<blocks, threads>>>(o, iters); break;
+                case 4: k<4><<<blocks, threads>>>(o, iters); break;
+                case 5: k<5><<<blocks, threads>>>(o, iters); break;
+            }
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+        }
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        const double ops = (double)blocks * threads * iters;
+        printf("%-34s %8.2f Gops/s  %6.3f ops/clk/SM (at 1.965 GHz)\n", names[mode], ops / ms / 1e6,
+               ops / (ms * 1e-3) / 1.965e9 / sms);
+    }
+    return 0;
+}
