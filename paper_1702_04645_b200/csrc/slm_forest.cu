@@ -90,7 +90,12 @@ __global__ void k_minv_step(const int32_t *minv, const int32_t *hop, int64_t n, 
 __global__ void k_fill_i32(int32_t *x, int64_t n, int32_t v) { GS_LOOP(i, n) x[i] = v; }
 
 __global__ void k_first_occ(const int32_t *key, int64_t n, int32_t *first) {
-    GS_LOOP(i, n) atomicMin(&first[key[i]], (int32_t)i);
+    // a hub component has millions of members: skip the same-address atomic once a smaller
+    // member is already recorded (a stale read only costs an extra atomic)
+    GS_LOOP(i, n) {
+        const int32_t k = key[i];
+        if ((int32_t)i < *(volatile int32_t *)&first[k]) atomicMin(&first[k], (int32_t)i);
+    }
 }
 __global__ void k_head_flag(const int32_t *key, const int32_t *first, int64_t n, int32_t *h) {
     GS_LOOP(i, n) h[i] = (first[key[i]] == (int32_t)i) ? 1 : 0;
@@ -106,6 +111,11 @@ __global__ void k_assign_label(const int32_t *key, const int32_t *first, const i
 
 __global__ void k_iota(int32_t *x, int64_t n) { GS_LOOP(i, n) x[i] = (int32_t)i; }
 
+// ptr[c] = first index of key c in a sorted array in which every key 0..nrows-1 occurs
+__global__ void k_run_starts(const int32_t *sorted, int64_t m, int64_t nrows, int32_t *ptr) {
+    GS_LOOP(i, m) if (i == 0 || sorted[i] != sorted[i - 1]) ptr[sorted[i]] = (int32_t)i;
+    if (blockIdx.x == 0 && threadIdx.x == 0) ptr[nrows] = (int32_t)m;
+}
 __global__ void k_lb_ptr32(const int32_t *sorted, int64_t m, int64_t nrows, int32_t *ptr) {
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= nrows;
          r += (int64_t)gridDim.x * blockDim.x) {
@@ -253,7 +263,9 @@ __global__ void k_depth(const int32_t *a, const int32_t *comm, const int32_t *cr
         if (y != r) atomicOr(&flags[0], 1);
         depth[x] = (uint32_t)d;
         iota[x] = (int32_t)x;
-        atomicMax(&flags[1], d);
+        const unsigned act = __activemask();
+        const int dm = (int)__reduce_max_sync(act, (unsigned)d);   // one atomic per warp
+        if ((threadIdx.x & 31) == __ffs(act) - 1) atomicMax(&flags[1], dm);
     }
 }
 __global__ void k_ones(int32_t *x, int64_t n) { GS_LOOP(i, n) x[i] = 1; }
@@ -402,7 +414,7 @@ void build_members_and_aggregates(slm_ctx *ctx, const LevelGraph &G, Forest &F) 
     if (n > 0)
         sort_pairs_u32_i32(ctx, (uint32_t *)F.comm.p, (uint32_t *)ksorted, iota, F.members.p, n,
                            bits_for(nc + 1));
-    k_lb_ptr32<<<grid_for(nc + 1, 256), 256, 0, s>>>(ksorted, n, nc, F.cptr.p);
+    k_run_starts<<<grid_for(n, 256), 256, 0, s>>>(ksorted, n, nc, F.cptr.p);
     // segmented sums over the member-ordered strengths (exact for integer weights in any
     // order; CUB's fixed reduction tree keeps real-valued sums deterministic)
     if (!G.integral) {
@@ -471,7 +483,7 @@ void build_layout(slm_ctx *ctx, Forest &F) {
     {
         static DBuf<int32_t> lb;   // grow-only scratch kept across calls
         lb.resize(maxd + 2);
-        k_lb_ptr32<<<1, 128, 0, s>>>((const int32_t *)depth_sorted.p, n, maxd + 1, lb.p);
+        k_run_starts<<<grid_for(n, 256), 256, 0, s>>>((const int32_t *)depth_sorted.p, n, maxd + 1, lb.p);
         std::vector<int32_t> h(maxd + 2);
         CUDA_TRY(cudaMemcpyAsync(h.data(), lb.p, (maxd + 2) * 4, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
