@@ -199,20 +199,36 @@ __global__ void __launch_bounds__(128) k_positive(PosArgs A) {
                 continue;
             }
             __syncwarp();
-            // LCA deposits: -u at the lowest ancestor of y whose DFS range holds z
-            for (int k = lane; k < len; k += 32) {
-                int32_t y = P[k];
-                for (int64_t e = A.uptr[y]; e < A.uptr[y + 1]; e++) {
-                    int32_t z = A.unbr[e];
-                    if (A.pmark[z] != (int32_t)stamp) continue;
-                    int32_t pz = A.ppos[z];
-                    int32_t anc = y;
-                    for (;;) {
-                        int32_t pa = A.ppos[anc];
-                        if (pz >= pa && pz < pa + A.psz[anc]) break;
-                        anc = A.a[anc];
-                    }
-                    atomicAdd(&A.dep[anc], -A.uu[e]);
+            // LCA deposits: -u at the lowest ancestor of y whose DFS range holds z (lanes over
+            // the entries of one member at a time: coarse-level rows can be long)
+            auto deposit = [&](int32_t y, int64_t e) {
+                const int32_t z = A.unbr[e];
+                if (A.pmark[z] != (int32_t)stamp) return;
+                const int32_t pz = A.ppos[z];
+                int32_t anc = y;
+                for (;;) {
+                    const int32_t pa = A.ppos[anc];
+                    if (pz >= pa && pz < pa + A.psz[anc]) break;
+                    anc = A.a[anc];
+                }
+                atomicAdd(&A.dep[anc], -A.uu[e]);
+            };
+            for (int cb = 0; cb < len; cb += 32) {
+                const int k = cb + lane;
+                bool longrow = false;
+                if (k < len) {
+                    const int32_t y = P[k];
+                    const int64_t e0 = A.uptr[y], e1 = A.uptr[y + 1];
+                    if (e1 - e0 > 32) longrow = true;
+                    else
+                        for (int64_t e = e0; e < e1; e++) deposit(y, e);
+                }
+                unsigned lm = __ballot_sync(0xffffffffu, longrow);
+                while (lm) {   // long rows: lanes over the entries
+                    const int src = __ffs(lm) - 1;
+                    lm &= lm - 1;
+                    const int32_t y = P[cb + src];
+                    for (int64_t e = A.uptr[y] + lane; e < A.uptr[y + 1]; e += 32) deposit(y, e);
                 }
             }
             __syncwarp();
