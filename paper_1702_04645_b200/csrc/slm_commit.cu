@@ -139,8 +139,25 @@ struct CommitArgs {
     double m, m2;
 };
 
-// speculative evaluation against the snapshot (one warp per accepted candidate)
-__global__ void k_spec(CommitArgs A, int64_t K, const int32_t *status, CandSpec *spec) {
+// candidates whose tail has more members than this are evaluated by a whole CTA
+constexpr int BIG_TAIL = 64;
+
+__device__ __forceinline__ void tail_range(const CommitArgs &A, int32_t i, int32_t frm, int32_t &lo,
+                                           int32_t &hi) {
+    const int32_t base = A.cptr[frm];
+    if (A.on_cycle[i]) {
+        lo = base;
+        hi = A.cptr[frm + 1];
+    } else {
+        lo = base + A.pos[i];
+        hi = lo + A.sz[i];
+    }
+}
+
+// speculative evaluation against the snapshot (one warp per accepted candidate; tails of
+// more than BIG_TAIL members are listed for k_spec_big)
+__global__ void k_spec(CommitArgs A, int64_t K, const int32_t *status, CandSpec *spec,
+                       int32_t *big, int32_t *nbig) {
     const int lane = threadIdx.x & 31;
     int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -150,12 +167,10 @@ __global__ void k_spec(CommitArgs A, int64_t K, const int32_t *status, CandSpec 
         const int32_t frm = A.comm[i], to = A.cstar[i];
         const int32_t base = A.cptr[frm];
         int32_t lo, hi;
-        if (A.on_cycle[i]) {
-            lo = base;
-            hi = A.cptr[frm + 1];
-        } else {
-            lo = base + A.pos[i];
-            hi = lo + A.sz[i];
+        tail_range(A, i, frm, lo, hi);
+        if (hi - lo > BIG_TAIL) {
+            if (lane == 0) big[atomicAdd(nbig, 1)] = (int32_t)k;
+            continue;
         }
         const int32_t plo = lo - base, phi = hi - base;
         double so = 0.0, si = 0.0, wf = 0.0;
@@ -201,6 +216,98 @@ __global__ void k_spec(CommitArgs A, int64_t K, const int32_t *status, CandSpec 
 }
 
 
+// one CTA per big-tail candidate: the tail's strengths, w_from and w_to by all warps
+// (members over warps, entries over lanes), the attach target over row i by warp 0
+constexpr int SPEC_BLOCK = 512;
+__global__ void __launch_bounds__(SPEC_BLOCK) k_spec_big(CommitArgs A, const int32_t *big,
+                                                         const int32_t *nbig, CandSpec *spec) {
+    __shared__ double red[4][SPEC_BLOCK / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    constexpr int NW = SPEC_BLOCK / 32;
+    const int32_t nb = *nbig;
+    for (int32_t b = blockIdx.x; b < nb; b += gridDim.x) {
+        const int32_t k = big[b];
+        const int32_t i = A.cand[k];
+        const int32_t frm = A.comm[i], to = A.cstar[i];
+        const int32_t base = A.cptr[frm];
+        int32_t lo, hi;
+        tail_range(A, i, frm, lo, hi);
+        const int32_t plo = lo - base, phi = hi - base;
+        double so = 0.0, si = 0.0, wf = 0.0, wt = 0.0;
+        for (int32_t q = lo + threadIdx.x; q < hi; q += SPEC_BLOCK) {
+            const int32_t x = A.order[q];
+            so += A.s_out[x];
+            si += A.s_in[x];
+        }
+        for (int32_t q = lo + wid; q < hi; q += NW) {
+            const int32_t x = A.order[q];
+            for (int64_t e = A.uptr[x] + lane; e < A.uptr[x + 1]; e += 32) {
+                const int32_t z = A.unbr[e];
+                const int32_t cz = A.comm[z];
+                if (cz == to) wt += A.uu[e];
+                if (cz != frm) continue;
+                const int32_t pz = A.pos[z];
+                if (pz >= plo && pz < phi) continue;   // z inside the moved tail
+                wf += A.uu[e];
+            }
+        }
+        so = warp_sum(so);
+        si = warp_sum(si);
+        wf = warp_sum(wf);
+        wt = warp_sum(wt);
+        if (lane == 0) {
+            red[0][wid] = so;
+            red[1][wid] = si;
+            red[2][wid] = wf;
+            red[3][wid] = wt;
+        }
+        __syncthreads();
+        if (wid == 0) {
+            double v[4];
+#pragma unroll
+            for (int f = 0; f < 4; f++) v[f] = warp_sum(lane < NW ? red[f][lane] : 0.0);
+            // attach target of i in `to` over i's row (detector.py:440-454)
+            const double soi = A.s_out[i], sii = A.s_in[i];
+            double bt = -INFINITY;
+            int64_t be = INT64_MAX;
+            for (int64_t e = A.uptr[i] + lane; e < A.uptr[i + 1]; e += 32) {
+                const int32_t z = A.unbr[e];
+                if (A.comm[z] != to) continue;
+                const double pg = A.uu[e] / A.m - (soi * A.s_in[z] + sii * A.s_out[z]) / A.m2;
+                if (pg > bt) {
+                    bt = pg;
+                    be = e;
+                }
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double ot = __shfl_xor_sync(0xffffffffu, bt, off);
+                const int64_t oe = __shfl_xor_sync(0xffffffffu, be, off);
+                if (ot > bt || (ot == bt && oe < be)) {
+                    bt = ot;
+                    be = oe;
+                }
+            }
+            if (lane == 0) {
+                CandSpec c;
+                c.w_to = v[3];
+                c.w_from = v[2];
+                c.so_b = v[0];
+                c.si_b = v[1];
+                c.pgj = bt;
+                c.je = be != INT64_MAX ? be : -1;
+                c.mv_off = 0;
+                c.j = be != INT64_MAX ? A.unbr[be] : -1;
+                c.tail_lo = lo;
+                c.tail_hi = hi;
+                c.mv_cnt = 0;
+                spec[k] = c;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // mark every node of an accepted candidate's tail (a node that may move this sweep)
 __global__ void k_mark_moving(const int32_t *cand, const int32_t *comm, const uint8_t *on_cycle,
                               const int32_t *cptr, const int32_t *pos, const int32_t *sz,
@@ -237,6 +344,7 @@ __global__ void k_mv_scan(CommitArgs A, int64_t K, const int32_t *status, CandSp
         if (status[k] != ST_UNRES) continue;
         const int32_t i = A.cand[k], frm = A.comm[i];
         const CandSpec c = spec[k];
+        if (c.tail_hi - c.tail_lo > BIG_TAIL) continue;   // k_mv_scan_big
         int64_t base = fill ? c.mv_off : 0, total = 0;
         for (int32_t q = c.tail_lo; q < c.tail_hi; q++) {
             const int32_t x = A.order[q];
@@ -265,6 +373,56 @@ __global__ void k_mv_scan(CommitArgs A, int64_t K, const int32_t *status, CandSp
         }
     }
 }
+// moving-neighbour scan of the big-tail candidates: one CTA each (entries in any order;
+// re-pricing breaks ties by entry index)
+__global__ void __launch_bounds__(SPEC_BLOCK) k_mv_scan_big(CommitArgs A, const int32_t *big,
+                                                            const int32_t *nbig, CandSpec *spec,
+                                                            const uint8_t *moving, int fill,
+                                                            int64_t *cnt, int32_t *mv_z, double *mv_u,
+                                                            int64_t *mv_e, uint8_t *mv_i) {
+    __shared__ unsigned long long s_tot;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    constexpr int NW = SPEC_BLOCK / 32;
+    const int32_t nb = *nbig;
+    for (int32_t b = blockIdx.x; b < nb; b += gridDim.x) {
+        const int32_t k = big[b];
+        const int32_t i = A.cand[k], frm = A.comm[i];
+        const CandSpec c = spec[k];
+        if (threadIdx.x == 0) s_tot = 0;
+        __syncthreads();
+        for (int32_t q = c.tail_lo + wid; q < c.tail_hi; q += NW) {
+            const int32_t x = A.order[q];
+            for (int64_t e0 = A.uptr[x]; e0 < A.uptr[x + 1]; e0 += 32) {
+                const int64_t e = e0 + lane;
+                bool hit = false;
+                int32_t z = 0;
+                if (e < A.uptr[x + 1]) {
+                    z = A.unbr[e];
+                    hit = moving[z] && A.comm[z] != frm;
+                }
+                const unsigned hm = __ballot_sync(0xffffffffu, hit);
+                if (!hm) continue;
+                unsigned long long at = 0;
+                if (lane == 0) at = atomicAdd(&s_tot, (unsigned long long)__popc(hm));
+                at = __shfl_sync(0xffffffffu, at, 0);
+                if (fill && hit) {
+                    const int64_t p = c.mv_off + (int64_t)at + __popc(hm & ((1u << lane) - 1));
+                    mv_z[p] = z;
+                    mv_u[p] = A.uu[e];
+                    mv_e[p] = e;
+                    mv_i[p] = (x == i);
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            if (fill) spec[k].mv_cnt = (int32_t)s_tot;
+            else cnt[k] = (int64_t)s_tot;
+        }
+        __syncthreads();
+    }
+}
+
 __global__ void k_mv_offsets(int64_t K, const int32_t *status, const int64_t *off, CandSpec *spec) {
     GS_LOOP(k, K) if (status[k] == ST_UNRES) spec[k].mv_off = off[k];
 }
@@ -658,6 +816,7 @@ __global__ void k_gather_gains(int64_t K, const int32_t *f, const int32_t *pos, 
 
 // per-call scratch of run_commit, kept across calls (grow-only)
 struct CommitScratch {
+    DBuf<int32_t> big;   // big-tail candidates + count
     DBuf<int32_t> flag, pos, cand;
     DBuf<int32_t> status;
     DBuf<uint8_t> moving;
@@ -727,8 +886,25 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     DBuf<CandSpec> &spec = CS.spec;
     spec.resize(K);
     phase_mark(ctx, PH_CAND);
+    const bool sprof = ctx->prof && getenv("SLM_PROFILE_SPEC");
+    double st_[8] = {0};
+    int st_i = 0;
+    double st_t = now_ms();
+    auto stick = [&]() {
+        if (!sprof) return;
+        CUDA_TRY(cudaStreamSynchronize(s));
+        const double t = now_ms();
+        st_[st_i++] = t - st_t;
+        st_t = t;
+    };
     unsigned GW = grid_for((int64_t)K * 32, 256, 148LL * 32);
-    k_spec<<<GW, 256, 0, s>>>(A, K, status.p, spec.p);
+    DBuf<int32_t> &big = CS.big;
+    big.resize(K + 1);   // [K] = count
+    int32_t *nbig = big.p + K;
+    CUDA_TRY(cudaMemsetAsync(nbig, 0, 4, s));
+    k_spec<<<GW, 256, 0, s>>>(A, K, status.p, spec.p, big.p, nbig);
+    k_spec_big<<<148 * 4, SPEC_BLOCK, 0, s>>>(A, big.p, nbig, spec.p);
+    stick();
     CUDA_TRY(cudaMemsetAsync(moving.p, 0, n, s));
     k_mark_moving<<<GW, 256, 0, s>>>(cand.p, F.comm.p, F.on_cycle.p, F.cptr.p, F.pos.p, F.sz.p,
                                      F.order.p, K, status.p, moving.p);
@@ -742,6 +918,9 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     CUDA_TRY(cudaMemsetAsync(mvcnt.p, 0, (K + 1) * 8, s));
     k_mv_scan<<<GW, 256, 0, s>>>(A, K, status.p, spec.p, moving.p, 0, mvcnt.p, nullptr, nullptr,
                                  nullptr, nullptr);
+    k_mv_scan_big<<<148 * 4, SPEC_BLOCK, 0, s>>>(A, big.p, nbig, spec.p, moving.p, 0, mvcnt.p,
+                                                 nullptr, nullptr, nullptr, nullptr);
+    stick();
     cub_exclusive_sum<int64_t>(ctx, mvcnt.p, mvoff.p, K + 1);
     int64_t NMV = 0;
     CUDA_TRY(cudaMemcpyAsync(&NMV, mvoff.p + K, 8, cudaMemcpyDeviceToHost, s));
@@ -753,6 +932,9 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     k_mv_offsets<<<grid_for(K, 256), 256, 0, s>>>(K, status.p, mvoff.p, spec.p);
     k_mv_scan<<<GW, 256, 0, s>>>(A, K, status.p, spec.p, moving.p, 1, nullptr, mv_z.p, mv_u.p,
                                  mv_e.p, mv_i.p);
+    k_mv_scan_big<<<148 * 4, SPEC_BLOCK, 0, s>>>(A, big.p, nbig, spec.p, moving.p, 1, nullptr,
+                                                 mv_z.p, mv_u.p, mv_e.p, mv_i.p);
+    stick();
     // accepted candidates -> (community, k) pairs -> timelines
     DBuf<int32_t> &af = CS.af, &apos = CS.apos;
     af.resize(K + 1);
@@ -791,6 +973,7 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
         tl_ev.resize(2 * (int64_t)NA);
         k_acc_pairs<<<grid_for(K, 256), 256, 0, s>>>(cand.p, F.comm.p, d_cstar, K, af.p, apos.p,
                                                      keys.p, vals.p);
+        stick();
         sort_pairs_u32_i32(ctx, keys.p, keys_sorted.p, vals.p, tl_ev.p, 2 * (int64_t)NA,
                            bits_for(nc + 1));
         tl_ptr.resize(nc + 1);
@@ -808,6 +991,7 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
         CUDA_TRY(cudaMemcpyAsync(&NW, wp.p + nc, 4, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
         wl.resize(NW);
+        stick();
         k_walker_scatter<<<grid_for(nc, 256), 256, 0, s>>>(wf.p, wp.p, tl_ptr.p, nc, wl.p, wpos.p,
                                                            atk.p);
         CUDA_TRY(cudaMemcpyAsync(remaining.p, &NA, 4, cudaMemcpyHostToDevice, s));
@@ -829,6 +1013,11 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
         V.mv.is_i = mv_i.p;
         V.gain = gbuf.p;
         V.remaining = remaining.p;
+        stick();
+        if (sprof)
+            fprintf(stderr, "[spec] K=%d NA=%d: spec %.2f mark+mvcount %.2f fill+acc %.2f state+pairs %.2f "
+                    "sort+walkers %.2f scatter %.2f ms\n", K, NA, st_[0], st_[1], st_[2], st_[3],
+                    st_[4], st_[5]);
         phase_mark(ctx, PH_SPEC);
         const unsigned GWK = grid_for((int64_t)NW * 32, 256, 148LL * 64);
         int32_t rem = NA;
