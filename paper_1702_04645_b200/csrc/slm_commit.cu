@@ -584,11 +584,16 @@ __device__ bool reprice_lane(const CommitArgs &A, const MvList &M, const int32_t
 // status is written only by its target's walker (the source side merely moves past a
 // certain skip), so resolutions need no CAS and `remaining` drops once per walker visit.
 __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_t *wl, int64_t nw_,
-                                              int32_t *status, const CandSpec *spec) {
+                                              int32_t *status, const CandSpec *spec, int persistent) {
     enum { C_PASS = 0, C_SKIP = 1, C_COMMIT = 2, C_OUTCOMMIT = 3, C_WAIT = 4, C_COOP = 5 };
     const int lane = threadIdx.x & 31;
     int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    // persistent: the (resident) warps keep revisiting their walkers until each has reached
+    // the end of its timeline, so a parked walker resumes as soon as its verdict is written
+    // instead of at the next launch
+    for (;;) {
+    int pending = 0, progressed = 0;
     for (int64_t wi = w; wi < nw_; wi += nwarps) {
         const int32_t C = wl[wi];
         int32_t p = V.wpos[C];
@@ -793,6 +798,11 @@ __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_
                 *(volatile int32_t *)(V.atk + C) = 0x7fffffff;
             }
         }
+        if (p > p_start) progressed = 1;
+        if (p < end) pending = 1;
+    }
+    if (!persistent || !pending) break;
+    if (!progressed) __nanosleep(256);
     }
 }
 
@@ -1030,10 +1040,20 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
             wst.resize(8);
             V.wst = wst.p;
         }
+        // one persistent launch on a resident grid (SLM_WALK_ROUNDS=1: relaunch per round)
+        static int walk_blocks = 0;
+        if (walk_blocks == 0) {
+            int per_sm = 0;
+            CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk, 256, 0));
+            walk_blocks = std::max(1, per_sm) * 148;
+        }
+        static const bool rounds_mode = getenv("SLM_WALK_ROUNDS") != nullptr;
+        const unsigned GWP = (unsigned)std::min<int64_t>(GWK, walk_blocks);
         for (int round = 0; rem > 0; round++) {
             if (wprof) CUDA_TRY(cudaMemsetAsync(wst.p, 0, 64, s));
             const double t0 = ctx->prof ? now_ms() : 0.0;
-            k_walk<<<GWK, 256, 0, s>>>(A, V, wl.p, NW, status.p, spec.p);
+            if (rounds_mode) k_walk<<<GWK, 256, 0, s>>>(A, V, wl.p, NW, status.p, spec.p, 0);
+            else k_walk<<<GWP, 256, 0, s>>>(A, V, wl.p, NW, status.p, spec.p, 1);
             CUDA_TRY(cudaMemcpyAsync(&rem, remaining.p, 4, cudaMemcpyDeviceToHost, s));
             CUDA_TRY(cudaStreamSynchronize(s));
             if (ctx->prof) rt.push_back(now_ms() - t0);
