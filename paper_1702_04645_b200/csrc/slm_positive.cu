@@ -345,6 +345,12 @@ struct GiantArgs {
     int32_t *gmark;
     double *wpart, *dep, *xw, *sob, *sib;
     double *accl;            // per-node deposit scratch of the cut update (kept zero)
+    // intra-part adjacency of the wave-0 parts (a superset for every descendant part):
+    // node x's entries to members of its part are (iz, iu)[ioff[x], ioff[x] + icnt[x])
+    int64_t *ioff;
+    int32_t *icnt;
+    int32_t *iz;
+    double *iu;
     double m, m2;
 };
 
@@ -468,7 +474,8 @@ __device__ __forceinline__ int slice_of(const GSlice *S, int ns, int64_t t) {
     }
     return a;
 }
-__global__ void k_gb_chunks(GiantArgs A, const GSlice *S, int ns, int64_t N, int32_t *nch) {
+__global__ void k_gb_chunks(GiantArgs A, const GSlice *S, int ns, int64_t N, int32_t *nch,
+                            int build_intra) {
     GS_LOOP(t, N) {
         const GSlice sl = S[slice_of(S, ns, t)];
         const int32_t x = A.order[sl.lo + (t - sl.flat)];
@@ -477,6 +484,7 @@ __global__ void k_gb_chunks(GiantArgs A, const GSlice *S, int ns, int64_t N, int
             const int64_t d = A.uptr[x + 1] - A.uptr[x];
             c = (int32_t)((d + GCH - 1) / GCH);
             A.wpart[x] = 0.0;
+            if (build_intra) A.icnt[x] = 0;
         }
         nch[t] = c;
     }
@@ -498,7 +506,8 @@ __device__ __forceinline__ int32_t chunk_node(const GiantArgs &A, const GSlice *
     e1 = b + min(d, (c + 1) * (int64_t)GCH);
     return x;
 }
-__global__ void k_gb_wpart(GiantArgs A, const GSlice *S, int ns, const int64_t *chunks, int64_t nck) {
+__global__ void k_gb_wpart(GiantArgs A, const GSlice *S, int ns, const int64_t *chunks, int64_t nck,
+                           int build_intra) {
     const int lane = threadIdx.x & 31;
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -507,10 +516,62 @@ __global__ void k_gb_wpart(GiantArgs A, const GSlice *S, int ns, const int64_t *
         const int32_t x = chunk_node(A, S, ns, chunks[k], e0, e1);
         const int32_t pid = A.gmark[x];
         double wp = 0.0;
+        int ni = 0;
         for (int64_t e = e0 + lane; e < e1; e += 32)
-            if (A.gmark[A.unbr[e]] == pid) wp += A.uu[e];
+            if (A.gmark[A.unbr[e]] == pid) {
+                wp += A.uu[e];
+                ni++;
+            }
         wp = wsum_d(wp);
+        ni = __reduce_add_sync(0xffffffffu, ni);
         if (lane == 0 && wp != 0.0) atomicAdd(&A.wpart[x], wp);
+        if (build_intra && lane == 0 && ni) atomicAdd(&A.icnt[x], ni);
+    }
+}
+__global__ void k_gb_icount(GiantArgs A, const GSlice *S, int ns, int64_t N, int64_t *cnt) {
+    GS_LOOP(t, N) {
+        const GSlice sl = S[slice_of(S, ns, t)];
+        const int32_t x = A.order[sl.lo + (t - sl.flat)];
+        cnt[t] = A.gmark[x] == sl.pid ? A.icnt[x] : 0;
+    }
+}
+__global__ void k_gb_ioff(GiantArgs A, const GSlice *S, int ns, int64_t N, const int64_t *off) {
+    GS_LOOP(t, N) {
+        const GSlice sl = S[slice_of(S, ns, t)];
+        const int32_t x = A.order[sl.lo + (t - sl.flat)];
+        if (A.gmark[x] == sl.pid) {
+            A.ioff[x] = off[t];
+            A.icnt[x] = 0;   // refilled by k_gb_ifill
+        }
+    }
+}
+__global__ void k_gb_ifill(GiantArgs A, const GSlice *S, int ns, const int64_t *chunks, int64_t nck) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t k = w; k < nck; k += nw) {
+        int64_t e0, e1;
+        const int32_t x = chunk_node(A, S, ns, chunks[k], e0, e1);
+        const int32_t pid = A.gmark[x];
+        for (int64_t eb = e0; eb < e1; eb += 32) {
+            const int64_t e = eb + lane;
+            int32_t z = 0;
+            bool hit = false;
+            if (e < e1) {
+                z = A.unbr[e];
+                hit = A.gmark[z] == pid;
+            }
+            const unsigned hm = __ballot_sync(0xffffffffu, hit);
+            if (!hm) continue;
+            int at = 0;
+            if (lane == 0) at = atomicAdd(&A.icnt[x], __popc(hm));
+            at = __shfl_sync(0xffffffffu, at, 0);
+            if (hit) {
+                const int64_t q = A.ioff[x] + at + __popc(hm & ((1u << lane) - 1));
+                A.iz[q] = z;
+                A.iu[q] = A.uu[e];
+            }
+        }
     }
 }
 __global__ void k_gb_dep(GiantArgs A, const GSlice *S, int ns, int64_t N) {
@@ -743,6 +804,7 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
         if (O.prof && tid == 0) {
             const long long t = clock64();
             atomicAdd(O.prof + k, (unsigned long long)(t - tsec));
+            atomicAdd(O.prof + 8 + 8 * (int64_t)blockIdx.x + k, (unsigned long long)(t - tsec));
             tsec = t;
         }
     };
@@ -955,10 +1017,11 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
             const int lane = tid & 31, wid = tid >> 5;
             if (tid == 0) s_nbig = 0;
             __syncthreads();
-            auto edge = [&](int64_t e, int32_t pz) {
-                const int32_t v = A.unbr[e];
+            // (entries from the wave-0 intra-part lists: a superset of the part's edges)
+            auto edge = [&](int64_t q, int32_t pz) {
+                const int32_t v = A.iz[q];
                 if (A.gmark[v] != pid) return;
-                const double u = A.uu[e];
+                const double u = A.iu[q];
                 atomicAdd(&A.wpart[v], -u);
                 mark_dirty(v, gflag, dirty, &s_ndirty, &s_overflow);
                 int32_t y = v;
@@ -976,7 +1039,7 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
             for (int64_t k = blo + wid; k < bhi; k += GB / 32) {
                 const int32_t z = A.order[k];
                 if (A.gmark[z] != pid_b) continue;
-                const int64_t e0 = A.uptr[z], e1 = A.uptr[z + 1];
+                const int64_t e0 = A.ioff[z], e1 = e0 + A.icnt[z];
                 if (e1 - e0 > BIG_ROW) {
                     int at = 0;
                     if (lane == 0) {
@@ -994,7 +1057,8 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
             for (int bi = 0; bi < nbig; bi++) {
                 const int32_t z = s_big[bi];
                 const int32_t pz = A.pos[z];
-                for (int64_t e = A.uptr[z] + tid; e < A.uptr[z + 1]; e += GB) edge(e, pz);
+                const int64_t e0 = A.ioff[z], e1 = e0 + A.icnt[z];
+                for (int64_t e = e0 + tid; e < e1; e += GB) edge(e, pz);
             }
         }
         __syncthreads();
@@ -1169,6 +1233,9 @@ struct PosScratch {
     DBuf<int32_t> dirty_pool;
     DBuf<GPart> dparts2;
     DBuf<double> accl;
+    DBuf<int64_t> ioff, icnt_flat, ioff_flat;
+    DBuf<int32_t> icnt, iz;
+    DBuf<double> iu;
 };
 
 void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_t scc_cap,
@@ -1332,6 +1399,13 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
         }
         SC.accl.resize(n);
         GA.accl = SC.accl.p;
+        SC.ioff.resize(n);
+        SC.icnt.resize(n);
+        GA.ioff = SC.ioff.p;
+        GA.icnt = SC.icnt.p;
+        GA.iz = nullptr;
+        GA.iu = nullptr;
+        bool first_wave = true;
         GA.m = m;
         GA.m2 = m * m;
         k_init_i32<<<grid_for(n, 256), 256, 0, s>>>(gmark.p, n, 0);
@@ -1393,8 +1467,8 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
         static DBuf<unsigned long long> gprof;
         O.prof = nullptr;
         if (plog) {
-            gprof.resize(8);
-            CUDA_TRY(cudaMemsetAsync(gprof.p, 0, 64, s));
+            gprof.resize(8 + 8 * 4096);
+            CUDA_TRY(cudaMemsetAsync(gprof.p, 0, gprof.bytes(), s));
             O.prof = gprof.p;
         }
         // wave 0: the giant bad communities
@@ -1449,7 +1523,8 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
             SC.nch.resize(N + 1);
             SC.choff.resize(N + 1);
             CUDA_TRY(cudaMemsetAsync(SC.nch.p + N, 0, 4, s));
-            k_gb_chunks<<<grid_for(N, 256), 256, 0, s>>>(GA, dsl, ns, N, SC.nch.p);
+            const int build_intra = first_wave ? 1 : 0;
+            k_gb_chunks<<<grid_for(N, 256), 256, 0, s>>>(GA, dsl, ns, N, SC.nch.p, build_intra);
             {
                 size_t tb = 0;
                 CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, SC.nch.p, SC.choff.p, N + 1, s));
@@ -1463,7 +1538,29 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
             k_gb_expand<<<grid_for(N, 256), 256, 0, s>>>(GA, dsl, ns, N, SC.nch.p, SC.choff.p,
                                                         SC.chunks.p);
             const unsigned GW = grid_for(nck * 32, 256, 148LL * 32);
-            k_gb_wpart<<<GW, 256, 0, s>>>(GA, dsl, ns, SC.chunks.p, nck);
+            k_gb_wpart<<<GW, 256, 0, s>>>(GA, dsl, ns, SC.chunks.p, nck, build_intra);
+            if (build_intra) {   // intra-part adjacency lists of the wave-0 members
+                SC.icnt_flat.resize(N + 1);
+                SC.ioff_flat.resize(N + 1);
+                k_gb_icount<<<grid_for(N, 256), 256, 0, s>>>(GA, dsl, ns, N, SC.icnt_flat.p);
+                CUDA_TRY(cudaMemsetAsync(SC.icnt_flat.p + N, 0, 8, s));
+                size_t tb = 0;
+                CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, SC.icnt_flat.p, SC.ioff_flat.p,
+                                                       N + 1, s));
+                ctx->tmp.resize(tb);
+                CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx->tmp.p, tb, SC.icnt_flat.p, SC.ioff_flat.p,
+                                                       N + 1, s));
+                int64_t nintra = 0;
+                CUDA_TRY(cudaMemcpyAsync(&nintra, SC.ioff_flat.p + N, 8, cudaMemcpyDeviceToHost, s));
+                CUDA_TRY(cudaStreamSynchronize(s));
+                SC.iz.resize(std::max<int64_t>(1, nintra));
+                SC.iu.resize(std::max<int64_t>(1, nintra));
+                GA.iz = SC.iz.p;
+                GA.iu = SC.iu.p;
+                k_gb_ioff<<<grid_for(N, 256), 256, 0, s>>>(GA, dsl, ns, N, SC.ioff_flat.p);
+                k_gb_ifill<<<GW, 256, 0, s>>>(GA, dsl, ns, SC.chunks.p, nck);
+                first_wave = false;
+            }
             k_gb_dep<<<grid_for(N, 256), 256, 0, s>>>(GA, dsl, ns, N);
             k_gb_lca<<<GW, 256, 0, s>>>(GA, dsl, ns, SC.chunks.p, nck);
             vso.resize(N + 1);
@@ -1544,8 +1641,20 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
             unsigned long long hp[8];
             CUDA_TRY(cudaMemcpy(hp, O.prof, 64, cudaMemcpyDeviceToHost));
             fprintf(stderr, "[giant] section cycles: incr %llu full %llu neg %llu cut %llu edges %llu "
-                    "record %llu | cut-subtree entries %llu max row %llu\n", hp[0], hp[1], hp[2],
+                    "record %llu | rest-edges %llu walk steps %llu\n", hp[0], hp[1], hp[2],
                     hp[3], hp[4], hp[5], hp[6], hp[7]);
+            std::vector<unsigned long long> pc(8 * 4096);
+            CUDA_TRY(cudaMemcpy(pc.data(), O.prof + 8, pc.size() * 8, cudaMemcpyDeviceToHost));
+            int wb = 0;
+            unsigned long long wt = 0;
+            for (int b = 0; b < 4096; b++) {
+                unsigned long long t = 0;
+                for (int k = 0; k < 6; k++) t += pc[8 * b + k];
+                if (t > wt) { wt = t; wb = b; }
+            }
+            fprintf(stderr, "[giant] slowest CTA %d: incr %llu full %llu neg %llu cut %llu edges %llu "
+                    "record %llu\n", wb, pc[8 * wb], pc[8 * wb + 1], pc[8 * wb + 2], pc[8 * wb + 3],
+                    pc[8 * wb + 4], pc[8 * wb + 5]);
         }
         CUDA_TRY(cudaMemcpyAsync(hc, cnt6.p, 16, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaMemcpyAsync(&hun, unres_d.p, 8, cudaMemcpyDeviceToHost, s));
