@@ -82,25 +82,35 @@ __global__ void k_run_heads(const uint64_t *keys, int64_t ne, int64_t *head) {
 }
 
 // one thread per run: out_w = first + pairwise(rest) (np.add.reduceat, graph.py:108)
+// runs longer than this (an aggregated giant community's self-loop run can hold 10^8
+// entries) are summed by device_pairwise_sum instead of one thread
+constexpr int64_t LONG_RUN = 4096;
+constexpr int32_t MAX_LONG = 1 << 20;
+
 __global__ void k_merge_runs(const uint64_t *keys, const double *vals, const int64_t *gid,
                              int64_t ne, int b, int32_t *out_src, int32_t *out_dst, double *out_w,
-                             uint32_t *integral_bad) {
+                             uint32_t *integral_bad, int64_t *long_runs, int32_t *nlong) {
     const uint64_t mask = (b >= 64) ? ~0ull : ((1ull << b) - 1);
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne;
          e += (int64_t)gridDim.x * blockDim.x) {
         if (!(e == 0 || keys[e] != keys[e - 1])) continue;
         int64_t end = e + 1;
-        while (end < ne && keys[end] == keys[e]) end++;
+        while (end < ne && end - e <= LONG_RUN && keys[end] == keys[e]) end++;
         int64_t g = gid[e];
-        double s = reduceat_seq(vals + e, end - e);
-        out_w[g] = s;
         out_src[g] = (int32_t)(keys[e] >> b);
         out_dst[g] = (int32_t)(keys[e] & mask);
+        if (end - e > LONG_RUN) {   // long run: summed (and its integrality checked) separately
+            const int at = atomicAdd(nlong, 1);
+            long_runs[2 * at] = e;
+            long_runs[2 * at + 1] = g;
+            continue;
+        }
+        double s = reduceat_seq(vals + e, end - e);
+        out_w[g] = s;
         for (int64_t q = e; q < end; q++)
             if (vals[q] != floor(vals[q])) atomicOr(integral_bad, 1u);
     }
 }
-
 // ptr[r] = first index i with key_of(i) >= r over a sorted int32 array (n_rows + 1 entries)
 __global__ void k_lower_bound_ptr(const int32_t *sorted_rows, int64_t m, int64_t n_rows,
                                   int64_t *ptr) {
@@ -405,14 +415,100 @@ static void build_bins(slm_ctx *ctx, LevelGraph &G) {
     }
 }
 
+// Long duplicate runs, all at once: run ends by binary search on the group ids, the numpy
+// reduceat sum first + pairwise(rest) of every run from one batched leaf kernel (the host walks
+// each run's pairwise recursion down to <= 32768-element leaves and recombines in its order),
+// and one integrality check kernel.
+__global__ void k_long_ends(const uint64_t *keys, int64_t ne, const int64_t *runs, int32_t nruns,
+                            int64_t *ends) {
+    for (int32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nruns; q += gridDim.x * blockDim.x) {
+        const int64_t e = runs[2 * q];
+        const uint64_t key = keys[e];
+        int64_t lo = e, hi = ne;   // first index with a larger key (keys sorted)
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (keys[mid] <= key) lo = mid + 1;
+            else hi = mid;
+        }
+        ends[q] = lo;
+    }
+}
+__global__ void k_nonint_runs(const double *v, const int64_t *runs, const int64_t *ends,
+                              int32_t nruns, uint32_t *bad) {
+    for (int32_t q = blockIdx.x; q < nruns; q += gridDim.x)
+        for (int64_t e = runs[2 * q] + threadIdx.x; e < ends[q]; e += blockDim.x)
+            if (v[e] != floor(v[e])) {
+                atomicOr(bad, 1u);
+                break;
+            }
+}
+__global__ void k_scatter_sums(const int64_t *runs, const double *sums, int32_t nruns, double *w) {
+    for (int32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nruns; q += gridDim.x * blockDim.x)
+        w[runs[2 * q + 1]] = sums[q];
+}
+
+static void merge_long_runs(slm_ctx *ctx, const double *vals, const uint64_t *keys, int64_t ne,
+                            const int64_t *d_runs, int32_t nruns, double *out_w, uint32_t *bad) {
+    cudaStream_t s = ctx->stream;
+    static DBuf<int64_t> ends, d_off, d_len;
+    static DBuf<double> leaf, sums;
+    ends.resize(nruns);
+    k_long_ends<<<grid_for(nruns, 128), 128, 0, s>>>(keys, ne, d_runs, nruns, ends.p);
+    k_nonint_runs<<<(unsigned)std::min<int32_t>(nruns, 148 * 8), 256, 0, s>>>(vals, d_runs, ends.p,
+                                                                               nruns, bad);
+    std::vector<int64_t> hr(2 * nruns), he(nruns);
+    CUDA_TRY(cudaMemcpyAsync(hr.data(), d_runs, nruns * 16, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(he.data(), ends.p, nruns * 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    std::vector<int64_t> offs, lens, first_leaf(nruns + 1), firsts(nruns);
+    for (int32_t q = 0; q < nruns; q++) {
+        first_leaf[q] = (int64_t)offs.size();
+        offs.push_back(hr[2 * q]);   // leaf 0 of a run: its first element alone
+        lens.push_back(1);
+        pw_segments(hr[2 * q] + 1, he[q] - hr[2 * q] - 1, offs, lens);
+    }
+    first_leaf[nruns] = (int64_t)offs.size();
+    const int64_t nl = (int64_t)offs.size();
+    d_off.resize(nl);
+    d_len.resize(nl);
+    leaf.resize(nl);
+    CUDA_TRY(cudaMemcpyAsync(d_off.p, offs.data(), nl * 8, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(d_len.p, lens.data(), nl * 8, cudaMemcpyHostToDevice, s));
+    k_pw_segments<<<grid_for(nl, 128), 128, 0, s>>>(vals, d_off.p, d_len.p, nl, leaf.p);
+    std::vector<double> hl(nl), hs(nruns);
+    CUDA_TRY(cudaMemcpyAsync(hl.data(), leaf.p, nl * 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    for (int32_t q = 0; q < nruns; q++) {
+        size_t k = (size_t)first_leaf[q] + 1;
+        const double rest = pw_combine(he[q] - hr[2 * q] - 1, hl.data(), k);
+        hs[q] = hl[first_leaf[q]] + rest;
+    }
+    sums.resize(nruns);
+    CUDA_TRY(cudaMemcpyAsync(sums.p, hs.data(), nruns * 8, cudaMemcpyHostToDevice, s));
+    k_scatter_sums<<<grid_for(nruns, 128), 128, 0, s>>>(d_runs, sums.p, nruns, out_w);
+    CUDA_TRY(cudaStreamSynchronize(s));
+}
+
 void build_level_from_keys(slm_ctx *ctx, LevelGraph &G, int64_t n, DBuf<uint64_t> &keys,
                            DBuf<double> &vals, int64_t ne_in) {
     cudaStream_t s = ctx->stream;
+    const bool aprof = getenv("SLM_PROFILE_AGG") != nullptr;
+    double at0 = now_ms();
+    auto amark = [&](const char *what) {
+        if (!aprof) return;
+        CUDA_TRY(cudaStreamSynchronize(s));
+        const double t = now_ms();
+        fprintf(stderr, "[level build n=%lld ne=%lld] %s %.2f ms\n", (long long)n, (long long)ne_in,
+                what, t - at0);
+        at0 = t;
+    };
+    amark("start");
     const int b = bits_for(n);
     SLM_REQUIRE(n < (int64_t(1) << 31), SLM_EUNSUP, "more than 2^31-1 nodes");
     G.n = n;
     // 1. stable sort by (src, dst)
     if (ne_in > 0) sort_pairs_u64_f64(ctx, keys, vals, ne_in, 2 * b);
+    amark("sort");
     // 2. run heads + group ids
     DBuf<int64_t> head, gid;
     head.resize(ne_in + 1);
@@ -434,13 +530,25 @@ void build_level_from_keys(slm_ctx *ctx, LevelGraph &G, int64_t n, DBuf<uint64_t
     G.csr_dst.resize(ng);
     G.csr_w.resize(ng);
     G.csr_ptr.resize(n + 1);
-    if (ne_in > 0)
+    if (ne_in > 0) {
+        static DBuf<int64_t> lr;
+        lr.resize(2 * MAX_LONG + 2);
+        int32_t *d_nlong = (int32_t *)(lr.p + 2 * MAX_LONG);
+        CUDA_TRY(cudaMemsetAsync(d_nlong, 0, 4, s));
         k_merge_runs<<<grid_for(ne_in, 256), 256, 0, s>>>(keys.p, vals.p, gid.p, ne_in, b,
                                                           src_of.p, G.csr_dst.p, G.csr_w.p,
-                                                          d_int_bad);
+                                                          d_int_bad, lr.p, d_nlong);
+        int32_t nlong = 0;
+        CUDA_TRY(cudaMemcpyAsync(&nlong, d_nlong, 4, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        SLM_REQUIRE(nlong <= MAX_LONG, SLM_EUNSUP, "too many long duplicate runs");
+        if (nlong) merge_long_runs(ctx, vals.p, keys.p, ne_in, lr.p, nlong, G.csr_w.p, d_int_bad);
+    }
     k_lower_bound_ptr<<<grid_for(n + 1, 256), 256, 0, s>>>(src_of.p, ng, n, G.csr_ptr.p);
+    amark("merge runs");
     head.release();
     gid.release();
+    amark("release");
     // 3. stable transpose (in-CSR, graph.py:111-115): sort entry ids by dst
     DBuf<int64_t> in_ptr;
     DBuf<int32_t> in_src;
@@ -453,14 +561,17 @@ void build_level_from_keys(slm_ctx *ctx, LevelGraph &G, int64_t n, DBuf<uint64_t
         perm_in.resize(ng);
         perm_out.resize(ng);
         kout.resize(ng);
+        amark("transpose alloc");
         k_iota_i32<<<grid_for(ng, 256), 256, 0, s>>>(perm_in.p, ng);
         if (ng > 0)
             sort_pairs_u32_i32(ctx, (uint32_t *)G.csr_dst.p, (uint32_t *)kout.p, perm_in.p,
                                perm_out.p, ng, b);
+        amark("transpose sort");
         k_gather_transpose<<<grid_for(ng, 256), 256, 0, s>>>(perm_out.p, src_of.p, G.csr_w.p, ng,
                                                              in_src.p, in_w.p);
         k_lower_bound_ptr<<<grid_for(n + 1, 256), 256, 0, s>>>(kout.p, ng, n, in_ptr.p);
     }
+    amark("transpose");
     // 4. symmetric?
     int32_t *d_asym = ctx->i32c.resize(1);
     CUDA_TRY(cudaMemsetAsync(d_asym, 0, 4, s));
@@ -472,6 +583,7 @@ void build_level_from_keys(slm_ctx *ctx, LevelGraph &G, int64_t n, DBuf<uint64_t
     CUDA_TRY(cudaMemcpyAsync(intbad, d_int_bad, 8, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     G.sym = (asym == 0);
+    amark("sym check");
     // 5. union
     if (G.sym) {
         DBuf<int64_t> keep, pos;
@@ -509,6 +621,7 @@ void build_level_from_keys(slm_ctx *ctx, LevelGraph &G, int64_t n, DBuf<uint64_t
                                                        in_ptr.p, in_src.p, in_w.p, n, 1,
                                                        G.uptr.p, G.unbr.p, G.uu.p);
     }
+    amark("union");
     // 6. strengths
     G.s_out.resize(n);
     G.s_in.resize(n);
@@ -519,7 +632,9 @@ void build_level_from_keys(slm_ctx *ctx, LevelGraph &G, int64_t n, DBuf<uint64_t
         k_row_seq_sum<<<grid_for(n, 128), 128, 0, s>>>(in_ptr.p, in_w.p, n, G.s_in.p);
     G.m_w = device_pairwise_sum(ctx, G.csr_w.p, ng);
     G.integral = (intbad[0] == 0) && (G.m_w < 9007199254740992.0);
+    amark("strengths");
     build_bins(ctx, G);
+    amark("bins");
     // compact integer weights for the plan sweep's fast path, interleaved strengths
     G.s2.resize(n);
     G.u32_ok = false;

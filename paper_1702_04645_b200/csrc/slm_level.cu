@@ -52,9 +52,16 @@ __global__ void k_compact_f64(const double *v, const int64_t *flag, const int64_
     GS_LOOP(e, m) if (flag[e]) out[pos[e]] = v[e];
 }
 __global__ void k_max_i32(const int32_t *x, int64_t n, int32_t *mx, int32_t *mn) {
+    int32_t a = INT32_MIN, b = INT32_MAX;
     GS_LOOP(i, n) {
-        atomicMax(mx, x[i]);
-        atomicMin(mn, x[i]);
+        a = max(a, x[i]);
+        b = min(b, x[i]);
+    }
+    a = __reduce_max_sync(0xffffffffu, a);   // one atomic pair per warp
+    b = __reduce_min_sync(0xffffffffu, b);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(mx, a);
+        atomicMin(mn, b);
     }
 }
 __global__ void k_null_terms(const double *So, const double *Si, int64_t nc, double m, double *out) {
