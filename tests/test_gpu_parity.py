@@ -313,3 +313,24 @@ def test_plan_all_degree_bins_vs_oracle(slm, oracle):
         ref = oracle.best_targets(og, labels, int(labels.max()) + 1)
         for _ in range(2):   # repeated sweeps reuse the emptied tables
             np.testing.assert_array_equal(ctx.plan(labels), ref)
+
+
+def test_aggregate_long_runs_real_weights_bit_exact(slm, oracle):
+    """Coarse edges merging >4096 duplicates (the batched long-run path) keep numpy's
+    reduceat order bit for bit, with real-valued weights."""
+    rng = np.random.default_rng(5)
+    n = 20_000
+    s = rng.integers(0, n, 300_000)
+    d = rng.integers(0, n, 300_000)
+    keep = s != d
+    s, d = s[keep], d[keep]
+    w = rng.random(s.size) * 3.0 + 0.01
+    labels = (np.arange(n) * 7 // n).astype(np.int64)   # 7 dense communities
+    g = slm.Graph.from_edges(n, s, d, w)
+    ga = slm.aggregate(g, labels)
+    og = oracle.aggregate(oracle.OGraph.from_edges(n, s, d, w), labels)
+    p, dst, ww = ga.context().csr()
+    op, odst, oww = og.csr()
+    np.testing.assert_array_equal(p, op)
+    np.testing.assert_array_equal(dst, odst)
+    np.testing.assert_array_equal(ww, oww)
