@@ -582,20 +582,25 @@ __global__ void k_gb_dep(GiantArgs A, const GSlice *S, int ns, int64_t N) {
     }
 }
 __global__ void k_gb_lca(GiantArgs A, const GSlice *S, int ns, const int64_t *chunks, int64_t nck) {
+    // over the intra-part lists (chunk c of a member covers its list range [c, c+1) * GCH;
+    // the lists are never longer than the rows, so some chunks are empty)
     const int lane = threadIdx.x & 31;
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t k = w; k < nck; k += nw) {
-        int64_t e0, e1;
-        const int32_t y = chunk_node(A, S, ns, chunks[k], e0, e1);
+        const int64_t t = chunks[k] >> 22, c = chunks[k] & 0x3FFFFF;
+        const GSlice sl = S[slice_of(S, ns, t)];
+        const int32_t y = A.order[sl.lo + (t - sl.flat)];
         const int32_t pid = A.gmark[y];
-        for (int64_t e = e0 + lane; e < e1; e += 32) {
-            const int32_t z = A.unbr[e];
+        const int64_t b0 = A.ioff[y], cnt = A.icnt[y];
+        const int64_t q0 = b0 + c * GCH, q1 = b0 + min(cnt, (c + 1) * (int64_t)GCH);
+        for (int64_t q = q0 + lane; q < q1; q += 32) {
+            const int32_t z = A.iz[q];
             if (A.gmark[z] != pid) continue;
             const int32_t pz = A.pos[z];
             int32_t anc = y;
             while (!in_range(A, anc, pz)) anc = A.a[anc];
-            atomicAdd(&A.dep[anc], -A.uu[e]);
+            atomicAdd(&A.dep[anc], -A.iu[q]);
         }
     }
 }
