@@ -510,7 +510,7 @@ void build_level_from_keys(slm_ctx *ctx, LevelGraph &G, int64_t n, DBuf<uint64_t
     if (ne_in > 0) sort_pairs_u64_f64(ctx, keys, vals, ne_in, 2 * b);
     amark("sort");
     // 2. run heads + group ids
-    DBuf<int64_t> head, gid;
+    static DBuf<int64_t> head, gid;   // grow-only scratch kept across builds
     head.resize(ne_in + 1);
     gid.resize(ne_in + 1);
     int64_t ng = 0;
@@ -525,7 +525,7 @@ void build_level_from_keys(slm_ctx *ctx, LevelGraph &G, int64_t n, DBuf<uint64_t
     }
     SLM_REQUIRE(ng < (int64_t(1) << 31), SLM_EUNSUP, "more than 2^31-1 merged edges");
     G.ne = ng;
-    DBuf<int32_t> src_of;
+    static DBuf<int32_t> src_of;   // grow-only scratch kept across builds
     src_of.resize(ng);
     G.csr_dst.resize(ng);
     G.csr_w.resize(ng);
@@ -546,8 +546,6 @@ void build_level_from_keys(slm_ctx *ctx, LevelGraph &G, int64_t n, DBuf<uint64_t
     }
     k_lower_bound_ptr<<<grid_for(n + 1, 256), 256, 0, s>>>(src_of.p, ng, n, G.csr_ptr.p);
     amark("merge runs");
-    head.release();
-    gid.release();
     amark("release");
     // 3. stable transpose (in-CSR, graph.py:111-115): sort entry ids by dst
     DBuf<int64_t> in_ptr;
@@ -557,7 +555,7 @@ void build_level_from_keys(slm_ctx *ctx, LevelGraph &G, int64_t n, DBuf<uint64_t
     in_src.resize(ng);
     in_w.resize(ng);
     {
-        DBuf<int32_t> perm_in, perm_out, kout;
+        static DBuf<int32_t> perm_in, perm_out, kout;   // grow-only scratch kept across builds
         perm_in.resize(ng);
         perm_out.resize(ng);
         kout.resize(ng);
@@ -586,7 +584,7 @@ void build_level_from_keys(slm_ctx *ctx, LevelGraph &G, int64_t n, DBuf<uint64_t
     amark("sym check");
     // 5. union
     if (G.sym) {
-        DBuf<int64_t> keep, pos;
+        static DBuf<int64_t> keep, pos;   // grow-only scratch kept across builds
         keep.resize(ng + 1);
         pos.resize(ng + 1);
         CUDA_TRY(cudaMemsetAsync(keep.p, 0, (ng + 1) * 8, s));
@@ -603,7 +601,7 @@ void build_level_from_keys(slm_ctx *ctx, LevelGraph &G, int64_t n, DBuf<uint64_t
                                                               G.csr_w.p, pos.p, n, ng, ue,
                                                               G.uptr.p, G.unbr.p, G.uu.p);
     } else {
-        DBuf<int64_t> cnt;
+        static DBuf<int64_t> cnt;   // grow-only scratch kept across builds
         cnt.resize(n + 1);
         CUDA_TRY(cudaMemsetAsync(cnt.p + n, 0, 8, s));
         k_union_merge<<<grid_for(n, 128), 128, 0, s>>>(G.csr_ptr.p, G.csr_dst.p, G.csr_w.p,

@@ -594,14 +594,24 @@ __global__ void k_gb_lca(GiantArgs A, const GSlice *S, int ns, const int64_t *ch
         const int32_t pid = A.gmark[y];
         const int64_t b0 = A.ioff[y], cnt = A.icnt[y];
         const int64_t q0 = b0 + c * GCH, q1 = b0 + min(cnt, (c + 1) * (int64_t)GCH);
+        // deposits are cached per lane while the LCA repeats (in a hub-centred tree most
+        // edges meet at the root: one atomic per run instead of one per edge)
+        int32_t ca = -1;
+        double cv = 0.0;
         for (int64_t q = q0 + lane; q < q1; q += 32) {
             const int32_t z = A.iz[q];
             if (A.gmark[z] != pid) continue;
             const int32_t pz = A.pos[z];
             int32_t anc = y;
             while (!in_range(A, anc, pz)) anc = A.a[anc];
-            atomicAdd(&A.dep[anc], -A.iu[q]);
+            if (anc != ca) {
+                if (ca >= 0) atomicAdd(&A.dep[ca], cv);
+                ca = anc;
+                cv = 0.0;
+            }
+            cv -= A.iu[q];
         }
+        if (ca >= 0) atomicAdd(&A.dep[ca], cv);
     }
 }
 __global__ void k_gb_gather(GiantArgs A, const GSlice *S, int ns, int64_t N, double *vso,
