@@ -509,6 +509,13 @@ __global__ void k_lb32c(const uint32_t *sorted, int64_t m, int64_t nrows, int32_
         ptr[r] = (int32_t)lo;
     }
 }
+__global__ void k_ev_rec(const int32_t *ev, int64_t m, const int32_t *cand, const int32_t *comm,
+                         const int32_t *cstar, int4 *rec) {
+    GS_LOOP(q, m) {
+        const int32_t k = ev[q], i = cand[k];
+        rec[q] = make_int4(k, i, comm[i], cstar[i]);
+    }
+}
 __global__ void k_walker_list(const int32_t *tl_ptr, int64_t nc, int32_t *f) {
     GS_LOOP(c, nc) f[c] = tl_ptr[c + 1] > tl_ptr[c] ? 1 : 0;
 }
@@ -530,6 +537,7 @@ struct Live {
     int32_t *a;
     int32_t *wpos, *atk;
     const int32_t *tl_ptr, *tl_ev;
+    const int4 *tl_rec;      // per timeline event: {k, i, frm, to}
     MvList mv;
     double *gain;
     int32_t *remaining;
@@ -605,10 +613,17 @@ __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_
         int32_t my_atk = V.atk[C];          // only this walker writes atk[C]
         int dirtyC = vload8(V.dirty + C);   // monotone
         int nres = 0;                       // candidates resolved by this visit
+        int ncommit = 0, nbarrier = 0;      // (profiling)
         bool parked = false;
         const int32_t p_start = p;
+        // event records {k, i, frm, to} of the next batch are loaded one batch ahead
+        int4 rec_next = make_int4(-1, 0, 0, -1);
+        if (p + lane < end) rec_next = V.tl_rec[p + lane];
         while (p < end && !parked) {
             const int nb = min(32, end - p);
+            const int4 rec = rec_next;
+            rec_next = make_int4(-1, 0, 0, -1);
+            if (p + nb + lane < end) rec_next = V.tl_rec[p + nb + lane];
             int32_t k = -1, i = 0, frm = 0, to = -1, atF = -1, st = ST_SKIP;
             int dF = 0;
             double SoF = 0.0, SiF = 0.0;
@@ -620,11 +635,11 @@ __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_
             cs.tail_lo = cs.tail_hi = 0;
             cs.mv_cnt = 0;
             if (lane < nb) {
-                k = V.tl_ev[p + lane];
+                k = rec.x;
+                i = rec.y;
+                frm = rec.z;
+                to = rec.w;
                 st = vload(status + k);
-                i = A.cand[k];
-                frm = A.comm[i];
-                to = A.cstar[i];
                 if (to == C && st == ST_UNRES) {
                     atF = vload(V.atk + frm);
                     __threadfence();
@@ -749,7 +764,9 @@ __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_
                     g = (wt - c.w_from) / A.m - d_null / (A.m * A.m);
                     commit = g > 0.0 && j >= 0;
                 }
+                nbarrier++;
                 if (commit) {
+                    ncommit++;
                     const int32_t len = thi - tlo;
                     if (V.wst && lane == 0) atomicAdd(V.wst + 5, (unsigned long long)len);
                     for (int32_t t = tlo + lane; t < thi; t += 32) V.lab[A.order[t]] = C;
@@ -789,6 +806,8 @@ __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_
             atomicAdd(V.wst, (unsigned long long)(p - p_start));
             atomicMax(V.wst + 1, (unsigned long long)(p - p_start));
             atomicAdd(V.wst + 2, 1ull);
+            atomicMax(V.wst + 6, (unsigned long long)ncommit);
+            atomicMax(V.wst + 7, (unsigned long long)nbarrier);
         }
         if (lane == 0) {
             if (nres) atomicSub(V.remaining, nres);
@@ -826,6 +845,7 @@ __global__ void k_gather_gains(int64_t K, const int32_t *f, const int32_t *pos, 
 
 // per-call scratch of run_commit, kept across calls (grow-only)
 struct CommitScratch {
+    DBuf<int4> tl_rec;   // timeline event records
     DBuf<int32_t> big;   // big-tail candidates + count
     DBuf<int32_t> flag, pos, cand;
     DBuf<int32_t> status;
@@ -984,10 +1004,13 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
         k_acc_pairs<<<grid_for(K, 256), 256, 0, s>>>(cand.p, F.comm.p, d_cstar, K, af.p, apos.p,
                                                      keys.p, vals.p);
         stick();
+        CS.tl_rec.resize(2 * (int64_t)NA);
         sort_pairs_u32_i32(ctx, keys.p, keys_sorted.p, vals.p, tl_ev.p, 2 * (int64_t)NA,
                            bits_for(nc + 1));
         tl_ptr.resize(nc + 1);
         k_lb32c<<<grid_for(nc + 1, 256), 256, 0, s>>>(keys_sorted.p, 2 * (int64_t)NA, nc, tl_ptr.p);
+        k_ev_rec<<<grid_for(2 * (int64_t)NA, 256), 256, 0, s>>>(tl_ev.p, 2 * (int64_t)NA, cand.p,
+                                                               F.comm.p, d_cstar, CS.tl_rec.p);
         // walkers: communities with a non-empty timeline
         DBuf<int32_t> &wf = CS.wf, &wp = CS.wp;
         wf.resize(nc + 1);
@@ -1017,6 +1040,7 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
         V.atk = atk.p;
         V.tl_ptr = tl_ptr.p;
         V.tl_ev = tl_ev.p;
+        V.tl_rec = CS.tl_rec.p;
         V.mv.z = mv_z.p;
         V.mv.u = mv_u.p;
         V.mv.e = mv_e.p;
@@ -1061,8 +1085,9 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
                 unsigned long long h[8];
                 CUDA_TRY(cudaMemcpy(h, wst.p, 64, cudaMemcpyDeviceToHost));
                 char buf[160];
-                snprintf(buf, sizeof buf, "[%.2fms ev %llu max %llu w %llu rp %llu/%llu tl %llu]",
-                         rt.back(), h[0], h[1], h[2], h[3], h[4], h[5]);
+                snprintf(buf, sizeof buf, "[%.2fms ev %llu max %llu w %llu rp %llu/%llu tl %llu "
+                         "maxcommit %llu maxbarrier %llu]",
+                         rt.back(), h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
                 rinfo.push_back(buf);
             }
             ctx->last_rounds = round + 1;
