@@ -345,6 +345,23 @@ static void build_bins(slm_ctx *ctx, LevelGraph &G) {
     CUDA_TRY(cudaMemcpyAsync(up.data(), G.uptr.p, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     G.max_deg = mx;
+    // bin 0 stably partitioned by degree: rows with d <= TINY_MAX first (the lane-per-row
+    // kernel), then the rest; both parts keep ascending row ids (their union entries and row
+    // metadata stay nearly sequential in memory)
+    {
+        const int64_t nb0 = G.bin_off[1] - G.bin_off[0];
+        std::vector<int32_t> part(nb0);
+        int64_t k0 = 0;
+        for (int64_t k = 0; k < nb0; k++)
+            if (up[rows[k] + 1] - up[rows[k]] <= TINY_MAX) part[k0++] = rows[k];
+        G.bin0_tiny = k0;
+        for (int64_t k = 0; k < nb0; k++)
+            if (up[rows[k] + 1] - up[rows[k]] > TINY_MAX) part[k0++] = rows[k];
+        std::copy(part.begin(), part.end(), rows.begin());
+        if (nb0)
+            CUDA_TRY(cudaMemcpyAsync(G.bin_rows.p, rows.data(), nb0 * 4, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+    }
     for (int b = 0; b < NBINS; b++) {
         int64_t e = 0;
         for (int64_t k = G.bin_off[b]; k < G.bin_off[b + 1]; k++) e += up[rows[k] + 1] - up[rows[k]];

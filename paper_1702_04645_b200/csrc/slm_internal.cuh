@@ -80,6 +80,7 @@ __host__ __device__ constexpr int64_t bin_hi(int b) {
     return b == 0 ? 32 : b == 1 ? 256 : b == 2 ? 1024 : b == 3 ? 4096 : b == 4 ? 16383 : INT64_MAX;
 }
 constexpr int SMALL_MAX = 32;     // warp lanes = entries (packed rows)
+constexpr int TINY_MAX = 8;       // bin-0 rows up to this degree: one lane per row
 constexpr int MID_MAX = 4096;     // generic path: CTA-per-row shared-memory hash up to here
 
 constexpr int HUB_SEG = 4096;     // entries per hub-row work item of the integer sweep
@@ -106,6 +107,7 @@ struct LevelGraph {
     DBuf<int32_t> bin_rows;
     int64_t bin_off[NBINS + 1] = {0, 0, 0, 0, 0, 0, 0};
     int64_t bin_entries[NBINS] = {0, 0, 0, 0, 0, 0};
+    int64_t bin0_tiny = 0;     // bin-0 rows: the first bin0_tiny have d <= TINY_MAX (stable partition)
     DBuf<int64_t> large_hoff;  // per row with d > MID_MAX (bins 4, 5): global hash offset
     int64_t large_hash_total = 0;
     // bin-5 (hub) rows of the integer sweep, in processing order j (descending degree):

@@ -237,12 +237,20 @@ __global__ void __launch_bounds__(256) k_sweep_small(SweepArgs<SYM> A, const int
             const unsigned long long key =
                 valid ? (((unsigned long long)s << 32) | (uint32_t)c) : ~0ull;
             const unsigned gm = __match_any_sync(0xffffffffu, key);
-            // group sums by a uniform shuffle loop (a REDUX with per-group masks would be
-            // serialised per group)
-            uint32_t gs = 0;
-            for (int q = 0; q < total; q++) {
-                const uint32_t v = __shfl_sync(0xffffffffu, wt, q);
-                if ((gm >> q) & 1u) gs += v;
+            // group sums: every lane adds its group's other members, one shuffle per member
+            // (uniform trip count = the largest group of the warp, usually 1-3)
+            uint32_t gs = wt;
+            {
+                unsigned rest = valid ? gm & ~(1u << lane) : 0u;
+                const int mx = (int)__reduce_max_sync(0xffffffffu, (unsigned)__popc(rest));
+                for (int t = 0; t < mx; t++) {
+                    const int src = rest ? __ffs(rest) - 1 : lane;
+                    const uint32_t v = __shfl_sync(0xffffffffu, wt, src);
+                    if (rest) {
+                        gs += v;
+                        rest &= rest - 1;
+                    }
+                }
             }
             const bool leader = valid && lane == __ffs(gm) - 1;
             if (A.groups) {
@@ -250,47 +258,123 @@ __global__ void __launch_bounds__(256) k_sweep_small(SweepArgs<SYM> A, const int
                 if (lane == 0 && lm) atomicAdd(A.groups, (unsigned long long)__popc(lm));
             }
             const bool own = (c == Lr);
-            double bt = -INFINITY, ts = -INFINITY;
+            double bt = -INFINITY;
             int32_t bc = 0x7fffffff;
-            int hs = 0;
+            // the own group's leader publishes the staying score for its row slot
+            const unsigned om = __ballot_sync(0xffffffffu, leader && own);
+            double ts = 0.0;
             if (leader) {
                 const double2 srr = node_s(A, rr);
                 const double t = exact_t(gs, null_P(own, srr, comm_S(A, c)), A.m, A.m2);
                 if (own) {
                     ts = t;
-                    hs = 1;
                 } else {
                     bt = t;
                     bc = c;
                 }
             }
-            // segmented inclusive scan over the lanes of one row
+            // segmented inclusive max over the lanes of one row (rst = the row's first lane)
 #pragma unroll
             for (int off = 1; off < 32; off <<= 1) {
                 const double obt = __shfl_up_sync(0xffffffffu, bt, off);
                 const int32_t obc = __shfl_up_sync(0xffffffffu, bc, off);
-                const double ots = __shfl_up_sync(0xffffffffu, ts, off);
-                const int ohs = __shfl_up_sync(0xffffffffu, hs, off);
-                const int os = __shfl_up_sync(0xffffffffu, s, off);
-                if (lane >= off && os == s) {
-                    if (better2(obt, obc, bt, bc)) {
-                        bt = obt;
-                        bc = obc;
-                    }
-                    if (ohs) {
-                        ts = ots;
-                        hs = 1;
-                    }
+                if (lane - off >= rst && better2(obt, obc, bt, bc)) {
+                    bt = obt;
+                    bc = obc;
                 }
             }
             const int nxt = __shfl_down_sync(0xffffffffu, s, 1);
             const bool last = valid && (lane == total - 1 || nxt != s);
+            // the row's own-group leader (if any) lies in [rst, lane]
+            const unsigned rowmask = (lane == 31 ? 0xffffffffu : ((2u << lane) - 1u)) & ~((1u << rst) - 1u);
+            const unsigned ol = om & rowmask;
+            const double tso = __shfl_sync(0xffffffffu, ts, ol ? __ffs(ol) - 1 : lane);
             if (last) {
                 const double t_stay =
-                    hs ? ts : stay_default(node_s(A, rr), comm_S(A, Lr), A.m2);
+                    ol ? tso : stay_default(node_s(A, rr), comm_S(A, Lr), A.m2);
                 A.cstar[rr] = (bc != 0x7fffffff && bt > t_stay) ? bc : Lr;
             }
             rcur += k;
+        }
+    }
+}
+
+// bin 0, rows of d <= TINY_MAX: one lane per row, rows in ascending id order (consecutive
+// lanes read nearly consecutive union entries; loads beyond d are predicated off).  The row's entries are deduplicated in registers (a D x D compare of
+// their communities), every group is scored with the fp32 bound filter, and only the groups
+// the filter cannot separate are evaluated in fp64 -- usually none (decide_fast).
+template <bool SYM, int D>
+__global__ void __launch_bounds__(256) k_sweep_tiny(SweepArgs<SYM> A, const int32_t *rows,
+                                                     int64_t nrows) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t r = rows[i];
+        const int64_t e0 = A.uptr[r];
+        const int d = (int)(A.uptr[r + 1] - e0);
+        const int32_t L = A.label[r];
+        int32_t z[D], c[D];
+        uint32_t w[D];
+#pragma unroll
+        for (int k = 0; k < D; k++) {
+            z[k] = k < d ? __ldcs(A.unbr + e0 + k) : -1;
+            w[k] = k < d ? __ldcs(A.u32 + e0 + k) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < D; k++) c[k] = z[k] >= 0 ? __ldg(A.label + z[k]) : -1 - k;
+        const double2 sr = node_s(A, r);
+        const float2 srf = make_float2((float)sr.x, (float)sr.y);
+        Sel S;
+        sel_init(S);
+        bool hown = false;
+        uint32_t gown = 0, ng = 0;
+        uint32_t first = 0;   // bit k: entry k opens its group
+        uint32_t gs[D];       // entry k's group sum
+#pragma unroll
+        for (int k = 0; k < D; k++) {
+            bool fst = k < d;
+            uint32_t g = w[k];
+#pragma unroll
+            for (int q = 0; q < D; q++) {
+                if (q == k) continue;
+                const bool same = c[q] == c[k];
+                if (q < k && same) fst = false;
+                g += same ? w[q] : 0u;
+            }
+            if (fst) {
+                first |= 1u << k;
+                ng++;
+                if (c[k] == L) {
+                    hown = true;
+                    gown = g;
+                } else {
+                    float lo;
+                    const float up = approx_up(g, comm_Sf(A, c[k]), srf, A.inv_mf, A.inv_m2f, lo);
+                    sel_add(S, c[k], g, up, lo);
+                }
+            }
+            gs[k] = g;
+        }
+        if (A.groups) atomicAdd(A.groups, (unsigned long long)ng);
+        if (S.lo == -INFINITY) {
+            A.cstar[r] = L;
+        } else if (S.up2 < S.lo) {
+            A.cstar[r] = decide_fast(A, S.g1, S.c1, S.lo, S.up1, hown, gown, sr, srf, L);
+        } else {
+            double bt = -INFINITY;
+            int32_t bc = 0x7fffffff;
+#pragma unroll
+            for (int k = 0; k < D; k++) {
+                if (!((first >> k) & 1u) || c[k] == L) continue;
+                float lo;
+                const float up = approx_up(gs[k], comm_Sf(A, c[k]), srf, A.inv_mf, A.inv_m2f, lo);
+                if (up < S.lo) continue;
+                const double t = exact_t(gs[k], null_P(false, sr, comm_S(A, c[k])), A.m, A.m2);
+                if (better2(t, c[k], bt, bc)) {
+                    bt = t;
+                    bc = c[k];
+                }
+            }
+            A.cstar[r] = decide(A, bt, bc, hown, gown, sr, L);
         }
     }
 }
@@ -892,6 +976,8 @@ struct HubArgs {
     uint32_t *ovf;           // per j: the sized table overflowed this sweep (left zero)
     int32_t *fb;             // rows to redo with the full table, count in fb_n
     uint32_t *fb_n;
+    uint8_t *route;          // per j: 0 = global-table kernels, 1 = done by the shared-table
+                             // kernel, 2 = shared table overflowed (fallback list only)
 };
 
 // slots used by hub row j this sweep: 4x the previous sweep's group count (rounded to a
@@ -920,6 +1006,7 @@ __global__ void __launch_bounds__(HUB_BLOCK, 2) k_sweep_hub_merge(SweepArgs<SYM>
     constexpr int MU = 4;
     for (int64_t q = blockIdx.x; q < Hb.nitems; q += gridDim.x) {
         const int64_t j = Hb.items[q] >> 20, sg = Hb.items[q] & 0xFFFFF;
+        if (Hb.route[j]) continue;   // CTA-uniform: k_sweep_hub_smem / the fallback own it
         const int32_t r = Hb.rows[Hb.row_of[j]];
         const int64_t e0 = A.uptr[r], d = A.uptr[r + 1] - e0;
         const int64_t lo = sg * HUB_SEG, hi = min(d, lo + HUB_SEG);
@@ -992,6 +1079,7 @@ __global__ void __launch_bounds__(HUB_BLOCK) k_sweep_hub_select(SweepArgs<SYM> A
     if (threadIdx.x == 0) B.hown = 0;
     __syncthreads();
     for (int64_t j = blockIdx.x; j < Hb.nrows; j += gridDim.x) {
+        if (Hb.route[j]) continue;   // k_sweep_hub_smem / the fallback own it
         const int32_t r = Hb.rows[Hb.row_of[j]];
         const uint32_t no = Hb.cnt[j];
         int2 *GT = Hb.tab + Hb.off[j];
@@ -1044,6 +1132,7 @@ __global__ void __launch_bounds__(HUB_BLOCK, 2) k_sweep_hub_row(SweepArgs<SYM> A
         __syncthreads();
         const int64_t j = s_row;
         if (j >= Hb.nrows) break;
+        if (Hb.route[j]) continue;   // k_sweep_hub_smem / the fallback own it
         const int32_t r = Hb.rows[Hb.row_of[j]];
         const int64_t e0 = A.uptr[r], d = A.uptr[r + 1] - e0;
         int2 *GT = Hb.tab + Hb.off[j];
@@ -1165,6 +1254,207 @@ __global__ void __launch_bounds__(HUB_BLOCK) k_sweep_hub_fallback(SweepArgs<SYM>
     }
 }
 
+// Hub rows whose groups fit one SM's shared memory: one CTA (HS_BLOCK threads) per row,
+// rows claimed largest first from a counter.  The table is split into a key array and a
+// sum array (HS_SLOTS each, 4-byte slots spread over all 32 banks), linear probing with
+// Fibonacci hashing, no occupied list: the selection and the clear scan every slot (rows
+// here have >= 16K entries, so the scan is a small fraction of the row).  A row is routed
+// here when its previous group count (or d / 4 when unknown) is at most HS_GMAX; one whose
+// groups do not fit (a probe sequence exceeds PROBE_MAX) is handed to the global fallback.
+// This replaces the global-table merge (an L2 round trip per segment group) for most rows.
+constexpr int HS_BLOCK = 1024;
+constexpr int HS_SLOTS = 16384;
+constexpr uint32_t HS_GMAX = 11000;
+
+template <int U>
+__device__ __forceinline__ void insert_soa(uint32_t kb, uint32_t sb, uint32_t hmask, uint32_t hsh,
+                                           const int32_t (&c)[U], const uint32_t (&w)[U],
+                                           int *ovf) {
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        if (c[u] < 0) continue;
+        uint32_t sl = ((uint32_t)c[u] * 2654435769u) >> hsh;
+        uint32_t p = 0;
+        bool ok = true;
+        for (;;) {
+            int32_t k = lds_vol(kb + sl * 4);
+            if (k == c[u]) break;
+            if (k == -1) {
+                k = cas_s(kb + sl * 4, -1, c[u]);
+                if (k == -1 || k == c[u]) break;
+            }
+            sl = (sl + 1) & hmask;
+            if (++p == PROBE_MAX) {
+                *ovf = 1;
+                ok = false;
+                break;
+            }
+        }
+        if (ok) red_add_s(sb + sl * 4, w[u]);
+    }
+}
+
+template <bool SYM>
+__global__ void __launch_bounds__(HS_BLOCK, 1) k_sweep_hub_smem(SweepArgs<SYM> A, HubArgs Hb,
+                                                                uint32_t *next) {
+    extern __shared__ int32_t hkeys[];
+    uint32_t *hsums = (uint32_t *)(hkeys + HS_SLOTS);
+    const uint32_t kb = smem_addr(hkeys), sb = smem_addr(hsums);
+    constexpr uint32_t hmask = HS_SLOTS - 1;
+    constexpr uint32_t hsh = 32 - 14;   // log2(HS_SLOTS) high bits of the product
+    static_assert(HS_SLOTS == 1 << 14, "hsh");
+    __shared__ uint32_t s_row, s_cnt;
+    __shared__ int s_ovf;
+    __shared__ BlockSel B;
+    constexpr int NW = HS_BLOCK / 32;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int k = threadIdx.x; k < HS_SLOTS; k += HS_BLOCK) {
+        hkeys[k] = -1;
+        hsums[k] = 0;
+    }
+    if (threadIdx.x == 0) {
+        s_ovf = 0;
+        s_cnt = 0;
+        B.hown = 0;
+    }
+    constexpr int U = 4;
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_row = atomicAdd(next, 1u);
+        __syncthreads();
+        const int64_t j = s_row;
+        if (j >= Hb.nrows) break;
+        const int32_t r = Hb.rows[Hb.row_of[j]];
+        const int64_t e0 = A.uptr[r];
+        const uint32_t d = (uint32_t)(A.uptr[r + 1] - e0);
+        const uint32_t gp = Hb.gprev[j];
+        const uint32_t pred = gp ? gp : d / 4;
+        if (pred > HS_GMAX) {
+            if (threadIdx.x == 0) Hb.route[j] = 0;
+            continue;
+        }
+        if (threadIdx.x == 0) Hb.route[j] = 1;
+        const int32_t L = A.label[r];
+        const double2 sr = node_s(A, r);
+        const float2 srf = make_float2((float)sr.x, (float)sr.y);
+        const int32_t *nb = A.unbr + e0;
+        const uint32_t *ub = A.u32 + e0;
+        int32_t z[U];
+        uint32_t wt[U];
+        load_raw<U, HS_BLOCK>(nb, ub, d, threadIdx.x, z, wt);
+        for (uint32_t cb = 0; cb < d; cb += HS_BLOCK * U) {
+            int32_t c[U];
+            uint32_t w2[U];
+            gather_labels<U>(A.label, z, c);
+#pragma unroll
+            for (int u = 0; u < U; u++) w2[u] = wt[u];
+            if (cb + HS_BLOCK * U < d) load_raw<U, HS_BLOCK>(nb, ub, d, cb + HS_BLOCK * U + threadIdx.x, z, wt);
+            insert_soa<U>(kb, sb, hmask, hsh, c, w2, &s_ovf);
+        }
+        __syncthreads();
+        const bool over = s_ovf != 0;
+        if (!over) {
+            // selection over every slot (approximate pass), as block_select
+            Sel S;
+            sel_init(S);
+            uint32_t nocc = 0;
+            for (uint32_t k0 = threadIdx.x; k0 < HS_SLOTS; k0 += HS_BLOCK * 4) {
+                int32_t kk[4];
+                uint32_t gg[4];
+                float2 Sc[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    kk[u] = hkeys[k0 + u * HS_BLOCK];
+                    gg[u] = hsums[k0 + u * HS_BLOCK];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    Sc[u] = (kk[u] >= 0 && kk[u] != L) ? comm_Sf(A, kk[u]) : make_float2(0.f, 0.f);
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    if (kk[u] < 0) continue;
+                    nocc++;
+                    if (kk[u] == L) {
+                        B.gown = gg[u];
+                        B.hown = 1;
+                    } else {
+                        float lo;
+                        const float up = approx_up(gg[u], Sc[u], srf, A.inv_mf, A.inv_m2f, lo);
+                        sel_add(S, kk[u], gg[u], up, lo);
+                    }
+                }
+            }
+            nocc = __reduce_add_sync(0xffffffffu, nocc);
+            if (lane == 0) atomicAdd(&s_cnt, nocc);
+            float lo = warp_maxf(S.lo);
+            if (lane == 0) B.lo[wid] = lo;
+            __syncthreads();
+            lo = warp_maxf(lane < NW ? B.lo[lane] : -INFINITY);
+            unsigned cnt = __reduce_add_sync(0xffffffffu, (S.up1 >= lo) + (S.up2 >= lo));
+            if (lane == 0) B.cnt[wid] = cnt;
+            __syncthreads();
+            cnt = __reduce_add_sync(0xffffffffu, lane < NW ? B.cnt[lane] : 0u);
+            const uint32_t ng = s_cnt;
+            if (A.groups && threadIdx.x == 0) atomicAdd(A.groups, (unsigned long long)ng);
+            if (lo == -INFINITY) {
+                if (threadIdx.x == 0) A.cstar[r] = L;
+            } else if (cnt == 1) {
+                if (S.up1 >= lo)
+                    A.cstar[r] = decide_fast(A, S.g1, S.c1, lo, S.up1, B.hown != 0, B.gown, sr, srf, L);
+            } else {
+                if (A.stats && threadIdx.x == 0) {
+                    atomicAdd(A.stats + 4, 1ull);
+                    atomicAdd(A.stats + 5, (unsigned long long)ng);
+                }
+                double bt = -INFINITY;
+                int32_t bc = 0x7fffffff;
+                for (uint32_t k = threadIdx.x; k < HS_SLOTS; k += HS_BLOCK) {
+                    const int32_t c = hkeys[k];
+                    if (c < 0 || c == L) continue;
+                    const uint32_t g = hsums[k];
+                    float lo2;
+                    const float up = approx_up(g, comm_Sf(A, c), srf, A.inv_mf, A.inv_m2f, lo2);
+                    if (up < lo) continue;
+                    const double t = exact_t(g, null_P(false, sr, comm_S(A, c)), A.m, A.m2);
+                    if (better2(t, c, bt, bc)) {
+                        bt = t;
+                        bc = c;
+                    }
+                }
+                warp_best(bt, bc);
+                if (lane == 0) {
+                    B.bt[wid] = bt;
+                    B.bc[wid] = bc;
+                }
+                __syncthreads();
+                if (wid == 0) {
+                    bt = lane < NW ? B.bt[lane] : -INFINITY;
+                    bc = lane < NW ? B.bc[lane] : 0x7fffffff;
+                    warp_best(bt, bc);
+                    if (lane == 0) A.cstar[r] = decide(A, bt, bc, B.hown != 0, B.gown, sr, L);
+                }
+            }
+            if (threadIdx.x == 0) Hb.gprev[j] = ng;
+        } else if (threadIdx.x == 0) {
+            Hb.route[j] = 2;   // not selected here: only the fallback redoes it (and records its groups)
+            Hb.fb[atomicAdd(Hb.fb_n, 1u)] = (int32_t)j;
+            if (A.stats) atomicAdd(A.stats + 6, 1ull);
+        }
+        __syncthreads();
+        for (int k = threadIdx.x; k < HS_SLOTS; k += HS_BLOCK) {
+            if (hkeys[k] != -1) {
+                hkeys[k] = -1;
+                hsums[k] = 0;
+            }
+        }
+        if (threadIdx.x == 0) {
+            s_ovf = 0;
+            s_cnt = 0;
+            B.hown = 0;
+        }
+    }
+}
+
 __global__ void k_copy_labels32(const int32_t *label, int64_t n, int32_t *out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -1209,7 +1499,7 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
     auto rows = [&](int b) { return G.bin_rows.p + G.bin_off[b]; };
     constexpr int W1 = 8;
     constexpr size_t SM1 = (size_t)W1 * 512 * 10, SM2 = 2048 * 10, SM3 = 2048 * 10,
-                     SM4 = 8192 * 10, SMH = HUB_H * 10 + HUB_SEG * 4;
+                     SM4 = 8192 * 10, SMH = HUB_H * 10 + HUB_SEG * 4, SMHS = HS_SLOTS * 8;
     auto k1 = k_sweep_warp<512, W1, SYM>;
     auto k2 = k_sweep_cta<128, 2048, 2, 8, SYM>;
     auto k3 = k_sweep_cta<256, 2048, 1, 4, SYM>;
@@ -1217,6 +1507,7 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
     auto khm = k_sweep_hub_merge<SYM>;
     auto khs = k_sweep_hub_select<SYM>;
     auto khr = k_sweep_hub_row<SYM>;
+    auto khsm = k_sweep_hub_smem<SYM>;
     static bool attrs[2] = {false, false};
     if (!attrs[SYM]) {
         set_smem(k1, SM1);
@@ -1225,13 +1516,20 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
         set_smem(k4, SM4);
         set_smem(khm, SMH);
         set_smem(khr, SMH);
+        set_smem(khsm, SMHS);
         attrs[SYM] = true;
     }
     if (nb(0) && (bin_mask & 1)) {
-        const int64_t warps = 148LL * 64;
-        int64_t rpw = std::max<int64_t>(64, (nb(0) + warps - 1) / warps);
-        int64_t nw = (nb(0) + rpw - 1) / rpw;
-        k_sweep_small<SYM><<<grid_for(nw * 32, 256), 256, 0, s>>>(A, rows(0), nb(0), rpw);
+        static const bool no_tiny = getenv("SLM_TINY") && atoi(getenv("SLM_TINY")) == 0;
+        const int64_t nt = no_tiny ? 0 : G.bin0_tiny, ns = nb(0) - nt;
+        if (nt)
+            k_sweep_tiny<SYM, TINY_MAX><<<grid_for(nt, 256), 256, 0, s>>>(A, rows(0), nt);
+        if (ns) {
+            const int64_t warps = 148LL * 64;
+            int64_t rpw = std::max<int64_t>(64, (ns + warps - 1) / warps);
+            int64_t nw = (ns + rpw - 1) / rpw;
+            k_sweep_small<SYM><<<grid_for(nw * 32, 256), 256, 0, s>>>(A, rows(0) + nt, ns, rpw);
+        }
     }
     if (nb(1) && (bin_mask & 2))
         k1<<<grid_for(nb(1) * 32, W1 * 32, 148LL * 4), W1 * 32, SM1, s>>>(A, rows(1), nb(1));
@@ -1290,15 +1588,25 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
             G.hub_gprev.resize(nh);
             CUDA_TRY(cudaMemsetAsync(G.hub_gprev.p, 0, nh * 4, s));
         }
-        if (ctx->hub_ovf.n < (size_t)(2 * nh + 2)) {
-            ctx->hub_ovf.resize(2 * nh + 2);
-            CUDA_TRY(cudaMemsetAsync(ctx->hub_ovf.p, 0, (2 * nh + 2) * 4, s));
+        // hub_ovf: [0, nh) overflow flags, [nh, 2nh) fallback rows, [2nh] their count,
+        // [2nh + 1] hub_row counter, [2nh + 2] hub_smem counter, then nh route bytes
+        const int64_t novf_words = 2 * nh + 4 + (nh + 3) / 4;
+        if (ctx->hub_ovf.n < (size_t)novf_words) {
+            ctx->hub_ovf.resize(novf_words);
+            CUDA_TRY(cudaMemsetAsync(ctx->hub_ovf.p, 0, novf_words * 4, s));
         }
-        CUDA_TRY(cudaMemsetAsync(ctx->hub_ovf.p + 2 * nh, 0, 4, s));
+        CUDA_TRY(cudaMemsetAsync(ctx->hub_ovf.p + 2 * nh, 0, 12, s));
         Hb.gprev = G.hub_gprev.p;
         Hb.ovf = ctx->hub_ovf.p;
         Hb.fb = (int32_t *)(ctx->hub_ovf.p + nh);
         Hb.fb_n = ctx->hub_ovf.p + 2 * nh;
+        Hb.route = (uint8_t *)(ctx->hub_ovf.p + 2 * nh + 4);
+        static const bool no_smem = getenv("SLM_HUB_SMEM") && atoi(getenv("SLM_HUB_SMEM")) == 0;
+        if (no_smem) {
+            CUDA_TRY(cudaMemsetAsync(Hb.route, 0, nh, s));
+        } else {
+            k_sweep_hub_smem<SYM><<<148, HS_BLOCK, SMHS, s>>>(A, Hb, ctx->hub_ovf.p + 2 * nh + 2);
+        }
         static const bool two_kernels = getenv("SLM_HUB_MODE") && atoi(getenv("SLM_HUB_MODE")) == 1;
         if (two_kernels) {
             khm<<<(unsigned)std::min<int64_t>(G.hub_nseg, 148LL * 2), HUB_BLOCK, SMH, s>>>(A, Hb);
@@ -1318,6 +1626,7 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
                 uint32_t *next = ctx->hub_ovf.p + 2 * nh + 1;   // row counter, starts at nbig
                 const uint32_t start = (uint32_t)nbig;
                 CUDA_TRY(cudaMemcpyAsync(next, &start, 4, cudaMemcpyHostToDevice, s));
+                // (pageable source: the copy completes before the call returns)
                 k_sweep_hub_row<SYM><<<(unsigned)std::min<int64_t>(nh - nbig, 148LL * 2), HUB_BLOCK,
                                        SMH, s>>>(A, Hb, next);
             }

@@ -1,6 +1,6 @@
 """Summarise an ncu launch list of bench.py's timed region (tools/prof.sh): per-kernel time
 and DRAM bytes for one sweep, and write profiles/plan_sweep_traffic.json.
-usage: python tools/summarize_launches.py gpurun_out/launches_TAG.csv TAG [steps]"""
+usage: python tools/summarize_launches.py gpurun_out/launches_TAG.csv TAG [steps] [write]"""
 import collections, csv, json, os, sys
 
 path, tag = sys.argv[1], sys.argv[2]
@@ -38,5 +38,6 @@ out = {"round": tag, "workload": "c5_rmat24", "dram_bytes_per_sweep": int(tot_b 
        "method": f"ncu --profile-from-start off (bench.py timed region, {steps} sweeps): sum of "
                  "dram__bytes_read.sum + dram__bytes_write.sum over every launch / sweeps",
        "source": os.path.basename(path)}
-json.dump(out, open(os.path.join(os.path.dirname(__file__), "..", "profiles",
+if len(sys.argv) > 4 and sys.argv[4] == "write":
+  json.dump(out, open(os.path.join(os.path.dirname(__file__), "..", "profiles",
                                  "plan_sweep_traffic.json"), "w"), indent=1)
