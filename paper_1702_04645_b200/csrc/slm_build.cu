@@ -313,7 +313,7 @@ double device_pairwise_sum(slm_ctx *ctx, const double *d_a, int64_t n) {
     return pw_combine(n, h.data(), idx);
 }
 
-static void build_bins(slm_ctx *ctx, LevelGraph &G) {
+void build_bins(slm_ctx *ctx, LevelGraph &G) {
     int64_t n = G.n;
     cudaStream_t s = ctx->stream;
     DBuf<int64_t> f, p;
@@ -692,4 +692,96 @@ void build_level_from_edges(slm_ctx *ctx, LevelGraph &G, int64_t n, const int32_
         k_make_keys<<<grid_for(ne_in, 256), 256, 0, s>>>(d_src, d_dst, d_w, ne_in, bits_for(n),
                                                          keys.p, vals.p);
     build_level_from_keys(ctx, G, n, keys, vals, ne_in);
+}
+
+// ------------------------------------------------- degree-ordered view of the union
+
+__global__ void k_view_keys(const int64_t *uptr, int64_t n, uint32_t *key, int32_t *idx) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        key[i] = ~(uint32_t)(uptr[i + 1] - uptr[i]);   // ascending key = descending degree
+        idx[i] = (int32_t)i;
+    }
+}
+
+__global__ void k_view_rows(const int64_t *uptr, const int32_t *order, int64_t n, int64_t *vdeg,
+                            int32_t *newid) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = order[k];
+        vdeg[k] = uptr[v + 1] - uptr[v];
+        newid[v] = (int32_t)k;
+    }
+}
+
+// one warp per view row: entries copied in order, neighbours renumbered
+__global__ void k_view_entries(const int64_t *uptr, const int32_t *unbr, const uint32_t *u32,
+                               const int32_t *order, const int32_t *newid, int64_t n,
+                               const int64_t *vptr, int32_t *vnbr, uint32_t *vu32) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; k < n;
+         k += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int32_t v = order[k];
+        const int64_t s0 = uptr[v], d = uptr[v + 1] - s0, t0 = vptr[k];
+        for (int64_t t = lane; t < d; t += 32) {
+            vnbr[t0 + t] = newid[unbr[s0 + t]];
+            vu32[t0 + t] = u32[s0 + t];
+        }
+    }
+}
+
+template <class T>
+__global__ void k_view_gather(const T *src, const int32_t *order, int64_t n, T *dst) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x)
+        dst[k] = src[order[k]];
+}
+
+SweepView &ensure_sweep_view(slm_ctx *ctx, const LevelGraph &G) {
+    if (G.view) return *G.view;
+    cudaStream_t s = ctx->stream;
+    auto W = std::make_shared<SweepView>();
+    LevelGraph &V = W->V;
+    const int64_t n = G.n, ue = G.ue;
+    V.n = n;
+    V.ne = 0;
+    V.ue = ue;
+    V.sym = G.sym;
+    V.integral = G.integral;
+    V.u32_ok = G.u32_ok;
+    V.m_w = G.m_w;
+    W->order.resize(n);
+    W->vlabel.resize(n);
+    W->vcstar.resize(n);
+    {
+        DBuf<uint32_t> k0, k1;
+        DBuf<int32_t> i0, nid;
+        k0.resize(n);
+        k1.resize(n);
+        i0.resize(n);
+        nid.resize(n);
+        k_view_keys<<<grid_for(n, 256), 256, 0, s>>>(G.uptr.p, n, k0.p, i0.p);
+        sort_pairs_u32_i32(ctx, k0.p, k1.p, i0.p, W->order.p, n, 32);   // stable (LSD)
+        DBuf<int64_t> vdeg;
+        vdeg.resize(n + 1);
+        CUDA_TRY(cudaMemsetAsync(vdeg.p + n, 0, 8, s));
+        k_view_rows<<<grid_for(n, 256), 256, 0, s>>>(G.uptr.p, W->order.p, n, vdeg.p, nid.p);
+        V.uptr.resize(n + 1);
+        cub_exclusive_sum<int64_t>(ctx, vdeg.p, V.uptr.p, n + 1);
+        V.unbr.resize(ue);
+        V.uu32.resize(ue);
+        k_view_entries<<<grid_for(n * 32, 256), 256, 0, s>>>(G.uptr.p, G.unbr.p, G.uu32.p,
+                                                               W->order.p, nid.p, n, V.uptr.p,
+                                                               V.unbr.p, V.uu32.p);
+    }
+    V.s_out.resize(n);
+    k_view_gather<double><<<grid_for(n, 256), 256, 0, s>>>(G.s_out.p, W->order.p, n, V.s_out.p);
+    if (!G.sym) {
+        V.s2.resize(n);
+        k_view_gather<double2><<<grid_for(n, 256), 256, 0, s>>>(G.s2.p, W->order.p, n, V.s2.p);
+    }
+    CUDA_TRY(cudaGetLastError());
+    build_bins(ctx, V);
+    G.view = W;
+    return *W;
 }

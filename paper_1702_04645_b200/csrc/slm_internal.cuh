@@ -86,6 +86,9 @@ constexpr int MID_MAX = 4096;     // generic path: CTA-per-row shared-memory has
 constexpr int HUB_SEG = 4096;     // entries per hub-row work item of the integer sweep
 constexpr int64_t HUB_BIG_DEG = 32768;   // hub rows spread over CTAs by segment above this
 
+struct SweepView;
+struct slm_ctx;
+
 // Canonical directed CSR + neighbour union + strengths of one hierarchy level
 // (graph.py:63-175, 257-263).  Node ids int32, entry offsets int64.
 struct LevelGraph {
@@ -117,7 +120,22 @@ struct LevelGraph {
     int64_t hub_nseg = 0, hub_rows_n = 0, hub_ring = 0;   // hub_ring: arena slots
     int64_t hub_big_rows = 0, hub_big_items = 0;        // rows with d > HUB_BIG_DEG (prefix)
     int32_t max_deg = 0;
+    // degree-ordered copy of the union for the integer plan sweep (built on first use)
+    mutable std::shared_ptr<SweepView> view;
 };
+
+// The integer plan sweep's view of a level: union rows renumbered by descending degree
+// (stable by id), neighbour ids mapped to the new numbering.  Group sums are exact integers
+// and the argmax compares community ids, so the sweep over the view yields the reference's
+// targets bit for bit; the numbering only changes where labels and rows sit in memory
+// (hub rows and the labels of hub neighbours become contiguous and cache-resident).
+struct SweepView {
+    LevelGraph V;                 // n, ue, uptr, unbr (view ids), uu32, s_out / s2, bins, hubs
+    DBuf<int32_t> order;          // view row k -> node
+    DBuf<int32_t> vlabel, vcstar; // per sweep: labels and targets in view order
+};
+SweepView &ensure_sweep_view(slm_ctx *ctx, const LevelGraph &G);
+void build_bins(slm_ctx *ctx, LevelGraph &G);
 
 // Assignment forest + derived community structure (forest.py:23-67, quality.py:52-79).
 struct Forest {

@@ -1467,14 +1467,14 @@ static void set_smem(K kern, size_t bytes) {
 }
 
 template <bool SYM>
-static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_t *d_cstar,
-                         int bin_mask, unsigned long long *d_groups) {
+static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, const int32_t *label,
+                         double m, int32_t *d_cstar, int bin_mask, unsigned long long *d_groups) {
     cudaStream_t s = ctx->stream;
     SweepArgs<SYM> A;
     A.uptr = G.uptr.p;
     A.unbr = G.unbr.p;
     A.u32 = G.uu32.p;
-    A.label = F.comm.p;
+    A.label = label;
     A.S1 = F.S_out.p;
     A.S2 = F.S2.p;
     A.S1f = F.S1f.p;
@@ -1644,12 +1644,43 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
     }
 }
 
+__global__ void k_view_labels(const int32_t *label, const int32_t *order, int64_t n,
+                              int32_t *vlabel, int32_t *vcstar) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t l = label[order[k]];
+        vlabel[k] = l;
+        if (vcstar) vcstar[k] = l;   // rows without entries keep their label
+    }
+}
+__global__ void k_view_scatter(const int32_t *vcstar, const int32_t *order, int64_t n,
+                               int32_t *cstar) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x)
+        cstar[order[k]] = vcstar[k];
+}
+
+// The integer sweep runs over the degree-ordered view of the level (SweepView): labels are
+// gathered into view order, the bin kernels write targets in view order, and the targets are
+// scattered back (two n-sized passes).  SLM_VIEW=0 sweeps the level graph directly.
 void run_plan_u32(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_t *d_cstar,
                   int bin_mask, unsigned long long *d_groups) {
-    if (bin_mask & 64)
-        k_copy_labels32<<<grid_for(G.n, 256), 256, 0, ctx->stream>>>(F.comm.p, G.n, d_cstar);
-    if (G.sym) launch_sweep<true>(ctx, G, F, m, d_cstar, bin_mask, d_groups);
-    else launch_sweep<false>(ctx, G, F, m, d_cstar, bin_mask, d_groups);
+    static const bool no_view = getenv("SLM_VIEW") && atoi(getenv("SLM_VIEW")) == 0;
+    cudaStream_t s = ctx->stream;
+    if (no_view) {
+        if (bin_mask & 64)
+            k_copy_labels32<<<grid_for(G.n, 256), 256, 0, s>>>(F.comm.p, G.n, d_cstar);
+        if (G.sym) launch_sweep<true>(ctx, G, F, F.comm.p, m, d_cstar, bin_mask, d_groups);
+        else launch_sweep<false>(ctx, G, F, F.comm.p, m, d_cstar, bin_mask, d_groups);
+        return;
+    }
+    SweepView &W = ensure_sweep_view(ctx, G);
+    const LevelGraph &V = W.V;
+    k_view_labels<<<grid_for(G.n, 256), 256, 0, s>>>(F.comm.p, W.order.p, G.n, W.vlabel.p,
+                                                     (bin_mask & 64) ? W.vcstar.p : nullptr);
+    if (V.sym) launch_sweep<true>(ctx, V, F, W.vlabel.p, m, W.vcstar.p, bin_mask, d_groups);
+    else launch_sweep<false>(ctx, V, F, W.vlabel.p, m, W.vcstar.p, bin_mask, d_groups);
+    k_view_scatter<<<grid_for(G.n, 256), 256, 0, s>>>(W.vcstar.p, W.order.p, G.n, d_cstar);
 }
 
 // ---------------------------------------------------------------- diagnostics
@@ -1690,10 +1721,22 @@ double sweep_floor_ms(slm_ctx *ctx, const LevelGraph &G, Forest &F, int mode) {
     cudaEventCreate(&b);
     DBuf<unsigned long long> o;
     o.resize(1);
-    k_floor<<<148 * 8, 256, 0, ctx->stream>>>(G.unbr.p, G.uu32.p, F.comm.p, F.S1f.p, G.ue, mode, o.p);
+    // modes 3-5: modes 0-2 over the degree-ordered view (labels gathered into view order)
+    const int32_t *nbr = G.unbr.p, *lab = F.comm.p;
+    const uint32_t *u32 = G.uu32.p;
+    if (mode >= 3) {
+        SweepView &W = ensure_sweep_view(ctx, G);
+        k_view_labels<<<grid_for(G.n, 256), 256, 0, ctx->stream>>>(F.comm.p, W.order.p, G.n,
+                                                                     W.vlabel.p, nullptr);
+        nbr = W.V.unbr.p;
+        u32 = W.V.uu32.p;
+        lab = W.vlabel.p;
+        mode -= 3;
+    }
+    k_floor<<<148 * 8, 256, 0, ctx->stream>>>(nbr, u32, lab, F.S1f.p, G.ue, mode, o.p);
     cudaEventRecord(a, ctx->stream);
     for (int it = 0; it < 5; it++)
-        k_floor<<<148 * 8, 256, 0, ctx->stream>>>(G.unbr.p, G.uu32.p, F.comm.p, F.S1f.p, G.ue, mode, o.p);
+        k_floor<<<148 * 8, 256, 0, ctx->stream>>>(nbr, u32, lab, F.S1f.p, G.ue, mode, o.p);
     cudaEventRecord(b, ctx->stream);
     cudaEventSynchronize(b);
     float ms = 0;

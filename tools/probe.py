@@ -59,7 +59,7 @@ def main():
     for mask, name in ((127, "sweep"), (1, "b0"), (2, "b1"), (4, "b2"), (8, "b3"), (16, "b4"), (32, "b5"), (64, "copy")):
         ms = ev_time(ctx, lambda: ctx.plan_async(mask))
         print(f"plan[{name}] ms {ms:.3f}  GTEPS(full E) {info['ue'] / ms / 1e6:.1f}")
-    for mode in (0, 1, 2):
+    for mode in (0, 1, 2, 3, 4, 5):
         print("floor mode", mode, "ms", round(ctx.sweep_floor(mode), 3))
     if a.no_maximal:
         return
