@@ -258,41 +258,53 @@ __global__ void __launch_bounds__(256) k_sweep_small(SweepArgs<SYM> A, const int
                 if (lane == 0 && lm) atomicAdd(A.groups, (unsigned long long)__popc(lm));
             }
             const bool own = (c == Lr);
-            double bt = -INFINITY;
-            int32_t bc = 0x7fffffff;
-            // the own group's leader publishes the staying score for its row slot
-            const unsigned om = __ballot_sync(0xffffffffu, leader && own);
-            double ts = 0.0;
-            if (leader) {
-                const double2 srr = node_s(A, rr);
-                const double t = exact_t(gs, null_P(own, srr, comm_S(A, c)), A.m, A.m2);
-                if (own) {
-                    ts = t;
-                } else {
-                    bt = t;
-                    bc = c;
-                }
-            }
-            // segmented inclusive max over the lanes of one row (rst = the row's first lane)
+            // the row occupies lanes [rst, rlast]
+            const int rdeg = __shfl_sync(0xffffffffu, deg, s);
+            const int rlast = rst + rdeg - 1;
+            const unsigned rowbits = (rlast >= 31 ? 0xffffffffu : ((2u << rlast) - 1u)) &
+                                     ~((1u << rst) - 1u);
+            const double2 srr = node_s(A, rr);
+            const float2 srf = make_float2((float)srr.x, (float)srr.y);
+            // fp32 bound filter per group (as the table kernels): row max of the lower bounds
+            float up = -INFINITY, lo = -INFINITY;
+            if (leader && !own) up = approx_up(gs, comm_Sf(A, c), srf, A.inv_mf, A.inv_m2f, lo);
+            float lom = lo;
 #pragma unroll
             for (int off = 1; off < 32; off <<= 1) {
-                const double obt = __shfl_up_sync(0xffffffffu, bt, off);
-                const int32_t obc = __shfl_up_sync(0xffffffffu, bc, off);
-                if (lane - off >= rst && better2(obt, obc, bt, bc)) {
-                    bt = obt;
-                    bc = obc;
-                }
+                const float o = __shfl_up_sync(0xffffffffu, lom, off);
+                if (lane - off >= rst) lom = fmaxf(lom, o);
             }
-            const int nxt = __shfl_down_sync(0xffffffffu, s, 1);
-            const bool last = valid && (lane == total - 1 || nxt != s);
-            // the row's own-group leader (if any) lies in [rst, lane]
-            const unsigned rowmask = (lane == 31 ? 0xffffffffu : ((2u << lane) - 1u)) & ~((1u << rst) - 1u);
-            const unsigned ol = om & rowmask;
-            const double tso = __shfl_sync(0xffffffffu, ts, ol ? __ffs(ol) - 1 : lane);
-            if (last) {
-                const double t_stay =
-                    ol ? tso : stay_default(node_s(A, rr), comm_S(A, Lr), A.m2);
-                A.cstar[rr] = (bc != 0x7fffffff && bt > t_stay) ? bc : Lr;
+            const float LO = __shfl_sync(0xffffffffu, lom, rlast & 31);
+            const bool cand = leader && !own && up >= LO;
+            const unsigned cm = __ballot_sync(0xffffffffu, cand);
+            const unsigned om = __ballot_sync(0xffffffffu, leader && own);
+            const unsigned ol = om & rowbits;
+            const uint32_t gown = __shfl_sync(0xffffffffu, gs, ol ? __ffs(ol) - 1 : lane);
+            const int ncand = __popc(cm & rowbits);
+            if (valid && LO == -INFINITY) {
+                if (lane == rlast) A.cstar[rr] = Lr;
+            } else if (valid && ncand == 1) {
+                if (cand) A.cstar[rr] = decide_fast(A, gs, c, LO, up, ol != 0, gown, srr, srf, Lr);
+            }
+            // rows the filter cannot settle: exact scores of their candidates, segmented argmax
+            const bool slow = valid && LO != -INFINITY && ncand > 1;
+            if (__any_sync(0xffffffffu, slow)) {
+                double bt = -INFINITY;
+                int32_t bc = 0x7fffffff;
+                if (slow && cand) {
+                    bt = exact_t(gs, null_P(false, srr, comm_S(A, c)), A.m, A.m2);
+                    bc = c;
+                }
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const double obt = __shfl_up_sync(0xffffffffu, bt, off);
+                    const int32_t obc = __shfl_up_sync(0xffffffffu, bc, off);
+                    if (lane - off >= rst && better2(obt, obc, bt, bc)) {
+                        bt = obt;
+                        bc = obc;
+                    }
+                }
+                if (slow && lane == rlast) A.cstar[rr] = decide(A, bt, bc, ol != 0, gown, srr, Lr);
             }
             rcur += k;
         }
