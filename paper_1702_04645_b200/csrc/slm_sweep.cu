@@ -693,14 +693,20 @@ __global__ void __launch_bounds__(WARPS * 32, 4) k_sweep_warp(SweepArgs<SYM> A, 
     __syncwarp();
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    // row metadata is fetched one row ahead
+    // software pipeline: the next row's metadata is fetched one row ahead, its first chunk
+    // of entries during this row's selection (labels gathered before the clear)
+    constexpr int U = 4;
     int32_t nr = 0;
     int64_t ne0 = 0, nd = 0;
+    int32_t zc[U];
+    uint32_t zw[U];
     if (w < nrows) {
         nr = rows[w];
         ne0 = A.uptr[nr];
         nd = A.uptr[nr + 1] - ne0;
     }
+    load_raw<U, 32>(A.unbr + ne0, A.u32 + ne0, (uint32_t)nd, lane, zc, zw);
+    gather_labels<U>(A.label, zc, zc);
     for (int64_t i = w; i < nrows; i += nw) {
         const int32_t r = nr;
         const int64_t e0 = ne0, d = nd;
@@ -708,21 +714,24 @@ __global__ void __launch_bounds__(WARPS * 32, 4) k_sweep_warp(SweepArgs<SYM> A, 
             nr = rows[i + nw];
             ne0 = A.uptr[nr];
             nd = A.uptr[nr + 1] - ne0;
+        } else {
+            nd = 0;
         }
         const uint32_t H = min(tab_size(d, 2, 32), (uint32_t)HMAX);   // > d either way
         const int32_t L = A.label[r];
         const double2 sr = node_s(A, r);
         const float2 srf = make_float2((float)sr.x, (float)sr.y);
         uint32_t no = 0;
-        constexpr int U = 4;
         const int32_t *nb = A.unbr + e0;
         const uint32_t *ub = A.u32 + e0;
-        for (uint32_t cb = 0; cb < (uint32_t)d; cb += 32 * U) {
+        insert_chunk<U, false>(tsa, H - 1, zc, zw, osa, (uint32_t *)nullptr, no, (int *)nullptr);
+        for (uint32_t cb = 32 * U; cb < (uint32_t)d; cb += 32 * U) {
             int32_t c[U];
             uint32_t wt[U];
             load_row<U, 32>(nb, ub, A.label, (uint32_t)d, cb + lane, c, wt);
             insert_chunk<U, false>(tsa, H - 1, c, wt, osa, (uint32_t *)nullptr, no, (int *)nullptr);
         }
+        load_raw<U, 32>(A.unbr + ne0, A.u32 + ne0, (uint32_t)nd, lane, zc, zw);
         __syncwarp();
         Sel S;
         sel_init(S);
@@ -752,6 +761,7 @@ __global__ void __launch_bounds__(WARPS * 32, 4) k_sweep_warp(SweepArgs<SYM> A, 
                 if (lane == 0) A.cstar[r] = decide(A, bt, bc, ob != 0, gown, sr, L);
             }
         }
+        gather_labels<U>(A.label, zc, zc);   // next row's first chunk
         occ_clear<false>(T, occ, no, lane, 32);
         __syncwarp();
     }
@@ -885,17 +895,15 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_sweep_cta(SweepArgs<SYM> A, con
     int32_t z[U];
     uint32_t wt[U];
     load_raw<U, BLOCK>(A.unbr + cur.e0, A.u32 + cur.e0, cur.d, threadIdx.x, z, wt);
+    gather_labels<U>(A.label, z, z);
     for (int64_t i = blockIdx.x; i < nrows; i += step) {
         const double2 sr = node_s(A, cur.r);
         const uint32_t H = min(tab_size(cur.d, F, 32), (uint32_t)HMAX);
         const int32_t *nb = A.unbr + cur.e0;
         const uint32_t *ub = A.u32 + cur.e0;
         uint32_t unused = 0;
-        {
-            int32_t c[U];
-            gather_labels<U>(A.label, z, c);
-            insert_chunk<U, true>(tsa, H - 1, c, wt, osa, &s_no, unused, &s_ovf);
-        }
+        // z holds the first chunk's communities (gathered at the end of the previous row)
+        insert_chunk<U, true>(tsa, H - 1, z, wt, osa, &s_no, unused, &s_ovf);
         for (uint32_t cb = BLOCK * U; cb < cur.d; cb += BLOCK * U) {
             int32_t c[U];
             uint32_t w2[U];
@@ -913,6 +921,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_sweep_cta(SweepArgs<SYM> A, con
         } else {
             block_select<BLOCK, SYM, false>(A, ctab, occ, no, cur.r, cur.L, sr, B);
         }
+        gather_labels<U>(A.label, z, z);   // next row's first chunk: its latency overlaps the clear
         occ_clear<false>(ctab, occ, no, threadIdx.x, BLOCK);
         __syncthreads();
         if (threadIdx.x == 0) {   // every thread read s_no / s_ovf before the barriers above
