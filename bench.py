@@ -249,8 +249,12 @@ def main():
 
     groups, bin_rows, bin_entries = ctx.plan_groups()
     stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=local)
-    bins_used = int((bin_rows > 0).sum())
-    launches_per_sweep = 1 + bins_used
+    # kernels per sweep (library launch sequence, slm_sweep.cu run_plan_u32): view labels in,
+    # bin 0 (lane-per-row + packed), bin 1, bins 2-4 (+ their overflow pass), bin 5 (shared-
+    # table rows, global merge + select, fallback), targets out
+    mid = int((bin_rows[2:5] > 0).sum())
+    launches_per_sweep = (2 + 2 * int(bin_rows[0] > 0) + int(bin_rows[1] > 0) + mid
+                          + int(mid > 0) + 4 * int(bin_rows[5] > 0))
 
     def timed(mask, iters):
         a = torch.cuda.Event(enable_timing=True)
@@ -288,10 +292,10 @@ def main():
 
     # per-bin device times (explanation only)
     per_bin = {}
-    for mask, name in ((1, "bin0_packed_warp"), (2, "bin1_warp_hash512"),
-                       (4, "bin2_warp_hash2048"), (8, "bin3_cta_hash8192"),
-                       (16, "bin4_cta_hash16384"), (32, "bin5_cta_global_hash"),
-                       (64, "label_copy")):
+    for mask, name in ((1, "bin0_lane_per_row_and_packed"), (2, "bin1_warp_hash512"),
+                       (4, "bin2_cta128_hash2048"), (8, "bin3_cta256_hash2048"),
+                       (16, "bin4_cta512_hash8192"), (32, "bin5_hub_smem_or_global"),
+                       (64, "view_labels_in_targets_out")):
         if mask < 64 and bin_rows[mask.bit_length() - 1] == 0:
             continue
         per_bin[name] = round(timed(mask, max(3, args.steps // 4)) / max(3, args.steps // 4), 4)

@@ -13,7 +13,7 @@ ncu --profile-from-start off --clock-control none --csv \
 echo LAUNCH $?
 if [ "$2" = "full" ]; then
   ncu --set full --clock-control none --import-source on --profile-from-start off \
-      -k regex:"k_sweep" -c 9 -o gpurun_out/prof_sweep_$TAG \
+      -k regex:"k_sweep|k_view" -c 16 -o gpurun_out/prof_sweep_$TAG \
       python bench.py --steps 1 --warmup 3 --no-cpu --no-partition > gpurun_out/ncu_full_$TAG.log 2>&1
   echo FULL $?
 fi
