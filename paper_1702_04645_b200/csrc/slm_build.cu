@@ -737,9 +737,137 @@ __global__ void k_view_gather(const T *src, const int32_t *order, int64_t n, T *
         dst[k] = src[order[k]];
 }
 
+// Bins of the view without flags or host passes: the view's degrees are non-increasing, so
+// every degree bin (and bin 0's d <= TINY_MAX tail) is a contiguous range of view rows.
+// bound[b] (b = 0..NBINS-1) = first row whose bin is below b (n if none); bound[NBINS] =
+// first row of degree <= TINY_MAX.
+__device__ __forceinline__ int view_bin(int64_t d) {
+    if (d <= 0) return -1;
+    int b = 0;
+    while (d > bin_hi(b)) b++;
+    return b;
+}
+__global__ void k_view_bounds(const int64_t *vptr, int64_t n, int64_t *bound) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t d = vptr[k + 1] - vptr[k];
+        const int64_t dp = k ? vptr[k] - vptr[k - 1] : INT64_MAX;
+        const int bk = view_bin(d), bp = k ? view_bin(dp) : NBINS;
+        for (int b = bk + 1; b <= bp && b < NBINS; b++) bound[b] = k;
+        if (d <= TINY_MAX && dp > TINY_MAX) bound[NBINS] = k;
+    }
+}
+// rows[off + i] = start + i over up to 8 segments {off, start, len}
+__global__ void k_view_fill_rows(const int64_t *seg, int nseg, int32_t *rows) {
+    for (int q = 0; q < nseg; q++) {
+        const int64_t off = seg[3 * q], st = seg[3 * q + 1], len = seg[3 * q + 2];
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
+             i += (int64_t)gridDim.x * blockDim.x)
+            rows[off + i] = (int32_t)(st + i);
+    }
+}
+
+static void build_bins_view(slm_ctx *ctx, LevelGraph &V) {
+    const int64_t n = V.n;
+    cudaStream_t s = ctx->stream;
+    int64_t *d_b = ctx->view_bound.resize(NBINS + 1 + 3 * 8);
+    std::vector<int64_t> hb(NBINS + 1, n);
+    CUDA_TRY(cudaMemcpyAsync(d_b, hb.data(), (NBINS + 1) * 8, cudaMemcpyHostToDevice, s));
+    if (n) k_view_bounds<<<grid_for(n, 256), 256, 0, s>>>(V.uptr.p, n, d_b);
+    CUDA_TRY(cudaMemcpyAsync(hb.data(), d_b, (NBINS + 1) * 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    // bin b = view rows [lo(b), hi(b)): hi(b) = bound[b], lo(b) = bound[b + 1] (lo(5) = 0)
+    auto lo = [&](int b) { return b == NBINS - 1 ? (int64_t)0 : hb[b + 1]; };
+    auto hi = [&](int b) { return hb[b]; };
+    // uptr at the boundaries
+    std::vector<int64_t> cut;
+    for (int b = 0; b < NBINS; b++) {
+        cut.push_back(lo(b));
+        cut.push_back(hi(b));
+    }
+    std::vector<int64_t> upc(cut.size());
+    for (size_t q = 0; q < cut.size(); q++)
+        CUDA_TRY(cudaMemcpyAsync(&upc[q], V.uptr.p + cut[q], 8, cudaMemcpyDeviceToHost, s));
+    const int64_t t0 = std::max(lo(0), std::min(hi(0), hb[NBINS]));   // first tiny row of bin 0
+    std::vector<int64_t> seg;
+    int64_t off = 0;
+    V.bin_rows.resize(n > 0 ? n : 1);
+    for (int b = 0; b < NBINS; b++) {
+        V.bin_off[b] = off;
+        if (b == 0) {
+            seg.insert(seg.end(), {off, t0, hi(0) - t0});   // d <= TINY_MAX first
+            seg.insert(seg.end(), {off + hi(0) - t0, lo(0), t0 - lo(0)});
+            V.bin0_tiny = hi(0) - t0;
+        } else {
+            seg.insert(seg.end(), {off, lo(b), hi(b) - lo(b)});
+        }
+        off += hi(b) - lo(b);
+    }
+    V.bin_off[NBINS] = off;
+    CUDA_TRY(cudaMemcpyAsync(d_b + NBINS + 1, seg.data(), seg.size() * 8, cudaMemcpyHostToDevice, s));
+    if (off) k_view_fill_rows<<<grid_for(off, 256), 256, 0, s>>>(d_b + NBINS + 1, (int)seg.size() / 3,
+                                                                 V.bin_rows.p);
+    CUDA_TRY(cudaStreamSynchronize(s));
+    for (int b = 0; b < NBINS; b++) V.bin_entries[b] = upc[2 * b + 1] - upc[2 * b];
+    V.max_deg = 0;
+    if (n) {
+        int64_t u01[2];
+        CUDA_TRY(cudaMemcpy(u01, V.uptr.p, 16, cudaMemcpyDeviceToHost));
+        V.max_deg = (int32_t)std::min<int64_t>(u01[1] - u01[0], 0x7fffffff);
+    }
+    V.large_hash_total = 0;   // the generic fp64 path never runs on a view
+    // hub rows (bin 5) = view rows [0, nh), already in descending degree: j = row
+    const int64_t nh = hi(NBINS - 1) - lo(NBINS - 1);
+    V.hub_rows_n = nh;
+    V.hub_nseg = 0;
+    V.hub_ring = 0;
+    V.hub_big_rows = 0;
+    V.hub_big_items = 0;
+    if (nh) {
+        std::vector<int64_t> up(nh + 1);
+        CUDA_TRY(cudaMemcpy(up.data(), V.uptr.p, (nh + 1) * 8, cudaMemcpyDeviceToHost));
+        std::vector<int64_t> hub(nh), segs, hoffr(nh), hsz(nh);
+        int64_t cur = 0;
+        for (int64_t j = 0; j < nh; j++) {
+            hub[j] = j;
+            const int64_t d = up[j + 1] - up[j];
+            int64_t H = 64;
+            while (H <= d) H <<= 1;
+            hoffr[j] = cur;
+            hsz[j] = H;
+            cur += H;
+            for (int64_t q = 0; q * HUB_SEG < d; q++) segs.push_back((j << 20) | q);
+            if (d > HUB_BIG_DEG && V.hub_big_rows == j) {
+                V.hub_big_rows++;
+                V.hub_big_items += (d + HUB_SEG - 1) / HUB_SEG;
+            }
+        }
+        V.hub_ring = cur;
+        V.hub_nseg = (int64_t)segs.size();
+        V.hub_seg.resize(segs.size());
+        V.hub_row.resize(nh);
+        V.hub_off.resize(nh);
+        V.hub_size.resize(nh);
+        CUDA_TRY(cudaMemcpyAsync(V.hub_seg.p, segs.data(), segs.size() * 8, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(V.hub_row.p, hub.data(), nh * 8, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(V.hub_off.p, hoffr.data(), nh * 8, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(V.hub_size.p, hsz.data(), nh * 8, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+    }
+}
+
 SweepView &ensure_sweep_view(slm_ctx *ctx, const LevelGraph &G) {
     if (G.view) return *G.view;
     cudaStream_t s = ctx->stream;
+    static const bool verbose = getenv("SLM_VIEW_VERBOSE") != nullptr;
+    double tv = now_ms();
+    auto vmark = [&](const char *what) {
+        if (!verbose) return;
+        cudaStreamSynchronize(s);
+        const double t = now_ms();
+        fprintf(stderr, "[view] %s %.1f ms\n", what, t - tv);
+        tv = t;
+    };
     auto W = std::make_shared<SweepView>();
     LevelGraph &V = W->V;
     const int64_t n = G.n, ue = G.ue;
@@ -754,15 +882,17 @@ SweepView &ensure_sweep_view(slm_ctx *ctx, const LevelGraph &G) {
     W->vlabel.resize(n);
     W->vcstar.resize(n);
     {
-        DBuf<uint32_t> k0, k1;
-        DBuf<int32_t> i0, nid;
+        DBuf<uint32_t> &k0 = ctx->view_k0, &k1 = ctx->view_k1;
+        DBuf<int32_t> &i0 = ctx->view_i0, &nid = ctx->view_nid;
         k0.resize(n);
         k1.resize(n);
         i0.resize(n);
         nid.resize(n);
         k_view_keys<<<grid_for(n, 256), 256, 0, s>>>(G.uptr.p, n, k0.p, i0.p);
+        vmark("alloc+keys");
         sort_pairs_u32_i32(ctx, k0.p, k1.p, i0.p, W->order.p, n, 32);   // stable (LSD)
-        DBuf<int64_t> vdeg;
+        vmark("sort");
+        DBuf<int64_t> &vdeg = ctx->view_deg;
         vdeg.resize(n + 1);
         CUDA_TRY(cudaMemsetAsync(vdeg.p + n, 0, 8, s));
         k_view_rows<<<grid_for(n, 256), 256, 0, s>>>(G.uptr.p, W->order.p, n, vdeg.p, nid.p);
@@ -773,6 +903,7 @@ SweepView &ensure_sweep_view(slm_ctx *ctx, const LevelGraph &G) {
         k_view_entries<<<grid_for(n * 32, 256), 256, 0, s>>>(G.uptr.p, G.unbr.p, G.uu32.p,
                                                                W->order.p, nid.p, n, V.uptr.p,
                                                                V.unbr.p, V.uu32.p);
+        vmark("entries");
     }
     V.s_out.resize(n);
     k_view_gather<double><<<grid_for(n, 256), 256, 0, s>>>(G.s_out.p, W->order.p, n, V.s_out.p);
@@ -781,7 +912,9 @@ SweepView &ensure_sweep_view(slm_ctx *ctx, const LevelGraph &G) {
         k_view_gather<double2><<<grid_for(n, 256), 256, 0, s>>>(G.s2.p, W->order.p, n, V.s2.p);
     }
     CUDA_TRY(cudaGetLastError());
-    build_bins(ctx, V);
+    vmark("strengths");
+    build_bins_view(ctx, V);
+    vmark("bins");
     G.view = W;
     return *W;
 }

@@ -190,6 +190,10 @@ struct slm_ctx {
     DBuf<uint32_t> ovf_cnt;      // [0] overflow rows, [1 + b] list length of overflow CTA b
     DBuf<int2> ovf_tab;          // per overflow CTA: global table (kept empty)
     DBuf<uint32_t> ovf_occ;
+    // sweep-view build scratch (grow-only, reused by every level)
+    DBuf<uint32_t> view_k0, view_k1;
+    DBuf<int32_t> view_i0, view_nid;
+    DBuf<int64_t> view_deg, view_bound;
     int32_t *h_flag = nullptr;   // pinned host scalars
     int64_t *h_i64 = nullptr;
     double *h_f64 = nullptr;
