@@ -918,3 +918,6 @@ SweepView &ensure_sweep_view(slm_ctx *ctx, const LevelGraph &G) {
     G.view = W;
     return *W;
 }
+
+// a kernel of this translation unit (module preloading, slm_capi.cu preload_modules)
+const void *slm_anchor_build() { return (const void *)k_validate; }

@@ -1,6 +1,7 @@
 // slm_capi.cu -- the extern "C" boundary (include/slm.h).  Every entry point catches
 // SlmError / CUDA failures, records the message in the context and returns a code.
 #include "slm_internal.cuh"
+#include <cuda.h>
 #include "../../include/slm.h"
 #include <cstring>
 
@@ -104,6 +105,44 @@ static void new_level0(slm_ctx *ctx) {
 
 extern "C" {
 
+// Load every kernel of the library now instead of at its first launch (default lazy module
+// loading: each first launch blocks the host for milliseconds).  Driver entry points: cuFuncGetModule,
+// cuModuleGetFunctionCount, cuModuleEnumerateFunctions, cuFuncLoad (CUDA 12.4+); when any is
+// unavailable the kernels simply keep loading lazily.
+static void preload_modules() {
+    typedef CUresult (*GetModule)(CUmodule *, CUfunction);
+    typedef CUresult (*Count)(unsigned int *, CUmodule);
+    typedef CUresult (*Enum)(CUfunction *, unsigned int, CUmodule);
+    typedef CUresult (*Load)(CUfunction);
+    void *p1 = nullptr, *p2 = nullptr, *p3 = nullptr, *p4 = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuFuncGetModule", &p1, cudaEnableDefault, &q) != cudaSuccess || !p1 ||
+        cudaGetDriverEntryPoint("cuModuleGetFunctionCount", &p2, cudaEnableDefault, &q) != cudaSuccess || !p2 ||
+        cudaGetDriverEntryPoint("cuModuleEnumerateFunctions", &p3, cudaEnableDefault, &q) != cudaSuccess || !p3 ||
+        cudaGetDriverEntryPoint("cuFuncLoad", &p4, cudaEnableDefault, &q) != cudaSuccess || !p4) {
+        cudaGetLastError();
+        return;
+    }
+    const void *anchors[] = {slm_anchor_build(), slm_anchor_capi(), slm_anchor_commit(),
+                             slm_anchor_forest(), slm_anchor_gen(), slm_anchor_level(),
+                             slm_anchor_lgains(), slm_anchor_plan(), slm_anchor_positive(),
+                             slm_anchor_sweep()};
+    for (const void *a : anchors) {
+        cudaFunction_t f;
+        CUmodule mod;
+        unsigned int cnt = 0;
+        if (cudaGetFuncBySymbol(&f, a) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        if (((GetModule)p1)(&mod, (CUfunction)f) != CUDA_SUCCESS) continue;
+        if (((Count)p2)(&cnt, mod) != CUDA_SUCCESS || cnt == 0) continue;
+        std::vector<CUfunction> fs(cnt);
+        if (((Enum)p3)(fs.data(), cnt, mod) != CUDA_SUCCESS) continue;
+        for (CUfunction g : fs) ((Load)p4)(g);
+    }
+}
+
 slm_ctx *slm_create(int device) {
     slm_ctx *ctx = new slm_ctx();
     ctx->device = device;
@@ -114,6 +153,14 @@ slm_ctx *slm_create(int device) {
         cudaGetLastError();
         delete ctx;
         return nullptr;
+    }
+    // profiling runs synchronise at every phase boundary, so a lazy first-launch load would
+    // be charged to the phase; preload there (and on request).  Otherwise the loads overlap
+    // the asynchronously queued device work and preloading every kernel costs more (~0.2 s).
+    static bool preloaded = false;
+    if (!preloaded && (ctx->prof || getenv("SLM_PRELOAD_MODULES"))) {
+        preload_modules();
+        preloaded = true;
     }
     return ctx;
 }
@@ -555,3 +602,6 @@ int slm_last_commit_stats(slm_ctx *ctx, int64_t *candidates, int64_t *rounds) {
 }
 
 }  // extern "C"
+
+// a kernel of this translation unit (module preloading, slm_capi.cu preload_modules)
+const void *slm_anchor_capi() { return (const void *)k_i64_to_i32; }

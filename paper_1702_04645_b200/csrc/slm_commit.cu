@@ -1128,3 +1128,6 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
         CUDA_TRY(cudaStreamSynchronize(s));
     }
 }
+
+// a kernel of this translation unit (module preloading, slm_capi.cu preload_modules)
+const void *slm_anchor_commit() { return (const void *)k_cand_flags; }

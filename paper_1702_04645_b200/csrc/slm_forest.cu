@@ -529,3 +529,6 @@ void forest_refresh(slm_ctx *ctx, const LevelGraph &G, Forest &F) {
     phase_mark(ctx, PH_REFRESH_LAYOUT);
     F.version++;
 }
+
+// a kernel of this translation unit (module preloading, slm_capi.cu preload_modules)
+const void *slm_anchor_forest() { return (const void *)k_cyc2; }

@@ -276,3 +276,6 @@ void gen_rgg_device(slm_ctx *ctx, int64_t n, double radius, uint64_t seed, DBuf<
                                                 src.p, dst.p, w.p);
     CUDA_TRY(cudaGetLastError());
 }
+
+// a kernel of this translation unit (module preloading, slm_capi.cu preload_modules)
+const void *slm_anchor_gen() { return (const void *)k_rmat_count; }

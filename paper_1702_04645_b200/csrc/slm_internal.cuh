@@ -342,3 +342,15 @@ void sort_pairs_u64_f64(slm_ctx *ctx, DBuf<uint64_t> &keys, DBuf<double> &vals, 
 void sort_pairs_u32_i32(slm_ctx *ctx, uint32_t *keys_in, uint32_t *keys_out, int32_t *vals_in,
                         int32_t *vals_out, int64_t n, int end_bit);
 int bits_for(int64_t v);
+
+// one kernel per translation unit: their modules are loaded at context creation
+const void *slm_anchor_build();
+const void *slm_anchor_capi();
+const void *slm_anchor_commit();
+const void *slm_anchor_forest();
+const void *slm_anchor_gen();
+const void *slm_anchor_level();
+const void *slm_anchor_lgains();
+const void *slm_anchor_plan();
+const void *slm_anchor_positive();
+const void *slm_anchor_sweep();

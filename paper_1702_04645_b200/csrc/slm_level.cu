@@ -145,3 +145,6 @@ double run_score(slm_ctx *ctx, const LevelGraph &G, const int32_t *d_labels, dou
     double null = device_pairwise_sum(ctx, terms.p, nc);
     return (intra - gamma * null) / m;
 }
+
+// a kernel of this translation unit (module preloading, slm_capi.cu preload_modules)
+const void *slm_anchor_level() { return (const void *)k_coarse_keys; }

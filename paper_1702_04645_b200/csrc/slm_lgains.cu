@@ -194,3 +194,6 @@ void run_local_gains_u32(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
     if (G.n) k_lg_empty<<<grid_for(G.n, 256), 256, 0, s>>>(A, G.n);
     CUDA_TRY(cudaGetLastError());
 }
+
+// a kernel of this translation unit (module preloading, slm_capi.cu preload_modules)
+const void *slm_anchor_lgains() { return (const void *)k_lg_small; }

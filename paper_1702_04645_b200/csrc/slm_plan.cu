@@ -358,3 +358,6 @@ void run_local_gains(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, dou
         d_lg, d_bad);
     CUDA_TRY(cudaGetLastError());
 }
+
+// a kernel of this translation unit (module preloading, slm_capi.cu preload_modules)
+const void *slm_anchor_plan() { return (const void *)k_assign; }

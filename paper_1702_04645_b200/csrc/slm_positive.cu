@@ -1760,3 +1760,6 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
         }
     }
 }
+
+// a kernel of this translation unit (module preloading, slm_capi.cu preload_modules)
+const void *slm_anchor_positive() { return (const void *)k_positive; }

@@ -1766,3 +1766,6 @@ double sweep_floor_ms(slm_ctx *ctx, const LevelGraph &G, Forest &F, int mode) {
     cudaEventDestroy(b);
     return ms / 5;
 }
+
+// a kernel of this translation unit (module preloading, slm_capi.cu preload_modules)
+const void *slm_anchor_sweep() { return (const void *)k_copy_labels32; }
