@@ -122,6 +122,10 @@ struct LevelGraph {
     int32_t max_deg = 0;
     // degree-ordered copy of the union for the integer plan sweep (built on first use)
     mutable std::shared_ptr<SweepView> view;
+    // nodes whose union rows exceed the POSITIVE warp executor's budget (found on first use)
+    mutable DBuf<int32_t> heavy_nodes;
+    mutable int64_t heavy_n = 0;
+    mutable bool heavy_valid = false;
 };
 
 // The integer plan sweep's view of a level: union rows renumbered by descending degree

@@ -456,6 +456,21 @@ __global__ void k_init_i32(int32_t *x, int64_t n, int32_t v) { GS_LOOP(i, n) x[i
 __global__ void k_bad_ranges(const int32_t *list, int64_t nbad, const int32_t *cptr, int2 *out) {
     GS_LOOP(i, nbad) out[i] = make_int2(cptr[list[i]], cptr[list[i] + 1]);
 }
+// members whose rows exceed HEAVY_DEG entries mark their community "heavy": a warp rescans
+// every member row at each split, so such parts go to the CTA executor instead
+constexpr int64_t HEAVY_DEG = 1 << 16;
+__global__ void k_heavy_flags(const int64_t *uptr, int64_t n, int32_t *f) {
+    GS_LOOP(i, n) f[i] = uptr[i + 1] - uptr[i] > HEAVY_DEG ? 1 : 0;
+}
+__global__ void k_heavy_scatter(const int32_t *f, const int32_t *pos, int64_t n, int32_t *out) {
+    GS_LOOP(i, n) if (f[i]) out[pos[i]] = (int32_t)i;
+}
+__global__ void k_heavy_mark(const int32_t *nodes, int64_t k, const int32_t *comm, uint8_t *heavy) {
+    GS_LOOP(i, k) heavy[comm[nodes[i]]] = 1;
+}
+__global__ void k_bad_heavy(const int32_t *list, int64_t nbad, const uint8_t *heavy, uint8_t *out) {
+    GS_LOOP(i, nbad) out[i] = heavy[list[i]];
+}
 
 // ---- batched init of every part of a giant wave.  Parts are slices [lo, hi) of the layout
 // (members: gmark == pid); their concatenation is indexed by a flat index t.  Member rows are
@@ -1294,11 +1309,39 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     // bad community ids and their layout ranges (only those: cptr itself stays on the device)
     std::vector<int32_t> hbad(nbad);
     std::vector<int2> hrng(nbad);
+    std::vector<uint8_t> hheavy(nbad, 0);
     {
         static DBuf<int2> drng;
         drng.resize(nbad);
         k_bad_ranges<<<grid_for(nbad, 256), 256, 0, s>>>(list.p, nbad, F.cptr.p, drng.p);
         CUDA_TRY(cudaMemcpyAsync(hrng.data(), drng.p, nbad * 8, cudaMemcpyDeviceToHost, s));
+        // heavy nodes of this level (found once per level graph)
+        if (!G.heavy_valid) {
+            DBuf<int32_t> hf, hp;
+            hf.resize(n + 1);
+            hp.resize(n + 1);
+            CUDA_TRY(cudaMemsetAsync(hf.p + n, 0, 4, s));
+            k_heavy_flags<<<grid_for(n, 256), 256, 0, s>>>(G.uptr.p, n, hf.p);
+            cub_exclusive_sum<int32_t>(ctx, hf.p, hp.p, n + 1);
+            int32_t nh = 0;
+            CUDA_TRY(cudaMemcpyAsync(&nh, hp.p + n, 4, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            G.heavy_nodes.resize(nh > 0 ? nh : 1);
+            if (nh) k_heavy_scatter<<<grid_for(n, 256), 256, 0, s>>>(hf.p, hp.p, n, G.heavy_nodes.p);
+            G.heavy_n = nh;
+            G.heavy_valid = true;
+            CUDA_TRY(cudaStreamSynchronize(s));
+        }
+        if (G.heavy_n) {
+            static DBuf<uint8_t> hc, hb;
+            hc.resize(nc);
+            hb.resize(nbad);
+            CUDA_TRY(cudaMemsetAsync(hc.p, 0, nc, s));
+            k_heavy_mark<<<grid_for(G.heavy_n, 256), 256, 0, s>>>(G.heavy_nodes.p, G.heavy_n,
+                                                                  F.comm.p, hc.p);
+            k_bad_heavy<<<grid_for(nbad, 256), 256, 0, s>>>(list.p, nbad, hc.p, hb.p);
+            CUDA_TRY(cudaMemcpyAsync(hheavy.data(), hb.p, nbad, cudaMemcpyDeviceToHost, s));
+        }
     }
     CUDA_TRY(cudaMemcpyAsync(hbad.data(), list.p, nbad * 4, cudaMemcpyDeviceToHost, s));
     if (g_stamp.p == nullptr) {
@@ -1353,9 +1396,12 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     std::vector<int64_t> order_kind(nbad);   // >=0: small1 index, <0: -(giant id)-1
     std::vector<int64_t> giant_of;
     std::vector<int32_t> giant_comm;   // bad-list indices of the giant communities
+    // a part goes to the warp executor when it is small and holds no heavy member (a warp
+    // rescans every member row at each split: coarse levels have hub members whose rows hold
+    // millions of entries, which the CTA executor processes cooperatively)
     for (int32_t i = 0; i < nbad; i++) {
         int32_t sz = hrng[i].y - hrng[i].x;
-        if (sz <= SMALL_PART) {
+        if (sz <= SMALL_PART && !hheavy[i]) {
             PartDesc d;
             d.off = hrng[i].x;
             d.len = sz;
