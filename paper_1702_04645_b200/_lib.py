@@ -307,7 +307,8 @@ class Context:
         self.call("slm_sync")
 
     PHASES = ("plan", "candidates", "spec", "walk", "components", "aggregates", "layout",
-              "positive_lg", "positive_small", "positive_giant", "assign", "aggregate")
+              "positive_lg", "positive_small", "positive_giant", "assign", "aggregate",
+              "alloc_ms", "alloc_calls")
 
     def phase_times(self, reset=False):
         ms = np.zeros(len(self.PHASES), np.float64)

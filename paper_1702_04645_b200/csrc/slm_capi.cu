@@ -4,6 +4,151 @@
 #include <cuda.h>
 #include "../../include/slm.h"
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <atomic>
+#include <unordered_map>
+#include <iterator>
+
+double dbuf_now_ms() { return now_ms(); }
+
+// ------------------------------------------------------------ device arena (DBuf)
+// cudaMalloc / cudaFree cost milliseconds each at this footprint and vary run to run (a level
+// loop makes hundreds of temporaries), so DBuf sub-allocates from one device arena reserved
+// when the first context of the process is created: best-fit free blocks indexed by size,
+// coalesced with their neighbours on release.  Requests the arena cannot hold fall back to
+// cudaMalloc.  SLM_ARENA_GB sets the arena size (default 75% of the free device memory;
+// 0 disables it).
+namespace {
+struct Arena {
+    char *base = nullptr;
+    size_t size = 0;
+    std::map<size_t, size_t> by_off;              // free blocks: offset -> length
+    std::multimap<size_t, size_t> by_len;         // free blocks: length -> offset
+    std::unordered_map<void *, size_t> live;      // arena allocations: pointer -> length
+};
+constexpr size_t ARENA_ALIGN = 512;
+constexpr int MAX_DEV = 64;
+}
+// heap objects never destroyed: static DBufs of other translation units release during exit
+static std::mutex &g_dc_mu = *new std::mutex;
+static Arena *g_arena = new Arena[MAX_DEV];
+
+static void arena_insert_free(Arena &A, size_t off, size_t len) {
+    auto nx = A.by_off.lower_bound(off);
+    if (nx != A.by_off.end() && off + len == nx->first) {   // merge with the next block
+        auto r = A.by_len.equal_range(nx->second);
+        for (auto it = r.first; it != r.second; ++it)
+            if (it->second == nx->first) { A.by_len.erase(it); break; }
+        len += nx->second;
+        nx = A.by_off.erase(nx);
+    }
+    if (nx != A.by_off.begin()) {                            // merge with the previous block
+        auto pv = std::prev(nx);
+        if (pv->first + pv->second == off) {
+            auto r = A.by_len.equal_range(pv->second);
+            for (auto it = r.first; it != r.second; ++it)
+                if (it->second == pv->first) { A.by_len.erase(it); break; }
+            off = pv->first;
+            len += pv->second;
+            A.by_off.erase(pv);
+        }
+    }
+    A.by_off.emplace(off, len);
+    A.by_len.emplace(len, off);
+}
+
+void dcache_reserve(int dev) {
+    std::lock_guard<std::mutex> lk(g_dc_mu);
+    Arena &A = g_arena[dev];
+    if (A.base) return;
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    size_t want = (size_t)(0.75 * (double)fr);
+    if (const char *e = getenv("SLM_ARENA_GB")) want = (size_t)(atof(e) * (double)(1ull << 30));
+    want &= ~(size_t)(ARENA_ALIGN - 1);
+    while (want >= (64ull << 20)) {
+        void *p = nullptr;
+        if (cudaMalloc(&p, want) == cudaSuccess) {
+            A.base = (char *)p;
+            A.size = want;
+            A.by_off.emplace(0, want);
+            A.by_len.emplace(want, 0);
+            return;
+        }
+        cudaGetLastError();
+        want /= 2;
+    }
+}
+
+void *dcache_alloc(size_t bytes, size_t *got) {
+    const size_t need = (bytes + ARENA_ALIGN - 1) / ARENA_ALIGN * ARENA_ALIGN;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lk(g_dc_mu);
+        Arena &A = g_arena[dev];
+        auto it = A.by_len.lower_bound(need);
+        if (it != A.by_len.end()) {
+            const size_t len = it->first, off = it->second;
+            A.by_len.erase(it);
+            A.by_off.erase(off);
+            if (len > need) {
+                A.by_off.emplace(off + need, len - need);
+                A.by_len.emplace(len - need, off + need);
+            }
+            void *p = A.base + off;
+            A.live.emplace(p, need);
+            *got = need;
+            return p;
+        }
+    }
+    const double t = now_ms();
+    void *p = nullptr;
+    cudaError_t e = cudaMalloc(&p, need);
+    g_alloc_ms += now_ms() - t;
+    g_alloc_calls++;
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *got = 0;
+        return nullptr;
+    }
+    *got = need;
+    return p;
+}
+static std::atomic<int> g_live_ctx{0};
+void dcache_free(void *p, size_t bytes) {
+    // Every kernel and copy of a context runs on its one stream, so a block released while
+    // queued work still uses it is only handed to later work of the same stream (ordered
+    // after it).  With several live contexts (several streams) the release waits for the
+    // device, as the cudaFree it replaces did.
+    if (g_live_ctx.load() > 1) {
+        const double t = now_ms();
+        cudaDeviceSynchronize();
+        g_alloc_ms += now_ms() - t;
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lk(g_dc_mu);
+        Arena &A = g_arena[dev];
+        auto it = A.live.find(p);
+        if (it != A.live.end()) {
+            const size_t len = it->second;
+            A.live.erase(it);
+            arena_insert_free(A, (size_t)((char *)p - A.base), len);
+            return;
+        }
+    }
+    (void)bytes;
+    const double t = now_ms();
+    cudaFree(p);
+    g_alloc_ms += now_ms() - t;
+    g_alloc_calls++;
+}
 
 void gen_rmat_device(slm_ctx *ctx, int scale, int edge_factor, double a, double b, double c,
                      uint64_t seed, int mode, DBuf<int32_t> &src, DBuf<int32_t> &dst,
@@ -157,6 +302,8 @@ slm_ctx *slm_create(int device) {
     // profiling runs synchronise at every phase boundary, so a lazy first-launch load would
     // be charged to the phase; preload there (and on request).  Otherwise the loads overlap
     // the asynchronously queued device work and preloading every kernel costs more (~0.2 s).
+    g_live_ctx++;
+    dcache_reserve(device);
     static bool preloaded = false;
     if (!preloaded && (ctx->prof || getenv("SLM_PRELOAD_MODULES"))) {
         preload_modules();
@@ -173,6 +320,7 @@ void slm_destroy(slm_ctx *ctx) {
     ctx->g0.reset();
     cudaStreamDestroy(ctx->stream);
     delete ctx;
+    g_live_ctx--;
 }
 
 const char *slm_last_error(slm_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
@@ -589,8 +737,15 @@ int slm_uniform01(slm_ctx *ctx, uint64_t seed, int64_t level, int64_t sweep, con
 int slm_phase_times(slm_ctx *ctx, double *ms, int32_t nmax, int32_t reset) {
     API_BEGIN
     for (int i = 0; i < NPHASE && i < nmax; i++) ms[i] = ctx->ph_ms[i];
-    if (reset)
+    // two extra slots: host ms spent in cudaMalloc / cudaFree and the number of such calls
+    // (process-wide)
+    if (nmax > NPHASE) ms[NPHASE] = g_alloc_ms;
+    if (nmax > NPHASE + 1) ms[NPHASE + 1] = (double)g_alloc_calls;
+    if (reset) {
         for (int i = 0; i < NPHASE; i++) ctx->ph_ms[i] = 0.0;
+        g_alloc_ms = 0.0;
+        g_alloc_calls = 0;
+    }
     API_END
 }
 

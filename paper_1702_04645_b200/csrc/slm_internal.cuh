@@ -39,6 +39,17 @@ struct SlmError {
 
 // ------------------------------------------------------------------ device buffers
 
+// host time spent in device allocation calls and their number (diagnostics, phase_times)
+inline double g_alloc_ms = 0.0;
+inline long long g_alloc_calls = 0;
+double dbuf_now_ms();
+
+// Device memory behind DBuf: a per-device arena reserved at context creation, sub-allocated
+// best-fit with coalescing (slm_capi.cu); cudaMalloc only beyond it.
+void *dcache_alloc(size_t bytes, size_t *got);
+void dcache_free(void *p, size_t bytes);
+void dcache_reserve(int device);
+
 template <class T>
 struct DBuf {
     T *p = nullptr;
@@ -49,7 +60,7 @@ struct DBuf {
     DBuf &operator=(const DBuf &) = delete;
     ~DBuf() { release(); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) dcache_free(p, cap * sizeof(T));
         p = nullptr;
         n = cap = 0;
     }
@@ -58,8 +69,10 @@ struct DBuf {
         if (cnt > cap) {
             release();
             size_t c = cnt ? cnt : 1;
-            CUDA_TRY(cudaMalloc(&p, c * sizeof(T)));
-            cap = c;
+            size_t got = 0;
+            p = (T *)dcache_alloc(c * sizeof(T), &got);
+            if (!p) CUDA_TRY(cudaErrorMemoryAllocation);
+            cap = got / sizeof(T);
         }
         n = cnt;
         return p;
