@@ -152,6 +152,7 @@ struct SweepView {
     DBuf<int32_t> vlabel, vcstar; // per sweep: labels and targets in view order
 };
 SweepView &ensure_sweep_view(slm_ctx *ctx, const LevelGraph &G);
+void view_gather_labels(slm_ctx *ctx, SweepView &W, const int32_t *label);   // vlabel = label[order]
 void build_bins(slm_ctx *ctx, LevelGraph &G);
 
 // Assignment forest + derived community structure (forest.py:23-67, quality.py:52-79).

@@ -20,13 +20,14 @@ struct LGArgs {
     double m;
     double *lg;
     uint8_t *bad;
+    const int32_t *order;   // rows of a sweep view: view row -> node (nullptr: rows are nodes)
 };
 
 __device__ __forceinline__ void lg_finish(const LGArgs &A, int32_t r, int32_t L, uint32_t own) {
     const double so = A.s_out[r], si = A.s_in[r];
     double g = (double)own / A.m - (so * (A.S_in[L] - si) + si * (A.S_out[L] - so)) / (A.m * A.m);
     if (A.m == 0.0) g = 0.0;
-    if (A.lg) A.lg[r] = g;
+    if (A.lg) A.lg[A.order ? A.order[r] : r] = g;
     if (g < 0.0) A.bad[L] = 1;
 }
 
@@ -165,21 +166,37 @@ __global__ void k_lg_empty(LGArgs A, int64_t n) {
         if (A.uptr[r + 1] == A.uptr[r]) lg_finish(A, (int32_t)r, A.label[r], 0u);
 }
 
-void run_local_gains_u32(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, double *d_lg,
+// Symmetric graphs run over the level's degree-ordered sweep view (slm_build.cu), whose
+// neighbour-label gathers stay in L2: labels are gathered into view order first and lg is
+// written back at the node (w_own is an exact integer sum, so the order is immaterial).
+void run_local_gains_u32(slm_ctx *ctx, const LevelGraph &G_, Forest &F, double m, double *d_lg,
                          uint8_t *d_bad) {
     cudaStream_t s = ctx->stream;
+    static const bool no_view = getenv("SLM_VIEW") && atoi(getenv("SLM_VIEW")) == 0;
+    const bool use_view = G_.sym && !no_view;
+    const LevelGraph *gp = &G_;
+    const int32_t *label = F.comm.p, *order = nullptr;
+    if (use_view) {
+        SweepView &W = ensure_sweep_view(ctx, G_);
+        view_gather_labels(ctx, W, F.comm.p);
+        gp = &W.V;
+        label = W.vlabel.p;
+        order = W.order.p;
+    }
+    const LevelGraph &G = *gp;
     LGArgs A;
     A.uptr = G.uptr.p;
     A.unbr = G.unbr.p;
     A.u32 = G.uu32.p;
-    A.label = F.comm.p;
+    A.label = label;
     A.S_out = F.S_out.p;
     A.S_in = F.S_in.p;
     A.s_out = G.s_out.p;
-    A.s_in = G.s_in.p;
+    A.s_in = use_view ? G.s_out.p : G.s_in.p;   // symmetric: s_in == s_out bitwise
     A.m = m;
     A.lg = d_lg;
     A.bad = d_bad;
+    A.order = order;
     auto nb = [&](int b0, int b1) { return G.bin_off[b1] - G.bin_off[b0]; };
     const int32_t *rows = G.bin_rows.p;
     if (nb(0, 1)) {

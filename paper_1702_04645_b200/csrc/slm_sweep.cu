@@ -1681,6 +1681,11 @@ __global__ void k_view_scatter(const int32_t *vcstar, const int32_t *order, int6
         cstar[order[k]] = vcstar[k];
 }
 
+void view_gather_labels(slm_ctx *ctx, SweepView &W, const int32_t *label) {
+    k_view_labels<<<grid_for(W.V.n, 256), 256, 0, ctx->stream>>>(label, W.order.p, W.V.n,
+                                                                 W.vlabel.p, nullptr);
+}
+
 // The integer sweep runs over the degree-ordered view of the level (SweepView): labels are
 // gathered into view order, the bin kernels write targets in view order, and the targets are
 // scattered back (two n-sized passes).  SLM_VIEW=0 sweeps the level graph directly.
