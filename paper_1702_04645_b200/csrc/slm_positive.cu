@@ -34,9 +34,14 @@
 // parts up to this size use the warp executor; SLM_SMALL_PART overrides it (tests force the
 // giant executor onto small graphs with it)
 static int SMALL_PART = 4096;
+// members whose union rows exceed HEAVY_DEG entries send their community to the CTA executor
+// (SLM_HEAVY_DEG overrides it; read with SLM_SMALL_PART at every call, cached per level graph)
+static int64_t HEAVY_DEG = 1 << 16;
 static void read_small_part() {
     const char *e = getenv("SLM_SMALL_PART");
     SMALL_PART = e ? std::max(1, atoi(e)) : 4096;
+    const char *h = getenv("SLM_HEAVY_DEG");
+    HEAVY_DEG = h ? std::max<int64_t>(1, atoll(h)) : (1 << 16);
 }
 
 #define GS_LOOP(i, n)                                                                      \
@@ -458,9 +463,8 @@ __global__ void k_bad_ranges(const int32_t *list, int64_t nbad, const int32_t *c
 }
 // members whose rows exceed HEAVY_DEG entries mark their community "heavy": a warp rescans
 // every member row at each split, so such parts go to the CTA executor instead
-constexpr int64_t HEAVY_DEG = 1 << 16;
-__global__ void k_heavy_flags(const int64_t *uptr, int64_t n, int32_t *f) {
-    GS_LOOP(i, n) f[i] = uptr[i + 1] - uptr[i] > HEAVY_DEG ? 1 : 0;
+__global__ void k_heavy_flags(const int64_t *uptr, int64_t n, int64_t heavy_deg, int32_t *f) {
+    GS_LOOP(i, n) f[i] = uptr[i + 1] - uptr[i] > heavy_deg ? 1 : 0;
 }
 __global__ void k_heavy_scatter(const int32_t *f, const int32_t *pos, int64_t n, int32_t *out) {
     GS_LOOP(i, n) if (f[i]) out[pos[i]] = (int32_t)i;
@@ -1321,7 +1325,7 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
             hf.resize(n + 1);
             hp.resize(n + 1);
             CUDA_TRY(cudaMemsetAsync(hf.p + n, 0, 4, s));
-            k_heavy_flags<<<grid_for(n, 256), 256, 0, s>>>(G.uptr.p, n, hf.p);
+            k_heavy_flags<<<grid_for(n, 256), 256, 0, s>>>(G.uptr.p, n, HEAVY_DEG, hf.p);
             cub_exclusive_sum<int32_t>(ctx, hf.p, hp.p, n + 1);
             int32_t nh = 0;
             CUDA_TRY(cudaMemcpyAsync(&nh, hp.p + n, 4, cudaMemcpyDeviceToHost, s));

@@ -334,3 +334,40 @@ def test_aggregate_long_runs_real_weights_bit_exact(slm, oracle):
     np.testing.assert_array_equal(p, op)
     np.testing.assert_array_equal(dst, odst)
     np.testing.assert_array_equal(ww, oww)
+
+
+def test_heavy_member_routing_parity(slm, oracle, monkeypatch):
+    """Communities holding a member whose union row exceeds SLM_HEAVY_DEG entries go to the
+    CTA executor even when they are small in members (coarse-level hubs).  Force the routing
+    with a tiny threshold and compare the whole hierarchy with the oracle."""
+    from paper_1702_04645_b200 import generators as GN
+    monkeypatch.setenv("SLM_HEAVY_DEG", "24")
+    for n, s, d, w in (GN.rmat(13, 16, 1, 6), GN.generate("c1_sbm")):
+        _vs_oracle(slm, oracle, n, s, d, w)
+
+
+def test_plan_without_sweep_view_matches(slm, tmp_path):
+    """The integer sweep over the degree-ordered view (default) and over the level graph
+    itself (SLM_VIEW=0, read once per process) give identical targets."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "plan.py"
+    script.write_text(
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {root!r})\n"
+        "import paper_1702_04645_b200 as slm\n"
+        "from tests.test_gpu_parity import _hub_graph\n"
+        "n, s, d, w = _hub_graph()\n"
+        "ctx = slm.Graph.from_edges(n, s, d, w).context()\n"
+        "rng = np.random.default_rng(3)\n"
+        "out = [ctx.plan(rng.integers(0, k, n).astype(np.int64)) for k in (30, 3000, n // 5)]\n"
+        "np.save(sys.argv[1], np.stack(out))\n")
+    res = {}
+    for view in ("1", "0"):
+        env = dict(os.environ, SLM_VIEW=view)
+        f = tmp_path / f"out{view}.npy"
+        subprocess.run([sys.executable, str(script), str(f)], check=True, env=env, cwd=root)
+        res[view] = np.load(f)
+    np.testing.assert_array_equal(res["1"], res["0"])
