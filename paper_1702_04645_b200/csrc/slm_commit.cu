@@ -545,6 +545,14 @@ struct Live {
 };
 
 __device__ __forceinline__ int32_t vload(const int32_t *p) { return *(volatile const int32_t *)p; }
+// acquire load (gpu scope): later loads are not performed before it, and writes released by a
+// fence + store on another SM are visible after it -- unlike __threadfence(), it does not wait
+// for this thread's own earlier stores to drain
+__device__ __forceinline__ int32_t ld_acq(const int32_t *p) {
+    int32_t v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 // resolve an accepted candidate as skipped exactly once (both of its walkers may try)
 __device__ __forceinline__ void resolve_skip(int32_t *status, int32_t k, int32_t *remaining) {
     if (atomicCAS(status + k, ST_UNRES, ST_SKIP) == ST_UNRES) atomicSub(remaining, 1);
@@ -639,10 +647,9 @@ __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_
                 i = rec.y;
                 frm = rec.z;
                 to = rec.w;
-                st = vload(status + k);
+                st = ld_acq(status + k);
                 if (to == C && st == ST_UNRES) {
-                    atF = vload(V.atk + frm);
-                    __threadfence();
+                    atF = ld_acq(V.atk + frm);
                     dF = vload8(V.dirty + frm);
                     SoF = V.S_out[frm];
                     SiF = V.S_in[frm];
@@ -661,7 +668,7 @@ __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_
                         if (st == ST_COMMIT) {
                             cls = C_OUTCOMMIT;
                         } else if (st == ST_UNRES && !(my_atk != k && dirtyC)) {
-                            st = vload(status + k);
+                            st = ld_acq(status + k);
                             cls = st == ST_COMMIT ? C_OUTCOMMIT : (st == ST_UNRES ? C_WAIT : C_PASS);
                         }
                     } else if (st == ST_UNRES) {   // C evaluates k
@@ -670,13 +677,12 @@ __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_
                             cls = C_SKIP;
                             undecided = 0;
                         } else if (atF != k) {
-                            atF = vload(V.atk + frm);
+                            atF = ld_acq(V.atk + frm);
                             if (atF != k) {
                                 cls = vload8(V.dirty + frm) ? C_SKIP : C_WAIT;
                                 if (cls == C_SKIP) dF = 1;
                                 undecided = 0;
                             } else {
-                                __threadfence();
                                 if (vload8(V.dirty + frm)) {
                                     dF = 1;
                                     cls = C_SKIP;
@@ -723,8 +729,8 @@ __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_
                     p += f;
                     break;
                 }
-                if (cf == C_OUTCOMMIT) {   // our state was changed by that commit
-                    __threadfence();
+                if (cf == C_OUTCOMMIT) {   // our state was changed by that commit (its status
+                                           // was read with acquire: the state is visible)
                     SoC = V.S_out[C];
                     SiC = V.S_in[C];
                     cntC = V.cnt[C];
