@@ -592,34 +592,375 @@ __device__ bool reprice_lane(const CommitArgs &A, const MvList &M, const int32_t
     return true;
 }
 
-// one warp per community timeline (see header comment).  Up to 32 upcoming events are
-// loaded by the lanes and classified in parallel against C's current state (speculation:
-// every event up to the first state-changing one -- a commit into C, an observed commit out
-// of C, or a wait -- sees exactly that state); skips before it are written at once, the
-// barrier event is applied, and the rest of the batch is reclassified.  A candidate's
-// status is written only by its target's walker (the source side merely moves past a
-// certain skip), so resolutions need no CAS and `remaining` drops once per walker visit.
-__global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_t *wl, int64_t nw_,
-                                              int32_t *status, const CandSpec *spec, int persistent) {
-    enum { C_PASS = 0, C_SKIP = 1, C_COMMIT = 2, C_OUTCOMMIT = 3, C_WAIT = 4, C_COOP = 5 };
+// A walker walks one community's timeline (see header comment).  Up to 32 upcoming events
+// are loaded by the lanes of a warp and classified in parallel against C's current state
+// (speculation: every event up to the first state-changing one -- a commit into C, an
+// observed commit out of C, or a wait -- sees exactly that state); skips before it are
+// written at once, the barrier event is applied, and the rest of the batch is reclassified.
+// A candidate's status is written only by its target's walker (the source side merely
+// moves past a certain skip), so resolutions need no CAS and `remaining` drops once per
+// walker visit.  Long timelines (hub communities: ~10^5 events, a few dozen commits) are
+// walked by a whole CTA: its threads classify 256 events at a time and write the skips
+// before the first state-changing event, and warp 0 applies that event with the warp logic.
+enum { C_PASS = 0, C_SKIP = 1, C_COMMIT = 2, C_OUTCOMMIT = 3, C_WAIT = 4, C_COOP = 5 };
+
+struct WalkState {
+    double SoC, SiC;
+    int32_t cntC, my_atk;
+    int dirtyC;
+};
+
+// one event as a lane sees it
+struct WalkEv {
+    int32_t k, i, frm, to, atF, st;
+    int dF;
+    double SoF, SiF;
+    CandSpec cs;
+};
+__device__ __forceinline__ void walk_load(const Live &V, const int32_t *status, const CandSpec *spec,
+                                          int32_t C, bool valid, int4 rec, WalkEv &e) {
+    e.k = -1;
+    e.i = 0;
+    e.frm = 0;
+    e.to = -1;
+    e.atF = -1;
+    e.st = ST_SKIP;
+    e.dF = 0;
+    e.SoF = e.SiF = 0.0;
+    e.cs.w_to = e.cs.w_from = e.cs.so_b = e.cs.si_b = e.cs.pgj = 0.0;
+    e.cs.je = -1;
+    e.cs.mv_off = 0;
+    e.cs.j = -1;
+    e.cs.tail_lo = e.cs.tail_hi = 0;
+    e.cs.mv_cnt = 0;
+    if (valid) {
+        e.k = rec.x;
+        e.i = rec.y;
+        e.frm = rec.z;
+        e.to = rec.w;
+        e.st = ld_acq(status + e.k);
+        if (e.to == C && e.st == ST_UNRES) {
+            e.atF = ld_acq(V.atk + e.frm);
+            e.dF = vload8(V.dirty + e.frm);
+            e.SoF = V.S_out[e.frm];
+            e.SiF = V.S_in[e.frm];
+            e.cs = spec[e.k];
+        }
+    }
+}
+
+// classification of one event against C's state W (lane-local; may refresh e's source state)
+__device__ __forceinline__ int walk_classify(const CommitArgs &A, const Live &V, int32_t *status,
+                                             int32_t C, const WalkState &W, WalkEv &e, double &gq,
+                                             double &wtq, int32_t &jq) {
+    int cls = C_PASS;
+    gq = 0.0;
+    wtq = 0.0;
+    jq = -1;
+    const int32_t k = e.k, frm = e.frm;
+    if (e.to != C) {   // C is the source
+        if (e.st == ST_COMMIT) {
+            cls = C_OUTCOMMIT;
+        } else if (e.st == ST_UNRES && !(W.my_atk != k && W.dirtyC)) {
+            e.st = ld_acq(status + k);
+            cls = e.st == ST_COMMIT ? C_OUTCOMMIT : (e.st == ST_UNRES ? C_WAIT : C_PASS);
+        }
+    } else if (e.st == ST_UNRES) {   // C evaluates k
+        int undecided = 1;
+        if (W.cntC == 0 || e.dF) {
+            cls = C_SKIP;
+            undecided = 0;
+        } else if (e.atF != k) {
+            e.atF = ld_acq(V.atk + frm);
+            if (e.atF != k) {
+                cls = vload8(V.dirty + frm) ? C_SKIP : C_WAIT;
+                if (cls == C_SKIP) e.dF = 1;
+                undecided = 0;
+            } else {
+                if (vload8(V.dirty + frm)) {
+                    e.dF = 1;
+                    cls = C_SKIP;
+                    undecided = 0;
+                } else {
+                    e.SoF = V.S_out[frm];
+                    e.SiF = V.S_in[frm];
+                }
+            }
+        }
+        if (undecided) {
+            const CandSpec &cs = e.cs;
+            wtq = cs.w_to;
+            jq = cs.j;
+            if (cs.mv_cnt > 0 && W.dirtyC &&
+                (cs.mv_cnt > 64 || !reprice_lane(A, V.mv, V.lab, cs, e.i, C, wtq, jq))) {
+                cls = C_COOP;   // long list or lost attach target: cooperative
+            } else {
+                const double so_b = cs.so_b, si_b = cs.si_b;
+                // gain_switch d_null (quality.py:216-219), exact operand order
+                const double d_null = -e.SoF * si_b - so_b * e.SiF + W.SoC * si_b +
+                                      so_b * W.SiC + 2.0 * so_b * si_b;
+                gq = (wtq - cs.w_from) / A.m - d_null / (A.m * A.m);
+                cls = (gq > 0.0 && jq >= 0) ? C_COMMIT : C_SKIP;   // detector.py:498-502
+            }
+        }
+    }
+    return cls;
+}
+
+// one warp batch: the events [p, p + nb) (lane < nb holds event p + lane, record rec) against
+// W; returns the events consumed (nb, or fewer when the walker parks)
+__device__ __forceinline__ int walk_batch(const CommitArgs &A, const Live &V, int32_t *status,
+                          const CandSpec *spec, int32_t C, int4 rec, int nb, WalkState &W,
+                          int &nres, bool &parked, int &ncommit, int &nbarrier, int &nchg) {
     const int lane = threadIdx.x & 31;
-    int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    // persistent: the (resident) warps keep revisiting their walkers until each has reached
-    // the end of its timeline, so a parked walker resumes as soon as its verdict is written
-    // instead of at the next launch
+    WalkEv e;
+    walk_load(V, status, spec, C, lane < nb, rec, e);
+    int start = 0;
+    while (start < nb) {
+        // ---- classify events [start, nb) against the current state
+        const bool act = lane >= start && lane < nb;
+        int cls = C_PASS;
+        double gq = 0.0, wtq = 0.0;
+        int32_t jq = -1;
+        if (act) cls = walk_classify(A, V, status, C, W, e, gq, wtq, jq);
+        // ---- skips before the first state-changing event
+        const unsigned bar = __ballot_sync(0xffffffffu, act && cls >= C_COMMIT);
+        const int f = bar ? __ffs(bar) - 1 : nb;
+        const bool sk = act && lane < f && cls == C_SKIP;
+        if (sk) *(volatile int32_t *)(status + e.k) = ST_SKIP;
+        nres += __popc(__ballot_sync(0xffffffffu, sk));
+        if (f >= nb) break;
+        const int cf = __shfl_sync(0xffffffffu, cls, f);
+        const int32_t kf = __shfl_sync(0xffffffffu, e.k, f);
+        if (cf == C_WAIT) {
+            if (lane == 0 && W.my_atk != kf) {
+                __threadfence();
+                *(volatile int32_t *)(V.atk + C) = kf;
+            }
+            W.my_atk = kf;
+            parked = true;
+            return f;
+        }
+        nchg++;
+        if (cf == C_OUTCOMMIT) {   // our state was changed by that commit (its status was
+                                   // read with acquire: the state is visible)
+            W.SoC = V.S_out[C];
+            W.SiC = V.S_in[C];
+            W.cntC = V.cnt[C];
+            W.dirtyC = 1;
+            start = f + 1;
+            continue;
+        }
+        // ---- evaluated candidate kf into C (commit, or a cooperative re-pricing)
+        const int32_t iq = __shfl_sync(0xffffffffu, e.i, f);
+        const int32_t fq = __shfl_sync(0xffffffffu, e.frm, f);
+        const double so_b = __shfl_sync(0xffffffffu, e.cs.so_b, f);
+        const double si_b = __shfl_sync(0xffffffffu, e.cs.si_b, f);
+        const int32_t tlo = __shfl_sync(0xffffffffu, e.cs.tail_lo, f);
+        const int32_t thi = __shfl_sync(0xffffffffu, e.cs.tail_hi, f);
+        double g = __shfl_sync(0xffffffffu, gq, f);
+        int32_t j = __shfl_sync(0xffffffffu, jq, f);
+        bool commit = cf == C_COMMIT;
+        if (cf == C_COOP) {
+            CandSpec c;
+            c.w_to = __shfl_sync(0xffffffffu, e.cs.w_to, f);
+            c.w_from = __shfl_sync(0xffffffffu, e.cs.w_from, f);
+            c.so_b = so_b;
+            c.si_b = si_b;
+            c.j = __shfl_sync(0xffffffffu, e.cs.j, f);
+            c.tail_lo = tlo;
+            c.tail_hi = thi;
+            c.pgj = __shfl_sync(0xffffffffu, e.cs.pgj, f);
+            c.je = __shfl_sync(0xffffffffu, e.cs.je, f);
+            c.mv_off = __shfl_sync(0xffffffffu, e.cs.mv_off, f);
+            c.mv_cnt = __shfl_sync(0xffffffffu, e.cs.mv_cnt, f);
+            const double SoFq = __shfl_sync(0xffffffffu, e.SoF, f);
+            const double SiFq = __shfl_sync(0xffffffffu, e.SiF, f);
+            double wt = c.w_to;
+            reprice(A, V.mv, V.lab, c, iq, C, wt, j);
+            const double d_null = -SoFq * si_b - so_b * SiFq + W.SoC * si_b + so_b * W.SiC +
+                                  2.0 * so_b * si_b;
+            g = (wt - c.w_from) / A.m - d_null / (A.m * A.m);
+            commit = g > 0.0 && j >= 0;
+        }
+        nbarrier++;
+        if (commit) {
+            ncommit++;
+            const int32_t len = thi - tlo;
+            if (V.wst && lane == 0) atomicAdd(V.wst + 5, (unsigned long long)len);
+            for (int32_t t = tlo + lane; t < thi; t += 32) V.lab[A.order[t]] = C;
+            W.SoC += so_b;
+            W.SiC += si_b;
+            W.cntC += len;
+            W.dirtyC = 1;
+            if (e.frm == fq) e.dF = 1;   // later candidates out of the same source skip
+            if (lane == 0) {
+                V.a[iq] = j;
+                // move_nodes (quality.py:87-95)
+                V.S_out[fq] -= so_b;
+                V.S_in[fq] -= si_b;
+                V.cnt[fq] -= len;
+                V.S_out[C] = W.SoC;
+                V.S_in[C] = W.SiC;
+                V.cnt[C] = W.cntC;
+                V.dirty[fq] = 1;
+                V.dirty[C] = 1;
+                atomicMin(&V.first_commit[fq], kf);
+                atomicMin(&V.first_commit[C], kf);
+                V.gain[kf] = g;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) {
+            if (commit) __threadfence();   // state and labels before the verdict
+            *(volatile int32_t *)(status + kf) = commit ? ST_COMMIT : ST_SKIP;
+        }
+        if (lane == f) e.st = commit ? ST_COMMIT : ST_SKIP;
+        nres++;
+        start = f + 1;
+    }
+    return nb;
+}
+
+__device__ __forceinline__ void walk_state_load(const Live &V, int32_t C, WalkState &W) {
+    W.SoC = V.S_out[C];
+    W.SiC = V.S_in[C];
+    W.cntC = V.cnt[C];
+    W.my_atk = V.atk[C];             // only this walker writes atk[C]
+    W.dirtyC = vload8(V.dirty + C);  // monotone
+}
+
+// end of a visit: resolved count, position, and release of waiters when the timeline is done
+__device__ __forceinline__ void walk_visit_end(const Live &V, int32_t C, int32_t p, int32_t end,
+                                               int nres) {
+    if (nres) atomicSub(V.remaining, nres);
+    V.wpos[C] = p;
+    if (p >= end) {
+        __threadfence();
+        *(volatile int32_t *)(V.atk + C) = 0x7fffffff;
+    }
+}
+
+constexpr int WALK_BLOCK = 256;
+constexpr int WALK_CLEAN = 4;   // clean warp batches before a CTA walker resumes scanning
+
+// persistent walkers: blocks [0, nlong) walk the long timelines wlong[b] with the whole CTA;
+// the warps of the other blocks walk wl (skipping the CTA-walked communities).  The grid is
+// resident, so a parked walker resumes as soon as its verdict is written.
+__global__ void __launch_bounds__(WALK_BLOCK) k_walk(CommitArgs A, Live V, const int32_t *wl,
+                                                     int64_t nw_, int32_t *status,
+                                                     const CandSpec *spec, int persistent,
+                                                     const int32_t *wlong, int32_t nlong,
+                                                     const uint8_t *cta_mode) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if ((int32_t)blockIdx.x < nlong) {
+        // ---------------------------------------------------------------- CTA walker
+        __shared__ int s_f, s_cnt, s_parked, s_p;
+        __shared__ WalkState s_W;
+        const int32_t C = wlong[blockIdx.x];
+        const int32_t end = V.tl_ptr[C + 1];
+        for (;;) {
+            int32_t p = V.wpos[C];
+            if (p >= end) break;
+            __threadfence();
+            WalkState W;
+            walk_state_load(V, C, W);
+            const int32_t p_start = p;
+            int nres = 0;   // (thread 0's count)
+            bool parked = false;
+            int ncommit = 0, nbarrier = 0;
+            while (p < end && !parked) {
+                // skip scan: WALK_BLOCK events against the current state
+                const int nbk = min(WALK_BLOCK, end - p);
+                const int t = threadIdx.x;
+                if (t == 0) {
+                    s_f = nbk;
+                    s_cnt = 0;
+                }
+                __syncthreads();
+                WalkEv e;
+                const bool valid = t < nbk;
+                walk_load(V, status, spec, C, valid, valid ? V.tl_rec[p + t] : make_int4(-1, 0, 0, -1), e);
+                int cls = C_PASS;
+                double gq, wtq;
+                int32_t jq;
+                if (valid) cls = walk_classify(A, V, status, C, W, e, gq, wtq, jq);
+                if (valid && cls >= C_COMMIT) atomicMin(&s_f, t);
+                __syncthreads();
+                const int f = s_f;
+                const bool sk = valid && t < f && cls == C_SKIP;
+                if (sk) *(volatile int32_t *)(status + e.k) = ST_SKIP;
+                const int ns = __popc(__ballot_sync(0xffffffffu, sk));
+                if (lane == 0 && ns) atomicAdd(&s_cnt, ns);
+                __syncthreads();
+                if (t == 0) nres += s_cnt;
+                p += f;
+                if (f >= nbk) continue;   // no state change in this window
+                // the state-changing event at p: warp 0 applies it with the warp logic and
+                // keeps walking by warp batches while state changes are dense (early sweeps);
+                // WALK_CLEAN consecutive batches without one return to the CTA scan
+                if (wid == 0) {
+                    int nr = 0;
+                    bool pk = false;
+                    int32_t q = p;
+                    int clean = 0;
+                    int4 rec_next = lane < min(32, end - q) ? V.tl_rec[q + lane]
+                                                            : make_int4(-1, 0, 0, -1);
+                    while (q < end) {
+                        const int nb = min(32, end - q);
+                        const int4 rec = rec_next;
+                        rec_next = q + nb + lane < end ? V.tl_rec[q + nb + lane]
+                                                       : make_int4(-1, 0, 0, -1);
+                        int nchg = 0;
+                        q += walk_batch(A, V, status, spec, C, rec, nb, W, nr, pk, ncommit,
+                                        nbarrier, nchg);
+                        if (pk) break;
+                        clean = nchg ? 0 : clean + 1;
+                        if (clean >= WALK_CLEAN) break;
+                    }
+                    if (lane == 0) {
+                        s_W = W;
+                        s_p = q;
+                        s_parked = pk ? 1 : 0;
+                        nres += nr;
+                    }
+                }
+                __syncthreads();
+                W = s_W;
+                p = s_p;
+                parked = s_parked != 0;
+                __syncthreads();
+            }
+            if (threadIdx.x == 0) {
+                if (V.wst && p > p_start) {
+                    atomicAdd(V.wst, (unsigned long long)(p - p_start));
+                    atomicMax(V.wst + 1, (unsigned long long)(p - p_start));
+                    atomicAdd(V.wst + 2, 1ull);
+                    atomicMax(V.wst + 6, (unsigned long long)ncommit);
+                    atomicMax(V.wst + 7, (unsigned long long)nbarrier);
+                }
+                walk_visit_end(V, C, p, end, nres);
+            }
+            __syncthreads();
+            if (!persistent || p >= end) break;
+            if (p == p_start) __nanosleep(256);
+        }
+        return;
+    }
+    // -------------------------------------------------------------------- warp walkers
+    int64_t w = ((blockIdx.x - nlong) * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((gridDim.x - nlong) * (int64_t)blockDim.x) >> 5;
     for (;;) {
     int pending = 0, progressed = 0;
     for (int64_t wi = w; wi < nw_; wi += nwarps) {
         const int32_t C = wl[wi];
+        if (cta_mode && cta_mode[C]) continue;
         int32_t p = V.wpos[C];
         const int32_t end = V.tl_ptr[C + 1];
         if (p >= end) continue;
         __threadfence();
-        double SoC = V.S_out[C], SiC = V.S_in[C];
-        int32_t cntC = V.cnt[C];
-        int32_t my_atk = V.atk[C];          // only this walker writes atk[C]
-        int dirtyC = vload8(V.dirty + C);   // monotone
+        WalkState W;
+        walk_state_load(V, C, W);
         int nres = 0;                       // candidates resolved by this visit
         int ncommit = 0, nbarrier = 0;      // (profiling)
         bool parked = false;
@@ -632,181 +973,8 @@ __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_
             const int4 rec = rec_next;
             rec_next = make_int4(-1, 0, 0, -1);
             if (p + nb + lane < end) rec_next = V.tl_rec[p + nb + lane];
-            int32_t k = -1, i = 0, frm = 0, to = -1, atF = -1, st = ST_SKIP;
-            int dF = 0;
-            double SoF = 0.0, SiF = 0.0;
-            CandSpec cs;
-            cs.w_to = cs.w_from = cs.so_b = cs.si_b = cs.pgj = 0.0;
-            cs.je = -1;
-            cs.mv_off = 0;
-            cs.j = -1;
-            cs.tail_lo = cs.tail_hi = 0;
-            cs.mv_cnt = 0;
-            if (lane < nb) {
-                k = rec.x;
-                i = rec.y;
-                frm = rec.z;
-                to = rec.w;
-                st = ld_acq(status + k);
-                if (to == C && st == ST_UNRES) {
-                    atF = ld_acq(V.atk + frm);
-                    dF = vload8(V.dirty + frm);
-                    SoF = V.S_out[frm];
-                    SiF = V.S_in[frm];
-                    cs = spec[k];
-                }
-            }
-            int start = 0;
-            while (start < nb) {
-                // ---- classify events [start, nb) against the current state
-                const bool act = lane >= start && lane < nb;
-                int cls = C_PASS;
-                double gq = 0.0, wtq = 0.0;
-                int32_t jq = -1;
-                if (act) {
-                    if (to != C) {   // C is the source
-                        if (st == ST_COMMIT) {
-                            cls = C_OUTCOMMIT;
-                        } else if (st == ST_UNRES && !(my_atk != k && dirtyC)) {
-                            st = ld_acq(status + k);
-                            cls = st == ST_COMMIT ? C_OUTCOMMIT : (st == ST_UNRES ? C_WAIT : C_PASS);
-                        }
-                    } else if (st == ST_UNRES) {   // C evaluates k
-                        int undecided = 1;
-                        if (cntC == 0 || dF) {
-                            cls = C_SKIP;
-                            undecided = 0;
-                        } else if (atF != k) {
-                            atF = ld_acq(V.atk + frm);
-                            if (atF != k) {
-                                cls = vload8(V.dirty + frm) ? C_SKIP : C_WAIT;
-                                if (cls == C_SKIP) dF = 1;
-                                undecided = 0;
-                            } else {
-                                if (vload8(V.dirty + frm)) {
-                                    dF = 1;
-                                    cls = C_SKIP;
-                                    undecided = 0;
-                                } else {
-                                    SoF = V.S_out[frm];
-                                    SiF = V.S_in[frm];
-                                }
-                            }
-                        }
-                        if (undecided) {
-                            wtq = cs.w_to;
-                            jq = cs.j;
-                            if (cs.mv_cnt > 0 && dirtyC &&
-                                (cs.mv_cnt > 64 || !reprice_lane(A, V.mv, V.lab, cs, i, C, wtq, jq))) {
-                                cls = C_COOP;   // long list or lost attach target: cooperative
-                            } else {
-                                const double so_b = cs.so_b, si_b = cs.si_b;
-                                // gain_switch d_null (quality.py:216-219), exact operand order
-                                const double d_null = -SoF * si_b - so_b * SiF + SoC * si_b +
-                                                      so_b * SiC + 2.0 * so_b * si_b;
-                                gq = (wtq - cs.w_from) / A.m - d_null / (A.m * A.m);
-                                cls = (gq > 0.0 && jq >= 0) ? C_COMMIT : C_SKIP;   // detector.py:498-502
-                            }
-                        }
-                    }
-                }
-                // ---- skips before the first state-changing event
-                const unsigned bar = __ballot_sync(0xffffffffu, act && cls >= C_COMMIT);
-                const int f = bar ? __ffs(bar) - 1 : nb;
-                const bool sk = act && lane < f && cls == C_SKIP;
-                if (sk) *(volatile int32_t *)(status + k) = ST_SKIP;
-                nres += __popc(__ballot_sync(0xffffffffu, sk));
-                if (f >= nb) break;
-                const int cf = __shfl_sync(0xffffffffu, cls, f);
-                const int32_t kf = __shfl_sync(0xffffffffu, k, f);
-                if (cf == C_WAIT) {
-                    if (lane == 0 && my_atk != kf) {
-                        __threadfence();
-                        *(volatile int32_t *)(V.atk + C) = kf;
-                    }
-                    my_atk = kf;
-                    parked = true;
-                    p += f;
-                    break;
-                }
-                if (cf == C_OUTCOMMIT) {   // our state was changed by that commit (its status
-                                           // was read with acquire: the state is visible)
-                    SoC = V.S_out[C];
-                    SiC = V.S_in[C];
-                    cntC = V.cnt[C];
-                    dirtyC = 1;
-                    start = f + 1;
-                    continue;
-                }
-                // ---- evaluated candidate kf into C (commit, or a cooperative re-pricing)
-                const int32_t iq = __shfl_sync(0xffffffffu, i, f);
-                const int32_t fq = __shfl_sync(0xffffffffu, frm, f);
-                const double so_b = __shfl_sync(0xffffffffu, cs.so_b, f);
-                const double si_b = __shfl_sync(0xffffffffu, cs.si_b, f);
-                const int32_t tlo = __shfl_sync(0xffffffffu, cs.tail_lo, f);
-                const int32_t thi = __shfl_sync(0xffffffffu, cs.tail_hi, f);
-                double g = __shfl_sync(0xffffffffu, gq, f);
-                int32_t j = __shfl_sync(0xffffffffu, jq, f);
-                bool commit = cf == C_COMMIT;
-                if (cf == C_COOP) {
-                    CandSpec c;
-                    c.w_to = __shfl_sync(0xffffffffu, cs.w_to, f);
-                    c.w_from = __shfl_sync(0xffffffffu, cs.w_from, f);
-                    c.so_b = so_b;
-                    c.si_b = si_b;
-                    c.j = __shfl_sync(0xffffffffu, cs.j, f);
-                    c.tail_lo = tlo;
-                    c.tail_hi = thi;
-                    c.pgj = __shfl_sync(0xffffffffu, cs.pgj, f);
-                    c.je = __shfl_sync(0xffffffffu, cs.je, f);
-                    c.mv_off = __shfl_sync(0xffffffffu, cs.mv_off, f);
-                    c.mv_cnt = __shfl_sync(0xffffffffu, cs.mv_cnt, f);
-                    const double SoFq = __shfl_sync(0xffffffffu, SoF, f);
-                    const double SiFq = __shfl_sync(0xffffffffu, SiF, f);
-                    double wt = c.w_to;
-                    reprice(A, V.mv, V.lab, c, iq, C, wt, j);
-                    const double d_null = -SoFq * si_b - so_b * SiFq + SoC * si_b + so_b * SiC +
-                                          2.0 * so_b * si_b;
-                    g = (wt - c.w_from) / A.m - d_null / (A.m * A.m);
-                    commit = g > 0.0 && j >= 0;
-                }
-                nbarrier++;
-                if (commit) {
-                    ncommit++;
-                    const int32_t len = thi - tlo;
-                    if (V.wst && lane == 0) atomicAdd(V.wst + 5, (unsigned long long)len);
-                    for (int32_t t = tlo + lane; t < thi; t += 32) V.lab[A.order[t]] = C;
-                    SoC += so_b;
-                    SiC += si_b;
-                    cntC += len;
-                    dirtyC = 1;
-                    if (frm == fq) dF = 1;   // later candidates out of the same source skip
-                    if (lane == 0) {
-                        V.a[iq] = j;
-                        // move_nodes (quality.py:87-95)
-                        V.S_out[fq] -= so_b;
-                        V.S_in[fq] -= si_b;
-                        V.cnt[fq] -= len;
-                        V.S_out[C] = SoC;
-                        V.S_in[C] = SiC;
-                        V.cnt[C] = cntC;
-                        V.dirty[fq] = 1;
-                        V.dirty[C] = 1;
-                        atomicMin(&V.first_commit[fq], kf);
-                        atomicMin(&V.first_commit[C], kf);
-                        V.gain[kf] = g;
-                    }
-                }
-                __syncwarp();
-                if (lane == 0) {
-                    if (commit) __threadfence();   // state and labels before the verdict
-                    *(volatile int32_t *)(status + kf) = commit ? ST_COMMIT : ST_SKIP;
-                }
-                if (lane == f) st = commit ? ST_COMMIT : ST_SKIP;
-                nres++;
-                start = f + 1;
-            }
-            if (!parked) p += nb;
+            int nchg = 0;
+            p += walk_batch(A, V, status, spec, C, rec, nb, W, nres, parked, ncommit, nbarrier, nchg);
         }
         if (V.wst && lane == 0 && p > p_start) {
             atomicAdd(V.wst, (unsigned long long)(p - p_start));
@@ -815,19 +983,29 @@ __global__ void __launch_bounds__(256) k_walk(CommitArgs A, Live V, const int32_
             atomicMax(V.wst + 6, (unsigned long long)ncommit);
             atomicMax(V.wst + 7, (unsigned long long)nbarrier);
         }
-        if (lane == 0) {
-            if (nres) atomicSub(V.remaining, nres);
-            V.wpos[C] = p;
-            if (p >= end) {
-                __threadfence();
-                *(volatile int32_t *)(V.atk + C) = 0x7fffffff;
-            }
-        }
+        if (lane == 0) walk_visit_end(V, C, p, end, nres);
         if (p > p_start) progressed = 1;
         if (p < end) pending = 1;
     }
     if (!persistent || !pending) break;
     if (!progressed) __nanosleep(256);
+    }
+}
+
+__global__ void k_long_flags(const int32_t *wl, int64_t nw, const int32_t *tl_ptr, int32_t lim,
+                             int32_t *f) {
+    GS_LOOP(q, nw) {
+        const int32_t c = wl[q];
+        f[q] = tl_ptr[c + 1] - tl_ptr[c] > lim ? 1 : 0;
+    }
+}
+__global__ void k_long_scatter(const int32_t *f, const int32_t *pos, const int32_t *wl, int64_t nw,
+                               int32_t nlong, int32_t *wlong, uint8_t *cmode) {
+    GS_LOOP(q, nw) {
+        if (f[q] && pos[q] < nlong) {
+            wlong[pos[q]] = wl[q];
+            cmode[wl[q]] = 1;
+        }
     }
 }
 
@@ -871,6 +1049,8 @@ struct CommitScratch {
     DBuf<int32_t> wf, wp;
     DBuf<int32_t> cf, cpos;
     DBuf<double> gg;
+    DBuf<int32_t> lf, lp, wlong;   // long timelines (CTA walkers)
+    DBuf<uint8_t> cmode;
 };
 
 void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const int32_t *d_cstar,
@@ -1074,16 +1254,47 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
         static int walk_blocks = 0;
         if (walk_blocks == 0) {
             int per_sm = 0;
-            CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk, 256, 0));
+            CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk, WALK_BLOCK, 0));
             walk_blocks = std::max(1, per_sm) * 148;
         }
         static const bool rounds_mode = getenv("SLM_WALK_ROUNDS") != nullptr;
         const unsigned GWP = (unsigned)std::min<int64_t>(GWK, walk_blocks);
+        // timelines longer than LONG_TL events (hub communities) are walked by whole CTAs,
+        // blocks [0, nlong) of the persistent grid (at most 16: the rest walk the many short
+        // timelines of the early sweeps)
+        static const int LONG_TL = getenv("SLM_WALK_LONG") ? std::max(32, atoi(getenv("SLM_WALK_LONG")))
+                                                           : 8192;
+        int32_t nlong = 0;
+        const uint8_t *cmode = nullptr;
+        if (!rounds_mode && NW > 0) {
+            DBuf<int32_t> &lf = CS.lf, &lp = CS.lp;
+            lf.resize(NW + 1);
+            lp.resize(NW + 1);
+            CUDA_TRY(cudaMemsetAsync(lf.p + NW, 0, 4, s));
+            k_long_flags<<<grid_for(NW, 256), 256, 0, s>>>(wl.p, NW, tl_ptr.p, LONG_TL, lf.p);
+            cub_exclusive_sum<int32_t>(ctx, lf.p, lp.p, NW + 1);
+            int32_t NL = 0;
+            CUDA_TRY(cudaMemcpyAsync(&NL, lp.p + NW, 4, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            nlong = std::min<int32_t>(NL, std::min<int32_t>(16, (int32_t)(GWP / 8)));
+            if (nlong > 0) {
+                CS.cmode.resize(nc);
+                CS.wlong.resize(nlong);
+                CUDA_TRY(cudaMemsetAsync(CS.cmode.p, 0, nc, s));
+                k_long_scatter<<<grid_for(NW, 256), 256, 0, s>>>(lf.p, lp.p, wl.p, NW, nlong,
+                                                                 CS.wlong.p, CS.cmode.p);
+                cmode = CS.cmode.p;
+            }
+        }
         for (int round = 0; rem > 0; round++) {
             if (wprof) CUDA_TRY(cudaMemsetAsync(wst.p, 0, 64, s));
             const double t0 = ctx->prof ? now_ms() : 0.0;
-            if (rounds_mode) k_walk<<<GWK, 256, 0, s>>>(A, V, wl.p, NW, status.p, spec.p, 0);
-            else k_walk<<<GWP, 256, 0, s>>>(A, V, wl.p, NW, status.p, spec.p, 1);
+            if (rounds_mode)
+                k_walk<<<GWK, WALK_BLOCK, 0, s>>>(A, V, wl.p, NW, status.p, spec.p, 0, nullptr, 0,
+                                                  nullptr);
+            else
+                k_walk<<<GWP, WALK_BLOCK, 0, s>>>(A, V, wl.p, NW, status.p, spec.p, 1, CS.wlong.p,
+                                                  nlong, cmode);
             CUDA_TRY(cudaMemcpyAsync(&rem, remaining.p, 4, cudaMemcpyDeviceToHost, s));
             CUDA_TRY(cudaStreamSynchronize(s));
             if (ctx->prof) rt.push_back(now_ms() - t0);
