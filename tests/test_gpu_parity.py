@@ -371,3 +371,29 @@ def test_plan_without_sweep_view_matches(slm, tmp_path):
         subprocess.run([sys.executable, str(script), str(f)], check=True, env=env, cwd=root)
         res[view] = np.load(f)
     np.testing.assert_array_equal(res["1"], res["0"])
+
+
+def test_cta_walkers_full_run_parity(tmp_path):
+    """Commit walkers over long timelines use a whole CTA (SLM_WALK_LONG events, read once
+    per process): force them onto short timelines and compare full hierarchies with the
+    oracle in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "walk.py"
+    script.write_text(
+        "import sys\n"
+        f"sys.path.insert(0, {root!r})\n"
+        "import paper_1702_04645_b200 as slm\n"
+        "from paper_1702_04645_b200 import generators as GN\n"
+        "from oracle import oracle as O\n"
+        "from tests.test_gpu_parity import _vs_oracle\n"
+        "O.build()\n"
+        "for n, s, d, w in (GN.rmat(13, 16, 1, 4), GN.rmat(12, 16, 0, 2), GN.generate('c1_sbm')):\n"
+        "    _vs_oracle(slm, O, n, s, d, w)\n"
+        "print('ok')\n")
+    env = dict(os.environ, SLM_WALK_LONG="40")
+    r = subprocess.run([sys.executable, str(script)], env=env, cwd=root, capture_output=True,
+                       text=True)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
