@@ -17,7 +17,7 @@ double dbuf_now_ms() { return now_ms(); }
 // loop makes hundreds of temporaries), so DBuf sub-allocates from one device arena reserved
 // when the first context of the process is created: best-fit free blocks indexed by size,
 // coalesced with their neighbours on release.  Requests the arena cannot hold fall back to
-// cudaMalloc.  SLM_ARENA_GB sets the arena size (default 75% of the free device memory;
+// cudaMalloc.  SLM_ARENA_GB sets the arena size (default 88% of the free device memory;
 // 0 disables it).
 namespace {
 struct Arena {
@@ -67,7 +67,7 @@ void dcache_reserve(int dev) {
         cudaGetLastError();
         return;
     }
-    size_t want = (size_t)(0.75 * (double)fr);
+    size_t want = (size_t)(0.88 * (double)fr);
     if (const char *e = getenv("SLM_ARENA_GB")) want = (size_t)(atof(e) * (double)(1ull << 30));
     want &= ~(size_t)(ARENA_ALIGN - 1);
     while (want >= (64ull << 20)) {
@@ -111,6 +111,16 @@ void *dcache_alloc(size_t bytes, size_t *got) {
     cudaError_t e = cudaMalloc(&p, need);
     g_alloc_ms += now_ms() - t;
     g_alloc_calls++;
+    if (getenv("SLM_ARENA_VERBOSE")) {
+        std::lock_guard<std::mutex> lk(g_dc_mu);
+        const Arena &A = g_arena[dev];
+        const size_t largest = A.by_len.empty() ? 0 : A.by_len.rbegin()->first;
+        size_t freeb = 0;
+        for (auto &kv : A.by_off) freeb += kv.second;
+        fprintf(stderr, "[arena] fallback cudaMalloc %.3f GB (arena %.1f GB, free %.2f GB, largest "
+                "free %.2f GB) %.1f ms\n", need / 1e9, A.size / 1e9, freeb / 1e9, largest / 1e9,
+                now_ms() - t);
+    }
     if (e != cudaSuccess) {
         cudaGetLastError();
         *got = 0;

@@ -139,8 +139,10 @@ struct CommitArgs {
     double m, m2;
 };
 
-// candidates whose tail has more members than this are evaluated by a whole CTA
+// candidates whose tail has more members than this, or whose tail rows hold more union
+// entries than BIG_VOL (coarse-level hubs), are evaluated by a whole CTA
 constexpr int BIG_TAIL = 64;
+constexpr int64_t BIG_VOL = 4096;
 
 __device__ __forceinline__ void tail_range(const CommitArgs &A, int32_t i, int32_t frm, int32_t &lo,
                                            int32_t &hi) {
@@ -168,7 +170,18 @@ __global__ void k_spec(CommitArgs A, int64_t K, const int32_t *status, CandSpec 
         const int32_t base = A.cptr[frm];
         int32_t lo, hi;
         tail_range(A, i, frm, lo, hi);
-        if (hi - lo > BIG_TAIL) {
+        bool isbig = hi - lo > BIG_TAIL;
+        if (!isbig) {
+            int64_t vol = 0;
+            for (int32_t q = lo + lane; q < hi; q += 32) {
+                const int32_t x = A.order[q];
+                vol += A.uptr[x + 1] - A.uptr[x];
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) vol += __shfl_xor_sync(0xffffffffu, vol, off);
+            isbig = vol > BIG_VOL;
+        }
+        if (isbig) {
             if (lane == 0) big[atomicAdd(nbig, 1)] = (int32_t)k;
             continue;
         }
@@ -300,7 +313,7 @@ __global__ void __launch_bounds__(SPEC_BLOCK) k_spec_big(CommitArgs A, const int
                 c.j = be != INT64_MAX ? A.unbr[be] : -1;
                 c.tail_lo = lo;
                 c.tail_hi = hi;
-                c.mv_cnt = 0;
+                c.mv_cnt = -1;   // big: k_mv_scan leaves it to k_mv_scan_big (which sets it)
                 spec[k] = c;
             }
         }
@@ -344,7 +357,7 @@ __global__ void k_mv_scan(CommitArgs A, int64_t K, const int32_t *status, CandSp
         if (status[k] != ST_UNRES) continue;
         const int32_t i = A.cand[k], frm = A.comm[i];
         const CandSpec c = spec[k];
-        if (c.tail_hi - c.tail_lo > BIG_TAIL) continue;   // k_mv_scan_big
+        if (c.mv_cnt < 0) continue;   // big candidate: k_mv_scan_big
         int64_t base = fill ? c.mv_off : 0, total = 0;
         for (int32_t q = c.tail_lo; q < c.tail_hi; q++) {
             const int32_t x = A.order[q];
