@@ -57,20 +57,32 @@ class Clocks:
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        self.t0 = self.t1 = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.device}", f"--query-gpu={q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # the sampler must be running before the timed region starts
+            deadline = time.perf_counter() + 5.0
+            while not self.lines and time.perf_counter() < deadline:
+                time.sleep(0.01)
         except OSError:
             self.proc = None
         return self
 
+    def start(self):
+        self.t0 = time.perf_counter()
+
+    def stop(self):
+        self.t1 = time.perf_counter()
+        time.sleep(0.12)   # the sample taken just after the last timed step
+
     def _read(self):
         for ln in self.proc.stdout:
-            self.lines.append(ln.strip())
+            self.lines.append((time.perf_counter(), ln.strip()))
 
     def __exit__(self, *a):
         if self.proc:
@@ -83,7 +95,16 @@ class Clocks:
     def summary(self):
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines
+        if self.t0 is not None and self.t1 is not None:
+            # samples taken during the timed region (one sampling interval of slack at its
+            # end); the first sample after its start when the region is shorter than that
+            inside = [ln for t, ln in lines if self.t0 <= t <= self.t1 + 0.1]
+            after = [ln for t, ln in lines if t >= self.t0][:1]
+            lines = inside or after
+        else:
+            lines = [ln for _, ln in lines]
+        for ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -180,7 +201,7 @@ def time_oracle(sample, threads, reps=1):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c5_rmat24")
@@ -278,7 +299,9 @@ def main():
     # `ncu --profile-from-start off` launch list covers exactly the timed region
     torch.cuda.profiler.start()
     with Clocks(local) as clk:
+        clk.start()
         ms = timed(127, args.steps)
+        clk.stop()
     ctx.sync()
     torch.cuda.profiler.stop()
     torch.cuda.synchronize()

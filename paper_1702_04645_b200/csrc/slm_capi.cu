@@ -84,12 +84,38 @@ void dcache_reserve(int dev) {
     }
 }
 
+// the stream of the API call in progress on this thread (set by API_BEGIN)
+static thread_local cudaStream_t g_tls_stream = nullptr;
+struct PendingFree {
+    int dev;
+    size_t off, len;
+    cudaEvent_t ev;
+};
+static std::vector<PendingFree> &g_pending = *new std::vector<PendingFree>;
+static std::vector<cudaEvent_t> &g_event_pool = *new std::vector<cudaEvent_t>;
+// blocks released while another context was alive become free once their stream passed
+// the release point (called with g_dc_mu held)
+static void drain_pending_locked() {
+    for (size_t q = 0; q < g_pending.size();) {
+        PendingFree &pf = g_pending[q];
+        if (cudaEventQuery(pf.ev) == cudaSuccess) {
+            arena_insert_free(g_arena[pf.dev], pf.off, pf.len);
+            g_event_pool.push_back(pf.ev);
+            pf = g_pending.back();
+            g_pending.pop_back();
+        } else {
+            cudaGetLastError();
+            q++;
+        }
+    }
+}
 void *dcache_alloc(size_t bytes, size_t *got) {
     const size_t need = (bytes + ARENA_ALIGN - 1) / ARENA_ALIGN * ARENA_ALIGN;
     int dev = 0;
     cudaGetDevice(&dev);
     {
         std::lock_guard<std::mutex> lk(g_dc_mu);
+        if (!g_pending.empty()) drain_pending_locked();
         Arena &A = g_arena[dev];
         auto it = A.by_len.lower_bound(need);
         if (it != A.by_len.end()) {
@@ -133,13 +159,8 @@ static std::atomic<int> g_live_ctx{0};
 void dcache_free(void *p, size_t bytes) {
     // Every kernel and copy of a context runs on its one stream, so a block released while
     // queued work still uses it is only handed to later work of the same stream (ordered
-    // after it).  With several live contexts (several streams) the release waits for the
-    // device, as the cudaFree it replaces did.
-    if (g_live_ctx.load() > 1) {
-        const double t = now_ms();
-        cudaDeviceSynchronize();
-        g_alloc_ms += now_ms() - t;
-    }
+    // after it).  With several live contexts (several streams) the block is parked until an
+    // event recorded on the releasing call's stream has completed.
     int dev = 0;
     cudaGetDevice(&dev);
     {
@@ -148,8 +169,26 @@ void dcache_free(void *p, size_t bytes) {
         auto it = A.live.find(p);
         if (it != A.live.end()) {
             const size_t len = it->second;
+            const size_t off = (size_t)((char *)p - A.base);
             A.live.erase(it);
-            arena_insert_free(A, (size_t)((char *)p - A.base), len);
+            if (g_live_ctx.load() > 1) {
+                cudaEvent_t ev = nullptr;
+                if (!g_event_pool.empty()) {
+                    ev = g_event_pool.back();
+                    g_event_pool.pop_back();
+                } else if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+                    cudaGetLastError();
+                    ev = nullptr;
+                }
+                if (ev && g_tls_stream && cudaEventRecord(ev, g_tls_stream) == cudaSuccess) {
+                    g_pending.push_back({dev, off, len, ev});
+                    return;
+                }
+                cudaGetLastError();
+                if (ev) g_event_pool.push_back(ev);
+                cudaDeviceSynchronize();   // no stream known: wait, as cudaFree did
+            }
+            arena_insert_free(A, off, len);
             return;
         }
     }
@@ -166,7 +205,14 @@ void gen_rmat_device(slm_ctx *ctx, int scale, int edge_factor, double a, double 
 void gen_rgg_device(slm_ctx *ctx, int64_t n, double radius, uint64_t seed, DBuf<int32_t> &src,
                     DBuf<int32_t> &dst, DBuf<double> &w, int64_t &ne);
 
-#define API_BEGIN try {
+struct SlmStreamScope {   // the stream DBuf releases are ordered on during an API call
+    cudaStream_t prev;
+    explicit SlmStreamScope(slm_ctx *c) : prev(g_tls_stream) {
+        if (c) g_tls_stream = c->stream;
+    }
+    ~SlmStreamScope() { g_tls_stream = prev; }
+};
+#define API_BEGIN try { SlmStreamScope _slm_stream_scope(ctx);
 #define API_END                                                                           \
     }                                                                                     \
     catch (const SlmError &e) {                                                           \
@@ -326,8 +372,11 @@ void slm_destroy(slm_ctx *ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    ctx->g.reset();
-    ctx->g0.reset();
+    {
+        SlmStreamScope scope(ctx);
+        ctx->g.reset();
+        ctx->g0.reset();
+    }
     cudaStreamDestroy(ctx->stream);
     delete ctx;
     g_live_ctx--;
