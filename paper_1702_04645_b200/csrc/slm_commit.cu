@@ -159,7 +159,7 @@ __device__ __forceinline__ void tail_range(const CommitArgs &A, int32_t i, int32
 // speculative evaluation against the snapshot (one warp per accepted candidate; tails of
 // more than BIG_TAIL members are listed for k_spec_big)
 __global__ void k_spec(CommitArgs A, int64_t K, const int32_t *status, CandSpec *spec,
-                       int32_t *big, int32_t *nbig) {
+                       int32_t *big, int32_t *nbig, int64_t *vol_out) {
     const int lane = threadIdx.x & 31;
     int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -180,6 +180,7 @@ __global__ void k_spec(CommitArgs A, int64_t K, const int32_t *status, CandSpec 
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) vol += __shfl_xor_sync(0xffffffffu, vol, off);
             isbig = vol > BIG_VOL;
+            if (lane == 0) vol_out[k] = vol;   // capacity of its moving-neighbour list
         }
         if (isbig) {
             if (lane == 0) big[atomicAdd(nbig, 1)] = (int32_t)k;
@@ -233,8 +234,10 @@ __global__ void k_spec(CommitArgs A, int64_t K, const int32_t *status, CandSpec 
 // (members over warps, entries over lanes), the attach target over row i by warp 0
 constexpr int SPEC_BLOCK = 512;
 __global__ void __launch_bounds__(SPEC_BLOCK) k_spec_big(CommitArgs A, const int32_t *big,
-                                                         const int32_t *nbig, CandSpec *spec) {
+                                                         const int32_t *nbig, CandSpec *spec,
+                                                         int64_t *vol_out) {
     __shared__ double red[4][SPEC_BLOCK / 32];
+    __shared__ unsigned long long s_vol;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     constexpr int NW = SPEC_BLOCK / 32;
     const int32_t nb = *nbig;
@@ -247,11 +250,16 @@ __global__ void __launch_bounds__(SPEC_BLOCK) k_spec_big(CommitArgs A, const int
         tail_range(A, i, frm, lo, hi);
         const int32_t plo = lo - base, phi = hi - base;
         double so = 0.0, si = 0.0, wf = 0.0, wt = 0.0;
+        if (threadIdx.x == 0) s_vol = 0;
+        __syncthreads();
+        unsigned long long vol = 0;
         for (int32_t q = lo + threadIdx.x; q < hi; q += SPEC_BLOCK) {
             const int32_t x = A.order[q];
             so += A.s_out[x];
             si += A.s_in[x];
+            vol += (unsigned long long)(A.uptr[x + 1] - A.uptr[x]);
         }
+        atomicAdd(&s_vol, vol);
         for (int32_t q = lo + wid; q < hi; q += NW) {
             const int32_t x = A.order[q];
             for (int64_t e = A.uptr[x] + lane; e < A.uptr[x + 1]; e += 32) {
@@ -302,6 +310,7 @@ __global__ void __launch_bounds__(SPEC_BLOCK) k_spec_big(CommitArgs A, const int
                 }
             }
             if (lane == 0) {
+                vol_out[k] = (int64_t)s_vol;   // capacity of its moving-neighbour list
                 CandSpec c;
                 c.w_to = v[3];
                 c.w_from = v[2];
@@ -1131,24 +1140,23 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     big.resize(K + 1);   // [K] = count
     int32_t *nbig = big.p + K;
     CUDA_TRY(cudaMemsetAsync(nbig, 0, 4, s));
-    k_spec<<<GW, 256, 0, s>>>(A, K, status.p, spec.p, big.p, nbig);
-    k_spec_big<<<148 * 4, SPEC_BLOCK, 0, s>>>(A, big.p, nbig, spec.p);
+    // moving-neighbour list capacities: each accepted candidate's tail entry volume (one
+    // scan fills the lists; they need no exact count pass)
+    DBuf<int64_t> &mvcnt = CS.mvcnt, &mvoff = CS.mvoff;
+    mvcnt.resize(K + 1);
+    mvoff.resize(K + 1);
+    CUDA_TRY(cudaMemsetAsync(mvcnt.p, 0, (K + 1) * 8, s));
+    k_spec<<<GW, 256, 0, s>>>(A, K, status.p, spec.p, big.p, nbig, mvcnt.p);
+    k_spec_big<<<148 * 4, SPEC_BLOCK, 0, s>>>(A, big.p, nbig, spec.p, mvcnt.p);
     stick();
     CUDA_TRY(cudaMemsetAsync(moving.p, 0, n, s));
     k_mark_moving<<<GW, 256, 0, s>>>(cand.p, F.comm.p, F.on_cycle.p, F.cptr.p, F.pos.p, F.sz.p,
                                      F.order.p, K, status.p, moving.p);
-    DBuf<int64_t> &mvcnt = CS.mvcnt, &mvoff = CS.mvoff;
     DBuf<int32_t> &mv_z = CS.mv_z;
     DBuf<double> &mv_u = CS.mv_u;
     DBuf<int64_t> &mv_e = CS.mv_e;
     DBuf<uint8_t> &mv_i = CS.mv_i;
-    mvcnt.resize(K + 1);
-    mvoff.resize(K + 1);
-    CUDA_TRY(cudaMemsetAsync(mvcnt.p, 0, (K + 1) * 8, s));
-    k_mv_scan<<<GW, 256, 0, s>>>(A, K, status.p, spec.p, moving.p, 0, mvcnt.p, nullptr, nullptr,
-                                 nullptr, nullptr);
-    k_mv_scan_big<<<148 * 4, SPEC_BLOCK, 0, s>>>(A, big.p, nbig, spec.p, moving.p, 0, mvcnt.p,
-                                                 nullptr, nullptr, nullptr, nullptr);
+
     stick();
     cub_exclusive_sum<int64_t>(ctx, mvcnt.p, mvoff.p, K + 1);
     int64_t NMV = 0;
