@@ -159,7 +159,7 @@ __device__ __forceinline__ void tail_range(const CommitArgs &A, int32_t i, int32
 // speculative evaluation against the snapshot (one warp per accepted candidate; tails of
 // more than BIG_TAIL members are listed for k_spec_big)
 __global__ void k_spec(CommitArgs A, int64_t K, const int32_t *status, CandSpec *spec,
-                       int32_t *big, int32_t *nbig, int64_t *vol_out) {
+                       int32_t *big, int32_t *nbig, int64_t *vol_out, int64_t big_vol) {
     const int lane = threadIdx.x & 31;
     int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -179,7 +179,7 @@ __global__ void k_spec(CommitArgs A, int64_t K, const int32_t *status, CandSpec 
             }
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) vol += __shfl_xor_sync(0xffffffffu, vol, off);
-            isbig = vol > BIG_VOL;
+            isbig = vol > big_vol;
             if (lane == 0) vol_out[k] = vol;   // capacity of its moving-neighbour list
         }
         if (isbig) {
@@ -443,6 +443,250 @@ __global__ void __launch_bounds__(SPEC_BLOCK) k_mv_scan_big(CommitArgs A, const 
         }
         __syncthreads();
     }
+}
+
+// ---- big candidates on integer-weight graphs, cut into work items of BIG_CH entries so that
+// a coarse-level hub candidate (rows of ~10^6 entries) is spread over the whole GPU instead
+// of one CTA.  Items: chunks of the tail members' rows (x >= 0) and of row i itself (x < 0,
+// the attach target).  Tail sums are accumulated with fp64 atomics -- exact, since every
+// partial sum is an integer below 2^53 -- and the attach target is reduced from per-item
+// (gain, entry) partials with the reference's first-maximum rule.
+constexpr int64_t BIG_CH = 4096;
+struct BigItem {
+    int32_t b, x;
+    int64_t e0, e1;
+};
+__global__ void __launch_bounds__(256) k_big_count(CommitArgs A, const int32_t *big,
+                                                   const int32_t *nbig, int64_t *cnt) {
+    __shared__ unsigned long long s_c;
+    const int32_t nb = *nbig;
+    for (int32_t b = blockIdx.x; b < nb; b += gridDim.x) {
+        const int32_t k = big[b];
+        const int32_t i = A.cand[k], frm = A.comm[i];
+        int32_t lo, hi;
+        tail_range(A, i, frm, lo, hi);
+        if (threadIdx.x == 0) s_c = 0;
+        __syncthreads();
+        unsigned long long c = 0;
+        for (int32_t q = lo + threadIdx.x; q < hi; q += blockDim.x) {
+            const int32_t x = A.order[q];
+            c += (unsigned long long)((A.uptr[x + 1] - A.uptr[x] + BIG_CH - 1) / BIG_CH);
+        }
+        if (threadIdx.x == 0) c += (unsigned long long)((A.uptr[i + 1] - A.uptr[i] + BIG_CH - 1) / BIG_CH);
+        atomicAdd(&s_c, c);
+        __syncthreads();
+        if (threadIdx.x == 0) cnt[b] = (int64_t)s_c;
+        __syncthreads();
+    }
+}
+__global__ void __launch_bounds__(256) k_big_fill(CommitArgs A, const int32_t *big,
+                                                  const int32_t *nbig, const int64_t *off,
+                                                  BigItem *items, int64_t *ri_off, int32_t *ri_cnt) {
+    __shared__ unsigned long long s_pos;
+    const int32_t nb = *nbig;
+    for (int32_t b = blockIdx.x; b < nb; b += gridDim.x) {
+        const int32_t k = big[b];
+        const int32_t i = A.cand[k], frm = A.comm[i];
+        int32_t lo, hi;
+        tail_range(A, i, frm, lo, hi);
+        if (threadIdx.x == 0) {
+            // row i's chunks first (a contiguous range: the attach partials of b)
+            const int64_t e0 = A.uptr[i], e1 = A.uptr[i + 1];
+            int32_t t = 0;
+            for (int64_t e = e0; e < e1; e += BIG_CH, t++)
+                items[off[b] + t] = BigItem{b, -1, e, min(e1, e + BIG_CH)};
+            ri_off[b] = off[b];
+            ri_cnt[b] = t;
+            s_pos = (unsigned long long)(off[b] + t);
+        }
+        __syncthreads();
+        for (int32_t q = lo + threadIdx.x; q < hi; q += blockDim.x) {
+            const int32_t x = A.order[q];
+            const int64_t e0 = A.uptr[x], e1 = A.uptr[x + 1];
+            const int64_t nch = (e1 - e0 + BIG_CH - 1) / BIG_CH;
+            if (!nch) continue;
+            const int64_t p = (int64_t)atomicAdd(&s_pos, (unsigned long long)nch);
+            for (int64_t t = 0; t < nch; t++)
+                items[p + t] = BigItem{b, x, e0 + t * BIG_CH, min(e1, e0 + (t + 1) * BIG_CH)};
+        }
+        __syncthreads();
+    }
+}
+// one warp per item: tail chunks accumulate w_to / w_from, row-i chunks give attach partials
+__global__ void k_big_items_spec(CommitArgs A, const int32_t *big, const BigItem *items,
+                                 int64_t nit, double *acc_wt, double *acc_wf, double *part_bt,
+                                 int64_t *part_be) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t it = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; it < nit;
+         it += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const BigItem I = items[it];
+        const int32_t k = big[I.b];
+        const int32_t i = A.cand[k], frm = A.comm[i], to = A.cstar[i];
+        if (I.x >= 0) {
+            int32_t lo, hi;
+            tail_range(A, i, frm, lo, hi);
+            const int32_t base = A.cptr[frm], plo = lo - base, phi = hi - base;
+            double wt = 0.0, wf = 0.0;
+            for (int64_t e = I.e0 + lane; e < I.e1; e += 32) {
+                const int32_t z = A.unbr[e];
+                const int32_t cz = A.comm[z];
+                if (cz == to) wt += A.uu[e];
+                if (cz != frm) continue;
+                const int32_t pz = A.pos[z];
+                if (pz >= plo && pz < phi) continue;   // z inside the moved tail
+                wf += A.uu[e];
+            }
+            wt = warp_sum(wt);
+            wf = warp_sum(wf);
+            if (lane == 0) {
+                if (wt != 0.0) atomicAdd(acc_wt + I.b, wt);
+                if (wf != 0.0) atomicAdd(acc_wf + I.b, wf);
+            }
+        } else {
+            const double soi = A.s_out[i], sii = A.s_in[i];
+            double bt = -INFINITY;
+            int64_t be = INT64_MAX;
+            for (int64_t e = I.e0 + lane; e < I.e1; e += 32) {
+                const int32_t z = A.unbr[e];
+                if (A.comm[z] != to) continue;
+                const double pg = A.uu[e] / A.m - (soi * A.s_in[z] + sii * A.s_out[z]) / A.m2;
+                if (pg > bt) {
+                    bt = pg;
+                    be = e;
+                }
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double ot = __shfl_xor_sync(0xffffffffu, bt, off);
+                const int64_t oe = __shfl_xor_sync(0xffffffffu, be, off);
+                if (ot > bt || (ot == bt && oe < be)) {
+                    bt = ot;
+                    be = oe;
+                }
+            }
+            if (lane == 0) {
+                part_bt[it] = bt;
+                part_be[it] = be;
+            }
+        }
+    }
+}
+// one CTA per big candidate: tail strengths and volume, the item sums, the attach partials
+__global__ void __launch_bounds__(256) k_big_finish(CommitArgs A, const int32_t *big,
+                                                    const int32_t *nbig, const double *acc_wt,
+                                                    const double *acc_wf, const double *part_bt,
+                                                    const int64_t *part_be, const int64_t *ri_off,
+                                                    const int32_t *ri_cnt, CandSpec *spec,
+                                                    int64_t *vol_out) {
+    __shared__ double s_so[8], s_si[8];
+    __shared__ unsigned long long s_vol;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int32_t nb = *nbig;
+    for (int32_t b = blockIdx.x; b < nb; b += gridDim.x) {
+        const int32_t k = big[b];
+        const int32_t i = A.cand[k], frm = A.comm[i];
+        int32_t lo, hi;
+        tail_range(A, i, frm, lo, hi);
+        if (threadIdx.x == 0) s_vol = 0;
+        __syncthreads();
+        double so = 0.0, si = 0.0;
+        unsigned long long vol = 0;
+        for (int32_t q = lo + threadIdx.x; q < hi; q += blockDim.x) {
+            const int32_t x = A.order[q];
+            so += A.s_out[x];
+            si += A.s_in[x];
+            vol += (unsigned long long)(A.uptr[x + 1] - A.uptr[x]);
+        }
+        so = warp_sum(so);
+        si = warp_sum(si);
+        atomicAdd(&s_vol, vol);
+        if (lane == 0) {
+            s_so[wid] = so;
+            s_si[wid] = si;
+        }
+        __syncthreads();
+        if (wid == 0) {
+            so = warp_sum(lane < 8 ? s_so[lane] : 0.0);
+            si = warp_sum(lane < 8 ? s_si[lane] : 0.0);
+            double bt = -INFINITY;
+            int64_t be = INT64_MAX;
+            for (int32_t t = lane; t < ri_cnt[b]; t += 32) {
+                const double ot = part_bt[ri_off[b] + t];
+                const int64_t oe = part_be[ri_off[b] + t];
+                if (ot > bt || (ot == bt && oe < be)) {
+                    bt = ot;
+                    be = oe;
+                }
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double ot = __shfl_xor_sync(0xffffffffu, bt, off);
+                const int64_t oe = __shfl_xor_sync(0xffffffffu, be, off);
+                if (ot > bt || (ot == bt && oe < be)) {
+                    bt = ot;
+                    be = oe;
+                }
+            }
+            if (lane == 0) {
+                vol_out[k] = (int64_t)s_vol;
+                CandSpec c;
+                c.w_to = acc_wt[b];
+                c.w_from = acc_wf[b];
+                c.so_b = so;
+                c.si_b = si;
+                c.pgj = bt;
+                c.je = be != INT64_MAX ? be : -1;
+                c.mv_off = 0;
+                c.j = be != INT64_MAX ? A.unbr[be] : -1;
+                c.tail_lo = lo;
+                c.tail_hi = hi;
+                c.mv_cnt = -1;   // big: k_mv_scan leaves it to the big moving-neighbour scan
+                spec[k] = c;
+            }
+        }
+        __syncthreads();
+    }
+}
+// moving-neighbour entries of the big candidates' tail items (any order: re-pricing breaks ties
+// by entry index); per-candidate positions from a counter, mv_cnt set by k_big_mv_finish
+__global__ void k_big_items_mv(CommitArgs A, const int32_t *big, const BigItem *items, int64_t nit,
+                               const CandSpec *spec, const uint8_t *moving,
+                               unsigned long long *ctr, int32_t *mv_z, double *mv_u, int64_t *mv_e,
+                               uint8_t *mv_i) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t it = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; it < nit;
+         it += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const BigItem I = items[it];
+        if (I.x < 0) continue;
+        const int32_t k = big[I.b];
+        const int32_t i = A.cand[k], frm = A.comm[i];
+        const int64_t mo = spec[k].mv_off;
+        for (int64_t e0 = I.e0; e0 < I.e1; e0 += 32) {
+            const int64_t e = e0 + lane;
+            bool hit = false;
+            int32_t z = 0;
+            if (e < I.e1) {
+                z = A.unbr[e];
+                hit = moving[z] && A.comm[z] != frm;
+            }
+            const unsigned hm = __ballot_sync(0xffffffffu, hit);
+            if (!hm) continue;
+            unsigned long long at = 0;
+            if (lane == 0) at = atomicAdd(ctr + I.b, (unsigned long long)__popc(hm));
+            at = __shfl_sync(0xffffffffu, at, 0);
+            if (hit) {
+                const int64_t p = mo + (int64_t)at + __popc(hm & ((1u << lane) - 1));
+                mv_z[p] = z;
+                mv_u[p] = A.uu[e];
+                mv_e[p] = e;
+                mv_i[p] = (I.x == i);
+            }
+        }
+    }
+}
+__global__ void k_big_mv_finish(const int32_t *big, const int32_t *nbig,
+                                const unsigned long long *ctr, CandSpec *spec) {
+    GS_LOOP(b, *nbig) spec[big[b]].mv_cnt = (int32_t)ctr[b];
 }
 
 __global__ void k_mv_offsets(int64_t K, const int32_t *status, const int64_t *off, CandSpec *spec) {
@@ -1073,6 +1317,12 @@ struct CommitScratch {
     DBuf<double> gg;
     DBuf<int32_t> lf, lp, wlong;   // long timelines (CTA walkers)
     DBuf<uint8_t> cmode;
+    // big candidates as work items (integer-weight graphs)
+    DBuf<int64_t> bcnt, boff, ri_off, part_be;
+    DBuf<int32_t> ri_cnt;
+    DBuf<BigItem> bitems;
+    DBuf<double> acc_wt, acc_wf, part_bt;
+    DBuf<unsigned long long> bctr;
 };
 
 void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const int32_t *d_cstar,
@@ -1146,8 +1396,47 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     mvcnt.resize(K + 1);
     mvoff.resize(K + 1);
     CUDA_TRY(cudaMemsetAsync(mvcnt.p, 0, (K + 1) * 8, s));
-    k_spec<<<GW, 256, 0, s>>>(A, K, status.p, spec.p, big.p, nbig, mvcnt.p);
-    k_spec_big<<<148 * 4, SPEC_BLOCK, 0, s>>>(A, big.p, nbig, spec.p, mvcnt.p);
+    // (SLM_BIG_VOL overrides the volume threshold; tests force the big path onto small tails)
+    const char *bve = getenv("SLM_BIG_VOL");
+    const int64_t big_vol = bve ? std::max<int64_t>(1, atoll(bve)) : BIG_VOL;
+    k_spec<<<GW, 256, 0, s>>>(A, K, status.p, spec.p, big.p, nbig, mvcnt.p, big_vol);
+    // big candidates: work items over the whole GPU on integer-weight graphs (exact atomics),
+    // one CTA each otherwise
+    static const bool big_cta = getenv("SLM_BIG_CTA") != nullptr;
+    const bool big_items = G.integral && !big_cta;
+    int64_t NIT = 0;
+    int32_t hnbig = 0;
+    if (big_items) {
+        CUDA_TRY(cudaMemcpyAsync(&hnbig, nbig, 4, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    if (big_items && hnbig > 0) {
+        const unsigned GB_ = (unsigned)std::min<int64_t>(hnbig, 148 * 8);
+        CS.bcnt.resize(hnbig + 1);
+        CS.boff.resize(hnbig + 1);
+        CUDA_TRY(cudaMemsetAsync(CS.bcnt.p + hnbig, 0, 8, s));
+        k_big_count<<<GB_, 256, 0, s>>>(A, big.p, nbig, CS.bcnt.p);
+        cub_exclusive_sum<int64_t>(ctx, CS.bcnt.p, CS.boff.p, hnbig + 1);
+        CUDA_TRY(cudaMemcpyAsync(&NIT, CS.boff.p + hnbig, 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        CS.bitems.resize(std::max<int64_t>(1, NIT));
+        CS.ri_off.resize(hnbig);
+        CS.ri_cnt.resize(hnbig);
+        CS.acc_wt.resize(hnbig);
+        CS.acc_wf.resize(hnbig);
+        CS.part_bt.resize(std::max<int64_t>(1, NIT));
+        CS.part_be.resize(std::max<int64_t>(1, NIT));
+        CUDA_TRY(cudaMemsetAsync(CS.acc_wt.p, 0, hnbig * 8, s));
+        CUDA_TRY(cudaMemsetAsync(CS.acc_wf.p, 0, hnbig * 8, s));
+        k_big_fill<<<GB_, 256, 0, s>>>(A, big.p, nbig, CS.boff.p, CS.bitems.p, CS.ri_off.p,
+                                       CS.ri_cnt.p);
+        k_big_items_spec<<<grid_for(NIT * 32, 256, 148LL * 64), 256, 0, s>>>(
+            A, big.p, CS.bitems.p, NIT, CS.acc_wt.p, CS.acc_wf.p, CS.part_bt.p, CS.part_be.p);
+        k_big_finish<<<GB_, 256, 0, s>>>(A, big.p, nbig, CS.acc_wt.p, CS.acc_wf.p, CS.part_bt.p,
+                                         CS.part_be.p, CS.ri_off.p, CS.ri_cnt.p, spec.p, mvcnt.p);
+    } else if (!big_items) {
+        k_spec_big<<<148 * 4, SPEC_BLOCK, 0, s>>>(A, big.p, nbig, spec.p, mvcnt.p);
+    }
     stick();
     CUDA_TRY(cudaMemsetAsync(moving.p, 0, n, s));
     k_mark_moving<<<GW, 256, 0, s>>>(cand.p, F.comm.p, F.on_cycle.p, F.cptr.p, F.pos.p, F.sz.p,
@@ -1169,8 +1458,19 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     k_mv_offsets<<<grid_for(K, 256), 256, 0, s>>>(K, status.p, mvoff.p, spec.p);
     k_mv_scan<<<GW, 256, 0, s>>>(A, K, status.p, spec.p, moving.p, 1, nullptr, mv_z.p, mv_u.p,
                                  mv_e.p, mv_i.p);
-    k_mv_scan_big<<<148 * 4, SPEC_BLOCK, 0, s>>>(A, big.p, nbig, spec.p, moving.p, 1, nullptr,
-                                                 mv_z.p, mv_u.p, mv_e.p, mv_i.p);
+    if (big_items) {
+        if (hnbig > 0) {
+            CS.bctr.resize(hnbig);
+            CUDA_TRY(cudaMemsetAsync(CS.bctr.p, 0, hnbig * 8, s));
+            k_big_items_mv<<<grid_for(NIT * 32, 256, 148LL * 64), 256, 0, s>>>(
+                A, big.p, CS.bitems.p, NIT, spec.p, moving.p, CS.bctr.p, mv_z.p, mv_u.p, mv_e.p,
+                mv_i.p);
+            k_big_mv_finish<<<grid_for(hnbig, 256), 256, 0, s>>>(big.p, nbig, CS.bctr.p, spec.p);
+        }
+    } else {
+        k_mv_scan_big<<<148 * 4, SPEC_BLOCK, 0, s>>>(A, big.p, nbig, spec.p, moving.p, 1, nullptr,
+                                                     mv_z.p, mv_u.p, mv_e.p, mv_i.p);
+    }
     stick();
     // accepted candidates -> (community, k) pairs -> timelines
     DBuf<int32_t> &af = CS.af, &apos = CS.apos;

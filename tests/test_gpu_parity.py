@@ -397,3 +397,13 @@ def test_cta_walkers_full_run_parity(tmp_path):
     r = subprocess.run([sys.executable, str(script)], env=env, cwd=root, capture_output=True,
                        text=True)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_big_candidate_items_parity(slm, oracle, monkeypatch):
+    """Commit candidates whose tails hold many entries are priced by work items spread over
+    the GPU (integer weights: exact fp64 atomics).  Force every candidate with more than 8
+    tail entries onto that path and compare whole hierarchies with the oracle."""
+    from paper_1702_04645_b200 import generators as GN
+    monkeypatch.setenv("SLM_BIG_VOL", "8")
+    for n, s, d, w in (GN.rmat(13, 16, 1, 4), GN.rmat(12, 16, 0, 7), GN.generate("c1_sbm")):
+        _vs_oracle(slm, oracle, n, s, d, w)
