@@ -187,17 +187,35 @@ __global__ void k_spec(CommitArgs A, int64_t K, const int32_t *status, CandSpec 
             continue;
         }
         const int32_t plo = lo - base, phi = hi - base;
-        double so = 0.0, si = 0.0, wf = 0.0;
+        double so = 0.0, si = 0.0, wf = 0.0, wt = 0.0;
         for (int32_t q = lo + lane; q < hi; q += 32) {
             int32_t x = A.order[q];
             so += A.s_out[x];
             si += A.s_in[x];
         }
+        // one pass over the tail rows: w_from, w_to, and on row i the attach target
+        // (detector.py:440-454: first maximum in entry order)
+        const double soi = A.s_out[i], sii = A.s_in[i];
+        double bt = -INFINITY;
+        int64_t be = INT64_MAX;
         for (int32_t q = lo; q < hi; q++) {
-            int32_t x = A.order[q];
+            const int32_t x = A.order[q];
+            const bool xi = x == i;
             for (int64_t e = A.uptr[x] + lane; e < A.uptr[x + 1]; e += 32) {
-                int32_t z = A.unbr[e];
-                if (A.comm[z] != frm) continue;
+                const int32_t z = A.unbr[e];
+                const int32_t cz = A.comm[z];
+                if (cz == to) {
+                    const double u = A.uu[e];
+                    wt += u;
+                    if (xi) {
+                        const double pg = u / A.m - (soi * A.s_in[z] + sii * A.s_out[z]) / A.m2;
+                        if (pg > bt) {
+                            bt = pg;
+                            be = e;
+                        }
+                    }
+                }
+                if (cz != frm) continue;
                 int32_t pz = A.pos[z];
                 if (pz >= plo && pz < phi) continue;   // z inside the moved tail
                 wf += A.uu[e];
@@ -206,11 +224,19 @@ __global__ void k_spec(CommitArgs A, int64_t K, const int32_t *status, CandSpec 
         so = warp_sum(so);
         si = warp_sum(si);
         wf = warp_sum(wf);
-        double wt, pgj;
-        int32_t j;
-        int64_t je;
-        eval_to_side(A.uptr, A.unbr, A.uu, A.s_out, A.s_in, A.comm, A.order, lo, hi, i, to, A.m,
-                     A.m2, wt, j, &je, &pgj);
+        wt = warp_sum(wt);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double ot = __shfl_xor_sync(0xffffffffu, bt, off);
+            const int64_t oe = __shfl_xor_sync(0xffffffffu, be, off);
+            if (ot > bt || (ot == bt && oe < be)) {
+                bt = ot;
+                be = oe;
+            }
+        }
+        const double pgj = bt;
+        const int32_t j = be != INT64_MAX ? A.unbr[be] : -1;
+        const int64_t je = be != INT64_MAX ? be : -1;
         if (lane == 0) {
             CandSpec c;
             c.w_to = wt;
