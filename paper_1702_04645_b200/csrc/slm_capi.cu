@@ -302,6 +302,7 @@ static void new_level0(slm_ctx *ctx) {
     ctx->f.n = -1;
     ctx->f.agg_valid = ctx->f.layout_valid = false;
     ctx->plan_version = ~0ull;
+    ctx->wown_version = ~0ull;
 }
 
 extern "C" {
@@ -523,6 +524,7 @@ int slm_set_resolution(slm_ctx *ctx, double gamma) {
     SLM_REQUIRE(gamma > 0.0 && std::isfinite(gamma), SLM_EINVAL, "resolution must be > 0");
     ctx->gamma = gamma;
     ctx->plan_version = ~0ull;
+    ctx->wown_version = ~0ull;
     API_END
 }
 
@@ -726,16 +728,24 @@ int slm_maximal(slm_ctx *ctx, const slm_config *cfg, int64_t level, int64_t swee
     if (ctx->plan_version != F.version || ctx->cstar.n != (size_t)G.n) {
         ctx->cstar.resize(G.n);
         phase_mark(ctx, -1);
+        ctx->wown_version = ~0ull;
+        ctx->wown_fresh = false;
         run_plan(ctx, G, F, m, ctx->cstar.p);
         phase_mark(ctx, PH_PLAN);
         ctx->plan_version = F.version;
+        if (ctx->wown_fresh) ctx->wown_version = F.version;   // the view sweep wrote it
     }
     int imp = 0;
     int64_t app = 0;
     std::vector<double> gains;
+    const bool keep_wown = ctx->wown_version == F.version && G.u32_ok;
     run_commit(ctx, G, F, m, ctx->cstar.p, cfg->seed, cfg->accept_prob, level, sweep, &imp, &app,
-               gains_out ? &gains : nullptr);
-    if (app) forest_refresh(ctx, G, F);
+               gains_out ? &gains : nullptr, keep_wown ? ctx->wown.p : nullptr);
+    if (app) {
+        forest_refresh(ctx, G, F);
+        // the commit carried wown over to the new partition (same components, new ids)
+        ctx->wown_version = keep_wown ? F.version : ~0ull;
+    }
     if (improved) *improved = imp;
     if (applied) *applied = app;
     if (gains_out)
@@ -754,6 +764,7 @@ int slm_aggregate(slm_ctx *ctx) {
     ctx->f.n = -1;
     ctx->f.agg_valid = ctx->f.layout_valid = false;
     ctx->plan_version = ~0ull;
+    ctx->wown_version = ~0ull;
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     API_END
 }

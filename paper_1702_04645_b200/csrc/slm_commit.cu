@@ -1353,7 +1353,7 @@ struct CommitScratch {
 
 void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const int32_t *d_cstar,
                 uint64_t seed, double accept_prob, int64_t level, int64_t sweep, int *improved,
-                int64_t *applied, std::vector<double> *gains) {
+                int64_t *applied, std::vector<double> *gains, uint32_t *wown) {
     cudaStream_t s = ctx->stream;
     static CommitScratch CS;
     const int64_t n = G.n, nc = F.n_comms;
@@ -1683,6 +1683,8 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     CUDA_TRY(cudaStreamSynchronize(s));
     *applied = hv[0];
     *improved = (hv[0] > 0) || hv[1];
+    // own-community sums follow the moved nodes (F.comm: labels before the commit, lab: after)
+    if (wown && hv[0] > 0) commit_wown_deltas(ctx, G, F.comm.p, CS.lab.p, wown);
     if (gains && hv[0] > 0) {
         DBuf<double> &gg = CS.gg;
         gg.resize(hv[0]);
@@ -1691,6 +1693,60 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
         CUDA_TRY(cudaMemcpyAsync(gains->data(), gg.p, hv[0] * 8, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
     }
+}
+
+// ---- own-community group sums across a commit: w_own[z] changes only for the neighbours of
+// moved nodes (a move a -> b of v takes u(z, v) from z's sum when z sits in a, adds it when z
+// sits in b); a moved node's sum is recomputed over its row.  uint32 wrap-around arithmetic is
+// exact whatever the order of the atomic updates.
+__global__ void k_wown_flags(const int32_t *pre, const int32_t *post, int64_t n, int32_t *f) {
+    GS_LOOP(i, n) f[i] = pre[i] != post[i] ? 1 : 0;
+}
+__global__ void k_wown_list(const int32_t *f, const int32_t *pos, int64_t n, int32_t *list) {
+    GS_LOOP(i, n) if (f[i]) list[pos[i]] = (int32_t)i;
+}
+__global__ void k_wown_delta(const int64_t *uptr, const int32_t *unbr, const uint32_t *u32,
+                             const int32_t *pre, const int32_t *post, const int32_t *moved,
+                             const int32_t *list, int64_t nm, uint32_t *wown) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; q < nm;
+         q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int32_t v = list[q];
+        const int32_t a = pre[v], b = post[v];
+        uint32_t own = 0;
+        for (int64_t e = uptr[v] + lane; e < uptr[v + 1]; e += 32) {
+            const int32_t z = unbr[e];
+            const uint32_t u = u32[e];
+            const int32_t pz = post[z];
+            if (pz == b) own += u;
+            if (moved[z]) continue;   // recomputed by its own warp
+            if (pz == a) atomicSub(wown + z, u);
+            else if (pz == b) atomicAdd(wown + z, u);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) own += __shfl_xor_sync(0xffffffffu, own, off);
+        if (lane == 0) wown[v] = own;
+    }
+}
+void commit_wown_deltas(slm_ctx *ctx, const LevelGraph &G, const int32_t *pre, const int32_t *post,
+                        uint32_t *wown) {
+    cudaStream_t s = ctx->stream;
+    const int64_t n = G.n;
+    static DBuf<int32_t> f, pos, list;   // grow-only scratch kept across calls
+    f.resize(n + 1);
+    pos.resize(n + 1);
+    CUDA_TRY(cudaMemsetAsync(f.p + n, 0, 4, s));
+    k_wown_flags<<<grid_for(n, 256), 256, 0, s>>>(pre, post, n, f.p);
+    cub_exclusive_sum<int32_t>(ctx, f.p, pos.p, n + 1);
+    int32_t nm = 0;
+    CUDA_TRY(cudaMemcpyAsync(&nm, pos.p + n, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (nm == 0) return;
+    list.resize(nm);
+    k_wown_list<<<grid_for(n, 256), 256, 0, s>>>(f.p, pos.p, n, list.p);
+    k_wown_delta<<<grid_for((int64_t)nm * 32, 256), 256, 0, s>>>(G.uptr.p, G.unbr.p, G.uu32.p, pre,
+                                                                post, f.p, list.p, nm, wown);
+    CUDA_TRY(cudaGetLastError());
 }
 
 // a kernel of this translation unit (module preloading, slm_capi.cu preload_modules)

@@ -101,6 +101,7 @@ constexpr int64_t HUB_BIG_DEG = 32768;   // hub rows spread over CTAs by segment
 
 struct SweepView;
 struct slm_ctx;
+struct Forest;
 
 // Canonical directed CSR + neighbour union + strengths of one hierarchy level
 // (graph.py:63-175, 257-263).  Node ids int32, entry offsets int64.
@@ -150,9 +151,14 @@ struct SweepView {
     LevelGraph V;                 // n, ue, uptr, unbr (view ids), uu32, s_out / s2, bins, hubs
     DBuf<int32_t> order;          // view row k -> node
     DBuf<int32_t> vlabel, vcstar; // per sweep: labels and targets in view order
+    DBuf<uint32_t> vwown;         // per sweep: own-community group sums in view order
 };
 SweepView &ensure_sweep_view(slm_ctx *ctx, const LevelGraph &G);
 void view_gather_labels(slm_ctx *ctx, SweepView &W, const int32_t *label);   // vlabel = label[order]
+void run_local_gains_wown(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
+                          const uint32_t *wown, double *d_lg, uint8_t *d_bad);
+void commit_wown_deltas(slm_ctx *ctx, const LevelGraph &G, const int32_t *pre, const int32_t *post,
+                        uint32_t *wown);
 void build_bins(slm_ctx *ctx, LevelGraph &G);
 
 // Assignment forest + derived community structure (forest.py:23-67, quality.py:52-79).
@@ -192,6 +198,12 @@ struct slm_ctx {
     // plan cache (exact fast-forward of coin-only sweeps)
     DBuf<int32_t> cstar;
     uint64_t plan_version = ~0ull;
+    // own-community group sum per node (integer sweep by-product, node order) and the forest
+    // version it is exact for: POSITIVE's local gains reuse it, kept exact across a commit by
+    // deltas over the moved nodes' rows (~0: invalid)
+    DBuf<uint32_t> wown;
+    uint64_t wown_version = ~0ull;
+    bool wown_fresh = false;   // set by the view sweep that just wrote wown
     // scratch
     DBuf<uint8_t> tmp;           // CUB temp storage
     DBuf<int64_t> i64a, i64b;
@@ -347,7 +359,7 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
                   int64_t *splits, int64_t *unresolved, int *changed, std::vector<double> *gains);
 void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const int32_t *d_cstar,
                 uint64_t seed, double accept_prob, int64_t level, int64_t sweep, int *improved,
-                int64_t *applied, std::vector<double> *gains);
+                int64_t *applied, std::vector<double> *gains, uint32_t *wown = nullptr);
 void run_aggregate(slm_ctx *ctx, const LevelGraph &G, const int32_t *d_labels, int64_t n_comms,
                    LevelGraph &out);
 double run_score(slm_ctx *ctx, const LevelGraph &G, const int32_t *d_labels, double gamma);

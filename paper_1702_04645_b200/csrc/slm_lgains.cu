@@ -214,3 +214,29 @@ void run_local_gains_u32(slm_ctx *ctx, const LevelGraph &G_, Forest &F, double m
 
 // a kernel of this translation unit (module preloading, slm_capi.cu preload_modules)
 const void *slm_anchor_lgains() { return (const void *)k_lg_small; }
+
+// local gains from the own-community sums the integer sweep left (ctx->wown, kept exact across
+// commits): one pass over the nodes instead of one over the union
+__global__ void k_lg_wown(LGArgs A, const uint32_t *wown, int64_t n) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x)
+        lg_finish(A, (int32_t)r, A.label[r], wown[r]);
+}
+void run_local_gains_wown(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
+                          const uint32_t *wown, double *d_lg, uint8_t *d_bad) {
+    LGArgs A;
+    A.uptr = G.uptr.p;
+    A.unbr = G.unbr.p;
+    A.u32 = G.uu32.p;
+    A.label = F.comm.p;
+    A.S_out = F.S_out.p;
+    A.S_in = F.S_in.p;
+    A.s_out = G.s_out.p;
+    A.s_in = G.s_in.p;
+    A.m = m;
+    A.lg = d_lg;
+    A.bad = d_bad;
+    A.order = nullptr;
+    if (G.n) k_lg_wown<<<grid_for(G.n, 256), 256, 0, ctx->stream>>>(A, wown, G.n);
+    CUDA_TRY(cudaGetLastError());
+}

@@ -1295,7 +1295,11 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     static DBuf<uint8_t> bad;   // grow-only scratch kept across calls
     bad.resize(nc);
     CUDA_TRY(cudaMemsetAsync(bad.p, 0, nc, s));
-    run_local_gains(ctx, G, F, m, nullptr, bad.p);
+    static const bool no_wown = getenv("SLM_WOWN") && atoi(getenv("SLM_WOWN")) == 0;
+    if (!no_wown && ctx->wown_version == F.version && G.u32_ok && ctx->wown.n == (size_t)n)
+        run_local_gains_wown(ctx, G, F, m, ctx->wown.p, nullptr, bad.p);
+    else
+        run_local_gains(ctx, G, F, m, nullptr, bad.p);
     static DBuf<int32_t> f, pos, list;
     f.resize(nc + 1);
     pos.resize(nc + 1);

@@ -51,6 +51,7 @@ struct SweepArgs {
     double m, m2;
     float inv_mf, inv_m2f; // float(1/m), float(1/m^2) of the approximate pass
     int32_t *cstar;
+    uint32_t *wown;        // optional: each row's own-community group sum (0 without one)
     unsigned long long *groups;
     unsigned long long *stats;   // development counters (SLM_SWEEP_STATS): fallback rows / groups
 };
@@ -281,6 +282,7 @@ __global__ void __launch_bounds__(256) k_sweep_small(SweepArgs<SYM> A, const int
             const unsigned ol = om & rowbits;
             const uint32_t gown = __shfl_sync(0xffffffffu, gs, ol ? __ffs(ol) - 1 : lane);
             const int ncand = __popc(cm & rowbits);
+            if (A.wown && valid && lane == rlast) A.wown[rr] = ol ? gown : 0u;
             if (valid && LO == -INFINITY) {
                 if (lane == rlast) A.cstar[rr] = Lr;
             } else if (valid && ncand == 1) {
@@ -367,6 +369,7 @@ __global__ void __launch_bounds__(256) k_sweep_tiny(SweepArgs<SYM> A, const int3
             gs[k] = g;
         }
         if (A.groups) atomicAdd(A.groups, (unsigned long long)ng);
+        if (A.wown) A.wown[r] = hown ? gown : 0u;
         if (S.lo == -INFINITY) {
             A.cstar[r] = L;
         } else if (S.up2 < S.lo) {
@@ -741,6 +744,7 @@ __global__ void __launch_bounds__(WARPS * 32, 4) k_sweep_warp(SweepArgs<SYM> A, 
         const unsigned ob = __ballot_sync(0xffffffffu, hown);
         gown = __shfl_sync(0xffffffffu, gown, ob ? __ffs(ob) - 1 : 0);
         if (A.groups && lane == 0) atomicAdd(A.groups, (unsigned long long)no);
+        if (A.wown && lane == 0) A.wown[r] = ob ? gown : 0u;
         const float lo = warp_maxf(S.lo);
         if (lo == -INFINITY) {
             if (lane == 0) A.cstar[r] = L;
@@ -804,6 +808,7 @@ __device__ __forceinline__ void block_select(const SweepArgs<SYM> &A, const int2
     __syncthreads();
     cnt = __reduce_add_sync(0xffffffffu, lane < NW ? B.cnt[lane] : 0u);
     if (A.groups && threadIdx.x == 0) atomicAdd(A.groups, (unsigned long long)no);
+    if (A.wown && threadIdx.x == 0) A.wown[r] = B.hown ? B.gown : 0u;
     if (lo == -INFINITY) {
         if (threadIdx.x == 0) {
             A.cstar[r] = L;
@@ -1417,6 +1422,7 @@ __global__ void __launch_bounds__(HS_BLOCK, 1) k_sweep_hub_smem(SweepArgs<SYM> A
             cnt = __reduce_add_sync(0xffffffffu, lane < NW ? B.cnt[lane] : 0u);
             const uint32_t ng = s_cnt;
             if (A.groups && threadIdx.x == 0) atomicAdd(A.groups, (unsigned long long)ng);
+            if (A.wown && threadIdx.x == 0) A.wown[r] = B.hown ? B.gown : 0u;
             if (lo == -INFINITY) {
                 if (threadIdx.x == 0) A.cstar[r] = L;
             } else if (cnt == 1) {
@@ -1489,7 +1495,8 @@ static void set_smem(K kern, size_t bytes) {
 
 template <bool SYM>
 static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, const int32_t *label,
-                         double m, int32_t *d_cstar, int bin_mask, unsigned long long *d_groups) {
+                         double m, int32_t *d_cstar, int bin_mask, unsigned long long *d_groups,
+                         uint32_t *d_wown = nullptr) {
     cudaStream_t s = ctx->stream;
     SweepArgs<SYM> A;
     A.uptr = G.uptr.p;
@@ -1507,6 +1514,7 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, const int
     A.inv_mf = (float)(1.0 / m);
     A.inv_m2f = (float)(1.0 / (m * m));
     A.cstar = d_cstar;
+    A.wown = d_wown;
     A.groups = d_groups;
     static DBuf<unsigned long long> stats;
     A.stats = nullptr;
@@ -1666,19 +1674,23 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, const int
 }
 
 __global__ void k_view_labels(const int32_t *label, const int32_t *order, int64_t n,
-                              int32_t *vlabel, int32_t *vcstar) {
+                              int32_t *vlabel, int32_t *vcstar, uint32_t *vwown = nullptr) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
          k += (int64_t)gridDim.x * blockDim.x) {
         const int32_t l = label[order[k]];
         vlabel[k] = l;
         if (vcstar) vcstar[k] = l;   // rows without entries keep their label
+        if (vwown) vwown[k] = 0u;    // ... and have no own group
     }
 }
-__global__ void k_view_scatter(const int32_t *vcstar, const int32_t *order, int64_t n,
-                               int32_t *cstar) {
+__global__ void k_view_scatter(const int32_t *vcstar, const uint32_t *vwown, const int32_t *order,
+                               int64_t n, int32_t *cstar, uint32_t *wown) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-         k += (int64_t)gridDim.x * blockDim.x)
-        cstar[order[k]] = vcstar[k];
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = order[k];
+        cstar[v] = vcstar[k];
+        if (wown) wown[v] = vwown[k];
+    }
 }
 
 void view_gather_labels(slm_ctx *ctx, SweepView &W, const int32_t *label) {
@@ -1702,11 +1714,21 @@ void run_plan_u32(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_
     }
     SweepView &W = ensure_sweep_view(ctx, G);
     const LevelGraph &V = W.V;
+    // full sweeps also record every row's own-community group sum (POSITIVE's local gains)
+    const bool full = bin_mask == 127;
+    uint32_t *vw = nullptr;
+    if (full) {
+        W.vwown.resize(G.n);
+        ctx->wown.resize(G.n);
+        vw = W.vwown.p;
+    }
     k_view_labels<<<grid_for(G.n, 256), 256, 0, s>>>(F.comm.p, W.order.p, G.n, W.vlabel.p,
-                                                     (bin_mask & 64) ? W.vcstar.p : nullptr);
-    if (V.sym) launch_sweep<true>(ctx, V, F, W.vlabel.p, m, W.vcstar.p, bin_mask, d_groups);
-    else launch_sweep<false>(ctx, V, F, W.vlabel.p, m, W.vcstar.p, bin_mask, d_groups);
-    k_view_scatter<<<grid_for(G.n, 256), 256, 0, s>>>(W.vcstar.p, W.order.p, G.n, d_cstar);
+                                                     (bin_mask & 64) ? W.vcstar.p : nullptr, vw);
+    if (V.sym) launch_sweep<true>(ctx, V, F, W.vlabel.p, m, W.vcstar.p, bin_mask, d_groups, vw);
+    else launch_sweep<false>(ctx, V, F, W.vlabel.p, m, W.vcstar.p, bin_mask, d_groups, vw);
+    k_view_scatter<<<grid_for(G.n, 256), 256, 0, s>>>(W.vcstar.p, vw, W.order.p, G.n, d_cstar,
+                                                      full ? ctx->wown.p : nullptr);
+    ctx->wown_fresh = full;
 }
 
 // ---------------------------------------------------------------- diagnostics

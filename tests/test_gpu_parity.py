@@ -407,3 +407,34 @@ def test_big_candidate_items_parity(slm, oracle, monkeypatch):
     monkeypatch.setenv("SLM_BIG_VOL", "8")
     for n, s, d, w in (GN.rmat(13, 16, 1, 4), GN.rmat(12, 16, 0, 7), GN.generate("c1_sbm")):
         _vs_oracle(slm, oracle, n, s, d, w)
+
+
+def test_local_gains_without_wown_matches(tmp_path):
+    """POSITIVE's local gains from the sweep's own-community sums (kept across commits by
+    deltas; default) and from a full pass over the union (SLM_WOWN=0) give the same
+    hierarchies."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "wown.py"
+    script.write_text(
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {root!r})\n"
+        "import paper_1702_04645_b200 as slm\n"
+        "from paper_1702_04645_b200 import generators as GN\n"
+        "out = []\n"
+        "for n, s, d, w in (GN.rmat(14, 16, 1, 4), GN.rgg(1 << 14, 8.0, 3)):\n"
+        "    r = slm.run(slm.Graph.from_edges(n, s, d, w), slm.RunConfig())\n"
+        "    out += list(r.hierarchy.levels) + [np.array(r.stats.sweeps_per_level),\n"
+        "            np.array([r.stats.accepted_moves, r.stats.accepted_splits, r.stats.unresolved_negative])]\n"
+        "np.savez(sys.argv[1], *out)\n")
+    res = {}
+    for mode in ("1", "0"):
+        f = tmp_path / f"w{mode}.npz"
+        subprocess.run([sys.executable, str(script), str(f)], check=True, cwd=root,
+                       env=dict(os.environ, SLM_WOWN=mode))
+        res[mode] = np.load(f)
+    assert res["1"].files == res["0"].files
+    for k in res["1"].files:
+        np.testing.assert_array_equal(res["1"][k], res["0"][k])
