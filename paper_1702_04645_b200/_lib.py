@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libslm.so")
+LIB_PATH = os.environ.get("SLM_LIB_PATH") or os.path.join(_HERE, "libslm.so")   # (override: A/B runs)
 
 SLM_OK, SLM_EINVAL, SLM_ECUDA, SLM_ENOMEM, SLM_ESTATE, SLM_EUNSUP = 0, -1, -2, -3, -4, -5
 
