@@ -828,6 +828,7 @@ struct Live {
     int32_t *first_commit;
     int32_t *a;
     int32_t *wpos, *atk;
+    int2 *wwait;             // per walker: what a parked walker waits for ({k, frm} or {-1, -1})
     const int32_t *tl_ptr, *tl_ev;
     const int4 *tl_rec;      // per timeline event: {k, i, frm, to}
     MvList mv;
@@ -1025,9 +1026,16 @@ __device__ __forceinline__ int walk_batch(const CommitArgs &A, const Live &V, in
         const int cf = __shfl_sync(0xffffffffu, cls, f);
         const int32_t kf = __shfl_sync(0xffffffffu, e.k, f);
         if (cf == C_WAIT) {
-            if (lane == 0 && W.my_atk != kf) {
-                __threadfence();
-                *(volatile int32_t *)(V.atk + C) = kf;
+            // what unblocks it: the verdict on kf (C is its source), or kf's source walker
+            // parking at kf / turning dirty (C is its target)
+            const int32_t tf = __shfl_sync(0xffffffffu, e.to, f);
+            const int32_t ff = __shfl_sync(0xffffffffu, e.frm, f);
+            if (lane == 0) {
+                if (W.my_atk != kf) {
+                    __threadfence();
+                    *(volatile int32_t *)(V.atk + C) = kf;
+                }
+                V.wwait[C] = make_int2(kf, tf == C ? ff : -1);
             }
             W.my_atk = kf;
             parked = true;
@@ -1250,6 +1258,18 @@ __global__ void __launch_bounds__(WALK_BLOCK) k_walk(CommitArgs A, Live V, const
         int32_t p = V.wpos[C];
         const int32_t end = V.tl_ptr[C + 1];
         if (p >= end) continue;
+        {   // a parked walker whose wait still holds is skipped without a visit
+            const int2 ww = V.wwait[C];
+            if (ww.x >= 0) {
+                const bool blocked =
+                    ww.y < 0 ? ld_acq(status + ww.x) == ST_UNRES
+                             : (ld_acq(V.atk + ww.y) != ww.x && !vload8(V.dirty + ww.y));
+                if (blocked) {
+                    pending = 1;
+                    continue;
+                }
+            }
+        }
         __threadfence();
         WalkState W;
         walk_state_load(V, C, W);
@@ -1342,6 +1362,7 @@ struct CommitScratch {
     DBuf<int32_t> cf, cpos;
     DBuf<double> gg;
     DBuf<int32_t> lf, lp, wlong;   // long timelines (CTA walkers)
+    DBuf<int2> wwait;
     DBuf<uint8_t> cmode;
     // big candidates as work items (integer-weight graphs)
     DBuf<int64_t> bcnt, boff, ri_off, part_be;
@@ -1550,6 +1571,8 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
         wp.resize(nc + 1);
         wpos.resize(nc);
         atk.resize(nc);
+        CS.wwait.resize(nc);
+        CUDA_TRY(cudaMemsetAsync(CS.wwait.p, 0xff, nc * sizeof(int2), s));   // {-1, -1}
         CUDA_TRY(cudaMemsetAsync(wf.p + nc, 0, 4, s));
         k_walker_list<<<grid_for(nc, 256), 256, 0, s>>>(tl_ptr.p, nc, wf.p);
         cub_exclusive_sum<int32_t>(ctx, wf.p, wp.p, nc + 1);
@@ -1571,6 +1594,7 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
         V.a = F.a.p;   // committed pointers are written in place (tails come from the layout)
         V.wpos = wpos.p;
         V.atk = atk.p;
+        V.wwait = CS.wwait.p;
         V.tl_ptr = tl_ptr.p;
         V.tl_ev = tl_ev.p;
         V.tl_rec = CS.tl_rec.p;
