@@ -156,6 +156,36 @@ void *dcache_alloc(size_t bytes, size_t *got) {
     return p;
 }
 static std::atomic<int> g_live_ctx{0};
+
+// DBuf registry: constructed on first use (file-scope static DBufs of other translation units
+// are built during static initialisation) and never destroyed
+struct DbufRegistry {
+    std::mutex mu;
+    std::unordered_map<void *, void (*)(void *)> live;
+};
+static DbufRegistry &dbuf_registry() {
+    static DbufRegistry *r = new DbufRegistry;
+    return *r;
+}
+void dbuf_track(void *self, void (*rel)(void *)) {
+    DbufRegistry &R = dbuf_registry();
+    std::lock_guard<std::mutex> lk(R.mu);
+    R.live[self] = rel;
+}
+void dbuf_untrack(void *self) {
+    DbufRegistry &R = dbuf_registry();
+    std::lock_guard<std::mutex> lk(R.mu);
+    R.live.erase(self);
+}
+void dbuf_release_all() {
+    DbufRegistry &R = dbuf_registry();
+    std::vector<std::pair<void *, void (*)(void *)>> all;
+    {
+        std::lock_guard<std::mutex> lk(R.mu);
+        all.assign(R.live.begin(), R.live.end());
+    }
+    for (auto &kv : all) kv.second(kv.first);
+}
 void dcache_free(void *p, size_t bytes) {
     // Every kernel and copy of a context runs on its one stream, so a block released while
     // queued work still uses it is only handed to later work of the same stream (ordered
@@ -380,7 +410,8 @@ void slm_destroy(slm_ctx *ctx) {
     }
     cudaStreamDestroy(ctx->stream);
     delete ctx;
-    g_live_ctx--;
+    // the last context: the static scratch kept across calls goes back to the arena too
+    if (--g_live_ctx == 0) dbuf_release_all();
 }
 
 const char *slm_last_error(slm_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }

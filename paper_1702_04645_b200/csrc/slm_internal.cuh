@@ -49,16 +49,24 @@ double dbuf_now_ms();
 void *dcache_alloc(size_t bytes, size_t *got);
 void dcache_free(void *p, size_t bytes);
 void dcache_reserve(int device);
+// every live DBuf is tracked, so the grow-only scratch kept in static DBufs across calls can be
+// returned to the arena when the last context goes away (slm_destroy)
+void dbuf_track(void *self, void (*rel)(void *));
+void dbuf_untrack(void *self);
+void dbuf_release_all();
 
 template <class T>
 struct DBuf {
     T *p = nullptr;
     size_t n = 0;     // logical length
     size_t cap = 0;   // allocated elements
-    DBuf() = default;
+    DBuf() { dbuf_track(this, [](void *self) { static_cast<DBuf *>(self)->release(); }); }
     DBuf(const DBuf &) = delete;
     DBuf &operator=(const DBuf &) = delete;
-    ~DBuf() { release(); }
+    ~DBuf() {
+        release();
+        dbuf_untrack(this);
+    }
     void release() {
         if (p) dcache_free(p, cap * sizeof(T));
         p = nullptr;
