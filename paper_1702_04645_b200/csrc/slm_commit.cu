@@ -811,12 +811,25 @@ __global__ void k_ev_rec(const int32_t *ev, int64_t m, const int32_t *cand, cons
 __global__ void k_walker_list(const int32_t *tl_ptr, int64_t nc, int32_t *f) {
     GS_LOOP(c, nc) f[c] = tl_ptr[c + 1] > tl_ptr[c] ? 1 : 0;
 }
+// walker list and initial walker state.  A walker whose first event moves a candidate out of
+// its community starts parked at that event (atk = k): its state is the initial one, exactly
+// what its first visit would publish, so the target's walker can evaluate the event at once
+// instead of waiting for that visit (a hub community's timeline is mostly such events).
 __global__ void k_walker_scatter(const int32_t *f, const int32_t *pos, const int32_t *tl_ptr,
-                                 int64_t nc, int32_t *wl, int32_t *wpos, int32_t *atk) {
+                                 const int4 *tl_rec, int64_t nc, int32_t *wl, int32_t *wpos,
+                                 int32_t *atk, int2 *wwait) {
     GS_LOOP(c, nc) {
-        if (f[c]) wl[pos[c]] = (int32_t)c;
+        int32_t at = 0x7fffffff;
+        if (f[c]) {
+            wl[pos[c]] = (int32_t)c;
+            const int4 r = tl_rec[tl_ptr[c]];
+            if (r.w != (int32_t)c) {   // first event: c is its source
+                at = r.x;
+                wwait[c] = make_int2(r.x, -1);
+            }
+        }
         wpos[c] = tl_ptr[c];
-        atk[c] = 0x7fffffff;
+        atk[c] = at;
     }
 }
 
@@ -901,6 +914,7 @@ struct WalkState {
     double SoC, SiC;
     int32_t cntC, my_atk;
     int dirtyC;
+    int win;   // classification window: events classified per round (adapts to barrier density)
 };
 
 // one event as a lane sees it
@@ -1010,19 +1024,28 @@ __device__ __forceinline__ int walk_batch(const CommitArgs &A, const Live &V, in
     walk_load(V, status, spec, C, lane < nb, rec, e);
     int start = 0;
     while (start < nb) {
-        // ---- classify events [start, nb) against the current state
-        const bool act = lane >= start && lane < nb;
+        // ---- classify events [start, hi) against the current state.  Every event after a
+        // state change is classified again, so dense stretches of commits (a hub community
+        // absorbing most of a sweep's candidates) shrink the window instead of re-pricing the
+        // whole batch after each commit
+        const int hi = min(nb, start + W.win);
+        const bool act = lane >= start && lane < hi;
         int cls = C_PASS;
         double gq = 0.0, wtq = 0.0;
         int32_t jq = -1;
         if (act) cls = walk_classify(A, V, status, C, W, e, gq, wtq, jq);
         // ---- skips before the first state-changing event
         const unsigned bar = __ballot_sync(0xffffffffu, act && cls >= C_COMMIT);
-        const int f = bar ? __ffs(bar) - 1 : nb;
+        const int f = bar ? __ffs(bar) - 1 : hi;
         const bool sk = act && lane < f && cls == C_SKIP;
         if (sk) *(volatile int32_t *)(status + e.k) = ST_SKIP;
         nres += __popc(__ballot_sync(0xffffffffu, sk));
-        if (f >= nb) break;
+        if (f >= hi) {   // no state change in the window
+            W.win = min(32, W.win * 2);
+            start = hi;
+            continue;
+        }
+        W.win = (f - start) * 4 < W.win ? max(1, W.win >> 1) : min(32, W.win * 2);
         const int cf = __shfl_sync(0xffffffffu, cls, f);
         const int32_t kf = __shfl_sync(0xffffffffu, e.k, f);
         if (cf == C_WAIT) {
@@ -1128,6 +1151,7 @@ __device__ __forceinline__ void walk_state_load(const Live &V, int32_t C, WalkSt
     W.cntC = V.cnt[C];
     W.my_atk = V.atk[C];             // only this walker writes atk[C]
     W.dirtyC = vload8(V.dirty + C);  // monotone
+    W.win = 32;
 }
 
 // end of a visit: resolved count, position, and release of waiters when the timeline is done
@@ -1581,8 +1605,8 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
         CUDA_TRY(cudaStreamSynchronize(s));
         wl.resize(NW);
         stick();
-        k_walker_scatter<<<grid_for(nc, 256), 256, 0, s>>>(wf.p, wp.p, tl_ptr.p, nc, wl.p, wpos.p,
-                                                           atk.p);
+        k_walker_scatter<<<grid_for(nc, 256), 256, 0, s>>>(wf.p, wp.p, tl_ptr.p, CS.tl_rec.p, nc,
+                                                           wl.p, wpos.p, atk.p, CS.wwait.p);
         CUDA_TRY(cudaMemcpyAsync(remaining.p, &NA, 4, cudaMemcpyHostToDevice, s));
         Live V;
         V.lab = lab.p;

@@ -12,8 +12,10 @@ from paper_1702_04645_b200 import _lib, generators as GN, RunConfig
 def main():
     cfg_name = sys.argv[1] if len(sys.argv) > 1 else "c5_rmat24"
     max_level = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+    gamma = float(sys.argv[3]) if len(sys.argv) > 3 else 1.0
     ctx = _lib.Context(0)
     GN.build_on_device(ctx, cfg_name)
+    ctx.set_resolution(gamma)
     cfg = RunConfig()._c()
     level = 0
     while level <= max_level:
