@@ -998,9 +998,11 @@ __device__ __forceinline__ int walk_classify(const CommitArgs &A, const Live &V,
             const CandSpec &cs = e.cs;
             wtq = cs.w_to;
             jq = cs.j;
+            // long list, lost attach target, or a dense stretch of commits (small window: the
+            // event is priced by the whole warp rather than one lane): cooperative
             if (cs.mv_cnt > 0 && W.dirtyC &&
-                (cs.mv_cnt > 64 || !reprice_lane(A, V.mv, V.lab, cs, e.i, C, wtq, jq))) {
-                cls = C_COOP;   // long list or lost attach target: cooperative
+                (cs.mv_cnt > 64 || W.win <= 4 || !reprice_lane(A, V.mv, V.lab, cs, e.i, C, wtq, jq))) {
+                cls = C_COOP;
             } else {
                 const double so_b = cs.so_b, si_b = cs.si_b;
                 // gain_switch d_null (quality.py:216-219), exact operand order
