@@ -223,10 +223,16 @@ __global__ void k_row_seq_sum(const int64_t *ptr, const double *w, int64_t n, do
 }
 
 __global__ void k_pw_segments(const double *a, const int64_t *off, const int64_t *len, int64_t k,
-                              double *out) {
+                              double *out, uint32_t *nonint = nullptr) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k;
-         i += (int64_t)gridDim.x * blockDim.x)
+         i += (int64_t)gridDim.x * blockDim.x) {
         out[i] = pw_sum_seq(a + off[i], len[i]);
+        if (nonint) {   // integrality of the leaf's elements (their sums' exactness)
+            bool bad = false;
+            for (int64_t q = 0; q < len[i] && !bad; q++) bad = a[off[i] + q] != floor(a[off[i] + q]);
+            if (bad) atomicOr(nonint, 1u);
+        }
+    }
 }
 
 __global__ void k_degree_bins(const int64_t *uptr, int64_t n, int64_t *flags, int32_t *maxdeg) {
@@ -450,15 +456,6 @@ __global__ void k_long_ends(const uint64_t *keys, int64_t ne, const int64_t *run
         ends[q] = lo;
     }
 }
-__global__ void k_nonint_runs(const double *v, const int64_t *runs, const int64_t *ends,
-                              int32_t nruns, uint32_t *bad) {
-    for (int32_t q = blockIdx.x; q < nruns; q += gridDim.x)
-        for (int64_t e = runs[2 * q] + threadIdx.x; e < ends[q]; e += blockDim.x)
-            if (v[e] != floor(v[e])) {
-                atomicOr(bad, 1u);
-                break;
-            }
-}
 __global__ void k_scatter_sums(const int64_t *runs, const double *sums, int32_t nruns, double *w) {
     for (int32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nruns; q += gridDim.x * blockDim.x)
         w[runs[2 * q + 1]] = sums[q];
@@ -471,8 +468,6 @@ static void merge_long_runs(slm_ctx *ctx, const double *vals, const uint64_t *ke
     static DBuf<double> leaf, sums;
     ends.resize(nruns);
     k_long_ends<<<grid_for(nruns, 128), 128, 0, s>>>(keys, ne, d_runs, nruns, ends.p);
-    k_nonint_runs<<<(unsigned)std::min<int32_t>(nruns, 148 * 8), 256, 0, s>>>(vals, d_runs, ends.p,
-                                                                               nruns, bad);
     std::vector<int64_t> hr(2 * nruns), he(nruns);
     CUDA_TRY(cudaMemcpyAsync(hr.data(), d_runs, nruns * 16, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(he.data(), ends.p, nruns * 8, cudaMemcpyDeviceToHost, s));
@@ -491,7 +486,9 @@ static void merge_long_runs(slm_ctx *ctx, const double *vals, const uint64_t *ke
     leaf.resize(nl);
     CUDA_TRY(cudaMemcpyAsync(d_off.p, offs.data(), nl * 8, cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(d_len.p, lens.data(), nl * 8, cudaMemcpyHostToDevice, s));
-    k_pw_segments<<<grid_for(nl, 128), 128, 0, s>>>(vals, d_off.p, d_len.p, nl, leaf.p);
+    // (the leaves cover every element of the runs: their integrality is checked there, by
+    // the ~32K-element leaves in parallel, not one CTA per run)
+    k_pw_segments<<<grid_for(nl, 128), 128, 0, s>>>(vals, d_off.p, d_len.p, nl, leaf.p, bad);
     std::vector<double> hl(nl), hs(nruns);
     CUDA_TRY(cudaMemcpyAsync(hl.data(), leaf.p, nl * 8, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
