@@ -1734,7 +1734,10 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     *applied = hv[0];
     *improved = (hv[0] > 0) || hv[1];
     // own-community sums follow the moved nodes (F.comm: labels before the commit, lab: after)
-    if (wown && hv[0] > 0) commit_wown_deltas(ctx, G, F.comm.p, CS.lab.p, wown);
+    if (wown && hv[0] > 0) {
+        wown_to_node_order(ctx, G);
+        commit_wown_deltas(ctx, G, F.comm.p, CS.lab.p, wown);
+    }
     if (gains && hv[0] > 0) {
         DBuf<double> &gg = CS.gg;
         gg.resize(hv[0]);

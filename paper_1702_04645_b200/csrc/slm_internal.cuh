@@ -163,6 +163,7 @@ struct SweepView {
 };
 SweepView &ensure_sweep_view(slm_ctx *ctx, const LevelGraph &G);
 void view_gather_labels(slm_ctx *ctx, SweepView &W, const int32_t *label);   // vlabel = label[order]
+void wown_to_node_order(slm_ctx *ctx, const LevelGraph &G);   // scatter vwown -> ctx->wown if pending
 void run_local_gains_wown(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
                           const uint32_t *wown, double *d_lg, uint8_t *d_bad);
 void commit_wown_deltas(slm_ctx *ctx, const LevelGraph &G, const int32_t *pre, const int32_t *post,
@@ -212,6 +213,7 @@ struct slm_ctx {
     DBuf<uint32_t> wown;
     uint64_t wown_version = ~0ull;
     bool wown_fresh = false;   // set by the view sweep that just wrote wown
+    bool wown_in_view = false; // wown still in the sweep view's row order (vwown), not scattered
     // scratch
     DBuf<uint8_t> tmp;           // CUB temp storage
     DBuf<int64_t> i64a, i64b;

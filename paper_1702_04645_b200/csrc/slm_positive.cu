@@ -1296,8 +1296,10 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     bad.resize(nc);
     CUDA_TRY(cudaMemsetAsync(bad.p, 0, nc, s));
     static const bool no_wown = getenv("SLM_WOWN") && atoi(getenv("SLM_WOWN")) == 0;
-    if (!no_wown && ctx->wown_version == F.version && G.u32_ok && ctx->wown.n == (size_t)n)
+    if (!no_wown && ctx->wown_version == F.version && G.u32_ok && ctx->wown.n == (size_t)n) {
+        wown_to_node_order(ctx, G);
         run_local_gains_wown(ctx, G, F, m, ctx->wown.p, nullptr, bad.p);
+    }
     else
         run_local_gains(ctx, G, F, m, nullptr, bad.p);
     static DBuf<int32_t> f, pos, list;

@@ -1693,6 +1693,19 @@ __global__ void k_view_scatter(const int32_t *vcstar, const uint32_t *vwown, con
     }
 }
 
+__global__ void k_view_wown(const uint32_t *vwown, const int32_t *order, int64_t n, uint32_t *wown) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x)
+        wown[order[k]] = vwown[k];
+}
+void wown_to_node_order(slm_ctx *ctx, const LevelGraph &G) {
+    if (!ctx->wown_in_view || !G.view) return;
+    SweepView &W = *G.view;
+    k_view_wown<<<grid_for(G.n, 256), 256, 0, ctx->stream>>>(W.vwown.p, W.order.p, G.n,
+                                                             ctx->wown.p);
+    ctx->wown_in_view = false;
+}
+
 void view_gather_labels(slm_ctx *ctx, SweepView &W, const int32_t *label) {
     k_view_labels<<<grid_for(W.V.n, 256), 256, 0, ctx->stream>>>(label, W.order.p, W.V.n,
                                                                  W.vlabel.p, nullptr);
@@ -1726,9 +1739,12 @@ void run_plan_u32(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_
                                                      (bin_mask & 64) ? W.vcstar.p : nullptr, vw);
     if (V.sym) launch_sweep<true>(ctx, V, F, W.vlabel.p, m, W.vcstar.p, bin_mask, d_groups, vw);
     else launch_sweep<false>(ctx, V, F, W.vlabel.p, m, W.vcstar.p, bin_mask, d_groups, vw);
+    // targets back to node order; the own-community sums stay in view order until a commit
+    // or POSITIVE needs them (wown_to_node_order)
     k_view_scatter<<<grid_for(G.n, 256), 256, 0, s>>>(W.vcstar.p, vw, W.order.p, G.n, d_cstar,
-                                                      full ? ctx->wown.p : nullptr);
+                                                      nullptr);
     ctx->wown_fresh = full;
+    ctx->wown_in_view = full;
 }
 
 // ---------------------------------------------------------------- diagnostics
