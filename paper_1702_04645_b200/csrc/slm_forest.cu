@@ -116,6 +116,15 @@ __global__ void k_run_starts(const int32_t *sorted, int64_t m, int64_t nrows, in
     GS_LOOP(i, m) if (i == 0 || sorted[i] != sorted[i - 1]) ptr[sorted[i]] = (int32_t)i;
     if (blockIdx.x == 0 && threadIdx.x == 0) ptr[nrows] = (int32_t)m;
 }
+__global__ void k_lb_one(const int32_t *sorted, int64_t m, int32_t key, int32_t *out) {
+    int64_t lo = 0, hi = m;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (sorted[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    *out = (int32_t)lo;
+}
 __global__ void k_lb_ptr32(const int32_t *sorted, int64_t m, int64_t nrows, int32_t *ptr) {
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= nrows;
          r += (int64_t)gridDim.x * blockDim.x) {
@@ -448,7 +457,8 @@ void build_layout(slm_ctx *ctx, Forest &F) {
     k_kid_keys<<<grid_for(n, 256), 256, 0, s>>>(F.a.p, n, kk);
     k_iota<<<grid_for(n, 256), 256, 0, s>>>(iota, n);
     if (n > 0) sort_pairs_u32_i32(ctx, kk, ks, iota, F.kids.p, n, bits_for(n + 1));
-    k_lb_ptr32<<<grid_for(n + 1, 256), 256, 0, s>>>((const int32_t *)ks, n, n, F.kptr.p);
+    // only kptr[n] (the number of kids) is needed unless the DFS fallback below runs
+    k_lb_one<<<1, 1, 0, s>>>((const int32_t *)ks, n, (int32_t)n, F.kptr.p + n);
     // depth of every node below its community root (parent = a[x])
     int32_t *flags = ctx->i32d.resize(2);
     CUDA_TRY(cudaMemsetAsync(flags, 0, 8, s));
@@ -461,11 +471,14 @@ void build_layout(slm_ctx *ctx, Forest &F) {
     k_depth<<<grid_for(n, 256), 256, 0, s>>>(F.a.p, F.comm.p, F.croot.p, n, 4096, depth.p,
                                               iota2, flags);
     int32_t hf[2];
+    int32_t nk = 0;
     CUDA_TRY(cudaMemcpyAsync(hf, flags, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(&nk, F.kptr.p + n, 4, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     const int maxd = hf[1];
     if (hf[0]) {
-        // pathological depth (> 4096): sequential DFS per community
+        // pathological depth (> 4096): sequential DFS per community (needs the kids pointers)
+        k_lb_ptr32<<<grid_for(n + 1, 256), 256, 0, s>>>((const int32_t *)ks, n, n, F.kptr.p);
         int32_t *stk_node = ctx->i32a.resize(n);
         static DBuf<int32_t> stk_it;   // grow-only scratch kept across calls
         stk_it.resize(n);
@@ -496,9 +509,6 @@ void build_layout(slm_ctx *ctx, Forest &F) {
             k_size_level<<<grid_for(hi - lo, 256), 256, 0, s>>>(by_depth.p, lo, hi, F.a.p, F.sz.p);
     }
     // offsets among siblings (kids ascending, the root never a kid) and pre-order positions
-    int32_t nk = 0;
-    CUDA_TRY(cudaMemcpyAsync(&nk, F.kptr.p + n, 4, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
     static DBuf<int32_t> val, ex, offp;   // grow-only scratch kept across calls
     val.resize(nk);
     ex.resize(nk);
