@@ -114,7 +114,8 @@ SLM_API int slm_plan_sweep_async(slm_ctx *ctx, int32_t bin_mask);
 SLM_API int slm_plan_groups(slm_ctx *ctx, int64_t *groups, int64_t *bin_rows, int64_t *bin_entries);
 SLM_API int slm_get_cstar(slm_ctx *ctx, int64_t *cstar_out);
 /* Diagnostics: device ms of a pure stream of the union (mode 0), + neighbour-label gathers
- * (1), + community-strength gathers (2) -- the memory-system floor of the sweep. */
+ * (1), + community-strength gathers (2) -- the memory-system floor of the sweep; modes 3-5:
+ * the same over the degree-ordered sweep view. */
 SLM_API int slm_debug_sweep_floor(slm_ctx *ctx, int32_t mode, double *ms);
 /* maximal_correction (detector.py:457-521) for (level, sweep); gains_out nullable. */
 SLM_API int slm_maximal(slm_ctx *ctx, const slm_config *cfg, int64_t level, int64_t sweep,
