@@ -958,14 +958,14 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
             need_full = false;
             sec(1);
         }
-        // negative members: the previous ones (re-evaluated) plus the dirty ones
+        // negative members: the previous ones plus the dirty ones.  Only the dirty members (a
+        // cut lowered their w_part) can turn negative -- every other member's gain grows as
+        // the part shrinks -- so they are added to the list; whether any negative member is
+        // left is then decided by scanning the list only up to the first one still negative,
+        // and the exact count is taken only when no positive cut remains (detector.py:275-277)
         {
-            const int nn = s_nneg, nd = min(s_ndirty, DIRTY_CAP);
+            const int nd = min(s_ndirty, DIRTY_CAP);
             int c = 0;
-            for (int t = tid; t < nn; t += GB) {
-                const int32_t x = negl[t];
-                if (A.gmark[x] == pid && g_member(A, x, so_c, si_c) < 0.0) c++;
-            }
             for (int t = tid; t < nd; t += GB) {
                 const int32_t x = dirty[t];
                 if (A.gmark[x] == pid && !negflag[x] && g_member(A, x, so_c, si_c) < 0.0) {
@@ -974,7 +974,19 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
                     negl[atomicAdd(&s_nneg, 1)] = x;
                 }
             }
-            negc = block_sum_i(c, si);
+            __syncthreads();
+            const int nn = s_nneg;
+            int any = __syncthreads_or(c);
+            for (int base = 0; !any && base < nn; base += GB) {
+                const int t = base + tid;
+                bool neg = false;
+                if (t < nn) {
+                    const int32_t x = negl[t];
+                    neg = A.gmark[x] == pid && g_member(A, x, so_c, si_c) < 0.0;
+                }
+                any = __syncthreads_or(neg);
+            }
+            negc = any ? -1 : 0;   // -1: some negative member (count taken when needed)
             sec(2);
         }
         if (negc == 0) break;   // no member with negative gain left (detector.py:224-225)
@@ -996,8 +1008,15 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
                 gain = pg;
             }
         }
-        if (xc < 0) {
-            if (tid == 0) atomicAdd(O.unresolved, (unsigned long long)negc);   // 275-277
+        if (xc < 0) {   // the exact number of negative members (detector.py:275-277)
+            const int nn = s_nneg;
+            int c = 0;
+            for (int t = tid; t < nn; t += GB) {
+                const int32_t x = negl[t];
+                if (A.gmark[x] == pid && g_member(A, x, so_c, si_c) < 0.0) c++;
+            }
+            negc = block_sum_i(c, si);
+            if (tid == 0) atomicAdd(O.unresolved, (unsigned long long)negc);
             break;
         }
         // ---- apply the cut: a, part totals, ancestors' subtree sums
