@@ -887,15 +887,35 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
                 lx[u] = 0x7fffffff;
             }
             double drop = -INFINITY;
-            for (int64_t k = P.lo + tid; k < P.hi; k += GB) {
-                const int32_t x = A.order[k];
-                if (A.gmark[x] != pid) continue;
-                if (g_member(A, x, so_c, si_c) < 0.0) {
+            // four strided members per step: their loads are issued together (the list is
+            // order-independent: (gain desc, id asc) top list, max of the dropped gains)
+            constexpr int FU = 4;
+            for (int64_t k0 = P.lo + tid; k0 < P.hi; k0 += (int64_t)FU * GB) {
+                int32_t xs[FU];
+                bool ok[FU];
+                double gmv[FU], gbv[FU];
+#pragma unroll
+                for (int u = 0; u < FU; u++) {
+                    const int64_t kk = k0 + (int64_t)u * GB;
+                    xs[u] = kk < P.hi ? A.order[kk] : -1;
+                }
+#pragma unroll
+                for (int u = 0; u < FU; u++) ok[u] = xs[u] >= 0 && A.gmark[xs[u]] == pid;
+#pragma unroll
+                for (int u = 0; u < FU; u++) {
+                    gmv[u] = ok[u] ? g_member(A, xs[u], so_c, si_c) : 0.0;
+                    gbv[u] = ok[u] ? g_branch(A, xs[u], so_c, si_c) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < FU; u++) {
+                const int32_t x = xs[u];
+                if (!ok[u]) continue;
+                if (gmv[u] < 0.0) {
                     negl[atomicAdd(&s_nneg, 1)] = x;
                     negflag[x] = 1;
                 }
                 if (x == r || (two && x == q)) continue;
-                double g = g_branch(A, x, so_c, si_c);
+                double g = gbv[u];
                 int32_t xx = x;
 #pragma unroll
                 for (int u = 0; u < GLOC; u++) {   // insertion into the local top list
@@ -909,6 +929,7 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
                     }
                 }
                 drop = fmax(drop, g);   // best candidate not kept locally
+                }
             }
 #pragma unroll
             for (int u = 0; u < GLOC; u++) {
