@@ -662,7 +662,7 @@ static DBuf<uint32_t> g_stamp;   // monotone part stamps (never reset)
 // ------------------------------------------------ giant parts: one CTA per part
 
 constexpr int GB = 1024;              // threads per giant-part CTA
-constexpr int GT = 128;               // top candidate list kept between full passes
+constexpr int GT = 512;               // top candidate list kept between full passes
 constexpr int GLOC = 2;               // per-thread candidates of a full pass
 constexpr int GSORT = GB * GLOC;      // sorted in shared memory
 constexpr int DIRTY_CAP = 1 << 16;    // locally updated nodes before a forced full pass
