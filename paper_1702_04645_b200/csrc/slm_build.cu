@@ -752,6 +752,7 @@ __global__ void k_view_bounds(const int64_t *vptr, int64_t n, int64_t *bound) {
         const int bk = view_bin(d), bp = k ? view_bin(dp) : NBINS;
         for (int b = bk + 1; b <= bp && b < NBINS; b++) bound[b] = k;
         if (d <= TINY_MAX && dp > TINY_MAX) bound[NBINS] = k;
+        if (d <= HALF_MAX && dp > HALF_MAX) bound[NBINS + 1] = k;
     }
 }
 // rows[off + i] = start + i over up to 8 segments {off, start, len}
@@ -767,11 +768,11 @@ __global__ void k_view_fill_rows(const int64_t *seg, int nseg, int32_t *rows) {
 static void build_bins_view(slm_ctx *ctx, LevelGraph &V) {
     const int64_t n = V.n;
     cudaStream_t s = ctx->stream;
-    int64_t *d_b = ctx->view_bound.resize(NBINS + 1 + 3 * 8);
-    std::vector<int64_t> hb(NBINS + 1, n);
-    CUDA_TRY(cudaMemcpyAsync(d_b, hb.data(), (NBINS + 1) * 8, cudaMemcpyHostToDevice, s));
+    int64_t *d_b = ctx->view_bound.resize(NBINS + 2 + 3 * 8);
+    std::vector<int64_t> hb(NBINS + 2, n);
+    CUDA_TRY(cudaMemcpyAsync(d_b, hb.data(), (NBINS + 2) * 8, cudaMemcpyHostToDevice, s));
     if (n) k_view_bounds<<<grid_for(n, 256), 256, 0, s>>>(V.uptr.p, n, d_b);
-    CUDA_TRY(cudaMemcpyAsync(hb.data(), d_b, (NBINS + 1) * 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(hb.data(), d_b, (NBINS + 2) * 8, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     // bin b = view rows [lo(b), hi(b)): hi(b) = bound[b], lo(b) = bound[b + 1] (lo(5) = 0)
     auto lo = [&](int b) { return b == NBINS - 1 ? (int64_t)0 : hb[b + 1]; };
@@ -801,8 +802,10 @@ static void build_bins_view(slm_ctx *ctx, LevelGraph &V) {
         off += hi(b) - lo(b);
     }
     V.bin_off[NBINS] = off;
-    CUDA_TRY(cudaMemcpyAsync(d_b + NBINS + 1, seg.data(), seg.size() * 8, cudaMemcpyHostToDevice, s));
-    if (off) k_view_fill_rows<<<grid_for(off, 256), 256, 0, s>>>(d_b + NBINS + 1, (int)seg.size() / 3,
+    // bin 1's rows of d <= HALF_MAX: the tail of its (descending-degree) segment
+    V.bin1_half = hi(1) - std::max(lo(1), std::min(hi(1), hb[NBINS + 1]));
+    CUDA_TRY(cudaMemcpyAsync(d_b + NBINS + 2, seg.data(), seg.size() * 8, cudaMemcpyHostToDevice, s));
+    if (off) k_view_fill_rows<<<grid_for(off, 256), 256, 0, s>>>(d_b + NBINS + 2, (int)seg.size() / 3,
                                                                  V.bin_rows.p);
     CUDA_TRY(cudaStreamSynchronize(s));
     for (int b = 0; b < NBINS; b++) V.bin_entries[b] = upc[2 * b + 1] - upc[2 * b];

@@ -102,6 +102,7 @@ __host__ __device__ constexpr int64_t bin_hi(int b) {
 }
 constexpr int SMALL_MAX = 32;     // warp lanes = entries (packed rows)
 constexpr int TINY_MAX = 8;       // bin-0 rows up to this degree: one lane per row
+constexpr int HALF_MAX = 64;      // bin-1 rows up to this degree: one half-warp per row
 constexpr int MID_MAX = 4096;     // generic path: CTA-per-row shared-memory hash up to here
 
 constexpr int HUB_SEG = 4096;     // entries per hub-row work item of the integer sweep
@@ -133,6 +134,7 @@ struct LevelGraph {
     int64_t bin_off[NBINS + 1] = {0, 0, 0, 0, 0, 0, 0};
     int64_t bin_entries[NBINS] = {0, 0, 0, 0, 0, 0};
     int64_t bin0_tiny = 0;     // bin-0 rows: the first bin0_tiny have d <= TINY_MAX (stable partition)
+    int64_t bin1_half = 0;     // sweep view only: the last bin1_half bin-1 rows have d <= HALF_MAX
     DBuf<int64_t> large_hoff;  // per row with d > MID_MAX (bins 4, 5): global hash offset
     int64_t large_hash_total = 0;
     // bin-5 (hub) rows of the integer sweep, in processing order j (descending degree):

@@ -771,6 +771,129 @@ __global__ void __launch_bounds__(WARPS * 32, 4) k_sweep_warp(SweepArgs<SYM> A, 
     }
 }
 
+// bin 1 rows of d <= HALF_MAX: two rows per warp, one per half-warp (16 lanes x 4 entries
+// cover a row in one chunk), so the per-row selection, reductions and clear are shared by two
+// rows.  Every collective is restricted to the half (mask hm, xor offsets below 16), so the
+// halves may diverge.  Same tables, list and decisions as k_sweep_warp.
+template <int U>
+__device__ __forceinline__ void insert_half(uint32_t tb, uint32_t hmask, const int32_t (&c)[U],
+                                            const uint32_t (&w)[U], uint32_t ob, uint32_t &rcnt,
+                                            unsigned hm, int hl) {
+    const uint32_t hsh = __clz(hmask);
+    bool fr[U];
+    uint32_t sl[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        fr[u] = false;
+        sl[u] = ((uint32_t)c[u] * 2654435769u) >> hsh;
+        if (c[u] >= 0) {
+            for (;;) {
+                int32_t k = lds_vol(tb + sl[u] * 8);
+                if (k == c[u]) break;
+                if (k == -1) {
+                    k = cas_s(tb + sl[u] * 8, -1, c[u]);
+                    if (k == -1) {
+                        fr[u] = true;
+                        break;
+                    }
+                    if (k == c[u]) break;
+                }
+                sl[u] = (sl[u] + 1) & hmask;
+            }
+            red_add_s(tb + sl[u] * 8 + 4, w[u]);
+        }
+    }
+    const int sh = (hm & 1u) ? 0 : 16;   // bit offset of this half in the ballots
+    const unsigned lt = (1u << hl) - 1u;
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        const unsigned m = __ballot_sync(hm, fr[u]) >> sh;
+        if (fr[u]) sts_u16(ob + 2 * (rcnt + __popc(m & lt)), sl[u]);
+        rcnt += __popc(m);
+    }
+}
+__device__ __forceinline__ float half_maxf(float v, unsigned hm) {
+#pragma unroll
+    for (int off = 8; off > 0; off >>= 1) v = fmaxf(v, __shfl_xor_sync(hm, v, off));
+    return v;
+}
+__device__ __forceinline__ unsigned half_sum(unsigned v, unsigned hm) {
+#pragma unroll
+    for (int off = 8; off > 0; off >>= 1) v += __shfl_xor_sync(hm, v, off);
+    return v;
+}
+__device__ __forceinline__ void half_best(double &bt, int32_t &bc, unsigned hm) {
+#pragma unroll
+    for (int off = 8; off > 0; off >>= 1) {
+        const double obt = __shfl_xor_sync(hm, bt, off);
+        const int32_t obc = __shfl_xor_sync(hm, bc, off);
+        if (better2(obt, obc, bt, bc)) {
+            bt = obt;
+            bc = obc;
+        }
+    }
+}
+template <int HM, int WARPS, bool SYM>
+__global__ void __launch_bounds__(WARPS * 32, 4) k_sweep_half(SweepArgs<SYM> A, const int32_t *rows,
+                                                               int64_t nrows) {
+    extern __shared__ int2 htab2[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int half = lane >> 4, hl = lane & 15;
+    const unsigned hm = half ? 0xffff0000u : 0x0000ffffu;
+    const int hb = wid * 2 + half;
+    int2 *T = htab2 + hb * HM;
+    uint16_t *occ = (uint16_t *)(htab2 + WARPS * 2 * HM) + hb * HM;
+    const uint32_t tsa = smem_addr(T), osa = smem_addr(occ);
+    for (int k = hl; k < HM; k += 16) T[k] = make_int2(-1, 0);
+    __syncwarp(hm);
+    const int64_t h0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * 2 + half;
+    const int64_t nh = (((int64_t)gridDim.x * blockDim.x) >> 5) * 2;
+    constexpr int U = HALF_MAX / 16;
+    for (int64_t i = h0; i < nrows; i += nh) {
+        const int32_t r = rows[i];
+        const int64_t e0 = A.uptr[r];
+        const uint32_t d = (uint32_t)(A.uptr[r + 1] - e0);
+        const uint32_t H = min(tab_size(d, 2, 32), (uint32_t)HM);   // > d
+        const int32_t L = A.label[r];
+        const double2 sr = node_s(A, r);
+        const float2 srf = make_float2((float)sr.x, (float)sr.y);
+        int32_t c[U];
+        uint32_t wt[U];
+        load_row<U, 16>(A.unbr + e0, A.u32 + e0, A.label, d, hl, c, wt);
+        uint32_t no = 0;
+        insert_half<U>(tsa, H - 1, c, wt, osa, no, hm, hl);
+        __syncwarp(hm);
+        Sel S;
+        sel_init(S);
+        uint32_t gown = 0;
+        bool hown = false;
+        occ_scan<SYM, false>(A, T, occ, no, hl, 16, L, srf, S, gown, hown);
+        const unsigned ob = __ballot_sync(hm, hown);
+        gown = __shfl_sync(hm, gown, ob ? __ffs(ob) - 1 : (half << 4));
+        if (A.groups && hl == 0) atomicAdd(A.groups, (unsigned long long)no);
+        if (A.wown && hl == 0) A.wown[r] = ob ? gown : 0u;
+        const float lo = half_maxf(S.lo, hm);
+        if (lo == -INFINITY) {
+            if (hl == 0) A.cstar[r] = L;
+        } else {
+            const unsigned cnt = half_sum((S.up1 >= lo) + (S.up2 >= lo), hm);
+            if (cnt == 1) {
+                if (S.up1 >= lo)
+                    A.cstar[r] = decide_fast(A, S.g1, S.c1, lo, S.up1, ob != 0, gown, sr, srf, L);
+            } else {
+                if (A.stats && hl == 0) atomicAdd(A.stats + 2, 1ull);
+                double bt = -INFINITY;
+                int32_t bc = 0x7fffffff;
+                occ_exact<SYM, false>(A, T, occ, no, hl, 16, L, sr, srf, lo, bt, bc);
+                half_best(bt, bc, hm);
+                if (hl == 0) A.cstar[r] = decide(A, bt, bc, ob != 0, gown, sr, L);
+            }
+        }
+        occ_clear<false>(T, occ, no, hl, 16);
+        __syncwarp(hm);
+    }
+}
+
 // per-CTA reduction scratch of the selection
 struct BlockSel {
     float lo[32];
@@ -1546,6 +1669,7 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, const int
         set_smem(khm, SMH);
         set_smem(khr, SMH);
         set_smem(khsm, SMHS);
+        set_smem(k_sweep_half<256, W1, SYM>, SM1);
         attrs[SYM] = true;
     }
     if (nb(0) && (bin_mask & 1)) {
@@ -1560,8 +1684,16 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, const int
             k_sweep_small<SYM><<<grid_for(nw * 32, 256), 256, 0, s>>>(A, rows(0) + nt, ns, rpw);
         }
     }
-    if (nb(1) && (bin_mask & 2))
-        k1<<<grid_for(nb(1) * 32, W1 * 32, 148LL * 4), W1 * 32, SM1, s>>>(A, rows(1), nb(1));
+    if (nb(1) && (bin_mask & 2)) {
+        // rows of d <= HALF_MAX (the tail of the view's descending-degree segment): two per warp
+        static const bool no_half = getenv("SLM_HALF") && atoi(getenv("SLM_HALF")) == 0;
+        const int64_t nh1 = no_half ? 0 : G.bin1_half, nf1 = nb(1) - nh1;
+        if (nf1)
+            k1<<<grid_for(nf1 * 32, W1 * 32, 148LL * 4), W1 * 32, SM1, s>>>(A, rows(1), nf1);
+        if (nh1)
+            k_sweep_half<256, W1, SYM><<<grid_for(nh1 * 16, W1 * 32, 148LL * 4), W1 * 32, SM1, s>>>(
+                A, rows(1) + nf1, nh1);
+    }
     if (bin_mask & 28) {
         const int64_t cap = nb(2) + nb(3) + nb(4);
         if (ctx->ovf_rows.n < (size_t)std::max<int64_t>(1, cap)) ctx->ovf_rows.resize(std::max<int64_t>(1, cap));
