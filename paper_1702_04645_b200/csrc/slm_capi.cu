@@ -381,7 +381,10 @@ slm_ctx *slm_create(int device) {
     const char *pe = getenv("SLM_PROFILE");
     ctx->prof = pe && pe[0] == '1';
     if (cudaSetDevice(device) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
         cudaGetLastError();
         delete ctx;
         return nullptr;
@@ -408,7 +411,11 @@ void slm_destroy(slm_ctx *ctx) {
         ctx->g.reset();
         ctx->g0.reset();
     }
+    cudaStreamSynchronize(ctx->stream2);
     cudaStreamDestroy(ctx->stream);
+    cudaStreamDestroy(ctx->stream2);
+    cudaEventDestroy(ctx->ev_fork);
+    cudaEventDestroy(ctx->ev_join);
     delete ctx;
     // the last context: the static scratch kept across calls goes back to the arena too
     if (--g_live_ctx == 0) dbuf_release_all();

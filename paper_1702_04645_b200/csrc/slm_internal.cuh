@@ -201,6 +201,8 @@ struct slm_ctx {
     double ph_t0 = 0.0;
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t stream2 = nullptr;              // side stream of the plan sweep (hub rows)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::string err;
     std::shared_ptr<LevelGraph> g0, g;   // original graph and current level
     Forest f;

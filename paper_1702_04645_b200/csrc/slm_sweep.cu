@@ -1672,56 +1672,16 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, const int
         set_smem(k_sweep_half<256, W1, SYM>, SM1);
         attrs[SYM] = true;
     }
-    if (nb(0) && (bin_mask & 1)) {
-        static const bool no_tiny = getenv("SLM_TINY") && atoi(getenv("SLM_TINY")) == 0;
-        const int64_t nt = no_tiny ? 0 : G.bin0_tiny, ns = nb(0) - nt;
-        if (nt)
-            k_sweep_tiny<SYM, TINY_MAX><<<grid_for(nt, 256), 256, 0, s>>>(A, rows(0), nt);
-        if (ns) {
-            const int64_t warps = 148LL * 64;
-            int64_t rpw = std::max<int64_t>(64, (ns + warps - 1) / warps);
-            int64_t nw = (ns + rpw - 1) / rpw;
-            k_sweep_small<SYM><<<grid_for(nw * 32, 256), 256, 0, s>>>(A, rows(0) + nt, ns, rpw);
-        }
+    // hub rows (bin 5) run on the side stream, concurrently with bins 0-4: their global-table
+    // kernels leave most of the GPU idle.  Forked after the labels are in place, joined before
+    // the sweep returns (disjoint rows: no shared outputs)
+    const bool hub_side = nb(5) && (bin_mask & 32) && ctx->stream2 && !getenv("SLM_HUB_SAME_STREAM");
+    if (hub_side) {
+        CUDA_TRY(cudaEventRecord(ctx->ev_fork, ctx->stream));
+        CUDA_TRY(cudaStreamWaitEvent(ctx->stream2, ctx->ev_fork, 0));
     }
-    if (nb(1) && (bin_mask & 2)) {
-        // rows of d <= HALF_MAX (the tail of the view's descending-degree segment): two per warp
-        static const bool no_half = getenv("SLM_HALF") && atoi(getenv("SLM_HALF")) == 0;
-        const int64_t nh1 = no_half ? 0 : G.bin1_half, nf1 = nb(1) - nh1;
-        if (nf1)
-            k1<<<grid_for(nf1 * 32, W1 * 32, 148LL * 4), W1 * 32, SM1, s>>>(A, rows(1), nf1);
-        if (nh1)
-            k_sweep_half<256, W1, SYM><<<grid_for(nh1 * 16, W1 * 32, 148LL * 4), W1 * 32, SM1, s>>>(
-                A, rows(1) + nf1, nh1);
-    }
-    if (bin_mask & 28) {
-        const int64_t cap = nb(2) + nb(3) + nb(4);
-        if (ctx->ovf_rows.n < (size_t)std::max<int64_t>(1, cap)) ctx->ovf_rows.resize(std::max<int64_t>(1, cap));
-        if (ctx->ovf_cnt.n < 1 + OVF_GRID) {
-            ctx->ovf_cnt.resize(1 + OVF_GRID);
-            CUDA_TRY(cudaMemsetAsync(ctx->ovf_cnt.p, 0, (1 + OVF_GRID) * 4, s));
-        } else {
-            CUDA_TRY(cudaMemsetAsync(ctx->ovf_cnt.p, 0, 4, s));
-        }
-    }
-    int32_t *ovf = ctx->ovf_rows.p;
-    uint32_t *novf = ctx->ovf_cnt.p;
-    if (nb(2) && (bin_mask & 4))
-        k2<<<(unsigned)std::min<int64_t>(nb(2), 148 * 8), 128, SM2, s>>>(A, rows(2), nb(2), ovf, novf);
-    if (nb(3) && (bin_mask & 8))
-        k3<<<(unsigned)std::min<int64_t>(nb(3), 148 * 4), 256, SM3, s>>>(A, rows(3), nb(3), ovf, novf);
-    if (nb(4) && (bin_mask & 16))
-        k4<<<(unsigned)std::min<int64_t>(nb(4), 148 * 2), 512, SM4, s>>>(A, rows(4), nb(4), ovf, novf);
-    if (bin_mask & 28) {
-        if (ctx->ovf_tab.n < (size_t)OVF_GRID * OVF_H) {
-            ctx->ovf_tab.resize((size_t)OVF_GRID * OVF_H);
-            ctx->ovf_occ.resize((size_t)OVF_GRID * OVF_H);
-            k_fill_empty<<<grid_for((int64_t)OVF_GRID * OVF_H, 256), 256, 0, s>>>(
-                ctx->ovf_tab.p, (int64_t)OVF_GRID * OVF_H);
-        }
-        k_sweep_overflow<SYM><<<OVF_GRID, OVF_BLOCK, 0, s>>>(A, ovf, novf, ctx->ovf_tab.p,
-                                                             ctx->ovf_occ.p, novf + 1);
-    }
+    {
+    cudaStream_t s = hub_side ? ctx->stream2 : ctx->stream;
     if (nb(5) && (bin_mask & 32)) {
         const int64_t RS = G.hub_ring, nh = G.hub_rows_n;
         if (ctx->hub_tab.n < (size_t)RS) {
@@ -1794,6 +1754,59 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, const int
         }
         k_sweep_hub_fallback<SYM><<<148, HUB_BLOCK, 0, s>>>(A, Hb);
     }
+    }
+    if (hub_side) CUDA_TRY(cudaEventRecord(ctx->ev_join, ctx->stream2));
+    if (nb(0) && (bin_mask & 1)) {
+        static const bool no_tiny = getenv("SLM_TINY") && atoi(getenv("SLM_TINY")) == 0;
+        const int64_t nt = no_tiny ? 0 : G.bin0_tiny, ns = nb(0) - nt;
+        if (nt)
+            k_sweep_tiny<SYM, TINY_MAX><<<grid_for(nt, 256), 256, 0, s>>>(A, rows(0), nt);
+        if (ns) {
+            const int64_t warps = 148LL * 64;
+            int64_t rpw = std::max<int64_t>(64, (ns + warps - 1) / warps);
+            int64_t nw = (ns + rpw - 1) / rpw;
+            k_sweep_small<SYM><<<grid_for(nw * 32, 256), 256, 0, s>>>(A, rows(0) + nt, ns, rpw);
+        }
+    }
+    if (nb(1) && (bin_mask & 2)) {
+        // rows of d <= HALF_MAX (the tail of the view's descending-degree segment): two per warp
+        static const bool no_half = getenv("SLM_HALF") && atoi(getenv("SLM_HALF")) == 0;
+        const int64_t nh1 = no_half ? 0 : G.bin1_half, nf1 = nb(1) - nh1;
+        if (nf1)
+            k1<<<grid_for(nf1 * 32, W1 * 32, 148LL * 4), W1 * 32, SM1, s>>>(A, rows(1), nf1);
+        if (nh1)
+            k_sweep_half<256, W1, SYM><<<grid_for(nh1 * 16, W1 * 32, 148LL * 4), W1 * 32, SM1, s>>>(
+                A, rows(1) + nf1, nh1);
+    }
+    if (bin_mask & 28) {
+        const int64_t cap = nb(2) + nb(3) + nb(4);
+        if (ctx->ovf_rows.n < (size_t)std::max<int64_t>(1, cap)) ctx->ovf_rows.resize(std::max<int64_t>(1, cap));
+        if (ctx->ovf_cnt.n < 1 + OVF_GRID) {
+            ctx->ovf_cnt.resize(1 + OVF_GRID);
+            CUDA_TRY(cudaMemsetAsync(ctx->ovf_cnt.p, 0, (1 + OVF_GRID) * 4, s));
+        } else {
+            CUDA_TRY(cudaMemsetAsync(ctx->ovf_cnt.p, 0, 4, s));
+        }
+    }
+    int32_t *ovf = ctx->ovf_rows.p;
+    uint32_t *novf = ctx->ovf_cnt.p;
+    if (nb(2) && (bin_mask & 4))
+        k2<<<(unsigned)std::min<int64_t>(nb(2), 148 * 8), 128, SM2, s>>>(A, rows(2), nb(2), ovf, novf);
+    if (nb(3) && (bin_mask & 8))
+        k3<<<(unsigned)std::min<int64_t>(nb(3), 148 * 4), 256, SM3, s>>>(A, rows(3), nb(3), ovf, novf);
+    if (nb(4) && (bin_mask & 16))
+        k4<<<(unsigned)std::min<int64_t>(nb(4), 148 * 2), 512, SM4, s>>>(A, rows(4), nb(4), ovf, novf);
+    if (bin_mask & 28) {
+        if (ctx->ovf_tab.n < (size_t)OVF_GRID * OVF_H) {
+            ctx->ovf_tab.resize((size_t)OVF_GRID * OVF_H);
+            ctx->ovf_occ.resize((size_t)OVF_GRID * OVF_H);
+            k_fill_empty<<<grid_for((int64_t)OVF_GRID * OVF_H, 256), 256, 0, s>>>(
+                ctx->ovf_tab.p, (int64_t)OVF_GRID * OVF_H);
+        }
+        k_sweep_overflow<SYM><<<OVF_GRID, OVF_BLOCK, 0, s>>>(A, ovf, novf, ctx->ovf_tab.p,
+                                                             ctx->ovf_occ.p, novf + 1);
+    }
+    if (hub_side) CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
     CUDA_TRY(cudaGetLastError());
     if (want_stats) {
         unsigned long long h[8];
