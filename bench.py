@@ -271,10 +271,10 @@ def main():
     groups, bin_rows, bin_entries = ctx.plan_groups()
     stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=local)
     # kernels per sweep (library launch sequence, slm_sweep.cu run_plan_u32): view labels in,
-    # bin 0 (lane-per-row + packed), bin 1, bins 2-4 (+ their overflow pass), bin 5 (shared-
-    # table rows, global merge + select, fallback), targets out
+    # bin 0 (lane-per-row + packed), bin 1 (warp + half-warp rows), bins 2-4 (+ their
+    # overflow pass), bin 5 (shared-table rows, global merge + select, fallback), targets out
     mid = int((bin_rows[2:5] > 0).sum())
-    launches_per_sweep = (2 + 2 * int(bin_rows[0] > 0) + int(bin_rows[1] > 0) + mid
+    launches_per_sweep = (2 + 2 * int(bin_rows[0] > 0) + 2 * int(bin_rows[1] > 0) + mid
                           + int(mid > 0) + 4 * int(bin_rows[5] > 0))
 
     def timed(mask, iters):
