@@ -140,9 +140,12 @@ __global__ void k_lb_ptr32(const int32_t *sorted, int64_t m, int64_t nrows, int3
 
 // per-community sums of integer strengths: runs of equal community inside a warp's 32
 // consecutive members are combined by a segmented shuffle scan, one atomic per run (exact:
-// every partial sum is an integer below 2^53)
-__global__ void k_comm_sums_runs(const int32_t *members, const int32_t *comm, const double *s_out,
-                                 const double *s_in, int64_t n, double *S_out, double *S_in) {
+// every partial sum is an integer below 2^53).  The community of the k-th member is the
+// k-th sorted key, so the only gather is the node's interleaved strength pair (one sector);
+// symmetric graphs accumulate s_out only (s_in is bitwise equal).
+__global__ void k_comm_sums_runs(const int32_t *members, const int32_t *ksorted,
+                                 const double2 *s2, int64_t n, bool sym, double *S_out,
+                                 double *S_in) {
     const int lane = threadIdx.x & 31;
     for (int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31LL; b < n;
          b += (int64_t)gridDim.x * blockDim.x) {
@@ -150,16 +153,16 @@ __global__ void k_comm_sums_runs(const int32_t *members, const int32_t *comm, co
         int32_t c = -1;
         double so = 0.0, si = 0.0;
         if (k < n) {
-            const int32_t x = members[k];
-            c = comm[x];
-            so = s_out[x];
-            si = s_in[x];
+            c = ksorted[k];
+            const double2 v = s2[members[k]];
+            so = v.x;
+            si = v.y;
         }
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
             const int32_t oc = __shfl_up_sync(0xffffffffu, c, off);
             const double oso = __shfl_up_sync(0xffffffffu, so, off);
-            const double osi = __shfl_up_sync(0xffffffffu, si, off);
+            const double osi = sym ? 0.0 : __shfl_up_sync(0xffffffffu, si, off);
             if (lane >= off && oc == c) {
                 so += oso;
                 si += osi;
@@ -168,7 +171,7 @@ __global__ void k_comm_sums_runs(const int32_t *members, const int32_t *comm, co
         const int32_t nc = __shfl_down_sync(0xffffffffu, c, 1);
         if (c >= 0 && (lane == 31 || nc != c)) {
             atomicAdd(&S_out[c], so);
-            atomicAdd(&S_in[c], si);
+            if (!sym) atomicAdd(&S_in[c], si);
         }
     }
 }
@@ -182,10 +185,11 @@ __global__ void k_gather_members(const int32_t *members, const double *s_out, co
         vi[k] = s_in[x];
     }
 }
-__global__ void k_comm_finish(const int32_t *cptr, const double *S_out, const double *S_in,
+__global__ void k_comm_finish(const int32_t *cptr, const double *S_out, double *S_in, bool sym,
                               int64_t nc, int32_t *count, double2 *S2, float *S1f, float2 *S2f) {
     GS_LOOP(c, nc) {
-        const double so = S_out[c], si = S_in[c];
+        const double so = S_out[c], si = sym ? so : S_in[c];
+        if (sym) S_in[c] = so;
         S2[c] = make_double2(so, si);
         S1f[c] = (float)so;
         S2f[c] = make_float2((float)so, (float)si);
@@ -435,10 +439,11 @@ void build_members_and_aggregates(slm_ctx *ctx, const LevelGraph &G, Forest &F) 
         return;
     }
     CUDA_TRY(cudaMemsetAsync(F.S_out.p, 0, nc * 8, s));
-    CUDA_TRY(cudaMemsetAsync(F.S_in.p, 0, nc * 8, s));
-    k_comm_sums_runs<<<grid_for(n, 256), 256, 0, s>>>(F.members.p, F.comm.p, G.s_out.p, G.s_in.p,
-                                                       n, F.S_out.p, F.S_in.p);
-    k_comm_finish<<<grid_for(nc, 256), 256, 0, s>>>(F.cptr.p, F.S_out.p, F.S_in.p, nc, F.count.p,
+    if (!G.sym) CUDA_TRY(cudaMemsetAsync(F.S_in.p, 0, nc * 8, s));
+    k_comm_sums_runs<<<grid_for(n, 256), 256, 0, s>>>(F.members.p, ksorted, G.s2.p, n, G.sym,
+                                                       F.S_out.p, F.S_in.p);
+    k_comm_finish<<<grid_for(nc, 256), 256, 0, s>>>(F.cptr.p, F.S_out.p, F.S_in.p, G.sym, nc,
+                                                    F.count.p,
                                                     F.S2.p, F.S1f.p, F.S2f.p);
     F.agg_valid = true;
 }

@@ -10,4 +10,4 @@ print("build", ctx.phase_times(reset=True))
 info = ctx.info(); g = Graph(info["n"], None, None, None); g._ctx = ctx; ctx.level = 0
 t = time.perf_counter(); r = detector.run(g, RunConfig()); el = time.perf_counter() - t
 pt = ctx.phase_times(reset=True)
-print(f"run {el:.3f} s alloc_ms {pt['alloc_ms']} calls {pt['alloc_calls']}", {k: round(v, 3) for k, v in r.stats.phase_seconds.items()})
+print(f"run {el:.3f} s Q {r.final_score:.9f} alloc_ms {pt['alloc_ms']} calls {pt['alloc_calls']}", {k: round(v, 3) for k, v in r.stats.phase_seconds.items()})
