@@ -789,8 +789,12 @@ __device__ __forceinline__ void mark_dirty(int32_t y, uint8_t *gflag, int32_t *d
     const unsigned int old = atomicOr(wp, bit);
     if (!(old & bit)) {
         const int at = atomicAdd(ndirty, 1);
-        if (at < DIRTY_CAP) dirty[at] = y;
-        else *overflow = 1;
+        if (at < DIRTY_CAP) {
+            dirty[at] = y;
+        } else {   // not listed: leave it unflagged (the overflow forces a full pass)
+            atomicAnd(wp, ~bit);
+            *overflow = 1;
+        }
     }
 }
 
@@ -809,10 +813,10 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
     __shared__ int si[32];
     __shared__ int s_nneg, s_ndirty, s_overflow;
     __shared__ double s_tau, s_so, s_si;
-    __shared__ int s_ntop, s_two;
+    __shared__ int s_ntop, s_two, s_nadd, s_topfull;
     __shared__ int32_t s_chain[CHAIN_CAP];
     __shared__ int32_t s_big[BIG_CAP];
-    __shared__ int s_nbig;
+    __shared__ int s_nbig, s_nch;
     const GPart P = parts[blockIdx.x];
     const int tid = threadIdx.x;
     const int32_t pid = P.pid, r = P.root;
@@ -827,6 +831,9 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
         s_nneg = 0;
         s_ndirty = 0;
         s_overflow = 0;
+        s_ntop = 0;
+        s_nadd = 0;
+        s_topfull = 0;
     }
     __syncthreads();
     if (s_two && A.a[q] != r) return;
@@ -849,8 +856,11 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
         int32_t bx = 0x7fffffff;
         int negc = 0;
         if (!need_full) {
-            // incremental: re-evaluate the top list and the dirty nodes
+            // incremental: re-evaluate the top list and the nodes the last cut touched.  A
+            // touched node above the bound tau joins the top list (flag bit 1 keeps it there
+            // once); the others are back under tau, so the touched list is cleared every cut
             const int ntop = s_ntop, nd = min(s_ndirty, DIRTY_CAP);
+            const double tau = s_tau;
             for (int t = tid; t < ntop + nd; t += GB) {
                 const int32_t x = t < ntop ? tx[t] : dirty[t - ntop];
                 if (A.gmark[x] != pid || x == r || (two && x == q)) continue;
@@ -859,9 +869,26 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
                     bg = g;
                     bx = x;
                 }
+                if (t >= ntop && g > tau) {
+                    unsigned int *wp = (unsigned int *)(gflag + (x & ~3));
+                    const unsigned int tb = 2u << ((x & 3) * 8);
+                    if (!(atomicOr(wp, tb) & tb)) {
+                        const int at = ntop + atomicAdd(&s_nadd, 1);
+                        if (at < GSORT) {
+                            tx[at] = x;
+                        } else {
+                            atomicAnd(wp, ~tb);
+                            s_topfull = 1;
+                        }
+                    }
+                }
             }
             block_best(bg, bx, sg, sxx);
-            if (!(bg > s_tau) || s_overflow) need_full = true;
+            if (tid == 0) {
+                s_ntop = min(ntop + s_nadd, GSORT);
+                s_nadd = 0;
+            }
+            if (!(bg > tau) || s_overflow || s_topfull) need_full = true;
             sec(0);
         }
         if (need_full) {
@@ -870,13 +897,18 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
                 atomicAdd(O.unresolved + 2, (unsigned long long)(P.hi - P.lo));
             }
             // reset the incremental state
+            __syncthreads();
             for (int t = tid; t < min(s_ndirty, DIRTY_CAP); t += GB) gflag[dirty[t]] = 0;
+            for (int t = tid; t < s_ntop; t += GB) gflag[tx[t]] = 0;
             for (int t = tid; t < s_nneg; t += GB) negflag[negl[t]] = 0;
             __syncthreads();
             if (tid == 0) {
                 s_ndirty = 0;
                 s_overflow = 0;
                 s_nneg = 0;
+                s_ntop = 0;
+                s_nadd = 0;
+                s_topfull = 0;
             }
             __syncthreads();
             double lg[GLOC];
@@ -974,6 +1006,7 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
                 s_ntop = nt;
             }
             __syncthreads();
+            for (int t = tid; t < s_ntop; t += GB) gflag[tx[t]] = 2;   // in the top list
             bg = tg[0];
             bx = tx[0];
             need_full = false;
@@ -1040,6 +1073,16 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
             if (tid == 0) atomicAdd(O.unresolved, (unsigned long long)negc);
             break;
         }
+        // the touched nodes are consumed: clear their flags (keeping the top-list bit)
+        {
+            const int nd = min(s_ndirty, DIRTY_CAP);
+            for (int t = tid; t < nd; t += GB) {
+                const int32_t y = dirty[t];
+                gflag[y] = __ldcg(gflag + y) & 2;
+            }
+            __syncthreads();
+            if (tid == 0) s_ndirty = 0;
+        }
         // ---- apply the cut: a, part totals, ancestors' subtree sums
         const int32_t xpar = A.a[xc];
         const double sb = A.sob[xc], ib = A.sib[xc];
@@ -1060,19 +1103,38 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
                 A.a[xc] = xc;
                 s_two = 0;
             } else {
+                // the ancestor chain xpar .. r (parents only: the loop carries one dependent
+                // load per step); the subtree-sum updates run CTA-wide below
                 A.a[xc] = xc;
-                int32_t y = xpar;
-                for (;;) {
-                    A.sob[y] -= sb;
-                    A.sib[y] -= ib;
-                    mark_dirty(y, gflag, dirty, &s_ndirty, &s_overflow);
+                int nch = 0;
+                for (int32_t y = xpar;; y = A.a[y]) {
+                    if (nch < CHAIN_CAP) s_chain[nch] = y;
+                    nch++;
                     if (y == r) break;
-                    y = A.a[y];
                 }
+                s_nch = nch;
             }
         }
         __syncthreads();
         pid_b = sxx[0];
+        if (!pair) {
+            const int nch = s_nch;
+            if (nch <= CHAIN_CAP) {
+                for (int c = tid; c < nch; c += GB) {
+                    const int32_t y = s_chain[c];
+                    A.sob[y] -= sb;
+                    A.sib[y] -= ib;
+                    mark_dirty(y, gflag, dirty, &s_ndirty, &s_overflow);
+                }
+            } else if (tid == 0) {
+                for (int32_t y = xpar;; y = A.a[y]) {
+                    A.sob[y] -= sb;
+                    A.sib[y] -= ib;
+                    mark_dirty(y, gflag, dirty, &s_ndirty, &s_overflow);
+                    if (y == r) break;
+                }
+            }
+        }
         // re-mark the cut subtree
         int cb = 0;
         for (int64_t k = blo + tid; k < bhi; k += GB) {
@@ -1098,13 +1160,17 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
                 const double u = A.iu[q];
                 atomicAdd(&A.wpart[v], -u);
                 mark_dirty(v, gflag, dirty, &s_ndirty, &s_overflow);
+                // one round trip per step: the parent, the DFS interval and the dirty byte are
+                // loaded together; the flag's atomic is issued only for nodes not yet dirty
+                // (a stale 0 only costs the atomic, which deduplicates)
                 int32_t y = v;
                 for (;;) {
-                    const int32_t pa = A.pos[y];
-                    if (pz >= pa && pz < pa + A.sz[y]) break;
+                    const int32_t pa = A.pos[y], sa = A.sz[y], nx = A.a[y];
+                    const uint8_t df = gflag[y];
+                    if (pz >= pa && pz < pa + sa) break;
                     atomicAdd(&A.xw[y], -u);
-                    mark_dirty(y, gflag, dirty, &s_ndirty, &s_overflow);
-                    y = A.a[y];
+                    if (!(df & 1)) mark_dirty(y, gflag, dirty, &s_ndirty, &s_overflow);
+                    y = nx;
                 }
                 // b-side: every ancestor of b strictly below lca = y loses u; deposited
                 // at the lca and applied in one walk of b's ancestor chain below
@@ -1136,24 +1202,39 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
             }
         }
         __syncthreads();
-        if (tid == 0) {   // top-down over b's ancestors: x_w(y) -= sum of deposits above y
-            int nch = 0;
-            for (int32_t y = xpar;; y = A.a[y]) {
-                if (nch < CHAIN_CAP) s_chain[nch] = y;
-                nch++;
-                if (y == r) break;
-            }
-            if (nch <= CHAIN_CAP) {
+        // top-down over b's ancestors: x_w(y) -= sum of deposits above y.  A pair cut has no
+        // chain (b's parent is the root and the root keeps no deposit reader above it).
+        if (!pair && s_nch <= CHAIN_CAP) {
+            // warp 0, 32 chain positions per step from the root down: the deposits are loaded
+            // together and every lane re-adds them in chain order (the serial sum, bit for bit)
+            if (tid < 32) {
+                const int nch = s_nch;
                 double run = 0.0;
-                for (int c = nch - 1; c >= 0; c--) {
-                    const int32_t y = s_chain[c];
-                    if (run != 0.0) {
-                        A.xw[y] -= run;
-                        mark_dirty(y, gflag, dirty, &s_ndirty, &s_overflow);
+                for (int top = nch - 1; top >= 0; top -= 32) {
+                    const int c = top - tid;
+                    const int32_t y = c >= 0 ? s_chain[c] : -1;
+                    const double dep = y >= 0 ? A.accl[y] : 0.0;
+                    double before = 0.0;
+#pragma unroll 8
+                    for (int j = 0; j < 32; j++) {
+                        const double dj = __shfl_sync(0xffffffffu, dep, j);
+                        if (j == tid) before = run;
+                        if (top - j >= 0) run += dj;
                     }
-                    run += A.accl[y];
-                    A.accl[y] = 0.0;
+                    if (y >= 0) {
+                        if (before != 0.0) {
+                            A.xw[y] -= before;
+                            mark_dirty(y, gflag, dirty, &s_ndirty, &s_overflow);
+                        }
+                        A.accl[y] = 0.0;
+                    }
                 }
+            }
+        } else if (tid == 0) {
+            if (pair) {
+                // pair cut: the chain is the root alone
+                const int32_t y = r;
+                A.accl[y] = 0.0;
             } else {   // very deep chain: per-node suffix via repeated upward walks
                 for (int32_t y = xpar;; y = A.a[y]) {
                     double above = 0.0;
@@ -1266,6 +1347,7 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
         atomicMax(O.unresolved + 4, (unsigned long long)(clock64() - t_cta));
     }
     for (int t = tid; t < min(s_ndirty, DIRTY_CAP); t += GB) gflag[dirty[t]] = 0;
+    for (int t = tid; t < s_ntop; t += GB) gflag[tx[t]] = 0;
     for (int t = tid; t < s_nneg; t += GB) negflag[negl[t]] = 0;
 }
 
