@@ -1156,21 +1156,29 @@ __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *part
             // (entries from the wave-0 intra-part lists: a superset of the part's edges)
             auto edge = [&](int64_t q, int32_t pz) {
                 const int32_t v = A.iz[q];
-                if (A.gmark[v] != pid) return;
                 const double u = A.iu[q];
+                // one round trip per step: the parent, the DFS interval and the dirty byte of
+                // the next node are loaded before this node's updates are issued (a stale 0
+                // flag only costs the deduplicating atomic); v's own come with its part mark
+                const int32_t gm = A.gmark[v];
+                int32_t pa = A.pos[v], sa = A.sz[v], nx = A.a[v];
+                uint8_t df = gflag[v];
+                if (gm != pid) return;
                 atomicAdd(&A.wpart[v], -u);
-                mark_dirty(v, gflag, dirty, &s_ndirty, &s_overflow);
-                // one round trip per step: the parent, the DFS interval and the dirty byte are
-                // loaded together; the flag's atomic is issued only for nodes not yet dirty
-                // (a stale 0 only costs the atomic, which deduplicates)
+                if (!(df & 1)) mark_dirty(v, gflag, dirty, &s_ndirty, &s_overflow);
+                df = 1;
                 int32_t y = v;
-                for (;;) {
-                    const int32_t pa = A.pos[y], sa = A.sz[y], nx = A.a[y];
-                    const uint8_t df = gflag[y];
-                    if (pz >= pa && pz < pa + sa) break;
+                while (!(pz >= pa && pz < pa + sa)) {
+                    const int32_t y2 = nx;
+                    const int32_t pa2 = A.pos[y2], sa2 = A.sz[y2], nx2 = A.a[y2];
+                    const uint8_t df2 = gflag[y2];
                     atomicAdd(&A.xw[y], -u);
                     if (!(df & 1)) mark_dirty(y, gflag, dirty, &s_ndirty, &s_overflow);
-                    y = nx;
+                    y = y2;
+                    pa = pa2;
+                    sa = sa2;
+                    nx = nx2;
+                    df = df2;
                 }
                 // b-side: every ancestor of b strictly below lca = y loses u; deposited
                 // at the lca and applied in one walk of b's ancestor chain below
