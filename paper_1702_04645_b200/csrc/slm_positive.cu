@@ -663,8 +663,9 @@ static DBuf<uint32_t> g_stamp;   // monotone part stamps (never reset)
 
 constexpr int GB = 1024;              // threads per giant-part CTA
 constexpr int GT = 512;               // top candidate list kept between full passes
-constexpr int GLOC = 2;               // per-thread candidates of a full pass
-constexpr int GSORT = GB * GLOC;      // sorted in shared memory
+constexpr int GLOC = 4;               // per-thread candidates of a full pass
+constexpr int GSORT = GB * GLOC;      // sorted in (dynamic) shared memory
+constexpr size_t GSMEM = (size_t)GSORT * (sizeof(double) + sizeof(int32_t));
 constexpr int DIRTY_CAP = 1 << 16;    // locally updated nodes before a forced full pass
 constexpr int CHAIN_CAP = 2048;       // ancestor chain of a cut kept in shared memory
 constexpr int BIG_ROW = 2048;         // cut-subtree members with longer rows: CTA-wide
@@ -806,8 +807,9 @@ __device__ __forceinline__ void mark_dirty(int32_t y, uint8_t *gflag, int32_t *d
 __global__ void __launch_bounds__(GB) k_giant_cta(GiantArgs A, const GPart *parts, GOut O,
                                                   int32_t *neg_pool, int32_t *dirty_pool,
                                                   uint8_t *gflag, uint8_t *negflag) {
-    __shared__ double tg[GSORT];
-    __shared__ int32_t tx[GSORT];
+    extern __shared__ __align__(16) unsigned char g_dyn[];
+    double *tg = (double *)g_dyn;
+    int32_t *tx = (int32_t *)(g_dyn + (size_t)GSORT * sizeof(double));
     __shared__ double sg[32];
     __shared__ int32_t sxx[32];
     __shared__ int si[32];
@@ -1794,7 +1796,13 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
             k_gb_totals<<<(unsigned)((np + 127) / 128), 128, 0, s>>>(dsl, ns, pso2.p, psi2.p,
                                                                      dparts2.p);
             CUDA_TRY(cudaMemsetAsync(cnt6.p + 3, 0, 4, s));
-            k_giant_cta<<<(unsigned)np, GB, 0, s>>>(GA, dparts2.p, O, neg_pool.p, dirty_pool.p,
+            static bool smem_set = false;
+            if (!smem_set) {
+                CUDA_TRY(cudaFuncSetAttribute(k_giant_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)GSMEM));
+                smem_set = true;
+            }
+            k_giant_cta<<<(unsigned)np, GB, GSMEM, s>>>(GA, dparts2.p, O, neg_pool.p, dirty_pool.p,
                                                     gflag.p, negflag.p);
             CUDA_TRY(cudaGetLastError());
             int32_t nnext = 0;
