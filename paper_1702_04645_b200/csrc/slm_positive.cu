@@ -613,22 +613,65 @@ __global__ void k_gb_lca(GiantArgs A, const GSlice *S, int ns, const int64_t *ch
         const int32_t pid = A.gmark[y];
         const int64_t b0 = A.ioff[y], cnt = A.icnt[y];
         const int64_t q0 = b0 + c * GCH, q1 = b0 + min(cnt, (c + 1) * (int64_t)GCH);
-        // deposits are cached per lane while the LCA repeats (in a hub-centred tree most
-        // edges meet at the root: one atomic per run instead of one per edge)
+        // y's ancestor chain is shared by the whole row: lane i holds level i (node and DFS
+        // interval), extended one level at a time only as far as some lane's entry needs, so
+        // every entry finds its LCA by shuffles; entries above 32 levels walk on from there.
+        // Deposits are cached per lane while the LCA repeats (in a hub-centred tree most
+        // edges meet at the root: one atomic per run instead of one per edge).
+        int32_t ch_node = -1, ch_lo = 0, ch_hi = 0;
+        int clen = 0;
+        int32_t nxt = y;   // next node to append to the chain
         int32_t ca = -1;
         double cv = 0.0;
-        for (int64_t q = q0 + lane; q < q1; q += 32) {
-            const int32_t z = A.iz[q];
-            if (A.gmark[z] != pid) continue;
-            const int32_t pz = A.pos[z];
-            int32_t anc = y;
-            while (!in_range(A, anc, pz)) anc = A.a[anc];
-            if (anc != ca) {
-                if (ca >= 0) atomicAdd(&A.dep[ca], cv);
-                ca = anc;
-                cv = 0.0;
+        for (int64_t qb = q0; qb < q1; qb += 32) {
+            const int64_t q = qb + lane;
+            bool need = false;
+            int32_t pz = 0;
+            double u = 0.0;
+            if (q < q1) {
+                const int32_t z = A.iz[q];
+                u = A.iu[q];
+                if (A.gmark[z] == pid) {
+                    need = true;
+                    pz = A.pos[z];
+                }
             }
-            cv -= A.iu[q];
+            int32_t anc = -1;
+            for (int L = 0; L < clen; L++) {
+                const int32_t lo = __shfl_sync(0xffffffffu, ch_lo, L);
+                const int32_t hi = __shfl_sync(0xffffffffu, ch_hi, L);
+                const int32_t nd = __shfl_sync(0xffffffffu, ch_node, L);
+                if (need && anc < 0 && pz >= lo && pz < hi) anc = nd;
+            }
+            while (clen < 32 && __any_sync(0xffffffffu, need && anc < 0)) {
+                const int32_t nd = nxt;   // uniform across the warp
+                const int32_t pa = A.pos[nd], sa = A.sz[nd], an = A.a[nd];
+                if (lane == clen) {
+                    ch_node = nd;
+                    ch_lo = pa;
+                    ch_hi = pa + sa;
+                }
+                clen++;
+                nxt = an;
+                if (need && anc < 0 && pz >= pa && pz < pa + sa) anc = nd;
+            }
+            if (need && anc < 0) {   // deeper than 32 levels: walk on from the chain's end
+                int32_t w2 = nxt;
+                for (;;) {
+                    const int32_t pa = A.pos[w2], sa = A.sz[w2], an = A.a[w2];
+                    if (pz >= pa && pz < pa + sa) break;
+                    w2 = an;
+                }
+                anc = w2;
+            }
+            if (need) {
+                if (anc != ca) {
+                    if (ca >= 0) atomicAdd(&A.dep[ca], cv);
+                    ca = anc;
+                    cv = 0.0;
+                }
+                cv -= u;
+            }
         }
         if (ca >= 0) atomicAdd(&A.dep[ca], cv);
     }
