@@ -356,6 +356,7 @@ struct GiantArgs {
     int32_t *icnt;
     int32_t *iz;
     double *iu;
+    int32_t *iy;             // owner of each entry (the flat LCA pass of wave 0)
     double m, m2;
 };
 
@@ -589,6 +590,7 @@ __global__ void k_gb_ifill(GiantArgs A, const GSlice *S, int ns, const int64_t *
                 const int64_t q = A.ioff[x] + at + __popc(hm & ((1u << lane) - 1));
                 A.iz[q] = z;
                 A.iu[q] = A.uu[e];
+                A.iy[q] = x;
             }
         }
     }
@@ -676,6 +678,47 @@ __global__ void k_gb_lca(GiantArgs A, const GSlice *S, int ns, const int64_t *ch
         if (ca >= 0) atomicAdd(&A.dep[ca], cv);
     }
 }
+// wave 0: one thread per intra-list entry (the lists are short, so a warp per member row
+// leaves most lanes idle).  The owner y walks up to the lowest ancestor whose DFS interval
+// holds z; runs of equal ancestors across the warp's lanes share one atomic.
+__global__ void k_gb_lca_flat(GiantArgs A, int64_t nintra) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31LL; b < nintra;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t q = b + lane;
+        int32_t anc = -1;
+        double v = 0.0;
+        if (q < nintra) {
+            const int32_t y = A.iy[q], z = A.iz[q];
+            const double u = A.iu[q];
+            const int32_t gy = A.gmark[y], gz = A.gmark[z], pz = A.pos[z];
+            if (gy == gz) {
+                int32_t w = y;
+                int32_t pa = A.pos[w], sa = A.sz[w], nx = A.a[w];
+                while (!(pz >= pa && pz < pa + sa)) {
+                    w = nx;
+                    pa = A.pos[w];
+                    sa = A.sz[w];
+                    nx = A.a[w];
+                }
+                anc = w;
+                v = -u;
+            }
+        }
+        // segmented scan over runs of equal ancestors (a value may recur in later runs)
+        const int32_t pa = __shfl_up_sync(0xffffffffu, anc, 1);
+        const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || pa != anc);
+        const int start = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const double ov = __shfl_up_sync(0xffffffffu, v, off);
+            if (lane - off >= start) v += ov;
+        }
+        const int32_t na = __shfl_down_sync(0xffffffffu, anc, 1);
+        if (anc >= 0 && (lane == 31 || na != anc)) atomicAdd(&A.dep[anc], v);
+    }
+}
+
 __global__ void k_gb_gather(GiantArgs A, const GSlice *S, int ns, int64_t N, double *vso,
                             double *vsi, double *vdp) {
     GS_LOOP(t, N) {
@@ -1443,7 +1486,7 @@ struct PosScratch {
     DBuf<GPart> dparts2;
     DBuf<double> accl;
     DBuf<int64_t> ioff, icnt_flat, ioff_flat;
-    DBuf<int32_t> icnt, iz;
+    DBuf<int32_t> icnt, iz, iy;
     DBuf<double> iu;
 };
 
@@ -1651,6 +1694,8 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
         GA.icnt = SC.icnt.p;
         GA.iz = nullptr;
         GA.iu = nullptr;
+        GA.iy = nullptr;
+        int64_t nintra_w0 = 0;
         bool first_wave = true;
         GA.m = m;
         GA.m2 = m * m;
@@ -1801,14 +1846,20 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
                 CUDA_TRY(cudaStreamSynchronize(s));
                 SC.iz.resize(std::max<int64_t>(1, nintra));
                 SC.iu.resize(std::max<int64_t>(1, nintra));
+                SC.iy.resize(std::max<int64_t>(1, nintra));
                 GA.iz = SC.iz.p;
                 GA.iu = SC.iu.p;
+                GA.iy = SC.iy.p;
+                nintra_w0 = nintra;
                 k_gb_ioff<<<grid_for(N, 256), 256, 0, s>>>(GA, dsl, ns, N, SC.ioff_flat.p);
                 k_gb_ifill<<<GW, 256, 0, s>>>(GA, dsl, ns, SC.chunks.p, nck);
                 first_wave = false;
             }
             k_gb_dep<<<grid_for(N, 256), 256, 0, s>>>(GA, dsl, ns, N);
-            k_gb_lca<<<GW, 256, 0, s>>>(GA, dsl, ns, SC.chunks.p, nck);
+            if (build_intra && getenv("SLM_LCA_CHUNKS") == nullptr)
+                k_gb_lca_flat<<<grid_for(nintra_w0, 256, 148LL * 32), 256, 0, s>>>(GA, nintra_w0);
+            else
+                k_gb_lca<<<GW, 256, 0, s>>>(GA, dsl, ns, SC.chunks.p, nck);
             vso.resize(N + 1);
             vsi.resize(N + 1);
             vdp.resize(N + 1);
