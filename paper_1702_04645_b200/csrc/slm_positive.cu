@@ -590,7 +590,7 @@ __global__ void k_gb_ifill(GiantArgs A, const GSlice *S, int ns, const int64_t *
                 const int64_t q = A.ioff[x] + at + __popc(hm & ((1u << lane) - 1));
                 A.iz[q] = z;
                 A.iu[q] = A.uu[e];
-                A.iy[q] = x;
+                if (A.iy) A.iy[q] = x;
             }
         }
     }
@@ -1846,17 +1846,24 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
                 CUDA_TRY(cudaStreamSynchronize(s));
                 SC.iz.resize(std::max<int64_t>(1, nintra));
                 SC.iu.resize(std::max<int64_t>(1, nintra));
-                SC.iy.resize(std::max<int64_t>(1, nintra));
                 GA.iz = SC.iz.p;
                 GA.iu = SC.iu.p;
-                GA.iy = SC.iy.p;
-                nintra_w0 = nintra;
+                // entry owners for the flat LCA pass; lists beyond 2^27 entries (a giant part
+                // spanning most of the graph) keep the warp-per-row pass and its memory
+                nintra_w0 = nintra <= (int64_t(1) << 27) ? nintra : 0;
+                if (nintra_w0 > 0) {
+                    SC.iy.resize(nintra_w0);
+                    GA.iy = SC.iy.p;
+                } else {
+                    SC.iy.release();
+                    GA.iy = nullptr;
+                }
                 k_gb_ioff<<<grid_for(N, 256), 256, 0, s>>>(GA, dsl, ns, N, SC.ioff_flat.p);
                 k_gb_ifill<<<GW, 256, 0, s>>>(GA, dsl, ns, SC.chunks.p, nck);
                 first_wave = false;
             }
             k_gb_dep<<<grid_for(N, 256), 256, 0, s>>>(GA, dsl, ns, N);
-            if (build_intra && getenv("SLM_LCA_CHUNKS") == nullptr)
+            if (build_intra && nintra_w0 > 0 && getenv("SLM_LCA_CHUNKS") == nullptr)
                 k_gb_lca_flat<<<grid_for(nintra_w0, 256, 148LL * 32), 256, 0, s>>>(GA, nintra_w0);
             else
                 k_gb_lca<<<GW, 256, 0, s>>>(GA, dsl, ns, SC.chunks.p, nck);

@@ -8,6 +8,7 @@ ctx = _lib.Context(0)
 GN.build_on_device(ctx, cfg)
 print("build", ctx.phase_times(reset=True))
 info = ctx.info(); g = Graph(info["n"], None, None, None); g._ctx = ctx; ctx.level = 0
-t = time.perf_counter(); r = detector.run(g, RunConfig()); el = time.perf_counter() - t
+gam = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
+t = time.perf_counter(); r = detector.run(g, RunConfig(resolution=gam)); el = time.perf_counter() - t
 pt = ctx.phase_times(reset=True)
 print(f"run {el:.3f} s Q {r.final_score:.9f} alloc_ms {pt['alloc_ms']} calls {pt['alloc_calls']}", {k: round(v, 3) for k, v in r.stats.phase_seconds.items()})
