@@ -12,3 +12,5 @@ gam = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
 t = time.perf_counter(); r = detector.run(g, RunConfig(resolution=gam)); el = time.perf_counter() - t
 pt = ctx.phase_times(reset=True)
 print(f"run {el:.3f} s Q {r.final_score:.9f} alloc_ms {pt['alloc_ms']} calls {pt['alloc_calls']}", {k: round(v, 3) for k, v in r.stats.phase_seconds.items()})
+if os.environ.get("SLM_PROFILE"):
+    print("phase_ms", pt)
