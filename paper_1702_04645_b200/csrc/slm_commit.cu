@@ -137,6 +137,7 @@ struct CommitArgs {
     const int32_t *cptr, *order, *pos, *sz;
     const int32_t *cand, *cstar;
     double m, m2;
+    int runs;                 // run commits after a commit (walk_run; SLM_WALK_RUNS=0 disables)
 };
 
 // candidates whose tail has more members than this, or whose tail rows hold more union
@@ -1016,6 +1017,111 @@ __device__ __forceinline__ int walk_classify(const CommitArgs &A, const Live &V,
     return cls;
 }
 
+// after a commit into C, the batch's following events [s0, nb) are decided in one pass while
+// they stay simple: candidates into C with a parked clean source and no moving neighbour
+// (their w_to is the snapshot's, whatever moved) and resolved skips out of C.  The
+// decisions are the serial ones: the lanes replay them in order with C's running totals (a
+// commit also marks later candidates out of the same source), then apply every commit's
+// state at once, fence, and publish the verdicts.  Returns the first event left undecided.
+__device__ __forceinline__ int walk_run(const CommitArgs &A, const Live &V, int32_t *status,
+                                        int32_t C, int s0, int nb, WalkEv &e, WalkState &W,
+                                        int &nres, int &ncommit) {
+    const int lane = threadIdx.x & 31;
+    // 0 stop, 1 no effect, 2 skip, 3 gain decides
+    int kind = 1;
+    if (lane >= s0 && lane < nb) {
+        if (e.to != C) {
+            kind = e.st == ST_SKIP ? 1 : 0;
+        } else if (e.st != ST_UNRES) {
+            kind = 1;
+        } else if (e.dF) {
+            kind = 2;
+        } else {
+            if (e.atF != e.k) {
+                e.atF = ld_acq(V.atk + e.frm);
+                if (e.atF == e.k) {
+                    e.SoF = V.S_out[e.frm];
+                    e.SiF = V.S_in[e.frm];
+                }
+            }
+            const int df = vload8(V.dirty + e.frm);
+            if (df) kind = 2;
+            else if (e.atF != e.k || e.cs.mv_cnt > 0) kind = 0;
+            else kind = 3;
+        }
+    }
+    int end = nb;
+    int mydec = 0;   // 1 skip, 2 commit
+    double myg = 0.0;
+    for (int l = s0; l < nb; l++) {
+        const int kl = __shfl_sync(0xffffffffu, kind, l);
+        if (kl == 0) {
+            end = l;
+            break;
+        }
+        if (kl == 1) continue;
+        const int dl = __shfl_sync(0xffffffffu, e.dF, l);
+        const double so_b = __shfl_sync(0xffffffffu, e.cs.so_b, l);
+        const double si_b = __shfl_sync(0xffffffffu, e.cs.si_b, l);
+        const double SoF = __shfl_sync(0xffffffffu, e.SoF, l);
+        const double SiF = __shfl_sync(0xffffffffu, e.SiF, l);
+        const double wt = __shfl_sync(0xffffffffu, e.cs.w_to, l);
+        const double wf = __shfl_sync(0xffffffffu, e.cs.w_from, l);
+        const int32_t jl = __shfl_sync(0xffffffffu, e.cs.j, l);
+        const int32_t fl = __shfl_sync(0xffffffffu, e.frm, l);
+        const int32_t len = __shfl_sync(0xffffffffu, e.cs.tail_hi - e.cs.tail_lo, l);
+        bool commit = false;
+        double g = 0.0;
+        if (kl == 3 && !dl) {
+            // gain_switch d_null (quality.py:216-219), exact operand order
+            const double d_null = -SoF * si_b - so_b * SiF + W.SoC * si_b + so_b * W.SiC +
+                                  2.0 * so_b * si_b;
+            g = (wt - wf) / A.m - d_null / (A.m * A.m);
+            commit = g > 0.0 && jl >= 0;   // detector.py:498-502
+        }
+        if (lane == l) {
+            mydec = commit ? 2 : 1;
+            myg = g;
+        }
+        if (commit) {
+            W.SoC += so_b;
+            W.SiC += si_b;
+            W.cntC += len;
+            if (lane > l && e.frm == fl) e.dF = 1;   // later candidates out of the same source
+        }
+    }
+    const unsigned cm = __ballot_sync(0xffffffffu, mydec == 2);
+    if (mydec == 2) {
+        const int32_t len = e.cs.tail_hi - e.cs.tail_lo;
+        for (int32_t t = e.cs.tail_lo; t < e.cs.tail_hi; t++) V.lab[A.order[t]] = C;
+        V.a[e.i] = e.cs.j;
+        // move_nodes (quality.py:87-95)
+        V.S_out[e.frm] -= e.cs.so_b;
+        V.S_in[e.frm] -= e.cs.si_b;
+        V.cnt[e.frm] -= len;
+        V.dirty[e.frm] = 1;
+        atomicMin(&V.first_commit[e.frm], e.k);
+        atomicMin(&V.first_commit[C], e.k);
+        V.gain[e.k] = myg;
+    }
+    if (cm && lane == 0) {
+        V.S_out[C] = W.SoC;
+        V.S_in[C] = W.SiC;
+        V.cnt[C] = W.cntC;
+        V.dirty[C] = 1;
+    }
+    __syncwarp();
+    if (cm) __threadfence();   // state and labels before the verdicts
+    __syncwarp();
+    if (mydec) {
+        *(volatile int32_t *)(status + e.k) = mydec == 2 ? ST_COMMIT : ST_SKIP;
+        e.st = mydec == 2 ? ST_COMMIT : ST_SKIP;
+    }
+    nres += __popc(__ballot_sync(0xffffffffu, mydec != 0));
+    ncommit += __popc(cm);
+    return end;
+}
+
 // one warp batch: the events [p, p + nb) (lane < nb holds event p + lane, record rec) against
 // W; returns the events consumed (nb, or fewer when the walker parks)
 __device__ __forceinline__ int walk_batch(const CommitArgs &A, const Live &V, int32_t *status,
@@ -1143,6 +1249,8 @@ __device__ __forceinline__ int walk_batch(const CommitArgs &A, const Live &V, in
         if (lane == f) e.st = commit ? ST_COMMIT : ST_SKIP;
         nres++;
         start = f + 1;
+        if (commit && A.runs && start < nb)
+            start = walk_run(A, V, status, C, start, nb, e, W, nres, ncommit);
     }
     return nb;
 }
@@ -1429,6 +1537,10 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     k_coins<<<grid_for(K, 256), 256, 0, s>>>(cand.p, K, mix_key2(seed, level, sweep), accept_prob,
                                              status.p);
     CommitArgs A;
+    {
+        static const bool no_runs = getenv("SLM_WALK_RUNS") && atoi(getenv("SLM_WALK_RUNS")) == 0;
+        A.runs = no_runs ? 0 : 1;
+    }
     A.uptr = G.uptr.p;
     A.unbr = G.unbr.p;
     A.uu = G.uu.p;

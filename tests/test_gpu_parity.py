@@ -438,3 +438,36 @@ def test_local_gains_without_wown_matches(tmp_path):
     assert res["1"].files == res["0"].files
     for k in res["1"].files:
         np.testing.assert_array_equal(res["1"][k], res["0"][k])
+
+
+@pytest.mark.gpu
+def test_walker_runs_match_single_commits(tmp_path):
+    """Commit walkers deciding the simple events after a commit in one pass (default) and
+    one event per step (SLM_WALK_RUNS=0) give the same hierarchies, at gamma 1 and 0.5."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "runs.py"
+    script.write_text(
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {root!r})\n"
+        "import paper_1702_04645_b200 as slm\n"
+        "from paper_1702_04645_b200 import generators as GN\n"
+        "out = []\n"
+        "for (n, s, d, w), gam in ((GN.rmat(15, 16, 1, 4), 1.0), (GN.rmat(15, 16, 1, 4), 0.5),\n"
+        "                          (GN.generate('c1_sbm'), 0.5)):\n"
+        "    r = slm.run(slm.Graph.from_edges(n, s, d, w), slm.RunConfig(resolution=gam))\n"
+        "    out += list(r.hierarchy.levels) + [np.array(r.stats.sweeps_per_level),\n"
+        "            np.array([r.stats.accepted_moves, r.stats.accepted_splits, r.stats.unresolved_negative]),\n"
+        "            np.array([r.final_score])]\n"
+        "np.savez(sys.argv[1], *out)\n")
+    res = {}
+    for mode in ("1", "0"):
+        f = tmp_path / f"r{mode}.npz"
+        subprocess.run([sys.executable, str(script), str(f)], check=True, cwd=root,
+                       env=dict(os.environ, SLM_WALK_RUNS=mode))
+        res[mode] = np.load(f)
+    assert res["1"].files == res["0"].files
+    for k in res["1"].files:
+        np.testing.assert_array_equal(res["1"][k], res["0"][k])
