@@ -1046,8 +1046,8 @@ __device__ __forceinline__ int walk_run(const CommitArgs &A, const Live &V, int3
             }
             const int df = vload8(V.dirty + e.frm);
             if (df) kind = 2;
-            else if (e.atF != e.k || e.cs.mv_cnt > 0) kind = 0;
-            else kind = 3;
+            else if (e.atF != e.k) kind = 0;
+            else kind = e.cs.mv_cnt > 0 ? 4 : 3;
         }
     }
     int end = nb;
@@ -1055,8 +1055,9 @@ __device__ __forceinline__ int walk_run(const CommitArgs &A, const Live &V, int3
     double myg = 0.0;
     for (int l = s0; l < nb; l++) {
         const int kl = __shfl_sync(0xffffffffu, kind, l);
-        if (kl == 0) {
+        if (kl <= 0) {
             end = l;
+            if (V.wst && lane == 0) atomicAdd(V.wst + (kl < 0 ? 3 : 4), 1ull);
             break;
         }
         if (kl == 1) continue;
@@ -1065,14 +1066,32 @@ __device__ __forceinline__ int walk_run(const CommitArgs &A, const Live &V, int3
         const double si_b = __shfl_sync(0xffffffffu, e.cs.si_b, l);
         const double SoF = __shfl_sync(0xffffffffu, e.SoF, l);
         const double SiF = __shfl_sync(0xffffffffu, e.SiF, l);
-        const double wt = __shfl_sync(0xffffffffu, e.cs.w_to, l);
+        double wt = __shfl_sync(0xffffffffu, e.cs.w_to, l);
         const double wf = __shfl_sync(0xffffffffu, e.cs.w_from, l);
-        const int32_t jl = __shfl_sync(0xffffffffu, e.cs.j, l);
+        int32_t jl = __shfl_sync(0xffffffffu, e.cs.j, l);
+        if (kl == 4 && !dl) {
+            // moving neighbours: the whole warp re-prices the candidate now, the labels of
+            // every commit before it (this run's included) being written
+            CandSpec c;
+            c.w_to = wt;
+            c.w_from = wf;
+            c.so_b = so_b;
+            c.si_b = si_b;
+            c.j = jl;
+            c.tail_lo = __shfl_sync(0xffffffffu, e.cs.tail_lo, l);
+            c.tail_hi = __shfl_sync(0xffffffffu, e.cs.tail_hi, l);
+            c.pgj = __shfl_sync(0xffffffffu, e.cs.pgj, l);
+            c.je = __shfl_sync(0xffffffffu, e.cs.je, l);
+            c.mv_off = __shfl_sync(0xffffffffu, e.cs.mv_off, l);
+            c.mv_cnt = __shfl_sync(0xffffffffu, e.cs.mv_cnt, l);
+            const int32_t il = __shfl_sync(0xffffffffu, e.i, l);
+            reprice(A, V.mv, V.lab, c, il, C, wt, jl);
+        }
         const int32_t fl = __shfl_sync(0xffffffffu, e.frm, l);
         const int32_t len = __shfl_sync(0xffffffffu, e.cs.tail_hi - e.cs.tail_lo, l);
         bool commit = false;
         double g = 0.0;
-        if (kl == 3 && !dl) {
+        if (kl >= 3 && !dl) {
             // gain_switch d_null (quality.py:216-219), exact operand order
             const double d_null = -SoF * si_b - so_b * SiF + W.SoC * si_b + so_b * W.SiC +
                                   2.0 * so_b * si_b;
@@ -1082,8 +1101,13 @@ __device__ __forceinline__ int walk_run(const CommitArgs &A, const Live &V, int3
         if (lane == l) {
             mydec = commit ? 2 : 1;
             myg = g;
+            if (commit) {
+                for (int32_t t = e.cs.tail_lo; t < e.cs.tail_hi; t++) V.lab[A.order[t]] = C;
+                e.cs.j = jl;
+            }
         }
         if (commit) {
+            __syncwarp();   // the labels before any later re-pricing
             W.SoC += so_b;
             W.SiC += si_b;
             W.cntC += len;
@@ -1093,8 +1117,7 @@ __device__ __forceinline__ int walk_run(const CommitArgs &A, const Live &V, int3
     const unsigned cm = __ballot_sync(0xffffffffu, mydec == 2);
     if (mydec == 2) {
         const int32_t len = e.cs.tail_hi - e.cs.tail_lo;
-        for (int32_t t = e.cs.tail_lo; t < e.cs.tail_hi; t++) V.lab[A.order[t]] = C;
-        V.a[e.i] = e.cs.j;
+        V.a[e.i] = e.cs.j;   // (the re-priced attach target)
         // move_nodes (quality.py:87-95)
         V.S_out[e.frm] -= e.cs.so_b;
         V.S_in[e.frm] -= e.cs.si_b;
