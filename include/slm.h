@@ -138,14 +138,10 @@ SLM_API int slm_phase_times(slm_ctx *ctx, double *ms, int32_t nmax, int32_t rese
 SLM_API int slm_last_commit_stats(slm_ctx *ctx, int64_t *candidates, int64_t *rounds);
 
 /* ---- synthetic inputs (BASELINE.json configs) ------------ */
-/* Symmetrised R-MAT with permuted ids, self-loops dropped; weight_mode 0 = unit,
- * 1 = uniform integers in [1, 100].  Host twin: pass src == NULL to query the count. */
-SLM_API int slm_gen_rmat_host(int scale, int edge_factor, double a, double b, double c, uint64_t seed,
-                      int weight_mode, int64_t *src, int64_t *dst, double *w, int64_t *n_edges);
-/* Random geometric graph in the unit square (both directions, unit weights). */
-SLM_API int slm_gen_rgg_host(int64_t n, double radius, uint64_t seed, int64_t *src, int64_t *dst,
-                     double *w, int64_t *n_edges);
-/* Device generation of the same edge lists straight into the level-0 build. */
+/* Device generators: symmetrised R-MAT with permuted ids, self-loops dropped (weight_mode
+ * 0 = unit, 1 = uniform integers in [1, 100]), and the random geometric graph in the unit
+ * square, generated in HBM straight into the level-0 build.  Their host twins (the same edge
+ * multisets, for the oracle and the tests) live outside this library, in workloads/gen_host.c. */
 SLM_API int slm_build_rmat(slm_ctx *ctx, int scale, int edge_factor, double a, double b, double c,
                    uint64_t seed, int weight_mode);
 SLM_API int slm_build_rgg(slm_ctx *ctx, int64_t n, double radius, uint64_t seed);

@@ -69,6 +69,10 @@ def lib():
         L.orc_positive.restype = C.c_int
         L.orc_positive.argtypes = [vp, C.c_double, _i64p, _i64p, i64, i64,
                                    C.POINTER(i64), C.POINTER(i64), _f64p, i64, C.POINTER(i64)]
+        L.orc_positive_fast.restype = C.c_int
+        L.orc_positive_fast.argtypes = L.orc_positive.argtypes
+        L.orc_graph_integral.restype = C.c_int
+        L.orc_graph_integral.argtypes = [vp]
         L.orc_plan.argtypes = [vp, C.c_double, _i64p, i64, _i64p]
         L.orc_plan_rows.argtypes = [vp, C.c_double, _i64p, _f64p, _f64p, i64, i64, _i64p]
         L.orc_plan_sample.argtypes = [_i64p, _i64p, _f64p, _f64p, _f64p, C.c_double, _i64p,
@@ -99,6 +103,7 @@ class OGraph:
         n, ne, ue, m = C.c_int64(), C.c_int64(), C.c_int64(), C.c_double()
         lib().orc_graph_sizes(handle, C.byref(n), C.byref(ne), C.byref(ue), C.byref(m))
         self.n, self.ne, self.ue, self.m_w = n.value, ne.value, ue.value, m.value
+        self.integral = bool(lib().orc_graph_integral(handle))
 
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None:
@@ -177,13 +182,22 @@ def local_gains(g: OGraph, labels, n_comms, m=None):
     return lg
 
 
-def positive_correction(g: OGraph, a, comm, n_comms, scc_cut_cap=10_000, m=None):
-    """detector.py:338-362 -> (a_new, changed, splits, unresolved, gains, n_warnings)."""
+def positive_correction(g: OGraph, a, comm, n_comms, scc_cut_cap=10_000, m=None, fast=None):
+    """detector.py:338-362 -> (a_new, changed, splits, unresolved, gains, n_warnings).
+
+    ``fast`` (default: whenever the graph's weights are integers) selects the exact-sum
+    evaluation order of orc_positive_fast -- the same outputs, O(part) per cut instead of a
+    subtree search per member (slm_oracle.c); ``fast=False`` forces the literal form."""
     a = _i64(a).copy()
     splits, unres, nw = C.c_int64(), C.c_int64(), C.c_int64()
     cap = g.n + 1
     gains = np.empty(cap, np.float64)
-    ch = lib().orc_positive(g._h, g.m_w if m is None else m, a, _i64(comm), n_comms,
+    if fast is None:
+        fast = g.integral
+    if fast and not g.integral:
+        raise ValueError("the fast POSITIVE form needs integer weights")
+    fn = lib().orc_positive_fast if fast else lib().orc_positive
+    ch = fn(g._h, g.m_w if m is None else m, a, _i64(comm), n_comms,
                             scc_cut_cap, C.byref(splits), C.byref(unres), gains, cap,
                             C.byref(nw))
     return a, bool(ch), splits.value, unres.value, list(gains[:min(splits.value, cap)]), nw.value

@@ -114,114 +114,170 @@ typedef struct {
     int64_t *uptr, *unbr;              /* graph.py:151-175 (NeighborUnion ptr/nbr) */
     double *uu;                        /* w_out + w_in per union entry (F6) */
     double *s_out, *s_in, m;           /* graph.py:257-263 */
+    int64_t *in_ptr, *in_e;            /* in-CSR: CSR entry indices per destination */
+    int integral;                      /* every weight an integer, m < 2^52: sums exact */
 } orc_graph;
+
+static int g_threads = 1;
+EXPORT void orc_set_threads(int t) { g_threads = t > 0 ? t : 1; }
+
+static int cmp_u64(const void *x, const void *y) {
+    uint64_t a = *(const uint64_t *)x, b = *(const uint64_t *)y;
+    return (a > b) - (a < b);
+}
+static void sort_u64(uint64_t *v, int64_t n) {
+    if (n <= 24) {
+        for (int64_t k = 1; k < n; k++) {
+            uint64_t x = v[k];
+            int64_t q = k - 1;
+            while (q >= 0 && v[q] > x) { v[q + 1] = v[q]; q--; }
+            v[q + 1] = x;
+        }
+    } else {
+        qsort(v, (size_t)n, sizeof(uint64_t), cmp_u64);
+    }
+}
+
+/* Bucket entries [0, m) by row[] into a CSR (ptr[n+1], idx[m]) holding, per row, the entry
+ * indices in ascending order: the order a stable sort by row produces.  Parallel (atomic
+ * counts and fills, then an ascending sort inside each row). */
+static void bucket_stable(const int64_t *row, int64_t m, int64_t n, int64_t *ptr, int64_t *idx) {
+    memset(ptr, 0, (size_t)(n + 1) * sizeof(int64_t));
+#pragma omp parallel for schedule(static) num_threads(g_threads)
+    for (int64_t i = 0; i < m; i++) __atomic_fetch_add(&ptr[row[i] + 1], 1, __ATOMIC_RELAXED);
+    for (int64_t r = 0; r < n; r++) ptr[r + 1] += ptr[r];
+    int64_t *fill = (int64_t *)malloc((size_t)(n ? n : 1) * sizeof(int64_t));
+    memcpy(fill, ptr, (size_t)n * sizeof(int64_t));
+#pragma omp parallel for schedule(static) num_threads(g_threads)
+    for (int64_t i = 0; i < m; i++)
+        idx[__atomic_fetch_add(&fill[row[i]], 1, __ATOMIC_RELAXED)] = i;
+    free(fill);
+#pragma omp parallel for schedule(dynamic, 1024) num_threads(g_threads)
+    for (int64_t r = 0; r < n; r++)
+        sort_u64((uint64_t *)idx + ptr[r], ptr[r + 1] - ptr[r]);
+}
 
 /* Union of out- and in-neighbours minus self-loops (graph.py:151-175).  The reference
  * lexsorts the concatenation [forward; reverse] and reduceats each (row, nbr) group; a
  * group holds at most one forward and one reverse entry, so w_out = W(i,j) (+0.0) and
- * w_in = W(j,i) (+0.0) exactly and the consumers' w_out + w_in is W(i,j) + W(j,i). */
+ * w_in = W(j,i) (+0.0) exactly and the consumers' w_out + w_in is W(i,j) + W(j,i).
+ * The in-CSR is the stable sort of the CSR entries by destination (graph.py:111-115):
+ * per destination, the entries in CSR order, i.e. by ascending source. */
 static void build_union(orc_graph *g) {
     int64_t n = g->n, ne = g->ne;
-    /* in-CSR: stable counting sort of CSR entries by dst (graph.py:111-115) */
-    int64_t *in_ptr = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
-    int64_t *in_src = (int64_t *)malloc((size_t)(ne ? ne : 1) * sizeof(int64_t));
-    double *in_w = (double *)malloc((size_t)(ne ? ne : 1) * sizeof(double));
-    for (int64_t e = 0; e < ne; e++) in_ptr[g->out_dst[e] + 1]++;
-    for (int64_t i = 0; i < n; i++) in_ptr[i + 1] += in_ptr[i];
-    int64_t *fill = (int64_t *)malloc((size_t)(n ? n : 1) * sizeof(int64_t));
-    memcpy(fill, in_ptr, (size_t)n * sizeof(int64_t));
+    int64_t *in_ptr = (int64_t *)malloc((size_t)(n + 1) * sizeof(int64_t));
+    int64_t *in_e = (int64_t *)malloc((size_t)(ne ? ne : 1) * sizeof(int64_t));
+    int64_t *esrc = (int64_t *)malloc((size_t)(ne ? ne : 1) * sizeof(int64_t));
+#pragma omp parallel for schedule(dynamic, 4096) num_threads(g_threads)
     for (int64_t i = 0; i < n; i++)
-        for (int64_t e = g->out_ptr[i]; e < g->out_ptr[i + 1]; e++) {
-            int64_t p = fill[g->out_dst[e]]++;
-            in_src[p] = i;
-            in_w[p] = g->out_w[e];
-        }
-    free(fill);
-    /* count */
+        for (int64_t e = g->out_ptr[i]; e < g->out_ptr[i + 1]; e++) esrc[e] = i;
+    bucket_stable(g->out_dst, ne, n, in_ptr, in_e);
+    g->in_ptr = in_ptr;
+    g->in_e = in_e;
     g->uptr = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
-    int64_t total = 0;
     for (int pass = 0; pass < 2; pass++) {
         if (pass == 1) {
-            g->ue = total;
-            g->unbr = (int64_t *)malloc((size_t)(total ? total : 1) * sizeof(int64_t));
-            g->uu = (double *)malloc((size_t)(total ? total : 1) * sizeof(double));
+            for (int64_t i = 0; i < n; i++) g->uptr[i + 1] += g->uptr[i];
+            g->ue = g->uptr[n];
+            g->unbr = (int64_t *)malloc((size_t)(g->ue ? g->ue : 1) * sizeof(int64_t));
+            g->uu = (double *)malloc((size_t)(g->ue ? g->ue : 1) * sizeof(double));
         }
-        total = 0;
+#pragma omp parallel for schedule(dynamic, 1024) num_threads(g_threads)
         for (int64_t i = 0; i < n; i++) {
-            if (pass == 0) g->uptr[i] = total;
             int64_t a = g->out_ptr[i], ae = g->out_ptr[i + 1];
             int64_t b = in_ptr[i], be = in_ptr[i + 1];
+            int64_t k = pass ? g->uptr[i] : 0;
             for (;;) {
                 while (a < ae && g->out_dst[a] == i) a++;
-                while (b < be && in_src[b] == i) b++;
+                while (b < be && esrc[in_e[b]] == i) b++;
                 if (a >= ae && b >= be) break;
                 int64_t j;
                 double u;
-                if (b >= be || (a < ae && g->out_dst[a] < in_src[b])) {
+                int64_t bs = b < be ? esrc[in_e[b]] : 0;
+                if (b >= be || (a < ae && g->out_dst[a] < bs)) {
                     j = g->out_dst[a]; u = g->out_w[a] + 0.0; a++;
-                } else if (a >= ae || in_src[b] < g->out_dst[a]) {
-                    j = in_src[b]; u = 0.0 + in_w[b]; b++;
+                } else if (a >= ae || bs < g->out_dst[a]) {
+                    j = bs; u = 0.0 + g->out_w[in_e[b]]; b++;
                 } else {
-                    j = g->out_dst[a]; u = g->out_w[a] + in_w[b]; a++; b++;
+                    j = g->out_dst[a]; u = g->out_w[a] + g->out_w[in_e[b]]; a++; b++;
                 }
-                if (pass == 1) { g->unbr[total] = j; g->uu[total] = u; }
-                total++;
+                if (pass) { g->unbr[k] = j; g->uu[k] = u; }
+                k++;
             }
+            if (!pass) g->uptr[i + 1] = k;
         }
-        if (pass == 0) g->uptr[n] = total;
     }
-    free(in_ptr); free(in_src); free(in_w);
+    free(esrc);
 }
 
-/* strengths (graph.py:257-263): bincount (sequential) for s_out, s_in; pairwise m_w. */
+/* strengths (graph.py:257-263): bincount (sequential in edge order) for s_out, s_in;
+ * pairwise m_w.  s_in[j] accumulates j's in-edges in CSR order = the in-CSR order. */
 static void build_strengths(orc_graph *g) {
     int64_t n = g->n;
     g->s_out = (double *)calloc((size_t)(n ? n : 1), sizeof(double));
     g->s_in = (double *)calloc((size_t)(n ? n : 1), sizeof(double));
-    for (int64_t i = 0; i < n; i++)
-        for (int64_t e = g->out_ptr[i]; e < g->out_ptr[i + 1]; e++) {
-            g->s_out[i] += g->out_w[e];
-            g->s_in[g->out_dst[e]] += g->out_w[e];
-        }
+#pragma omp parallel for schedule(dynamic, 4096) num_threads(g_threads)
+    for (int64_t i = 0; i < n; i++) {
+        double so = 0.0, si = 0.0;
+        for (int64_t e = g->out_ptr[i]; e < g->out_ptr[i + 1]; e++) so += g->out_w[e];
+        for (int64_t b = g->in_ptr[i]; b < g->in_ptr[i + 1]; b++) si += g->out_w[g->in_e[b]];
+        g->s_out[i] = so;
+        g->s_in[i] = si;
+    }
     g->m = pw_sum(g->out_w, g->ne);
+    int integral = 1;
+    for (int64_t e = 0; e < g->ne && integral; e++)
+        integral = g->out_w[e] == floor(g->out_w[e]);
+    g->integral = integral && g->m < 0x1p52;
 }
 
 /* Graph.from_edges (graph.py:84-116): stable lexsort by (src, dst), merge each
  * duplicate run with np.add.reduceat (first + pairwise(rest)), out_ptr by bincount.
+ * Done as a stable bucket by src, then per row a sort by (dst, input position): the same
+ * order as the stable lexsort, so the runs are merged in the reference's order.
  * Inputs must already be validated by the caller (ValueError path is host-side). */
 EXPORT orc_graph *orc_graph_new(int64_t n, const int64_t *src, const int64_t *dst,
                                 const double *w, int64_t ne_in) {
     orc_graph *g = (orc_graph *)calloc(1, sizeof(orc_graph));
     g->n = n;
+    int64_t *rptr = (int64_t *)malloc((size_t)(n + 1) * sizeof(int64_t));
     uint64_t *key = (uint64_t *)malloc((size_t)(ne_in ? ne_in : 1) * sizeof(uint64_t));
-    int64_t *perm = (int64_t *)malloc((size_t)(ne_in ? ne_in : 1) * sizeof(int64_t));
-    for (int64_t i = 0; i < ne_in; i++) key[i] = (uint64_t)src[i] * (uint64_t)n + (uint64_t)dst[i];
-    radix_argsort_u64(key, ne_in, perm);
-    /* count groups */
-    int64_t ng = 0;
-    for (int64_t i = 0; i < ne_in; i++)
-        if (i == 0 || key[perm[i]] != key[perm[i - 1]]) ng++;
-    g->ne = ng;
-    g->out_ptr = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
-    g->out_dst = (int64_t *)malloc((size_t)(ng ? ng : 1) * sizeof(int64_t));
-    g->out_w = (double *)malloc((size_t)(ng ? ng : 1) * sizeof(double));
-    dvec seg = {0};
-    int64_t k = -1;
-    for (int64_t i = 0; i < ne_in; i++) {
-        int64_t p = perm[i];
-        if (i == 0 || key[p] != key[perm[i - 1]]) {
-            if (k >= 0) g->out_w[k] = reduceat_seg(seg.v, seg.n);
-            k++;
-            dv_clear(&seg);
-            g->out_dst[k] = dst[p];
-            g->out_ptr[src[p] + 1]++;
-        }
-        dv_push(&seg, w[p]);
+    bucket_stable(src, ne_in, n, rptr, (int64_t *)key);
+    /* key = dst * 2^31 + position (n, ne_in < 2^31 here: int32 ids) */
+    int64_t *gcnt = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+#pragma omp parallel for schedule(dynamic, 1024) num_threads(g_threads)
+    for (int64_t r = 0; r < n; r++) {
+        int64_t lo = rptr[r], hi = rptr[r + 1], c = 0;
+        for (int64_t k = lo; k < hi; k++) key[k] = ((uint64_t)dst[key[k]] << 31) | key[k];
+        sort_u64(key + lo, hi - lo);
+        for (int64_t k = lo; k < hi; k++)
+            if (k == lo || (key[k] >> 31) != (key[k - 1] >> 31)) c++;
+        gcnt[r + 1] = c;
     }
-    if (k >= 0) g->out_w[k] = reduceat_seg(seg.v, seg.n);
-    dv_free(&seg);
-    for (int64_t i = 0; i < n; i++) g->out_ptr[i + 1] += g->out_ptr[i];
-    free(key); free(perm);
+    for (int64_t r = 0; r < n; r++) gcnt[r + 1] += gcnt[r];
+    g->out_ptr = gcnt;
+    g->ne = gcnt[n];
+    g->out_dst = (int64_t *)malloc((size_t)(g->ne ? g->ne : 1) * sizeof(int64_t));
+    g->out_w = (double *)malloc((size_t)(g->ne ? g->ne : 1) * sizeof(double));
+#pragma omp parallel num_threads(g_threads)
+    {
+        dvec seg = {0};
+#pragma omp for schedule(dynamic, 1024)
+        for (int64_t r = 0; r < n; r++) {
+            int64_t lo = rptr[r], hi = rptr[r + 1], o = gcnt[r];
+            int64_t k = lo;
+            while (k < hi) {
+                uint64_t d = key[k] >> 31;
+                dv_clear(&seg);
+                while (k < hi && (key[k] >> 31) == d) { dv_push(&seg, w[key[k] & 0x7FFFFFFFULL]); k++; }
+                g->out_dst[o] = (int64_t)d;
+                g->out_w[o] = reduceat_seg(seg.v, seg.n);
+                o++;
+            }
+        }
+        dv_free(&seg);
+    }
+    free(rptr); free(key);
     build_union(g);
     build_strengths(g);
     return g;
@@ -229,11 +285,14 @@ EXPORT orc_graph *orc_graph_new(int64_t n, const int64_t *src, const int64_t *ds
 
 EXPORT void orc_graph_free(orc_graph *g) {
     if (!g) return;
+    free(g->in_ptr); free(g->in_e);
     free(g->out_ptr); free(g->out_dst); free(g->out_w);
     free(g->uptr); free(g->unbr); free(g->uu);
     free(g->s_out); free(g->s_in);
     free(g);
 }
+
+EXPORT int orc_graph_integral(const orc_graph *g) { return g->integral; }
 
 EXPORT void orc_graph_sizes(const orc_graph *g, int64_t *n, int64_t *ne, int64_t *ue, double *m) {
     *n = g->n; *ne = g->ne; *ue = g->ue; *m = g->m;
@@ -258,6 +317,7 @@ EXPORT orc_graph *orc_aggregate(const orc_graph *g, const int64_t *labels, int64
     int64_t ne = g->ne;
     int64_t *s = (int64_t *)malloc((size_t)(ne ? ne : 1) * sizeof(int64_t));
     int64_t *d = (int64_t *)malloc((size_t)(ne ? ne : 1) * sizeof(int64_t));
+#pragma omp parallel for schedule(dynamic, 4096) num_threads(g_threads)
     for (int64_t i = 0; i < g->n; i++)
         for (int64_t e = g->out_ptr[i]; e < g->out_ptr[i + 1]; e++) {
             s[e] = labels[i];
@@ -269,9 +329,6 @@ EXPORT orc_graph *orc_aggregate(const orc_graph *g, const int64_t *labels, int64
 }
 
 /* ------------------------------------------------------------------ ASSIGN */
-
-static int g_threads = 1;
-EXPORT void orc_set_threads(int t) { g_threads = t > 0 ? t : 1; }
 
 /* _assign_targets / find_assignment (detector.py:123-158): per row the first
  * neighbour (lowest id) maximising the pairwise merge gain; self unless max > 0. */
@@ -361,6 +418,7 @@ EXPORT void orc_local_gains(const orc_graph *g, double m, const int64_t *lab, in
     double *S_in = (double *)malloc((size_t)(nc ? nc : 1) * sizeof(double));
     int64_t *cnt = (int64_t *)malloc((size_t)(nc ? nc : 1) * sizeof(int64_t));
     aggregates(g, lab, nc, S_out, S_in, cnt);
+#pragma omp parallel for schedule(dynamic, 4096) num_threads(g_threads)
     for (int64_t i = 0; i < n; i++) {
         double w_own = 0.0;
         for (int64_t e = g->uptr[i]; e < g->uptr[i + 1]; e++)
@@ -691,6 +749,378 @@ EXPORT int orc_positive(const orc_graph *g, double m, int64_t *a, const int64_t 
     int changed = P.changed;
     free(P.stamp); free(P.in_b); free(P.posof); free(seen_pos);
     dv_free(&P.ws); dv_free(&P.tmp); dv_free(&P.gains);
+    free(cptr); free(cmem); free(bad);
+    return changed;
+}
+
+/* ------------------------------------------------- POSITIVE, exact-sum fast form */
+/*
+ * orc_positive_fast: the same function as orc_positive (detector.py:197-362) for graphs
+ * whose weights are integers with m < 2^52 (orc_graph_integral), where every sum the
+ * reference forms -- w_in_c, so_c, si_c, x_w, so_b, si_b -- is an exact integer in fp64
+ * whatever the summation order.  Only the ORDER of evaluation is changed; every gain is
+ * then computed with the reference's fp64 expression on identical operands, so the cuts,
+ * the gains list and the unresolved counts are bit-identical.  Cross-checked against the
+ * literal restatement above on every integer-weight golden graph and on random graphs
+ * (tests/test_oracle.py::test_positive_fast_matches_literal).
+ *
+ * Per community, over the assignment tree (cycle nodes = roots, depth 0):
+ *   W[y]  = weight from y to the members of y's current part      (w_in_c of y)
+ *   D[v]  = weight of the part's internal edges whose tree LCA is v
+ *   SW, SD, SO, SI = subtree sums of W, D, s_out, s_in
+ * so that for the branch cut at x (detector.py:238-253): b = subtree(x),
+ *   x_w(b) = SW[x] - 2 SD[x],  so_b = SO[x],  si_b = SI[x]
+ * and for the 2-cycle pair cut (detector.py:288-335 with s = 2): b = tree of cyc[1],
+ *   x_w = SW[cyc[1]] - 2 SD[cyc[1]] (cross-tree edges have no LCA).  A cut moves b out of
+ * the part: ancestors of the cut lose b's sums, every cross edge (y in b, z in rest)
+ * lowers W[y], W[z] (and their ancestors' SW) and drops its deposit.  Each part
+ * evaluation is then one O(part) scan instead of a breadth-first search per member.
+ * Communities whose cycle is longer than 2 (never produced by run()) are
+ * handed to the literal form.
+ */
+typedef struct {
+    const orc_graph *g;
+    double m, m2;
+    int64_t *a;
+    int64_t *part;            /* current part id per node (globally unique ids) */
+    int64_t *depth;
+    uint8_t *root, *cycf;     /* part root (cycle node or cut node); on the part's cycle */
+    double *W, *D, *SW, *SD, *SO, *SI;
+    int64_t *pos;             /* position of a node inside its community's member list */
+} pf_ctx;
+
+static int64_t g_part_next = 1;
+static inline int64_t pf_new_part(void) { return __atomic_fetch_add(&g_part_next, 1, __ATOMIC_RELAXED); }
+static inline int64_t pf_part(const pf_ctx *F, int64_t z) { return __atomic_load_n(&F->part[z], __ATOMIC_RELAXED); }
+
+static int64_t pf_lca(const pf_ctx *F, int64_t y, int64_t z) {
+    const int64_t *a = F->a, *dp = F->depth;
+    while (dp[y] > dp[z]) y = a[y];
+    while (dp[z] > dp[y]) z = a[z];
+    while (y != z) {
+        if (F->root[y] || F->root[z]) return -1;
+        y = a[y];
+        z = a[z];
+    }
+    return y;
+}
+/* add dx to SW (which = 0) or SD (which = 1) from v up to its part root */
+static void pf_up(pf_ctx *F, int64_t v, double dx, int which) {
+    double *S = which ? F->SD : F->SW;
+    for (;;) {
+        S[v] += dx;
+        if (F->root[v]) break;
+        v = F->a[v];
+    }
+}
+
+typedef struct { int64_t *v; int64_t n; int64_t pid; } pf_part_t;
+
+/* one community; returns 0, or -1 when it must go to the literal form (cycle > 2) */
+static int pf_split(pf_ctx *F, const int64_t *members, int64_t nmem, dvec *gains_out,
+                    int64_t *unresolved_out, int *changed_out, int par) {
+    const orc_graph *g = F->g;
+    const double m = F->m, m2 = F->m2;
+    int64_t *a = F->a;
+    /* cycle of the community (from its smallest member, like _find_cycle) */
+    int64_t c0 = -1, c1 = -1;
+    {
+        int64_t x = members[0];
+        for (int64_t k = 0; k <= nmem + 1; k++) x = a[x];   /* now on the cycle */
+        int64_t y = a[x], len = 1, mn = x;
+        while (y != x) { if (y < mn) mn = y; y = a[y]; len++; if (len > 2) return -1; }
+        c0 = mn;
+        c1 = (len == 2) ? a[mn] : -1;
+    }
+    const int64_t pid0 = pf_new_part();
+    for (int64_t k = 0; k < nmem; k++) {
+        int64_t x = members[k];
+        F->pos[x] = k;
+        __atomic_store_n(&F->part[x], pid0, __ATOMIC_RELAXED);
+        F->root[x] = (x == c0 || x == c1);
+        F->cycf[x] = F->root[x];
+    }
+    /* children (non-cycle nodes under their target), community-local CSR by position */
+    int64_t *kids = NULL;
+    int64_t *cp = (int64_t *)calloc((size_t)nmem + 1, sizeof(int64_t));
+    for (int64_t k = 0; k < nmem; k++) {
+        int64_t x = members[k];
+        if (!F->cycf[x]) cp[F->pos[a[x]] + 1]++;
+    }
+    for (int64_t k = 0; k < nmem; k++) cp[k + 1] += cp[k];
+    kids = (int64_t *)malloc((size_t)(cp[nmem] ? cp[nmem] : 1) * sizeof(int64_t));
+    {
+        int64_t *fill = (int64_t *)malloc((size_t)(nmem ? nmem : 1) * sizeof(int64_t));
+        memcpy(fill, cp, (size_t)nmem * sizeof(int64_t));
+        for (int64_t k = 0; k < nmem; k++) {
+            int64_t x = members[k];
+            if (!F->cycf[x]) kids[fill[F->pos[a[x]]]++] = x;
+        }
+        free(fill);
+    }
+    /* depth-ordered layout (BFS from the roots): depths, then bottom-up subtree sums */
+    int64_t *bfs = (int64_t *)malloc((size_t)nmem * sizeof(int64_t));
+    int64_t nb = 0;
+    bfs[nb++] = c0;
+    F->depth[c0] = 0;
+    if (c1 >= 0) { bfs[nb++] = c1; F->depth[c1] = 0; }
+    for (int64_t q = 0; q < nb; q++) {
+        int64_t v = bfs[q];
+        for (int64_t c = cp[F->pos[v]]; c < cp[F->pos[v] + 1]; c++) {
+            F->depth[kids[c]] = F->depth[v] + 1;
+            bfs[nb++] = kids[c];
+        }
+    }
+    /* W and the LCA deposits */
+    for (int64_t k = 0; k < nmem; k++) {
+        int64_t x = members[k];
+        double wsum = 0.0;
+        for (int64_t e = g->uptr[x]; e < g->uptr[x + 1]; e++) {
+            int64_t z = g->unbr[e];
+            if (pf_part(F, z) != pid0) continue;
+            wsum += g->uu[e];
+        }
+        F->W[x] = wsum;
+        F->D[x] = 0.0;
+    }
+    for (int64_t k = 0; k < nmem; k++) {
+        int64_t x = members[k];
+        for (int64_t e = g->uptr[x]; e < g->uptr[x + 1]; e++) {
+            int64_t z = g->unbr[e];
+            if (z <= x || pf_part(F, z) != pid0) continue;
+            int64_t l = pf_lca(F, x, z);
+            if (l >= 0) F->D[l] += g->uu[e];
+        }
+    }
+    for (int64_t k = 0; k < nmem; k++) {
+        int64_t x = members[k];
+        F->SW[x] = F->W[x]; F->SD[x] = F->D[x];
+        F->SO[x] = g->s_out[x]; F->SI[x] = g->s_in[x];
+    }
+    for (int64_t q = nb - 1; q >= 0; q--) {
+        int64_t x = bfs[q];
+        if (F->cycf[x]) continue;
+        int64_t p = a[x];
+        F->SW[p] += F->SW[x]; F->SD[p] += F->SD[x];
+        F->SO[p] += F->SO[x]; F->SI[p] += F->SI[x];
+    }
+    free(bfs);
+    /* LIFO stack of parts (detector.py:208-284) */
+    pf_part_t *stack = (pf_part_t *)malloc(16 * sizeof(pf_part_t));
+    int64_t sn = 0, scap = 16;
+    {
+        int64_t *first = (int64_t *)malloc((size_t)nmem * sizeof(int64_t));
+        memcpy(first, members, (size_t)nmem * sizeof(int64_t));
+        stack[sn++] = (pf_part_t){first, nmem, pid0};
+    }
+    int64_t *sub = (int64_t *)malloc((size_t)nmem * sizeof(int64_t));
+    while (sn > 0) {
+        pf_part_t pt = stack[--sn];
+        int64_t *mem = pt.v, pn = pt.n, pid = pt.pid;
+        if (pn <= 1) { free(mem); continue; }
+        /* roots of this part: its cycle */
+        int64_t r0 = -1, r1 = -1;
+        {
+            int64_t x = mem[0];
+            while (!F->root[x]) x = a[x];
+            if (a[x] == x) r0 = x;
+            else { r0 = x < a[x] ? x : a[x]; r1 = x < a[x] ? a[x] : x; }
+        }
+        const double so_c = F->SO[r0] + (r1 >= 0 ? F->SO[r1] : 0.0);
+        const double si_c = F->SI[r0] + (r1 >= 0 ? F->SI[r1] : 0.0);
+        int64_t nneg = 0;
+        double best_gain = 0.0;
+        int64_t best_x = -1;
+#pragma omp parallel num_threads(g_threads) if (par && pn > 65536)
+        {
+            int64_t my_neg = 0, my_x = -1;
+            double my_best = 0.0;
+#pragma omp for schedule(static) nowait
+            for (int64_t k = 0; k < pn; k++) {
+                int64_t x = mem[k];
+                double so = g->s_out[x], si = g->s_in[x];
+                double gx = F->W[x] / m - (so * (si_c - si) + si * (so_c - so)) / m2;
+                if (gx < 0.0) my_neg++;
+                if (x == r0 || x == r1) continue;
+                double x_w = F->SW[x] - 2.0 * F->SD[x];
+                double so_b = F->SO[x], si_b = F->SI[x];
+                double null = (-so_c * si_b - so_b * si_c) + 2.0 * so_b * si_b;
+                double gsp = -x_w / m - null / (m * m);
+                if (gsp > my_best) { my_best = gsp; my_x = x; }   /* first max in this chunk */
+            }
+#pragma omp critical
+            {
+                nneg += my_neg;
+                if (my_x >= 0 && (my_best > best_gain || (my_best == best_gain && best_x >= 0 && my_x < best_x))) {
+                    best_gain = my_best;
+                    best_x = my_x;
+                }
+            }
+        }
+        if (nneg == 0) { free(mem); continue; }
+        int pair = 0;
+        if (best_x < 0 && r1 >= 0) {
+            /* pair cut of the 2-cycle: b = tree of the larger cycle node */
+            double x_w = F->SW[r1] - 2.0 * F->SD[r1];
+            double so_b = F->SO[r1], si_b = F->SI[r1];
+            double null = (-so_c * si_b - so_b * si_c) + 2.0 * so_b * si_b;
+            double gain = -x_w / m - null / m2;
+            if (gain > 0.0) { best_gain = gain; best_x = r1; pair = 1; }
+        }
+        if (best_x < 0) { *unresolved_out += nneg; free(mem); continue; }
+        /* apply the cut: b = subtree(best_x) (tree of r1 for the pair cut) */
+        const int64_t x = best_x;
+        const int64_t px = pair ? -1 : a[x];
+        int64_t bn = 0;
+        sub[bn++] = x;
+        for (int64_t q = 0; q < bn; q++) {
+            int64_t v = sub[q];
+            for (int64_t c = cp[F->pos[v]]; c < cp[F->pos[v] + 1]; c++)
+                if (a[kids[c]] == v) sub[bn++] = kids[c];
+        }
+        const int64_t pidb = pf_new_part();
+        for (int64_t q = 0; q < bn; q++) __atomic_store_n(&F->part[sub[q]], pidb, __ATOMIC_RELAXED);
+        if (!pair) {
+            for (int64_t v = px;; v = a[v]) {
+                F->SW[v] -= F->SW[x]; F->SD[v] -= F->SD[x];
+                F->SO[v] -= F->SO[x]; F->SI[v] -= F->SI[x];
+                if (F->root[v]) break;
+            }
+        }
+        for (int64_t q = 0; q < bn; q++) {
+            int64_t y = sub[q];
+            for (int64_t e = g->uptr[y]; e < g->uptr[y + 1]; e++) {
+                int64_t z = g->unbr[e];
+                if (pf_part(F, z) != pid) continue;      /* z in the rest */
+                double u = g->uu[e];
+                F->W[y] -= u;
+                F->W[z] -= u;
+                /* y's ancestors inside b: stop at x (the new root) */
+                for (int64_t v = y;; v = a[v]) { F->SW[v] -= u; if (v == x) break; }
+                pf_up(F, z, -u, 0);
+                if (!pair) {
+                    int64_t l = pf_lca(F, px, z);
+                    if (l >= 0) { F->D[l] -= u; pf_up(F, l, -u, 1); }
+                }
+            }
+        }
+        a[x] = x;
+        F->root[x] = 1;
+        if (pair) { a[r0] = r0; F->cycf[r0] = F->cycf[r1] = 0; }
+        *changed_out = 1;
+        dv_push(gains_out, best_gain);
+        sort_u64((uint64_t *)sub, bn);
+        int64_t *bpart = (int64_t *)malloc((size_t)bn * sizeof(int64_t));
+        memcpy(bpart, sub, (size_t)bn * sizeof(int64_t));
+        int64_t *rest = (int64_t *)malloc((size_t)pn * sizeof(int64_t));
+        int64_t rn = 0, bi = 0;
+        for (int64_t k = 0; k < pn; k++) {
+            while (bi < bn && bpart[bi] < mem[k]) bi++;
+            if (bi < bn && bpart[bi] == mem[k]) continue;
+            rest[rn++] = mem[k];
+        }
+        free(mem);
+        if (sn + 2 > scap) { scap *= 2; stack = (pf_part_t *)realloc(stack, (size_t)scap * sizeof(pf_part_t)); }
+        stack[sn++] = (pf_part_t){rest, rn, pid};
+        stack[sn++] = (pf_part_t){bpart, bn, pidb};
+    }
+    free(stack); free(sub); free(cp); free(kids);
+    return 0;
+}
+
+EXPORT int orc_positive_fast(const orc_graph *g, double m, int64_t *a, const int64_t *comm,
+                             int64_t nc, int64_t scc_cap, int64_t *splits, int64_t *unresolved,
+                             double *gains_out, int64_t gains_cap, int64_t *n_warn) {
+    int64_t n = g->n;
+    double *lg = (double *)malloc((size_t)(n ? n : 1) * sizeof(double));
+    orc_local_gains(g, m, comm, nc, lg);
+    uint8_t *bad = (uint8_t *)calloc((size_t)(nc ? nc : 1), 1);
+    int64_t nbad = 0;
+    for (int64_t i = 0; i < n; i++) if (lg[i] < 0.0 && !bad[comm[i]]) { bad[comm[i]] = 1; nbad++; }
+    free(lg);
+    *splits = 0; *unresolved = 0; *n_warn = 0;
+    if (nbad == 0) { free(bad); return 0; }
+    int64_t *cptr = (int64_t *)calloc((size_t)nc + 1, sizeof(int64_t));
+    for (int64_t i = 0; i < n; i++) cptr[comm[i] + 1]++;
+    for (int64_t c = 0; c < nc; c++) cptr[c + 1] += cptr[c];
+    int64_t *cmem = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    {
+        int64_t *fill = (int64_t *)malloc((size_t)(nc ? nc : 1) * sizeof(int64_t));
+        memcpy(fill, cptr, (size_t)nc * sizeof(int64_t));
+        for (int64_t i = 0; i < n; i++) cmem[fill[comm[i]]++] = i;
+        free(fill);
+    }
+    int64_t *blist = (int64_t *)malloc((size_t)nbad * sizeof(int64_t));
+    nbad = 0;
+    for (int64_t c = 0; c < nc; c++) if (bad[c]) blist[nbad++] = c;
+    pf_ctx F;
+    memset(&F, 0, sizeof(F));
+    F.g = g; F.m = m; F.m2 = m * m; F.a = a;
+    F.part = (int64_t *)calloc((size_t)n, sizeof(int64_t));
+    F.depth = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    F.pos = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    F.root = (uint8_t *)calloc((size_t)n, 1);
+    F.cycf = (uint8_t *)calloc((size_t)n, 1);
+    double *buf = (double *)malloc((size_t)n * 6 * sizeof(double));
+    F.W = buf; F.D = buf + n; F.SW = buf + 2 * n; F.SD = buf + 3 * n; F.SO = buf + 4 * n; F.SI = buf + 5 * n;
+    dvec *gl = (dvec *)calloc((size_t)nbad, sizeof(dvec));
+    int64_t *un = (int64_t *)calloc((size_t)nbad, sizeof(int64_t));
+    int *ch = (int *)calloc((size_t)nbad, sizeof(int));
+    int *lit = (int *)calloc((size_t)nbad, sizeof(int));
+    const int64_t BIG = 1 << 16;
+    /* small communities in parallel, then the big ones with parallel scans */
+#pragma omp parallel for schedule(dynamic, 1) num_threads(g_threads)
+    for (int64_t k = 0; k < nbad; k++) {
+        int64_t c = blist[k];
+        int64_t sz = cptr[c + 1] - cptr[c];
+        if (sz >= BIG) continue;
+        lit[k] = pf_split(&F, cmem + cptr[c], sz, &gl[k], &un[k], &ch[k], 0) < 0;
+    }
+    for (int64_t k = 0; k < nbad; k++) {
+        int64_t c = blist[k];
+        int64_t sz = cptr[c + 1] - cptr[c];
+        if (sz < BIG) continue;
+        lit[k] = pf_split(&F, cmem + cptr[c], sz, &gl[k], &un[k], &ch[k], 1) < 0;
+    }
+    free(F.part); free(F.depth); free(F.pos); free(F.root); free(F.cycf); free(buf);
+    /* communities with a longer cycle: the literal form */
+    int any_lit = 0;
+    for (int64_t k = 0; k < nbad; k++) any_lit |= lit[k];
+    if (any_lit) {
+        pos_ctx P;
+        memset(&P, 0, sizeof(P));
+        P.g = g; P.m = m; P.m2 = m * m; P.a = a; P.scc_cap = scc_cap;
+        P.stamp = (int64_t *)calloc((size_t)n, sizeof(int64_t));
+        P.in_b = (uint8_t *)calloc((size_t)n, 1);
+        P.posof = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+        int64_t *seen_pos = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+        for (int64_t i = 0; i < n; i++) seen_pos[i] = -1;
+        for (int64_t k = 0; k < nbad; k++) {
+            if (!lit[k]) continue;
+            int64_t c = blist[k];
+            P.gains.n = 0; P.unresolved = 0; P.changed = 0;
+            split_community(&P, cmem + cptr[c], cptr[c + 1] - cptr[c], seen_pos);
+            for (int64_t q = 0; q < P.gains.n; q++) dv_push(&gl[k], P.gains.v[q]);
+            un[k] = P.unresolved;
+            ch[k] = P.changed;
+        }
+        *n_warn = P.n_warn;
+        free(P.stamp); free(P.in_b); free(P.posof); free(seen_pos);
+        dv_free(&P.ws); dv_free(&P.tmp); dv_free(&P.gains);
+    }
+    int changed = 0;
+    int64_t ng = 0;
+    for (int64_t k = 0; k < nbad; k++) {
+        for (int64_t q = 0; q < gl[k].n; q++) {
+            if (gains_out && ng < gains_cap) gains_out[ng] = gl[k].v[q];
+            ng++;
+        }
+        *unresolved += un[k];
+        changed |= ch[k];
+        dv_free(&gl[k]);
+    }
+    *splits = ng;
+    free(gl); free(un); free(ch); free(lit); free(blist);
     free(cptr); free(cmem); free(bad);
     return changed;
 }

@@ -68,9 +68,6 @@ SIGNATURES = {
     "slm_plan_groups": (C.c_int, [_VP, _PI64, _VP, _VP]),
     "slm_get_cstar": (C.c_int, [_VP, _VP]),
     "slm_debug_sweep_floor": (C.c_int, [_VP, C.c_int32, _PD]),
-    "slm_gen_rmat_host": (C.c_int, [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
-                                    C.c_uint64, C.c_int, _VP, _VP, _VP, _PI64]),
-    "slm_gen_rgg_host": (C.c_int, [_I64, C.c_double, C.c_uint64, _VP, _VP, _VP, _PI64]),
     "slm_build_rmat": (C.c_int, [_VP, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                  C.c_uint64, C.c_int]),
     "slm_build_rgg": (C.c_int, [_VP, _I64, C.c_double, C.c_uint64]),
@@ -320,29 +317,3 @@ class Context:
         self.call("slm_last_commit_stats", C.byref(c), C.byref(r))
         return c.value, r.value
 
-
-def gen_rmat_host(scale, edge_factor, a, b, c, seed, weight_mode):
-    """Host twin of the device R-MAT generator (same edge multiset)."""
-    L = load()
-    cnt = C.c_int64()
-    L.slm_gen_rmat_host(scale, edge_factor, a, b, c, seed, weight_mode, None, None, None,
-                        C.byref(cnt))
-    k = cnt.value
-    src = np.empty(k, np.int64)
-    dst = np.empty(k, np.int64)
-    w = np.empty(k, np.float64)
-    L.slm_gen_rmat_host(scale, edge_factor, a, b, c, seed, weight_mode, ptr(src), ptr(dst), ptr(w),
-                        C.byref(cnt))
-    return src, dst, w
-
-
-def gen_rgg_host(n, radius, seed):
-    L = load()
-    cnt = C.c_int64()
-    L.slm_gen_rgg_host(n, radius, seed, None, None, None, C.byref(cnt))
-    k = cnt.value
-    src = np.empty(k, np.int64)
-    dst = np.empty(k, np.int64)
-    w = np.empty(k, np.float64)
-    L.slm_gen_rgg_host(n, radius, seed, ptr(src), ptr(dst), ptr(w), C.byref(cnt))
-    return src, dst, w

@@ -1,9 +1,10 @@
 // slm_gen.cu -- counter-based generators for the BASELINE.json synthetic graphs.
 //
-// Every random draw is a pure hash of (seed, edge or point id, stream), evaluated by the
-// same __host__ __device__ code on the CPU and on the GPU, so the device-generated graph
-// used by the bench and the host-generated edge list handed to the CPU oracle are the same
-// edge multiset ("the oracle and the GPU consume the same edge list").
+// Every random draw is a pure hash of (seed, edge or point id, stream), so the graph
+// generated here in HBM for the bench and the host edge list handed to the CPU oracle
+// (workloads/gen_host.c, a separate plain-C twin outside this library) are the same edge
+// multiset ("the oracle and the GPU consume the same edge list");
+// tests/test_gpu_parity.py checks the two builds bit for bit.
 #include "slm_internal.cuh"
 #include "../../include/slm.h"
 #include <cub/cub.cuh>
@@ -52,30 +53,6 @@ __host__ __device__ inline double rmat_weight(int mode, uint64_t wh) {
     return mode ? (double)(1 + (wh % 100ull)) : 1.0;
 }
 
-// --------------------------------------------------------------------- host
-
-extern "C" int slm_gen_rmat_host(int scale, int edge_factor, double a, double b, double c,
-                                 uint64_t seed, int weight_mode, int64_t *src, int64_t *dst,
-                                 double *w, int64_t *n_edges) {
-    const uint64_t base = gen_base(seed);
-    const int64_t m = (int64_t)edge_factor << scale;
-    const double t1 = a, t2 = a + b, t3 = a + b + c;
-    int64_t cnt = 0;
-    for (int64_t k = 0; k < m; k++) {
-        uint64_t s, d, wh;
-        rmat_edge(base, scale, k, t1, t2, t3, s, d, wh);
-        if (s == d) continue;
-        if (src) {
-            double x = rmat_weight(weight_mode, wh);
-            src[cnt] = (int64_t)s; dst[cnt] = (int64_t)d; w[cnt] = x;
-            src[cnt + 1] = (int64_t)d; dst[cnt + 1] = (int64_t)s; w[cnt + 1] = x;
-        }
-        cnt += 2;
-    }
-    *n_edges = cnt;
-    return SLM_OK;
-}
-
 __host__ __device__ inline void rgg_point(uint64_t base, int64_t i, double &x, double &y) {
     uint64_t h1 = fin64(base + (uint64_t)i * RNG_GAMMA);
     uint64_t h2 = fin64(h1 ^ RNG_MIX2);
@@ -85,51 +62,6 @@ __host__ __device__ inline void rgg_point(uint64_t base, int64_t i, double &x, d
 __host__ __device__ inline int rgg_cell(double v, int G) {
     int c = (int)(v * G);
     return c >= G ? G - 1 : c;
-}
-
-extern "C" int slm_gen_rgg_host(int64_t n, double radius, uint64_t seed, int64_t *src,
-                                int64_t *dst, double *w, int64_t *n_edges) {
-    const uint64_t base = gen_base(seed);
-    int G = (int)std::floor(1.0 / radius);
-    if (G < 1) G = 1;
-    const double r2 = radius * radius;
-    std::vector<double> X(n), Y(n);
-    std::vector<int64_t> cell(n), cptr((size_t)G * G + 1, 0), pts(n);
-    for (int64_t i = 0; i < n; i++) {
-        rgg_point(base, i, X[i], Y[i]);
-        cell[i] = (int64_t)rgg_cell(Y[i], G) * G + rgg_cell(X[i], G);
-        cptr[cell[i] + 1]++;
-    }
-    for (size_t k = 0; k + 1 < cptr.size(); k++) cptr[k + 1] += cptr[k];
-    {
-        std::vector<int64_t> fill(cptr.begin(), cptr.end() - 1);
-        for (int64_t i = 0; i < n; i++) pts[fill[cell[i]]++] = i;
-    }
-    int64_t cnt = 0;
-    for (int64_t i = 0; i < n; i++) {
-        int cx = (int)(cell[i] % G), cy = (int)(cell[i] / G);
-        for (int dy = -1; dy <= 1; dy++)
-            for (int dx = -1; dx <= 1; dx++) {
-                int ux = cx + dx, uy = cy + dy;
-                if (ux < 0 || uy < 0 || ux >= G || uy >= G) continue;
-                int64_t cc = (int64_t)uy * G + ux;
-                for (int64_t q = cptr[cc]; q < cptr[cc + 1]; q++) {
-                    int64_t j = pts[q];
-                    if (j == i) continue;
-                    double ddx = X[i] - X[j], ddy = Y[i] - Y[j];
-                    if (ddx * ddx + ddy * ddy < r2) {
-                        if (src) {
-                            src[cnt] = i;
-                            dst[cnt] = j;
-                            w[cnt] = 1.0;
-                        }
-                        cnt++;
-                    }
-                }
-            }
-    }
-    *n_edges = cnt;
-    return SLM_OK;
 }
 
 // ------------------------------------------------------------------- device

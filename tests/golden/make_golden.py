@@ -109,7 +109,7 @@ if __name__ == "__main__" and "--configs" not in sys.argv:
 def configs():
     """Full-run fixtures of config 1 and scaled stand-ins of configs 3-5 (same generators)."""
     sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
-    from paper_1702_04645_b200 import generators as GN
+    import workloads as GN
     out = {}
     specs = [("c1_sbm", GN.generate("c1_sbm")),
              ("c2_dcsbm_small", GN.dcsbm(n=3000, k=20, size_lo=50, size_hi=300, seed=1)),

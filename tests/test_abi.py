@@ -65,7 +65,7 @@ def test_label_helpers():
 
 
 def test_host_generators_deterministic_and_symmetric():
-    from paper_1702_04645_b200 import generators as GN
+    import workloads as GN
     n, s, d, w = GN.rmat(10, 8, 1, 4)
     n2, s2, d2, w2 = GN.rmat(10, 8, 1, 4)
     assert np.array_equal(s, s2) and np.array_equal(d, d2) and np.array_equal(w, w2)
@@ -86,7 +86,7 @@ def test_host_generators_deterministic_and_symmetric():
 
 
 def test_dcsbm_shape():
-    from paper_1702_04645_b200 import generators as GN
+    import workloads as GN
     n, s, d, w = GN.dcsbm(n=5000, k=20, size_lo=50, size_hi=500, seed=1)
     assert n == 5000 and (s != d).all()
     assert 10 < s.size / n < 30

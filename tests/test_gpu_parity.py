@@ -126,7 +126,7 @@ def test_full_runs_golden(slm, golden):
 
 
 def test_config_fixtures_full_runs(slm, golden_configs):
-    from paper_1702_04645_b200 import generators as GN
+    import workloads as GN
     G = golden_configs
     specs = {"c1_sbm": lambda: GN.generate("c1_sbm"),
              "c2_dcsbm_small": lambda: GN.dcsbm(n=3000, k=20, size_lo=50, size_hi=300, seed=1),
@@ -161,7 +161,7 @@ def _vs_oracle(slm, oracle, n, s, d, w, seed=0, p=0.5, gamma=1.0):
 
 
 def test_scaled_configs_vs_oracle(slm, oracle):
-    from paper_1702_04645_b200 import generators as GN
+    import workloads as GN
     oracle.set_threads(8)
     cases = [GN.rmat(13, 16, 0, 2), GN.rmat(13, 16, 1, 4), GN.rgg(1 << 14, 8.0, 3),
              GN.dcsbm(n=20_000, k=60, size_lo=100, size_hi=1000, seed=1)]
@@ -170,7 +170,7 @@ def test_scaled_configs_vs_oracle(slm, oracle):
 
 
 def test_resolution_vs_oracle(slm, oracle):
-    from paper_1702_04645_b200 import generators as GN
+    import workloads as GN
     n, s, d, w = GN.rmat(12, 8, 1, 4)
     for gamma in (0.5, 2.0):
         _vs_oracle(slm, oracle, n, s, d, w, gamma=gamma)
@@ -180,7 +180,7 @@ def test_resolution_vs_oracle(slm, oracle):
 
 
 def test_accept_prob_and_seeds_vs_oracle(slm, oracle):
-    from paper_1702_04645_b200 import generators as GN
+    import workloads as GN
     n, s, d, w = GN.rmat(11, 16, 1, 7)
     for seed, p in ((3, 1.0), (5, 0.25), (9, 0.75)):
         _vs_oracle(slm, oracle, n, s, d, w, seed=seed, p=p)
@@ -228,12 +228,13 @@ def test_uniform01_device(slm, golden):
 
 
 def test_device_generators_match_host(slm):
+    import workloads as W
     from paper_1702_04645_b200 import _lib, generators as GN
     for name, over in (("c3_rmat22", dict(scale=12)), ("c5_rmat24", dict(scale=12, edge_factor=8)),
                        ("c4_rgg24", dict(n=1 << 13))):
         ctx_d = _lib.Context(0)
-        GN.build_on_device(ctx_d, name, **over)
-        n, s, d, w = GN.generate(name, **over)
+        GN.build_on_device(ctx_d, {**W.CONFIGS[name], **over})
+        n, s, d, w = W.generate(name, **over)
         ctx_h = _lib.Context(0)
         ctx_h.build_graph(n, s, d, w)
         for x, y in zip(ctx_d.csr(), ctx_h.csr()):
@@ -243,7 +244,7 @@ def test_device_generators_match_host(slm):
 def test_giant_part_executor_parity(slm, golden, oracle, monkeypatch):
     """Force the incremental grid executor (normally for parts > 4096 members) onto every
     bad community and check the same bit-exact outcomes."""
-    from paper_1702_04645_b200 import generators as GN
+    import workloads as GN
     monkeypatch.setenv("SLM_SMALL_PART", "3")
     for key in case_names(golden):
         if not exact_sums(key):
@@ -266,7 +267,7 @@ def test_giant_part_executor_parity(slm, golden, oracle, monkeypatch):
 
 def test_positive_large_rmat_vs_oracle(slm, oracle):
     """Hub communities well beyond the warp executor (R-MAT 16): one POSITIVE call."""
-    from paper_1702_04645_b200 import generators as GN
+    import workloads as GN
     n, s, d, w = GN.rmat(16, 16, 1, 4)
     g = slm.Graph.from_edges(n, s, d, w)
     a = slm.find_assignment(g)
@@ -340,7 +341,7 @@ def test_heavy_member_routing_parity(slm, oracle, monkeypatch):
     """Communities holding a member whose union row exceeds SLM_HEAVY_DEG entries go to the
     CTA executor even when they are small in members (coarse-level hubs).  Force the routing
     with a tiny threshold and compare the whole hierarchy with the oracle."""
-    from paper_1702_04645_b200 import generators as GN
+    import workloads as GN
     monkeypatch.setenv("SLM_HEAVY_DEG", "24")
     for n, s, d, w in (GN.rmat(13, 16, 1, 6), GN.generate("c1_sbm")):
         _vs_oracle(slm, oracle, n, s, d, w)
@@ -386,7 +387,7 @@ def test_cta_walkers_full_run_parity(tmp_path):
         "import sys\n"
         f"sys.path.insert(0, {root!r})\n"
         "import paper_1702_04645_b200 as slm\n"
-        "from paper_1702_04645_b200 import generators as GN\n"
+        "import workloads as GN\n"
         "from oracle import oracle as O\n"
         "from tests.test_gpu_parity import _vs_oracle\n"
         "O.build()\n"
@@ -403,7 +404,7 @@ def test_big_candidate_items_parity(slm, oracle, monkeypatch):
     """Commit candidates whose tails hold many entries are priced by work items spread over
     the GPU (integer weights: exact fp64 atomics).  Force every candidate with more than 8
     tail entries onto that path and compare whole hierarchies with the oracle."""
-    from paper_1702_04645_b200 import generators as GN
+    import workloads as GN
     monkeypatch.setenv("SLM_BIG_VOL", "8")
     for n, s, d, w in (GN.rmat(13, 16, 1, 4), GN.rmat(12, 16, 0, 7), GN.generate("c1_sbm")):
         _vs_oracle(slm, oracle, n, s, d, w)
@@ -422,7 +423,7 @@ def test_local_gains_without_wown_matches(tmp_path):
         "import sys, numpy as np\n"
         f"sys.path.insert(0, {root!r})\n"
         "import paper_1702_04645_b200 as slm\n"
-        "from paper_1702_04645_b200 import generators as GN\n"
+        "import workloads as GN\n"
         "out = []\n"
         "for n, s, d, w in (GN.rmat(14, 16, 1, 4), GN.rgg(1 << 14, 8.0, 3)):\n"
         "    r = slm.run(slm.Graph.from_edges(n, s, d, w), slm.RunConfig())\n"
@@ -453,7 +454,7 @@ def test_walker_runs_match_single_commits(tmp_path):
         "import sys, numpy as np\n"
         f"sys.path.insert(0, {root!r})\n"
         "import paper_1702_04645_b200 as slm\n"
-        "from paper_1702_04645_b200 import generators as GN\n"
+        "import workloads as GN\n"
         "out = []\n"
         "for (n, s, d, w), gam in ((GN.rmat(15, 16, 1, 4), 1.0), (GN.rmat(15, 16, 1, 4), 0.5),\n"
         "                          (GN.generate('c1_sbm'), 0.5)):\n"

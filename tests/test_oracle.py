@@ -98,7 +98,7 @@ def test_full_runs_match_reference(oracle, golden):
 
 
 def test_config_fixtures(oracle, golden_configs):
-    from paper_1702_04645_b200 import generators as GN
+    import workloads as GN
     from tests.golden.make_golden import hash_edges
     specs = {"c1_sbm": lambda: GN.generate("c1_sbm"),
              "c2_dcsbm_small": lambda: GN.dcsbm(n=3000, k=20, size_lo=50, size_hi=300, seed=1),
@@ -153,7 +153,7 @@ def test_oracle_vs_live_reference_random(oracle, ref):
 
 def test_oracle_resolution_matches_patched_reference(oracle, ref, monkeypatch):
     """gamma in {0.5, 2}: the reference with m_w -> m_w/gamma."""
-    from paper_1702_04645_b200 import generators as GN
+    import workloads as GN
     import synclouvain.detector as D
     n, s, d, w = GN.generate("c1_sbm")
     for gamma in (0.5, 2.0):
@@ -202,3 +202,69 @@ def test_oracle_kats():
         O.OGraph.from_edges(2, [0], [2], [1.0])
     with pytest.raises(ValueError):
         O.OGraph.from_edges(2, [0], [1], [0.0])
+
+
+# ------------------------------------------------ fast POSITIVE vs the literal form
+
+def _loop_compare_positive(O, n, s, d, w, seed=0, accept_prob=0.5, resolution=1.0, sweeps=6):
+    """Run the level loop (detector.py:573-641, capped sweeps) and, at every POSITIVE call,
+    check the exact-sum fast form against the literal restatement on the same state."""
+    g = O.OGraph.from_edges(n, s, d, w)
+    calls = 0
+    level = 0
+    while True:
+        m = g.m_w / resolution
+        a = O.find_assignment(g, m)
+        comm, nc, _ = O.extract_components(a)
+
+        def pos(a, comm, nc):
+            r1 = O.positive_correction(g, a, comm, nc, m=m, fast=False)
+            r2 = O.positive_correction(g, a, comm, nc, m=m, fast=True)
+            np.testing.assert_array_equal(r1[0], r2[0])
+            assert r1[1:] == r2[1:]
+            return r1
+        a, ch, *_ = pos(a, comm, nc)
+        calls += 1
+        if ch:
+            comm, nc, _ = O.extract_components(a)
+        for sw in range(sweeps):
+            a, improved, applied, _, _ = O.maximal_correction(g, a, comm, nc, seed, accept_prob,
+                                                              level, sw, m)
+            if applied:
+                comm, nc, _ = O.extract_components(a)
+            if not improved:
+                break
+            a, ch, *_ = pos(a, comm, nc)
+            calls += 1
+            if ch:
+                comm, nc, _ = O.extract_components(a)
+        if nc == g.n or level >= 3:
+            return calls
+        g = O.aggregate(g, comm)
+        level += 1
+
+
+def test_positive_fast_matches_literal(oracle, golden):
+    import workloads as W
+    cases = []
+    for key in _cases(golden):
+        n, s, d, w = case_edges(golden, key)
+        if np.all(w == np.floor(w)):
+            cases.append((n, s, d, w))
+    cases += [W.rmat(10, 16, 0, 2), W.rmat(10, 8, 1, 4), W.rgg(3000, 8.0, 3),
+              W.dcsbm(n=3000, k=20, size_lo=50, size_hi=300, seed=1), W.generate("c1_sbm")]
+    rng = np.random.default_rng(77)
+    for t in range(30):
+        n = int(rng.integers(5, 300))
+        k = int(rng.integers(n, 8 * n))
+        s = rng.integers(0, n, k)
+        d = rng.integers(0, n, k)
+        keep = s != d
+        w = rng.integers(1, 5, k).astype(np.float64)
+        cases.append((n, s[keep], d[keep], w[keep]))
+    calls = 0
+    for i, (n, s, d, w) in enumerate(cases):
+        for gam in ((1.0, 0.5) if i % 3 == 0 else (1.0,)):
+            calls += _loop_compare_positive(oracle, n, s, d, w, seed=i, resolution=gam,
+                                            accept_prob=(0.5, 1.0)[i % 2])
+    assert calls > 100
