@@ -15,8 +15,11 @@ Contract (one JSON line from rank 0):
   * roofline: algorithmic bytes per sweep B = E*12 + n*32 + G*16 over the
               sweep's average device time, against MEASURED_PEAKS.json hbm_gbs.
   * cpu_baseline: the C oracle port of _best_targets on the host's cores over a bounded
-              contiguous row sample of the same snapshot (also checked for equal targets).
-  * --impl reference: the oracle port alone (the reference's CPU path), same metric.
+              contiguous row sample of the same snapshot (also checked for equal targets);
+              warm-up passes, then the mean over --steps passes.
+  * --impl reference: the oracle port alone (the reference's CPU path), same metric and
+              timing method, on a snapshot the oracle builds on the host from the workload's
+              host twin (workloads/); the product package is never imported in that arm.
   * N > 1 (torchrun): replicas only: every rank runs the same sweep on
     its own GPU; rank 0 prints.
 """
@@ -151,9 +154,12 @@ def _traffic():
 
 def setup_snapshot(ctx, cfgname, over):
     """Build the workload in HBM and produce the first MAXIMAL sweep's snapshot."""
+    import workloads as W
     from paper_1702_04645_b200 import RunConfig, generators as GN
+    spec = {**W.CONFIGS[cfgname], **over}
     t0 = time.perf_counter()
-    GN.build_on_device(ctx, cfgname, **over)
+    GN.build_on_device(ctx, spec, None if spec["kind"] in ("rmat", "rgg")
+                       else W.generate(cfgname, **over))
     t1 = time.perf_counter()
     ctx.assign(want=False)
     ctx.components(want=False)
@@ -183,19 +189,52 @@ def cpu_sample(ctx, info, target_entries, snap):
                 s_in=s_in, m=m, entries=int(uptr[-1]))
 
 
-def time_oracle(sample, threads, reps=1):
+def time_oracle(sample, threads, warmup, steps):
+    """The CPU plan sweep (_best_targets, oracle port) over the sample: ``warmup`` untimed
+    passes, then the mean of ``steps`` timed passes -- the same method in the reference arm
+    and in the ours-arm's cpu_baseline."""
     from oracle import oracle as O
     O.build()
     O.set_threads(threads)
     ts = []
     out = None
-    for _ in range(reps):
+    for i in range(warmup + steps):
         t = time.perf_counter()
         out = O.plan_sample(sample["uptr"], sample["unbr"], sample["uu"], sample["s_out"],
                             sample["s_in"], sample["m"], sample["comm"], sample["S_out"],
                             sample["S_in"], 0, sample["R"])
-        ts.append(time.perf_counter() - t)
-    return min(ts), out
+        if i >= warmup:
+            ts.append(time.perf_counter() - t)
+    return sum(ts) / len(ts), out
+
+
+def oracle_snapshot(cfgname, over, threads, target_entries):
+    """Reference arm: the first MAXIMAL sweep's snapshot built on the host by the oracle
+    (host twin of the workload -> Graph.from_edges -> ASSIGN -> COMPONENTS -> POSITIVE), and
+    the bounded row sample the CPU plan sweep is timed on.  Nothing of the product is
+    loaded."""
+    import workloads as W
+    from oracle import oracle as O
+    O.build()
+    O.set_threads(threads)
+    t0 = time.perf_counter()
+    n, s, d, w = W.generate(cfgname, **over)
+    g = O.OGraph.from_edges(n, s, d, w)
+    del s, d, w
+    a = O.find_assignment(g)
+    comm, nc, _ = O.extract_components(a)
+    a, ch, *_ = O.positive_correction(g, a, comm, nc)
+    if ch:
+        comm, nc, _ = O.extract_components(a)
+    so, si, _ = O.aggregates(g, comm, nc)
+    uptr, unbr, uu = g.union()
+    s_out, s_in, m = g.strengths()
+    avg = max(1.0, uptr[-1] / max(1, n))
+    R = int(min(n, max(1024, target_entries / avg)))
+    sample = dict(R=R, uptr=uptr[:R + 1].copy(), unbr=unbr[:uptr[R]].copy(),
+                  uu=uu[:uptr[R]].copy(), comm=comm, S_out=so, S_in=si, s_out=s_out,
+                  s_in=s_in, m=m, entries=int(uptr[R]))
+    return sample, time.perf_counter() - t0
 
 
 def main():
@@ -215,58 +254,65 @@ def main():
     args.warmup = max(3, args.warmup)
 
     ws, rank, local = _dist()
-    import torch
-    if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group(backend="nccl" if args.impl == "ours" else "gloo")
-    torch.cuda.set_device(local)
-    from paper_1702_04645_b200 import _lib
-    from paper_1702_04645_b200.generators import CONFIGS
-
+    import workloads as W
     over = {}
     if args.scale is not None:
         over["scale"] = args.scale
-    spec = dict(CONFIGS[args.config])
+    spec = dict(W.CONFIGS[args.config])
     spec.update(over)
     workload = {"workload": args.config, **{k: v for k, v in spec.items()}}
     threads = os.cpu_count() or 1
+
+    if args.impl == "reference":
+        # the reference's CPU path (oracle port of _best_targets) on the host cores; the
+        # snapshot is the oracle's own -- the product library is never imported here
+        if ws > 1:
+            import torch.distributed as dist
+            dist.init_process_group(backend="gloo")
+        if rank == 0:
+            sample, prep_s = oracle_snapshot(args.config, over, threads, args.cpu_entries)
+            t, _ = time_oracle(sample, threads, args.warmup, args.steps)
+            val = sample["entries"] / t / 1e9
+            line = {"impl": "reference", "metric": "local-move GTEPS", "value": val,
+                    "unit": "GTEPS", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+                    "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+                    "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                    "config": workload,
+                    "cpu_baseline": {"value": val, "unit": "GTEPS", "cores": threads,
+                                     "kind": "port",
+                                     "sample": f"_best_targets over rows [0,{sample['R']}) "
+                                               f"({sample['entries']} union entries) of the "
+                                               f"{args.config} first-sweep snapshot (built by "
+                                               f"the oracle on the host in {prep_s:.0f} s, "
+                                               f"untimed)"},
+                    "e2e": {"value": val, "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                            "d2h_bytes_per_step": 0}}
+            print(json.dumps(line), flush=True)
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    import torch
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group(backend="nccl")
+    torch.cuda.set_device(local)
+    from paper_1702_04645_b200 import _lib
 
     ctx = _lib.Context(local)
     build_s, setup_s = setup_snapshot(ctx, args.config, over)
     info = ctx.info()
     snap = snapshot_arrays(ctx)
     E, n = info["ue"], info["n"]
-
-    if args.impl == "reference":
-        if rank != 0:
-            if ws > 1:
-                import torch.distributed as dist
-                dist.barrier()
-            return
-        sample = cpu_sample(ctx, info, args.cpu_entries, snap)
-        times = []
-        for i in range(args.warmup + args.steps):
-            t, _ = time_oracle(sample, threads)
-            if i >= args.warmup:
-                times.append(t)
-        tot = sum(times)
-        val = sample["entries"] * len(times) / tot / 1e9
-        line = {"impl": "reference", "metric": "local-move GTEPS", "value": val, "unit": "GTEPS",
-                "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": tot / len(times) * 1e3, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": workload,
-                "cpu_baseline": {"value": val, "unit": "GTEPS", "cores": threads, "kind": "port",
-                                 "sample": f"_best_targets over rows [0,{sample['R']}) "
-                                           f"({sample['entries']} union entries) of the "
-                                           f"{args.config} first-sweep snapshot"},
-                "e2e": {"value": val, "unit": "GTEPS", "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
-        if ws > 1:
-            import torch.distributed as dist
-            dist.barrier()
-        return
+    # the first sweep of a level also builds the level's degree-ordered sweep view (once per
+    # level, amortised over up to 100 sweeps): timed here, outside the timed steps
+    ctx.sync()
+    t0 = time.perf_counter()
+    ctx.plan_async(127)
+    ctx.sync()
+    first_sweep_ms = (time.perf_counter() - t0) * 1e3
 
     groups, bin_rows, bin_entries = ctx.plan_groups()
     stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=local)
@@ -328,7 +374,7 @@ def main():
     lab_pin = torch.from_numpy(comm).pin_memory().numpy()
     out_pin = torch.empty(n, dtype=torch.int64).pin_memory().numpy()
     from paper_1702_04645_b200._lib import ptr
-    ke = max(3, min(args.steps, 5))
+    ke = args.steps
     ctx.call("slm_plan_sweep", ptr(lab_pin), ptr(out_pin))
     t0 = time.perf_counter()
     for _ in range(ke):
@@ -359,10 +405,11 @@ def main():
             "per_kernel_ms": per_bin,
             "bins": {"rows": bin_rows.tolist(), "entries": bin_entries.tolist()},
             "setup_s": {"build_csr_union": round(build_s, 3),
-                        "assign_components_positive": round(setup_s, 3)}}
+                        "assign_components_positive": round(setup_s, 3),
+                        "first_sweep_with_view_build_ms": round(first_sweep_ms, 2)}}
     if rank == 0 and not args.no_cpu:
         sample = cpu_sample(ctx, info, args.cpu_entries, snap)
-        t_cpu, cst = time_oracle(sample, threads)
+        t_cpu, cst = time_oracle(sample, threads, args.warmup, args.steps)
         ok = bool(np.array_equal(cst, gpu_cstar[:sample["R"]]))
         line["cpu_baseline"] = {
             "value": round(sample["entries"] / t_cpu / 1e9, 5), "unit": "GTEPS",
@@ -384,7 +431,8 @@ def partition_runs(ctx, args, rank, threads):
     config, graph already in HBM (device-generated), full level loop through the public
     run(); (2) C2 (DC-SBM, 10^5 nodes) from host edges through Graph.from_edges + run(),
     next to the C oracle's full hierarchy on the host cores (same partitions required)."""
-    from paper_1702_04645_b200 import RunConfig, detector, generators as GN
+    import workloads as W
+    from paper_1702_04645_b200 import RunConfig, detector
     from paper_1702_04645_b200.graph import Graph
     out = {}
     info = ctx.info()
@@ -402,7 +450,7 @@ def partition_runs(ctx, args, rank, threads):
                         "phase_seconds": {k: round(v, 3) for k, v in res.stats.phase_seconds.items()},
                         "input": "graph resident in HBM (device generator); timed: run()"}
     if rank == 0:
-        n, s, d, w = GN.generate("c2_dcsbm")
+        n, s, d, w = W.generate("c2_dcsbm")
         t0 = time.perf_counter()
         g2 = Graph.from_edges(n, s, d, w)
         r2 = detector.run(g2, RunConfig())

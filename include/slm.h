@@ -81,6 +81,10 @@ SLM_API int slm_get_strengths(slm_ctx *ctx, double *s_out, double *s_in);
  * nullable (call once with NULL to size them from ptr_out[r1-r0]). */
 SLM_API int slm_get_union_rows(slm_ctx *ctx, int64_t r0, int64_t r1, int64_t *ptr_out,
                                int64_t *nbr_out, double *u_out);
+/* Canonical CSR rows [r0, r1) (Graph.out_ptr / out_dst / out_w slices, graph.py:97-110), in
+ * the same convention as slm_get_union_rows (bounded downloads of 1e9-entry graphs). */
+SLM_API int slm_get_csr_rows(slm_ctx *ctx, int64_t r0, int64_t r1, int64_t *ptr_out,
+                             int64_t *dst_out, double *w_out);
 SLM_API int slm_set_resolution(slm_ctx *ctx, double gamma);
 
 /* ---- phases (current level) ----------------------------------------------------- */

@@ -71,6 +71,7 @@ def lib():
                                    C.POINTER(i64), C.POINTER(i64), _f64p, i64, C.POINTER(i64)]
         L.orc_positive_fast.restype = C.c_int
         L.orc_positive_fast.argtypes = L.orc_positive.argtypes
+        L.orc_graph_rows.argtypes = [vp, C.c_int, i64, i64, vp, vp, vp]
         L.orc_graph_integral.restype = C.c_int
         L.orc_graph_integral.argtypes = [vp]
         L.orc_plan.argtypes = [vp, C.c_double, _i64p, i64, _i64p]
@@ -139,6 +140,15 @@ class OGraph:
         u = np.empty(self.ue, np.float64)
         lib().orc_graph_union(self._h, p, d, u)
         return p, d, u
+
+    def rows(self, which, r0, r1):
+        """rows [r0, r1) of the CSR (which = 0) or the union (which = 1)."""
+        p = np.empty(r1 - r0 + 1, np.int64)
+        lib().orc_graph_rows(self._h, which, r0, r1, p.ctypes.data, None, None)
+        d = np.empty(int(p[-1]), np.int64)
+        w = np.empty(int(p[-1]), np.float64)
+        lib().orc_graph_rows(self._h, which, r0, r1, p.ctypes.data, d.ctypes.data, w.ctypes.data)
+        return p, d, w
 
     def strengths(self):
         so = np.empty(self.n, np.float64)

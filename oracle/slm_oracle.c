@@ -307,6 +307,18 @@ EXPORT void orc_graph_union(const orc_graph *g, int64_t *uptr, int64_t *unbr, do
     memcpy(unbr, g->unbr, (size_t)g->ue * sizeof(int64_t));
     memcpy(uu, g->uu, (size_t)g->ue * sizeof(double));
 }
+/* rows [r0, r1) of the CSR (which = 0) or the union (which = 1), offsets relative to r0;
+ * nbr / w nullable (size them from ptr[r1 - r0]) */
+EXPORT void orc_graph_rows(const orc_graph *g, int which, int64_t r0, int64_t r1, int64_t *ptr,
+                           int64_t *nbr, double *w) {
+    const int64_t *P = which ? g->uptr : g->out_ptr;
+    const int64_t *N = which ? g->unbr : g->out_dst;
+    const double *Wt = which ? g->uu : g->out_w;
+    for (int64_t i = 0; i <= r1 - r0; i++) ptr[i] = P[r0 + i] - P[r0];
+    int64_t cnt = P[r1] - P[r0];
+    if (nbr) memcpy(nbr, N + P[r0], (size_t)cnt * sizeof(int64_t));
+    if (w) memcpy(w, Wt + P[r0], (size_t)cnt * sizeof(double));
+}
 EXPORT void orc_graph_strengths(const orc_graph *g, double *s_out, double *s_in) {
     memcpy(s_out, g->s_out, (size_t)g->n * sizeof(double));
     memcpy(s_in, g->s_in, (size_t)g->n * sizeof(double));

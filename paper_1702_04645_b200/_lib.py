@@ -49,6 +49,7 @@ SIGNATURES = {
     "slm_get_union": (C.c_int, [_VP, _VP, _VP, _VP]),
     "slm_get_strengths": (C.c_int, [_VP, _VP, _VP]),
     "slm_get_union_rows": (C.c_int, [_VP, _I64, _I64, _VP, _VP, _VP]),
+    "slm_get_csr_rows": (C.c_int, [_VP, _I64, _I64, _VP, _VP, _VP]),
     "slm_set_resolution": (C.c_int, [_VP, C.c_double]),
     "slm_assign": (C.c_int, [_VP, _VP]),
     "slm_set_assignment": (C.c_int, [_VP, _VP]),
@@ -187,6 +188,14 @@ class Context:
         u = np.empty(int(p[-1]), np.float64)
         self.call("slm_get_union_rows", int(r0), int(r1), ptr(p), ptr(nb), ptr(u))
         return p, nb, u
+
+    def csr_rows(self, r0, r1):
+        p = np.empty(r1 - r0 + 1, np.int64)
+        self.call("slm_get_csr_rows", int(r0), int(r1), ptr(p), None, None)
+        d = np.empty(int(p[-1]), np.int64)
+        w = np.empty(int(p[-1]), np.float64)
+        self.call("slm_get_csr_rows", int(r0), int(r1), ptr(p), ptr(d), ptr(w))
+        return p, d, w
 
     def strengths(self):
         d = self.info()

@@ -543,6 +543,26 @@ int slm_get_union_rows(slm_ctx *ctx, int64_t r0, int64_t r1, int64_t *ptr_out, i
     API_END
 }
 
+int slm_get_csr_rows(slm_ctx *ctx, int64_t r0, int64_t r1, int64_t *ptr_out, int64_t *dst_out,
+                     double *w_out) {
+    API_BEGIN
+    require_graph(ctx);
+    const LevelGraph &G = *ctx->g;
+    SLM_REQUIRE(r0 >= 0 && r0 <= r1 && r1 <= G.n, SLM_EINVAL, "row range out of bounds");
+    std::vector<int64_t> p(r1 - r0 + 1);
+    CUDA_TRY(cudaMemcpy(p.data(), G.csr_ptr.p + r0, (r1 - r0 + 1) * 8, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i <= r1 - r0; i++) ptr_out[i] = p[i] - p[0];
+    const int64_t cnt = p[r1 - r0] - p[0];
+    if (dst_out && cnt) {
+        std::vector<int32_t> tmp(cnt);
+        CUDA_TRY(cudaMemcpy(tmp.data(), G.csr_dst.p + p[0], cnt * 4, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < cnt; i++) dst_out[i] = tmp[i];
+    }
+    if (w_out && cnt)
+        CUDA_TRY(cudaMemcpy(w_out, G.csr_w.p + p[0], cnt * 8, cudaMemcpyDeviceToHost));
+    API_END
+}
+
 int slm_get_strengths(slm_ctx *ctx, double *s_out, double *s_in) {
     API_BEGIN
     require_graph(ctx);
