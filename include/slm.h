@@ -121,6 +121,15 @@ SLM_API int slm_get_cstar(slm_ctx *ctx, int64_t *cstar_out);
  * (1), + community-strength gathers (2) -- the memory-system floor of the sweep; modes 3-5:
  * the same over the degree-ordered sweep view. */
 SLM_API int slm_debug_sweep_floor(slm_ctx *ctx, int32_t mode, double *ms);
+/* Diagnostics of the device primitives (slm_prim.cu), on host arrays, in place:
+ * slm_debug_sort: stable LSD radix sort by bits [0, end_bit) of (kind 0) uint64 keys with
+ * double values or (kind 1) uint32 keys with int32 values; *ms = device time of the sort.
+ * slm_debug_scan: exclusive prefix sum, kind 0 int64, 1 int32, 2 int32 -> int64, 3 double,
+ * 4 int32 restarting at every change of keys[] (keys nullable otherwise). */
+SLM_API int slm_debug_sort(slm_ctx *ctx, int32_t kind, void *keys, void *vals, int64_t n,
+                           int32_t end_bit, double *ms);
+SLM_API int slm_debug_scan(slm_ctx *ctx, int32_t kind, const void *in, void *out,
+                           const uint32_t *keys, int64_t n);
 /* maximal_correction (detector.py:457-521) for (level, sweep); gains_out nullable. */
 SLM_API int slm_maximal(slm_ctx *ctx, const slm_config *cfg, int64_t level, int64_t sweep,
                 int32_t *improved, int64_t *applied, double *gains_out, int64_t gains_cap);

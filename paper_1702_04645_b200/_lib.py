@@ -69,6 +69,8 @@ SIGNATURES = {
     "slm_plan_groups": (C.c_int, [_VP, _PI64, _VP, _VP]),
     "slm_get_cstar": (C.c_int, [_VP, _VP]),
     "slm_debug_sweep_floor": (C.c_int, [_VP, C.c_int32, _PD]),
+    "slm_debug_sort": (C.c_int, [_VP, C.c_int32, _VP, _VP, _I64, C.c_int32, _PD]),
+    "slm_debug_scan": (C.c_int, [_VP, C.c_int32, _VP, _VP, _VP, _I64]),
     "slm_build_rmat": (C.c_int, [_VP, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                  C.c_uint64, C.c_int]),
     "slm_build_rgg": (C.c_int, [_VP, _I64, C.c_double, C.c_uint64]),
@@ -308,6 +310,29 @@ class Context:
         ms = C.c_double()
         self.call("slm_debug_sweep_floor", int(mode), C.byref(ms))
         return ms.value
+
+    def debug_sort(self, keys, vals, end_bit):
+        """Stable radix sort of (uint64 keys, f64 vals) or (uint32 keys, int32 vals) by bits
+        [0, end_bit) on the device; returns (keys, vals, device ms)."""
+        keys = np.ascontiguousarray(keys).copy()
+        vals = np.ascontiguousarray(vals).copy()
+        kind = 0 if keys.dtype == np.uint64 else 1
+        ms = C.c_double()
+        self.call("slm_debug_sort", kind, ptr(keys), ptr(vals), keys.size, int(end_bit),
+                  C.byref(ms))
+        return keys, vals, ms.value
+
+    def debug_scan(self, x, keys=None, out_dtype=None):
+        """Exclusive prefix sum on the device (restarting at key changes when keys given)."""
+        x = np.ascontiguousarray(x)
+        kinds = {(np.int64, np.int64): 0, (np.int32, np.int32): 1, (np.int32, np.int64): 2,
+                 (np.float64, np.float64): 3}
+        od = np.dtype(out_dtype or x.dtype)
+        kind = 4 if keys is not None else kinds[(x.dtype.type, od.type)]
+        out = np.empty(x.size, od)
+        k = None if keys is None else np.ascontiguousarray(keys, np.uint32)
+        self.call("slm_debug_scan", kind, ptr(x), ptr(out), ptr(k), x.size)
+        return out
 
     def sync(self):
         self.call("slm_sync")

@@ -7,7 +7,6 @@
 // symmetric graph is the CSR minus self-loops with u = w + w (no second sort); a directed
 // graph merges its out-row with its in-row (stable transpose).
 #include "slm_internal.cuh"
-#include <cub/cub.cuh>
 #include <algorithm>
 #include <cstdlib>
 
@@ -15,42 +14,6 @@ int bits_for(int64_t v) {
     int b = 1;
     while ((int64_t(1) << b) < v) b++;
     return b;
-}
-
-template <class T>
-void cub_exclusive_sum(slm_ctx *ctx, const T *in, T *out, int64_t n) {
-    size_t tb = 0;
-    CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n, ctx->stream));
-    ctx->tmp.resize(tb);
-    CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx->tmp.p, tb, in, out, n, ctx->stream));
-}
-template void cub_exclusive_sum<int64_t>(slm_ctx *, const int64_t *, int64_t *, int64_t);
-template void cub_exclusive_sum<int32_t>(slm_ctx *, const int32_t *, int32_t *, int64_t);
-
-void sort_pairs_u64_f64(slm_ctx *ctx, DBuf<uint64_t> &keys, DBuf<double> &vals, int64_t n,
-                        int end_bit) {
-    ctx->u64b.resize(n);
-    ctx->f64b.resize(n);
-    cub::DoubleBuffer<uint64_t> kb(keys.p, ctx->u64b.p);
-    cub::DoubleBuffer<double> vb(vals.p, ctx->f64b.p);
-    size_t tb = 0;
-    CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, vb, n, 0, end_bit, ctx->stream));
-    ctx->tmp.resize(tb);
-    CUDA_TRY(cub::DeviceRadixSort::SortPairs(ctx->tmp.p, tb, kb, vb, n, 0, end_bit, ctx->stream));
-    if (kb.Current() != keys.p) keys.swap(ctx->u64b);
-    if (vb.Current() != vals.p) vals.swap(ctx->f64b);
-    keys.n = n;
-    vals.n = n;
-}
-
-void sort_pairs_u32_i32(slm_ctx *ctx, uint32_t *keys_in, uint32_t *keys_out, int32_t *vals_in,
-                        int32_t *vals_out, int64_t n, int end_bit) {
-    size_t tb = 0;
-    CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys_in, keys_out, vals_in, vals_out, n,
-                                             0, end_bit, ctx->stream));
-    ctx->tmp.resize(tb);
-    CUDA_TRY(cub::DeviceRadixSort::SortPairs(ctx->tmp.p, tb, keys_in, keys_out, vals_in, vals_out,
-                                             n, 0, end_bit, ctx->stream));
 }
 
 // ------------------------------------------------------------------- kernels
@@ -334,7 +297,7 @@ void build_bins(slm_ctx *ctx, LevelGraph &G) {
     for (int b = 0; b < NBINS; b++) {
         int64_t *fb = f.p + b * (n + 1);
         CUDA_TRY(cudaMemsetAsync(fb + n, 0, 8, s));
-        cub_exclusive_sum<int64_t>(ctx, fb, p.p, n + 1);
+        dev_exclusive_sum<int64_t, int64_t>(ctx, fb, p.p, n + 1);
         CUDA_TRY(cudaMemcpyAsync(&tot[b], p.p + n, 8, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
         G.bin_off[b + 1] = G.bin_off[b] + tot[b];
@@ -533,7 +496,7 @@ void build_level_from_keys(slm_ctx *ctx, LevelGraph &G, int64_t n, DBuf<uint64_t
     if (ne_in > 0) {
         k_run_heads<<<grid_for(ne_in, 256), 256, 0, s>>>(keys.p, ne_in, head.p);
         CUDA_TRY(cudaMemsetAsync(head.p + ne_in, 0, 8, s));
-        cub_exclusive_sum<int64_t>(ctx, head.p, gid.p, ne_in + 1);
+        dev_exclusive_sum<int64_t, int64_t>(ctx, head.p, gid.p, ne_in + 1);
         CUDA_TRY(cudaMemcpyAsync(&ng, gid.p + ne_in, 8, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
     }
@@ -603,7 +566,7 @@ void build_level_from_keys(slm_ctx *ctx, LevelGraph &G, int64_t n, DBuf<uint64_t
         pos.resize(ng + 1);
         CUDA_TRY(cudaMemsetAsync(keep.p, 0, (ng + 1) * 8, s));
         k_keep_nonself<<<grid_for(n * 32, 256), 256, 0, s>>>(G.csr_ptr.p, G.csr_dst.p, n, keep.p);
-        cub_exclusive_sum<int64_t>(ctx, keep.p, pos.p, ng + 1);
+        dev_exclusive_sum<int64_t, int64_t>(ctx, keep.p, pos.p, ng + 1);
         int64_t ue = 0;
         CUDA_TRY(cudaMemcpyAsync(&ue, pos.p + ng, 8, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
@@ -622,7 +585,7 @@ void build_level_from_keys(slm_ctx *ctx, LevelGraph &G, int64_t n, DBuf<uint64_t
                                                        in_ptr.p, in_src.p, in_w.p, n, 0, cnt.p,
                                                        nullptr, nullptr);
         G.uptr.resize(n + 1);
-        cub_exclusive_sum<int64_t>(ctx, cnt.p, G.uptr.p, n + 1);
+        dev_exclusive_sum<int64_t, int64_t>(ctx, cnt.p, G.uptr.p, n + 1);
         int64_t ue = 0;
         CUDA_TRY(cudaMemcpyAsync(&ue, G.uptr.p + n, 8, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
@@ -897,7 +860,7 @@ SweepView &ensure_sweep_view(slm_ctx *ctx, const LevelGraph &G) {
         CUDA_TRY(cudaMemsetAsync(vdeg.p + n, 0, 8, s));
         k_view_rows<<<grid_for(n, 256), 256, 0, s>>>(G.uptr.p, W->order.p, n, vdeg.p, nid.p);
         V.uptr.resize(n + 1);
-        cub_exclusive_sum<int64_t>(ctx, vdeg.p, V.uptr.p, n + 1);
+        dev_exclusive_sum<int64_t, int64_t>(ctx, vdeg.p, V.uptr.p, n + 1);
         V.unbr.resize(ue);
         V.uu32.resize(ue);
         k_view_entries<<<grid_for(n * 32, 256), 256, 0, s>>>(G.uptr.p, G.unbr.p, G.uu32.p,

@@ -86,6 +86,8 @@ void dcache_reserve(int dev) {
 
 // the stream of the API call in progress on this thread (set by API_BEGIN)
 static thread_local cudaStream_t g_tls_stream = nullptr;
+static thread_local int g_tls_sms = 148;
+int64_t slm_sms() { return g_tls_sms; }
 struct PendingFree {
     int dev;
     size_t off, len;
@@ -235,12 +237,20 @@ void gen_rmat_device(slm_ctx *ctx, int scale, int edge_factor, double a, double 
 void gen_rgg_device(slm_ctx *ctx, int64_t n, double radius, uint64_t seed, DBuf<int32_t> &src,
                     DBuf<int32_t> &dst, DBuf<double> &w, int64_t &ne);
 
-struct SlmStreamScope {   // the stream DBuf releases are ordered on during an API call
-    cudaStream_t prev;
-    explicit SlmStreamScope(slm_ctx *c) : prev(g_tls_stream) {
-        if (c) g_tls_stream = c->stream;
+struct SlmStreamScope {   // the stream DBuf releases are ordered on during an API call,
+    cudaStream_t prev;       // and the SM count grids are sized by
+    int prev_sms;
+    explicit SlmStreamScope(slm_ctx *c) : prev(g_tls_stream), prev_sms(g_tls_sms) {
+        if (c) {
+            g_tls_stream = c->stream;
+            g_tls_sms = c->num_sms;
+            cudaSetDevice(c->device);
+        }
     }
-    ~SlmStreamScope() { g_tls_stream = prev; }
+    ~SlmStreamScope() {
+        g_tls_stream = prev;
+        g_tls_sms = prev_sms;
+    }
 };
 #define API_BEGIN try { SlmStreamScope _slm_stream_scope(ctx);
 #define API_END                                                                           \
@@ -357,7 +367,7 @@ static void preload_modules() {
     }
     const void *anchors[] = {slm_anchor_build(), slm_anchor_capi(), slm_anchor_commit(),
                              slm_anchor_forest(), slm_anchor_gen(), slm_anchor_level(),
-                             slm_anchor_lgains(), slm_anchor_plan(), slm_anchor_positive(),
+                             slm_anchor_lgains(), slm_anchor_plan(), slm_anchor_positive(), slm_anchor_prim(),
                              slm_anchor_sweep()};
     for (const void *a : anchors) {
         cudaFunction_t f;
@@ -375,7 +385,12 @@ static void preload_modules() {
     }
 }
 
+// context creation / destruction (and the release of the shared scratch with the last
+// context) are serialised; a context itself is single-threaded (include/slm.h)
+static std::mutex g_ctx_mu;
+
 slm_ctx *slm_create(int device) {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
     slm_ctx *ctx = new slm_ctx();
     ctx->device = device;
     const char *pe = getenv("SLM_PROFILE");
@@ -389,6 +404,8 @@ slm_ctx *slm_create(int device) {
         delete ctx;
         return nullptr;
     }
+    cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (ctx->num_sms <= 0) ctx->num_sms = 148;
     // profiling runs synchronise at every phase boundary, so a lazy first-launch load would
     // be charged to the phase; preload there (and on request).  Otherwise the loads overlap
     // the asynchronously queued device work and preloading every kernel costs more (~0.2 s).
@@ -403,6 +420,7 @@ slm_ctx *slm_create(int device) {
 }
 
 void slm_destroy(slm_ctx *ctx) {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
@@ -761,6 +779,26 @@ int slm_debug_sweep_floor(slm_ctx *ctx, int32_t mode, double *ms) {
     require_agg(ctx);
     SLM_REQUIRE(ctx->g->u32_ok, SLM_EUNSUP, "needs the integer fast path");
     *ms = sweep_floor_ms(ctx, *ctx->g, ctx->f, mode);
+    API_END
+}
+
+int slm_debug_sort(slm_ctx *ctx, int32_t kind, void *keys, void *vals, int64_t n, int32_t end_bit,
+                   double *ms) {
+    API_BEGIN
+    SLM_REQUIRE(ctx && keys && vals && n >= 0 && (kind == 0 || kind == 1), SLM_EINVAL,
+                "bad sort arguments");
+    SLM_REQUIRE(end_bit >= 0 && end_bit <= (kind == 0 ? 64 : 32), SLM_EINVAL, "bad end_bit");
+    const double t = n ? debug_sort(ctx, kind, keys, vals, n, end_bit) : 0.0;
+    if (ms) *ms = t;
+    API_END
+}
+
+int slm_debug_scan(slm_ctx *ctx, int32_t kind, const void *in, void *out, const uint32_t *keys,
+                   int64_t n) {
+    API_BEGIN
+    SLM_REQUIRE(ctx && in && out && n >= 0 && kind >= 0 && kind <= 4 && (kind != 4 || keys),
+                SLM_EINVAL, "bad scan arguments");
+    if (n) debug_scan(ctx, kind, in, out, keys, n);
     API_END
 }
 

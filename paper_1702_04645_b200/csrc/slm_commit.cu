@@ -23,7 +23,6 @@
 // tail is its whole community, any other node's tail is its DFS subtree.
 #include "slm_internal.cuh"
 #include <string>
-#include <cub/cub.cuh>
 
 #define GS_LOOP(i, n)                                                                      \
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n);              \
@@ -1545,7 +1544,7 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     pos.resize(n + 1);
     CUDA_TRY(cudaMemsetAsync(flag.p + n, 0, 4, s));
     k_cand_flags<<<grid_for(n, 256), 256, 0, s>>>(d_cstar, F.comm.p, n, flag.p);
-    cub_exclusive_sum<int32_t>(ctx, flag.p, pos.p, n + 1);
+    dev_exclusive_sum<int32_t, int32_t>(ctx, flag.p, pos.p, n + 1);
     int32_t K = 0;
     CUDA_TRY(cudaMemcpyAsync(&K, pos.p + n, 4, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -1593,7 +1592,7 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
         st_[st_i++] = t - st_t;
         st_t = t;
     };
-    unsigned GW = grid_for((int64_t)K * 32, 256, 148LL * 32);
+    unsigned GW = grid_for((int64_t)K * 32, 256, SMS() * 32);
     DBuf<int32_t> &big = CS.big;
     big.resize(K + 1);   // [K] = count
     int32_t *nbig = big.p + K;
@@ -1619,12 +1618,12 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
         CUDA_TRY(cudaStreamSynchronize(s));
     }
     if (big_items && hnbig > 0) {
-        const unsigned GB_ = (unsigned)std::min<int64_t>(hnbig, 148 * 8);
+        const unsigned GB_ = (unsigned)std::min<int64_t>(hnbig, SMS() * 8);
         CS.bcnt.resize(hnbig + 1);
         CS.boff.resize(hnbig + 1);
         CUDA_TRY(cudaMemsetAsync(CS.bcnt.p + hnbig, 0, 8, s));
         k_big_count<<<GB_, 256, 0, s>>>(A, big.p, nbig, CS.bcnt.p);
-        cub_exclusive_sum<int64_t>(ctx, CS.bcnt.p, CS.boff.p, hnbig + 1);
+        dev_exclusive_sum<int64_t, int64_t>(ctx, CS.bcnt.p, CS.boff.p, hnbig + 1);
         CUDA_TRY(cudaMemcpyAsync(&NIT, CS.boff.p + hnbig, 8, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
         CS.bitems.resize(std::max<int64_t>(1, NIT));
@@ -1638,12 +1637,12 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
         CUDA_TRY(cudaMemsetAsync(CS.acc_wf.p, 0, hnbig * 8, s));
         k_big_fill<<<GB_, 256, 0, s>>>(A, big.p, nbig, CS.boff.p, CS.bitems.p, CS.ri_off.p,
                                        CS.ri_cnt.p);
-        k_big_items_spec<<<grid_for(NIT * 32, 256, 148LL * 64), 256, 0, s>>>(
+        k_big_items_spec<<<grid_for(NIT * 32, 256, SMS() * 64), 256, 0, s>>>(
             A, big.p, CS.bitems.p, NIT, CS.acc_wt.p, CS.acc_wf.p, CS.part_bt.p, CS.part_be.p);
         k_big_finish<<<GB_, 256, 0, s>>>(A, big.p, nbig, CS.acc_wt.p, CS.acc_wf.p, CS.part_bt.p,
                                          CS.part_be.p, CS.ri_off.p, CS.ri_cnt.p, spec.p, mvcnt.p);
     } else if (!big_items) {
-        k_spec_big<<<148 * 4, SPEC_BLOCK, 0, s>>>(A, big.p, nbig, spec.p, mvcnt.p);
+        k_spec_big<<<SMS() * 4, SPEC_BLOCK, 0, s>>>(A, big.p, nbig, spec.p, mvcnt.p);
     }
     stick();
     CUDA_TRY(cudaMemsetAsync(moving.p, 0, n, s));
@@ -1655,7 +1654,7 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     DBuf<uint8_t> &mv_i = CS.mv_i;
 
     stick();
-    cub_exclusive_sum<int64_t>(ctx, mvcnt.p, mvoff.p, K + 1);
+    dev_exclusive_sum<int64_t, int64_t>(ctx, mvcnt.p, mvoff.p, K + 1);
     int64_t NMV = 0;
     CUDA_TRY(cudaMemcpyAsync(&NMV, mvoff.p + K, 8, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -1670,13 +1669,13 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
         if (hnbig > 0) {
             CS.bctr.resize(hnbig);
             CUDA_TRY(cudaMemsetAsync(CS.bctr.p, 0, hnbig * 8, s));
-            k_big_items_mv<<<grid_for(NIT * 32, 256, 148LL * 64), 256, 0, s>>>(
+            k_big_items_mv<<<grid_for(NIT * 32, 256, SMS() * 64), 256, 0, s>>>(
                 A, big.p, CS.bitems.p, NIT, spec.p, moving.p, CS.bctr.p, mv_z.p, mv_u.p, mv_e.p,
                 mv_i.p);
             k_big_mv_finish<<<grid_for(hnbig, 256), 256, 0, s>>>(big.p, nbig, CS.bctr.p, spec.p);
         }
     } else {
-        k_mv_scan_big<<<148 * 4, SPEC_BLOCK, 0, s>>>(A, big.p, nbig, spec.p, moving.p, 1, nullptr,
+        k_mv_scan_big<<<SMS() * 4, SPEC_BLOCK, 0, s>>>(A, big.p, nbig, spec.p, moving.p, 1, nullptr,
                                                      mv_z.p, mv_u.p, mv_e.p, mv_i.p);
     }
     stick();
@@ -1686,7 +1685,7 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     apos.resize(K + 1);
     CUDA_TRY(cudaMemsetAsync(af.p + K, 0, 4, s));
     k_acc_flags<<<grid_for(K, 256), 256, 0, s>>>(K, status.p, af.p);
-    cub_exclusive_sum<int32_t>(ctx, af.p, apos.p, K + 1);
+    dev_exclusive_sum<int32_t, int32_t>(ctx, af.p, apos.p, K + 1);
     int32_t NA = 0;
     CUDA_TRY(cudaMemcpyAsync(&NA, apos.p + K, 4, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -1736,7 +1735,7 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
         CUDA_TRY(cudaMemsetAsync(CS.wwait.p, 0xff, nc * sizeof(int2), s));   // {-1, -1}
         CUDA_TRY(cudaMemsetAsync(wf.p + nc, 0, 4, s));
         k_walker_list<<<grid_for(nc, 256), 256, 0, s>>>(tl_ptr.p, nc, wf.p);
-        cub_exclusive_sum<int32_t>(ctx, wf.p, wp.p, nc + 1);
+        dev_exclusive_sum<int32_t, int32_t>(ctx, wf.p, wp.p, nc + 1);
         int32_t NW = 0;
         CUDA_TRY(cudaMemcpyAsync(&NW, wp.p + nc, 4, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
@@ -1771,7 +1770,7 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
                     "sort+walkers %.2f scatter %.2f ms\n", K, NA, st_[0], st_[1], st_[2], st_[3],
                     st_[4], st_[5]);
         phase_mark(ctx, PH_SPEC);
-        const unsigned GWK = grid_for((int64_t)NW * 32, 256, 148LL * 64);
+        const unsigned GWK = grid_for((int64_t)NW * 32, 256, SMS() * 64);
         int32_t rem = NA;
         std::vector<double> rt;
         const bool wprof = ctx->prof && getenv("SLM_PROFILE_WALK");
@@ -1783,14 +1782,17 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
             V.wst = wst.p;
         }
         // one persistent launch on a resident grid (SLM_WALK_ROUNDS=1: relaunch per round)
-        static int walk_blocks = 0;
-        if (walk_blocks == 0) {
+        // walkers park and spin on verdicts of other blocks, so the persistent grid must be
+        // co-resident: occupancy x the device's SMs, launched cooperatively (the launch fails
+        // instead of deadlocking when the grid cannot be resident, e.g. under MPS limits;
+        // then this call falls back to one launch per round)
+        if (ctx->walk_blocks == 0) {
             int per_sm = 0;
             CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk, WALK_BLOCK, 0));
-            walk_blocks = std::max(1, per_sm) * 148;
+            ctx->walk_blocks = std::max(1, per_sm) * ctx->num_sms;
         }
-        static const bool rounds_mode = getenv("SLM_WALK_ROUNDS") != nullptr;
-        const unsigned GWP = (unsigned)std::min<int64_t>(GWK, walk_blocks);
+        bool rounds_mode = getenv("SLM_WALK_ROUNDS") != nullptr;
+        const unsigned GWP = (unsigned)std::min<int64_t>(GWK, ctx->walk_blocks);
         // timelines longer than LONG_TL events (hub communities) are walked by whole CTAs,
         // blocks [0, nlong) of the persistent grid (at most 16: the rest walk the many short
         // timelines of the early sweeps)
@@ -1804,7 +1806,7 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
             lp.resize(NW + 1);
             CUDA_TRY(cudaMemsetAsync(lf.p + NW, 0, 4, s));
             k_long_flags<<<grid_for(NW, 256), 256, 0, s>>>(wl.p, NW, tl_ptr.p, LONG_TL, lf.p);
-            cub_exclusive_sum<int32_t>(ctx, lf.p, lp.p, NW + 1);
+            dev_exclusive_sum<int32_t, int32_t>(ctx, lf.p, lp.p, NW + 1);
             int32_t NL = 0;
             CUDA_TRY(cudaMemcpyAsync(&NL, lp.p + NW, 4, cudaMemcpyDeviceToHost, s));
             CUDA_TRY(cudaStreamSynchronize(s));
@@ -1824,9 +1826,24 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
             if (rounds_mode)
                 k_walk<<<GWK, WALK_BLOCK, 0, s>>>(A, V, wl.p, NW, status.p, spec.p, 0, nullptr, 0,
                                                   nullptr);
-            else
-                k_walk<<<GWP, WALK_BLOCK, 0, s>>>(A, V, wl.p, NW, status.p, spec.p, 1, CS.wlong.p,
-                                                  nlong, cmode);
+            else {
+                int one = 1;
+                int64_t nw64 = NW;
+                const int32_t *wlp = wl.p, *wlg = CS.wlong.p;
+                int32_t *stp = status.p;
+                const CandSpec *spp = spec.p;
+                void *kargs[] = {(void *)&A, (void *)&V, (void *)&wlp, (void *)&nw64, (void *)&stp,
+                                 (void *)&spp, (void *)&one, (void *)&wlg, (void *)&nlong,
+                                 (void *)&cmode};
+                cudaError_t le = cudaLaunchCooperativeKernel((const void *)k_walk, dim3(GWP),
+                                                             dim3(WALK_BLOCK), kargs, 0, s);
+                if (le != cudaSuccess) {
+                    cudaGetLastError();
+                    rounds_mode = true;
+                    k_walk<<<GWK, WALK_BLOCK, 0, s>>>(A, V, wl.p, NW, status.p, spec.p, 0, nullptr,
+                                                      0, nullptr);
+                }
+            }
             CUDA_TRY(cudaMemcpyAsync(&rem, remaining.p, 4, cudaMemcpyDeviceToHost, s));
             CUDA_TRY(cudaStreamSynchronize(s));
             if (ctx->prof) rt.push_back(now_ms() - t0);
@@ -1861,7 +1878,7 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
     cpos.resize(K + 1);
     CUDA_TRY(cudaMemsetAsync(cf.p + K, 0, 4, s));
     k_commit_flags<<<GK, 256, 0, s>>>(K, status.p, cf.p);
-    cub_exclusive_sum<int32_t>(ctx, cf.p, cpos.p, K + 1);
+    dev_exclusive_sum<int32_t, int32_t>(ctx, cf.p, cpos.p, K + 1);
     int32_t hv[2] = {0, 0};
     CUDA_TRY(cudaMemcpyAsync(&hv[0], cpos.p + K, 4, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(&hv[1], dflags, 4, cudaMemcpyDeviceToHost, s));
@@ -1925,7 +1942,7 @@ void commit_wown_deltas(slm_ctx *ctx, const LevelGraph &G, const int32_t *pre, c
     pos.resize(n + 1);
     CUDA_TRY(cudaMemsetAsync(f.p + n, 0, 4, s));
     k_wown_flags<<<grid_for(n, 256), 256, 0, s>>>(pre, post, n, f.p);
-    cub_exclusive_sum<int32_t>(ctx, f.p, pos.p, n + 1);
+    dev_exclusive_sum<int32_t, int32_t>(ctx, f.p, pos.p, n + 1);
     int32_t nm = 0;
     CUDA_TRY(cudaMemcpyAsync(&nm, pos.p + n, 4, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));

@@ -17,7 +17,6 @@
 // Arbitrary functional graphs (longer cycles) fall back to the reference's pointer
 // doubling, so extract_components keeps its full contract.
 #include "slm_internal.cuh"
-#include <cub/cub.cuh>
 
 #define GS_LOOP(i, n)                                                                      \
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n);              \
@@ -399,7 +398,7 @@ void run_components(slm_ctx *ctx, Forest &F, int64_t n) {
     lab.resize(n + 1);
     CUDA_TRY(cudaMemsetAsync(h.p + n, 0, 4, s));
     k_head_flag<<<G, 256, 0, s>>>(key, first, n, h.p);
-    cub_exclusive_sum<int32_t>(ctx, h.p, lab.p, n + 1);
+    dev_exclusive_sum<int32_t, int32_t>(ctx, h.p, lab.p, n + 1);
     F.croot.resize(n);
     k_assign_label<<<G, 256, 0, s>>>(key, first, lab.p, n, F.comm.p, F.croot.p);
     int32_t nc = 0;
@@ -520,12 +519,7 @@ void build_layout(slm_ctx *ctx, Forest &F) {
     offp.resize(n);
     if (nk > 0) {
         k_kid_vals<<<grid_for(nk, 256), 256, 0, s>>>(F.kids.p, nk, F.comm.p, F.croot.p, F.sz.p, val.p);
-        size_t tb = 0;
-        CUDA_TRY(cub::DeviceScan::ExclusiveSumByKey(nullptr, tb, (const uint32_t *)ks, val.p, ex.p,
-                                                    (int64_t)nk, cub::Equality(), s));
-        ctx->tmp.resize(tb);
-        CUDA_TRY(cub::DeviceScan::ExclusiveSumByKey(ctx->tmp.p, tb, (const uint32_t *)ks, val.p,
-                                                    ex.p, (int64_t)nk, cub::Equality(), s));
+        dev_exclusive_sum_by_key(ctx, (const uint32_t *)ks, val.p, ex.p, (int64_t)nk);
         k_kid_off<<<grid_for(nk, 256), 256, 0, s>>>(F.kids.p, ex.p, nk, offp.p);
     }
     k_positions<<<grid_for(n, 256), 256, 0, s>>>(F.a.p, F.comm.p, F.croot.p, offp.p, F.cptr.p, n,

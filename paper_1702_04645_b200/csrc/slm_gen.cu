@@ -7,7 +7,6 @@
 // tests/test_gpu_parity.py checks the two builds bit for bit.
 #include "slm_internal.cuh"
 #include "../../include/slm.h"
-#include <cub/cub.cuh>
 #include <cmath>
 
 #define GS_LOOP(i, n)                                                                      \
@@ -104,7 +103,7 @@ void gen_rmat_device(slm_ctx *ctx, int scale, int edge_factor, double a, double 
     k_i32_to_i64<<<grid_for(m, 256), 256, 0, s>>>(keep.p, m, keep64.p);
     CUDA_TRY(cudaMemsetAsync(keep64.p + m, 0, 8, s));
     keep.release();
-    cub_exclusive_sum<int64_t>(ctx, keep64.p, pos.p, m + 1);
+    dev_exclusive_sum<int64_t, int64_t>(ctx, keep64.p, pos.p, m + 1);
     int64_t kept = 0;
     CUDA_TRY(cudaMemcpyAsync(&kept, pos.p + m, 8, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -198,7 +197,7 @@ void gen_rgg_device(slm_ctx *ctx, int64_t n, double radius, uint64_t seed, DBuf<
     const double r2 = radius * radius;
     k_rgg_pass<<<grid_for(n, 128), 128, 0, s>>>(X.p, Y.p, cptr.p, pts.p, n, G, r2, nullptr, cnt.p,
                                                 nullptr, nullptr, nullptr);
-    cub_exclusive_sum<int64_t>(ctx, cnt.p, pos.p, n + 1);
+    dev_exclusive_sum<int64_t, int64_t>(ctx, cnt.p, pos.p, n + 1);
     CUDA_TRY(cudaMemcpyAsync(&ne, pos.p + n, 8, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     src.resize(ne);

@@ -200,6 +200,8 @@ struct slm_ctx {
     double ph_ms[NPHASE] = {};
     double ph_t0 = 0.0;
     int device = 0;
+    int num_sms = 148;           // cudaDevAttrMultiProcessorCount of the device
+    int walk_blocks = 0;         // co-resident grid of the persistent commit walker (cached)
     cudaStream_t stream = nullptr;
     cudaStream_t stream2 = nullptr;              // side stream of the plan sweep (hub rows)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -219,7 +221,11 @@ struct slm_ctx {
     bool wown_fresh = false;   // set by the view sweep that just wrote wown
     bool wown_in_view = false; // wown still in the sweep view's row order (vwown), not scattered
     // scratch
-    DBuf<uint8_t> tmp;           // CUB temp storage
+    DBuf<uint8_t> tmp;           // scan / sort status and histogram scratch (slm_prim.cu)
+    DBuf<uint64_t> sort_k64;     // radix sort ping-pong buffers
+    DBuf<double> sort_v64;
+    DBuf<uint32_t> sort_k32;
+    DBuf<int32_t> sort_v32;
     DBuf<int64_t> i64a, i64b;
     DBuf<int32_t> i32a, i32b, i32c, i32d;
     DBuf<double> f64a, f64b;
@@ -261,7 +267,11 @@ static inline void phase_mark(slm_ctx *ctx, int ph) {
     ctx->ph_t0 = t;
 }
 
-static inline unsigned grid_for(int64_t work, int block, int64_t cap = 148LL * 64) {
+// SM count of the device of the API call in flight (set with the call's stream, slm_capi.cu)
+int64_t slm_sms();
+#define SMS() slm_sms()
+
+static inline unsigned grid_for(int64_t work, int block, int64_t cap = SMS() * 64) {
     int64_t g = (work + block - 1) / block;
     if (g < 1) g = 1;
     if (g > cap) g = cap;
@@ -379,13 +389,18 @@ void run_aggregate(slm_ctx *ctx, const LevelGraph &G, const int32_t *d_labels, i
 double run_score(slm_ctx *ctx, const LevelGraph &G, const int32_t *d_labels, double gamma);
 void forest_refresh(slm_ctx *ctx, const LevelGraph &G, Forest &F);   // comps + agg + layout
 
-template <class T>
-void cub_exclusive_sum(slm_ctx *ctx, const T *in, T *out, int64_t n);
+// slm_prim.cu: single-pass decoupled look-back scans and the onesweep LSD radix sort
+template <class TI, class TO>
+void dev_exclusive_sum(slm_ctx *ctx, const TI *in, TO *out, int64_t n);
+void dev_exclusive_sum_by_key(slm_ctx *ctx, const uint32_t *keys, const int32_t *in, int32_t *out,
+                              int64_t n);
 void sort_pairs_u64_f64(slm_ctx *ctx, DBuf<uint64_t> &keys, DBuf<double> &vals, int64_t n,
                         int end_bit);
 void sort_pairs_u32_i32(slm_ctx *ctx, uint32_t *keys_in, uint32_t *keys_out, int32_t *vals_in,
                         int32_t *vals_out, int64_t n, int end_bit);
 int bits_for(int64_t v);
+double debug_sort(slm_ctx *ctx, int kind, void *keys, void *vals, int64_t n, int end_bit);
+void debug_scan(slm_ctx *ctx, int kind, const void *in, void *out, const uint32_t *keys, int64_t n);
 
 // one kernel per translation unit: their modules are loaded at context creation
 const void *slm_anchor_build();
@@ -397,4 +412,5 @@ const void *slm_anchor_level();
 const void *slm_anchor_lgains();
 const void *slm_anchor_plan();
 const void *slm_anchor_positive();
+const void *slm_anchor_prim();
 const void *slm_anchor_sweep();

@@ -32,7 +32,7 @@ void run_aggregate(slm_ctx *ctx, const LevelGraph &G, const int32_t *d_labels, i
     keys.resize(G.ne);
     vals.resize(G.ne);
     if (G.ne > 0)
-        k_coarse_keys<<<grid_for(G.n * 32, 256, 148LL * 64), 256, 0, ctx->stream>>>(
+        k_coarse_keys<<<grid_for(G.n * 32, 256, SMS() * 64), 256, 0, ctx->stream>>>(
             G.csr_ptr.p, G.csr_dst.p, G.csr_w.p, d_labels, G.n, bits_for(n_comms), keys.p, vals.p);
     build_level_from_keys(ctx, out, n_comms, keys, vals, G.ne);
 }
@@ -104,9 +104,9 @@ double run_score(slm_ctx *ctx, const LevelGraph &G, const int32_t *d_labels, dou
     flag.resize(ne + 1);
     pos.resize(ne + 1);
     CUDA_TRY(cudaMemsetAsync(flag.p + ne, 0, 8, s));
-    k_intra_flags<<<grid_for(n * 32, 256, 148LL * 64), 256, 0, s>>>(G.csr_ptr.p, G.csr_dst.p,
+    k_intra_flags<<<grid_for(n * 32, 256, SMS() * 64), 256, 0, s>>>(G.csr_ptr.p, G.csr_dst.p,
                                                                      d_labels, n, flag.p);
-    cub_exclusive_sum<int64_t>(ctx, flag.p, pos.p, ne + 1);
+    dev_exclusive_sum<int64_t, int64_t>(ctx, flag.p, pos.p, ne + 1);
     int64_t nin = 0;
     CUDA_TRY(cudaMemcpyAsync(&nin, pos.p + ne, 8, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));

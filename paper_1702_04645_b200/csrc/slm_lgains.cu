@@ -206,7 +206,7 @@ void run_local_gains_u32(slm_ctx *ctx, const LevelGraph &G_, Forest &F, double m
     if (nb(1, 4))
         k_lg_warp<<<grid_for(nb(1, 4) * 32, 256), 256, 0, s>>>(A, rows + G.bin_off[1], nb(1, 4));
     if (nb(4, NBINS))
-        k_lg_cta<<<(unsigned)std::min<int64_t>(nb(4, NBINS), 148 * 8), 256, 0, s>>>(
+        k_lg_cta<<<(unsigned)std::min<int64_t>(nb(4, NBINS), SMS() * 8), 256, 0, s>>>(
             A, rows + G.bin_off[4], nb(4, NBINS));
     if (G.n) k_lg_empty<<<grid_for(G.n, 256), 256, 0, s>>>(A, G.n);
     CUDA_TRY(cudaGetLastError());

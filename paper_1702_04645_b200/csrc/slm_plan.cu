@@ -254,7 +254,7 @@ void run_plan(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_t *d
     int64_t nm = G.bin_off[4] - G.bin_off[1];
     int64_t nl = G.bin_off[6] - G.bin_off[4];
     if (ns && (bin_mask & 1))
-        k_plan_small<<<grid_for(ns * 32, 256, 148LL * 64), 256, 0, s>>>(A, G.bin_rows.p + G.bin_off[0], ns);
+        k_plan_small<<<grid_for(ns * 32, 256, SMS() * 64), 256, 0, s>>>(A, G.bin_rows.p + G.bin_off[0], ns);
     if (nm && (bin_mask & 14)) {
         size_t sm = MID_H * (sizeof(double) + sizeof(int32_t));
         static bool attr = false;
@@ -262,12 +262,12 @@ void run_plan(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_t *d
             CUDA_TRY(cudaFuncSetAttribute(k_plan_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             attr = true;
         }
-        k_plan_mid<<<(unsigned)std::min<int64_t>(nm, 148 * 2 * 8), MID_BLOCK, sm, s>>>(A, G.bin_rows.p + G.bin_off[1], nm);
+        k_plan_mid<<<(unsigned)std::min<int64_t>(nm, SMS() * 2 * 8), MID_BLOCK, sm, s>>>(A, G.bin_rows.p + G.bin_off[1], nm);
     }
     if (nl && (bin_mask & 48)) {
         ctx->hash_keys.resize(G.large_hash_total);
         ctx->hash_vals.resize(G.large_hash_total);
-        k_plan_large<<<(unsigned)std::min<int64_t>(nl, 148 * 2), LARGE_BLOCK, 0, s>>>(
+        k_plan_large<<<(unsigned)std::min<int64_t>(nl, SMS() * 2), LARGE_BLOCK, 0, s>>>(
             A, G.bin_rows.p + G.bin_off[4], nl, G.large_hoff.p, ctx->hash_keys.p, ctx->hash_vals.p);
     }
     CUDA_TRY(cudaGetLastError());
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(256) k_assign(const int64_t *uptr, const int32
 
 void run_assign(slm_ctx *ctx, const LevelGraph &G, double m, int32_t *d_a) {
     int64_t n = G.n;
-    k_assign<<<grid_for(n * 32, 256, 148LL * 64), 256, 0, ctx->stream>>>(
+    k_assign<<<grid_for(n * 32, 256, SMS() * 64), 256, 0, ctx->stream>>>(
         G.uptr.p, G.unbr.p, G.uu.p, G.s_out.p, G.s_in.p, n, m, m * m, d_a);
     CUDA_TRY(cudaGetLastError());
 }
@@ -353,7 +353,7 @@ void run_local_gains(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, dou
         run_local_gains_u32(ctx, G, F, m, d_lg, d_bad);
         return;
     }
-    k_local_gains<<<grid_for(n * 32, 256, 148LL * 64), 256, 0, ctx->stream>>>(
+    k_local_gains<<<grid_for(n * 32, 256, SMS() * 64), 256, 0, ctx->stream>>>(
         G.uptr.p, G.unbr.p, G.uu.p, F.comm.p, F.S_out.p, F.S_in.p, G.s_out.p, G.s_in.p, n, m,
         d_lg, d_bad);
     CUDA_TRY(cudaGetLastError());

@@ -24,7 +24,6 @@
 //    full O(edges(part)) recomputation.  Subtree ranges keep the community's original DFS
 //    coordinates; removed members are masked by their part id.
 #include "slm_internal.cuh"
-#include <cub/cub.cuh>
 #include <algorithm>
 #include <cstring>
 #include <cstdlib>
@@ -1463,7 +1462,7 @@ static void launch_small(slm_ctx *ctx, PosArgs &A, const std::vector<PartDesc> &
     A.nparts = np;
     A.ngains = ngains.p;
     A.neg_unres = nunres.p;
-    k_positive<<<grid_for(np * 32, 128, 148LL * 64), 128, 0, s>>>(A);
+    k_positive<<<grid_for(np * 32, 128, SMS() * 64), 128, 0, s>>>(A);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(hng.data(), ngains.p, np * 4, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(hun.data(), nunres.p, np * 4, cudaMemcpyDeviceToHost, s));
@@ -1525,7 +1524,7 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     pos.resize(nc + 1);
     CUDA_TRY(cudaMemsetAsync(f.p + nc, 0, 4, s));
     k_bad_flags<<<grid_for(nc, 256), 256, 0, s>>>(bad.p, nc, f.p);
-    cub_exclusive_sum<int32_t>(ctx, f.p, pos.p, nc + 1);
+    dev_exclusive_sum<int32_t, int32_t>(ctx, f.p, pos.p, nc + 1);
     int32_t nbad = 0;
     CUDA_TRY(cudaMemcpyAsync(&nbad, pos.p + nc, 4, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -1550,7 +1549,7 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
             hp.resize(n + 1);
             CUDA_TRY(cudaMemsetAsync(hf.p + n, 0, 4, s));
             k_heavy_flags<<<grid_for(n, 256), 256, 0, s>>>(G.uptr.p, n, HEAVY_DEG, hf.p);
-            cub_exclusive_sum<int32_t>(ctx, hf.p, hp.p, n + 1);
+            dev_exclusive_sum<int32_t, int32_t>(ctx, hf.p, hp.p, n + 1);
             int32_t nh = 0;
             CUDA_TRY(cudaMemcpyAsync(&nh, hp.p + n, 4, cudaMemcpyDeviceToHost, s));
             CUDA_TRY(cudaStreamSynchronize(s));
@@ -1816,31 +1815,21 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
             CUDA_TRY(cudaMemsetAsync(SC.nch.p + N, 0, 4, s));
             const int build_intra = first_wave ? 1 : 0;
             k_gb_chunks<<<grid_for(N, 256), 256, 0, s>>>(GA, dsl, ns, N, SC.nch.p, build_intra);
-            {
-                size_t tb = 0;
-                CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, SC.nch.p, SC.choff.p, N + 1, s));
-                ctx->tmp.resize(tb);
-                CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx->tmp.p, tb, SC.nch.p, SC.choff.p, N + 1, s));
-            }
+            dev_exclusive_sum<int32_t, int64_t>(ctx, SC.nch.p, SC.choff.p, N + 1);
             int64_t nck = 0;
             CUDA_TRY(cudaMemcpyAsync(&nck, SC.choff.p + N, 8, cudaMemcpyDeviceToHost, s));
             CUDA_TRY(cudaStreamSynchronize(s));
             SC.chunks.resize(std::max<int64_t>(1, nck));
             k_gb_expand<<<grid_for(N, 256), 256, 0, s>>>(GA, dsl, ns, N, SC.nch.p, SC.choff.p,
                                                         SC.chunks.p);
-            const unsigned GW = grid_for(nck * 32, 256, 148LL * 32);
+            const unsigned GW = grid_for(nck * 32, 256, SMS() * 32);
             k_gb_wpart<<<GW, 256, 0, s>>>(GA, dsl, ns, SC.chunks.p, nck, build_intra);
             if (build_intra) {   // intra-part adjacency lists of the wave-0 members
                 SC.icnt_flat.resize(N + 1);
                 SC.ioff_flat.resize(N + 1);
                 k_gb_icount<<<grid_for(N, 256), 256, 0, s>>>(GA, dsl, ns, N, SC.icnt_flat.p);
                 CUDA_TRY(cudaMemsetAsync(SC.icnt_flat.p + N, 0, 8, s));
-                size_t tb = 0;
-                CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, SC.icnt_flat.p, SC.ioff_flat.p,
-                                                       N + 1, s));
-                ctx->tmp.resize(tb);
-                CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx->tmp.p, tb, SC.icnt_flat.p, SC.ioff_flat.p,
-                                                       N + 1, s));
+                dev_exclusive_sum<int64_t, int64_t>(ctx, SC.icnt_flat.p, SC.ioff_flat.p, N + 1);
                 int64_t nintra = 0;
                 CUDA_TRY(cudaMemcpyAsync(&nintra, SC.ioff_flat.p + N, 8, cudaMemcpyDeviceToHost, s));
                 CUDA_TRY(cudaStreamSynchronize(s));
@@ -1864,7 +1853,7 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
             }
             k_gb_dep<<<grid_for(N, 256), 256, 0, s>>>(GA, dsl, ns, N);
             if (build_intra && nintra_w0 > 0 && getenv("SLM_LCA_CHUNKS") == nullptr)
-                k_gb_lca_flat<<<grid_for(nintra_w0, 256, 148LL * 32), 256, 0, s>>>(GA, nintra_w0);
+                k_gb_lca_flat<<<grid_for(nintra_w0, 256, SMS() * 32), 256, 0, s>>>(GA, nintra_w0);
             else
                 k_gb_lca<<<GW, 256, 0, s>>>(GA, dsl, ns, SC.chunks.p, nck);
             vso.resize(N + 1);
@@ -1877,14 +1866,9 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
             CUDA_TRY(cudaMemsetAsync(vso.p + N, 0, 8, s));
             CUDA_TRY(cudaMemsetAsync(vsi.p + N, 0, 8, s));
             CUDA_TRY(cudaMemsetAsync(vdp.p + N, 0, 8, s));
-            {
-                size_t tb = 0;
-                CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, vso.p, pso2.p, N + 1, s));
-                ctx->tmp.resize(tb);
-                CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx->tmp.p, tb, vso.p, pso2.p, N + 1, s));
-                CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx->tmp.p, tb, vsi.p, psi2.p, N + 1, s));
-                CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx->tmp.p, tb, vdp.p, pdp2.p, N + 1, s));
-            }
+            dev_exclusive_sum<double, double>(ctx, vso.p, pso2.p, N + 1);
+            dev_exclusive_sum<double, double>(ctx, vsi.p, psi2.p, N + 1);
+            dev_exclusive_sum<double, double>(ctx, vdp.p, pdp2.p, N + 1);
             k_gb_subsums<<<grid_for(N, 256), 256, 0, s>>>(GA, dsl, ns, N, pso2.p, psi2.p, pdp2.p);
             tmark(7);
             tp[3] += tp[7] - tp[6];

@@ -1,0 +1,515 @@
+// slm_prim.cu -- the library's own device primitives: single-pass prefix scans and a stable
+// onesweep LSD radix sort (no CUB).  They carry the sort + segmented-reduce of the CSR build
+// and the aggregation (Graph.from_edges / aggregate: graph.py:97-116, 266-280 -- numpy's
+// stable lexsort, reduceat offsets and bincount/cumsum pointers), the forest's member and
+// child lists, the commit timelines and the POSITIVE layouts.
+//
+// Scan.  One launch: every CTA takes the next tile id from an atomic counter (so a tile only
+// ever waits on tiles that are already running), reduces its tile, publishes the aggregate,
+// then walks back over its predecessors' published aggregates / inclusive prefixes
+// ("decoupled look-back") until it meets an inclusive prefix, publishes its own inclusive
+// prefix and writes the tile.  The segmented form (exclusive sum restarting at every key
+// change) scans (value, head) pairs with the segmented operator.  Tiles combine in a fixed
+// order, so results are deterministic (for fp64 operands too).
+//
+// Radix sort.  8-bit digits, least significant first; one histogram kernel counts the
+// digits of every pass in a single read of the keys, then one onesweep kernel per pass:
+//   - a tile of 16 keys per thread is ranked warp by warp: each warp walks its contiguous
+//     segment in input order in 32-key chunks, __match_any_sync groups equal digits, the
+//     group leader bumps the warp's private digit counter (stable by construction);
+//   - per digit, warp offsets and the tile count, then the tile's global offset by
+//     decoupled look-back over the preceding tiles (one 64-bit {flag, count} word per
+//     (tile, digit));
+//   - keys (then values) are staged in shared memory in digit order and written out from
+//     there, so every digit's run leaves the CTA as contiguous stores.
+#include "slm_internal.cuh"
+
+namespace {
+
+constexpr int SCAN_BLOCK = 256;
+constexpr int SCAN_ITEMS = 8;
+constexpr int SCAN_TILE = SCAN_BLOCK * SCAN_ITEMS;
+
+__device__ __forceinline__ int ld_flag(const int *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_flag(int *p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// scan state: value plus (segmented form) "a segment starts inside" flag
+template <class T, bool SEG>
+struct SS {
+    T v;
+    int h;
+};
+template <class T, bool SEG>
+__device__ __forceinline__ SS<T, SEG> sop(SS<T, SEG> a, SS<T, SEG> b) {
+    if (SEG && b.h) return b;
+    return {a.v + b.v, a.h | b.h};
+}
+
+template <class T, bool SEG>
+__device__ __forceinline__ SS<T, SEG> shfl_up_ss(SS<T, SEG> x, int d) {
+    SS<T, SEG> y;
+    y.v = __shfl_up_sync(0xffffffffu, x.v, d);
+    y.h = __shfl_up_sync(0xffffffffu, x.h, d);
+    return y;
+}
+
+// tile status: flag 0 = not ready, 1 = aggregate, 2 = inclusive prefix
+template <class T>
+struct ScanStatus {
+    int *flag;
+    T *agg, *inc;
+    int *hagg, *hinc;
+    unsigned *ticket;
+};
+
+template <class TI, class TO, bool SEG>
+__global__ void __launch_bounds__(SCAN_BLOCK) k_scan(const TI *in, TO *out, const uint32_t *keys,
+                                                     int64_t n, ScanStatus<TO> st) {
+    __shared__ unsigned s_tile;
+    __shared__ SS<TO, SEG> s_warp[SCAN_BLOCK / 32];
+    __shared__ SS<TO, SEG> s_prefix;
+    if (threadIdx.x == 0) s_tile = atomicAdd(st.ticket, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t base = tile * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    SS<TO, SEG> x[SCAN_ITEMS];
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; i++) {
+        const int64_t k = base + i;
+        x[i].v = k < n ? (TO)in[k] : (TO)0;
+        x[i].h = 0;
+        if (SEG && k < n) x[i].h = (k == 0 || keys[k] != keys[k - 1]) ? 1 : 0;
+    }
+    // thread inclusive scan
+    SS<TO, SEG> t = x[0];
+#pragma unroll
+    for (int i = 1; i < SCAN_ITEMS; i++) t = sop<TO, SEG>(t, x[i]);
+    // warp inclusive scan of thread totals
+    SS<TO, SEG> w = t;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        SS<TO, SEG> y = shfl_up_ss<TO, SEG>(w, d);
+        if (lane >= d) w = sop<TO, SEG>(y, w);
+    }
+    if (lane == 31) s_warp[wid] = w;
+    __syncthreads();
+    if (wid == 0) {
+        SS<TO, SEG> v = lane < SCAN_BLOCK / 32 ? s_warp[lane] : SS<TO, SEG>{(TO)0, 0};
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            SS<TO, SEG> y = shfl_up_ss<TO, SEG>(v, d);
+            if (lane >= d) v = sop<TO, SEG>(y, v);
+        }
+        if (lane < SCAN_BLOCK / 32) s_warp[lane] = v;   // inclusive over warps
+        if (lane == SCAN_BLOCK / 32 - 1) {
+            // tile aggregate: publish, then look back
+            SS<TO, SEG> agg = v;
+            if (tile == 0) {
+                st.inc[0] = agg.v;
+                st.hinc[0] = agg.h;
+                st_flag(st.flag, 2);
+                s_prefix = SS<TO, SEG>{(TO)0, 0};
+            } else {
+                st.agg[tile] = agg.v;
+                st.hagg[tile] = agg.h;
+                st_flag(st.flag + tile, 1);
+                SS<TO, SEG> pre{(TO)0, 0};
+                bool have = false;
+                for (int64_t p = tile - 1; p >= 0; p--) {
+                    int f;
+                    while ((f = ld_flag(st.flag + p)) == 0) {
+                    }
+                    SS<TO, SEG> q;
+                    if (f == 2) {
+                        q.v = st.inc[p];
+                        q.h = st.hinc[p];
+                    } else {
+                        q.v = st.agg[p];
+                        q.h = st.hagg[p];
+                    }
+                    pre = have ? sop<TO, SEG>(q, pre) : q;
+                    have = true;
+                    if (f == 2 || (SEG && q.h)) break;
+                }
+                SS<TO, SEG> inc = sop<TO, SEG>(pre, agg);
+                st.inc[tile] = inc.v;
+                st.hinc[tile] = inc.h;
+                st_flag(st.flag + tile, 2);
+                s_prefix = pre;
+            }
+        }
+    }
+    __syncthreads();
+    // exclusive prefix of this thread = tile prefix (+) warps before (+) lanes before
+    SS<TO, SEG> run = s_prefix;
+    if (wid > 0) run = sop<TO, SEG>(run, s_warp[wid - 1]);
+    SS<TO, SEG> wl = shfl_up_ss<TO, SEG>(w, 1);
+    if (lane > 0) run = sop<TO, SEG>(run, wl);
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; i++) {
+        const int64_t k = base + i;
+        if (SEG && x[i].h) run = SS<TO, SEG>{(TO)0, 1};
+        if (k < n) out[k] = run.v;
+        run = sop<TO, SEG>(run, SS<TO, SEG>{x[i].v, 0});
+    }
+}
+
+template <class TO>
+void scan_launch_status(slm_ctx *ctx, int64_t ntiles, ScanStatus<TO> &st) {
+    // [ticket | flags (ntiles) | hagg | hinc | agg | inc]
+    const size_t ib = (size_t)(3 * ntiles + 4) * sizeof(int);
+    const size_t vb = (size_t)(2 * ntiles) * sizeof(TO);
+    ctx->tmp.resize(ib + vb + 16);
+    char *p = (char *)ctx->tmp.p;
+    st.ticket = (unsigned *)p;
+    st.flag = (int *)p + 4;
+    st.hagg = st.flag + ntiles;
+    st.hinc = st.hagg + ntiles;
+    char *q = p + ((ib + 15) & ~(size_t)15);
+    st.agg = (TO *)q;
+    st.inc = st.agg + ntiles;
+    CUDA_TRY(cudaMemsetAsync(p, 0, (size_t)(ntiles + 4) * sizeof(int), ctx->stream));
+}
+
+template <class TI, class TO, bool SEG>
+void scan_run(slm_ctx *ctx, const TI *in, TO *out, const uint32_t *keys, int64_t n) {
+    if (n <= 0) return;
+    const int64_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+    ScanStatus<TO> st;
+    scan_launch_status<TO>(ctx, ntiles, st);
+    k_scan<TI, TO, SEG><<<(unsigned)ntiles, SCAN_BLOCK, 0, ctx->stream>>>(in, out, keys, n, st);
+    CUDA_TRY(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------- radix sort
+
+constexpr int RS_BLOCK = 512;
+constexpr int RS_WARPS = RS_BLOCK / 32;
+constexpr int RS_ITEMS = 16;
+constexpr int RS_TILE = RS_BLOCK * RS_ITEMS;
+constexpr int RS_MAXP = 8;
+
+template <class K>
+__global__ void __launch_bounds__(256) k_rs_hist(const K *keys, int64_t n, int begin_bit, int np,
+                                                 unsigned long long *hist) {
+    __shared__ unsigned sh[RS_MAXP][256];
+    for (int i = threadIdx.x; i < RS_MAXP * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const K k = keys[i];
+        for (int p = 0; p < np; p++) {
+            const unsigned d = (unsigned)(k >> (begin_bit + 8 * p)) & 255u;
+            atomicAdd(&sh[p][d], 1u);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < np * 256; i += blockDim.x) {
+        const unsigned v = (&sh[0][0])[i];
+        if (v) atomicAdd(hist + i, (unsigned long long)v);
+    }
+}
+
+// exclusive scan of each pass's 256 digit counts (one CTA per pass)
+__global__ void k_rs_hist_scan(unsigned long long *hist) {
+    __shared__ unsigned long long s[256];
+    unsigned long long *h = hist + blockIdx.x * 256;
+    const int t = threadIdx.x;
+    s[t] = h[t];
+    __syncthreads();
+    for (int d = 1; d < 256; d <<= 1) {
+        unsigned long long v = t >= d ? s[t - d] : 0ull;
+        __syncthreads();
+        s[t] += v;
+        __syncthreads();
+    }
+    h[t] = s[t] - h[t];
+}
+
+constexpr unsigned long long RS_AGG = 1ull << 62, RS_INC = 2ull << 62, RS_VAL = RS_AGG - 1;
+
+__device__ __forceinline__ unsigned long long ld_status(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_status(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+template <class K, class V>
+__global__ void __launch_bounds__(RS_BLOCK) k_rs_onesweep(const K *kin, K *kout, const V *vin,
+                                                          V *vout, int64_t n, int shift,
+                                                          const unsigned long long *dbase,
+                                                          unsigned long long *status,
+                                                          unsigned *ticket) {
+    extern __shared__ __align__(16) unsigned char rs_smem[];
+    unsigned *wcnt = (unsigned *)rs_smem;                                   // [WARPS][256]
+    unsigned long long *dest = (unsigned long long *)(wcnt + RS_WARPS * 256);   // [256]
+    unsigned *tstart = (unsigned *)(dest + 256);                            // [256]
+    unsigned char *sdig = (unsigned char *)(tstart + 256);                  // [TILE]
+    K *sk = (K *)(sdig + RS_TILE);                                          // [TILE] (keys, then values)
+    __shared__ unsigned s_tile;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int i = lane; i < 256; i += 32) wcnt[wid * 256 + i] = 0;
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t t0 = tile * RS_TILE;
+    const int64_t wb = t0 + (int64_t)wid * 32 * RS_ITEMS;
+    K key[RS_ITEMS];
+    unsigned pos[RS_ITEMS];
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int i = 0; i < RS_ITEMS; i++) {
+        const int64_t idx = wb + i * 32 + lane;
+        const bool ok = idx < n;
+        key[i] = ok ? kin[idx] : (K)0;
+        const unsigned d = (unsigned)(key[i] >> shift) & 255u;
+        const unsigned m = __match_any_sync(0xffffffffu, ok ? d : 256u + lane);
+        unsigned r = 0;
+        if (ok) r = wcnt[wid * 256 + d] + __popc(m & lt);
+        __syncwarp();
+        if (ok && (m & lt) == 0) wcnt[wid * 256 + d] += __popc(m);
+        __syncwarp();
+        pos[i] = ok ? (r | (d << 24)) : 0xffffffffu;   // warp-local rank (< 2^24) | digit
+    }
+    __syncthreads();
+    // per digit: warp offsets, tile count, tile start in digit order
+    unsigned cnt = 0;
+    if (threadIdx.x < 256) {
+        const int d = threadIdx.x;
+        for (int w = 0; w < RS_WARPS; w++) {
+            const unsigned c = wcnt[w * 256 + d];
+            wcnt[w * 256 + d] = cnt;
+            cnt += c;
+        }
+        // publish the tile's count, look back for the global prefix of this digit
+        unsigned long long *mine = status + tile * 256 + d;
+        unsigned long long excl = 0;
+        if (tile == 0) {
+            st_status(mine, RS_INC | cnt);
+        } else {
+            st_status(mine, RS_AGG | cnt);
+            for (int64_t p = tile - 1; p >= 0; p--) {
+                unsigned long long s;
+                while (((s = ld_status(status + p * 256 + d)) >> 62) == 0) {
+                }
+                excl += s & RS_VAL;
+                if ((s >> 62) == 2) break;
+            }
+            st_status(mine, RS_INC | (excl + cnt));
+        }
+        dest[d] = dbase[d] + excl;
+    }
+    // tile start of every digit in digit order: exclusive scan of cnt over 256 threads
+    {
+        __shared__ unsigned s_w[8];
+        unsigned v = cnt;
+        if (threadIdx.x < 256) {
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += y;
+            }
+            if (lane == 31) s_w[wid] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < 256) {
+            unsigned off = 0;
+            for (int w = 0; w < wid; w++) off += s_w[w];
+            tstart[threadIdx.x] = off + v - cnt;
+        }
+    }
+    __syncthreads();
+    // stage keys in digit order
+    const int64_t nt = min((int64_t)RS_TILE, n - t0);
+#pragma unroll
+    for (int i = 0; i < RS_ITEMS; i++) {
+        if (pos[i] == 0xffffffffu) continue;
+        const unsigned d = pos[i] >> 24;
+        const unsigned lp = tstart[d] + wcnt[wid * 256 + d] + (pos[i] & 0xffffffu);
+        pos[i] = lp;
+        sk[lp] = key[i];
+        sdig[lp] = (unsigned char)d;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < nt; j += RS_BLOCK) {
+        const unsigned d = sdig[j];
+        kout[dest[d] + (j - tstart[d])] = sk[j];
+    }
+    if (vin) {
+        __syncthreads();
+        V *sv = (V *)sk;
+#pragma unroll
+        for (int i = 0; i < RS_ITEMS; i++) {
+            const int64_t idx = wb + i * 32 + lane;
+            if (idx < n) sv[pos[i]] = vin[idx];
+        }
+        __syncthreads();
+        for (int j = threadIdx.x; j < nt; j += RS_BLOCK) {
+            const unsigned d = sdig[j];
+            vout[dest[d] + (j - tstart[d])] = sv[j];
+        }
+    }
+}
+
+template <class K, class V>
+size_t rs_smem_bytes() {
+    const size_t kv = sizeof(K) > sizeof(V) ? sizeof(K) : sizeof(V);
+    return RS_WARPS * 256 * 4 + 256 * 8 + 256 * 4 + RS_TILE + RS_TILE * kv;
+}
+
+// stable sort of (kin, vin) by bits [begin_bit, end_bit) into (kout, vout); kalt / valt are
+// n-element scratch; vin == nullptr sorts keys only.  Inputs are left untouched.
+template <class K, class V>
+void radix_sort_impl(slm_ctx *ctx, const K *kin, K *kout, const V *vin, V *vout, K *kalt, V *valt,
+                     int64_t n, int begin_bit, int end_bit) {
+    cudaStream_t s = ctx->stream;
+    if (n <= 0) return;
+    const int np = end_bit > begin_bit ? (end_bit - begin_bit + 7) / 8 : 0;
+    if (np == 0) {
+        if (kout != kin) CUDA_TRY(cudaMemcpyAsync(kout, kin, n * sizeof(K), cudaMemcpyDeviceToDevice, s));
+        if (vin && vout != vin)
+            CUDA_TRY(cudaMemcpyAsync(vout, vin, n * sizeof(V), cudaMemcpyDeviceToDevice, s));
+        return;
+    }
+    const int64_t ntiles = (n + RS_TILE - 1) / RS_TILE;
+    // scratch: [hist np*256 u64 | tickets np u32 (padded) | status ntiles*256 u64]
+    const size_t hb = (size_t)np * 256 * 8, tb = 64, sb = (size_t)ntiles * 256 * 8;
+    ctx->tmp.resize(hb + tb + sb);
+    unsigned long long *hist = (unsigned long long *)ctx->tmp.p;
+    unsigned *tickets = (unsigned *)((char *)ctx->tmp.p + hb);
+    unsigned long long *status = (unsigned long long *)((char *)ctx->tmp.p + hb + tb);
+    CUDA_TRY(cudaMemsetAsync(ctx->tmp.p, 0, hb + tb, s));
+    k_rs_hist<K><<<grid_for(n, 256, SMS() * 8), 256, 0, s>>>(kin, n, begin_bit, np, hist);
+    k_rs_hist_scan<<<np, 256, 0, s>>>(hist);
+    const size_t smem = rs_smem_bytes<K, V>();
+    CUDA_TRY(cudaFuncSetAttribute(k_rs_onesweep<K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    // ping-pong so that the last pass lands in kout / vout
+    const K *ks = kin;
+    const V *vs = vin;
+    for (int p = 0; p < np; p++) {
+        const bool to_out = ((np - 1 - p) % 2) == 0;
+        K *kd = to_out ? kout : kalt;
+        V *vd = vin ? (to_out ? vout : valt) : nullptr;
+        CUDA_TRY(cudaMemsetAsync(status, 0, sb, s));
+        k_rs_onesweep<K, V><<<(unsigned)ntiles, RS_BLOCK, smem, s>>>(
+            ks, kd, vs, vd, n, begin_bit + 8 * p, hist + p * 256, status, tickets + p);
+        ks = kd;
+        vs = vd;
+    }
+    CUDA_TRY(cudaGetLastError());
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ internal API
+
+template <class TI, class TO>
+void dev_exclusive_sum(slm_ctx *ctx, const TI *in, TO *out, int64_t n) {
+    scan_run<TI, TO, false>(ctx, in, out, nullptr, n);
+}
+template void dev_exclusive_sum<int64_t, int64_t>(slm_ctx *, const int64_t *, int64_t *, int64_t);
+template void dev_exclusive_sum<int32_t, int32_t>(slm_ctx *, const int32_t *, int32_t *, int64_t);
+template void dev_exclusive_sum<int32_t, int64_t>(slm_ctx *, const int32_t *, int64_t *, int64_t);
+template void dev_exclusive_sum<double, double>(slm_ctx *, const double *, double *, int64_t);
+
+void dev_exclusive_sum_by_key(slm_ctx *ctx, const uint32_t *keys, const int32_t *in, int32_t *out,
+                              int64_t n) {
+    scan_run<int32_t, int32_t, true>(ctx, in, out, keys, n);
+}
+
+void sort_pairs_u64_f64(slm_ctx *ctx, DBuf<uint64_t> &keys, DBuf<double> &vals, int64_t n,
+                        int end_bit) {
+    // ping-pong through the context's sort buffers, ending in the second pair, which is then
+    // swapped in (no copy); the caller's old buffers become the context's scratch
+    ctx->u64b.resize(n);
+    ctx->f64b.resize(n);
+    ctx->sort_k64.resize(n);
+    ctx->sort_v64.resize(n);
+    radix_sort_impl<uint64_t, double>(ctx, keys.p, ctx->u64b.p, vals.p, ctx->f64b.p,
+                                      ctx->sort_k64.p, ctx->sort_v64.p, n, 0, end_bit);
+    keys.swap(ctx->u64b);
+    vals.swap(ctx->f64b);
+    keys.n = n;
+    vals.n = n;
+}
+
+void sort_pairs_u32_i32(slm_ctx *ctx, uint32_t *keys_in, uint32_t *keys_out, int32_t *vals_in,
+                        int32_t *vals_out, int64_t n, int end_bit) {
+    ctx->sort_k32.resize(n);
+    ctx->sort_v32.resize(n);
+    radix_sort_impl<uint32_t, int32_t>(ctx, keys_in, keys_out, vals_in, vals_out, ctx->sort_k32.p,
+                                       ctx->sort_v32.p, n, 0, end_bit);
+}
+
+// diagnostics hooks (slm_capi.cu slm_debug_sort / slm_debug_scan)
+double debug_sort(slm_ctx *ctx, int kind, void *keys, void *vals, int64_t n, int end_bit) {
+    cudaStream_t s = ctx->stream;
+    const size_t kb = kind == 0 ? 8 : 4;
+    DBuf<uint8_t> k, v, k2, v2;
+    k.resize(n * kb);
+    v.resize(n * kb);
+    k2.resize(n * kb);
+    v2.resize(n * kb);
+    CUDA_TRY(cudaMemcpyAsync(k.p, keys, n * kb, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(v.p, vals, n * kb, cudaMemcpyHostToDevice, s));
+    cudaEvent_t e0, e1;
+    CUDA_TRY(cudaEventCreate(&e0));
+    CUDA_TRY(cudaEventCreate(&e1));
+    CUDA_TRY(cudaEventRecord(e0, s));
+    if (kind == 0) {
+        ctx->sort_k64.resize(n);
+        ctx->sort_v64.resize(n);
+        radix_sort_impl<uint64_t, double>(ctx, (uint64_t *)k.p, (uint64_t *)k2.p, (double *)v.p,
+                                          (double *)v2.p, ctx->sort_k64.p, ctx->sort_v64.p, n, 0,
+                                          end_bit);
+    } else {
+        sort_pairs_u32_i32(ctx, (uint32_t *)k.p, (uint32_t *)k2.p, (int32_t *)v.p, (int32_t *)v2.p,
+                           n, end_bit);
+    }
+    CUDA_TRY(cudaEventRecord(e1, s));
+    CUDA_TRY(cudaMemcpyAsync(keys, k2.p, n * kb, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(vals, v2.p, n * kb, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return ms;
+}
+
+void debug_scan(slm_ctx *ctx, int kind, const void *in, void *out, const uint32_t *keys, int64_t n) {
+    cudaStream_t s = ctx->stream;
+    const size_t ib = (kind == 1 || kind == 2 || kind == 4) ? 4 : 8;
+    const size_t ob = (kind == 1 || kind == 4) ? 4 : 8;
+    DBuf<uint8_t> di, dout, dk;
+    di.resize(n * ib);
+    dout.resize(n * ob);
+    CUDA_TRY(cudaMemcpyAsync(di.p, in, n * ib, cudaMemcpyHostToDevice, s));
+    if (kind == 4) {
+        dk.resize(n * 4);
+        CUDA_TRY(cudaMemcpyAsync(dk.p, keys, n * 4, cudaMemcpyHostToDevice, s));
+    }
+    switch (kind) {
+    case 0: dev_exclusive_sum<int64_t, int64_t>(ctx, (int64_t *)di.p, (int64_t *)dout.p, n); break;
+    case 1: dev_exclusive_sum<int32_t, int32_t>(ctx, (int32_t *)di.p, (int32_t *)dout.p, n); break;
+    case 2: dev_exclusive_sum<int32_t, int64_t>(ctx, (int32_t *)di.p, (int64_t *)dout.p, n); break;
+    case 3: dev_exclusive_sum<double, double>(ctx, (double *)di.p, (double *)dout.p, n); break;
+    default:
+        dev_exclusive_sum_by_key(ctx, (uint32_t *)dk.p, (int32_t *)di.p, (int32_t *)dout.p, n);
+    }
+    CUDA_TRY(cudaMemcpyAsync(out, dout.p, n * ob, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+}
+
+const void *slm_anchor_prim() { return (const void *)k_rs_hist_scan; }

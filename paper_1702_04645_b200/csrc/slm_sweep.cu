@@ -1726,12 +1726,12 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, const int
         if (no_smem) {
             CUDA_TRY(cudaMemsetAsync(Hb.route, 0, nh, s));
         } else {
-            k_sweep_hub_smem<SYM><<<148, HS_BLOCK, SMHS, s>>>(A, Hb, ctx->hub_ovf.p + 2 * nh + 2);
+            k_sweep_hub_smem<SYM><<<(unsigned)SMS(), HS_BLOCK, SMHS, s>>>(A, Hb, ctx->hub_ovf.p + 2 * nh + 2);
         }
         static const bool two_kernels = getenv("SLM_HUB_MODE") && atoi(getenv("SLM_HUB_MODE")) == 1;
         if (two_kernels) {
-            khm<<<(unsigned)std::min<int64_t>(G.hub_nseg, 148LL * 2), HUB_BLOCK, SMH, s>>>(A, Hb);
-            khs<<<(unsigned)std::min<int64_t>(nh, 148LL * 4), HUB_BLOCK, 0, s>>>(A, Hb);
+            khm<<<(unsigned)std::min<int64_t>(G.hub_nseg, SMS() * 2), HUB_BLOCK, SMH, s>>>(A, Hb);
+            khs<<<(unsigned)std::min<int64_t>(nh, SMS() * 4), HUB_BLOCK, 0, s>>>(A, Hb);
         } else {
             // the largest rows by segment (merge + select kernels over their prefix of the
             // work list), the rest one CTA per row
@@ -1740,19 +1740,19 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, const int
                 HubArgs Hbig = Hb;
                 Hbig.nitems = G.hub_big_items;
                 Hbig.nrows = nbig;
-                khm<<<(unsigned)std::min<int64_t>(Hbig.nitems, 148LL * 2), HUB_BLOCK, SMH, s>>>(A, Hbig);
-                khs<<<(unsigned)std::min<int64_t>(nbig, 148LL * 4), HUB_BLOCK, 0, s>>>(A, Hbig);
+                khm<<<(unsigned)std::min<int64_t>(Hbig.nitems, SMS() * 2), HUB_BLOCK, SMH, s>>>(A, Hbig);
+                khs<<<(unsigned)std::min<int64_t>(nbig, SMS() * 4), HUB_BLOCK, 0, s>>>(A, Hbig);
             }
             if (nh > nbig) {
                 uint32_t *next = ctx->hub_ovf.p + 2 * nh + 1;   // row counter, starts at nbig
                 const uint32_t start = (uint32_t)nbig;
                 CUDA_TRY(cudaMemcpyAsync(next, &start, 4, cudaMemcpyHostToDevice, s));
                 // (pageable source: the copy completes before the call returns)
-                k_sweep_hub_row<SYM><<<(unsigned)std::min<int64_t>(nh - nbig, 148LL * 2), HUB_BLOCK,
+                k_sweep_hub_row<SYM><<<(unsigned)std::min<int64_t>(nh - nbig, SMS() * 2), HUB_BLOCK,
                                        SMH, s>>>(A, Hb, next);
             }
         }
-        k_sweep_hub_fallback<SYM><<<148, HUB_BLOCK, 0, s>>>(A, Hb);
+        k_sweep_hub_fallback<SYM><<<(unsigned)SMS(), HUB_BLOCK, 0, s>>>(A, Hb);
     }
     }
     if (hub_side) CUDA_TRY(cudaEventRecord(ctx->ev_join, ctx->stream2));
@@ -1762,7 +1762,7 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, const int
         if (nt)
             k_sweep_tiny<SYM, TINY_MAX><<<grid_for(nt, 256), 256, 0, s>>>(A, rows(0), nt);
         if (ns) {
-            const int64_t warps = 148LL * 64;
+            const int64_t warps = SMS() * 64;
             int64_t rpw = std::max<int64_t>(64, (ns + warps - 1) / warps);
             int64_t nw = (ns + rpw - 1) / rpw;
             k_sweep_small<SYM><<<grid_for(nw * 32, 256), 256, 0, s>>>(A, rows(0) + nt, ns, rpw);
@@ -1773,9 +1773,9 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, const int
         static const bool no_half = getenv("SLM_HALF") && atoi(getenv("SLM_HALF")) == 0;
         const int64_t nh1 = no_half ? 0 : G.bin1_half, nf1 = nb(1) - nh1;
         if (nf1)
-            k1<<<grid_for(nf1 * 32, W1 * 32, 148LL * 4), W1 * 32, SM1, s>>>(A, rows(1), nf1);
+            k1<<<grid_for(nf1 * 32, W1 * 32, SMS() * 4), W1 * 32, SM1, s>>>(A, rows(1), nf1);
         if (nh1)
-            k_sweep_half<256, W1, SYM><<<grid_for(nh1 * 16, W1 * 32, 148LL * 4), W1 * 32, SM1, s>>>(
+            k_sweep_half<256, W1, SYM><<<grid_for(nh1 * 16, W1 * 32, SMS() * 4), W1 * 32, SM1, s>>>(
                 A, rows(1) + nf1, nh1);
     }
     if (bin_mask & 28) {
@@ -1791,11 +1791,11 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, const int
     int32_t *ovf = ctx->ovf_rows.p;
     uint32_t *novf = ctx->ovf_cnt.p;
     if (nb(2) && (bin_mask & 4))
-        k2<<<(unsigned)std::min<int64_t>(nb(2), 148 * 8), 128, SM2, s>>>(A, rows(2), nb(2), ovf, novf);
+        k2<<<(unsigned)std::min<int64_t>(nb(2), SMS() * 8), 128, SM2, s>>>(A, rows(2), nb(2), ovf, novf);
     if (nb(3) && (bin_mask & 8))
-        k3<<<(unsigned)std::min<int64_t>(nb(3), 148 * 4), 256, SM3, s>>>(A, rows(3), nb(3), ovf, novf);
+        k3<<<(unsigned)std::min<int64_t>(nb(3), SMS() * 4), 256, SM3, s>>>(A, rows(3), nb(3), ovf, novf);
     if (nb(4) && (bin_mask & 16))
-        k4<<<(unsigned)std::min<int64_t>(nb(4), 148 * 2), 512, SM4, s>>>(A, rows(4), nb(4), ovf, novf);
+        k4<<<(unsigned)std::min<int64_t>(nb(4), SMS() * 2), 512, SM4, s>>>(A, rows(4), nb(4), ovf, novf);
     if (bin_mask & 28) {
         if (ctx->ovf_tab.n < (size_t)OVF_GRID * OVF_H) {
             ctx->ovf_tab.resize((size_t)OVF_GRID * OVF_H);
@@ -1942,10 +1942,10 @@ double sweep_floor_ms(slm_ctx *ctx, const LevelGraph &G, Forest &F, int mode) {
         lab = W.vlabel.p;
         mode -= 3;
     }
-    k_floor<<<148 * 8, 256, 0, ctx->stream>>>(nbr, u32, lab, F.S1f.p, G.ue, mode, o.p);
+    k_floor<<<SMS() * 8, 256, 0, ctx->stream>>>(nbr, u32, lab, F.S1f.p, G.ue, mode, o.p);
     cudaEventRecord(a, ctx->stream);
     for (int it = 0; it < 5; it++)
-        k_floor<<<148 * 8, 256, 0, ctx->stream>>>(nbr, u32, lab, F.S1f.p, G.ue, mode, o.p);
+        k_floor<<<SMS() * 8, 256, 0, ctx->stream>>>(nbr, u32, lab, F.S1f.p, G.ue, mode, o.p);
     cudaEventRecord(b, ctx->stream);
     cudaEventSynchronize(b);
     float ms = 0;

@@ -9,8 +9,8 @@ reference's row-chunk thread pool, detector.py:77-111).
 
 Exact fast-forward: when a MAXIMAL sweep commits nothing, the forest is
 unchanged, so the following POSITIVE call would return its own input (POSITIVE is
-idempotent on its own output) with the same unresolved count; it is skipped and its
-statistics are replayed.  The device likewise reuses the sweep's plan while the forest is
+idempotent on its own output) with the same unresolved count; on integer-weight graphs it
+is skipped and its statistics are replayed.  The device likewise reuses the sweep's plan while the forest is
 unchanged and only redraws the coins.  Partitions, sweep counts and statistics are
 identical to the reference's.
 """
@@ -132,7 +132,9 @@ def run(graph: Graph, config: RunConfig | None = None) -> RunResult:
     levels = []
     level = 0
     while True:
-        n_level = ctx.info()["n"]
+        info = ctx.info()
+        n_level = info["n"]
+        integral = info["integral"]
         if trace is not None:
             stats.trace_level_starts.append(len(trace))
         clock["t"] = time.perf_counter()
@@ -171,9 +173,11 @@ def run(graph: Graph, config: RunConfig | None = None) -> RunResult:
                 _debug_validate(ctx, f"maximal@{level}", stats, False)
             if not improved:
                 break
-            if applied == 0:
+            if applied == 0 and integral:
                 # forest unchanged since the last POSITIVE, which is idempotent on its own
                 # output: the call would change nothing and report the same unresolved count
+                # (integer weights: local_gains' and the split's sums are exact, so their
+                # signs agree; with real weights the call is made as in the reference)
                 stats.unresolved_negative += last_unresolved
                 stats.skipped_positive_calls += 1
                 if config.debug_checks:
