@@ -427,8 +427,11 @@ __global__ void k_scatter_sums(const int64_t *runs, const double *sums, int32_t 
 static void merge_long_runs(slm_ctx *ctx, const double *vals, const uint64_t *keys, int64_t ne,
                             const int64_t *d_runs, int32_t nruns, double *out_w, uint32_t *bad) {
     cudaStream_t s = ctx->stream;
-    static DBuf<int64_t> ends, d_off, d_len;
-    static DBuf<double> leaf, sums;
+    CTX_SCRATCH(DBuf<int64_t>, ends);
+    CTX_SCRATCH(DBuf<int64_t>, d_off);
+    CTX_SCRATCH(DBuf<int64_t>, d_len);
+    CTX_SCRATCH(DBuf<double>, leaf);
+    CTX_SCRATCH(DBuf<double>, sums);
     ends.resize(nruns);
     k_long_ends<<<grid_for(nruns, 128), 128, 0, s>>>(keys, ne, d_runs, nruns, ends.p);
     std::vector<int64_t> hr(2 * nruns), he(nruns);
@@ -487,7 +490,8 @@ void build_level_from_keys(slm_ctx *ctx, LevelGraph &G, int64_t n, DBuf<uint64_t
     if (ne_in > 0) sort_pairs_u64_f64(ctx, keys, vals, ne_in, 2 * b);
     amark("sort");
     // 2. run heads + group ids
-    static DBuf<int64_t> head, gid;   // grow-only scratch kept across builds
+    CTX_SCRATCH(DBuf<int64_t>, head);   // grow-only scratch kept across builds
+    CTX_SCRATCH(DBuf<int64_t>, gid);
     head.resize(ne_in + 1);
     gid.resize(ne_in + 1);
     int64_t ng = 0;
@@ -502,13 +506,13 @@ void build_level_from_keys(slm_ctx *ctx, LevelGraph &G, int64_t n, DBuf<uint64_t
     }
     SLM_REQUIRE(ng < (int64_t(1) << 31), SLM_EUNSUP, "more than 2^31-1 merged edges");
     G.ne = ng;
-    static DBuf<int32_t> src_of;   // grow-only scratch kept across builds
+    CTX_SCRATCH(DBuf<int32_t>, src_of);   // grow-only scratch kept across builds
     src_of.resize(ng);
     G.csr_dst.resize(ng);
     G.csr_w.resize(ng);
     G.csr_ptr.resize(n + 1);
     if (ne_in > 0) {
-        static DBuf<int64_t> lr;
+        CTX_SCRATCH(DBuf<int64_t>, lr);
         lr.resize(2 * MAX_LONG + 2);
         int32_t *d_nlong = (int32_t *)(lr.p + 2 * MAX_LONG);
         CUDA_TRY(cudaMemsetAsync(d_nlong, 0, 4, s));
@@ -532,7 +536,9 @@ void build_level_from_keys(slm_ctx *ctx, LevelGraph &G, int64_t n, DBuf<uint64_t
     in_src.resize(ng);
     in_w.resize(ng);
     {
-        static DBuf<int32_t> perm_in, perm_out, kout;   // grow-only scratch kept across builds
+        CTX_SCRATCH(DBuf<int32_t>, perm_in);   // grow-only scratch kept across builds
+        CTX_SCRATCH(DBuf<int32_t>, perm_out);
+        CTX_SCRATCH(DBuf<int32_t>, kout);
         perm_in.resize(ng);
         perm_out.resize(ng);
         kout.resize(ng);
@@ -561,7 +567,8 @@ void build_level_from_keys(slm_ctx *ctx, LevelGraph &G, int64_t n, DBuf<uint64_t
     amark("sym check");
     // 5. union
     if (G.sym) {
-        static DBuf<int64_t> keep, pos;   // grow-only scratch kept across builds
+        CTX_SCRATCH(DBuf<int64_t>, keep);   // grow-only scratch kept across builds
+        CTX_SCRATCH(DBuf<int64_t>, pos);
         keep.resize(ng + 1);
         pos.resize(ng + 1);
         CUDA_TRY(cudaMemsetAsync(keep.p, 0, (ng + 1) * 8, s));
@@ -578,7 +585,7 @@ void build_level_from_keys(slm_ctx *ctx, LevelGraph &G, int64_t n, DBuf<uint64_t
                                                               G.csr_w.p, pos.p, n, ng, ue,
                                                               G.uptr.p, G.unbr.p, G.uu.p);
     } else {
-        static DBuf<int64_t> cnt;   // grow-only scratch kept across builds
+        CTX_SCRATCH(DBuf<int64_t>, cnt);   // grow-only scratch kept across builds
         cnt.resize(n + 1);
         CUDA_TRY(cudaMemsetAsync(cnt.p + n, 0, 8, s));
         k_union_merge<<<grid_for(n, 128), 128, 0, s>>>(G.csr_ptr.p, G.csr_dst.p, G.csr_w.p,

@@ -428,6 +428,7 @@ void slm_destroy(slm_ctx *ctx) {
         SlmStreamScope scope(ctx);
         ctx->g.reset();
         ctx->g0.reset();
+        ctx->scratch.clear();
     }
     cudaStreamSynchronize(ctx->stream2);
     cudaStreamDestroy(ctx->stream);

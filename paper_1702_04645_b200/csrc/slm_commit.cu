@@ -1532,7 +1532,7 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
                 uint64_t seed, double accept_prob, int64_t level, int64_t sweep, int *improved,
                 int64_t *applied, std::vector<double> *gains, uint32_t *wown) {
     cudaStream_t s = ctx->stream;
-    static CommitScratch CS;
+    CTX_SCRATCH(CommitScratch, CS);
     const int64_t n = G.n, nc = F.n_comms;
     *improved = 0;
     *applied = 0;
@@ -1774,7 +1774,7 @@ void run_commit(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, const in
         int32_t rem = NA;
         std::vector<double> rt;
         const bool wprof = ctx->prof && getenv("SLM_PROFILE_WALK");
-        static DBuf<unsigned long long> wst;
+        CTX_SCRATCH(DBuf<unsigned long long>, wst);
         V.wst = nullptr;
         std::vector<std::string> rinfo;
         if (wprof) {
@@ -1937,7 +1937,9 @@ void commit_wown_deltas(slm_ctx *ctx, const LevelGraph &G, const int32_t *pre, c
                         uint32_t *wown) {
     cudaStream_t s = ctx->stream;
     const int64_t n = G.n;
-    static DBuf<int32_t> f, pos, list;   // grow-only scratch kept across calls
+    CTX_SCRATCH(DBuf<int32_t>, f);   // grow-only scratch kept across calls
+    CTX_SCRATCH(DBuf<int32_t>, pos);
+    CTX_SCRATCH(DBuf<int32_t>, list);
     f.resize(n + 1);
     pos.resize(n + 1);
     CUDA_TRY(cudaMemsetAsync(f.p + n, 0, 4, s));

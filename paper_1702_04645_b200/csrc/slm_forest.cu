@@ -325,7 +325,7 @@ void run_components(slm_ctx *ctx, Forest &F, int64_t n) {
         F.n_comms = 0;
         return;
     }
-    static DBuf<uint8_t> c2;   // grow-only scratch kept across calls
+    CTX_SCRATCH(DBuf<uint8_t>, c2);   // grow-only scratch kept across calls
     c2.resize(n);
     int32_t *root = ctx->i32a.resize(n);
     int32_t *key = ctx->i32b.resize(n);
@@ -374,7 +374,9 @@ void run_components(slm_ctx *ctx, Forest &F, int64_t n) {
         }
         CUDA_TRY(cudaMemsetAsync(F.on_cycle.p, 0, n, s));
         k_mark_cycle<<<G, 256, 0, s>>>(f, n, F.on_cycle.p);
-        static DBuf<int32_t> hop, hop2, mv2;   // grow-only scratch kept across calls
+        CTX_SCRATCH(DBuf<int32_t>, hop);   // grow-only scratch kept across calls
+        CTX_SCRATCH(DBuf<int32_t>, hop2);
+        CTX_SCRATCH(DBuf<int32_t>, mv2);
         hop.resize(n);
         hop2.resize(n);
         mv2.resize(n);
@@ -393,7 +395,8 @@ void run_components(slm_ctx *ctx, Forest &F, int64_t n) {
     int32_t *first = ctx->i32c.resize(n);
     k_fill_i32<<<G, 256, 0, s>>>(first, n, 0x7fffffff);
     k_first_occ<<<G, 256, 0, s>>>(key, n, first);
-    static DBuf<int32_t> h, lab;   // grow-only scratch kept across calls
+    CTX_SCRATCH(DBuf<int32_t>, h);   // grow-only scratch kept across calls
+    CTX_SCRATCH(DBuf<int32_t>, lab);
     h.resize(n + 1);
     lab.resize(n + 1);
     CUDA_TRY(cudaMemsetAsync(h.p + n, 0, 4, s));
@@ -466,8 +469,9 @@ void build_layout(slm_ctx *ctx, Forest &F) {
     // depth of every node below its community root (parent = a[x])
     int32_t *flags = ctx->i32d.resize(2);
     CUDA_TRY(cudaMemsetAsync(flags, 0, 8, s));
-    static DBuf<uint32_t> depth, depth_sorted;   // grow-only scratch kept across calls
-    static DBuf<int32_t> by_depth;   // grow-only scratch kept across calls
+    CTX_SCRATCH(DBuf<uint32_t>, depth);   // grow-only scratch kept across calls
+    CTX_SCRATCH(DBuf<uint32_t>, depth_sorted);
+    CTX_SCRATCH(DBuf<int32_t>, by_depth);   // grow-only scratch kept across calls
     depth.resize(n);
     depth_sorted.resize(n);
     by_depth.resize(n);
@@ -484,7 +488,7 @@ void build_layout(slm_ctx *ctx, Forest &F) {
         // pathological depth (> 4096): sequential DFS per community (needs the kids pointers)
         k_lb_ptr32<<<grid_for(n + 1, 256), 256, 0, s>>>((const int32_t *)ks, n, n, F.kptr.p);
         int32_t *stk_node = ctx->i32a.resize(n);
-        static DBuf<int32_t> stk_it;   // grow-only scratch kept across calls
+        CTX_SCRATCH(DBuf<int32_t>, stk_it);   // grow-only scratch kept across calls
         stk_it.resize(n);
         k_dfs_layout<<<grid_for(nc, 64), 64, 0, s>>>(F.cptr.p, F.members.p, F.on_cycle.p, F.kptr.p,
                                                      F.kids.p, nc, F.order.p, F.pos.p, F.sz.p,
@@ -498,7 +502,7 @@ void build_layout(slm_ctx *ctx, Forest &F) {
         sort_pairs_u32_i32(ctx, depth.p, depth_sorted.p, iota2, by_depth.p, n, bits_for(maxd + 2));
     std::vector<int64_t> lvl(maxd + 2, 0);
     {
-        static DBuf<int32_t> lb;   // grow-only scratch kept across calls
+        CTX_SCRATCH(DBuf<int32_t>, lb);   // grow-only scratch kept across calls
         lb.resize(maxd + 2);
         k_run_starts<<<grid_for(n, 256), 256, 0, s>>>((const int32_t *)depth_sorted.p, n, maxd + 1, lb.p);
         std::vector<int32_t> h(maxd + 2);
@@ -513,7 +517,9 @@ void build_layout(slm_ctx *ctx, Forest &F) {
             k_size_level<<<grid_for(hi - lo, 256), 256, 0, s>>>(by_depth.p, lo, hi, F.a.p, F.sz.p);
     }
     // offsets among siblings (kids ascending, the root never a kid) and pre-order positions
-    static DBuf<int32_t> val, ex, offp;   // grow-only scratch kept across calls
+    CTX_SCRATCH(DBuf<int32_t>, val);   // grow-only scratch kept across calls
+    CTX_SCRATCH(DBuf<int32_t>, ex);
+    CTX_SCRATCH(DBuf<int32_t>, offp);
     val.resize(nk);
     ex.resize(nk);
     offp.resize(n);

@@ -10,6 +10,8 @@
 #include <cstdio>
 #include <string>
 #include <vector>
+#include <unordered_map>
+#include <memory>
 #include <memory>
 
 #define SLM_OK 0
@@ -249,7 +251,22 @@ struct slm_ctx {
     double *h_f64 = nullptr;
     // counters of the last phase calls
     int64_t last_rounds = 0, last_candidates = 0, last_accepted = 0;
+    // per-context grow-only scratch of the phase functions (CTX_SCRATCH below)
+    std::unordered_map<const void *, std::shared_ptr<void>> scratch;
 };
+
+// Grow-only scratch kept across calls, owned by the context (released with it): the
+// phase functions' scratch is per context, so several contexts (threads, devices) never
+// share device buffers.
+template <class T>
+T &ctx_scratch(slm_ctx *ctx, const void *tag) {
+    std::shared_ptr<void> &p = ctx->scratch[tag];
+    if (!p) p = std::shared_ptr<void>(new T(), [](void *q) { delete static_cast<T *>(q); });
+    return *static_cast<T *>(p.get());
+}
+#define CTX_SCRATCH(T, name)                                                               \
+    static const char name##_tag_ = 0;                                                     \
+    T &name = ctx_scratch<T>(ctx, &name##_tag_)
 
 // ------------------------------------------------------------------------- helpers
 

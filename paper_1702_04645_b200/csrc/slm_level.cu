@@ -27,8 +27,8 @@ __global__ void k_coarse_keys(const int64_t *ptr, const int32_t *dst, const doub
 
 void run_aggregate(slm_ctx *ctx, const LevelGraph &G, const int32_t *d_labels, int64_t n_comms,
                    LevelGraph &out) {
-    static DBuf<uint64_t> keys;   // grow-only scratch kept across levels
-    static DBuf<double> vals;
+    CTX_SCRATCH(DBuf<uint64_t>, keys);   // grow-only scratch kept across levels
+    CTX_SCRATCH(DBuf<double>, vals);
     keys.resize(G.ne);
     vals.resize(G.ne);
     if (G.ne > 0)

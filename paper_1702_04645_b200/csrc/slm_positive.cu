@@ -742,7 +742,6 @@ __global__ void k_gb_subsums(GiantArgs A, const GSlice *S, int ns, int64_t N, co
     }
 }
 
-static DBuf<uint32_t> g_stamp;   // monotone part stamps (never reset)
 
 // ------------------------------------------------ giant parts: one CTA per part
 
@@ -1509,7 +1508,7 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     };
     read_small_part();
     phase_mark(ctx, -1);
-    static DBuf<uint8_t> bad;   // grow-only scratch kept across calls
+    CTX_SCRATCH(DBuf<uint8_t>, bad);   // grow-only scratch kept across calls
     bad.resize(nc);
     CUDA_TRY(cudaMemsetAsync(bad.p, 0, nc, s));
     static const bool no_wown = getenv("SLM_WOWN") && atoi(getenv("SLM_WOWN")) == 0;
@@ -1519,7 +1518,9 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     }
     else
         run_local_gains(ctx, G, F, m, nullptr, bad.p);
-    static DBuf<int32_t> f, pos, list;
+    CTX_SCRATCH(DBuf<int32_t>, f);
+    CTX_SCRATCH(DBuf<int32_t>, pos);
+    CTX_SCRATCH(DBuf<int32_t>, list);
     f.resize(nc + 1);
     pos.resize(nc + 1);
     CUDA_TRY(cudaMemsetAsync(f.p + nc, 0, 4, s));
@@ -1538,7 +1539,7 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     std::vector<int2> hrng(nbad);
     std::vector<uint8_t> hheavy(nbad, 0);
     {
-        static DBuf<int2> drng;
+        CTX_SCRATCH(DBuf<int2>, drng);
         drng.resize(nbad);
         k_bad_ranges<<<grid_for(nbad, 256), 256, 0, s>>>(list.p, nbad, F.cptr.p, drng.p);
         CUDA_TRY(cudaMemcpyAsync(hrng.data(), drng.p, nbad * 8, cudaMemcpyDeviceToHost, s));
@@ -1560,7 +1561,8 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
             CUDA_TRY(cudaStreamSynchronize(s));
         }
         if (G.heavy_n) {
-            static DBuf<uint8_t> hc, hb;
+            CTX_SCRATCH(DBuf<uint8_t>, hc);
+            CTX_SCRATCH(DBuf<uint8_t>, hb);
             hc.resize(nc);
             hb.resize(nbad);
             CUDA_TRY(cudaMemsetAsync(hc.p, 0, nc, s));
@@ -1571,6 +1573,7 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
         }
     }
     CUDA_TRY(cudaMemcpyAsync(hbad.data(), list.p, nbad * 4, cudaMemcpyDeviceToHost, s));
+    CTX_SCRATCH(DBuf<uint32_t>, g_stamp);   // monotone part stamps (never reset)
     if (g_stamp.p == nullptr) {
         g_stamp.resize(1);
         CUDA_TRY(cudaMemsetAsync(g_stamp.p, 0, 4, s));
@@ -1578,7 +1581,7 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     CUDA_TRY(cudaStreamSynchronize(s));
     // n-sized scratch, kept across calls (grow-only; pmark holds monotone stamps, so it is
     // cleared only when reallocated)
-    static PosScratch SC;
+    CTX_SCRATCH(PosScratch, SC);
     DBuf<int32_t> &pbuf = SC.pbuf, &pbuf2 = SC.pbuf2, &tbuf = SC.tbuf, &pmark = SC.pmark,
                   &ppos = SC.ppos, &psz = SC.psz, &gmark = SC.gmark, &flags = SC.flags;
     DBuf<int2> &sstk = SC.sstk, &sstk2 = SC.sstk2;
@@ -1754,7 +1757,7 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
         O.unresolved = unres_d.p;
         O.flags = flags.p;
         O.small_part = SMALL_PART;
-        static DBuf<unsigned long long> gprof;
+        CTX_SCRATCH(DBuf<unsigned long long>, gprof);
         O.prof = nullptr;
         if (plog) {
             gprof.resize(8 + 8 * 4096);

@@ -1639,7 +1639,7 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, const int
     A.cstar = d_cstar;
     A.wown = d_wown;
     A.groups = d_groups;
-    static DBuf<unsigned long long> stats;
+    CTX_SCRATCH(DBuf<unsigned long long>, stats);
     A.stats = nullptr;
     const bool want_stats = getenv("SLM_SWEEP_STATS") != nullptr;
     if (want_stats) {
