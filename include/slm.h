@@ -121,6 +121,32 @@ SLM_API int slm_get_cstar(slm_ctx *ctx, int64_t *cstar_out);
  * (1), + community-strength gathers (2) -- the memory-system floor of the sweep; modes 3-5:
  * the same over the degree-ordered sweep view. */
 SLM_API int slm_debug_sweep_floor(slm_ctx *ctx, int32_t mode, double *ms);
+/* ---- the rest of the reference's hot-path API (slm_surface.cu) ------------------- */
+/* CommunityAggregates.from_labels (quality.py:71-79) over caller strengths: S_out / S_in
+ * by sequential per-community sums in node order (np.bincount), member counts. */
+SLM_API int slm_community_sums(slm_ctx *ctx, int64_t n, const int64_t *labels, int64_t n_comms,
+                               const double *s_out, const double *s_in, double *S_out,
+                               double *S_in, int64_t *count);
+/* gain_switch (quality.py:186-219) on the current level graph: exact score change of
+ * relabeling nodes[0..k) from frm to to (to < 0: a fresh empty community); agg4 =
+ * {S_out[frm], S_in[frm], S_out[to], S_in[to]} of the caller's aggregates; m = st.m_w. */
+SLM_API int slm_gain_switch(slm_ctx *ctx, const int64_t *labels, const int64_t *nodes, int64_t k,
+                            int64_t frm, int64_t to, const double *agg4, double m, double *gain);
+/* reverse_assignment (forest.py:70-80): ptr_out[n+1], kids_out[n] (children j != i with
+ * a[j] == i, ascending), *n_kids = ptr_out[n]. */
+SLM_API int slm_reverse_assignment(slm_ctx *ctx, int64_t n, const int64_t *a, int64_t *ptr_out,
+                                   int64_t *kids_out, int64_t *n_kids);
+/* NeighborUnion.w_out / w_in (graph.py:46-60, 151-175) of the current level: W(i, j) and
+ * W(j, i) per union entry (w_out + w_in == the stored u bit for bit). */
+SLM_API int slm_get_union_split(slm_ctx *ctx, double *w_out, double *w_in);
+/* canonicalize_labels (graph.py:283-291): dense labels ordered by first occurrence. */
+SLM_API int slm_canonicalize_labels(slm_ctx *ctx, int64_t n, const int64_t *labels, int64_t *out,
+                                    int64_t *n_comms);
+/* aggregate(graph, labels) (graph.py:266-280) of src's current level graph, built on the
+ * device as level 0 of ctx (same device; labels dense 0..n_comms-1). */
+SLM_API int slm_build_aggregate(slm_ctx *ctx, slm_ctx *src, const int64_t *labels,
+                                int64_t n_comms);
+
 /* Diagnostics of the device primitives (slm_prim.cu), on host arrays, in place:
  * slm_debug_sort: stable LSD radix sort by bits [0, end_bit) of (kind 0) uint64 keys with
  * double values or (kind 1) uint32 keys with int32 values; *ms = device time of the sort.

@@ -69,6 +69,12 @@ SIGNATURES = {
     "slm_plan_groups": (C.c_int, [_VP, _PI64, _VP, _VP]),
     "slm_get_cstar": (C.c_int, [_VP, _VP]),
     "slm_debug_sweep_floor": (C.c_int, [_VP, C.c_int32, _PD]),
+    "slm_community_sums": (C.c_int, [_VP, _I64, _VP, _I64, _VP, _VP, _VP, _VP, _VP]),
+    "slm_gain_switch": (C.c_int, [_VP, _VP, _VP, _I64, _I64, _I64, _VP, C.c_double, _PD]),
+    "slm_reverse_assignment": (C.c_int, [_VP, _I64, _VP, _VP, _VP, _PI64]),
+    "slm_get_union_split": (C.c_int, [_VP, _VP, _VP]),
+    "slm_canonicalize_labels": (C.c_int, [_VP, _I64, _VP, _VP, _PI64]),
+    "slm_build_aggregate": (C.c_int, [_VP, _VP, _VP, _I64]),
     "slm_debug_sort": (C.c_int, [_VP, C.c_int32, _VP, _VP, _I64, C.c_int32, _PD]),
     "slm_debug_scan": (C.c_int, [_VP, C.c_int32, _VP, _VP, _VP, _I64]),
     "slm_build_rmat": (C.c_int, [_VP, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
@@ -88,6 +94,8 @@ def load():
                                "`python -m paper_1702_04645_b200._build`")
         L = C.CDLL(LIB_PATH)
         for name, (res, args) in SIGNATURES.items():
+            if os.environ.get("SLM_LIB_PATH") and not hasattr(L, name):
+                continue   # A/B runs against an older build: its missing entries stay unbound
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
@@ -310,6 +318,51 @@ class Context:
         ms = C.c_double()
         self.call("slm_debug_sweep_floor", int(mode), C.byref(ms))
         return ms.value
+
+    # ----- reference API surface (slm_surface.cu)
+    def community_sums(self, labels, n_comms, s_out, s_in):
+        labels, s_out, s_in = i64(labels), f64(s_out), f64(s_in)
+        So = np.empty(n_comms, np.float64)
+        Si = np.empty(n_comms, np.float64)
+        cnt = np.empty(n_comms, np.int64)
+        self.call("slm_community_sums", labels.size, ptr(labels), int(n_comms), ptr(s_out),
+                  ptr(s_in), ptr(So), ptr(Si), ptr(cnt))
+        return So, Si, cnt
+
+    def gain_switch(self, labels, nodes, frm, to, agg4, m):
+        labels, nodes = i64(labels), i64(nodes)
+        a4 = f64(agg4)
+        g = C.c_double()
+        self.call("slm_gain_switch", ptr(labels), ptr(nodes), nodes.size, int(frm),
+                  -1 if to is None else int(to), ptr(a4), float(m), C.byref(g))
+        return g.value
+
+    def reverse_assignment(self, a):
+        a = i64(a)
+        p = np.empty(a.size + 1, np.int64)
+        kids = np.empty(a.size, np.int64)
+        nk = C.c_int64()
+        self.call("slm_reverse_assignment", a.size, ptr(a), ptr(p), ptr(kids), C.byref(nk))
+        return p, kids[:nk.value].copy()
+
+    def union_split(self):
+        ue = self.info()["ue"]
+        wo = np.empty(ue, np.float64)
+        wi = np.empty(ue, np.float64)
+        self.call("slm_get_union_split", ptr(wo), ptr(wi))
+        return wo, wi
+
+    def canonicalize(self, labels):
+        labels = i64(labels)
+        out = np.empty(labels.size, np.int64)
+        nc = C.c_int64()
+        self.call("slm_canonicalize_labels", labels.size, ptr(labels), ptr(out), C.byref(nc))
+        return out, nc.value
+
+    def build_aggregate(self, src: "Context", labels, n_comms):
+        labels = i64(labels)
+        self.call("slm_build_aggregate", src.handle, ptr(labels), int(n_comms))
+        self.level = 0
 
     def debug_sort(self, keys, vals, end_bit):
         """Stable radix sort of (uint64 keys, f64 vals) or (uint32 keys, int32 vals) by bits

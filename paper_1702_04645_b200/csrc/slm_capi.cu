@@ -367,7 +367,7 @@ static void preload_modules() {
     }
     const void *anchors[] = {slm_anchor_build(), slm_anchor_capi(), slm_anchor_commit(),
                              slm_anchor_forest(), slm_anchor_gen(), slm_anchor_level(),
-                             slm_anchor_lgains(), slm_anchor_plan(), slm_anchor_positive(), slm_anchor_prim(),
+                             slm_anchor_lgains(), slm_anchor_plan(), slm_anchor_positive(), slm_anchor_prim(), slm_anchor_surface(),
                              slm_anchor_sweep()};
     for (const void *a : anchors) {
         cudaFunction_t f;
@@ -800,6 +800,133 @@ int slm_debug_scan(slm_ctx *ctx, int32_t kind, const void *in, void *out, const 
     SLM_REQUIRE(ctx && in && out && n >= 0 && kind >= 0 && kind <= 4 && (kind != 4 || keys),
                 SLM_EINVAL, "bad scan arguments");
     if (n) debug_scan(ctx, kind, in, out, keys, n);
+    API_END
+}
+
+// ----------------------------------------------------- reference API surface helpers
+
+int slm_community_sums(slm_ctx *ctx, int64_t n, const int64_t *labels, int64_t n_comms,
+                       const double *s_out, const double *s_in, double *S_out, double *S_in,
+                       int64_t *count) {
+    API_BEGIN
+    SLM_REQUIRE(n >= 0 && n_comms >= 0 && n_comms < (int64_t(1) << 31), SLM_EINVAL, "bad sizes");
+    for (int64_t i = 0; i < n; i++)
+        SLM_REQUIRE(labels[i] >= 0 && labels[i] < n_comms, SLM_EINVAL, "label out of range");
+    cudaStream_t s = ctx->stream;
+    DBuf<int32_t> lab, cnt;
+    DBuf<double> so, si, So, Si;
+    lab.resize(n); so.resize(n); si.resize(n);
+    cnt.resize(n_comms); So.resize(n_comms); Si.resize(n_comms);
+    upload_i64_as_i32(ctx, labels, n, lab.p);
+    if (n) {
+        CUDA_TRY(cudaMemcpyAsync(so.p, s_out, n * 8, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(si.p, s_in, n * 8, cudaMemcpyHostToDevice, s));
+    }
+    comm_sums_device(ctx, lab.p, n, n_comms, so.p, si.p, So.p, Si.p, cnt.p);
+    std::vector<int32_t> c(n_comms);
+    if (n_comms) {
+        CUDA_TRY(cudaMemcpyAsync(S_out, So.p, n_comms * 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(S_in, Si.p, n_comms * 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(c.data(), cnt.p, n_comms * 4, cudaMemcpyDeviceToHost, s));
+    }
+    CUDA_TRY(cudaStreamSynchronize(s));
+    for (int64_t k = 0; k < n_comms; k++) count[k] = c[k];
+    API_END
+}
+
+int slm_gain_switch(slm_ctx *ctx, const int64_t *labels, const int64_t *nodes, int64_t k,
+                    int64_t frm, int64_t to, const double *agg4, double m, double *gain) {
+    API_BEGIN
+    require_graph(ctx);
+    const LevelGraph &G = *ctx->g;
+    SLM_REQUIRE(k >= 0, SLM_EINVAL, "negative node count");
+    for (int64_t q = 0; q < k; q++)
+        SLM_REQUIRE(nodes[q] >= 0 && nodes[q] < G.n, SLM_EINVAL, "node out of range");
+    if (to >= 0 && to == frm) {
+        *gain = 0.0;
+    } else {
+        DBuf<int32_t> lab, nd;
+        lab.resize(G.n);
+        nd.resize(k);
+        upload_i64_as_i32(ctx, labels, G.n, lab.p);
+        upload_i64_as_i32(ctx, nodes, k, nd.p);
+        *gain = gain_switch_device(ctx, G, lab.p, nd.p, k, (int32_t)frm, (int32_t)(to < 0 ? -1 : to),
+                                   agg4, m);
+    }
+    API_END
+}
+
+int slm_reverse_assignment(slm_ctx *ctx, int64_t n, const int64_t *a, int64_t *ptr_out,
+                           int64_t *kids_out, int64_t *n_kids) {
+    API_BEGIN
+    SLM_REQUIRE(n >= 0 && n < (int64_t(1) << 31), SLM_EINVAL, "bad size");
+    for (int64_t i = 0; i < n; i++)
+        SLM_REQUIRE(a[i] >= 0 && a[i] < n, SLM_EINVAL, "assignment out of range");
+    DBuf<int32_t> da;
+    da.resize(n);
+    upload_i64_as_i32(ctx, a, n, da.p);
+    reverse_assignment_device(ctx, da.p, n, ptr_out, kids_out, n_kids);
+    API_END
+}
+
+int slm_get_union_split(slm_ctx *ctx, double *w_out, double *w_in) {
+    API_BEGIN
+    require_graph(ctx);
+    const LevelGraph &G = *ctx->g;
+    DBuf<double> wo, wi;
+    wo.resize(G.ue);
+    wi.resize(G.ue);
+    union_split_device(ctx, G, wo.p, wi.p);
+    if (G.ue) {
+        CUDA_TRY(cudaMemcpyAsync(w_out, wo.p, G.ue * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(w_in, wi.p, G.ue * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    API_END
+}
+
+int slm_canonicalize_labels(slm_ctx *ctx, int64_t n, const int64_t *labels, int64_t *out,
+                            int64_t *n_comms) {
+    API_BEGIN
+    SLM_REQUIRE(n >= 0 && n < (int64_t(1) << 31), SLM_EINVAL, "bad size");
+    int64_t lo = 0, hi = -1;
+    for (int64_t i = 0; i < n; i++) {
+        if (i == 0 || labels[i] < lo) lo = labels[i];
+        if (i == 0 || labels[i] > hi) hi = labels[i];
+    }
+    SLM_REQUIRE(n == 0 || (uint64_t)(hi - lo) < (uint64_t(1) << 32) - 1, SLM_EINVAL,
+                "label range exceeds 2^32");
+    std::vector<uint32_t> off(n);
+    for (int64_t i = 0; i < n; i++) off[i] = (uint32_t)(labels[i] - lo);
+    DBuf<uint32_t> dl;
+    DBuf<int32_t> dout;
+    dl.resize(n);
+    dout.resize(n);
+    if (n) CUDA_TRY(cudaMemcpyAsync(dl.p, off.data(), n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    *n_comms = canonicalize_device(ctx, dl.p, n, bits_for(hi - lo + 2), dout.p);
+    download_i32_as_i64(ctx, dout.p, n, out);
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    API_END
+}
+
+int slm_build_aggregate(slm_ctx *ctx, slm_ctx *src, const int64_t *labels, int64_t n_comms) {
+    API_BEGIN
+    SLM_REQUIRE(src && src->g, SLM_ESTATE, "source context has no graph");
+    SLM_REQUIRE(src->device == ctx->device, SLM_EINVAL, "contexts on different devices");
+    const LevelGraph &G = *src->g;
+    SLM_REQUIRE(n_comms >= 0 && n_comms <= G.n, SLM_EINVAL, "bad community count");
+    for (int64_t i = 0; i < G.n; i++)
+        SLM_REQUIRE(labels[i] >= 0 && labels[i] < n_comms, SLM_EINVAL, "label out of range");
+    CUDA_TRY(cudaStreamSynchronize(src->stream));
+    DBuf<int32_t> lab;
+    lab.resize(G.n);
+    upload_i64_as_i32(ctx, labels, G.n, lab.p);
+    auto next = std::make_shared<LevelGraph>();
+    run_aggregate(ctx, G, lab.p, n_comms, *next);
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    new_level0(ctx);
+    ctx->g0 = next;
+    ctx->g = next;
     API_END
 }
 

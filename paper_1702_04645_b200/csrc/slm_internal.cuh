@@ -430,4 +430,18 @@ const void *slm_anchor_lgains();
 const void *slm_anchor_plan();
 const void *slm_anchor_positive();
 const void *slm_anchor_prim();
+const void *slm_anchor_surface();
+
+// slm_surface.cu: the rest of the reference's hot-path API surface
+void comm_sums_device(slm_ctx *ctx, const int32_t *d_lab, int64_t n, int64_t nc,
+                      const double *d_so, const double *d_si, double *d_So, double *d_Si,
+                      int32_t *d_cnt);
+double gain_switch_device(slm_ctx *ctx, const LevelGraph &G, const int32_t *d_lab,
+                          const int32_t *d_nodes, int64_t k, int32_t frm, int32_t to,
+                          const double agg[4], double m);
+void reverse_assignment_device(slm_ctx *ctx, const int32_t *d_a, int64_t n, int64_t *h_ptr,
+                               int64_t *h_kids, int64_t *h_nk);
+void union_split_device(slm_ctx *ctx, const LevelGraph &G, double *d_wo, double *d_wi);
+int64_t canonicalize_device(slm_ctx *ctx, const uint32_t *d_lab, int64_t n, int end_bit,
+                            int32_t *d_out);
 const void *slm_anchor_sweep();

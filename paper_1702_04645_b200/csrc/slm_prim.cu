@@ -23,6 +23,7 @@
 //   - keys (then values) are staged in shared memory in digit order and written out from
 //     there, so every digit's run leaves the CTA as contiguous stores.
 #include "slm_internal.cuh"
+#include <type_traits>
 
 namespace {
 
@@ -68,6 +69,69 @@ struct ScanStatus {
     unsigned *ticket;
 };
 
+// per-thread items, thread/warp/block inclusive scan of a tile (shared by both scan forms)
+template <class TI, class TO, bool SEG>
+struct TileScan {
+    SS<TO, SEG> x[SCAN_ITEMS];
+    SS<TO, SEG> w;   // warp-inclusive scan of the thread totals
+    __device__ __forceinline__ void load(const TI *in, const uint32_t *keys, int64_t n,
+                                         int64_t base) {
+#pragma unroll
+        for (int i = 0; i < SCAN_ITEMS; i++) {
+            const int64_t k = base + i;
+            x[i].v = k < n ? (TO)in[k] : (TO)0;
+            x[i].h = 0;
+            if (SEG && k < n) x[i].h = (k == 0 || keys[k] != keys[k - 1]) ? 1 : 0;
+        }
+    }
+    // returns the tile aggregate (valid in every thread after the call); s_warp gets the
+    // inclusive scan over warps
+    __device__ __forceinline__ SS<TO, SEG> reduce(SS<TO, SEG> *s_warp) {
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        SS<TO, SEG> t = x[0];
+#pragma unroll
+        for (int i = 1; i < SCAN_ITEMS; i++) t = sop<TO, SEG>(t, x[i]);
+        w = t;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            SS<TO, SEG> y = shfl_up_ss<TO, SEG>(w, d);
+            if (lane >= d) w = sop<TO, SEG>(y, w);
+        }
+        if (lane == 31) s_warp[wid] = w;
+        __syncthreads();
+        if (wid == 0) {
+            SS<TO, SEG> v = lane < SCAN_BLOCK / 32 ? s_warp[lane] : SS<TO, SEG>{(TO)0, 0};
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                SS<TO, SEG> y = shfl_up_ss<TO, SEG>(v, d);
+                if (lane >= d) v = sop<TO, SEG>(y, v);
+            }
+            if (lane < SCAN_BLOCK / 32) s_warp[lane] = v;
+        }
+        __syncthreads();
+        return s_warp[SCAN_BLOCK / 32 - 1];
+    }
+    // write the exclusive scan given the tile's exclusive prefix
+    __device__ __forceinline__ void write(TO *out, int64_t n, int64_t base, SS<TO, SEG> prefix,
+                                          const SS<TO, SEG> *s_warp) {
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        SS<TO, SEG> run = prefix;
+        if (wid > 0) run = sop<TO, SEG>(run, s_warp[wid - 1]);
+        SS<TO, SEG> wl = shfl_up_ss<TO, SEG>(w, 1);
+        if (lane > 0) run = sop<TO, SEG>(run, wl);
+#pragma unroll
+        for (int i = 0; i < SCAN_ITEMS; i++) {
+            const int64_t k = base + i;
+            if (SEG && x[i].h) run = SS<TO, SEG>{(TO)0, 1};
+            if (k < n) out[k] = run.v;
+            run = sop<TO, SEG>(run, SS<TO, SEG>{x[i].v, 0});
+        }
+    }
+};
+
+// single pass, integer operands (exact, so the look-back's grouping is immaterial): warp 0
+// looks back 32 predecessor tiles at a time; the nearest one holding an inclusive prefix
+// (or, segmented, a segment start) ends the walk
 template <class TI, class TO, bool SEG>
 __global__ void __launch_bounds__(SCAN_BLOCK) k_scan(const TI *in, TO *out, const uint32_t *keys,
                                                      int64_t n, ScanStatus<TO> st) {
@@ -79,66 +143,52 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan(const TI *in, TO *out, cons
     const int64_t tile = s_tile;
     const int64_t base = tile * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    SS<TO, SEG> x[SCAN_ITEMS];
-#pragma unroll
-    for (int i = 0; i < SCAN_ITEMS; i++) {
-        const int64_t k = base + i;
-        x[i].v = k < n ? (TO)in[k] : (TO)0;
-        x[i].h = 0;
-        if (SEG && k < n) x[i].h = (k == 0 || keys[k] != keys[k - 1]) ? 1 : 0;
-    }
-    // thread inclusive scan
-    SS<TO, SEG> t = x[0];
-#pragma unroll
-    for (int i = 1; i < SCAN_ITEMS; i++) t = sop<TO, SEG>(t, x[i]);
-    // warp inclusive scan of thread totals
-    SS<TO, SEG> w = t;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        SS<TO, SEG> y = shfl_up_ss<TO, SEG>(w, d);
-        if (lane >= d) w = sop<TO, SEG>(y, w);
-    }
-    if (lane == 31) s_warp[wid] = w;
-    __syncthreads();
+    TileScan<TI, TO, SEG> T;
+    T.load(in, keys, n, base);
+    const SS<TO, SEG> agg = T.reduce(s_warp);
     if (wid == 0) {
-        SS<TO, SEG> v = lane < SCAN_BLOCK / 32 ? s_warp[lane] : SS<TO, SEG>{(TO)0, 0};
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            SS<TO, SEG> y = shfl_up_ss<TO, SEG>(v, d);
-            if (lane >= d) v = sop<TO, SEG>(y, v);
-        }
-        if (lane < SCAN_BLOCK / 32) s_warp[lane] = v;   // inclusive over warps
-        if (lane == SCAN_BLOCK / 32 - 1) {
-            // tile aggregate: publish, then look back
-            SS<TO, SEG> agg = v;
-            if (tile == 0) {
+        if (tile == 0) {
+            if (lane == 0) {
                 st.inc[0] = agg.v;
                 st.hinc[0] = agg.h;
                 st_flag(st.flag, 2);
                 s_prefix = SS<TO, SEG>{(TO)0, 0};
-            } else {
+            }
+        } else {
+            if (lane == 0) {
                 st.agg[tile] = agg.v;
                 st.hagg[tile] = agg.h;
                 st_flag(st.flag + tile, 1);
-                SS<TO, SEG> pre{(TO)0, 0};
-                bool have = false;
-                for (int64_t p = tile - 1; p >= 0; p--) {
-                    int f;
-                    while ((f = ld_flag(st.flag + p)) == 0) {
-                    }
-                    SS<TO, SEG> q;
-                    if (f == 2) {
-                        q.v = st.inc[p];
-                        q.h = st.hinc[p];
-                    } else {
-                        q.v = st.agg[p];
-                        q.h = st.hagg[p];
-                    }
-                    pre = have ? sop<TO, SEG>(q, pre) : q;
-                    have = true;
-                    if (f == 2 || (SEG && q.h)) break;
+            }
+            TO pv = 0;
+            int ph = 0;
+            for (int64_t p = tile - 1;; p -= 32) {
+                const int64_t q = p - lane;
+                int f = q >= 0 ? ld_flag(st.flag + q) : 2;
+                while (__any_sync(0xffffffffu, f == 0))
+                    if (f == 0) f = ld_flag(st.flag + q);
+                TO v = 0;
+                int h = 0;
+                if (q >= 0) {
+                    v = f == 2 ? st.inc[q] : st.agg[q];
+                    if (SEG) h = f == 2 ? st.hinc[q] : st.hagg[q];
                 }
-                SS<TO, SEG> inc = sop<TO, SEG>(pre, agg);
+                const unsigned stop = __ballot_sync(0xffffffffu, f == 2 || (SEG && h));
+                const int last = stop ? __ffs(stop) - 1 : 31;   // lanes 0..last contribute
+                TO sum = lane <= last ? v : (TO)0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+                const int hl = __shfl_sync(0xffffffffu, h, last);
+                // earlier window (+) later prefix: a segment start in the later part wins
+                if (!ph) {
+                    pv += sum;
+                    ph = SEG ? hl : 0;
+                }
+                if (stop) break;
+            }
+            if (lane == 0) {
+                const SS<TO, SEG> pre{pv, ph};
+                const SS<TO, SEG> inc = sop<TO, SEG>(pre, agg);
                 st.inc[tile] = inc.v;
                 st.hinc[tile] = inc.h;
                 st_flag(st.flag + tile, 2);
@@ -147,18 +197,47 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan(const TI *in, TO *out, cons
         }
     }
     __syncthreads();
-    // exclusive prefix of this thread = tile prefix (+) warps before (+) lanes before
-    SS<TO, SEG> run = s_prefix;
-    if (wid > 0) run = sop<TO, SEG>(run, s_warp[wid - 1]);
-    SS<TO, SEG> wl = shfl_up_ss<TO, SEG>(w, 1);
-    if (lane > 0) run = sop<TO, SEG>(run, wl);
-#pragma unroll
-    for (int i = 0; i < SCAN_ITEMS; i++) {
-        const int64_t k = base + i;
-        if (SEG && x[i].h) run = SS<TO, SEG>{(TO)0, 1};
-        if (k < n) out[k] = run.v;
-        run = sop<TO, SEG>(run, SS<TO, SEG>{x[i].v, 0});
+    T.write(out, n, base, s_prefix, s_warp);
+}
+
+// deterministic reduce-then-scan for fp64 operands (the look-back's grouping would make
+// the rounding depend on timing): tile sums, one CTA scans them in order, tiles rescan
+template <class T>
+__global__ void __launch_bounds__(SCAN_BLOCK) k_scan_reduce(const T *in, int64_t n, T *tsum) {
+    __shared__ SS<T, false> s_warp[SCAN_BLOCK / 32];
+    TileScan<T, T, false> S;
+    const int64_t base = blockIdx.x * (int64_t)SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+    S.load(in, nullptr, n, base);
+    const SS<T, false> agg = S.reduce(s_warp);
+    if (threadIdx.x == 0) tsum[blockIdx.x] = agg.v;
+}
+template <class T>
+__global__ void __launch_bounds__(SCAN_BLOCK) k_scan_tiles(T *tsum, int64_t nt) {
+    __shared__ SS<T, false> s_warp[SCAN_BLOCK / 32];
+    __shared__ T carry;
+    if (threadIdx.x == 0) carry = (T)0;
+    __syncthreads();
+    for (int64_t b0 = 0; b0 < nt; b0 += SCAN_TILE) {
+        TileScan<T, T, false> S;
+        const int64_t base = b0 + (int64_t)threadIdx.x * SCAN_ITEMS;
+        S.load(tsum, nullptr, nt, base);
+        const SS<T, false> agg = S.reduce(s_warp);
+        const T c = carry;
+        S.write(tsum, nt, base, SS<T, false>{c, 0}, s_warp);
+        __syncthreads();
+        if (threadIdx.x == 0) carry = c + agg.v;
+        __syncthreads();
     }
+}
+template <class T>
+__global__ void __launch_bounds__(SCAN_BLOCK) k_scan_down(const T *in, T *out, int64_t n,
+                                                          const T *tpre) {
+    __shared__ SS<T, false> s_warp[SCAN_BLOCK / 32];
+    TileScan<T, T, false> S;
+    const int64_t base = blockIdx.x * (int64_t)SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+    S.load(in, nullptr, n, base);
+    S.reduce(s_warp);
+    S.write(out, n, base, SS<T, false>{tpre[blockIdx.x], 0}, s_warp);
 }
 
 template <class TO>
@@ -182,9 +261,17 @@ template <class TI, class TO, bool SEG>
 void scan_run(slm_ctx *ctx, const TI *in, TO *out, const uint32_t *keys, int64_t n) {
     if (n <= 0) return;
     const int64_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
-    ScanStatus<TO> st;
-    scan_launch_status<TO>(ctx, ntiles, st);
-    k_scan<TI, TO, SEG><<<(unsigned)ntiles, SCAN_BLOCK, 0, ctx->stream>>>(in, out, keys, n, st);
+    if (std::is_floating_point<TO>::value) {
+        ctx->tmp.resize(ntiles * sizeof(TO));
+        TO *tsum = (TO *)ctx->tmp.p;
+        k_scan_reduce<TO><<<(unsigned)ntiles, SCAN_BLOCK, 0, ctx->stream>>>((const TO *)in, n, tsum);
+        k_scan_tiles<TO><<<1, SCAN_BLOCK, 0, ctx->stream>>>(tsum, ntiles);
+        k_scan_down<TO><<<(unsigned)ntiles, SCAN_BLOCK, 0, ctx->stream>>>((const TO *)in, out, n, tsum);
+    } else {
+        ScanStatus<TO> st;
+        scan_launch_status<TO>(ctx, ntiles, st);
+        k_scan<TI, TO, SEG><<<(unsigned)ntiles, SCAN_BLOCK, 0, ctx->stream>>>(in, out, keys, n, st);
+    }
     CUDA_TRY(cudaGetLastError());
 }
 
@@ -196,9 +283,16 @@ constexpr int RS_ITEMS = 16;
 constexpr int RS_TILE = RS_BLOCK * RS_ITEMS;
 constexpr int RS_MAXP = 8;
 
+// digit of pass p: bits [begin + 8p, min(begin + 8p + 8, end)) (bits at or above end_bit
+// are ignored, as a sort "by bits [begin, end)" must)
+__device__ __forceinline__ unsigned pass_mask(int shift, int end_bit) {
+    const int w = end_bit - shift;
+    return w >= 8 ? 255u : ((1u << w) - 1u);
+}
+
 template <class K>
 __global__ void __launch_bounds__(256) k_rs_hist(const K *keys, int64_t n, int begin_bit, int np,
-                                                 unsigned long long *hist) {
+                                                 int end_bit, unsigned long long *hist) {
     __shared__ unsigned sh[RS_MAXP][256];
     for (int i = threadIdx.x; i < RS_MAXP * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
     __syncthreads();
@@ -206,7 +300,8 @@ __global__ void __launch_bounds__(256) k_rs_hist(const K *keys, int64_t n, int b
          i += (int64_t)gridDim.x * blockDim.x) {
         const K k = keys[i];
         for (int p = 0; p < np; p++) {
-            const unsigned d = (unsigned)(k >> (begin_bit + 8 * p)) & 255u;
+            const int sh_ = begin_bit + 8 * p;
+            const unsigned d = (unsigned)(k >> sh_) & pass_mask(sh_, end_bit);
             atomicAdd(&sh[p][d], 1u);
         }
     }
@@ -247,6 +342,7 @@ __device__ __forceinline__ void st_status(unsigned long long *p, unsigned long l
 template <class K, class V>
 __global__ void __launch_bounds__(RS_BLOCK) k_rs_onesweep(const K *kin, K *kout, const V *vin,
                                                           V *vout, int64_t n, int shift,
+                                                          unsigned dmask,
                                                           const unsigned long long *dbase,
                                                           unsigned long long *status,
                                                           unsigned *ticket) {
@@ -272,7 +368,7 @@ __global__ void __launch_bounds__(RS_BLOCK) k_rs_onesweep(const K *kin, K *kout,
         const int64_t idx = wb + i * 32 + lane;
         const bool ok = idx < n;
         key[i] = ok ? kin[idx] : (K)0;
-        const unsigned d = (unsigned)(key[i] >> shift) & 255u;
+        const unsigned d = (unsigned)(key[i] >> shift) & dmask;
         const unsigned m = __match_any_sync(0xffffffffu, ok ? d : 256u + lane);
         unsigned r = 0;
         if (ok) r = wcnt[wid * 256 + d] + __popc(m & lt);
@@ -298,12 +394,26 @@ __global__ void __launch_bounds__(RS_BLOCK) k_rs_onesweep(const K *kin, K *kout,
             st_status(mine, RS_INC | cnt);
         } else {
             st_status(mine, RS_AGG | cnt);
-            for (int64_t p = tile - 1; p >= 0; p--) {
-                unsigned long long s;
-                while (((s = ld_status(status + p * 256 + d)) >> 62) == 0) {
+            // 8 predecessors per step with independent loads: the walk costs one memory
+            // latency per 8 tiles, not per tile
+            for (int64_t p = tile - 1; p >= 0;) {
+                constexpr int LB = 8;
+                unsigned long long sv[LB];
+#pragma unroll
+                for (int k = 0; k < LB; k++)
+                    sv[k] = p - k >= 0 ? ld_status(status + (p - k) * 256 + d) : RS_INC;
+                int k = 0;
+                bool done = false;
+                for (; k < LB; k++) {
+                    if ((sv[k] >> 62) == 0) break;           // not published yet: reload
+                    excl += sv[k] & RS_VAL;
+                    if ((sv[k] >> 62) == 2) {
+                        done = true;
+                        break;
+                    }
                 }
-                excl += s & RS_VAL;
-                if ((s >> 62) == 2) break;
+                if (done) break;
+                p -= k;
             }
             st_status(mine, RS_INC | (excl + cnt));
         }
@@ -389,7 +499,7 @@ void radix_sort_impl(slm_ctx *ctx, const K *kin, K *kout, const V *vin, V *vout,
     unsigned *tickets = (unsigned *)((char *)ctx->tmp.p + hb);
     unsigned long long *status = (unsigned long long *)((char *)ctx->tmp.p + hb + tb);
     CUDA_TRY(cudaMemsetAsync(ctx->tmp.p, 0, hb + tb, s));
-    k_rs_hist<K><<<grid_for(n, 256, SMS() * 8), 256, 0, s>>>(kin, n, begin_bit, np, hist);
+    k_rs_hist<K><<<grid_for(n, 256, SMS() * 8), 256, 0, s>>>(kin, n, begin_bit, np, end_bit, hist);
     k_rs_hist_scan<<<np, 256, 0, s>>>(hist);
     const size_t smem = rs_smem_bytes<K, V>();
     CUDA_TRY(cudaFuncSetAttribute(k_rs_onesweep<K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -402,8 +512,10 @@ void radix_sort_impl(slm_ctx *ctx, const K *kin, K *kout, const V *vin, V *vout,
         K *kd = to_out ? kout : kalt;
         V *vd = vin ? (to_out ? vout : valt) : nullptr;
         CUDA_TRY(cudaMemsetAsync(status, 0, sb, s));
+        const int shift = begin_bit + 8 * p;
+        const unsigned dmask = end_bit - shift >= 8 ? 255u : ((1u << (end_bit - shift)) - 1u);
         k_rs_onesweep<K, V><<<(unsigned)ntiles, RS_BLOCK, smem, s>>>(
-            ks, kd, vs, vd, n, begin_bit + 8 * p, hist + p * 256, status, tickets + p);
+            ks, kd, vs, vd, n, shift, dmask, hist + p * 256, status, tickets + p);
         ks = kd;
         vs = vd;
     }

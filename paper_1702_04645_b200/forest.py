@@ -4,11 +4,13 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import threading
+
 import numpy as np
 
 from . import _lib
 
-__all__ = ["AssignmentForest", "extract_components"]
+__all__ = ["AssignmentForest", "extract_components", "reverse_assignment"]
 
 
 @dataclass
@@ -28,21 +30,34 @@ class AssignmentForest:
         return self._members
 
 
-_scratch: dict = {}
+_tls = threading.local()
 
 
 def _scratch_ctx(n: int) -> _lib.Context:
-    """An edgeless n-node device graph used to run extract_components on raw maps."""
-    ctx = _scratch.get("ctx")
+    """This thread's device context for map-only calls (extract_components on raw maps,
+    reverse_assignment, canonicalize_labels, uniform01): an edgeless n-node graph (n = 0:
+    any graph; the map-only entry points do not use it)."""
+    ctx = getattr(_tls, "ctx", None)
     if ctx is None:
         ctx = _lib.Context(0)
-        _scratch["ctx"] = ctx
-        _scratch["n"] = -1
-    if _scratch["n"] != n:
+        _tls.ctx = ctx
+        _tls.n = -1
+    if n > 0 and _tls.n != n:
         e = np.empty(0, np.int64)
         ctx.build_graph(n, e, e, np.empty(0))
-        _scratch["n"] = n
+        _tls.n = n
     return ctx
+
+
+def reverse_assignment(a):
+    """forest.py:70-80 on the device: CSR (ptr, kids) of the children j != i with a[j] == i,
+    ascending per parent (stable radix sort by target)."""
+    a = np.asarray(a, dtype=np.int64)
+    if a.size == 0:
+        return np.zeros(1, np.int64), np.empty(0, np.int64)
+    if a.min() < 0 or a.max() >= a.size:
+        raise ValueError("assignment out of range")
+    return _scratch_ctx(0).reverse_assignment(a)
 
 
 def extract_components(a) -> AssignmentForest:

@@ -35,12 +35,16 @@ class Strengths:
 class NeighborUnion:
     """Per-node union of out- and in-neighbours, self-loops excluded (graph.py:46-60).
 
-    Every gain kernel consumes only w_out + w_in, so the device stores the
-    pre-summed ``u``; ``w_out + w_in`` of the reference equals ``u`` bit for bit.
+    ``w_out[e] = W(i, j)`` and ``w_in[e] = W(j, i)`` (0.0 when absent) for entry e = (i, j),
+    split on the device from the canonical CSR (slm_get_union_split).  Every gain kernel
+    consumes only w_out + w_in (SURVEY.md F6), which the device stores pre-summed as ``u``;
+    ``w_out + w_in == u`` bit for bit.
     """
     ptr: np.ndarray
     nbr: np.ndarray
     row: np.ndarray
+    w_out: np.ndarray
+    w_in: np.ndarray
     u: np.ndarray
 
 
@@ -52,6 +56,7 @@ class Graph:
         self._src = src
         self._dst = dst
         self._w = w
+        self._parent = None   # (graph, labels, n_comms) of a graph made by aggregate()
         self._ctx = None
         self._csr = None
         self._union = None
@@ -75,11 +80,14 @@ class Graph:
     # --------------------------------------------------------------- device state
     def context(self, level0: bool = True) -> _lib.Context:
         """Device context holding this graph as hierarchy level 0 (built on first use)."""
-        if self._ctx is None:
-            self._ctx = _lib.Context(0)
-            self._ctx.build_graph(self.n, self._src, self._dst, self._w)
-        elif level0 and self._ctx.level != 0:
-            self._ctx.build_graph(self.n, self._src, self._dst, self._w)
+        if self._ctx is None or (level0 and self._ctx.level != 0):
+            if self._ctx is None:
+                self._ctx = _lib.Context(0)
+            if self._parent is not None:
+                parent, labels, c = self._parent
+                self._ctx.build_aggregate(parent.context(), labels, c)
+            else:
+                self._ctx.build_graph(self.n, self._src, self._dst, self._w)
         return self._ctx
 
     def _canonical(self):
@@ -111,11 +119,13 @@ class Graph:
 
     def neighbor_union(self) -> NeighborUnion:
         if self._union is None:
-            p, nb, u = self.context().union()
+            ctx = self.context()
+            p, nb, u = ctx.union()
+            wo, wi = ctx.union_split()
             row = np.repeat(np.arange(self.n, dtype=np.int64), np.diff(p))
-            for arr in (p, nb, row, u):
+            for arr in (p, nb, row, wo, wi, u):
                 arr.setflags(write=False)
-            self._union = NeighborUnion(p, nb, row, u)
+            self._union = NeighborUnion(p, nb, row, wo, wi, u)
         return self._union
 
     def out_slice(self, i):
@@ -143,7 +153,9 @@ def strengths(graph: Graph) -> Strengths:
 
 
 def aggregate(graph: Graph, labels) -> Graph:
-    """graph.py:266-280: collapse communities into super-nodes (device sort + merge)."""
+    """graph.py:266-280: collapse communities into super-nodes.  The coarse graph is built on
+    the device from the parent's resident CSR (relabel + the level build's radix sort and
+    run merge: slm_build_aggregate); intra-community weight becomes self-loops."""
     labels = np.asarray(labels, dtype=np.int64)
     if labels.shape != (graph.n,):
         raise ValueError("labels must cover every node exactly once")
@@ -152,18 +164,22 @@ def aggregate(graph: Graph, labels) -> Graph:
     c = int(labels.max()) + 1
     if labels.min() < 0 or np.bincount(labels, minlength=c).min() == 0:
         raise ValueError("labels must be a dense relabeling 0..c-1")
-    return Graph.from_edges(c, labels[graph.edge_rows()], labels[graph.out_dst], graph.out_w)
+    out = Graph(c, None, None, None, _validated=True)
+    out._parent = (graph, labels.copy(), c)
+    out._ctx = _lib.Context(0)
+    out._ctx.build_aggregate(graph.context(), labels, c)
+    return out
 
 
 def canonicalize_labels(labels) -> np.ndarray:
-    """Dense labels 0..c-1 ordered by each community's smallest member (graph.py:283-291)."""
+    """Dense labels 0..c-1 ordered by each community's smallest member (graph.py:283-291),
+    on the device (stable radix sort by label, first occurrences ranked)."""
     labels = np.asarray(labels, dtype=np.int64)
     if labels.size == 0:
         return labels.copy()
-    uniq, first = np.unique(labels, return_index=True)
-    remap = np.empty(uniq.size, dtype=np.int64)
-    remap[np.argsort(first, kind="stable")] = np.arange(uniq.size)
-    return remap[np.searchsorted(uniq, labels)]
+    from .forest import _scratch_ctx
+    out, _ = _scratch_ctx(0).canonicalize(labels)
+    return out
 
 
 def compose_labels(inner, outer) -> np.ndarray:

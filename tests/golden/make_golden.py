@@ -102,7 +102,7 @@ def main():
     print("wrote", len(cases), "cases")
 
 
-if __name__ == "__main__" and "--configs" not in sys.argv:
+if __name__ == "__main__" and "--configs" not in sys.argv and "--surface" not in sys.argv:
     main()
 
 
@@ -142,3 +142,53 @@ def hash_edges(s, d, w):
 
 if __name__ == "__main__" and "--configs" in sys.argv:
     configs()
+
+
+def surface():
+    """reference_surface.npz: the rest of the hot-path API surface on the same golden graphs --
+    NeighborUnion.w_out / w_in, reverse_assignment, canonicalize_labels,
+    CommunityAggregates.from_labels, gain_switch (incl. to=None) and aggregate()."""
+    from synclouvain.forest import reverse_assignment
+    from synclouvain.graph import aggregate, canonicalize_labels
+    from synclouvain.quality import gain_switch
+    ph = np.load(os.path.join(HERE, "reference_phases.npz"))
+    out = {}
+    rng = np.random.default_rng(5150)
+    for key in [str(c) for c in ph["cases"]]:
+        n = int(ph[f"{key}/n"])
+        G = S.Graph.from_edges(n, ph[f"{key}/src"], ph[f"{key}/dst"], ph[f"{key}/w"])
+        st = S.strengths(G)
+        U = G.neighbor_union()
+        out[f"{key}/w_out"], out[f"{key}/w_in"] = U.w_out, U.w_in
+        for tag in ("assign", "pos_a", "max_a"):
+            p, kids = reverse_assignment(ph[f"{key}/{tag}"])
+            out[f"{key}/rev_{tag}_ptr"], out[f"{key}/rev_{tag}_kids"] = p, kids
+        raw = rng.integers(-7, 3 * n, n)
+        out[f"{key}/canon_in"] = raw
+        out[f"{key}/canon_out"] = canonicalize_labels(raw)
+        comm = ph[f"{key}/pos_comm"]
+        nc = int(comm.max()) + 1
+        agg = S.CommunityAggregates.from_labels(st, comm, nc)
+        out[f"{key}/agg_s_out"], out[f"{key}/agg_s_in"], out[f"{key}/agg_count"] = \
+            agg.s_out, agg.s_in, agg.count
+        gs = []
+        for t in range(8):
+            frm = int(comm[rng.integers(0, n)])
+            mem = np.flatnonzero(comm == frm)
+            k = int(rng.integers(1, mem.size + 1))
+            nodes = np.sort(rng.choice(mem, size=k, replace=False))
+            to = None if t % 4 == 3 else int(rng.integers(0, nc))
+            g = gain_switch(G, st, comm, agg, nodes, frm, to)
+            gs.append((frm, -1 if to is None else to, k, g))
+            out[f"{key}/gs{t}_nodes"] = nodes
+        out[f"{key}/gs"] = np.array(gs, np.float64)
+        H = aggregate(G, comm)
+        out[f"{key}/agg_graph_ptr"], out[f"{key}/agg_graph_dst"], out[f"{key}/agg_graph_w"] = \
+            H.out_ptr, H.out_dst, H.out_w
+    out["cases"] = ph["cases"]
+    np.savez_compressed(os.path.join(HERE, "reference_surface.npz"), **out)
+    print("wrote surface fixtures")
+
+
+if __name__ == "__main__" and "--surface" in sys.argv:
+    surface()
