@@ -279,7 +279,7 @@ void scan_run(slm_ctx *ctx, const TI *in, TO *out, const uint32_t *keys, int64_t
 
 constexpr int RS_BLOCK = 512;
 constexpr int RS_WARPS = RS_BLOCK / 32;
-constexpr int RS_ITEMS = 16;
+constexpr int RS_ITEMS = 12;
 constexpr int RS_TILE = RS_BLOCK * RS_ITEMS;
 constexpr int RS_MAXP = 8;
 
@@ -340,7 +340,7 @@ __device__ __forceinline__ void st_status(unsigned long long *p, unsigned long l
 }
 
 template <class K, class V>
-__global__ void __launch_bounds__(RS_BLOCK) k_rs_onesweep(const K *kin, K *kout, const V *vin,
+__global__ void __launch_bounds__(RS_BLOCK, 2) k_rs_onesweep(const K *kin, K *kout, const V *vin,
                                                           V *vout, int64_t n, int shift,
                                                           unsigned dmask,
                                                           const unsigned long long *dbase,
@@ -362,20 +362,26 @@ __global__ void __launch_bounds__(RS_BLOCK) k_rs_onesweep(const K *kin, K *kout,
     const int64_t wb = t0 + (int64_t)wid * 32 * RS_ITEMS;
     K key[RS_ITEMS];
     unsigned pos[RS_ITEMS];
+    // 4-byte values are loaded with the keys (their latency overlaps the ranking)
+    constexpr bool VPRE = sizeof(V) == 4;
+    V val[VPRE ? RS_ITEMS : 1];
     const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
     for (int i = 0; i < RS_ITEMS; i++) {
         const int64_t idx = wb + i * 32 + lane;
-        const bool ok = idx < n;
-        key[i] = ok ? kin[idx] : (K)0;
+        key[i] = idx < n ? kin[idx] : (K)0;
+        if (VPRE && vin) val[VPRE ? i : 0] = idx < n ? vin[idx] : (V)0;
+    }
+#pragma unroll
+    for (int i = 0; i < RS_ITEMS; i++) {
+        const bool ok = wb + i * 32 + lane < n;
         const unsigned d = (unsigned)(key[i] >> shift) & dmask;
         const unsigned m = __match_any_sync(0xffffffffu, ok ? d : 256u + lane);
-        unsigned r = 0;
-        if (ok) r = wcnt[wid * 256 + d] + __popc(m & lt);
-        __syncwarp();
-        if (ok && (m & lt) == 0) wcnt[wid * 256 + d] += __popc(m);
-        __syncwarp();
-        pos[i] = ok ? (r | (d << 24)) : 0xffffffffu;   // warp-local rank (< 2^24) | digit
+        const int leader = __ffs(m) - 1;
+        unsigned base = 0;
+        if (ok && lane == leader) base = atomicAdd(&wcnt[wid * 256 + d], (unsigned)__popc(m));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        pos[i] = ok ? ((base + __popc(m & lt)) | (d << 24)) : 0xffffffffu;   // rank | digit
     }
     __syncthreads();
     // per digit: warp offsets, tile count, tile start in digit order
@@ -461,7 +467,7 @@ __global__ void __launch_bounds__(RS_BLOCK) k_rs_onesweep(const K *kin, K *kout,
 #pragma unroll
         for (int i = 0; i < RS_ITEMS; i++) {
             const int64_t idx = wb + i * 32 + lane;
-            if (idx < n) sv[pos[i]] = vin[idx];
+            if (idx < n) sv[pos[i]] = VPRE ? val[VPRE ? i : 0] : vin[idx];
         }
         __syncthreads();
         for (int j = threadIdx.x; j < nt; j += RS_BLOCK) {
