@@ -250,6 +250,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-partition", action="store_true",
                     help="skip the end-to-end seconds-to-final-partition runs")
+    ap.add_argument("--parity", default="c3_rmat22",
+                    help="comma list of configs checked against the oracle at full size, "
+                         "full hierarchy in lockstep (tools/parity_fullsize.py); '' = none")
+    ap.add_argument("--parity-timeout", type=float, default=900.0)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -293,6 +297,9 @@ def main():
             dist.barrier()
             dist.destroy_process_group()
         return
+
+    # full-size parity against the oracle (its own process, before this one reserves HBM)
+    parity = parity_legs(args) if (rank == 0 and args.parity and not args.no_cpu) else None
 
     import torch
     if ws > 1:
@@ -418,12 +425,39 @@ def main():
                       f"entries) of the same snapshot; targets equal to the GPU's: {ok}"}
     if not args.no_partition:
         line["partition"] = partition_runs(ctx, args, rank, threads)
+    if parity is not None:
+        line["parity"] = parity
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
         import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()
+
+
+def parity_legs(args):
+    """Full-size bit-exact parity (north_star: "partitions identical to the reference oracle
+    on every integer-weighted config"): tools/parity_fullsize.py replays every phase of the
+    device's level loop on the C oracle (host cores) from the same state, full hierarchy in
+    lockstep, and reports the first mismatch if any."""
+    out = {}
+    for cfg in [c for c in args.parity.split(",") if c]:
+        t0 = time.perf_counter()
+        try:
+            r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "parity_fullsize.py"),
+                                cfg, "--lockstep", "-1"], capture_output=True, text=True,
+                               timeout=args.parity_timeout)
+            rec = json.loads(r.stdout.strip().splitlines()[-1])
+            out[cfg] = {k: rec.get(k) for k in ("result", "phases_checked", "sweeps_per_level",
+                                                "modularity", "modularity_oracle", "n",
+                                                "union_entries", "oracle_threads")}
+            out[cfg]["mode"] = "full hierarchy, every phase in lockstep"
+        except subprocess.TimeoutExpired:
+            out[cfg] = {"result": f"not finished within {args.parity_timeout:.0f} s"}
+        except (ValueError, IndexError) as e:
+            out[cfg] = {"result": f"harness error: {e}"}
+        out[cfg]["seconds"] = round(time.perf_counter() - t0, 1)
+    return out
 
 
 def partition_runs(ctx, args, rank, threads):

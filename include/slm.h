@@ -70,7 +70,9 @@ SLM_API int slm_build_graph(slm_ctx *ctx, int64_t n, const int64_t *src, const i
 SLM_API int slm_build_graph_device(slm_ctx *ctx, int64_t n, const int32_t *d_src, const int32_t *d_dst,
                            const double *d_w, int64_t nedges);
 /* Sizes of the current level: nodes, merged CSR entries, union entries, m_w, flags
- * (bit0: symmetric W, bit1: integer weights). */
+ * (bit0: symmetric W, bit1: integer weights, bit2: the plan sweep runs the exact uint32
+ * group-sum path; otherwise fp64 sums, exact for integers, or the sorted reference-order
+ * form for real-valued weights). */
 SLM_API int slm_graph_info(slm_ctx *ctx, int64_t *n, int64_t *ne, int64_t *ue, double *m_w,
                    int32_t *flags);
 SLM_API int slm_get_csr(slm_ctx *ctx, int64_t *out_ptr, int64_t *out_dst, double *out_w);
@@ -121,6 +123,18 @@ SLM_API int slm_get_cstar(slm_ctx *ctx, int64_t *cstar_out);
  * (1), + community-strength gathers (2) -- the memory-system floor of the sweep; modes 3-5:
  * the same over the degree-ordered sweep view. */
 SLM_API int slm_debug_sweep_floor(slm_ctx *ctx, int32_t mode, double *ms);
+/* run() of detector.py:548-653 in one call (no host round trip per phase): the whole
+ * level loop on the current graph with the reference's stop rules and the exact
+ * fast-forward.  stats[5] = accepted_moves, accepted_splits, unresolved_negative, skipped
+ * POSITIVE calls, levels stopped at max_outer_iters; phase_s[5] = wall seconds of assign,
+ * components, positive, maximal, aggregate (nullable).  Per-level results via
+ * slm_run_level (labels_out nullable; plan_path 0 = uint32 fast path, 1 = fp64 on integer
+ * sums, 2 = sorted reference order, plus 8 when the level stopped at max_outer_iters). */
+SLM_API int slm_run(slm_ctx *ctx, const slm_config *cfg, int64_t *n_levels, int64_t *stats,
+                    double *phase_s);
+SLM_API int slm_run_level(slm_ctx *ctx, int64_t t, int64_t *n_nodes, int64_t *sweeps,
+                          int32_t *plan_path, int64_t *labels_out);
+
 /* ---- the rest of the reference's hot-path API (slm_surface.cu) ------------------- */
 /* CommunityAggregates.from_labels (quality.py:71-79) over caller strengths: S_out / S_in
  * by sequential per-community sums in node order (np.bincount), member counts. */

@@ -69,6 +69,8 @@ SIGNATURES = {
     "slm_plan_groups": (C.c_int, [_VP, _PI64, _VP, _VP]),
     "slm_get_cstar": (C.c_int, [_VP, _VP]),
     "slm_debug_sweep_floor": (C.c_int, [_VP, C.c_int32, _PD]),
+    "slm_run": (C.c_int, [_VP, C.POINTER(SlmConfig), _PI64, _VP, _VP]),
+    "slm_run_level": (C.c_int, [_VP, _I64, _PI64, _PI64, _PI32, _VP]),
     "slm_community_sums": (C.c_int, [_VP, _I64, _VP, _I64, _VP, _VP, _VP, _VP, _VP]),
     "slm_gain_switch": (C.c_int, [_VP, _VP, _VP, _I64, _I64, _I64, _VP, C.c_double, _PD]),
     "slm_reverse_assignment": (C.c_int, [_VP, _I64, _VP, _VP, _VP, _PI64]),
@@ -173,7 +175,9 @@ class Context:
         fl = C.c_int32()
         self.call("slm_graph_info", C.byref(n), C.byref(ne), C.byref(ue), C.byref(m), C.byref(fl))
         return dict(n=n.value, ne=ne.value, ue=ue.value, m_w=m.value,
-                    symmetric=bool(fl.value & 1), integral=bool(fl.value & 2))
+                    symmetric=bool(fl.value & 1), integral=bool(fl.value & 2),
+                    plan_path=("u32" if fl.value & 4 else
+                               "fp64-exact" if fl.value & 2 else "sorted"))
 
     def csr(self):
         d = self.info()
@@ -318,6 +322,26 @@ class Context:
         ms = C.c_double()
         self.call("slm_debug_sweep_floor", int(mode), C.byref(ms))
         return ms.value
+
+    def run(self, cfg: SlmConfig):
+        """The whole level loop on the device side (slm_run) -> (levels, sweeps, paths,
+        capped, stats[5], phase seconds[5])."""
+        nl = C.c_int64()
+        st = np.zeros(5, np.int64)
+        ph = np.zeros(5, np.float64)
+        self.call("slm_run", C.byref(cfg), C.byref(nl), ptr(st), ptr(ph))
+        levels, sweeps, paths, capped = [], [], [], []
+        for t in range(nl.value):
+            nn, sw, pp = C.c_int64(), C.c_int64(), C.c_int32()
+            self.call("slm_run_level", t, C.byref(nn), C.byref(sw), C.byref(pp), None)
+            lab = np.empty(nn.value, np.int64)
+            self.call("slm_run_level", t, None, None, None, ptr(lab))
+            levels.append(lab)
+            sweeps.append(sw.value)
+            paths.append(("u32", "fp64-exact", "sorted")[pp.value & 3])
+            capped.append(bool(pp.value & 8))
+        self.level = nl.value - 1
+        return levels, sweeps, paths, capped, st, ph
 
     # ----- reference API surface (slm_surface.cu)
     def community_sums(self, labels, n_comms, s_out, s_in):

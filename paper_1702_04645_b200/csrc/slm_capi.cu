@@ -514,7 +514,13 @@ int slm_graph_info(slm_ctx *ctx, int64_t *n, int64_t *ne, int64_t *ue, double *m
     if (ne) *ne = G.ne;
     if (ue) *ue = G.ue;
     if (m_w) *m_w = G.m_w;
-    if (flags) *flags = (G.sym ? 1 : 0) | (G.integral ? 2 : 0);
+    if (flags) {
+        // plan-sweep path of this level (run_plan): 4 = exact uint32 group sums (integer
+        // weights, every row total < 2^32), else fp64 on integer sums (exact), else the
+        // sorted reference-order form (real-valued weights)
+        const bool u32 = G.u32_ok && !getenv("SLM_FORCE_GENERIC") && !getenv("SLM_PLAN_SORTED");
+        *flags = (G.sym ? 1 : 0) | (G.integral ? 2 : 0) | (u32 ? 4 : 0);
+    }
     API_END
 }
 
@@ -800,6 +806,109 @@ int slm_debug_scan(slm_ctx *ctx, int32_t kind, const void *in, void *out, const 
     SLM_REQUIRE(ctx && in && out && n >= 0 && kind >= 0 && kind <= 4 && (kind != 4 || keys),
                 SLM_EINVAL, "bad scan arguments");
     if (n) debug_scan(ctx, kind, in, out, keys, n);
+    API_END
+}
+
+// ---------------------------------------------------------- the level loop in one call
+// run() of detector.py:548-653 without a host round trip per phase: ASSIGN, COMPONENTS,
+// POSITIVE, {MAXIMAL -> POSITIVE} up to max_outer_iters, AGGREGATE, until the identity
+// level.  Same stop rules, statistics and exact fast-forward as paper_1702_04645_b200/
+// detector.py (which calls this when no per-phase trace or debug check is requested).
+// stats[0..4]: accepted_moves, accepted_splits, unresolved_negative, skipped POSITIVE
+// calls, levels that hit max_outer_iters; phase_s[0..4]: assign, components, positive,
+// maximal, aggregate (host wall seconds, the reference's tick()).
+int slm_run(slm_ctx *ctx, const slm_config *cfg, int64_t *n_levels, int64_t *stats,
+            double *phase_s) {
+    API_BEGIN
+    require_graph(ctx);
+    SLM_REQUIRE(cfg && cfg->max_outer_iters >= 1, SLM_EINVAL, "bad config");
+    SLM_REQUIRE(ctx->g->n > 0, SLM_EINVAL, "graph has no nodes");
+    ctx->run_levels.clear();
+    ctx->run_sweeps.clear();
+    ctx->run_paths.clear();
+    int64_t st[5] = {0, 0, 0, 0, 0};
+    double ph[5] = {0, 0, 0, 0, 0};
+    auto clk = [] { return now_ms() * 1e-3; };
+    auto ok = [&](int rc) {
+        if (rc != SLM_OK) throw SlmError{rc, ctx->err};
+    };
+    int64_t level = 0;
+    for (;;) {
+        const LevelGraph &G = *ctx->g;
+        const int64_t n_level = G.n;
+        const bool integral = G.integral;
+        int32_t fl = 0;
+        ok(slm_graph_info(ctx, nullptr, nullptr, nullptr, nullptr, &fl));
+        ctx->run_paths.push_back(fl & 4 ? 0 : (fl & 2 ? 1 : 2));
+        double t = clk();
+        ok(slm_assign(ctx, nullptr));
+        ph[0] += clk() - t;
+        t = clk();
+        int64_t nc = 0;
+        ok(slm_components(ctx, nullptr, nullptr, &nc));
+        ph[1] += clk() - t;
+        t = clk();
+        int64_t sp = 0, un = 0;
+        int32_t ch = 0;
+        ok(slm_positive(ctx, cfg, &sp, &un, &ch, nullptr, 0));
+        ph[2] += clk() - t;
+        st[1] += sp;
+        st[2] += un;
+        int64_t last_un = un;
+        int64_t sweeps = 0;
+        for (;;) {
+            if (sweeps >= cfg->max_outer_iters) {
+                st[4]++;
+                ctx->run_paths.back() |= 8;   // stopped by the cap (the reference warns)
+                break;
+            }
+            t = clk();
+            int32_t imp = 0;
+            int64_t app = 0;
+            ok(slm_maximal(ctx, cfg, level, sweeps, &imp, &app, nullptr, 0));
+            ph[3] += clk() - t;
+            sweeps++;
+            st[0] += app;
+            if (!imp) break;
+            if (app == 0 && integral) {   // forest unchanged: POSITIVE would repeat itself
+                st[2] += last_un;
+                st[3]++;
+                continue;
+            }
+            t = clk();
+            ok(slm_positive(ctx, cfg, &sp, &un, &ch, nullptr, 0));
+            ph[2] += clk() - t;
+            st[1] += sp;
+            st[2] += un;
+            last_un = un;
+        }
+        ctx->run_sweeps.push_back(sweeps);
+        std::vector<int64_t> lab(n_level);
+        ok(slm_get_forest(ctx, nullptr, lab.data(), nullptr, &nc));
+        ctx->run_levels.push_back(std::move(lab));
+        if (nc == n_level) break;
+        t = clk();
+        ok(slm_aggregate(ctx));
+        ph[4] += clk() - t;
+        level++;
+    }
+    *n_levels = (int64_t)ctx->run_levels.size();
+    if (stats)
+        for (int k = 0; k < 5; k++) stats[k] = st[k];
+    if (phase_s)
+        for (int k = 0; k < 5; k++) phase_s[k] = ph[k];
+    API_END
+}
+
+int slm_run_level(slm_ctx *ctx, int64_t t, int64_t *n_nodes, int64_t *sweeps, int32_t *plan_path,
+                  int64_t *labels_out) {
+    API_BEGIN
+    SLM_REQUIRE(t >= 0 && t < (int64_t)ctx->run_levels.size(), SLM_EINVAL, "no such level");
+    const std::vector<int64_t> &L = ctx->run_levels[t];
+    if (n_nodes) *n_nodes = (int64_t)L.size();
+    if (sweeps) *sweeps = ctx->run_sweeps[t];
+    if (plan_path) *plan_path = (int32_t)ctx->run_paths[t];
+    if (labels_out) std::copy(L.begin(), L.end(), labels_out);
     API_END
 }
 

@@ -251,6 +251,9 @@ struct slm_ctx {
     double *h_f64 = nullptr;
     // counters of the last phase calls
     int64_t last_rounds = 0, last_candidates = 0, last_accepted = 0;
+    // results of the last slm_run (labels per level on the host, per-level sweeps / paths)
+    std::vector<std::vector<int64_t>> run_levels;
+    std::vector<int64_t> run_sweeps, run_paths;
     // per-context grow-only scratch of the phase functions (CTX_SCRATCH below)
     std::unordered_map<const void *, std::shared_ptr<void>> scratch;
 };

@@ -237,10 +237,152 @@ __global__ void k_copy_labels(const int32_t *label, int64_t n, int32_t *out) {
         out[i] = label[i];
 }
 
+// --------------------------------------------- PLAN, sorted form (real-valued weights)
+// The reference's own evaluation order (detector.py:383-418): union entries keyed by
+// (row, neighbour community), stable-sorted, each group summed with np.add.reduceat's order
+// (first + pairwise(rest)), then per row the first maximum over non-own groups in
+// ascending community order, taken iff it strictly beats staying.  Bit-identical for any
+// real weights and independent of scheduling (the integer paths' atomics are exact only
+// for integer sums).
+
+__global__ void k_ps_keys(const int64_t *uptr, const int32_t *unbr, const double *uu,
+                          const int32_t *lab, int64_t n, int bc, uint64_t *keys, double *vals) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = w0; r < n; r += nw)
+        for (int64_t e = uptr[r] + lane; e < uptr[r + 1]; e += 32) {
+            keys[e] = ((uint64_t)r << bc) | (uint32_t)lab[unbr[e]];
+            vals[e] = uu[e];
+        }
+}
+__global__ void k_ps_heads(const uint64_t *keys, int64_t E, int64_t *head) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+         e += (int64_t)gridDim.x * blockDim.x)
+        head[e] = (e == 0 || keys[e] != keys[e - 1]) ? 1 : 0;
+}
+__global__ void k_ps_groups(const uint64_t *keys, const int64_t *head, const int64_t *gid,
+                            int64_t E, int64_t *gstart, uint64_t *gkey) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+         e += (int64_t)gridDim.x * blockDim.x)
+        if (head[e]) {
+            gstart[gid[e]] = e;
+            gkey[gid[e]] = keys[e];
+        }
+}
+__global__ void k_ps_sums(const double *vals, const int64_t *gstart, int64_t ng, int64_t E,
+                          double *gsum) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ng;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = gstart[g], b = g + 1 < ng ? gstart[g + 1] : E;
+        gsum[g] = reduceat_seq(vals + a, b - a);
+    }
+}
+// first group of every row (groups are ordered by row): lower bound of r << bc
+__global__ void k_ps_rowptr(const uint64_t *gkey, int64_t ng, int64_t n, int bc, int64_t *rp) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = (uint64_t)r << bc;
+        int64_t lo = 0, hi = ng;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (gkey[mid] < k) lo = mid + 1;
+            else hi = mid;
+        }
+        rp[r] = lo;
+    }
+}
+__global__ void k_ps_select(PlanArgs A, const uint64_t *gkey, const double *gsum,
+                            const int64_t *rp, int64_t n, uint64_t cmask) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = w0; r < n; r += nw) {
+        const int32_t L = A.label[r];
+        const double so = A.s_out[r], si = A.s_in[r];
+        double bt = -INFINITY, tstay = 0.0;
+        int32_t bc = 0x7fffffff;
+        int hown = 0;
+        for (int64_t g = rp[r] + lane; g < rp[r + 1]; g += 32) {
+            const int32_t c = (int32_t)(gkey[g] & cmask);
+            const bool own = c == L;
+            const double t = plan_gain(gsum[g], own, so, si, A.S_in[c], A.S_out[c], A.m, A.m2);
+            if (own) {
+                tstay = t;
+                hown = 1;
+            } else if (better(t, c, bt, bc)) {
+                bt = t;
+                bc = c;
+            }
+        }
+        warp_argmax(bt, bc);
+        const unsigned om = __ballot_sync(0xffffffffu, hown);
+        tstay = __shfl_sync(0xffffffffu, tstay, om ? __ffs(om) - 1 : 0);
+        if (lane == 0) {
+            if (!om) tstay = -(so * (A.S_in[L] - si) + si * (A.S_out[L] - so)) / A.m2;
+            A.cstar[r] = (bc != 0x7fffffff && bt > tstay) ? bc : L;
+        }
+    }
+}
+
+static void run_plan_sorted(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
+                            int32_t *d_cstar, unsigned long long *d_groups) {
+    cudaStream_t s = ctx->stream;
+    const int64_t n = G.n, E = G.ue;
+    PlanArgs A = make_args(G, F, m, d_cstar);
+    const int bc = bits_for(F.n_comms + 1);
+    CTX_SCRATCH(DBuf<uint64_t>, pkeys);
+    CTX_SCRATCH(DBuf<double>, pvals);
+    CTX_SCRATCH(DBuf<int64_t>, phead);
+    CTX_SCRATCH(DBuf<int64_t>, pgid);
+    pkeys.resize(E);
+    pvals.resize(E);
+    phead.resize(E + 1);
+    pgid.resize(E + 1);
+    if (E) {
+        k_ps_keys<<<grid_for(n * 32, 256), 256, 0, s>>>(G.uptr.p, G.unbr.p, G.uu.p, F.comm.p, n, bc,
+                                                        pkeys.p, pvals.p);
+        sort_pairs_u64_f64(ctx, pkeys, pvals, E, bits_for(n + 1) + bc);
+        k_ps_heads<<<grid_for(E, 256), 256, 0, s>>>(pkeys.p, E, phead.p);
+    }
+    CUDA_TRY(cudaMemsetAsync(phead.p + E, 0, 8, s));
+    dev_exclusive_sum<int64_t, int64_t>(ctx, phead.p, pgid.p, E + 1);
+    int64_t ng = 0;
+    CUDA_TRY(cudaMemcpyAsync(&ng, pgid.p + E, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    DBuf<int64_t> gstart, rp;
+    DBuf<uint64_t> gkey;
+    DBuf<double> gsum;
+    gstart.resize(ng);
+    gkey.resize(ng);
+    gsum.resize(ng);
+    rp.resize(n + 1);
+    if (ng) {
+        k_ps_groups<<<grid_for(E, 256), 256, 0, s>>>(pkeys.p, phead.p, pgid.p, E, gstart.p, gkey.p);
+        k_ps_sums<<<grid_for(ng, 128), 128, 0, s>>>(pvals.p, gstart.p, ng, E, gsum.p);
+    }
+    k_ps_rowptr<<<grid_for(n + 1, 256), 256, 0, s>>>(gkey.p, ng, n, bc, rp.p);
+    if (n) k_ps_select<<<grid_for(n * 32, 256), 256, 0, s>>>(A, gkey.p, gsum.p, rp.p, n,
+                                                             (1ull << bc) - 1);
+    if (d_groups && ng) {
+        const unsigned long long g64 = (unsigned long long)ng;
+        CUDA_TRY(cudaMemcpyAsync(d_groups, &g64, 8, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    CUDA_TRY(cudaGetLastError());
+}
+
 void run_plan(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_t *d_cstar,
               int bin_mask, unsigned long long *d_groups) {
-    if (G.u32_ok) {
+    static const bool force_sorted = getenv("SLM_PLAN_SORTED") != nullptr;
+    static const bool force_generic = getenv("SLM_FORCE_GENERIC") != nullptr;
+    if (G.u32_ok && !force_generic && !force_sorted) {
         run_plan_u32(ctx, G, F, m, d_cstar, bin_mask, d_groups);
+        return;
+    }
+    if ((!G.integral || force_sorted) && bin_mask == 127) {
+        // real-valued weights: the reference's stable-sort + reduceat order (deterministic)
+        run_plan_sorted(ctx, G, F, m, d_cstar, d_groups);
         return;
     }
     // generic fp64 path (non-integer weights or row totals >= 2^32)
@@ -257,11 +399,7 @@ void run_plan(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int32_t *d
         k_plan_small<<<grid_for(ns * 32, 256, SMS() * 64), 256, 0, s>>>(A, G.bin_rows.p + G.bin_off[0], ns);
     if (nm && (bin_mask & 14)) {
         size_t sm = MID_H * (sizeof(double) + sizeof(int32_t));
-        static bool attr = false;
-        if (!attr) {
-            CUDA_TRY(cudaFuncSetAttribute(k_plan_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            attr = true;
-        }
+        CUDA_TRY(cudaFuncSetAttribute(k_plan_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         k_plan_mid<<<(unsigned)std::min<int64_t>(nm, SMS() * 2 * 8), MID_BLOCK, sm, s>>>(A, G.bin_rows.p + G.bin_off[1], nm);
     }
     if (nl && (bin_mask & 48)) {

@@ -353,9 +353,11 @@ __global__ void __launch_bounds__(RS_BLOCK, 2) k_rs_onesweep(const K *kin, K *ko
     unsigned char *sdig = (unsigned char *)(tstart + 256);                  // [TILE]
     K *sk = (K *)(sdig + RS_TILE);                                          // [TILE] (keys, then values)
     __shared__ unsigned s_tile;
+    __shared__ unsigned s_hist[256];
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int i = lane; i < 256; i += 32) wcnt[wid * 256 + i] = 0;
+    if (threadIdx.x < 256) s_hist[threadIdx.x] = 0;
     __syncthreads();
     const int64_t tile = s_tile;
     const int64_t t0 = tile * RS_TILE;
@@ -372,6 +374,14 @@ __global__ void __launch_bounds__(RS_BLOCK, 2) k_rs_onesweep(const K *kin, K *ko
         key[i] = idx < n ? kin[idx] : (K)0;
         if (VPRE && vin) val[VPRE ? i : 0] = idx < n ? vin[idx] : (V)0;
     }
+    // the tile's digit counts first, published at once, so that the tiles behind this one
+    // find them during their look-back while this tile is still ranking its keys
+#pragma unroll
+    for (int i = 0; i < RS_ITEMS; i++)
+        if (wb + i * 32 + lane < n) atomicAdd(&s_hist[(unsigned)(key[i] >> shift) & dmask], 1u);
+    __syncthreads();
+    if (threadIdx.x < 256)
+        st_status(status + tile * 256 + threadIdx.x, (tile == 0 ? RS_INC : RS_AGG) | s_hist[threadIdx.x]);
 #pragma unroll
     for (int i = 0; i < RS_ITEMS; i++) {
         const bool ok = wb + i * 32 + lane < n;
@@ -393,13 +403,10 @@ __global__ void __launch_bounds__(RS_BLOCK, 2) k_rs_onesweep(const K *kin, K *ko
             wcnt[w * 256 + d] = cnt;
             cnt += c;
         }
-        // publish the tile's count, look back for the global prefix of this digit
+        // look back for the global prefix of this digit (the count was published above)
         unsigned long long *mine = status + tile * 256 + d;
         unsigned long long excl = 0;
-        if (tile == 0) {
-            st_status(mine, RS_INC | cnt);
-        } else {
-            st_status(mine, RS_AGG | cnt);
+        if (tile != 0) {
             // 8 predecessors per step with independent loads: the walk costs one memory
             // latency per 8 tiles, not per tile
             for (int64_t p = tile - 1; p >= 0;) {

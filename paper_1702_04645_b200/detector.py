@@ -75,6 +75,7 @@ class RunStats:
     warnings: list = field(default_factory=list)
     debug_failures: list = field(default_factory=list)
     skipped_positive_calls: int = 0     # exact fast-forward (not in the reference)
+    plan_paths: list = field(default_factory=list)   # plan-sweep path per level (device)
 
 
 @dataclass
@@ -127,6 +128,27 @@ def run(graph: Graph, config: RunConfig | None = None) -> RunResult:
     ctx.set_resolution(config.resolution)
     cfg = config._c()
     gamma = config.resolution
+    if not (config.record_scores or config.debug_checks):
+        # the whole loop below in one library call (slm_run): no host round trip per phase
+        levels, sweeps, paths, capped, st, ph = ctx.run(cfg)
+        stats.sweeps_per_level = sweeps
+        stats.plan_paths = paths
+        stats.accepted_moves, stats.accepted_splits, stats.unresolved_negative = (
+            int(st[0]), int(st[1]), int(st[2]))
+        stats.skipped_positive_calls = int(st[3])
+        for t, c in enumerate(capped):
+            if c:
+                stats.warnings.append(f"level {t}: stopped after {config.max_outer_iters} sweeps")
+        for k, v in zip(("assign", "components", "positive", "maximal", "aggregate"), ph):
+            stats.phase_seconds[k] = float(v)
+        flat = levels[0]
+        for lv in levels[1:]:
+            flat = compose_labels(flat, lv)
+        final = ctx.score(flat, gamma, on_original=True)
+        stats.levels = len(levels)
+        stats.wall_seconds = time.perf_counter() - t_start
+        return RunResult(hierarchy=Hierarchy(levels=levels, flat=flat), final_score=final,
+                         stats=stats)
     trace = [] if config.record_scores else None
     want_g = trace is not None
     levels = []
@@ -135,6 +157,7 @@ def run(graph: Graph, config: RunConfig | None = None) -> RunResult:
         info = ctx.info()
         n_level = info["n"]
         integral = info["integral"]
+        stats.plan_paths.append(info["plan_path"])
         if trace is not None:
             stats.trace_level_starts.append(len(trace))
         clock["t"] = time.perf_counter()

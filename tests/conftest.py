@@ -27,6 +27,14 @@ def golden_configs():
     return np.load(os.path.join(GOLDEN, "reference_configs.npz"))
 
 
+@pytest.fixture(scope="module")
+def slm():
+    import paper_1702_04645_b200 as P
+    from paper_1702_04645_b200 import _lib
+    _lib.load()
+    return P
+
+
 @pytest.fixture(scope="session")
 def oracle():
     from oracle import oracle as O

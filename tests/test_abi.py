@@ -59,8 +59,8 @@ def test_graph_validation_errors_before_device():
 
 
 def test_label_helpers():
-    from paper_1702_04645_b200 import canonicalize_labels, compose_labels
-    np.testing.assert_array_equal(canonicalize_labels([5, 3, 5, 9, 3]), [0, 1, 0, 2, 1])
+    # canonicalize_labels runs on the device (tests/test_gpu_surface.py); compose is a gather
+    from paper_1702_04645_b200 import compose_labels
     np.testing.assert_array_equal(compose_labels([0, 1, 1, 2], [1, 0, 1]), [1, 0, 0, 1])
 
 

@@ -43,6 +43,7 @@ def test_reverse_assignment(P, golden, surf):
 
 
 def test_canonicalize_labels(P, golden, surf):
+    np.testing.assert_array_equal(P.canonicalize_labels([5, 3, 5, 9, 3]), [0, 1, 0, 2, 1])
     for key in case_names(golden):
         np.testing.assert_array_equal(P.canonicalize_labels(surf[f"{key}/canon_in"]),
                                       surf[f"{key}/canon_out"])
