@@ -448,6 +448,15 @@ template <bool GLOBALT>
 __device__ __forceinline__ int2 tab_load(const int2 *T, uint32_t k) {
     return GLOBALT ? __ldcg(T + k) : T[k];
 }
+// struct-of-arrays shared table (k_sweep_cta2): keys[H], then sums[H]
+struct SoaTab {
+    int32_t *key;
+    uint32_t *sum;
+};
+template <bool GLOBALT>
+__device__ __forceinline__ int2 tab_load(const SoaTab &T, uint32_t k) {
+    return make_int2(T.key[k], (int32_t)T.sum[k]);
+}
 template <bool GLOBALT, class IDX>
 __device__ __forceinline__ uint32_t occ_load(const IDX *occ, uint32_t k) {
     if (GLOBALT) return __ldcg((const unsigned int *)occ + k);
@@ -462,8 +471,8 @@ __device__ __forceinline__ uint32_t tab_size(int64_t d, int f, uint32_t lo) {
 }
 
 // list entries t0, t0 + stride, ... < no: approximate selection, own group
-template <bool SYM, bool GLOBALT, class IDX>
-__device__ __forceinline__ void occ_scan(const SweepArgs<SYM> &A, const int2 *T, const IDX *occ,
+template <bool SYM, bool GLOBALT, class IDX, class TAB>
+__device__ __forceinline__ void occ_scan(const SweepArgs<SYM> &A, const TAB &T, const IDX *occ,
                                          uint32_t no, uint32_t t0, uint32_t stride, int32_t L,
                                          float2 srf, Sel &S, uint32_t &gown, bool &hown) {
     constexpr int U = 4;
@@ -494,8 +503,8 @@ __device__ __forceinline__ void occ_scan(const SweepArgs<SYM> &A, const int2 *T,
 }
 
 // exact fallback: best (t, c) over the listed groups whose upper bound reaches lob
-template <bool SYM, bool GLOBALT, class IDX>
-__device__ __forceinline__ void occ_exact(const SweepArgs<SYM> &A, const int2 *T, const IDX *occ,
+template <bool SYM, bool GLOBALT, class IDX, class TAB>
+__device__ __forceinline__ void occ_exact(const SweepArgs<SYM> &A, const TAB &T, const IDX *occ,
                                           uint32_t no, uint32_t t0, uint32_t stride, int32_t L,
                                           double2 sr, float2 srf, float lob, double &bt,
                                           int32_t &bc) {
@@ -906,8 +915,8 @@ struct BlockSel {
 
 // CTA-wide decision for row r over a filled table T with list occ[0, no) (visible to every
 // thread): writes cstar[r]; no trailing barrier (the caller clears the table and syncs).
-template <int BLOCK, bool SYM, bool GLOBALT, class IDX>
-__device__ __forceinline__ void block_select(const SweepArgs<SYM> &A, const int2 *T, const IDX *occ,
+template <int BLOCK, bool SYM, bool GLOBALT, class IDX, class TAB>
+__device__ __forceinline__ void block_select(const SweepArgs<SYM> &A, const TAB &T, const IDX *occ,
                                              uint32_t no, int32_t r, int32_t L, double2 sr,
                                              BlockSel &B) {
     constexpr int NW = BLOCK / 32;
@@ -1053,6 +1062,169 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_sweep_cta(SweepArgs<SYM> A, con
         occ_clear<false>(ctab, occ, no, threadIdx.x, BLOCK);
         __syncthreads();
         if (threadIdx.x == 0) {   // every thread read s_no / s_ovf before the barriers above
+            s_no = 0;
+            s_ovf = 0;
+        }
+        cur = nxt;
+        nxt = nn;
+    }
+}
+
+// ------------------------------------------------ bins 2-4, bucketed form (default)
+// Same CTA-per-row structure as k_sweep_cta, two changes to the insert:
+//  (1) warp pre-combine: each 32-entry chunk is grouped by community with __match_any_sync
+//      and summed with __reduce_add_sync; only one lane per (chunk, community) touches the
+//      table, so a hub community repeated across a chunk costs one atomic, not one per lane
+//      (same-address shared atomics serialise);
+//  (2) struct-of-arrays table probed by 4-key buckets: one 16-byte load checks 4 slots, so
+//      the probe loop -- which a warp runs until its slowest lane is done -- rarely takes a
+//      second step even at load 0.6.
+__device__ __forceinline__ int4 lds_v4(uint32_t a) {
+    int4 v;
+    asm volatile("ld.volatile.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int32_t cas_s2(uint32_t a, int32_t cmp, int32_t val) {
+    int32_t old;
+    asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "r"(a), "r"(cmp), "r"(val));
+    return old;
+}
+__device__ __forceinline__ void red_add_s2(uint32_t a, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v));
+}
+constexpr uint32_t PROBE_MAX_B = 32;   // buckets (128 slots) before a row overflows
+__device__ __forceinline__ int first_of(int4 k, int32_t x) {
+    return k.x == x ? 0 : k.y == x ? 1 : k.z == x ? 2 : k.w == x ? 3 : -1;
+}
+template <int U>
+__device__ __forceinline__ void insert_chunk_soa(uint32_t ka, uint32_t sa, uint32_t hmask,
+                                                 const int32_t (&c)[U], const uint32_t (&w)[U],
+                                                 uint32_t ob, uint32_t *scnt, int *ovf) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const uint32_t hsh = __clz(hmask);
+    bool lead[U], fr[U];
+    uint32_t g[U], sl[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        const unsigned m = __match_any_sync(0xffffffffu, c[u]);   // invalid lanes: c = -1
+        g[u] = __reduce_add_sync(m, w[u]);
+        lead[u] = c[u] >= 0 && (m & lt) == 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        fr[u] = false;
+        sl[u] = 0;
+        if (lead[u]) {
+            uint32_t b = (((uint32_t)c[u] * 2654435769u) >> hsh) & ~3u;
+            uint32_t p = 0;
+            for (;;) {
+                const int4 k = lds_v4(ka + 4 * b);
+                const int hit = first_of(k, c[u]);
+                if (hit >= 0) {
+                    sl[u] = b + hit;
+                    break;
+                }
+                const int emp = first_of(k, -1);
+                if (emp >= 0) {
+                    const int32_t old = cas_s2(ka + 4 * (b + emp), -1, c[u]);
+                    if (old == -1 || old == c[u]) {
+                        fr[u] = old == -1;
+                        sl[u] = b + emp;
+                        break;
+                    }
+                    continue;   // another key took the slot: read the bucket again
+                }
+                b = (b + 4) & hmask;
+                if (++p == PROBE_MAX_B) {
+                    *ovf = 1;
+                    lead[u] = false;
+                    break;
+                }
+            }
+            if (lead[u]) red_add_s2(sa + 4 * sl[u], g[u]);
+        }
+    }
+    unsigned m[U];
+    uint32_t tot = 0;
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        m[u] = __ballot_sync(0xffffffffu, fr[u]);
+        tot += __popc(m[u]);
+    }
+    if (tot == 0) return;
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(scnt, tot);
+    base = __shfl_sync(0xffffffffu, base, 0);
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        if (fr[u]) sts_u16(ob + 2 * (base + __popc(m[u] & lt)), sl[u]);
+        base += __popc(m[u]);
+    }
+}
+
+template <int BLOCK, int HMAX, int MINB, bool SYM>
+__global__ void __launch_bounds__(BLOCK, MINB) k_sweep_cta2(SweepArgs<SYM> A, const int32_t *rows,
+                                                             int64_t nrows, int32_t *ovf,
+                                                             uint32_t *novf) {
+    extern __shared__ int32_t stab[];
+    int32_t *keys = stab;
+    uint32_t *sums = (uint32_t *)(stab + HMAX);
+    uint16_t *occ = (uint16_t *)(sums + HMAX);
+    const uint32_t ka = smem_addr(keys), sa = smem_addr(sums), oa = smem_addr(occ);
+    const SoaTab T{keys, sums};
+    __shared__ BlockSel B;
+    __shared__ uint32_t s_no;
+    __shared__ int s_ovf;
+    for (int k = threadIdx.x; k < HMAX; k += BLOCK) {
+        keys[k] = -1;
+        sums[k] = 0;
+    }
+    if (threadIdx.x == 0) {
+        B.hown = 0;
+        s_no = 0;
+        s_ovf = 0;
+    }
+    __syncthreads();
+    constexpr int U = 4;
+    const int64_t step = gridDim.x;
+    RowMeta cur = row_meta(A, rows, blockIdx.x, nrows);
+    RowMeta nxt = row_meta(A, rows, blockIdx.x + step, nrows);
+    int32_t z[U];
+    uint32_t wt[U];
+    load_raw<U, BLOCK>(A.unbr + cur.e0, A.u32 + cur.e0, cur.d, threadIdx.x, z, wt);
+    gather_labels<U>(A.label, z, z);
+    for (int64_t i = blockIdx.x; i < nrows; i += step) {
+        const double2 sr = node_s(A, cur.r);
+        const uint32_t H = min(tab_size(cur.d, 2, 32), (uint32_t)HMAX);
+        const int32_t *nb = A.unbr + cur.e0;
+        const uint32_t *ub = A.u32 + cur.e0;
+        insert_chunk_soa<U>(ka, sa, H - 1, z, wt, oa, &s_no, &s_ovf);
+        for (uint32_t cb = BLOCK * U; cb < cur.d; cb += BLOCK * U) {
+            int32_t c[U];
+            uint32_t w2[U];
+            load_row<U, BLOCK>(nb, ub, A.label, cur.d, cb + threadIdx.x, c, w2);
+            insert_chunk_soa<U>(ka, sa, H - 1, c, w2, oa, &s_no, &s_ovf);
+        }
+        __syncthreads();
+        load_raw<U, BLOCK>(A.unbr + nxt.e0, A.u32 + nxt.e0, nxt.d, threadIdx.x, z, wt);
+        const RowMeta nn = row_meta(A, rows, i + 2 * step, nrows);
+        const uint32_t no = s_no;
+        if (s_ovf) {
+            if (threadIdx.x == 0) ovf[atomicAdd(novf, 1u)] = cur.r;
+            if (A.stats && threadIdx.x == 0) atomicAdd(A.stats + 6, 1ull);
+        } else {
+            block_select<BLOCK, SYM, false>(A, T, occ, no, cur.r, cur.L, sr, B);
+        }
+        gather_labels<U>(A.label, z, z);
+        for (uint32_t k = threadIdx.x; k < no; k += BLOCK) {
+            const uint32_t sl = occ[k];
+            keys[sl] = -1;
+            sums[sl] = 0;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
             s_no = 0;
             s_ovf = 0;
         }
@@ -1790,12 +1962,28 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, const int
     }
     int32_t *ovf = ctx->ovf_rows.p;
     uint32_t *novf = ctx->ovf_cnt.p;
-    if (nb(2) && (bin_mask & 4))
-        k2<<<(unsigned)std::min<int64_t>(nb(2), SMS() * 8), 128, SM2, s>>>(A, rows(2), nb(2), ovf, novf);
-    if (nb(3) && (bin_mask & 8))
-        k3<<<(unsigned)std::min<int64_t>(nb(3), SMS() * 4), 256, SM3, s>>>(A, rows(3), nb(3), ovf, novf);
-    if (nb(4) && (bin_mask & 16))
-        k4<<<(unsigned)std::min<int64_t>(nb(4), SMS() * 2), 512, SM4, s>>>(A, rows(4), nb(4), ovf, novf);
+    static const bool cta1 = getenv("SLM_CTA2") && atoi(getenv("SLM_CTA2")) == 0;
+    if (cta1) {
+        if (nb(2) && (bin_mask & 4))
+            k2<<<(unsigned)std::min<int64_t>(nb(2), SMS() * 8), 128, SM2, s>>>(A, rows(2), nb(2), ovf, novf);
+        if (nb(3) && (bin_mask & 8))
+            k3<<<(unsigned)std::min<int64_t>(nb(3), SMS() * 4), 256, SM3, s>>>(A, rows(3), nb(3), ovf, novf);
+        if (nb(4) && (bin_mask & 16))
+            k4<<<(unsigned)std::min<int64_t>(nb(4), SMS() * 2), 512, SM4, s>>>(A, rows(4), nb(4), ovf, novf);
+    } else {
+        auto c2 = k_sweep_cta2<128, 2048, 8, SYM>;
+        auto c3 = k_sweep_cta2<256, 2048, 4, SYM>;
+        auto c4 = k_sweep_cta2<512, 8192, 2, SYM>;
+        set_smem(c2, SM2);
+        set_smem(c3, SM3);
+        set_smem(c4, SM4);
+        if (nb(2) && (bin_mask & 4))
+            c2<<<(unsigned)std::min<int64_t>(nb(2), SMS() * 8), 128, SM2, s>>>(A, rows(2), nb(2), ovf, novf);
+        if (nb(3) && (bin_mask & 8))
+            c3<<<(unsigned)std::min<int64_t>(nb(3), SMS() * 4), 256, SM3, s>>>(A, rows(3), nb(3), ovf, novf);
+        if (nb(4) && (bin_mask & 16))
+            c4<<<(unsigned)std::min<int64_t>(nb(4), SMS() * 2), 512, SM4, s>>>(A, rows(4), nb(4), ovf, novf);
+    }
     if (bin_mask & 28) {
         if (ctx->ovf_tab.n < (size_t)OVF_GRID * OVF_H) {
             ctx->ovf_tab.resize((size_t)OVF_GRID * OVF_H);
