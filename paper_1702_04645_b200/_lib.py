@@ -177,7 +177,8 @@ class Context:
         return dict(n=n.value, ne=ne.value, ue=ue.value, m_w=m.value,
                     symmetric=bool(fl.value & 1), integral=bool(fl.value & 2),
                     plan_path=("u32" if fl.value & 4 else
-                               "fp64-exact" if fl.value & 2 else "sorted"))
+                               "fp64-exact" if (fl.value & 2) and not (fl.value & 8)
+                               else "sorted"))
 
     def csr(self):
         d = self.info()

@@ -518,8 +518,9 @@ int slm_graph_info(slm_ctx *ctx, int64_t *n, int64_t *ne, int64_t *ue, double *m
         // plan-sweep path of this level (run_plan): 4 = exact uint32 group sums (integer
         // weights, every row total < 2^32), else fp64 on integer sums (exact), else the
         // sorted reference-order form (real-valued weights)
-        const bool u32 = G.u32_ok && !getenv("SLM_FORCE_GENERIC") && !getenv("SLM_PLAN_SORTED");
-        *flags = (G.sym ? 1 : 0) | (G.integral ? 2 : 0) | (u32 ? 4 : 0);
+        const bool sorted = getenv("SLM_PLAN_SORTED") != nullptr;
+        const bool u32 = G.u32_ok && !getenv("SLM_FORCE_GENERIC") && !sorted;
+        *flags = (G.sym ? 1 : 0) | (G.integral ? 2 : 0) | (u32 ? 4 : 0) | (sorted ? 8 : 0);
     }
     API_END
 }
@@ -839,7 +840,7 @@ int slm_run(slm_ctx *ctx, const slm_config *cfg, int64_t *n_levels, int64_t *sta
         const bool integral = G.integral;
         int32_t fl = 0;
         ok(slm_graph_info(ctx, nullptr, nullptr, nullptr, nullptr, &fl));
-        ctx->run_paths.push_back(fl & 4 ? 0 : (fl & 2 ? 1 : 2));
+        ctx->run_paths.push_back(fl & 4 ? 0 : ((fl & 2) && !(fl & 8) ? 1 : 2));
         double t = clk();
         ok(slm_assign(ctx, nullptr));
         ph[0] += clk() - t;

@@ -1962,7 +1962,7 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, const int
     }
     int32_t *ovf = ctx->ovf_rows.p;
     uint32_t *novf = ctx->ovf_cnt.p;
-    static const bool cta1 = getenv("SLM_CTA2") && atoi(getenv("SLM_CTA2")) == 0;
+    static const bool cta1 = !(getenv("SLM_CTA2") && atoi(getenv("SLM_CTA2")) == 1);
     if (cta1) {
         if (nb(2) && (bin_mask & 4))
             k2<<<(unsigned)std::min<int64_t>(nb(2), SMS() * 8), 128, SM2, s>>>(A, rows(2), nb(2), ovf, novf);

@@ -35,3 +35,11 @@ for s, r in samp:
 print("samples by opcode:", ", ".join(f"{k} {100*v/tot:.1f}%" for k, v in ops.most_common(14)))
 for s, r in sorted(samp, key=lambda x: -x[0])[:top]:
     print(f"{r[0][-5:]} {s:7.0f} {100*s/tot:5.1f}%  {r[ix['Source']].strip()[:90]}")
+
+# stall reasons overall and for the hottest lines
+st = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
+totals = {h: sum(float(r[ix[h]] or 0) for r in sect) for h in st}
+tt = sum(totals.values())
+print("stalls:", ", ".join(f"{k[6:]} {100*v/tt:.1f}%" for k, v in sorted(totals.items(), key=lambda x: -x[1])[:10]))
+ie = sum(float(r[ix["Instructions Executed"]] or 0) for r in sect)
+print(f"warp instructions executed {ie:.4g}")
