@@ -198,6 +198,15 @@ SLM_API int slm_last_commit_stats(slm_ctx *ctx, int64_t *candidates, int64_t *ro
 SLM_API int slm_build_rmat(slm_ctx *ctx, int scale, int edge_factor, double a, double b, double c,
                    uint64_t seed, int weight_mode);
 SLM_API int slm_build_rgg(slm_ctx *ctx, int64_t n, double radius, uint64_t seed);
+/* Pair-model graphs generated in HBM, one Bernoulli draw per node pair i < j (both
+ * directions, unit weights): mode 0 = planted-partition SBM (blocks of n / blocks
+ * consecutive ids, p_in / p_out); mode 1 = Chung-Lu DC-SBM over per-node parameters
+ * (community comm[i], kin[i], kout[i], per-community K, total O; p = min(1, kin_i kin_j / K_c)
+ * inside a community, min(1, kout_i kout_j / O) across).  Host twin: workloads/gen_host.c. */
+SLM_API int slm_build_pairs(slm_ctx *ctx, int32_t mode, int64_t n, int64_t blocks, double p_in,
+                            double p_out, const int32_t *comm, const double *kin,
+                            const double *kout, const double *K, int64_t n_comms, double O,
+                            uint64_t seed);
 
 #ifdef __cplusplus
 }

@@ -82,6 +82,8 @@ SIGNATURES = {
     "slm_build_rmat": (C.c_int, [_VP, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                  C.c_uint64, C.c_int]),
     "slm_build_rgg": (C.c_int, [_VP, _I64, C.c_double, C.c_uint64]),
+    "slm_build_pairs": (C.c_int, [_VP, C.c_int32, _I64, _I64, C.c_double, C.c_double, _VP, _VP,
+                                  _VP, _VP, _I64, C.c_double, C.c_uint64]),
 }
 
 _lib = None
@@ -167,6 +169,19 @@ class Context:
 
     def build_rgg(self, n, radius, seed):
         self.call("slm_build_rgg", int(n), float(radius), int(seed))
+        self.level = 0
+
+    def build_pairs(self, mode, n, blocks=0, p_in=0.0, p_out=0.0, params=None, seed=0):
+        if params is None:
+            comm = kin = kout = K = None
+            O, nc = 1.0, 0
+        else:
+            comm, kin, kout, K, O = params
+            comm = np.ascontiguousarray(comm, np.int32)
+            kin, kout, K = f64(kin), f64(kout), f64(K)
+            nc = K.size
+        self.call("slm_build_pairs", int(mode), int(n), int(blocks), float(p_in), float(p_out),
+                  ptr(comm), ptr(kin), ptr(kout), ptr(K), int(nc), float(O), int(seed))
         self.level = 0
 
     def info(self):

@@ -505,6 +505,37 @@ int slm_build_rgg(slm_ctx *ctx, int64_t n, double radius, uint64_t seed) {
     API_END
 }
 
+int slm_build_pairs(slm_ctx *ctx, int32_t mode, int64_t n, int64_t blocks, double p_in,
+                    double p_out, const int32_t *comm, const double *kin, const double *kout,
+                    const double *K, int64_t n_comms, double O, uint64_t seed) {
+    API_BEGIN
+    SLM_REQUIRE(n >= 0 && n < (int64_t(1) << 31) && (mode == 0 || mode == 1), SLM_EINVAL,
+                "bad pair-model arguments");
+    SLM_REQUIRE(mode == 0 || (comm && kin && kout && K && n_comms > 0), SLM_EINVAL,
+                "DC-SBM needs comm, kin, kout, K");
+    cudaSetDevice(ctx->device);
+    new_level0(ctx);
+    DBuf<int32_t> dc;
+    DBuf<double> dki, dko, dK;
+    if (mode == 1) {
+        dc.resize(n);
+        dki.resize(n);
+        dko.resize(n);
+        dK.resize(n_comms);
+        CUDA_TRY(cudaMemcpyAsync(dc.p, comm, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(dki.p, kin, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(dko.p, kout, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(dK.p, K, n_comms * 8, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    const PairArgs P = make_pair_args(mode, n, blocks, p_in, p_out, dc.p, dki.p, dko.p, dK.p, O, seed);
+    DBuf<int32_t> src, dst;
+    DBuf<double> w;
+    int64_t ne = 0;
+    gen_pairs_device(ctx, P, src, dst, w, ne);
+    build_level_from_edges(ctx, *ctx->g, n, src.p, dst.p, w.p, ne);
+    API_END
+}
+
 int slm_graph_info(slm_ctx *ctx, int64_t *n, int64_t *ne, int64_t *ue, double *m_w,
                    int32_t *flags) {
     API_BEGIN

@@ -208,5 +208,82 @@ void gen_rgg_device(slm_ctx *ctx, int64_t n, double radius, uint64_t seed, DBuf<
     CUDA_TRY(cudaGetLastError());
 }
 
+// ---------------------------------------------------------------- pair models
+// Planted-partition SBM (mode 0) and Chung-Lu DC-SBM (mode 1): one Bernoulli draw per node
+// pair i < j, u = unit(fin(base + (i n + j) GAMMA)) < p_ij, both directions emitted
+// (workloads/gen_host.c gen_pairs is the host twin; p_ij uses only * / min, so both sides
+// draw the identical edge set).  One warp per row i, lanes over j: count, scan, fill.
+__device__ __forceinline__ bool pair_hit(const PairArgs &P, int64_t i, int64_t j) {
+    double p;
+    if (P.mode == 0) {
+        p = (i / P.bs == j / P.bs) ? P.p_in : P.p_out;
+    } else {
+        p = (P.comm[i] == P.comm[j]) ? __ddiv_rn(__dmul_rn(P.kin[i], P.kin[j]), P.K[P.comm[i]])
+                                     : __ddiv_rn(__dmul_rn(P.kout[i], P.kout[j]), P.O);
+        p = p < 1.0 ? p : 1.0;
+    }
+    return u01_of(fin64(P.base + (uint64_t)(i * P.n + j) * RNG_GAMMA)) < p;
+}
+__global__ void k_pairs(PairArgs P, int64_t *cnt, const int64_t *pos, int32_t *src, int32_t *dst,
+                        double *w) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int64_t i = w0; i < P.n; i += nw) {
+        int64_t k = pos ? pos[i] : 0;
+        for (int64_t j0 = i + 1; j0 < P.n; j0 += 32) {
+            const int64_t j = j0 + lane;
+            const bool hit = j < P.n && pair_hit(P, i, j);
+            const unsigned m = __ballot_sync(0xffffffffu, hit);
+            if (pos && hit) {
+                const int64_t q = 2 * (k + __popc(m & lt));
+                src[q] = (int32_t)i; dst[q] = (int32_t)j; w[q] = 1.0;
+                src[q + 1] = (int32_t)j; dst[q + 1] = (int32_t)i; w[q + 1] = 1.0;
+            }
+            k += __popc(m);
+        }
+        if (!pos && lane == 0) cnt[i] = k;
+    }
+}
+
+void gen_pairs_device(slm_ctx *ctx, const PairArgs &P, DBuf<int32_t> &src, DBuf<int32_t> &dst,
+                      DBuf<double> &w, int64_t &ne) {
+    cudaStream_t s = ctx->stream;
+    DBuf<int64_t> cnt, pos;
+    cnt.resize(P.n + 1);
+    pos.resize(P.n + 1);
+    CUDA_TRY(cudaMemsetAsync(cnt.p + P.n, 0, 8, s));
+    if (P.n) k_pairs<<<grid_for(P.n * 32, 256), 256, 0, s>>>(P, cnt.p, nullptr, nullptr, nullptr, nullptr);
+    dev_exclusive_sum<int64_t, int64_t>(ctx, cnt.p, pos.p, P.n + 1);
+    int64_t pairs = 0;
+    CUDA_TRY(cudaMemcpyAsync(&pairs, pos.p + P.n, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    ne = 2 * pairs;
+    src.resize(ne);
+    dst.resize(ne);
+    w.resize(ne);
+    if (P.n) k_pairs<<<grid_for(P.n * 32, 256), 256, 0, s>>>(P, nullptr, pos.p, src.p, dst.p, w.p);
+    CUDA_TRY(cudaGetLastError());
+}
+
+PairArgs make_pair_args(int mode, int64_t n, int64_t blocks, double p_in, double p_out,
+                        const int32_t *d_comm, const double *d_kin, const double *d_kout,
+                        const double *d_K, double O, uint64_t seed) {
+    PairArgs P;
+    P.mode = mode;
+    P.n = n;
+    P.bs = blocks > 0 ? std::max<int64_t>(1, n / blocks) : 1;
+    P.p_in = p_in;
+    P.p_out = p_out;
+    P.O = O;
+    P.comm = d_comm;
+    P.kin = d_kin;
+    P.kout = d_kout;
+    P.K = d_K;
+    P.base = gen_base(seed);
+    return P;
+}
+
 // a kernel of this translation unit (module preloading, slm_capi.cu preload_modules)
 const void *slm_anchor_gen() { return (const void *)k_rmat_count; }

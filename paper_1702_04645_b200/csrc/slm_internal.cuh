@@ -409,6 +409,21 @@ void run_aggregate(slm_ctx *ctx, const LevelGraph &G, const int32_t *d_labels, i
 double run_score(slm_ctx *ctx, const LevelGraph &G, const int32_t *d_labels, double gamma);
 void forest_refresh(slm_ctx *ctx, const LevelGraph &G, Forest &F);   // comps + agg + layout
 
+// slm_gen.cu: pair-model generators (SBM / DC-SBM), one Bernoulli draw per node pair
+struct PairArgs {
+    int mode;
+    int64_t n, bs;
+    double p_in, p_out, O;
+    const int32_t *comm;
+    const double *kin, *kout, *K;
+    uint64_t base;
+};
+PairArgs make_pair_args(int mode, int64_t n, int64_t blocks, double p_in, double p_out,
+                        const int32_t *d_comm, const double *d_kin, const double *d_kout,
+                        const double *d_K, double O, uint64_t seed);
+void gen_pairs_device(slm_ctx *ctx, const PairArgs &P, DBuf<int32_t> &src, DBuf<int32_t> &dst,
+                      DBuf<double> &w, int64_t &ne);
+
 // slm_prim.cu: single-pass decoupled look-back scans and the onesweep LSD radix sort
 template <class TI, class TO>
 void dev_exclusive_sum(slm_ctx *ctx, const TI *in, TO *out, int64_t n);

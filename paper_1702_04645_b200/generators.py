@@ -1,4 +1,5 @@
-"""Device generation of the BASELINE.json synthetic graphs straight into the level-0 build.
+"""Device generation of the BASELINE.json synthetic graphs straight into the level-0 build
+(R-MAT, RGG, and the pair-model SBM / DC-SBM twins of C1 / C2).
 
 The counter-based R-MAT (C3, C5) and RGG (C4) generators run in HBM (libslm
 ``slm_build_rmat`` / ``slm_build_rgg``), so the bench never moves the 1e9-entry edge list
@@ -32,6 +33,19 @@ def rgg_device(ctx: _lib.Context, n, avg_deg=8.0, seed=0):
     ctx.build_rgg(n, rgg_radius(n, avg_deg), seed)
 
 
+def sbm_device(ctx: _lib.Context, n, blocks, p_in, p_out, seed=0):
+    """Planted-partition SBM drawn in HBM: one counter-hash Bernoulli draw per node pair
+    (slm_build_pairs mode 0), blocks of n / blocks consecutive ids."""
+    ctx.build_pairs(0, n, blocks, p_in, p_out, seed=seed)
+
+
+def dcsbm_device(ctx: _lib.Context, params, seed=1):
+    """Chung-Lu DC-SBM drawn in HBM (slm_build_pairs mode 1) over per-node parameters
+    params = (comm, kin, kout, K, O) -- the O(n) parameters are host-side input, the O(n^2)
+    pair draws run on the device."""
+    ctx.build_pairs(1, len(params[0]), params=params, seed=seed)
+
+
 def build_on_device(ctx: _lib.Context, spec: dict, edges=None):
     """Build a config described by ``spec`` (workloads.CONFIGS entry) as level 0 of ``ctx``:
     device-generated for R-MAT / RGG, from the host ``edges`` (n, src, dst, w) otherwise."""
@@ -40,6 +54,10 @@ def build_on_device(ctx: _lib.Context, spec: dict, edges=None):
         rmat_device(ctx, spec["scale"], spec["edge_factor"], spec["weight_mode"], spec["seed"])
     elif kind == "rgg":
         rgg_device(ctx, spec["n"], spec["avg_deg"], spec["seed"])
+    elif kind == "sbm_hash":
+        sbm_device(ctx, spec["n"], spec["blocks"], spec["p_in"], spec["p_out"], spec["seed"])
+    elif kind == "dcsbm_hash" and edges is not None and len(edges) == 5:
+        dcsbm_device(ctx, edges, spec["seed"])   # edges = the pair-model parameters
     else:
         if edges is None:
             raise ValueError(f"config kind {kind!r} needs host edges")

@@ -34,6 +34,9 @@ CONFIGS = {
     "c3_rmat22": dict(kind="rmat", scale=22, edge_factor=16, weight_mode=0, seed=2),
     "c4_rgg24": dict(kind="rgg", n=1 << 24, avg_deg=8.0, seed=3),
     "c5_rmat24": dict(kind="rmat", scale=24, edge_factor=32, weight_mode=1, seed=4),
+    # device-generated pair-model twins of C1 / C2 (counter hashes instead of numpy's PCG64)
+    "c1_sbm_hash": dict(kind="sbm_hash", n=1000, blocks=10, p_in=0.10, p_out=0.005, seed=0),
+    "c2_dcsbm_hash": dict(kind="dcsbm_hash", n=100_000, k=200, seed=1),
 }
 
 
@@ -57,6 +60,9 @@ def _L():
         L.gen_rmat.restype = C.c_int64
         L.gen_rmat.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                C.c_uint64, C.c_int, vp, vp, vp]
+        L.gen_pairs.restype = C.c_int64
+        L.gen_pairs.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_double, C.c_double, vp, vp,
+                                vp, vp, C.c_double, C.c_uint64, vp, vp, vp]
         L.gen_rgg.restype = C.c_int64
         L.gen_rgg.argtypes = [C.c_int64, C.c_double, C.c_uint64, vp, vp, vp]
         _lib = L
@@ -172,6 +178,48 @@ def rgg(n, avg_deg=8.0, seed=0):
     return n, src, dst, w
 
 
+def dcsbm_params(n=100_000, k=200, size_lo=100, size_hi=1000, size_exp=1.0, deg_lo=5.0,
+                 deg_hi=200.0, deg_exp=2.5, mu=0.3, seed=1):
+    """Per-node parameters of the pair-model DC-SBM (C2's shape): community of every node
+    (consecutive blocks of power-law sizes renormalised to n), kin = (1-mu) theta,
+    kout = mu theta (theta power law on [deg_lo, deg_hi]), K per community, O."""
+    rng = np.random.default_rng(seed)
+    raw = _powerlaw(rng, k, size_lo, size_hi, size_exp)
+    exact = raw / raw.sum() * n
+    sizes = np.floor(exact).astype(np.int64)
+    sizes[np.argsort(-(exact - sizes), kind="stable")[:n - int(sizes.sum())]] += 1
+    comm = np.repeat(np.arange(k, dtype=np.int32), sizes)
+    theta = _powerlaw(rng, n, deg_lo, deg_hi, deg_exp)
+    kin = (1.0 - mu) * theta
+    kout = mu * theta
+    K = np.bincount(comm, weights=kin, minlength=k)
+    return comm, kin, kout, K, float(kout.sum())
+
+
+def _pairs(mode, n, blocks, p_in, p_out, params, seed):
+    L = _L()
+    comm, kin, kout, K, O = params if params is not None else (None,) * 4 + (1.0,)
+    arrs = [None if a is None else np.ascontiguousarray(a) for a in (comm, kin, kout, K)]
+    ptrs = [None if a is None else _p(a) for a in arrs]
+    k = L.gen_pairs(mode, n, blocks, p_in, p_out, *ptrs, O, seed, None, None, None)
+    src = np.empty(k, np.int64)
+    dst = np.empty(k, np.int64)
+    w = np.empty(k, np.float64)
+    L.gen_pairs(mode, n, blocks, p_in, p_out, *ptrs, O, seed, _p(src), _p(dst), _p(w))
+    return n, src, dst, w
+
+
+def sbm_hash(n=1000, blocks=10, p_in=0.10, p_out=0.005, seed=0):
+    """Counter-hash planted partition (host twin of the device generator slm_build_pairs)."""
+    return _pairs(0, n, blocks, p_in, p_out, None, seed)
+
+
+def dcsbm_hash(seed=1, **kw):
+    """Counter-hash DC-SBM over dcsbm_params (host twin of slm_build_pairs, mode 1)."""
+    params = dcsbm_params(seed=seed, **kw)
+    return _pairs(1, params[0].size, 0, 0.0, 0.0, params, seed)
+
+
 def generate(name, **over):
     """Host edge list (n, src, dst, w) of a named config (overrides allowed)."""
     spec = dict(CONFIGS[name])
@@ -185,4 +233,8 @@ def generate(name, **over):
         return rmat(spec["scale"], spec["edge_factor"], spec["weight_mode"], spec["seed"])
     if kind == "rgg":
         return rgg(spec["n"], spec["avg_deg"], spec["seed"])
+    if kind == "sbm_hash":
+        return sbm_hash(**spec)
+    if kind == "dcsbm_hash":
+        return dcsbm_hash(**spec)
     raise KeyError(name)

@@ -170,3 +170,54 @@ EXPORT int64_t gen_rgg(int64_t n, double radius, uint64_t seed, int64_t *src, in
     free(X); free(Y); free(cell); free(cptr); free(pts); free(deg);
     return total;
 }
+
+/* ---------------------------------------------------------------- pair models
+ * Planted-partition SBM and degree-corrected (Chung-Lu) SBM by one Bernoulli draw per node
+ * pair i < j: edge iff unit(fin(base + (i * n + j) * GAMMA)) < p_ij, both directions.
+ *   mode 0 (SBM):  p_ij = p_in if i / bs == j / bs else p_out  (bs = n / blocks)
+ *   mode 1 (DC-SBM): p_ij = min(1, kin_i kin_j / K[c_i]) if c_i == c_j
+ *                    else min(1, kout_i kout_j / O)
+ * Only IEEE-exact operations (* / < min) touch the per-node parameters, so the device twin
+ * (libslm slm_build_pairs) draws the identical edge set. */
+static inline double pair_p(int mode, int64_t i, int64_t j, int64_t bs, double p_in, double p_out,
+                            const int32_t *comm, const double *kin, const double *kout,
+                            const double *K, double O) {
+    if (mode == 0) return (i / bs == j / bs) ? p_in : p_out;
+    double p = (comm[i] == comm[j]) ? (kin[i] * kin[j]) / K[comm[i]] : (kout[i] * kout[j]) / O;
+    return p < 1.0 ? p : 1.0;
+}
+
+EXPORT int64_t gen_pairs(int mode, int64_t n, int64_t blocks, double p_in, double p_out,
+                         const int32_t *comm, const double *kin, const double *kout,
+                         const double *K, double O, uint64_t seed, int64_t *src, int64_t *dst,
+                         double *w) {
+    const uint64_t base = base_of(seed);
+    const int64_t bs = blocks > 0 ? (n / blocks > 0 ? n / blocks : 1) : 1;
+    int64_t *cnt = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+    for (int pass = 0; pass < 2; pass++) {
+        if (pass == 1) {
+            if (!src) break;
+            for (int64_t i = 0; i < n; i++) cnt[i + 1] += cnt[i];
+        }
+#pragma omp parallel for schedule(dynamic, 64)
+        for (int64_t i = 0; i < n; i++) {
+            int64_t k = pass ? cnt[i] : 0;
+            for (int64_t j = i + 1; j < n; j++) {
+                const double u = unit(fin(base + (uint64_t)(i * n + j) * GAMMA64));
+                if (u < pair_p(mode, i, j, bs, p_in, p_out, comm, kin, kout, K, O)) {
+                    if (pass) {
+                        src[2 * k] = i; dst[2 * k] = j; w[2 * k] = 1.0;
+                        src[2 * k + 1] = j; dst[2 * k + 1] = i; w[2 * k + 1] = 1.0;
+                    }
+                    k++;
+                }
+            }
+            if (!pass) cnt[i + 1] = k;
+        }
+    }
+    int64_t total = 0;
+    if (src) total = 2 * cnt[n];
+    else for (int64_t i = 0; i < n; i++) total += 2 * cnt[i + 1];
+    free(cnt);
+    return total;
+}
