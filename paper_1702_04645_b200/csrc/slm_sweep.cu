@@ -614,30 +614,65 @@ __device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
 // (scnt: shared counter; else the warp-private register counter rcnt).  BOUNDED: give up
 // after PROBE_MAX probes and set *ovf (the row is redone by the overflow kernel).
 constexpr uint32_t PROBE_MAX = 128;
+// predicated shared-memory atomics: no branch, so a warp whose lanes take different paths
+// (hit / claim an empty slot / nothing to do) stays converged
+__device__ __forceinline__ void cas_pred(uint32_t a, bool p, int32_t val, int32_t &old) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+                 "@q atom.shared.cas.b32 %0, [%1], -1, %3;\n\t}"
+                 : "+r"(old) : "r"(a), "r"((int)p), "r"(val) : "memory");
+}
+__device__ __forceinline__ void red_pred(uint32_t a, bool p, uint32_t v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t"
+                 "@q red.shared.add.u32 [%0], %2;\n\t}" ::"r"(a), "r"((int)p), "r"(v) : "memory");
+}
+
+// Insert.  First probe of all U entries without branches: U independent loads, then per
+// entry one predicated CAS (when the slot is empty) and one predicated add (when the slot
+// holds, or now holds, the community).  Entries whose first slot belongs to another
+// community (a minority at load <= 1/2) continue in the linear-probing loop.
 template <int U, bool BOUNDED>
 __device__ __forceinline__ void insert_chunk(uint32_t tb, uint32_t hmask, const int32_t (&c)[U],
                                              const uint32_t (&w)[U], uint32_t ob, uint32_t *scnt,
                                              uint32_t &rcnt, int *ovf) {
     const int lane = threadIdx.x & 31;
     const uint32_t hsh = __clz(hmask);
-    bool fr[U];
+    bool fr[U], pend[U];
     uint32_t sl[U];
+    int32_t k[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
-        fr[u] = false;
         sl[u] = ((uint32_t)c[u] * 2654435769u) >> hsh;
-        if (c[u] >= 0) {
-            uint32_t p = 0;
+        k[u] = c[u] >= 0 ? lds_vol(tb + sl[u] * 8) : 0;
+    }
+    bool anyp = false;
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        const bool valid = c[u] >= 0;
+        const bool emp = valid && k[u] == -1;
+        int32_t old = k[u];
+        cas_pred(tb + sl[u] * 8, emp, c[u], old);
+        fr[u] = emp && old == -1;
+        const bool got = valid && (old == c[u] || fr[u]);
+        red_pred(tb + sl[u] * 8 + 4, got, w[u]);
+        pend[u] = valid && !got;
+        anyp |= pend[u];
+    }
+    if (__any_sync(0xffffffffu, anyp)) {
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            if (!pend[u]) continue;
+            sl[u] = (sl[u] + 1) & hmask;
+            uint32_t p = 1;
             for (;;) {
-                int32_t k = lds_vol(tb + sl[u] * 8);
-                if (k == c[u]) break;
-                if (k == -1) {
-                    k = cas_s(tb + sl[u] * 8, -1, c[u]);
-                    if (k == -1) {
+                int32_t kk = lds_vol(tb + sl[u] * 8);
+                if (kk == c[u]) break;
+                if (kk == -1) {
+                    kk = cas_s(tb + sl[u] * 8, -1, c[u]);
+                    if (kk == -1) {
                         fr[u] = true;
                         break;
                     }
-                    if (k == c[u]) break;
+                    if (kk == c[u]) break;
                 }
                 sl[u] = (sl[u] + 1) & hmask;
                 if (BOUNDED && ++p == PROBE_MAX) {
