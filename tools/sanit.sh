@@ -1,4 +1,17 @@
-# memcheck of the sweep path on a mid-size R-MAT, and which sweep kernel fails under ncu replay
-cd /root/repo
-timeout 900 compute-sanitizer --tool memcheck --print-limit 5 python bench.py --steps 1 --warmup 3 --no-cpu --no-partition --scale 18 > gpurun_out/sanit.log 2>&1; echo SAN $?; grep -E "ERROR SUMMARY|Invalid|at 0x|by thread" gpurun_out/sanit.log | head -12
-timeout 600 ncu --clock-control none --profile-from-start off -k regex:"k_sweep_warp|k_sweep_half|k_sweep_cta" -c 6 --metrics gpu__time_duration.sum python bench.py --steps 1 --warmup 3 --no-cpu --no-partition > gpurun_out/ncu_k.log 2>&1; echo NCU $?; grep -E "Profiling|ERROR" gpurun_out/ncu_k.log | head
+# compute-sanitizer evidence on small configs (profiles/r02_sanitizer_*.log): memcheck of a
+# full level loop (every phase: build, ASSIGN, COMPONENTS, POSITIVE, MAXIMAL with the
+# persistent commit walkers, AGGREGATE, score) and of the plan sweep / primitives;
+# racecheck / synccheck of the same run (shared-memory hazards in the table kernels).
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+cat > /tmp/san_run.py <<'PY'
+import sys; sys.path.insert(0, ".")
+import numpy as np, workloads as W, paper_1702_04645_b200 as P
+for n, s, d, w in (W.rmat(11, 8, 1, 4), W.rgg(4096, 8.0, 3), W.generate("c1_sbm")):
+    r = P.run(P.Graph.from_edges(n, s, d, w), P.RunConfig())
+    print(n, r.stats.sweeps_per_level, r.final_score)
+PY
+for tool in memcheck racecheck synccheck initcheck; do
+  timeout 1500 compute-sanitizer --tool $tool --print-limit 20 python /tmp/san_run.py > gpurun_out/sanit_$tool.log 2>&1
+  echo "$tool rc=$?" >> gpurun_out/sanit_$tool.log
+done
