@@ -457,10 +457,8 @@ template <bool GLOBALT>
 __device__ __forceinline__ int2 tab_load(const SoaTab &T, uint32_t k) {
     return make_int2(T.key[k], (int32_t)T.sum[k]);
 }
-// occ == nullptr: a dense table, scanned slot by slot (k is the slot; empty slots skipped)
 template <bool GLOBALT, class IDX>
 __device__ __forceinline__ uint32_t occ_load(const IDX *occ, uint32_t k) {
-    if (!occ) return k;
     if (GLOBALT) return __ldcg((const unsigned int *)occ + k);
     return occ[k];
 }
@@ -512,7 +510,7 @@ __device__ __forceinline__ void occ_exact(const SweepArgs<SYM> &A, const TAB &T,
                                           int32_t &bc) {
     for (uint32_t k = t0; k < no; k += stride) {
         const int2 e = tab_load<GLOBALT>(T, occ_load<GLOBALT>(occ, k));
-        if (e.x < 0 || e.x == L) continue;
+        if (e.x == L) continue;
         float lo;
         const float up = approx_up((uint32_t)e.y, comm_Sf(A, e.x), srf, A.inv_mf, A.inv_m2f, lo);
         if (up < lob) continue;
@@ -616,7 +614,6 @@ __device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
 // (scnt: shared counter; else the warp-private register counter rcnt).  BOUNDED: give up
 // after PROBE_MAX probes and set *ovf (the row is redone by the overflow kernel).
 constexpr uint32_t PROBE_MAX = 128;
-constexpr uint32_t DENSE_TAB = 0xFFFFFFFFu;   // list address sentinel: no occupied-slot list
 // predicated shared-memory atomics: no branch, so a warp whose lanes take different paths
 // (hit / claim an empty slot / nothing to do) stays converged
 __device__ __forceinline__ void cas_pred(uint32_t a, bool p, int32_t val, int32_t &old) {
@@ -686,11 +683,6 @@ __device__ __forceinline__ void insert_chunk(uint32_t tb, uint32_t hmask, const 
             red_add_s(tb + sl[u] * 8 + 4, w[u]);   // (after a failed probe: a stray add to a
                                                     //  slot of a row that is redone anyway)
         }
-    }
-    if (ob == DENSE_TAB) {   // dense table: no slot list, count this lane's fresh groups
-#pragma unroll
-        for (int u = 0; u < U; u++) rcnt += fr[u] ? 1u : 0u;
-        return;
     }
     unsigned m[U];
     uint32_t tot = 0;
@@ -961,8 +953,7 @@ struct BlockSel {
 template <int BLOCK, bool SYM, bool GLOBALT, class IDX, class TAB>
 __device__ __forceinline__ void block_select(const SweepArgs<SYM> &A, const TAB &T, const IDX *occ,
                                              uint32_t no, int32_t r, int32_t L, double2 sr,
-                                             BlockSel &B, uint32_t ngroups = 0xFFFFFFFFu) {
-    if (ngroups == 0xFFFFFFFFu) ngroups = no;
+                                             BlockSel &B) {
     constexpr int NW = BLOCK / 32;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const float2 srf = make_float2((float)sr.x, (float)sr.y);
@@ -983,7 +974,7 @@ __device__ __forceinline__ void block_select(const SweepArgs<SYM> &A, const TAB 
     if (lane == 0) B.cnt[wid] = cnt;
     __syncthreads();
     cnt = __reduce_add_sync(0xffffffffu, lane < NW ? B.cnt[lane] : 0u);
-    if (A.groups && threadIdx.x == 0) atomicAdd(A.groups, (unsigned long long)ngroups);
+    if (A.groups && threadIdx.x == 0) atomicAdd(A.groups, (unsigned long long)no);
     if (A.wown && threadIdx.x == 0) A.wown[r] = B.hown ? B.gown : 0u;
     if (lo == -INFINITY) {
         if (threadIdx.x == 0) {
@@ -1082,22 +1073,14 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_sweep_cta(SweepArgs<SYM> A, con
         const uint32_t H = min(tab_size(cur.d, F, 32), (uint32_t)HMAX);
         const int32_t *nb = A.unbr + cur.e0;
         const uint32_t *ub = A.u32 + cur.e0;
-        // dense rows (H <= 4 d): no occupied-slot list; the selection and the clear walk all
-        // H slots, which costs less than appending every fresh group to a list
-        const bool dense = H <= 4 * cur.d;
-        const uint32_t ob = dense ? DENSE_TAB : osa;
-        uint32_t nfresh = 0;
+        uint32_t unused = 0;
         // z holds the first chunk's communities (gathered at the end of the previous row)
-        insert_chunk<U, true>(tsa, H - 1, z, wt, ob, &s_no, nfresh, &s_ovf);
+        insert_chunk<U, true>(tsa, H - 1, z, wt, osa, &s_no, unused, &s_ovf);
         for (uint32_t cb = BLOCK * U; cb < cur.d; cb += BLOCK * U) {
             int32_t c[U];
             uint32_t w2[U];
             load_row<U, BLOCK>(nb, ub, A.label, cur.d, cb + threadIdx.x, c, w2);
-            insert_chunk<U, true>(tsa, H - 1, c, w2, ob, &s_no, nfresh, &s_ovf);
-        }
-        if (dense && A.groups) {   // group count (only the bench's G query asks for it)
-            const uint32_t wsum = __reduce_add_sync(0xffffffffu, nfresh);
-            if ((threadIdx.x & 31) == 0 && wsum) atomicAdd(&s_no, wsum);
+            insert_chunk<U, true>(tsa, H - 1, c, w2, osa, &s_no, unused, &s_ovf);
         }
         __syncthreads();
         // prefetch: next row's first chunk, the metadata of the row after it
@@ -1107,19 +1090,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_sweep_cta(SweepArgs<SYM> A, con
         if (s_ovf) {
             if (threadIdx.x == 0) ovf[atomicAdd(novf, 1u)] = cur.r;
             if (A.stats && threadIdx.x == 0) atomicAdd(A.stats + 6, 1ull);
-        } else if (dense) {
-            block_select<BLOCK, SYM, false>(A, ctab, (const uint16_t *)nullptr, H, cur.r, cur.L, sr,
-                                            B, no);
         } else {
             block_select<BLOCK, SYM, false>(A, ctab, occ, no, cur.r, cur.L, sr, B);
         }
         gather_labels<U>(A.label, z, z);   // next row's first chunk: its latency overlaps the clear
-        if (dense) {
-            int4 *T4 = (int4 *)ctab;
-            for (uint32_t k = threadIdx.x; k < H / 2; k += BLOCK) T4[k] = make_int4(-1, 0, -1, 0);
-        } else {
-            occ_clear<false>(ctab, occ, no, threadIdx.x, BLOCK);
-        }
+        occ_clear<false>(ctab, occ, no, threadIdx.x, BLOCK);
         __syncthreads();
         if (threadIdx.x == 0) {   // every thread read s_no / s_ovf before the barriers above
             s_no = 0;

@@ -25,7 +25,7 @@ t = time.perf_counter()
 r = detector.run(g, RunConfig(resolution=gamma))
 el = time.perf_counter() - t
 print(json.dumps({"lib": os.environ.get("SLM_LIB_PATH", "libslm.so"), "config": name,
-                  "gamma": gamma, "seconds": round(el, 3), "sweeps": r.stats.sweeps_per_level,
+                  "gamma": gamma, "seconds": round(el, 3), "sweeps": r.stats.sweeps_per_level, "plan_paths": r.stats.plan_paths,
                   "q": r.final_score,
                   "phase_s": {k: round(v, 3) for k, v in r.stats.phase_seconds.items()},
                   "lib_ms": ctx.phase_times()}))
