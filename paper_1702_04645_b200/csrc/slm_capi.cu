@@ -367,7 +367,7 @@ static void preload_modules() {
     }
     const void *anchors[] = {slm_anchor_build(), slm_anchor_capi(), slm_anchor_commit(),
                              slm_anchor_forest(), slm_anchor_gen(), slm_anchor_level(),
-                             slm_anchor_lgains(), slm_anchor_plan(), slm_anchor_positive(), slm_anchor_prim(), slm_anchor_surface(),
+                             slm_anchor_lgains(), slm_anchor_plan(), slm_anchor_positive(), slm_anchor_prim(), slm_anchor_surface(), slm_anchor_positive_lit(),
                              slm_anchor_sweep()};
     for (const void *a : anchors) {
         cudaFunction_t f;

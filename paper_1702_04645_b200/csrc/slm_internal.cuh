@@ -251,6 +251,7 @@ struct slm_ctx {
     double *h_f64 = nullptr;
     // counters of the last phase calls
     int64_t last_rounds = 0, last_candidates = 0, last_accepted = 0;
+    int64_t last_pos_warnings = 0;   // scc_cut_cap peels of the last POSITIVE call
     // results of the last slm_run (labels per level on the host, per-level sweeps / paths)
     std::vector<std::vector<int64_t>> run_levels;
     std::vector<int64_t> run_sweeps, run_paths;
@@ -449,6 +450,13 @@ const void *slm_anchor_plan();
 const void *slm_anchor_positive();
 const void *slm_anchor_prim();
 const void *slm_anchor_surface();
+const void *slm_anchor_positive_lit();
+void bad_cycle_lengths(slm_ctx *ctx, const Forest &F, const int32_t *d_list, int32_t nbad,
+                       std::vector<int32_t> &h_len);
+void run_positive_literal(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m,
+                          int64_t scc_cap, const std::vector<int2> &ranges,
+                          std::vector<std::vector<double>> &gains, std::vector<int32_t> &unres,
+                          std::vector<int32_t> &changed, int64_t *nwarn);
 
 // slm_surface.cu: the rest of the reference's hot-path API surface
 void comm_sums_device(slm_ctx *ctx, const int32_t *d_lab, int64_t n, int64_t nc,

@@ -1490,7 +1490,6 @@ struct PosScratch {
 
 void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_t scc_cap,
                   int64_t *splits, int64_t *unresolved, int *changed, std::vector<double> *gains) {
-    (void)scc_cap;   // the scc_cut_cap branch needs cycles > cap >= 2: unreachable (F5)
     cudaStream_t s = ctx->stream;
     const int64_t n = G.n, nc = F.n_comms;
     *splits = 0;
@@ -1629,8 +1628,19 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     // a part goes to the warp executor when it is small and holds no heavy member (a warp
     // rescans every member row at each split: coarse levels have hub members whose rows hold
     // millions of entries, which the CTA executor processes cooperatively)
+    // communities whose assignment cycle is longer than 2 (never produced by run(), F5)
+    // take the literal executor (slm_positive_lit.cu); the fast executors assume <= 2
+    std::vector<int32_t> clen;
+    bad_cycle_lengths(ctx, F, list.p, nbad, clen);
+    std::vector<int2> lit_rng;
+    constexpr int64_t LIT_BASE = -(int64_t(1) << 40);
     for (int32_t i = 0; i < nbad; i++) {
         int32_t sz = hrng[i].y - hrng[i].x;
+        if (clen[i] > 2) {
+            order_kind[i] = LIT_BASE - (int64_t)lit_rng.size();
+            lit_rng.push_back(hrng[i]);
+            continue;
+        }
         if (sz <= SMALL_PART && !hheavy[i]) {
             PartDesc d;
             d.off = hrng[i].x;
@@ -2003,9 +2013,21 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
     }
     phase_mark(ctx, PH_POS_GIANT);
     SLM_REQUIRE(!hflags[1], SLM_EUNSUP, "assignment cycle longer than 2 in POSITIVE");
+    std::vector<std::vector<double>> lit_gains;
+    std::vector<int32_t> lit_unres, lit_changed;
+    int64_t lit_warn = 0;
+    run_positive_literal(ctx, G, F, m, scc_cap, lit_rng, lit_gains, lit_unres, lit_changed,
+                         &lit_warn);
+    bool lchanged = false;
+    for (size_t j = 0; j < lit_rng.size(); j++) {
+        tot += (int64_t)lit_gains[j].size();
+        un += lit_unres[j];
+        lchanged |= lit_changed[j] != 0;
+    }
+    ctx->last_pos_warnings = lit_warn;
     *splits = tot;
     *unresolved = un;
-    *changed = hflags[0] || gchanged;
+    *changed = hflags[0] || gchanged || lchanged;
     if (gains && tot > 0) {
         // the reference's order: communities ascending; within a community its LIFO stack,
         // i.e. a cut's gain, then the cut subtree's gains, then the rest's
@@ -2033,7 +2055,10 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
             }
         };
         for (int32_t i = 0; i < nbad; i++) {
-            if (order_kind[i] >= 0) {
+            if (order_kind[i] <= LIT_BASE) {
+                const auto &lg = lit_gains[LIT_BASE - order_kind[i]];
+                gains->insert(gains->end(), lg.begin(), lg.end());
+            } else if (order_kind[i] >= 0) {
                 const PartDesc &d = small1[order_kind[i]];
                 for (int k = 0; k < hng1[order_kind[i]]; k++) gains->push_back(hg1[d.off + k]);
             } else {

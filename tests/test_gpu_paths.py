@@ -83,3 +83,38 @@ def test_real_weights_sorted_path(slm, oracle):
         o = oracle.run(n, s, d, w)
         q_ok = abs(r1.final_score - o.final_score) <= 1e-9
         assert nmi(r1.hierarchy.flat, o.flat) >= 0.999 or q_ok, (n, r1.final_score, o.final_score)
+
+
+def test_positive_long_cycles_and_scc_cap(slm, oracle):
+    """POSITIVE on forests with assignment cycles longer than 2 (only a caller-supplied
+    forest has them): the literal executor (slm_positive_lit.cu) against the
+    reference's algorithm in the oracle -- branch cuts, pair cuts over the cycle's arcs,
+    and the scc_cut_cap peel -- bit for bit, integer and real weights."""
+    rng = np.random.default_rng(2024)
+    checked = 0
+    for t in range(24):
+        n = int(rng.integers(6, 60))
+        k = int(rng.integers(2 * n, 6 * n))
+        s = rng.integers(0, n, k)
+        d = rng.integers(0, n, k)
+        keep = s != d
+        s, d = s[keep], d[keep]
+        w = (rng.integers(1, 9, s.size).astype(np.float64) if t % 2 == 0
+             else rng.uniform(0.1, 3.0, s.size))
+        g = slm.Graph.from_edges(n, s, d, w)
+        og = oracle.OGraph.from_edges(n, s, d, w)
+        a = rng.integers(0, n, n)          # random functional graph: cycles of any length
+        f = slm.extract_components(a)
+        comm, nc, _ = oracle.extract_components(a)
+        np.testing.assert_array_equal(f.comm, comm)
+        for cap in (10_000, 3, 2):
+            cfg = slm.RunConfig(scc_cut_cap=cap)
+            f2, sp, un, gains = slm.positive_correction(g, None, f, cfg)
+            a2, ch, sp2, un2, gains2, _ = oracle.positive_correction(og, a, comm, nc,
+                                                                     scc_cut_cap=cap)
+            np.testing.assert_array_equal(f2.a, a2)
+            assert (sp, un) == (sp2, un2), (t, cap)
+            np.testing.assert_array_equal(np.asarray(gains, np.float64),
+                                          np.asarray(gains2, np.float64))
+            checked += 1
+    assert checked == 72
