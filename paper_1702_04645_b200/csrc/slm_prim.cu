@@ -555,16 +555,22 @@ void dev_exclusive_sum_by_key(slm_ctx *ctx, const uint32_t *keys, const int32_t 
 
 void sort_pairs_u64_f64(slm_ctx *ctx, DBuf<uint64_t> &keys, DBuf<double> &vals, int64_t n,
                         int end_bit) {
-    // ping-pong through the context's sort buffers, ending in the second pair, which is then
-    // swapped in (no copy); the caller's old buffers become the context's scratch
+    // two buffers, like a double-buffered sort: the caller's arrays (whose input may be
+    // overwritten) and the context's u64b / f64b; the result is swapped into keys / vals
     ctx->u64b.resize(n);
     ctx->f64b.resize(n);
-    ctx->sort_k64.resize(n);
-    ctx->sort_v64.resize(n);
-    radix_sort_impl<uint64_t, double>(ctx, keys.p, ctx->u64b.p, vals.p, ctx->f64b.p,
-                                      ctx->sort_k64.p, ctx->sort_v64.p, n, 0, end_bit);
-    keys.swap(ctx->u64b);
-    vals.swap(ctx->f64b);
+    const int np = end_bit > 0 ? (end_bit + 7) / 8 : 0;
+    if (np % 2 == 1) {
+        // odd pass count: keys -> u64b -> keys ... ends in u64b
+        radix_sort_impl<uint64_t, double>(ctx, keys.p, ctx->u64b.p, vals.p, ctx->f64b.p, keys.p,
+                                          vals.p, n, 0, end_bit);
+        keys.swap(ctx->u64b);
+        vals.swap(ctx->f64b);
+    } else if (np > 0) {
+        // even pass count: keys -> u64b -> keys ... ends in keys
+        radix_sort_impl<uint64_t, double>(ctx, keys.p, keys.p, vals.p, vals.p, ctx->u64b.p,
+                                          ctx->f64b.p, n, 0, end_bit);
+    }
     keys.n = n;
     vals.n = n;
 }
