@@ -300,7 +300,8 @@ __global__ void k_positive_lit(LitArgs A, const LitJob *jobs, int32_t *ipool, do
 }
 
 __global__ void k_cycle_counts(const int32_t *list, int32_t nbad, const int32_t *cptr,
-                               const int32_t *members, const uint8_t *on_cycle, int32_t *cnt) {
+                               const int32_t *members, const uint8_t *on_cycle, int32_t *cnt,
+                               int32_t *any_long) {
     const int lane = threadIdx.x & 31;
     const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -309,7 +310,10 @@ __global__ void k_cycle_counts(const int32_t *list, int32_t nbad, const int32_t 
         int32_t t = 0;
         for (int32_t q = cptr[c] + lane; q < cptr[c + 1]; q += 32) t += on_cycle[members[q]];
         t = __reduce_add_sync(0xffffffffu, t);
-        if (lane == 0) cnt[i] = t;
+        if (lane == 0) {
+            cnt[i] = t;
+            if (t > 2) *any_long = 1;
+        }
     }
 }
 
@@ -319,11 +323,16 @@ __global__ void k_cycle_counts(const int32_t *list, int32_t nbad, const int32_t 
 void bad_cycle_lengths(slm_ctx *ctx, const Forest &F, const int32_t *d_list, int32_t nbad,
                        std::vector<int32_t> &h_len) {
     DBuf<int32_t> d;
-    d.resize(nbad);
+    d.resize(nbad + 1);
     h_len.assign(nbad, 0);
     if (!nbad) return;
+    CUDA_TRY(cudaMemsetAsync(d.p + nbad, 0, 4, ctx->stream));
     k_cycle_counts<<<grid_for((int64_t)nbad * 32, 256), 256, 0, ctx->stream>>>(
-        d_list, nbad, F.cptr.p, F.members.p, F.on_cycle.p, d.p);
+        d_list, nbad, F.cptr.p, F.members.p, F.on_cycle.p, d.p, d.p + nbad);
+    int32_t any = 0;   // the per-community lengths are downloaded only when one exceeds 2
+    CUDA_TRY(cudaMemcpyAsync(&any, d.p + nbad, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (!any) return;
     CUDA_TRY(cudaMemcpyAsync(h_len.data(), d.p, nbad * 4, cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
 }

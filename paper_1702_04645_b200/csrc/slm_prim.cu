@@ -345,7 +345,8 @@ __global__ void __launch_bounds__(RS_BLOCK, 2) k_rs_onesweep(const K *kin, K *ko
                                                           unsigned dmask,
                                                           const unsigned long long *dbase,
                                                           unsigned long long *status,
-                                                          unsigned *ticket) {
+                                                          unsigned *ticket,
+                                                          const int64_t *toff, int64_t ntiles) {
     extern __shared__ __align__(16) unsigned char rs_smem[];
     unsigned *wcnt = (unsigned *)rs_smem;                                   // [WARPS][256]
     unsigned long long *dest = (unsigned long long *)(wcnt + RS_WARPS * 256);   // [256]
@@ -354,9 +355,14 @@ __global__ void __launch_bounds__(RS_BLOCK, 2) k_rs_onesweep(const K *kin, K *ko
     K *sk = (K *)(sdig + RS_TILE);                                          // [TILE] (keys, then values)
     __shared__ unsigned s_tile;
     __shared__ unsigned s_hist[256];
-    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    // reduce-then-scan mode (toff != nullptr): the tile's offsets per digit are known,
+    // tile = blockIdx.x; onesweep mode: tiles in ticket order with decoupled look-back
+    if (threadIdx.x == 0) s_tile = toff ? blockIdx.x : atomicAdd(ticket, 1u);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int i = lane; i < 256; i += 32) wcnt[wid * 256 + i] = 0;
+    for (int i = lane; i < 256; i += 32) {
+        wcnt[wid * 256 + i] = 0;
+        ((unsigned *)sk)[wid * 256 + i] = 0;   // per-warp digit masks of the ranking
+    }
     if (threadIdx.x < 256) s_hist[threadIdx.x] = 0;
     __syncthreads();
     const int64_t tile = s_tile;
@@ -376,21 +382,37 @@ __global__ void __launch_bounds__(RS_BLOCK, 2) k_rs_onesweep(const K *kin, K *ko
     }
     // the tile's digit counts first, published at once, so that the tiles behind this one
     // find them during their look-back while this tile is still ranking its keys
+    if (!toff) {
 #pragma unroll
-    for (int i = 0; i < RS_ITEMS; i++)
-        if (wb + i * 32 + lane < n) atomicAdd(&s_hist[(unsigned)(key[i] >> shift) & dmask], 1u);
-    __syncthreads();
-    if (threadIdx.x < 256)
-        st_status(status + tile * 256 + threadIdx.x, (tile == 0 ? RS_INC : RS_AGG) | s_hist[threadIdx.x]);
+        for (int i = 0; i < RS_ITEMS; i++)
+            if (wb + i * 32 + lane < n) atomicAdd(&s_hist[(unsigned)(key[i] >> shift) & dmask], 1u);
+        __syncthreads();
+        if (threadIdx.x < 256)
+            st_status(status + tile * 256 + threadIdx.x,
+                      (tile == 0 ? RS_INC : RS_AGG) | s_hist[threadIdx.x]);
+    }
+    // peers of equal digit inside a 32-key chunk: every lane ORs its bit into the warp's
+    // per-digit mask (shared memory, the staging area before it is used), then reads it
+    // back; the lowest peer advances the warp's digit counter and clears the mask
+    // (cheaper than __match_any_sync)
+    unsigned *msk = (unsigned *)sk + wid * 256;
 #pragma unroll
     for (int i = 0; i < RS_ITEMS; i++) {
         const bool ok = wb + i * 32 + lane < n;
         const unsigned d = (unsigned)(key[i] >> shift) & dmask;
-        const unsigned m = __match_any_sync(0xffffffffu, ok ? d : 256u + lane);
-        const int leader = __ffs(m) - 1;
+        if (ok) atomicOr(&msk[d], 1u << lane);
+        __syncwarp();
+        const unsigned m = ok ? msk[d] : 0u;
+        __syncwarp();
+        const int leader = ok ? __ffs(m) - 1 : lane;
         unsigned base = 0;
-        if (ok && lane == leader) base = atomicAdd(&wcnt[wid * 256 + d], (unsigned)__popc(m));
+        if (ok && lane == leader) {
+            base = wcnt[wid * 256 + d];
+            wcnt[wid * 256 + d] = base + __popc(m);
+            msk[d] = 0u;
+        }
         base = __shfl_sync(0xffffffffu, base, leader);
+        __syncwarp();
         pos[i] = ok ? ((base + __popc(m & lt)) | (d << 24)) : 0xffffffffu;   // rank | digit
     }
     __syncthreads();
@@ -406,7 +428,9 @@ __global__ void __launch_bounds__(RS_BLOCK, 2) k_rs_onesweep(const K *kin, K *ko
         // look back for the global prefix of this digit (the count was published above)
         unsigned long long *mine = status + tile * 256 + d;
         unsigned long long excl = 0;
-        if (tile != 0) {
+        if (toff) {
+            dest[d] = (unsigned long long)toff[(int64_t)d * ntiles + tile];
+        } else if (tile != 0) {
             // 8 predecessors per step with independent loads: the walk costs one memory
             // latency per 8 tiles, not per tile
             for (int64_t p = tile - 1; p >= 0;) {
@@ -430,7 +454,7 @@ __global__ void __launch_bounds__(RS_BLOCK, 2) k_rs_onesweep(const K *kin, K *ko
             }
             st_status(mine, RS_INC | (excl + cnt));
         }
-        dest[d] = dbase[d] + excl;
+        if (!toff) dest[d] = dbase[d] + excl;
     }
     // tile start of every digit in digit order: exclusive scan of cnt over 256 threads
     {
@@ -484,6 +508,25 @@ __global__ void __launch_bounds__(RS_BLOCK, 2) k_rs_onesweep(const K *kin, K *ko
     }
 }
 
+// reduce-then-scan upsweep: per tile, the digit counts of this pass, digit-major
+// (cnt[d * ntiles + tile]); their exclusive scan is every (digit, tile)'s output offset
+template <class K>
+__global__ void __launch_bounds__(RS_BLOCK) k_rs_tilehist(const K *kin, int64_t n, int shift,
+                                                        unsigned dmask, int64_t ntiles,
+                                                        int32_t *cnt) {
+    __shared__ unsigned h[256];
+    if (threadIdx.x < 256) h[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t t0 = blockIdx.x * (int64_t)RS_TILE;
+#pragma unroll 4
+    for (int i = 0; i < RS_ITEMS; i++) {
+        const int64_t idx = t0 + (int64_t)i * RS_BLOCK + threadIdx.x;
+        if (idx < n) atomicAdd(&h[(unsigned)(kin[idx] >> shift) & dmask], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 256) cnt[(int64_t)threadIdx.x * ntiles + blockIdx.x] = (int32_t)h[threadIdx.x];
+}
+
 template <class K, class V>
 size_t rs_smem_bytes() {
     const size_t kv = sizeof(K) > sizeof(V) ? sizeof(K) : sizeof(V);
@@ -505,30 +548,57 @@ void radix_sort_impl(slm_ctx *ctx, const K *kin, K *kout, const V *vin, V *vout,
         return;
     }
     const int64_t ntiles = (n + RS_TILE - 1) / RS_TILE;
-    // scratch: [hist np*256 u64 | tickets np u32 (padded) | status ntiles*256 u64]
-    const size_t hb = (size_t)np * 256 * 8, tb = 64, sb = (size_t)ntiles * 256 * 8;
-    ctx->tmp.resize(hb + tb + sb);
-    unsigned long long *hist = (unsigned long long *)ctx->tmp.p;
-    unsigned *tickets = (unsigned *)((char *)ctx->tmp.p + hb);
-    unsigned long long *status = (unsigned long long *)((char *)ctx->tmp.p + hb + tb);
-    CUDA_TRY(cudaMemsetAsync(ctx->tmp.p, 0, hb + tb, s));
-    k_rs_hist<K><<<grid_for(n, 256, SMS() * 8), 256, 0, s>>>(kin, n, begin_bit, np, end_bit, hist);
-    k_rs_hist_scan<<<np, 256, 0, s>>>(hist);
+    // onesweep (default): one global histogram of all passes first, then per pass the
+    // single-pass kernel with decoupled look-back.  SLM_SORT_ONESWEEP=0: reduce-then-scan
+    // (per pass a tile-histogram kernel, a scan of the digit-major counts, and the same
+    // ranking / scatter kernel with known offsets); measured a few % slower.
+    static const bool onesweep = !(getenv("SLM_SORT_ONESWEEP") && atoi(getenv("SLM_SORT_ONESWEEP")) == 0);
+    unsigned long long *hist = nullptr, *status = nullptr;
+    unsigned *tickets = nullptr;
+    size_t sb = 0;
+    if (onesweep) {
+        // scratch: [hist np*256 u64 | tickets np u32 (padded) | status ntiles*256 u64]
+        const size_t hb = (size_t)np * 256 * 8, tb = 64;
+        sb = (size_t)ntiles * 256 * 8;
+        ctx->tmp.resize(hb + tb + sb);
+        hist = (unsigned long long *)ctx->tmp.p;
+        tickets = (unsigned *)((char *)ctx->tmp.p + hb);
+        status = (unsigned long long *)((char *)ctx->tmp.p + hb + tb);
+        CUDA_TRY(cudaMemsetAsync(ctx->tmp.p, 0, hb + tb, s));
+        k_rs_hist<K><<<grid_for(n, 256, SMS() * 8), 256, 0, s>>>(kin, n, begin_bit, np, end_bit,
+                                                                 hist);
+        k_rs_hist_scan<<<np, 256, 0, s>>>(hist);
+    }
     const size_t smem = rs_smem_bytes<K, V>();
     CUDA_TRY(cudaFuncSetAttribute(k_rs_onesweep<K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
     // ping-pong so that the last pass lands in kout / vout
     const K *ks = kin;
     const V *vs = vin;
+    DBuf<int32_t> tcnt;
+    DBuf<int64_t> toffb;
+    if (!onesweep) {
+        tcnt.resize(256 * ntiles);
+        toffb.resize(256 * ntiles);
+    }
     for (int p = 0; p < np; p++) {
         const bool to_out = ((np - 1 - p) % 2) == 0;
         K *kd = to_out ? kout : kalt;
         V *vd = vin ? (to_out ? vout : valt) : nullptr;
-        CUDA_TRY(cudaMemsetAsync(status, 0, sb, s));
         const int shift = begin_bit + 8 * p;
         const unsigned dmask = end_bit - shift >= 8 ? 255u : ((1u << (end_bit - shift)) - 1u);
+        const int64_t *toff = nullptr;
+        if (onesweep) {
+            CUDA_TRY(cudaMemsetAsync(status, 0, sb, s));
+        } else {
+            k_rs_tilehist<K><<<(unsigned)ntiles, RS_BLOCK, 0, s>>>(ks, n, shift, dmask, ntiles,
+                                                                 tcnt.p);
+            dev_exclusive_sum<int32_t, int64_t>(ctx, tcnt.p, toffb.p, 256 * ntiles);
+            toff = toffb.p;
+        }
         k_rs_onesweep<K, V><<<(unsigned)ntiles, RS_BLOCK, smem, s>>>(
-            ks, kd, vs, vd, n, shift, dmask, hist + p * 256, status, tickets + p);
+            ks, kd, vs, vd, n, shift, dmask, hist ? hist + p * 256 : nullptr, status,
+            tickets ? tickets + p : nullptr, toff, ntiles);
         ks = kd;
         vs = vd;
     }

@@ -114,7 +114,10 @@ def test_positive_long_cycles_and_scc_cap(slm, oracle):
                                                                      scc_cut_cap=cap)
             np.testing.assert_array_equal(f2.a, a2)
             assert (sp, un) == (sp2, un2), (t, cap)
-            np.testing.assert_array_equal(np.asarray(gains, np.float64),
-                                          np.asarray(gains2, np.float64))
+            g1, g2 = np.asarray(gains, np.float64), np.asarray(gains2, np.float64)
+            if t % 2 == 0:
+                np.testing.assert_array_equal(g1, g2)
+            else:   # real weights: the <= 2-cycle executors sum in DFS order
+                np.testing.assert_allclose(g1, g2, rtol=1e-12, atol=0)
             checked += 1
     assert checked == 72
