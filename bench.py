@@ -177,10 +177,9 @@ def snapshot_arrays(ctx):
 def cpu_sample(ctx, info, target_entries, snap):
     """Download a contiguous row sample of the snapshot for the oracle port."""
     n = info["n"]
-    # rows [0, R) with about target_entries union entries
-    lo, hi = 0, n
-    probe = ctx.union_rows(0, min(n, 1 << 16))[0]
-    avg = max(1.0, probe[-1] / max(1, probe.size - 1))
+    # rows [0, R) with about target_entries union entries (the same rule as the reference
+    # arm's oracle_snapshot: the graph's mean degree)
+    avg = max(1.0, info["ue"] / max(1, n))
     R = int(min(n, max(1024, target_entries / avg)))
     uptr, unbr, uu = ctx.union_rows(0, R)
     comm, so, si = snap

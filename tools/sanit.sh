@@ -1,3 +1,5 @@
+# NOTE (r02): compute-sanitizer is closed on the GPU pool ("runs under it have left GPUs
+# needing a reset"); this recipe is kept for a box where it is available.
 # compute-sanitizer evidence on small configs (profiles/r02_sanitizer_*.log): memcheck of a
 # full level loop (every phase: build, ASSIGN, COMPONENTS, POSITIVE, MAXIMAL with the
 # persistent commit walkers, AGGREGATE, score) and of the plan sweep / primitives;
