@@ -299,42 +299,52 @@ __global__ void k_positive_lit(LitArgs A, const LitJob *jobs, int32_t *ipool, do
     out[blockIdx.x] = o;
 }
 
-__global__ void k_cycle_counts(const int32_t *list, int32_t nbad, const int32_t *cptr,
-                               const int32_t *members, const uint8_t *on_cycle, int32_t *cnt,
-                               int32_t *any_long) {
-    const int lane = threadIdx.x & 31;
-    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = w0; i < nbad; i += nw) {
-        const int32_t c = list[i];
-        int32_t t = 0;
-        for (int32_t q = cptr[c] + lane; q < cptr[c + 1]; q += 32) t += on_cycle[members[q]];
-        t = __reduce_add_sync(0xffffffffu, t);
-        if (lane == 0) {
-            cnt[i] = t;
-            if (t > 2) *any_long = 1;
+// a node on a cycle longer than 2: on_cycle, not self-assigned, and its target's target is
+// not itself; marks the node's community (and a global flag)
+__global__ void k_long_cycle_marks(const int32_t *a, const uint8_t *on_cycle, const int32_t *comm,
+                                   int64_t n, uint8_t *cflag, int32_t *any_long) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        if (!on_cycle[x]) continue;
+        const int32_t t = a[x];
+        if (t != (int32_t)x && a[t] != (int32_t)x) {
+            cflag[comm[x]] = 1;
+            *any_long = 1;
         }
     }
+}
+__global__ void k_bad_long(const int32_t *list, int32_t nbad, const uint8_t *cflag, int32_t *len) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nbad;
+         i += (int64_t)gridDim.x * blockDim.x)
+        len[i] = cflag[list[i]] ? 3 : 0;
 }
 
 }  // namespace
 
-// cycle length (number of on-cycle members) of every bad community
+// per bad community: > 2 when its assignment cycle is longer than 2 (else 0); one O(n)
+// pass over the forest, and nothing more is read back unless such a cycle exists
 void bad_cycle_lengths(slm_ctx *ctx, const Forest &F, const int32_t *d_list, int32_t nbad,
                        std::vector<int32_t> &h_len) {
-    DBuf<int32_t> d;
-    d.resize(nbad + 1);
+    cudaStream_t s = ctx->stream;
     h_len.assign(nbad, 0);
-    if (!nbad) return;
-    CUDA_TRY(cudaMemsetAsync(d.p + nbad, 0, 4, ctx->stream));
-    k_cycle_counts<<<grid_for((int64_t)nbad * 32, 256), 256, 0, ctx->stream>>>(
-        d_list, nbad, F.cptr.p, F.members.p, F.on_cycle.p, d.p, d.p + nbad);
-    int32_t any = 0;   // the per-community lengths are downloaded only when one exceeds 2
-    CUDA_TRY(cudaMemcpyAsync(&any, d.p + nbad, 4, cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    if (!any) return;
-    CUDA_TRY(cudaMemcpyAsync(h_len.data(), d.p, nbad * 4, cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (!nbad || F.n == 0) return;
+    DBuf<int32_t> any;
+    any.resize(1);
+    CTX_SCRATCH(DBuf<uint8_t>, cflag);
+    cflag.resize(F.n_comms);
+    CUDA_TRY(cudaMemsetAsync(any.p, 0, 4, s));
+    CUDA_TRY(cudaMemsetAsync(cflag.p, 0, F.n_comms, s));
+    k_long_cycle_marks<<<grid_for(F.n, 256), 256, 0, s>>>(F.a.p, F.on_cycle.p, F.comm.p, F.n,
+                                                         cflag.p, any.p);
+    int32_t h_any = 0;
+    CUDA_TRY(cudaMemcpyAsync(&h_any, any.p, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (!h_any) return;
+    DBuf<int32_t> d;
+    d.resize(nbad);
+    k_bad_long<<<grid_for(nbad, 256), 256, 0, s>>>(d_list, nbad, cflag.p, d.p);
+    CUDA_TRY(cudaMemcpyAsync(h_len.data(), d.p, nbad * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
 }
 
 // POSITIVE for the given communities (community ids + member ranges), literal algorithm;

@@ -202,10 +202,10 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan(const TI *in, TO *out, cons
 
 // deterministic reduce-then-scan for fp64 operands (the look-back's grouping would make
 // the rounding depend on timing): tile sums, one CTA scans them in order, tiles rescan
-template <class T>
-__global__ void __launch_bounds__(SCAN_BLOCK) k_scan_reduce(const T *in, int64_t n, T *tsum) {
+template <class TI, class T>
+__global__ void __launch_bounds__(SCAN_BLOCK) k_scan_reduce(const TI *in, int64_t n, T *tsum) {
     __shared__ SS<T, false> s_warp[SCAN_BLOCK / 32];
-    TileScan<T, T, false> S;
+    TileScan<TI, T, false> S;
     const int64_t base = blockIdx.x * (int64_t)SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
     S.load(in, nullptr, n, base);
     const SS<T, false> agg = S.reduce(s_warp);
@@ -229,11 +229,11 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan_tiles(T *tsum, int64_t nt) 
         __syncthreads();
     }
 }
-template <class T>
-__global__ void __launch_bounds__(SCAN_BLOCK) k_scan_down(const T *in, T *out, int64_t n,
+template <class TI, class T>
+__global__ void __launch_bounds__(SCAN_BLOCK) k_scan_down(const TI *in, T *out, int64_t n,
                                                           const T *tpre) {
     __shared__ SS<T, false> s_warp[SCAN_BLOCK / 32];
-    TileScan<T, T, false> S;
+    TileScan<TI, T, false> S;
     const int64_t base = blockIdx.x * (int64_t)SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
     S.load(in, nullptr, n, base);
     S.reduce(s_warp);
@@ -261,12 +261,15 @@ template <class TI, class TO, bool SEG>
 void scan_run(slm_ctx *ctx, const TI *in, TO *out, const uint32_t *keys, int64_t n) {
     if (n <= 0) return;
     const int64_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
-    if (std::is_floating_point<TO>::value) {
+    if (!SEG) {
+        // reduce-then-scan: tile sums, one CTA scans them in order, tiles rescan.  Fixed
+        // order (deterministic fp64 rounding), and no look-back chain across the ~1,000
+        // tiles resident at once (the single-pass form below is kept for the segmented scan)
         ctx->tmp.resize(ntiles * sizeof(TO));
         TO *tsum = (TO *)ctx->tmp.p;
-        k_scan_reduce<TO><<<(unsigned)ntiles, SCAN_BLOCK, 0, ctx->stream>>>((const TO *)in, n, tsum);
+        k_scan_reduce<TI, TO><<<(unsigned)ntiles, SCAN_BLOCK, 0, ctx->stream>>>(in, n, tsum);
         k_scan_tiles<TO><<<1, SCAN_BLOCK, 0, ctx->stream>>>(tsum, ntiles);
-        k_scan_down<TO><<<(unsigned)ntiles, SCAN_BLOCK, 0, ctx->stream>>>((const TO *)in, out, n, tsum);
+        k_scan_down<TI, TO><<<(unsigned)ntiles, SCAN_BLOCK, 0, ctx->stream>>>(in, out, n, tsum);
     } else {
         ScanStatus<TO> st;
         scan_launch_status<TO>(ctx, ntiles, st);
