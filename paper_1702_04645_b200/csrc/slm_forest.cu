@@ -216,8 +216,15 @@ __global__ void k_comm_sums(const int32_t *cptr, const int32_t *members, const d
     }
 }
 
-__global__ void k_kid_keys(const int32_t *a, int64_t n, uint32_t *key) {
-    GS_LOOP(i, n) key[i] = (a[i] != (int32_t)i) ? (uint32_t)a[i] : (uint32_t)n;
+__global__ void k_kid_flags(const int32_t *a, int64_t n, int32_t *f) {
+    GS_LOOP(i, n) f[i] = a[i] != (int32_t)i;
+}
+__global__ void k_kid_compact(const int32_t *a, int64_t n, const int32_t *f, const int32_t *pos,
+                              uint32_t *key, int32_t *node) {
+    GS_LOOP(i, n) if (f[i]) {
+        key[pos[i]] = (uint32_t)a[i];
+        node[pos[i]] = (int32_t)i;
+    }
 }
 
 // one thread per community: iterative DFS pre-order from the smallest cycle node
@@ -461,11 +468,25 @@ void build_layout(slm_ctx *ctx, Forest &F) {
     uint32_t *kk = (uint32_t *)ctx->i32a.resize(n);
     uint32_t *ks = (uint32_t *)ctx->i32b.resize(n);
     int32_t *iota = ctx->i32c.resize(n);
-    k_kid_keys<<<grid_for(n, 256), 256, 0, s>>>(F.a.p, n, kk);
-    k_iota<<<grid_for(n, 256), 256, 0, s>>>(iota, n);
-    if (n > 0) sort_pairs_u32_i32(ctx, kk, ks, iota, F.kids.p, n, bits_for(n + 1));
-    // only kptr[n] (the number of kids) is needed unless the DFS fallback below runs
-    k_lb_one<<<1, 1, 0, s>>>((const int32_t *)ks, n, (int32_t)n, F.kptr.p + n);
+    // the children lists: nodes with a[i] != i, stably sorted by parent.  They are compacted
+    // first, so the sort runs on parent ids alone (bits_for(n) bits: 3 passes at n = 2^24,
+    // where keys with a sentinel for self-assigned nodes would need a fourth)
+    {
+        CTX_SCRATCH(DBuf<int32_t>, kf);
+        CTX_SCRATCH(DBuf<int32_t>, kpos);
+        kf.resize(n + 1);
+        kpos.resize(n + 1);
+        CUDA_TRY(cudaMemsetAsync(kf.p + n, 0, 4, s));
+        k_kid_flags<<<grid_for(n, 256), 256, 0, s>>>(F.a.p, n, kf.p);
+        dev_exclusive_sum<int32_t, int32_t>(ctx, kf.p, kpos.p, n + 1);
+        k_kid_compact<<<grid_for(n, 256), 256, 0, s>>>(F.a.p, n, kf.p, kpos.p, kk, iota);
+        int32_t nkids = 0;
+        CUDA_TRY(cudaMemcpyAsync(&nkids, kpos.p + n, 4, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (nkids > 0) sort_pairs_u32_i32(ctx, kk, ks, iota, F.kids.p, nkids, bits_for(n));
+        // only kptr[n] (the number of kids) is needed unless the DFS fallback below runs
+        CUDA_TRY(cudaMemcpyAsync(F.kptr.p + n, kpos.p + n, 4, cudaMemcpyDeviceToDevice, s));
+    }
     // depth of every node below its community root (parent = a[x])
     int32_t *flags = ctx->i32d.resize(2);
     CUDA_TRY(cudaMemsetAsync(flags, 0, 8, s));
@@ -486,7 +507,7 @@ void build_layout(slm_ctx *ctx, Forest &F) {
     const int maxd = hf[1];
     if (hf[0]) {
         // pathological depth (> 4096): sequential DFS per community (needs the kids pointers)
-        k_lb_ptr32<<<grid_for(n + 1, 256), 256, 0, s>>>((const int32_t *)ks, n, n, F.kptr.p);
+        k_lb_ptr32<<<grid_for(n + 1, 256), 256, 0, s>>>((const int32_t *)ks, nk, n, F.kptr.p);
         int32_t *stk_node = ctx->i32a.resize(n);
         CTX_SCRATCH(DBuf<int32_t>, stk_it);   // grow-only scratch kept across calls
         stk_it.resize(n);
