@@ -697,6 +697,36 @@ __global__ void k_view_entries(const int64_t *uptr, const int32_t *unbr, const u
     }
 }
 
+// Sorted form of the view's rows (neighbours ascending in VIEW numbering), by transposition:
+// the union's pattern and u = w_out + w_in are symmetric, so a stable sort of the view's
+// row-major entries (k, j, u) by the destination j groups them by j with k ascending --
+// which is row j of the view with its neighbours in ascending order.  Key = j, payload =
+// (k, u); row offsets are unchanged (deg is symmetric too).  Hub neighbours (the low view
+// ids) then sit at the front of every row and the label gathers of consecutive lanes share
+// 128-byte lines.
+__global__ void k_view_entries_kv(const int64_t *uptr, const int32_t *unbr, const uint32_t *u32,
+                                  const int32_t *order, const int32_t *newid, int64_t n,
+                                  const int64_t *vptr, uint32_t *key, uint64_t *val) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; k < n;
+         k += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int32_t v = order[k];
+        const int64_t s0 = uptr[v], d = uptr[v + 1] - s0, t0 = vptr[k];
+        for (int64_t t = lane; t < d; t += 32) {
+            key[t0 + t] = (uint32_t)newid[unbr[s0 + t]];
+            val[t0 + t] = ((uint64_t)k << 32) | u32[s0 + t];
+        }
+    }
+}
+__global__ void k_view_split(const uint64_t *val, int64_t ue, int32_t *vnbr, uint32_t *vu32) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ue;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t v = val[e];
+        vnbr[e] = (int32_t)(v >> 32);
+        vu32[e] = (uint32_t)v;
+    }
+}
+
 template <class T>
 __global__ void k_view_gather(const T *src, const int32_t *order, int64_t n, T *dst) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
@@ -870,10 +900,30 @@ SweepView &ensure_sweep_view(slm_ctx *ctx, const LevelGraph &G) {
         dev_exclusive_sum<int64_t, int64_t>(ctx, vdeg.p, V.uptr.p, n + 1);
         V.unbr.resize(ue);
         V.uu32.resize(ue);
-        k_view_entries<<<grid_for(n * 32, 256), 256, 0, s>>>(G.uptr.p, G.unbr.p, G.uu32.p,
-                                                               W->order.p, nid.p, n, V.uptr.p,
-                                                               V.unbr.p, V.uu32.p);
-        vmark("entries");
+        static const bool sorted_rows =
+            !(getenv("SLM_VIEW_SORTED") && atoi(getenv("SLM_VIEW_SORTED")) == 0);
+        if (sorted_rows && ue > 0) {
+            DBuf<uint32_t> kA, kB;
+            DBuf<uint64_t> vA, vB;
+            kA.resize(ue);
+            kB.resize(ue);
+            vA.resize(ue);
+            vB.resize(ue);
+            k_view_entries_kv<<<grid_for(n * 32, 256), 256, 0, s>>>(
+                G.uptr.p, G.unbr.p, G.uu32.p, W->order.p, nid.p, n, V.uptr.p, kA.p, vA.p);
+            vmark("entries (key, payload)");
+            const bool inB = sort_pairs_u32_u64(ctx, kA.p, kB.p, vA.p, vB.p, ue, bits_for(n));
+            vmark("transpose sort");
+            k_view_split<<<grid_for(ue, 256), 256, 0, s>>>(inB ? vB.p : vA.p, ue, V.unbr.p,
+                                                            V.uu32.p);
+            CUDA_TRY(cudaStreamSynchronize(s));   // the local buffers go back to the arena
+            vmark("split");
+        } else {
+            k_view_entries<<<grid_for(n * 32, 256), 256, 0, s>>>(G.uptr.p, G.unbr.p, G.uu32.p,
+                                                                   W->order.p, nid.p, n, V.uptr.p,
+                                                                   V.unbr.p, V.uu32.p);
+            vmark("entries");
+        }
     }
     V.s_out.resize(n);
     k_view_gather<double><<<grid_for(n, 256), 256, 0, s>>>(G.s_out.p, W->order.p, n, V.s_out.p);

@@ -434,6 +434,8 @@ void sort_pairs_u64_f64(slm_ctx *ctx, DBuf<uint64_t> &keys, DBuf<double> &vals, 
                         int end_bit);
 void sort_pairs_u32_i32(slm_ctx *ctx, uint32_t *keys_in, uint32_t *keys_out, int32_t *vals_in,
                         int32_t *vals_out, int64_t n, int end_bit);
+bool sort_pairs_u32_u64(slm_ctx *ctx, uint32_t *kA, uint32_t *kB, uint64_t *vA, uint64_t *vB,
+                        int64_t n, int end_bit);
 int bits_for(int64_t v);
 double debug_sort(slm_ctx *ctx, int kind, void *keys, void *vals, int64_t n, int end_bit);
 void debug_scan(slm_ctx *ctx, int kind, const void *in, void *out, const uint32_t *keys, int64_t n);

@@ -656,6 +656,21 @@ void sort_pairs_u32_i32(slm_ctx *ctx, uint32_t *keys_in, uint32_t *keys_out, int
                                        ctx->sort_v32.p, n, 0, end_bit);
 }
 
+// 32-bit keys with 64-bit payloads (the sweep view's row transposition, slm_build.cu).  A is
+// the input and is overwritten; the result lands in B for an odd number of 8-bit passes and
+// in A for an even number: returns true when it is in B.
+bool sort_pairs_u32_u64(slm_ctx *ctx, uint32_t *kA, uint32_t *kB, uint64_t *vA, uint64_t *vB,
+                        int64_t n, int end_bit) {
+    const int np = end_bit > 0 ? (end_bit + 7) / 8 : 0;
+    if (np == 0) return false;
+    if (np % 2 == 1) {
+        radix_sort_impl<uint32_t, uint64_t>(ctx, kA, kB, vA, vB, kA, vA, n, 0, end_bit);
+        return true;
+    }
+    radix_sort_impl<uint32_t, uint64_t>(ctx, kA, kA, vA, vA, kB, vB, n, 0, end_bit);
+    return false;
+}
+
 // diagnostics hooks (slm_capi.cu slm_debug_sort / slm_debug_scan)
 double debug_sort(slm_ctx *ctx, int kind, void *keys, void *vals, int64_t n, int end_bit) {
     cudaStream_t s = ctx->stream;
