@@ -162,8 +162,9 @@ __device__ __forceinline__ int32_t decide(const SweepArgs<SYM> &A, double tb, in
 template <bool SYM>
 __device__ __forceinline__ int32_t decide_fast(const SweepArgs<SYM> &A, uint32_t gb, int32_t cb,
                                                float lo_b, float up_b, bool hown, uint32_t gown,
-                                               double2 sr, float2 srf, int32_t L) {
-    const float2 SL = comm_Sf(A, L);
+                                               double2 sr, float2 srf, int32_t L, float2 SL) {
+    // SL = comm_Sf(A, L): the lane-per-row, packed, warp and half-warp kernels load it at the
+    // start of the row, off the row's serial tail
     const float a = hown ? __uint2float_rn(gown) * A.inv_mf : 0.0f;
     const float P = srf.x * (SL.y - srf.y) + srf.y * (SL.x - srf.x);
     const float Pabs = srf.x * (SL.y + srf.y) + srf.y * (SL.x + srf.x);
@@ -266,6 +267,7 @@ __global__ void __launch_bounds__(256) k_sweep_small(SweepArgs<SYM> A, const int
                                      ~((1u << rst) - 1u);
             const double2 srr = node_s(A, rr);
             const float2 srf = make_float2((float)srr.x, (float)srr.y);
+            const float2 SLf = valid ? comm_Sf(A, Lr) : make_float2(0.f, 0.f);
             // fp32 bound filter per group (as the table kernels): row max of the lower bounds
             float up = -INFINITY, lo = -INFINITY;
             if (leader && !own) up = approx_up(gs, comm_Sf(A, c), srf, A.inv_mf, A.inv_m2f, lo);
@@ -286,7 +288,7 @@ __global__ void __launch_bounds__(256) k_sweep_small(SweepArgs<SYM> A, const int
             if (valid && LO == -INFINITY) {
                 if (lane == rlast) A.cstar[rr] = Lr;
             } else if (valid && ncand == 1) {
-                if (cand) A.cstar[rr] = decide_fast(A, gs, c, LO, up, ol != 0, gown, srr, srf, Lr);
+                if (cand) A.cstar[rr] = decide_fast(A, gs, c, LO, up, ol != 0, gown, srr, srf, Lr, SLf);
             }
             // rows the filter cannot settle: exact scores of their candidates, segmented argmax
             const bool slow = valid && LO != -INFINITY && ncand > 1;
@@ -326,6 +328,7 @@ __global__ void __launch_bounds__(256) k_sweep_tiny(SweepArgs<SYM> A, const int3
         const int64_t e0 = A.uptr[r];
         const int d = (int)(A.uptr[r + 1] - e0);
         const int32_t L = A.label[r];
+        const float2 SLf = comm_Sf(A, L);   // (consumed by decide_fast at the end of the row)
         int32_t z[D], c[D];
         uint32_t w[D];
 #pragma unroll
@@ -373,7 +376,7 @@ __global__ void __launch_bounds__(256) k_sweep_tiny(SweepArgs<SYM> A, const int3
         if (S.lo == -INFINITY) {
             A.cstar[r] = L;
         } else if (S.up2 < S.lo) {
-            A.cstar[r] = decide_fast(A, S.g1, S.c1, S.lo, S.up1, hown, gown, sr, srf, L);
+            A.cstar[r] = decide_fast(A, S.g1, S.c1, S.lo, S.up1, hown, gown, sr, srf, L, SLf);
         } else {
             double bt = -INFINITY;
             int32_t bc = 0x7fffffff;
@@ -532,6 +535,16 @@ __device__ __forceinline__ void occ_clear(int2 *T, const IDX *occ, uint32_t no, 
     }
 }
 
+template <bool GLOBALT, class IDX>
+__device__ __forceinline__ void occ_clear(const SoaTab &T, const IDX *occ, uint32_t no, uint32_t t0,
+                                          uint32_t stride) {
+    for (uint32_t k = t0; k < no; k += stride) {
+        const uint32_t sl = occ[k];
+        T.key[sl] = -1;
+        T.sum[sl] = 0u;
+    }
+}
+
 // stride-`stride` unrolled load of entries of a row: neighbour labels + weights
 template <int U, bool SYM>
 __device__ __forceinline__ void load_entries(const SweepArgs<SYM> &A, int64_t e0, int64_t d,
@@ -630,10 +643,14 @@ __device__ __forceinline__ void red_pred(uint32_t a, bool p, uint32_t v) {
 // entry one predicated CAS (when the slot is empty) and one predicated add (when the slot
 // holds, or now holds, the community).  Entries whose first slot belongs to another
 // community (a minority at load <= 1/2) continue in the linear-probing loop.
-template <int U, bool BOUNDED>
+// Table layout: SO = 4: array of {key, sum} slots (8-byte stride, sum 4 bytes after the key);
+// SO = 4 * HMAX: keys[HMAX] then sums[HMAX] (4-byte stride: the 32 lanes of a probe or an
+// add spread over all 32 banks instead of the 16 even / odd ones).
+template <int U, bool BOUNDED, int SO = 4>
 __device__ __forceinline__ void insert_chunk(uint32_t tb, uint32_t hmask, const int32_t (&c)[U],
                                              const uint32_t (&w)[U], uint32_t ob, uint32_t *scnt,
                                              uint32_t &rcnt, int *ovf) {
+    constexpr uint32_t KS = SO == 4 ? 8 : 4;
     const int lane = threadIdx.x & 31;
     const uint32_t hsh = __clz(hmask);
     bool fr[U], pend[U];
@@ -642,7 +659,7 @@ __device__ __forceinline__ void insert_chunk(uint32_t tb, uint32_t hmask, const 
 #pragma unroll
     for (int u = 0; u < U; u++) {
         sl[u] = ((uint32_t)c[u] * 2654435769u) >> hsh;
-        k[u] = c[u] >= 0 ? lds_vol(tb + sl[u] * 8) : 0;
+        k[u] = c[u] >= 0 ? lds_vol(tb + sl[u] * KS) : 0;
     }
     bool anyp = false;
 #pragma unroll
@@ -650,10 +667,10 @@ __device__ __forceinline__ void insert_chunk(uint32_t tb, uint32_t hmask, const 
         const bool valid = c[u] >= 0;
         const bool emp = valid && k[u] == -1;
         int32_t old = k[u];
-        cas_pred(tb + sl[u] * 8, emp, c[u], old);
+        cas_pred(tb + sl[u] * KS, emp, c[u], old);
         fr[u] = emp && old == -1;
         const bool got = valid && (old == c[u] || fr[u]);
-        red_pred(tb + sl[u] * 8 + 4, got, w[u]);
+        red_pred(tb + sl[u] * KS + SO, got, w[u]);
         pend[u] = valid && !got;
         anyp |= pend[u];
     }
@@ -664,10 +681,10 @@ __device__ __forceinline__ void insert_chunk(uint32_t tb, uint32_t hmask, const 
             sl[u] = (sl[u] + 1) & hmask;
             uint32_t p = 1;
             for (;;) {
-                int32_t kk = lds_vol(tb + sl[u] * 8);
+                int32_t kk = lds_vol(tb + sl[u] * KS);
                 if (kk == c[u]) break;
                 if (kk == -1) {
-                    kk = cas_s(tb + sl[u] * 8, -1, c[u]);
+                    kk = cas_s(tb + sl[u] * KS, -1, c[u]);
                     if (kk == -1) {
                         fr[u] = true;
                         break;
@@ -680,7 +697,7 @@ __device__ __forceinline__ void insert_chunk(uint32_t tb, uint32_t hmask, const 
                     break;
                 }
             }
-            red_add_s(tb + sl[u] * 8 + 4, w[u]);   // (after a failed probe: a stray add to a
+            red_add_s(tb + sl[u] * KS + SO, w[u]);   // (after a failed probe: a stray add to a
                                                     //  slot of a row that is redone anyway)
         }
     }
@@ -766,6 +783,7 @@ __global__ void __launch_bounds__(WARPS * 32, 4) k_sweep_warp(SweepArgs<SYM> A, 
         }
         const uint32_t H = min(tab_size(d, 2, 32), (uint32_t)HMAX);   // > d either way
         const int32_t L = A.label[r];
+        const float2 SLf = comm_Sf(A, L);   // (consumed by decide_fast at the end of the row)
         const double2 sr = node_s(A, r);
         const float2 srf = make_float2((float)sr.x, (float)sr.y);
         uint32_t no = 0;
@@ -796,7 +814,7 @@ __global__ void __launch_bounds__(WARPS * 32, 4) k_sweep_warp(SweepArgs<SYM> A, 
             const unsigned cnt = (S.up1 >= lo) + (S.up2 >= lo);
             if (__reduce_add_sync(0xffffffffu, cnt) == 1) {
                 if (S.up1 >= lo)
-                    A.cstar[r] = decide_fast(A, S.g1, S.c1, lo, S.up1, ob != 0, gown, sr, srf, L);
+                    A.cstar[r] = decide_fast(A, S.g1, S.c1, lo, S.up1, ob != 0, gown, sr, srf, L, SLf);
             } else {
                 if (A.stats && lane == 0) {
                     atomicAdd(A.stats + 2, 1ull);
@@ -899,6 +917,7 @@ __global__ void __launch_bounds__(WARPS * 32, 4) k_sweep_half(SweepArgs<SYM> A, 
         const uint32_t d = (uint32_t)(A.uptr[r + 1] - e0);
         const uint32_t H = min(tab_size(d, 2, 32), (uint32_t)HM);   // > d
         const int32_t L = A.label[r];
+        const float2 SLf = comm_Sf(A, L);   // (consumed by decide_fast at the end of the row)
         const double2 sr = node_s(A, r);
         const float2 srf = make_float2((float)sr.x, (float)sr.y);
         int32_t c[U];
@@ -923,7 +942,7 @@ __global__ void __launch_bounds__(WARPS * 32, 4) k_sweep_half(SweepArgs<SYM> A, 
             const unsigned cnt = half_sum((S.up1 >= lo) + (S.up2 >= lo), hm);
             if (cnt == 1) {
                 if (S.up1 >= lo)
-                    A.cstar[r] = decide_fast(A, S.g1, S.c1, lo, S.up1, ob != 0, gown, sr, srf, L);
+                    A.cstar[r] = decide_fast(A, S.g1, S.c1, lo, S.up1, ob != 0, gown, sr, srf, L, SLf);
             } else {
                 if (A.stats && hl == 0) atomicAdd(A.stats + 2, 1ull);
                 double bt = -INFINITY;
@@ -983,7 +1002,7 @@ __device__ __forceinline__ void block_select(const SweepArgs<SYM> &A, const TAB 
         }
     } else if (cnt == 1) {
         if (S.up1 >= lo) {
-            A.cstar[r] = decide_fast(A, S.g1, S.c1, lo, S.up1, B.hown != 0, B.gown, sr, srf, L);
+            A.cstar[r] = decide_fast(A, S.g1, S.c1, lo, S.up1, B.hown != 0, B.gown, sr, srf, L, comm_Sf(A, L));
             B.hown = 0;
         }
     } else {
@@ -1041,17 +1060,38 @@ __device__ __forceinline__ RowMeta row_meta(const SweepArgs<SYM> &A, const int32
     return m;
 }
 
-template <int BLOCK, int HMAX, int F, int MINB, bool SYM>
+// table handle of a kernel's layout: int2 slots or split key / sum arrays
+template <bool SOA, int HMAX>
+struct TabOf {
+    using type = int2 *;
+    static __device__ __forceinline__ type make(int2 *base) { return base; }
+    static __device__ __forceinline__ void fill(int2 *base, int k) { base[k] = make_int2(-1, 0); }
+};
+template <int HMAX>
+struct TabOf<true, HMAX> {
+    using type = SoaTab;
+    static __device__ __forceinline__ type make(int2 *base) {
+        return SoaTab{(int32_t *)base, (uint32_t *)base + HMAX};
+    }
+    static __device__ __forceinline__ void fill(int2 *base, int k) {
+        ((int32_t *)base)[k] = -1;
+        ((uint32_t *)base)[HMAX + k] = 0u;
+    }
+};
+
+template <int BLOCK, int HMAX, int F, int MINB, bool SYM, bool SOA = false>
 __global__ void __launch_bounds__(BLOCK, MINB) k_sweep_cta(SweepArgs<SYM> A, const int32_t *rows,
                                                             int64_t nrows, int32_t *ovf,
                                                             uint32_t *novf) {
-    extern __shared__ int2 ctab[];
-    uint16_t *occ = (uint16_t *)(ctab + HMAX);
-    const uint32_t tsa = smem_addr(ctab), osa = smem_addr(occ);
+    extern __shared__ int2 ctab_raw[];
+    constexpr int SO = SOA ? 4 * HMAX : 4;
+    const typename TabOf<SOA, HMAX>::type ctab = TabOf<SOA, HMAX>::make(ctab_raw);
+    uint16_t *occ = (uint16_t *)(ctab_raw + HMAX);
+    const uint32_t tsa = smem_addr(ctab_raw), osa = smem_addr(occ);
     __shared__ BlockSel B;
     __shared__ uint32_t s_no;
     __shared__ int s_ovf;
-    for (int k = threadIdx.x; k < HMAX; k += BLOCK) ctab[k] = make_int2(-1, 0);
+    for (int k = threadIdx.x; k < HMAX; k += BLOCK) TabOf<SOA, HMAX>::fill(ctab_raw, k);
     if (threadIdx.x == 0) {
         B.hown = 0;
         s_no = 0;
@@ -1075,12 +1115,12 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_sweep_cta(SweepArgs<SYM> A, con
         const uint32_t *ub = A.u32 + cur.e0;
         uint32_t unused = 0;
         // z holds the first chunk's communities (gathered at the end of the previous row)
-        insert_chunk<U, true>(tsa, H - 1, z, wt, osa, &s_no, unused, &s_ovf);
+        insert_chunk<U, true, SO>(tsa, H - 1, z, wt, osa, &s_no, unused, &s_ovf);
         for (uint32_t cb = BLOCK * U; cb < cur.d; cb += BLOCK * U) {
             int32_t c[U];
             uint32_t w2[U];
             load_row<U, BLOCK>(nb, ub, A.label, cur.d, cb + threadIdx.x, c, w2);
-            insert_chunk<U, true>(tsa, H - 1, c, w2, osa, &s_no, unused, &s_ovf);
+            insert_chunk<U, true, SO>(tsa, H - 1, c, w2, osa, &s_no, unused, &s_ovf);
         }
         __syncthreads();
         // prefetch: next row's first chunk, the metadata of the row after it
@@ -1691,6 +1731,7 @@ __global__ void __launch_bounds__(HS_BLOCK, 1) k_sweep_hub_smem(SweepArgs<SYM> A
         }
         if (threadIdx.x == 0) Hb.route[j] = 1;
         const int32_t L = A.label[r];
+        const float2 SLf = comm_Sf(A, L);   // (consumed by decide_fast at the end of the row)
         const double2 sr = node_s(A, r);
         const float2 srf = make_float2((float)sr.x, (float)sr.y);
         const int32_t *nb = A.unbr + e0;
@@ -1757,7 +1798,7 @@ __global__ void __launch_bounds__(HS_BLOCK, 1) k_sweep_hub_smem(SweepArgs<SYM> A
                 if (threadIdx.x == 0) A.cstar[r] = L;
             } else if (cnt == 1) {
                 if (S.up1 >= lo)
-                    A.cstar[r] = decide_fast(A, S.g1, S.c1, lo, S.up1, B.hown != 0, B.gown, sr, srf, L);
+                    A.cstar[r] = decide_fast(A, S.g1, S.c1, lo, S.up1, B.hown != 0, B.gown, sr, srf, L, comm_Sf(A, L));
             } else {
                 if (A.stats && threadIdx.x == 0) {
                     atomicAdd(A.stats + 4, 1ull);
@@ -1860,9 +1901,11 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, const int
     constexpr size_t SM1 = (size_t)W1 * 512 * 10, SM2 = 2048 * 10, SM3 = 2048 * 10,
                      SM4 = 8192 * 10, SMH = HUB_H * 10 + HUB_SEG * 4, SMHS = HS_SLOTS * 8;
     auto k1 = k_sweep_warp<512, W1, SYM>;
-    auto k2 = k_sweep_cta<128, 2048, 2, 8, SYM>;
-    auto k3 = k_sweep_cta<256, 2048, 1, 4, SYM>;
-    auto k4 = k_sweep_cta<512, 8192, 1, 2, SYM>;
+    // bins 2-4: split key / sum tables (SLM_SOA=0: {key, sum} slots)
+    static const bool soa = !(getenv("SLM_SOA") && atoi(getenv("SLM_SOA")) == 0);
+    auto k2 = soa ? k_sweep_cta<128, 2048, 2, 8, SYM, true> : k_sweep_cta<128, 2048, 2, 8, SYM, false>;
+    auto k3 = soa ? k_sweep_cta<256, 2048, 1, 4, SYM, true> : k_sweep_cta<256, 2048, 1, 4, SYM, false>;
+    auto k4 = soa ? k_sweep_cta<512, 8192, 1, 2, SYM, true> : k_sweep_cta<512, 8192, 1, 2, SYM, false>;
     auto khm = k_sweep_hub_merge<SYM>;
     auto khs = k_sweep_hub_select<SYM>;
     auto khr = k_sweep_hub_row<SYM>;
