@@ -203,6 +203,10 @@ struct slm_ctx {
     double ph_t0 = 0.0;
     int device = 0;
     int num_sms = 148;           // cudaDevAttrMultiProcessorCount of the device
+    // per-context (= per-device) "function attributes set" flags: the opt-in dynamic shared
+    // memory size of a kernel is a per-device property
+    bool sweep_attr_set[2] = {false, false};
+    bool giant_attr_set = false;
     int walk_blocks = 0;         // co-resident grid of the persistent commit walker (cached)
     cudaStream_t stream = nullptr;
     cudaStream_t stream2 = nullptr;              // side stream of the plan sweep (hub rows)

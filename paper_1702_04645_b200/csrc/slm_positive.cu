@@ -1894,11 +1894,10 @@ void run_positive(slm_ctx *ctx, const LevelGraph &G, Forest &F, double m, int64_
             k_gb_totals<<<(unsigned)((np + 127) / 128), 128, 0, s>>>(dsl, ns, pso2.p, psi2.p,
                                                                      dparts2.p);
             CUDA_TRY(cudaMemsetAsync(cnt6.p + 3, 0, 4, s));
-            static bool smem_set = false;
-            if (!smem_set) {
+            if (!ctx->giant_attr_set) {
                 CUDA_TRY(cudaFuncSetAttribute(k_giant_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)GSMEM));
-                smem_set = true;
+                ctx->giant_attr_set = true;
             }
             k_giant_cta<<<(unsigned)np, GB, GSMEM, s>>>(GA, dparts2.p, O, neg_pool.p, dirty_pool.p,
                                                     gflag.p, negflag.p);

@@ -237,7 +237,8 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan_down(const TI *in, T *out, 
     const int64_t base = blockIdx.x * (int64_t)SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
     S.load(in, nullptr, n, base);
     S.reduce(s_warp);
-    S.write(out, n, base, SS<T, false>{tpre[blockIdx.x], 0}, s_warp);
+    // tpre == nullptr: a single tile, nothing before it
+    S.write(out, n, base, SS<T, false>{tpre ? tpre[blockIdx.x] : T(0), 0}, s_warp);
 }
 
 template <class TO>
@@ -261,7 +262,11 @@ template <class TI, class TO, bool SEG>
 void scan_run(slm_ctx *ctx, const TI *in, TO *out, const uint32_t *keys, int64_t n) {
     if (n <= 0) return;
     const int64_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
-    if (!SEG) {
+    if (!SEG && ntiles == 1) {
+        // one tile: the down-sweep kernel alone (the same arithmetic with a zero prefix) --
+        // small levels are launch-bound, so every kernel saved counts
+        k_scan_down<TI, TO><<<1, SCAN_BLOCK, 0, ctx->stream>>>(in, out, n, (const TO *)nullptr);
+    } else if (!SEG) {
         // reduce-then-scan: tile sums, one CTA scans them in order, tiles rescan.  Fixed
         // order (deterministic fp64 rounding), and no look-back chain across the ~1,000
         // tiles resident at once (the single-pass form below is kept for the segmented scan)
@@ -360,7 +365,10 @@ __global__ void __launch_bounds__(RS_BLOCK, 2) k_rs_onesweep(const K *kin, K *ko
     __shared__ unsigned s_hist[256];
     // reduce-then-scan mode (toff != nullptr): the tile's offsets per digit are known,
     // tile = blockIdx.x; onesweep mode: tiles in ticket order with decoupled look-back
-    if (threadIdx.x == 0) s_tile = toff ? blockIdx.x : atomicAdd(ticket, 1u);
+    // single-tile mode (dbase == nullptr, toff == nullptr): the staged digit order is the
+    // output order -- no histogram, no status words, no ticket
+    const bool single = !toff && !dbase;
+    if (threadIdx.x == 0) s_tile = (toff || single) ? blockIdx.x : atomicAdd(ticket, 1u);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int i = lane; i < 256; i += 32) {
         wcnt[wid * 256 + i] = 0;
@@ -385,7 +393,7 @@ __global__ void __launch_bounds__(RS_BLOCK, 2) k_rs_onesweep(const K *kin, K *ko
     }
     // the tile's digit counts first, published at once, so that the tiles behind this one
     // find them during their look-back while this tile is still ranking its keys
-    if (!toff) {
+    if (!toff && !single) {
 #pragma unroll
         for (int i = 0; i < RS_ITEMS; i++)
             if (wb + i * 32 + lane < n) atomicAdd(&s_hist[(unsigned)(key[i] >> shift) & dmask], 1u);
@@ -433,7 +441,7 @@ __global__ void __launch_bounds__(RS_BLOCK, 2) k_rs_onesweep(const K *kin, K *ko
         unsigned long long excl = 0;
         if (toff) {
             dest[d] = (unsigned long long)toff[(int64_t)d * ntiles + tile];
-        } else if (tile != 0) {
+        } else if (tile != 0 && !single) {
             // 8 predecessors per step with independent loads: the walk costs one memory
             // latency per 8 tiles, not per tile
             for (int64_t p = tile - 1; p >= 0;) {
@@ -457,7 +465,7 @@ __global__ void __launch_bounds__(RS_BLOCK, 2) k_rs_onesweep(const K *kin, K *ko
             }
             st_status(mine, RS_INC | (excl + cnt));
         }
-        if (!toff) dest[d] = dbase[d] + excl;
+        if (!toff && !single) dest[d] = dbase[d] + excl;
     }
     // tile start of every digit in digit order: exclusive scan of cnt over 256 threads
     {
@@ -476,6 +484,7 @@ __global__ void __launch_bounds__(RS_BLOCK, 2) k_rs_onesweep(const K *kin, K *ko
             unsigned off = 0;
             for (int w = 0; w < wid; w++) off += s_w[w];
             tstart[threadIdx.x] = off + v - cnt;
+            if (single) dest[threadIdx.x] = off + v - cnt;
         }
     }
     __syncthreads();
@@ -559,7 +568,8 @@ void radix_sort_impl(slm_ctx *ctx, const K *kin, K *kout, const V *vin, V *vout,
     unsigned long long *hist = nullptr, *status = nullptr;
     unsigned *tickets = nullptr;
     size_t sb = 0;
-    if (onesweep) {
+    const bool single = ntiles == 1 && onesweep;   // one kernel per pass, nothing else
+    if (onesweep && !single) {
         // scratch: [hist np*256 u64 | tickets np u32 (padded) | status ntiles*256 u64]
         const size_t hb = (size_t)np * 256 * 8, tb = 64;
         sb = (size_t)ntiles * 256 * 8;
@@ -591,7 +601,8 @@ void radix_sort_impl(slm_ctx *ctx, const K *kin, K *kout, const V *vin, V *vout,
         const int shift = begin_bit + 8 * p;
         const unsigned dmask = end_bit - shift >= 8 ? 255u : ((1u << (end_bit - shift)) - 1u);
         const int64_t *toff = nullptr;
-        if (onesweep) {
+        if (single) {
+        } else if (onesweep) {
             CUDA_TRY(cudaMemsetAsync(status, 0, sb, s));
         } else {
             k_rs_tilehist<K><<<(unsigned)ntiles, RS_BLOCK, 0, s>>>(ks, n, shift, dmask, ntiles,

@@ -1910,7 +1910,7 @@ static void launch_sweep(slm_ctx *ctx, const LevelGraph &G, Forest &F, const int
     auto khs = k_sweep_hub_select<SYM>;
     auto khr = k_sweep_hub_row<SYM>;
     auto khsm = k_sweep_hub_smem<SYM>;
-    static bool attrs[2] = {false, false};
+    bool *attrs = ctx->sweep_attr_set;
     if (!attrs[SYM]) {
         set_smem(k1, SM1);
         set_smem(k2, SM2);
