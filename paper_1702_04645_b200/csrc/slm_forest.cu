@@ -296,6 +296,20 @@ __global__ void k_size_level(const int32_t *nodes, int64_t lo, int64_t hi, const
         atomicAdd(&sz[a[x]], sz[x]);
     }
 }
+// small levels: every depth level in one launch (one CTA, a barrier between levels; lb[d] =
+// first position of depth d in `nodes`).  The sizes are read around L1: the atomics of the
+// level below land in L2.
+__global__ void __launch_bounds__(1024) k_size_levels_cta(const int32_t *nodes, const int32_t *lb,
+                                                          int maxd, const int32_t *a, int32_t *sz) {
+    for (int d = maxd; d >= 1; d--) {
+        const int lo = lb[d], hi = lb[d + 1];
+        for (int k = lo + (int)threadIdx.x; k < hi; k += (int)blockDim.x) {
+            const int32_t x = nodes[k];
+            atomicAdd(&sz[a[x]], __ldcg(sz + x));
+        }
+        __syncthreads();
+    }
+}
 __global__ void k_kid_vals(const int32_t *kids, int64_t nk, const int32_t *comm,
                            const int32_t *croot, const int32_t *sz, int32_t *val) {
     GS_LOOP(j, nk) {
@@ -521,21 +535,25 @@ void build_layout(slm_ctx *ctx, Forest &F) {
     // subtree sizes bottom-up, one launch per depth level
     if (n > 0)
         sort_pairs_u32_i32(ctx, depth.p, depth_sorted.p, iota2, by_depth.p, n, bits_for(maxd + 2));
-    std::vector<int64_t> lvl(maxd + 2, 0);
-    {
-        CTX_SCRATCH(DBuf<int32_t>, lb);   // grow-only scratch kept across calls
-        lb.resize(maxd + 2);
-        k_run_starts<<<grid_for(n, 256), 256, 0, s>>>((const int32_t *)depth_sorted.p, n, maxd + 1, lb.p);
+    CTX_SCRATCH(DBuf<int32_t>, lb);   // grow-only scratch kept across calls
+    lb.resize(maxd + 2);
+    k_run_starts<<<grid_for(n, 256), 256, 0, s>>>((const int32_t *)depth_sorted.p, n, maxd + 1, lb.p);
+    k_ones<<<grid_for(n, 256), 256, 0, s>>>(F.sz.p, n);
+    if (n <= 32768) {
+        // launch-bound sizes: one CTA walks the depth levels (no host copy of the bounds)
+        if (maxd >= 1)
+            k_size_levels_cta<<<1, 1024, 0, s>>>(by_depth.p, lb.p, maxd, F.a.p, F.sz.p);
+    } else {
+        std::vector<int64_t> lvl(maxd + 2, 0);
         std::vector<int32_t> h(maxd + 2);
         CUDA_TRY(cudaMemcpyAsync(h.data(), lb.p, (maxd + 2) * 4, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
         for (int d = 0; d <= maxd + 1; d++) lvl[d] = h[d];
-    }
-    k_ones<<<grid_for(n, 256), 256, 0, s>>>(F.sz.p, n);
-    for (int d = maxd; d >= 1; d--) {
-        int64_t lo = lvl[d], hi = lvl[d + 1];
-        if (hi > lo)
-            k_size_level<<<grid_for(hi - lo, 256), 256, 0, s>>>(by_depth.p, lo, hi, F.a.p, F.sz.p);
+        for (int d = maxd; d >= 1; d--) {
+            int64_t lo = lvl[d], hi = lvl[d + 1];
+            if (hi > lo)
+                k_size_level<<<grid_for(hi - lo, 256), 256, 0, s>>>(by_depth.p, lo, hi, F.a.p, F.sz.p);
+        }
     }
     // offsets among siblings (kids ascending, the root never a kid) and pre-order positions
     CTX_SCRATCH(DBuf<int32_t>, val);   // grow-only scratch kept across calls
