@@ -185,7 +185,9 @@ SLM_API int slm_uniform01(slm_ctx *ctx, uint64_t seed, int64_t level, int64_t sw
                   int64_t k, double *out);
 /* Phase timers (enabled by SLM_PROFILE=1, which synchronises at phase boundaries): ms per
  * phase in the order plan, candidates, spec, walk, components, aggregates, layout,
- * positive-local-gains, positive-small, positive-giant, assign, aggregate. */
+ * positive-local-gains, positive-small, positive-giant, assign, aggregate; then (always
+ * measured) host ms in cudaMalloc / cudaFree, their count, and host ms spent building the
+ * levels' sweep views. */
 SLM_API int slm_phase_times(slm_ctx *ctx, double *ms, int32_t nmax, int32_t reset);
 /* Diagnostics of the last slm_maximal: candidates, commit rounds. */
 SLM_API int slm_last_commit_stats(slm_ctx *ctx, int64_t *candidates, int64_t *rounds);

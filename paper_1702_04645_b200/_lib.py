@@ -432,7 +432,7 @@ class Context:
 
     PHASES = ("plan", "candidates", "spec", "walk", "components", "aggregates", "layout",
               "positive_lg", "positive_small", "positive_giant", "assign", "aggregate",
-              "alloc_ms", "alloc_calls")
+              "alloc_ms", "alloc_calls", "view_build_ms")
 
     def phase_times(self, reset=False):
         ms = np.zeros(len(self.PHASES), np.float64)

@@ -860,7 +860,8 @@ SweepView &ensure_sweep_view(slm_ctx *ctx, const LevelGraph &G) {
     if (G.view) return *G.view;
     cudaStream_t s = ctx->stream;
     static const bool verbose = getenv("SLM_VIEW_VERBOSE") != nullptr;
-    double tv = now_ms();
+    const double t_begin = now_ms();
+    double tv = t_begin;
     auto vmark = [&](const char *what) {
         if (!verbose) return;
         cudaStreamSynchronize(s);
@@ -933,8 +934,9 @@ SweepView &ensure_sweep_view(slm_ctx *ctx, const LevelGraph &G) {
     }
     CUDA_TRY(cudaGetLastError());
     vmark("strengths");
-    build_bins_view(ctx, V);
+    build_bins_view(ctx, V);   // (ends with a stream synchronisation)
     vmark("bins");
+    ctx->view_build_ms += now_ms() - t_begin;
     G.view = W;
     return *W;
 }

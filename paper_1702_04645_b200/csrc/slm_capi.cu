@@ -1176,7 +1176,10 @@ int slm_phase_times(slm_ctx *ctx, double *ms, int32_t nmax, int32_t reset) {
     // (process-wide)
     if (nmax > NPHASE) ms[NPHASE] = g_alloc_ms;
     if (nmax > NPHASE + 1) ms[NPHASE + 1] = (double)g_alloc_calls;
+    // ... and the host ms spent building sweep views (always measured; once per level)
+    if (nmax > NPHASE + 2) ms[NPHASE + 2] = ctx->view_build_ms;
     if (reset) {
+        ctx->view_build_ms = 0.0;
         for (int i = 0; i < NPHASE; i++) ctx->ph_ms[i] = 0.0;
         g_alloc_ms = 0.0;
         g_alloc_calls = 0;

@@ -207,6 +207,7 @@ struct slm_ctx {
     // memory size of a kernel is a per-device property
     bool sweep_attr_set[2] = {false, false};
     bool giant_attr_set = false;
+    double view_build_ms = 0.0;  // host ms spent building sweep views (once per level)
     int walk_blocks = 0;         // co-resident grid of the persistent commit walker (cached)
     cudaStream_t stream = nullptr;
     cudaStream_t stream2 = nullptr;              // side stream of the plan sweep (hub rows)

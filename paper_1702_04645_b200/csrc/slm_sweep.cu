@@ -1128,18 +1128,19 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_sweep_cta(SweepArgs<SYM> A, con
         const RowMeta nn = row_meta(A, rows, i + 2 * step, nrows);
         const uint32_t no = s_no;
         if (s_ovf) {
+            __syncthreads();   // (every thread has read s_no / s_ovf)
             if (threadIdx.x == 0) ovf[atomicAdd(novf, 1u)] = cur.r;
             if (A.stats && threadIdx.x == 0) atomicAdd(A.stats + 6, 1ull);
         } else {
             block_select<BLOCK, SYM, false>(A, ctab, occ, no, cur.r, cur.L, sr, B);
         }
+        if (threadIdx.x == 0) {   // block_select's barriers lie behind every read of them; the
+            s_no = 0;             // barrier below orders the reset before the next row's inserts
+            s_ovf = 0;
+        }
         gather_labels<U>(A.label, z, z);   // next row's first chunk: its latency overlaps the clear
         occ_clear<false>(ctab, occ, no, threadIdx.x, BLOCK);
         __syncthreads();
-        if (threadIdx.x == 0) {   // every thread read s_no / s_ovf before the barriers above
-            s_no = 0;
-            s_ovf = 0;
-        }
         cur = nxt;
         nxt = nn;
     }
@@ -1287,10 +1288,15 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_sweep_cta2(SweepArgs<SYM> A, co
         const RowMeta nn = row_meta(A, rows, i + 2 * step, nrows);
         const uint32_t no = s_no;
         if (s_ovf) {
+            __syncthreads();   // (every thread has read s_no / s_ovf)
             if (threadIdx.x == 0) ovf[atomicAdd(novf, 1u)] = cur.r;
             if (A.stats && threadIdx.x == 0) atomicAdd(A.stats + 6, 1ull);
         } else {
             block_select<BLOCK, SYM, false>(A, T, occ, no, cur.r, cur.L, sr, B);
+        }
+        if (threadIdx.x == 0) {
+            s_no = 0;
+            s_ovf = 0;
         }
         gather_labels<U>(A.label, z, z);
         for (uint32_t k = threadIdx.x; k < no; k += BLOCK) {
@@ -1299,10 +1305,6 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_sweep_cta2(SweepArgs<SYM> A, co
             sums[sl] = 0;
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            s_no = 0;
-            s_ovf = 0;
-        }
         cur = nxt;
         nxt = nn;
     }
