@@ -14,7 +14,9 @@ from paper_1702_04645_b200.graph import Graph
 def run(name, gamma=1.0):
     ctx = _lib.Context(0)
     t0 = time.perf_counter()
-    GN.build_on_device(ctx, name)
+    import workloads as W
+    spec = W.CONFIGS[name]
+    GN.build_on_device(ctx, spec, None if spec["kind"] in ("rmat", "rgg") else W.generate(name))
     tb = time.perf_counter() - t0
     info = ctx.info()
     g = Graph(info["n"], None, None, None)

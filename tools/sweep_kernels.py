@@ -8,7 +8,9 @@ from paper_1702_04645_b200 import _lib, generators as GN, RunConfig
 cfg_name = sys.argv[1] if len(sys.argv) > 1 else "c5_rmat24"
 target = int(sys.argv[2]) if len(sys.argv) > 2 else 60
 ctx = _lib.Context(0)
-GN.build_on_device(ctx, cfg_name)
+import workloads as W
+spec = W.CONFIGS[cfg_name]
+GN.build_on_device(ctx, spec, None if spec["kind"] in ("rmat", "rgg") else W.generate(cfg_name))
 cfg = RunConfig()._c()
 ctx.assign(want=False); ctx.components(want=False); ctx.positive(cfg)
 for sw in range(target + 1):
