@@ -19,6 +19,13 @@ __global__ void k(unsigned *out, int iters) {
         else if (MODE == 3) { volatile unsigned *v = t; acc += v[a]; }   // LDS
         else if (MODE == 4) { t[a] = x; }                        // STS
         else if (MODE == 5) { atomicAdd(&t[threadIdx.x & 4095], 1u); }   // lane-distinct banks
+        else if (MODE == 6) { atomicAdd(&t[7], 1u); }                    // one address, every lane
+        else if (MODE == 7) { atomicAdd(&t[(x >> 29) == 0 ? 7u : a], 1u); }   // 1/8 of the lanes on one address
+        else if (MODE == 8) { atomicAdd(&t[(x >> 28) == 0 ? 7u : a], 1u); }   // 1/16 ...
+        else if (MODE == 9) {   // skewed like the sweep: 43% of the adds on 64 addresses
+            const unsigned b = (x >> 8) & 63;
+            atomicAdd(&t[(x & 127) < 55 ? b * 61u : a], 1u);
+        }
     }
     __syncthreads();
     if (threadIdx.x == 0) out[blockIdx.x] = t[blockIdx.x & 4095] + acc;
@@ -31,8 +38,10 @@ int main() {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const int iters = 4096, blocks = sms * 8, threads = 256;
     const char *names[] = {"RED.shared add (spread)", "ATOMS add w/ return (spread)", "ATOMS CAS (spread)",
-                           "LDS volatile (spread)", "STS (spread)", "RED.shared add (lane-distinct)"};
-    for (int mode = 0; mode < 6; mode++) {
+                           "LDS volatile (spread)", "STS (spread)", "RED.shared add (lane-distinct)",
+                           "RED.shared add (one address)", "RED.shared add (1/8 on one address)",
+                           "RED.shared add (1/16 on one address)", "RED.shared add (43% on 64 addresses)"};
+    for (int mode = 0; mode < 10; mode++) {
         cudaEvent_t a, b;
         cudaEventCreate(&a);
         cudaEventCreate(&b);
@@ -45,6 +54,10 @@ int main() {
                 case 3: k<3><<<blocks, threads>>>(o, iters); break;
                 case 4: k<4><<<blocks, threads>>>(o, iters); break;
                 case 5: k<5><<<blocks, threads>>>(o, iters); break;
+                case 6: k<6><<<blocks, threads>>>(o, iters); break;
+                case 7: k<7><<<blocks, threads>>>(o, iters); break;
+                case 8: k<8><<<blocks, threads>>>(o, iters); break;
+                case 9: k<9><<<blocks, threads>>>(o, iters); break;
             }
             cudaEventRecord(b);
             cudaEventSynchronize(b);
