@@ -55,6 +55,18 @@ def test_forced_paths_vs_oracle(tmp_path, env, path):
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
 
 
+@pytest.mark.parametrize("env", ["SLM_VIEW_SORTED", "SLM_SOA", "SLM_VIEW"])
+def test_integer_sweep_variants_vs_oracle(tmp_path, env):
+    """The integer sweep's switches -- view rows in the level graph's entry order instead of
+    sorted by view id, {key, sum} slots instead of split tables, no degree-ordered view at
+    all -- change the work, never a target or a partition (same checks as the default)."""
+    f = tmp_path / "p.py"
+    f.write_text(_SCRIPT.format(root=ROOT, path="u32"))
+    r = subprocess.run([sys.executable, str(f)], env=dict(os.environ, **{env: "0"}), cwd=ROOT,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
 def _real(n, s, d, seed):
     rng = np.random.default_rng(seed)
     w = rng.uniform(0.1, 3.0, s.size)
